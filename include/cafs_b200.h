@@ -1,0 +1,174 @@
+/*
+ * cafs_b200.h -- C ABI of libcafs_b200.so, the B200 (sm_100a) CAFS sort.
+ *
+ * Plain pointers, sizes and status codes; no torch or CUDA types in the
+ * signatures (streams travel as `void*` = cudaStream_t).  Every call is
+ * stream-ordered on the given stream and thread-safe across distinct contexts.
+ *
+ * Each entry point replaces one interface of the reference package
+ * (paths relative to /root/reference/pkg/src/cafs):
+ *
+ *   cafs_sort_i64            sorter.py:335-386   cafs_sort(x, telemetry, hash_mult)
+ *   cafs_sort_i64_host       sorter.py:335-386   same call on host (numpy) buffers
+ *   cafs_dispatch_i64        sorter.py:141-162   dispatch(x, n, hash_mult)
+ *   cafs_estimate_i64        cardinality.py:113-125  sample_and_estimate(x, n, hash_mult)
+ *                            (+ _kernels.py:131-153 freqset_insert_many, cardinality.py:63-69)
+ *   cafs_is_monotone_i64     sorter.py:115-129   is_monotone(x)
+ *   cafs_tiny_counts_i64     _kernels.py:156-169 tiny_counts(x, keys)
+ *   cafs_count_pairs_i64     sorter.py:183-196 + 254-288  main_count_loop -> reconstruct's
+ *                            sorted (key, count) pairs (count_sequence _kernels.py:25-81,
+ *                            fold_sorted :219-225, pair_sort :228-241)
+ *   cafs_pair_sort           _kernels.py:185-214 radix_sort_pairs / sorter.py:228-241 pair_sort
+ *   cafs_emit_i64            sorter.py:244-251 + _kernels.py:172-182  emit / emit_fill
+ *   cafs_fallback_sort_i64   sorter.py:132-138   fallback_sort(x)
+ *
+ * Keys are 64-bit.  `is_signed` = 1 for int64 (order-mapped by flipping bit 63,
+ * sorter.py:84-94, folded into the kernels' loads/stores), 0 for uint64.
+ * Errors: the reference raises TypeError/ValueError from Python; here the same
+ * conditions return CAFS_EINVAL and the Python layer raises the reference's
+ * exception type.
+ */
+#ifndef CAFS_B200_H
+#define CAFS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CAFS_ABI_VERSION 1
+#define CAFS_TINY_MAX_KEYS 8      /* sorter.py:30  TINY_MAX_KEYS */
+#define CAFS_SMALL_N_CUTOFF 2048  /* sorter.py:29  SMALL_N_CUTOFF */
+#define CAFS_SAMPLE_TARGET 1024   /* cardinality.py:26 */
+#define CAFS_DEFAULT_HASH_MULT 0x9E3779B97F4A7C15ull /* buckets.py:30 */
+
+/* cafs.sorter.Route (sorter.py:44-49), same order */
+typedef enum {
+  CAFS_ALREADY_SORTED = 0,
+  CAFS_FALLBACK_SMALL_N = 1,
+  CAFS_TINY_COUNT = 2,
+  CAFS_FALLBACK_HIGH_ENTROPY = 3,
+  CAFS_MAIN = 4
+} cafs_route_t;
+
+typedef enum {
+  CAFS_OK = 0,
+  CAFS_EINVAL = -1,    /* bad argument (reference: ValueError/TypeError) */
+  CAFS_ECUDA = -2,     /* CUDA runtime error */
+  CAFS_ENOMEM = -3,    /* device allocation failed */
+  CAFS_ESUM = -4,      /* pair counts do not sum to n (reference emit ValueError) */
+  CAFS_EINTERNAL = -5
+} cafs_status_t;
+
+/* cafs.cardinality.CardinalityEstimate (cardinality.py:76-82) + the sampled
+ * distinct keys (FreqSet.distinct_keys, ascending, unsigned domain) when u <= 8 */
+typedef struct {
+  double k_hat;
+  int64_t u, f1, f2;
+  int32_t saturated;
+  int32_t nkeys;
+  uint64_t keys[CAFS_TINY_MAX_KEYS];
+} cafs_estimate_t;
+
+/* cafs.sorter.DispatchDecision (sorter.py:52-57) */
+typedef struct {
+  int32_t route;
+  int32_t has_estimate;
+  cafs_estimate_t est;
+} cafs_decision_t;
+
+/* Stage indices of cafs_telemetry_t.stage_ms (sorter.py:64-66 labels) */
+enum { CAFS_STAGE_COUNT = 0, CAFS_STAGE_SORT_K = 1, CAFS_STAGE_EMIT = 2 };
+
+/* cafs.sorter.SortTelemetry (sorter.py:60-81).  stage_ms[i] < 0: stage not run. */
+typedef struct {
+  uint64_t n;
+  cafs_decision_t decision;      /* final decision (MAIN after a tiny-count failure) */
+  int32_t tiny_count_failed;
+  int32_t guard_fired;           /* device guard: global table overflow -> fallback */
+  uint64_t counted_total;        /* elements counted into (key, count) pairs */
+  uint64_t pairs;                /* distinct keys emitted (K') */
+  uint64_t table_buckets;        /* reference table_size_for(max(1,k_hat), n, 4) on MAIN */
+  uint64_t global_updates;       /* device: elements resolved in the L2 global table */
+  float stage_ms[3];
+  uint32_t kernels_launched;     /* kernels this call put on the stream */
+} cafs_telemetry_t;
+
+typedef struct cafs_ctx cafs_ctx_t;
+
+/* Context: per-device persistent state (control block, the L2-resident global
+ * (key, count) table, pair buffers).  One context per device and stream user. */
+int cafs_ctx_create(int device, cafs_ctx_t** out);
+void cafs_ctx_destroy(cafs_ctx_t* ctx);
+int cafs_abi_version(void);
+const char* cafs_status_string(int status);
+const char* cafs_last_error(cafs_ctx_t* ctx);
+
+/* Flags for cafs_sort_i64 */
+#define CAFS_FLAG_TIMING 1u      /* fill stage_ms with CUDA-event timings */
+#define CAFS_FLAG_NO_DIRECT 2u   /* disable the dense-range direct-count path */
+
+/* cafs_sort(x) in place on device memory (sorter.py:335-386).  n < 2^32. */
+int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed,
+                  uint64_t hash_mult, uint32_t flags, cafs_telemetry_t* tel, void* stream);
+
+/* Same on host memory: h_in -> device -> sort -> h_out (h_out may equal h_in).
+ * Page-locked buffers give full PCIe bandwidth; pageable ones work too. */
+int cafs_sort_i64_host(cafs_ctx_t* ctx, const int64_t* h_in, int64_t* h_out, uint64_t n,
+                       int is_signed, uint64_t hash_mult, uint32_t flags,
+                       cafs_telemetry_t* tel, void* stream);
+
+/* dispatch(x) -> decision (sorter.py:141-162); requires n >= 2 */
+int cafs_dispatch_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                      uint64_t hash_mult, cafs_decision_t* out, void* stream);
+
+/* sample_and_estimate(x, n) (cardinality.py:113-125); n >= 1 */
+int cafs_estimate_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                      cafs_estimate_t* out, void* stream);
+
+/* is_monotone(x) (sorter.py:115-129) */
+int cafs_is_monotone_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                         int* out, void* stream);
+
+/* tiny_counts(x, keys) (_kernels.py:156-169): keys in the unsigned domain, distinct,
+ * nk <= 8; h_counts[j] = #{i : x_u[i] == keys[j]} */
+int cafs_tiny_counts_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                         const uint64_t* h_keys, int nk, int64_t* h_counts, void* stream);
+
+/* Count x into distinct (key, count) pairs sorted by unsigned key (the count +
+ * reconstruct stages of the main route).  d_keys/d_counts hold `cap` entries;
+ * *h_npairs receives K'.  Returns CAFS_EINVAL if K' > cap. */
+int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                         uint64_t hash_mult, uint64_t* d_keys, uint64_t* d_counts,
+                         uint64_t cap, uint64_t* h_npairs, void* stream);
+
+/* pair_sort: sort (key, count) pairs by unsigned key in place (keys distinct) */
+int cafs_pair_sort(cafs_ctx_t* ctx, uint64_t* d_keys, uint64_t* d_counts, uint64_t npairs,
+                   void* stream);
+
+/* emit: expand sorted pairs into out[0 .. sum(counts)) restricted to the output
+ * slice [out_begin, out_end) of the global sorted order (whole array:
+ * 0 .. total); d_out receives out_end - out_begin keys.  Keys are unsigned-domain;
+ * is_signed un-flips them on store.  Sum check as sorter.py:247-248. */
+int cafs_emit_i64(cafs_ctx_t* ctx, const uint64_t* d_keys, const uint64_t* d_counts,
+                  uint64_t npairs, int64_t* d_out, uint64_t out_begin, uint64_t out_end,
+                  uint64_t total, int is_signed, void* stream);
+
+/* fallback_sort(x): on-device LSD radix sort (sorter.py:132-138 replaced) */
+int cafs_fallback_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed,
+                           void* stream);
+
+/* ---- synthetic inputs (bench / tests; bit-identical to oracle/gen.py) ---- */
+/* out[i] = fmix64(seed + (skip + i + 1) * 0x9E3779B97F4A7C15) */
+int cafs_gen_mix(uint64_t* d_out, uint64_t count, uint64_t seed, uint64_t skip, void* stream);
+/* rows [start, start+n): out[i] = palette[idx(start+i)], idx uniform (mulhi) or,
+ * when d_cdf != NULL, Zipf by searchsorted(cdf, u, 'right'); palette NULL = codes */
+int cafs_gen_draw(int64_t* d_out, uint64_t n, uint64_t start, uint64_t seed,
+                  const int64_t* d_palette, uint64_t k, const double* d_cdf, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CAFS_B200_H */

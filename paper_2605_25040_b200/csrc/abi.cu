@@ -1,0 +1,734 @@
+// abi.cu -- the C ABI of libcafs_b200.so and the native pipeline orchestrator.
+//
+// cafs_sort_i64 is the B200 restatement of cafs_sort (sorter.py:335-386):
+//
+//   n <= 1                        -> ALREADY_SORTED                 (:353-355)
+//   K0/K1 estimate kernel         -> route, k_hat, u, f1, f2, keys  (:141-162)
+//     prefix sorted and n > 64 Ki -> full monotone scan kernel
+//   FALLBACK_SMALL_N / HIGH_ENT.  -> on-device sort (radix.cu)      (:362-366)
+//   TINY_COUNT                    -> K2 count, finalize, K5 emit    (:367-377)
+//     any miss                    -> MAIN with the same k_hat       (:378-385)
+//   MAIN                          -> K3 hash count, compact, K4 pair sort + scan,
+//                                    K5 emit; global-table overflow -> guard
+//                                    -> fallback sort               (:317-332, :254-293)
+//
+// Host round trips: one after the estimate kernel (the route decides which
+// kernels exist) and one at the end of the call (telemetry, guard).  Every
+// stage in between is stream-ordered and gated on the device control block.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace cafs;
+
+struct cafs_ctx {
+  int device = 0;
+  int num_sms = 148;
+  DevCtl* d_ctl = nullptr;
+  DevCtl* h_ctl = nullptr;  // pinned mirror
+  // main route: global table + pair buffers
+  u64* gkeys = nullptr;
+  u64* gcnt = nullptr;
+  u32* glist = nullptr;
+  u64* pk_a = nullptr;  // compacted pairs (unsorted)
+  u64* pc_a = nullptr;
+  u64* pk_b = nullptr;  // sorted pairs
+  u64* pc_b = nullptr;
+  u64* poffs = nullptr;  // exclusive offsets, npairs + 1
+  u64* bsum = nullptr;
+  // radix sort scratch
+  u32* ghist = nullptr;  // [8][256]
+  u32* gbase = nullptr;  // [8][256]
+  int* trivial = nullptr;
+  int* h_trivial = nullptr;
+  u32* tile_counters = nullptr;  // [8]
+  u64* tile_state = nullptr;
+  size_t tile_state_words = 0;
+  u64* tmp = nullptr;
+  size_t tmp_elems = 0;
+  u64* stage = nullptr;  // host-path device staging buffer
+  size_t stage_elems = 0;
+  u32 epoch = 0;
+  cudaEvent_t ev[4] = {};
+  std::string last_error;
+  uint32_t launches = 0;
+};
+
+namespace {
+
+constexpr u64 kPairCap = kGlobalCap + 1;
+
+int fail(cafs_ctx_t* c, int code, const char* what, cudaError_t e = cudaSuccess) {
+  if (c) {
+    c->last_error = what;
+    if (e != cudaSuccess) {
+      c->last_error += ": ";
+      c->last_error += cudaGetErrorString(e);
+    }
+  }
+  return code;
+}
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess) return fail(ctx, CAFS_ECUDA, #call, e_);           \
+  } while (0)
+
+#define CKL()                                                                 \
+  do {                                                                        \
+    cudaError_t e_ = cudaGetLastError();                                      \
+    if (e_ != cudaSuccess) return fail(ctx, CAFS_ECUDA, "kernel launch", e_); \
+  } while (0)
+
+#define TRY(expr)             \
+  do {                        \
+    int r_ = (expr);          \
+    if (r_ != CAFS_OK) return r_; \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+u64 bit_ceil(u64 v) { return v <= 1 ? 1 : 1ull << (64 - __builtin_clzll(v - 1)); }
+
+// buckets.py:92-105 (reported in telemetry; the GPU tables are sized on their own)
+u64 table_size_for(double k_hat, u64 n, int cap) {
+  u64 m = bit_ceil((u64)std::ceil(8.0 * k_hat / cap));
+  u64 m2 = bit_ceil((u64)std::ceil((double)n / cap));
+  if (m2 < m) m = m2;
+  return m < 8 ? 8 : m;
+}
+
+int ensure_main(cafs_ctx_t* ctx) {
+  if (ctx->gkeys) return CAFS_OK;
+  CK(cudaMalloc(&ctx->gkeys, kGlobalSlots * 8));
+  CK(cudaMalloc(&ctx->gcnt, kGlobalSlots * 8));
+  CK(cudaMalloc(&ctx->glist, kGlobalCap * 4));
+  CK(cudaMemset(ctx->gkeys, 0xFF, kGlobalSlots * 8));
+  CK(cudaMemset(ctx->gcnt, 0, kGlobalSlots * 8));
+  CK(cudaMalloc(&ctx->pk_a, kPairCap * 8));
+  CK(cudaMalloc(&ctx->pc_a, kPairCap * 8));
+  CK(cudaMalloc(&ctx->pk_b, kPairCap * 8));
+  CK(cudaMalloc(&ctx->pc_b, kPairCap * 8));
+  CK(cudaMalloc(&ctx->poffs, (kPairCap + 1) * 8));
+  CK(cudaMalloc(&ctx->bsum, (kPairCap / 8192 + 2) * 8));
+  return CAFS_OK;
+}
+
+int ensure_radix(cafs_ctx_t* ctx, u64 n, bool need_tmp) {
+  if (!ctx->ghist) {
+    CK(cudaMalloc(&ctx->ghist, 8 * 256 * 4));
+    CK(cudaMalloc(&ctx->gbase, 8 * 256 * 4));
+    CK(cudaMalloc(&ctx->trivial, 8 * sizeof(int)));
+    CK(cudaMallocHost(&ctx->h_trivial, 8 * sizeof(int)));
+    CK(cudaMalloc(&ctx->tile_counters, 8 * 4));
+  }
+  const size_t words = (size_t)onesweep_tiles(n) * 256;
+  if (words > ctx->tile_state_words) {
+    if (ctx->tile_state) CK(cudaFree(ctx->tile_state));
+    ctx->tile_state = nullptr;
+    size_t w = words < (size_t)65536 ? (size_t)65536 : words;
+    CK(cudaMalloc(&ctx->tile_state, w * 8));
+    CK(cudaMemset(ctx->tile_state, 0, w * 8));  // epoch 0 is never used
+    ctx->tile_state_words = w;
+  }
+  if (need_tmp && n > ctx->tmp_elems) {
+    if (ctx->tmp) CK(cudaFree(ctx->tmp));
+    ctx->tmp = nullptr;
+    CK(cudaMalloc(&ctx->tmp, n * 8));
+    ctx->tmp_elems = n;
+  }
+  return CAFS_OK;
+}
+
+u32 next_epoch(cafs_ctx_t* ctx) {
+  ctx->epoch = (ctx->epoch + 1) & 0x3FFFFFFFu;
+  if (ctx->epoch == 0) ctx->epoch = 1;
+  return ctx->epoch;
+}
+
+// LSD radix sort of keys (optionally with a u64 payload) -> result in (k_out, v_out).
+// k_in may equal k_out (in place via the ctx temp buffer) for keys-only sorts.
+int radix_sort(cafs_ctx_t* ctx, u64* keys, u64* vals, u64* kalt, u64* valt, u64 n, u64 flip,
+               cudaStream_t st, u64** result_k, u64** result_v) {
+  CK(cudaMemsetAsync(ctx->ghist, 0, 8 * 256 * 4, st));
+  CK(cudaMemsetAsync(ctx->tile_counters, 0, 8 * 4, st));
+  launch_radix_hist(keys, n, flip, ctx->ghist, ctx->num_sms, st);
+  launch_radix_prep(ctx->ghist, n, ctx->gbase, ctx->trivial, st);
+  ctx->launches += 2;
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_trivial, ctx->trivial, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int passes[8], np = 0;
+  for (int p = 0; p < 8; ++p)
+    if (!ctx->h_trivial[p]) passes[np++] = p;
+  u64 *sk = keys, *sv = vals, *dk = kalt, *dv = valt;
+  for (int i = 0; i < np; ++i) {
+    const u64 fin = i == 0 ? flip : 0, fout = i == np - 1 ? flip : 0;
+    cudaError_t e = launch_onesweep(sk, sv, dk, dv, n, passes[i], fin, fout,
+                                    ctx->gbase + passes[i] * 256, ctx->tile_state,
+                                    ctx->tile_counters + i, next_epoch(ctx), st);
+    if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "onesweep", e);
+    ctx->launches++;
+    u64* t = sk; sk = dk; dk = t;
+    t = sv; sv = dv; dv = t;
+  }
+  *result_k = sk;
+  *result_v = sv;
+  return CAFS_OK;
+}
+
+// fallback_sort (sorter.py:132-138) on device, in place
+int fallback_sort(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cudaStream_t st) {
+  if (n < 2) return CAFS_OK;
+  if (n <= kSmallSortMax) {
+    cudaError_t e = launch_small_sort_keys(x, n, flip, st);
+    if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "small sort", e);
+    ctx->launches++;
+    return CAFS_OK;
+  }
+  TRY(ensure_radix(ctx, n, true));
+  u64 *rk, *rv;
+  TRY(radix_sort(ctx, x, nullptr, ctx->tmp, nullptr, n, flip, st, &rk, &rv));
+  if (rk != x) CK(cudaMemcpyAsync(x, rk, n * 8, cudaMemcpyDeviceToDevice, st));
+  return CAFS_OK;
+}
+
+int sync_ctl(cafs_ctx_t* ctx, cudaStream_t st) {
+  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->d_ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return CAFS_OK;
+}
+
+void fill_decision(const DevCtl& c, int route, bool has_est, cafs_decision_t* d) {
+  memset(d, 0, sizeof(*d));
+  d->route = route;
+  d->has_estimate = has_est ? 1 : 0;
+  if (!has_est) return;
+  d->est.k_hat = c.k_hat;
+  d->est.u = c.u;
+  d->est.f1 = c.f1;
+  d->est.f2 = c.f2;
+  d->est.saturated = c.saturated;
+  d->est.nkeys = c.u <= CAFS_TINY_MAX_KEYS ? (int)c.u : 0;
+  for (int j = 0; j < d->est.nkeys; ++j) d->est.keys[j] = c.keys[j];
+}
+
+// K0/K1 (+ the full monotone scan when the prefix is sorted).  Leaves the
+// device control block filled and *monotone / *route set.
+int run_dispatch(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, cudaStream_t st, bool* monotone,
+                 int* route) {
+  launch_estimate(x, n, flip, 1, ctx->d_ctl, st);
+  ctx->launches++;
+  CKL();
+  TRY(sync_ctl(ctx, st));
+  *monotone = false;
+  if (ctx->h_ctl->prefix_sorted) {
+    if (n <= kMonoPrefix) {
+      *monotone = true;
+    } else {
+      launch_monotone_scan(x, n, flip, ctx->d_ctl, ctx->num_sms, st);
+      ctx->launches++;
+      CKL();
+      TRY(sync_ctl(ctx, st));
+      *monotone = !ctx->h_ctl->scan_inversion;
+    }
+  }
+  *route = *monotone ? CAFS_ALREADY_SORTED : ctx->h_ctl->route;
+  return CAFS_OK;
+}
+
+struct StageTimer {
+  cafs_ctx_t* ctx;
+  cudaStream_t st;
+  bool on;
+  cafs_telemetry_t* tel;
+  void begin() {
+    if (on) cudaEventRecord(ctx->ev[0], st);
+  }
+  void end(int stage) {
+    if (!on) return;
+    cudaEventRecord(ctx->ev[1], st);
+    cudaEventSynchronize(ctx->ev[1]);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+    tel->stage_ms[stage] = (tel->stage_ms[stage] < 0 ? 0.f : tel->stage_ms[stage]) + ms;
+  }
+};
+
+// count -> compact -> pair sort -> emit, with the guard (sorter.py:317-332, 254-293)
+int run_main(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
+             cafs_telemetry_t* tel, StageTimer& tm, cudaStream_t st) {
+  TRY(ensure_main(ctx));
+  tm.begin();
+  cudaError_t e = launch_hash_count(x, n, flip, mult, ctx->d_ctl, ctx->gkeys, ctx->gcnt,
+                                    ctx->glist, (flags & CAFS_FLAG_NO_DIRECT) ? 0 : 1,
+                                    ctx->num_sms, st);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
+  launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
+                 ctx->num_sms, st);
+  ctx->launches += 2;
+  CKL();
+  tm.end(CAFS_STAGE_COUNT);
+  tm.begin();
+  e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, n, ctx->pk_b, ctx->pc_b,
+                              ctx->poffs, st);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+  ctx->launches++;
+  tm.end(CAFS_STAGE_SORT_K);
+  tm.begin();
+  launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st);
+  ctx->launches++;
+  CKL();
+  tm.end(CAFS_STAGE_EMIT);
+  TRY(sync_ctl(ctx, st));
+  DevCtl& c = *ctx->h_ctl;
+  if (tel) tel->global_updates = c.g_updates;
+  if (c.overflow) {
+    // guard: the count is dropped; x is untouched, sort it with the fallback
+    CK(cudaMemsetAsync(ctx->gkeys, 0xFF, kGlobalSlots * 8, st));
+    CK(cudaMemsetAsync(ctx->gcnt, 0, kGlobalSlots * 8, st));
+    if (tel) {
+      tel->guard_fired = 1;
+      tel->stage_ms[CAFS_STAGE_EMIT] = -1.f;
+    }
+    tm.begin();
+    TRY(fallback_sort(ctx, x, n, flip, st));
+    tm.end(CAFS_STAGE_SORT_K);
+    return CAFS_OK;
+  }
+  if (c.need_large) {
+    const u64 np = c.npairs;
+    tm.begin();
+    TRY(ensure_radix(ctx, np, false));
+    u64 *rk, *rv;
+    TRY(radix_sort(ctx, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, np, 0, st, &rk, &rv));
+    if (rk != ctx->pk_b) {
+      CK(cudaMemcpyAsync(ctx->pk_b, rk, np * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(ctx->pc_b, rv, np * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    launch_scan(ctx->pc_b, np, ctx->bsum, ctx->poffs, ctx->d_ctl, n, st);
+    ctx->launches += 3;
+    CKL();
+    tm.end(CAFS_STAGE_SORT_K);
+    tm.begin();
+    launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st);
+    ctx->launches++;
+    CKL();
+    tm.end(CAFS_STAGE_EMIT);
+    TRY(sync_ctl(ctx, st));
+  }
+  if (c.sum_error || !c.pairs_ready) return fail(ctx, CAFS_ESUM, "pair counts do not sum to n");
+  if (tel) {
+    tel->counted_total = c.total;
+    tel->pairs = c.npairs;
+  }
+  return CAFS_OK;
+}
+
+int check_common(cafs_ctx_t* ctx, const void* p, u64 n) {
+  if (!ctx) return CAFS_EINVAL;
+  if (n >= (1ull << 32)) return fail(ctx, CAFS_EINVAL, "arrays of 2**32 or more elements");
+  if (n > 0 && !p) return fail(ctx, CAFS_EINVAL, "null data pointer");
+  if (((uintptr_t)p) & 7) return fail(ctx, CAFS_EINVAL, "data must be 8-byte aligned");
+  return CAFS_OK;
+}
+
+// host-side perfect hash for caller-given tiny keys (same family as estimate.cu)
+u64 host_fmix64(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+}  // namespace
+
+extern "C" {
+
+int cafs_abi_version(void) { return CAFS_ABI_VERSION; }
+
+const char* cafs_status_string(int s) {
+  switch (s) {
+    case CAFS_OK: return "ok";
+    case CAFS_EINVAL: return "invalid argument";
+    case CAFS_ECUDA: return "CUDA error";
+    case CAFS_ENOMEM: return "out of device memory";
+    case CAFS_ESUM: return "pair counts do not sum to the output length";
+    default: return "internal error";
+  }
+}
+
+const char* cafs_last_error(cafs_ctx_t* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+int cafs_ctx_create(int device, cafs_ctx_t** out) {
+  if (!out) return CAFS_EINVAL;
+  *out = nullptr;
+  cafs_ctx_t* ctx = new (std::nothrow) cafs_ctx_t();
+  if (!ctx) return CAFS_ENOMEM;
+  ctx->device = device;
+  DeviceGuard g(device);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { delete ctx; return CAFS_ECUDA; }
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) { delete ctx; return CAFS_ECUDA; }
+  if (prop.major != 10) { delete ctx; return CAFS_EINVAL; }  // sm_100a only
+  ctx->num_sms = prop.multiProcessorCount;
+  if (cudaMalloc(&ctx->d_ctl, sizeof(DevCtl)) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_ctl, sizeof(DevCtl)) != cudaSuccess ||
+      cudaMemset(ctx->d_ctl, 0, sizeof(DevCtl)) != cudaSuccess) {
+    cafs_ctx_destroy(ctx);
+    return CAFS_ENOMEM;
+  }
+  for (int i = 0; i < 4; ++i) cudaEventCreate(&ctx->ev[i]);
+  *out = ctx;
+  return CAFS_OK;
+}
+
+void cafs_ctx_destroy(cafs_ctx_t* ctx) {
+  if (!ctx) return;
+  DeviceGuard g(ctx->device);
+  cudaDeviceSynchronize();
+  void* dev[] = {ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
+                 ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->ghist, ctx->gbase,
+                 ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+  if (ctx->h_trivial) cudaFreeHost(ctx->h_trivial);
+  for (int i = 0; i < 4; ++i)
+    if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  delete ctx;
+}
+
+int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint64_t hash_mult,
+                  uint32_t flags, cafs_telemetry_t* tel, void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  if ((hash_mult & 1) == 0) return fail(ctx, CAFS_EINVAL, "hash multiplier must be odd");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  ctx->launches = 0;
+  cafs_telemetry_t local;
+  const bool want_tel = tel != nullptr;
+  if (!tel) tel = &local;
+  memset(tel, 0, sizeof(*tel));
+  tel->n = n;
+  for (int i = 0; i < 3; ++i) tel->stage_ms[i] = -1.f;
+  if (n <= 1) {
+    tel->decision.route = CAFS_ALREADY_SORTED;
+    return CAFS_OK;
+  }
+  StageTimer tm{ctx, st, want_tel && (flags & CAFS_FLAG_TIMING), tel};
+  u64* x = (u64*)d_x;
+  const u64 flip = is_signed ? kSign : 0;
+  bool mono;
+  int route;
+  TRY(run_dispatch(ctx, x, n, flip, st, &mono, &route));
+  const DevCtl c = *ctx->h_ctl;
+  fill_decision(c, route, !mono && n >= CAFS_SMALL_N_CUTOFF, &tel->decision);
+  int rc = CAFS_OK;
+  switch (route) {
+    case CAFS_ALREADY_SORTED:
+      break;
+    case CAFS_FALLBACK_SMALL_N:
+    case CAFS_FALLBACK_HIGH_ENTROPY:
+      tm.begin();
+      rc = fallback_sort(ctx, x, n, flip, st);
+      tm.end(CAFS_STAGE_SORT_K);
+      break;
+    case CAFS_TINY_COUNT: {
+      TRY(ensure_main(ctx));
+      tm.begin();
+      launch_tiny_count(x, n, flip, ctx->d_ctl, ctx->num_sms, st);
+      launch_tiny_finalize(ctx->d_ctl, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st);
+      ctx->launches += 2;
+      CKL();
+      tm.end(CAFS_STAGE_COUNT);
+      tm.begin();
+      launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st);
+      ctx->launches++;
+      CKL();
+      TRY(sync_ctl(ctx, st));
+      if (ctx->h_ctl->pairs_ready) {
+        tm.end(CAFS_STAGE_EMIT);
+        tel->counted_total = n;
+        tel->pairs = (u64)c.nkeys;
+        break;
+      }
+      // the sample missed a value: MAIN with the same k_hat (sorter.py:378-385)
+      tel->tiny_count_failed = 1;
+      tel->decision.route = CAFS_MAIN;
+      tel->table_buckets = table_size_for(c.k_hat > 1.0 ? c.k_hat : 1.0, n, 4);
+      rc = run_main(ctx, x, n, flip, hash_mult, flags, tel, tm, st);
+      break;
+    }
+    default:
+      tel->table_buckets = table_size_for(c.k_hat > 1.0 ? c.k_hat : 1.0, n, 4);
+      rc = run_main(ctx, x, n, flip, hash_mult, flags, tel, tm, st);
+      break;
+  }
+  if (rc != CAFS_OK) return rc;
+  CK(cudaStreamSynchronize(st));
+  tel->kernels_launched = ctx->launches;
+  return CAFS_OK;
+}
+
+int cafs_sort_i64_host(cafs_ctx_t* ctx, const int64_t* h_in, int64_t* h_out, uint64_t n,
+                       int is_signed, uint64_t hash_mult, uint32_t flags, cafs_telemetry_t* tel,
+                       void* stream) {
+  if (!ctx) return CAFS_EINVAL;
+  if (n >= (1ull << 32)) return fail(ctx, CAFS_EINVAL, "arrays of 2**32 or more elements");
+  if (n > 0 && (!h_in || !h_out)) return fail(ctx, CAFS_EINVAL, "null host pointer");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n > ctx->stage_elems) {
+    if (ctx->stage) CK(cudaFree(ctx->stage));
+    ctx->stage = nullptr;
+    ctx->stage_elems = 0;
+    CK(cudaMalloc(&ctx->stage, (n ? n : 1) * 8));
+    ctx->stage_elems = n;
+  }
+  if (n) CK(cudaMemcpyAsync(ctx->stage, h_in, n * 8, cudaMemcpyHostToDevice, st));
+  TRY(cafs_sort_i64(ctx, (int64_t*)ctx->stage, n, is_signed, hash_mult, flags, tel, stream));
+  if (n) CK(cudaMemcpyAsync(h_out, ctx->stage, n * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return CAFS_OK;
+}
+
+int cafs_dispatch_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                      uint64_t hash_mult, cafs_decision_t* out, void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  if (!out || n < 2) return fail(ctx, CAFS_EINVAL, "dispatch needs n >= 2");
+  if ((hash_mult & 1) == 0) return fail(ctx, CAFS_EINVAL, "hash multiplier must be odd");
+  DeviceGuard g(ctx->device);
+  bool mono;
+  int route;
+  TRY(run_dispatch(ctx, (const u64*)d_x, n, is_signed ? kSign : 0, (cudaStream_t)stream, &mono,
+                   &route));
+  fill_decision(*ctx->h_ctl, route, !mono && n >= CAFS_SMALL_N_CUTOFF, out);
+  return CAFS_OK;
+}
+
+int cafs_estimate_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                      cafs_estimate_t* out, void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  if (!out || n < 1) return fail(ctx, CAFS_EINVAL, "n must be >= 1");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_estimate((const u64*)d_x, n, is_signed ? kSign : 0, 0, ctx->d_ctl, st);
+  CKL();
+  TRY(sync_ctl(ctx, st));
+  cafs_decision_t d;
+  fill_decision(*ctx->h_ctl, 0, true, &d);
+  *out = d.est;
+  return CAFS_OK;
+}
+
+int cafs_is_monotone_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed, int* out,
+                         void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  if (!out) return CAFS_EINVAL;
+  if (n < 2) { *out = 1; return CAFS_OK; }
+  DeviceGuard g(ctx->device);
+  bool mono;
+  int route;
+  TRY(run_dispatch(ctx, (const u64*)d_x, n, is_signed ? kSign : 0, (cudaStream_t)stream, &mono,
+                   &route));
+  *out = mono ? 1 : 0;
+  return CAFS_OK;
+}
+
+int cafs_tiny_counts_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                         const uint64_t* h_keys, int nk, int64_t* h_counts, void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  if (nk < 0 || nk > CAFS_TINY_MAX_KEYS || (nk && (!h_keys || !h_counts)))
+    return fail(ctx, CAFS_EINVAL, "tiny-count takes at most 8 keys");
+  if (nk == 0) return CAFS_OK;
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  // distinct keys -> perfect hash into 16 slots
+  u64 uk[CAFS_TINY_MAX_KEYS];
+  int nu = 0, map[CAFS_TINY_MAX_KEYS];
+  for (int j = 0; j < nk; ++j) {
+    int f = -1;
+    for (int q = 0; q < nu; ++q)
+      if (uk[q] == h_keys[j]) f = q;
+    if (f < 0) { uk[nu] = h_keys[j]; f = nu++; }
+    map[j] = f;
+  }
+  DevCtl& c = *ctx->h_ctl;
+  memset(&c, 0, sizeof(c));
+  c.nkeys = nu;
+  for (int q = 0; q < nu; ++q) c.keys[q] = uk[q];
+  for (u64 t = 0;; ++t) {
+    const u64 m = host_fmix64(t + 0x5851F42D4C957F2Dull) | 1ull;
+    u32 used = 0;
+    bool ok = true;
+    for (int q = 0; q < nu; ++q) {
+      const u32 s = (u32)((uk[q] * m) >> 60);
+      ok &= !((used >> s) & 1u);
+      used |= 1u << s;
+    }
+    if (ok) {
+      c.tiny_mult = m;
+      for (int q = 0; q < nu; ++q) c.tiny_slot[q] = (int)((uk[q] * m) >> 60);
+      break;
+    }
+  }
+  CK(cudaMemcpyAsync(ctx->d_ctl, &c, sizeof(DevCtl), cudaMemcpyHostToDevice, st));
+  if (n) launch_tiny_count((const u64*)d_x, n, is_signed ? kSign : 0, ctx->d_ctl, ctx->num_sms, st);
+  CKL();
+  TRY(sync_ctl(ctx, st));
+  for (int j = 0; j < nk; ++j) h_counts[j] = (int64_t)ctx->h_ctl->tiny_counts[c.tiny_slot[map[j]]];
+  return CAFS_OK;
+}
+
+int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                         uint64_t hash_mult, uint64_t* d_keys, uint64_t* d_counts, uint64_t cap,
+                         uint64_t* h_npairs, void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  if (!h_npairs || (hash_mult & 1) == 0) return fail(ctx, CAFS_EINVAL, "bad arguments");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  *h_npairs = 0;
+  if (n == 0) return CAFS_OK;
+  TRY(ensure_main(ctx));
+  // the estimate kernel resets the per-call control block and sets the range window
+  launch_estimate((const u64*)d_x, n, is_signed ? kSign : 0, 0, ctx->d_ctl, st);
+  cudaError_t e = launch_hash_count((const u64*)d_x, n, is_signed ? kSign : 0, hash_mult,
+                                    ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
+                                    ctx->num_sms, st);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
+  launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
+                 ctx->num_sms, st);
+  e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, n, ctx->pk_b, ctx->pc_b,
+                              ctx->poffs, st);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+  TRY(sync_ctl(ctx, st));
+  DevCtl c = *ctx->h_ctl;
+  if (c.overflow) {
+    CK(cudaMemsetAsync(ctx->gkeys, 0xFF, kGlobalSlots * 8, st));
+    CK(cudaMemsetAsync(ctx->gcnt, 0, kGlobalSlots * 8, st));
+    CK(cudaStreamSynchronize(st));
+    return fail(ctx, CAFS_EINVAL, "more distinct keys than the global table holds");
+  }
+  const u64 np = c.npairs;
+  if (c.need_large) {
+    TRY(ensure_radix(ctx, np, false));
+    u64 *rk, *rv;
+    TRY(radix_sort(ctx, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, np, 0, st, &rk, &rv));
+    if (rk != ctx->pk_b) {
+      CK(cudaMemcpyAsync(ctx->pk_b, rk, np * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(ctx->pc_b, rv, np * 8, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  *h_npairs = np;
+  if (np > cap) return fail(ctx, CAFS_EINVAL, "output capacity too small");
+  CK(cudaMemcpyAsync(d_keys, ctx->pk_b, np * 8, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(d_counts, ctx->pc_b, np * 8, cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  return CAFS_OK;
+}
+
+int cafs_pair_sort(cafs_ctx_t* ctx, uint64_t* d_keys, uint64_t* d_counts, uint64_t npairs,
+                   void* stream) {
+  if (!ctx) return CAFS_EINVAL;
+  if (npairs > kGlobalCap) return fail(ctx, CAFS_EINVAL, "too many pairs");
+  if (npairs < 2) return CAFS_OK;
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(ensure_main(ctx));
+  if (npairs <= kSmallSortMax) {
+    CK(cudaMemcpyAsync(ctx->pk_a, d_keys, npairs * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(ctx->pc_a, d_counts, npairs * 8, cudaMemcpyDeviceToDevice, st));
+    cudaError_t e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, npairs, nullptr, 0, (u64*)d_keys,
+                                            (u64*)d_counts, ctx->poffs, st);
+    if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+  } else {
+    TRY(ensure_radix(ctx, npairs, false));
+    u64 *rk, *rv;
+    TRY(radix_sort(ctx, (u64*)d_keys, (u64*)d_counts, ctx->pk_b, ctx->pc_b, npairs, 0, st, &rk,
+                   &rv));
+    if (rk != (u64*)d_keys) {
+      CK(cudaMemcpyAsync(d_keys, rk, npairs * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(d_counts, rv, npairs * 8, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  return CAFS_OK;
+}
+
+int cafs_emit_i64(cafs_ctx_t* ctx, const uint64_t* d_keys, const uint64_t* d_counts,
+                  uint64_t npairs, int64_t* d_out, uint64_t out_begin, uint64_t out_end,
+                  uint64_t total, int is_signed, void* stream) {
+  if (!ctx) return CAFS_EINVAL;
+  if (out_begin > out_end || out_end > total || npairs > kGlobalCap)
+    return fail(ctx, CAFS_EINVAL, "bad output slice");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(ensure_main(ctx));
+  DevCtl& c = *ctx->h_ctl;
+  memset(&c, 0, sizeof(c));
+  CK(cudaMemcpyAsync(ctx->d_ctl, &c, sizeof(DevCtl), cudaMemcpyHostToDevice, st));
+  launch_scan((const u64*)d_counts, npairs, ctx->bsum, ctx->poffs, ctx->d_ctl, total, st);
+  if (npairs && out_end > out_begin)
+    launch_emit((const u64*)d_keys, ctx->poffs, 0, ctx->d_ctl, (u64*)d_out, out_begin, out_end,
+                is_signed ? kSign : 0, ctx->num_sms, st);
+  CKL();
+  TRY(sync_ctl(ctx, st));
+  if (ctx->h_ctl->sum_error)
+    return fail(ctx, CAFS_ESUM, "pair counts do not sum to the output length");
+  return CAFS_OK;
+}
+
+int cafs_fallback_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed,
+                           void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(fallback_sort(ctx, (u64*)d_x, n, is_signed ? kSign : 0, st));
+  CK(cudaStreamSynchronize(st));
+  return CAFS_OK;
+}
+
+int cafs_gen_mix(uint64_t* d_out, uint64_t count, uint64_t seed, uint64_t skip, void* stream) {
+  if (count && !d_out) return CAFS_EINVAL;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (count) launch_gen_mix((u64*)d_out, count, seed, skip, sms, (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? CAFS_OK : CAFS_ECUDA;
+}
+
+int cafs_gen_draw(int64_t* d_out, uint64_t n, uint64_t start, uint64_t seed,
+                  const int64_t* d_palette, uint64_t k, const double* d_cdf, void* stream) {
+  if ((n && !d_out) || k == 0 || k >= (1ull << 32)) return CAFS_EINVAL;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (n)
+    launch_gen_draw((u64*)d_out, n, start, seed, (const u64*)d_palette, k, d_cdf, sms,
+                    (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? CAFS_OK : CAFS_ECUDA;
+}
+
+}  // extern "C"

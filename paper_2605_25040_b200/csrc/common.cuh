@@ -1,0 +1,157 @@
+// common.cuh -- shared device helpers and the device control block.
+//
+// B200 (sm_100a) only.  All kernels fold the int64 -> uint64 order map
+// (bit-63 flip, reference sorter.py:84-94) into their loads and stores, so no
+// pass ever materialises the unsigned copy the reference allocates.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/cafs_b200.h"
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+namespace cafs {
+
+constexpr u64 kSign = 0x8000000000000000ull;
+constexpr u64 kGamma = 0x9E3779B97F4A7C15ull;
+constexpr u64 kEmpty = ~0ull;            // empty-slot sentinel of the hash tables
+constexpr int kSampleTarget = 1024;      // cardinality.py:26
+constexpr u64 kMonoPrefix = 1u << 16;    // rows the dispatch kernel checks for an inversion
+
+// Global (L2-resident) (key, count) table of the main route.
+constexpr int kGlobalLog2 = 22;                       // 4 Mi slots: 32 MB keys + 32 MB counts
+constexpr u64 kGlobalSlots = 1ull << kGlobalLog2;
+constexpr u64 kGlobalCap = kGlobalSlots / 2;          // max distinct keys before the guard fires
+constexpr int kGlobalMaxProbe = 128;
+
+// Device control block: dispatch result + per-call flags/counters.
+struct DevCtl {
+  // --- dispatch (estimate kernel) ---
+  int32_t route;           // route assuming the input is not monotone
+  int32_t prefix_sorted;   // no inversion within the first kMonoPrefix rows
+  int32_t scan_inversion;  // full monotone scan found an inversion
+  int32_t saturated;
+  int64_t u, f1, f2;
+  double k_hat;
+  int32_t nkeys;
+  int32_t _pad0;
+  u64 keys[CAFS_TINY_MAX_KEYS];  // ascending, unsigned domain
+  u64 tiny_mult;                 // perfect-hash multiplier for the tiny keys (16 slots)
+  int32_t tiny_slot[CAFS_TINY_MAX_KEYS];
+  u64 range_base;                // dense-range direct-count window (unsigned domain)
+  u32 range_len;                 // 0 = disabled
+  u32 _pad1;
+  // --- tiny route ---
+  u64 tiny_counts[16];           // per perfect-hash slot
+  u64 tiny_miss;
+  // --- main route ---
+  u64 g_used;                    // occupied global slots (append-list length)
+  u64 g_updates;                 // elements resolved in the global table
+  u64 empty_key_count;           // occurrences of the sentinel key value ~0
+  int32_t overflow;              // global table overflow -> guard
+  int32_t need_large;            // K' too large for the single-CTA pair sort
+  u64 npairs;
+  u64 total;                     // sum of pair counts
+  int32_t pairs_ready;
+  int32_t sum_error;
+};
+
+__device__ __forceinline__ u64 fmix64(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// buckets.py:70-85 fast_hash: top m bits of the 64-bit product
+__device__ __forceinline__ u32 mhash(u64 v, u64 mult, int shift) {
+  return (u32)((v * mult) >> shift);
+}
+
+__device__ __forceinline__ ulonglong2 ld_stream_v2(const void* p) {
+  ulonglong2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
+               : "=l"(v.x), "=l"(v.y) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_stream_v2(void* p, u64 a, u64 b) {
+  asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(a), "l"(b)
+               : "memory");
+}
+
+// ---- mbarrier / TMA bulk copy (PTX ISA: mbarrier, cp.async.bulk) ----
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+  return (u32)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared, completion on an mbarrier (bytes % 16 == 0)
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gsrc, u32 bytes,
+                                            u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(0x12F0000000000000ull)  // evict_first
+      : "memory");
+}
+
+__device__ __forceinline__ u32 lanemask_lt() {
+  u32 m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Insert (key, inc) into the global open-addressing table (linear probing).
+// Claims append the slot to `list` so compaction touches only occupied slots.
+__device__ __forceinline__ void global_insert(u64* gkeys, u64* gcnt, u32* list, DevCtl* ctl,
+                                              u64 key, u64 inc, u64 mult) {
+  u32 h = mhash(key, mult, 64 - kGlobalLog2);
+  for (int p = 0; p < kGlobalMaxProbe; ++p) {
+    u64 k = *((volatile u64*)&gkeys[h]);
+    if (k == kEmpty) {
+      u64 old = atomicCAS(&gkeys[h], kEmpty, key);
+      if (old == kEmpty) {
+        u64 idx = atomicAdd(&ctl->g_used, 1ull);
+        if (idx < kGlobalCap) list[idx] = h;
+        else ctl->overflow = 1;
+        atomicAdd(&gcnt[h], inc);
+        return;
+      }
+      k = old;
+    }
+    if (k == key) {
+      atomicAdd(&gcnt[h], inc);
+      return;
+    }
+    h = (h + 1) & (u32)(kGlobalSlots - 1);
+  }
+  ctl->overflow = 1;
+}
+
+}  // namespace cafs

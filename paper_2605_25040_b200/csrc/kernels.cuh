@@ -1,0 +1,48 @@
+// kernels.cuh -- host-side launchers of the device kernels (internal).
+#pragma once
+
+#include "common.cuh"
+
+namespace cafs {
+
+constexpr u32 kSmallSortMax = 8192;  // single-CTA bitonic sort capacity (keys or pairs)
+
+// estimate.cu
+void launch_estimate(const u64* x, u64 n, u64 flip, int check_prefix, DevCtl* ctl,
+                     cudaStream_t st);
+void launch_monotone_scan(const u64* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
+                          cudaStream_t st);
+// tiny.cu
+void launch_tiny_count(const u64* x, u64 n, u64 flip, DevCtl* ctl, int num_sms, cudaStream_t st);
+void launch_tiny_finalize(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,
+                          cudaStream_t st);
+// hashcount.cu
+size_t hash_count_smem();
+cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
+                              u64* gcnt, u32* glist, int use_range, int num_sms, cudaStream_t st);
+void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys, u64* pcnt,
+                    int num_sms, cudaStream_t st);
+// emit.cu
+void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, u64* out,
+                 u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st);
+// radix.cu
+size_t onesweep_smem(bool has_val);
+u64 onesweep_tiles(u64 n);
+void launch_radix_hist(const u64* keys, u64 n, u64 flip, u32* ghist, int num_sms,
+                       cudaStream_t st);
+void launch_radix_prep(const u32* ghist, u64 n, u32* gbase, int* trivial, cudaStream_t st);
+cudaError_t launch_onesweep(const u64* src, const u64* srcv, u64* dst, u64* dstv, u64 n, int pass,
+                            u64 flip_in, u64 flip_out, const u32* gbase, u64* tile_state,
+                            u32* tile_counter, u32 epoch, cudaStream_t st);
+size_t small_sort_smem();
+cudaError_t launch_small_sort_keys(u64* keys, u64 n, u64 flip, cudaStream_t st);
+cudaError_t launch_small_sort_pairs(u64* keys, const u64* cnt, u64 n, DevCtl* ctl, u64 expect,
+                                    u64* out_keys, u64* out_cnt, u64* out_offs, cudaStream_t st);
+void launch_scan(const u64* in, u64 n, u64* bsum, u64* out_offs, DevCtl* ctl, u64 expect,
+                 cudaStream_t st);
+// gen.cu
+void launch_gen_mix(u64* out, u64 count, u64 seed, u64 skip, int num_sms, cudaStream_t st);
+void launch_gen_draw(u64* out, u64 n, u64 start, u64 seed, const u64* palette, u64 k,
+                     const double* cdf, int num_sms, cudaStream_t st);
+
+}  // namespace cafs

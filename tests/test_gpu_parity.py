@@ -1,0 +1,299 @@
+"""GPU parity: the sm_100a pipeline against the oracle and the reference's goldens.
+
+Every case compares the sorted bytes (bit-exact) and the dispatch tuple
+(route, k_hat, u, f1, f2, saturated, tiny keys, tiny_count_failed) with the
+values the real reference produced (tests/golden/*.json), and where useful
+with the C oracle run on the same box.  All calls go through the package's
+public API and therefore the C ABI of libcafs_b200.so.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import load_json, special_input, sweep_input  # noqa: E402
+from oracle import cafs_oracle as orc  # noqa: E402
+from oracle import gen as ogen  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2605_25040_b200 as cafs  # noqa: E402
+from paper_2605_25040_b200 import Route, SortTelemetry  # noqa: E402
+
+
+def sha(a) -> str:
+    if isinstance(a, torch.Tensor):
+        a = a.cpu().numpy()
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def to_dev(x: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def check_decision(tel: SortTelemetry, rec: dict):
+    assert tel.route.value == rec["route"]
+    assert tel.tiny_count_failed == rec.get("tiny_count_failed", False)
+    if rec["k_hat"] is None:
+        assert tel.decision.estimate is None
+    else:
+        e = tel.decision.estimate
+        assert (e.k_hat, e.u, e.f1, e.f2, e.saturated) == (
+            rec["k_hat"], rec["u"], rec["f1"], rec["f2"], rec["saturated"])
+    if rec["route"] == "main" and "table_buckets" in rec:
+        assert tel.table_buckets == rec["table_buckets"]
+
+
+def run_case(x: np.ndarray, rec: dict, mult=None):
+    t = to_dev(x)
+    tel = SortTelemetry()
+    cafs.cafs_sort(t, telemetry=tel, hash_mult=mult)
+    torch.cuda.synchronize()
+    assert sha(t) == rec["sha256"], "sorted bytes differ from the reference"
+    check_decision(tel, rec)
+    if x.shape[0] > 1:
+        d = cafs.dispatch(to_dev(x), hash_mult=mult)
+        assert d.route.value == rec["dispatch_route"]
+        if rec.get("tiny_keys") is not None:
+            assert d.keys.tolist() == rec["tiny_keys"]
+    assert set(tel.stage_ms) <= {"count", "sort_k", "emit"}
+    return tel
+
+
+@pytest.mark.parametrize("rec", load_json("special_cases.json"), ids=lambda r: r["name"])
+def test_special_cases(rec):
+    x = special_input(rec["name"])
+    tel = run_case(x, rec, rec.get("hash_mult"))
+    # stage labels as the reference records them (the GPU guard is its own)
+    if not tel.guard_fired and not rec["guard_fired"]:
+        assert sorted(tel.stage_ms) == rec["stage_keys"]
+
+
+def test_reference_sweep():
+    cases = load_json("sweep_cases.json")
+    routes = set()
+    for rec in cases:
+        tel = run_case(sweep_input(rec), rec)
+        routes.add(tel.route)
+    assert routes == set(Route)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5"])
+def test_baseline_config(name):
+    rec = {r["name"]: r for r in load_json("config_cases.json")}[name]
+    x = ogen.CONFIGS[name].generate()
+    tel = run_case(x, rec)
+    assert tel.counted_total in (0, x.shape[0])
+
+
+def _device_config(name, n=None, start=0):
+    c = ogen.CONFIGS[name]
+    n = c.n - start if n is None else n
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    pal = None if c.palette == "codes" else to_dev(c.palette_values())
+    cdf = None if c.dist != "zipf" else to_dev(c.cdf())
+    lib = cafs.sorter._lib.load()
+    rc = lib.cafs_gen_draw(out.data_ptr(), n, start, c.seed, 0 if pal is None else pal.data_ptr(),
+                           c.k, 0 if cdf is None else cdf.data_ptr(),
+                           torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    return out
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+def test_device_generator_matches_numpy(name):
+    c = ogen.CONFIGS[name]
+    for start in (0, c.n // 3, c.n - 5000):
+        d = _device_config(name, 5000, start).cpu().numpy()
+        assert np.array_equal(d, c.generate(5000, start))
+
+
+def test_cfg4_full_size_properties():
+    """N = 2^30: sortedness, per-code histogram and the dispatch tuple."""
+    rec = {r["name"]: r for r in load_json("config_cases.json")}["cfg4"]
+    x = _device_config("cfg4")
+    hist_in = torch.bincount(x, minlength=4096)
+    tel = SortTelemetry()
+    cafs.cafs_sort(x, telemetry=tel)
+    torch.cuda.synchronize()
+    check_decision(tel, rec)
+    assert not tel.guard_fired and tel.counted_total == x.shape[0]
+    assert bool((x[1:] >= x[:-1]).all())
+    assert torch.equal(torch.bincount(x, minlength=4096), hist_in)
+    del x
+
+
+def test_numpy_dropin_matches_reference():
+    """numpy input takes the host entry point (H2D, device pipeline, D2H)."""
+    for rec in load_json("special_cases.json")[:8]:
+        x = special_input(rec["name"])
+        tel = SortTelemetry()
+        cafs.cafs_sort(x, telemetry=tel, hash_mult=rec.get("hash_mult"))
+        assert sha(x) == rec["sha256"]
+        check_decision(tel, rec)
+
+
+@pytest.mark.parametrize("dtype", [np.int64, np.uint64, np.int32, np.uint32])
+@pytest.mark.parametrize("seed", range(3))
+def test_all_dtypes_torch_and_numpy(dtype, seed):
+    rng = np.random.default_rng(seed * 31 + 1)
+    info = np.iinfo(dtype)
+    n = int(rng.integers(2, 200_000))
+    k = int(rng.integers(1, min(n, 3000)))
+    pal = rng.integers(info.min, int(info.max) + 1, k, dtype=dtype)
+    x = pal[rng.integers(0, k, n)]
+    want = np.sort(x)
+    y = x.copy()
+    cafs.cafs_sort(y)
+    assert np.array_equal(y, want)
+    t = torch.from_numpy(x.copy()).cuda()
+    cafs.cafs_sort(t)
+    assert np.array_equal(t.cpu().numpy(), want)
+
+
+def test_strided_views():
+    base = ogen.gen_input(40_000, 32)
+    x = base[::2]
+    want = np.sort(x)
+    cafs.cafs_sort(x)
+    assert np.array_equal(x, want)
+    t = torch.from_numpy(ogen.gen_input(40_000, 32).view(np.int64)).cuda()[::2]
+    want = np.sort(t.cpu().numpy())
+    cafs.cafs_sort(t)
+    assert np.array_equal(t.cpu().numpy(), want)
+
+
+def test_empty_singleton_and_two():
+    for x in (np.empty(0, np.int64), np.array([9], np.int64)):
+        tel = SortTelemetry()
+        cafs.cafs_sort(x, telemetry=tel)
+        assert tel.route is Route.ALREADY_SORTED
+    t = torch.tensor([5, -3], dtype=torch.int64, device="cuda")
+    tel = SortTelemetry()
+    cafs.cafs_sort(t, telemetry=tel)
+    assert t.tolist() == [-3, 5] and tel.route is Route.FALLBACK_SMALL_N
+
+
+def test_sliced_unaligned_tensor():
+    """x[1:] is 8-byte but not 16-byte aligned: head/tail paths of every kernel."""
+    for name in ("cfg1", "cfg2", "cfg5"):
+        full = torch.from_numpy(ogen.CONFIGS[name].generate(300_001)).cuda()
+        t = full[1:]
+        want = np.sort(t.cpu().numpy())
+        cafs.cafs_sort(t)
+        assert np.array_equal(t.cpu().numpy(), want)
+        assert full[0].item() == ogen.CONFIGS[name].generate(1)[0]
+
+
+def test_stage_apis_against_oracle():
+    x = ogen.CONFIGS["cfg1"].generate(200_000)
+    est = cafs.sample_and_estimate(to_dev(x))
+    oe = orc.sample_and_estimate(x)
+    assert (est.k_hat, est.u, est.f1, est.f2, est.saturated) == (
+        oe.k_hat, oe.u, oe.f1, oe.f2, oe.saturated)
+    e = cafs.sample_and_estimate(np.array([3, 3, 5], np.uint64))
+    assert (e.u, e.f1, e.f2, e.k_hat) == (2, 1, 1, min(2 + 1 / 4, 3))
+    e = cafs.sample_and_estimate(np.full(1024, 7, np.uint64))
+    assert (e.k_hat, e.u, e.f1, e.f2, e.saturated) == (1.0, 1, 0, 0, False)
+    # tiny counts (keys in the unsigned domain of the array)
+    x2 = ogen.CONFIGS["cfg2"].generate(100_000)
+    vals = np.unique(x2)  # int64, the array's own domain
+    got = cafs.tiny_counts(to_dev(x2), vals)
+    assert got.tolist() == orc.tiny_counts(x2, vals.view(np.uint64) ^ np.uint64(1 << 63)).tolist()
+    assert int(got.sum()) == x2.shape[0]
+    # monotone
+    assert cafs.is_monotone(to_dev(np.arange(200_000, dtype=np.int64)))
+    y = np.arange(200_000, dtype=np.int64)
+    y[150_000] = -1
+    assert not cafs.is_monotone(to_dev(y))
+    assert cafs.is_monotone(np.array([-5, -1, 0, 3], np.int64))
+    assert not cafs.is_monotone(np.array([0, -1], np.int64))
+
+
+def test_tiny_count_sort_semantics():
+    rng = np.random.default_rng(1)
+    keys = np.arange(1, 9, dtype=np.uint64)
+    x = keys[rng.integers(0, 8, 5000)]
+    x[17] = 1000
+    out = np.full_like(x, 77)
+    assert not cafs.tiny_count_sort(x, keys, out)
+    assert np.all(out == 77)
+    x = np.array([2, 1, 2, 1, 1], np.uint64)
+    assert cafs.tiny_count_sort(x, np.array([1, 2], np.uint64), x)
+    assert x.tolist() == [1, 1, 1, 2, 2]
+    with pytest.raises(ValueError):
+        cafs.tiny_count_sort(np.zeros(4, np.uint64), np.arange(9, dtype=np.uint64),
+                             np.zeros(4, np.uint64))
+
+
+@pytest.mark.parametrize("n", [1, 5, 255, 256, 8192, 8193, 100_000])
+def test_pair_sort_and_emit(n):
+    rng = np.random.default_rng(n)
+    keys = np.unique(rng.integers(0, 1 << 64, n, dtype=np.uint64))
+    rng.shuffle(keys)
+    counts = rng.integers(1, 5, keys.shape[0]).astype(np.int64)
+    pl = cafs.pair_sort(cafs.PairList(keys, counts))
+    order = np.argsort(keys)
+    assert np.array_equal(pl.keys, keys[order]) and np.array_equal(pl.counts, counts[order])
+    out = np.empty(int(counts.sum()), np.uint64)
+    cafs.emit(pl, out)
+    assert np.array_equal(out, np.repeat(keys[order], counts[order]))
+    with pytest.raises(ValueError):
+        cafs.emit(pl, np.empty(int(counts.sum()) + 1, np.uint64))
+
+
+def test_fallback_sort_large_random():
+    for n in (8191, 8192, 8193, 1_000_003):
+        x = ogen.mix_outputs(n, n).view(np.int64)
+        want = np.sort(x)
+        t = to_dev(x)
+        cafs.fallback_sort(t)
+        assert np.array_equal(t.cpu().numpy(), want)
+
+
+def test_guard_reroutes_to_fallback():
+    """More distinct keys than the global table holds, under a low estimate."""
+    n = 5_000_000
+    x = ogen.mix_outputs(77, n).view(np.int64).copy()
+    stride = n // 1024
+    x[::stride][:1024] = np.arange(1024, dtype=np.int64) % 100  # sample sees 100 keys
+    want = np.sort(x)
+    t = to_dev(x)
+    tel = SortTelemetry()
+    cafs.cafs_sort(t, telemetry=tel)
+    assert tel.route is Route.MAIN and tel.guard_fired
+    assert np.array_equal(t.cpu().numpy(), want)
+
+
+def test_hash_mult_validation_and_override():
+    x = to_dev(ogen.gen_input(100_000, 300).view(np.int64))
+    with pytest.raises(ValueError):
+        cafs.cafs_sort(x, hash_mult=2)
+    want = np.sort(x.cpu().numpy())
+    cafs.cafs_sort(x, hash_mult=0xC2B2AE3D27D4EB4F)
+    assert np.array_equal(x.cpu().numpy(), want)
+
+
+def test_direct_range_off_matches():
+    x = ogen.CONFIGS["cfg4"].generate(3_000_000)
+    want = np.sort(x)
+    for direct in (True, False):
+        t = to_dev(x)
+        cafs.cafs_sort(t, direct_range=direct)
+        assert np.array_equal(t.cpu().numpy(), want)
+
+
+def test_determinism_and_repeat_calls():
+    x = ogen.CONFIGS["cfg3"].generate(2_000_000)
+    outs = set()
+    for _ in range(3):
+        t = to_dev(x)
+        cafs.cafs_sort(t)
+        outs.add(sha(t))
+    assert len(outs) == 1 and outs == {sha(np.sort(x))}
