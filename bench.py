@@ -1,0 +1,338 @@
+#!/usr/bin/env python3
+"""Benchmark: int64 keys sorted/sec on B200 (BASELINE.json metric), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl b200|reference]
+
+N > 1 runs under torchrun (one process per GPU, NCCL); the column of the config
+is sharded by rows and sorted with ``cafs_sort_sharded`` (strong scaling: the
+total N is fixed).  A "step" is one full ``cafs_sort`` of the config's column
+with the input resident in HBM; between steps the unsorted input is restored
+by a device-to-device copy that is NOT timed (each sort is bracketed by CUDA
+events on the launching stream; the step times are summed, max over ranks).
+The input (8 GiB for cfg4) is far larger than the 126 MB L2.
+
+``e2e`` is the same metric through the C ABI host entry point
+(``cafs_sort_i64_host``: pinned host buffer -> H2D -> device pipeline -> D2H).
+``--impl reference`` times the reference algorithm's CPU restatement
+(oracle/, single-threaded like the reference) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "int64 keys sorted/sec (Gkeys/s) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "Gkeys/s"
+
+
+def measured_peaks() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy r+w)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        loaded = [r for r in self.rows if (num(r[4]) or 0) > 0] or self.rows
+        sm = [num(r[1]) for r in loaded if num(r[1]) is not None]
+        mx = [num(r[2]) for r in self.rows if num(r[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows), "samples_under_load": len(loaded)}
+
+
+def ncu_traffic(config: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(config)
+    except Exception:
+        return None
+
+
+def cpu_baseline(config: str, rows: int) -> dict:
+    """The C oracle (a restatement of the reference algorithm; 1 thread, like the
+    reference) timed on a bounded sample of the same workload."""
+    from oracle import cafs_oracle as orc
+    from oracle import gen as ogen
+
+    c = ogen.CONFIGS[config]
+    rows = min(rows, c.n)
+    x = c.generate(rows, 0)
+    best = float("inf")
+    for _ in range(2):
+        y = x.copy()
+        t0 = time.perf_counter()
+        orc.cafs_sort(y)
+        best = min(best, time.perf_counter() - t0)
+    return {"value": rows / best / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"first {rows} rows of {config} (C restatement of the reference, "
+                      f"min of 2, {best * 1e3:.1f} ms; nproc={os.cpu_count()})"}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import cafs_oracle as orc
+    from oracle import gen as ogen
+
+    c = ogen.CONFIGS[args.config]
+    rows = min(args.cpu_rows, c.n)
+    x = c.generate(rows, 0)
+    for _ in range(args.warmup):
+        orc.cafs_sort(x.copy())
+    times = []
+    for _ in range(args.steps):
+        y = x.copy()
+        t0 = time.perf_counter()
+        orc.cafs_sort(y)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = rows * args.steps / tot / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": args.config, "n": rows, "k": c.k, "sample_of_n": c.n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"first {rows} rows of {args.config}; C restatement of the "
+                                   "reference (single-threaded by design, SPEC.md:284); "
+                                   f"nproc={os.cpu_count()}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-rows", type=int, default=1 << 24)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-direct", action="store_true", help="disable the dense-range count path")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+
+    import paper_2605_25040_b200 as cafs
+    from paper_2605_25040_b200 import _lib, datagen
+    from paper_2605_25040_b200.sharded import cafs_sort_sharded
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = datagen.CONFIGS[args.config]
+    N = cfg.n
+    per = N // world
+    start = rank * per
+    n_local = per if rank < world - 1 else N - per * (world - 1)
+    pristine = datagen.generate(cfg, n_local, start)
+    x = torch.empty_like(pristine)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def one_step(tel):
+        if world == 1:
+            cafs.cafs_sort(x, telemetry=tel, direct_range=not args.no_direct)
+        else:
+            cafs_sort_sharded(x, telemetry=tel)
+
+    for _ in range(args.warmup):
+        x.copy_(pristine)
+        one_step(cafs.SortTelemetry())
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    tels = []
+    barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        x.copy_(pristine)  # restore the unsorted input (untimed)
+        tel = cafs.SortTelemetry()
+        ev0[i].record(stream)
+        one_step(tel)
+        ev1[i].record(stream)
+        tels.append(tel)
+    torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - wall0
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    tot_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([tot_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    clk = clocks.stop()
+
+    # correctness of the last step (cheap property checks at full size)
+    ok = bool((x[1:] >= x[:-1]).all().item())
+    if cfg.palette == "codes":
+        ok &= bool(torch.equal(torch.bincount(x, minlength=cfg.k),
+                               torch.bincount(pristine, minlength=cfg.k)))
+
+    value = N * args.steps / (tot_ms / 1e3) / 1e9
+    peak, peak_src = measured_peaks()
+    t0 = tels[-1]
+    route = t0.route.value if t0.route else None
+    # dominant kernel of the step: the count pass (reads 8 B/key) or the emit (writes 8 B/key)
+    k_count = [t.kernel_ms.get("count_kernel") for t in tels if "count_kernel" in t.kernel_ms]
+    k_emit = [t.kernel_ms.get("emit_kernel") for t in tels if "emit_kernel" in t.kernel_ms]
+    roof = None
+    kernels = {}
+    for name, vals, kname in (("count", k_count, "hash_count_kernel" if route == "main"
+                               else "tiny_count_kernel"), ("emit", k_emit, "emit_kernel")):
+        if vals:
+            avg = sum(vals) / len(vals)
+            gbs = n_local * 8 / (avg / 1e3) / 1e9
+            kernels[name] = {"kernel": kname, "avg_ms": avg, "GB/s": gbs,
+                             "share_of_step": avg / (tot_ms / args.steps)}
+    if kernels:
+        dom = max(kernels, key=lambda k: kernels[k]["avg_ms"])
+        d = kernels[dom]
+        roof = {"bound": "hbm", "kernel": d["kernel"], "achieved": d["GB/s"], "peak": peak,
+                "unit": "GB/s", "frac": d["GB/s"] / peak, "traffic": ncu_traffic(args.config),
+                "algorithmic_bytes_per_launch": n_local * 8, "peak_source": peak_src,
+                "step_frac": (16 * N / (tot_ms / args.steps / 1e3) / 1e9) / world / peak,
+                "kernels": kernels}
+
+    # ---- e2e through the C ABI host entry point (pinned host buffers) ----
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        h_in = torch.empty(N, dtype=torch.int64, pin_memory=True)
+        h_out = torch.empty(N, dtype=torch.int64, pin_memory=True)
+        h_in.copy_(pristine)
+        lib = _lib.load()
+        ctx = _lib.context(local)
+        tel_c = _lib.Telemetry()
+        lib.cafs_sort_i64_host(ctx, h_in.data_ptr(), h_out.data_ptr(), N, 1, cafs.HASH_MULT, 0,
+                               ctypes.byref(tel_c), stream.cuda_stream)  # warm
+        torch.cuda.synchronize()
+        e_t = []
+        for _ in range(args.e2e_steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            rc = lib.cafs_sort_i64_host(ctx, h_in.data_ptr(), h_out.data_ptr(), N, 1,
+                                        cafs.HASH_MULT, 0, ctypes.byref(tel_c), stream.cuda_stream)
+            b.record(stream)
+            b.synchronize()
+            _lib.check(rc, ctx, "cafs_sort_i64_host")
+            e_t.append(a.elapsed_time(b))
+        ok &= bool((h_out[1:] >= h_out[:-1]).all().item())
+        e2e = {"value": N * len(e_t) / (sum(e_t) / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": N * 8, "d2h_bytes_per_step": N * 8,
+               "ms_per_step": sum(e_t) / len(e_t),
+               "path": "cafs_sort_i64_host (C ABI), pinned host in/out buffers"}
+        del h_in, h_out
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.config, args.cpu_rows)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "data": f"synthetic, device-generated ({cfg.desc}; seed {cfg.seed})",
+            "config": {"workload": args.config, "n": N, "k": cfg.k, "dist": cfg.dist, "s": cfg.s,
+                       "route": route, "parallelism": f"rows sharded x{world}",
+                       "l2": "input 8 B x N >> 126 MB L2; unsorted input restored by an untimed "
+                             "D2D copy before each step",
+                       "direct_range": not args.no_direct},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(sum(t.kernels_launched for t in tels)),
+            "clocks": clk, "correct": ok, "wall_s_timed_region": wall,
+            "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms),
+                        "max": max(step_ms)},
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -18,6 +18,7 @@
  *   cafs_count_pairs_i64     sorter.py:183-196 + 254-288  main_count_loop -> reconstruct's
  *                            sorted (key, count) pairs (count_sequence _kernels.py:25-81,
  *                            fold_sorted :219-225, pair_sort :228-241)
+ *   cafs_merge_pairs         sorter.py:276-285   spill fold + union of pair lists (sharded merge)
  *   cafs_pair_sort           _kernels.py:185-214 radix_sort_pairs / sorter.py:228-241 pair_sort
  *   cafs_emit_i64            sorter.py:244-251 + _kernels.py:172-182  emit / emit_fill
  *   cafs_fallback_sort_i64   sorter.py:132-138   fallback_sort(x)
@@ -81,6 +82,8 @@ typedef struct {
 
 /* Stage indices of cafs_telemetry_t.stage_ms (sorter.py:64-66 labels) */
 enum { CAFS_STAGE_COUNT = 0, CAFS_STAGE_SORT_K = 1, CAFS_STAGE_EMIT = 2 };
+/* Kernel indices of cafs_telemetry_t.kernel_ms (single-kernel CUDA-event times) */
+enum { CAFS_KERNEL_COUNT = 0, CAFS_KERNEL_EMIT = 1, CAFS_KERNEL_ESTIMATE = 2 };
 
 /* cafs.sorter.SortTelemetry (sorter.py:60-81).  stage_ms[i] < 0: stage not run. */
 typedef struct {
@@ -93,6 +96,7 @@ typedef struct {
   uint64_t table_buckets;        /* reference table_size_for(max(1,k_hat), n, 4) on MAIN */
   uint64_t global_updates;       /* device: elements resolved in the L2 global table */
   float stage_ms[3];
+  float kernel_ms[4];            /* count kernel (hash or tiny), emit kernel, estimate kernel */
   uint32_t kernels_launched;     /* kernels this call put on the stream */
 } cafs_telemetry_t;
 
@@ -143,6 +147,13 @@ int cafs_tiny_counts_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
 int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
                          uint64_t hash_mult, uint64_t* d_keys, uint64_t* d_counts,
                          uint64_t cap, uint64_t* h_npairs, void* stream);
+
+/* Merge (key, count) pairs whose keys may repeat (e.g. the all-gathered tables
+ * of a sharded sort) into distinct pairs sorted by key with summed counts --
+ * the union + fold of reconstruct (sorter.py:276-285) across shards. */
+int cafs_merge_pairs(cafs_ctx_t* ctx, const uint64_t* d_keys_in, const uint64_t* d_counts_in,
+                     uint64_t m, uint64_t* d_keys, uint64_t* d_counts, uint64_t cap,
+                     uint64_t* h_npairs, void* stream);
 
 /* pair_sort: sort (key, count) pairs by unsigned key in place (keys distinct) */
 int cafs_pair_sort(cafs_ctx_t* ctx, uint64_t* d_keys, uint64_t* d_counts, uint64_t npairs,

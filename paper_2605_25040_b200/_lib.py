@@ -39,7 +39,8 @@ class Telemetry(ctypes.Structure):
                 ("tiny_count_failed", ctypes.c_int32), ("guard_fired", ctypes.c_int32),
                 ("counted_total", ctypes.c_uint64), ("pairs", ctypes.c_uint64),
                 ("table_buckets", ctypes.c_uint64), ("global_updates", ctypes.c_uint64),
-                ("stage_ms", ctypes.c_float * 3), ("kernels_launched", ctypes.c_uint32)]
+                ("stage_ms", ctypes.c_float * 3), ("kernel_ms", ctypes.c_float * 4),
+                ("kernels_launched", ctypes.c_uint32)]
 
 
 # every symbol include/cafs_b200.h declares, with its ctypes signature
@@ -61,6 +62,7 @@ SIGNATURES = {
     "cafs_tiny_counts_i64": (_I, [_P, _P, _U64, _I, ctypes.POINTER(_U64), _I,
                                   ctypes.POINTER(ctypes.c_int64), _P]),
     "cafs_count_pairs_i64": (_I, [_P, _P, _U64, _I, _U64, _P, _P, _U64, ctypes.POINTER(_U64), _P]),
+    "cafs_merge_pairs": (_I, [_P, _P, _P, _U64, _P, _P, _U64, ctypes.POINTER(_U64), _P]),
     "cafs_pair_sort": (_I, [_P, _P, _P, _U64, _P]),
     "cafs_emit_i64": (_I, [_P, _P, _P, _U64, _P, _U64, _U64, _U64, _I, _P]),
     "cafs_fallback_sort_i64": (_I, [_P, _P, _U64, _I, _P]),

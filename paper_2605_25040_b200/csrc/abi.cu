@@ -57,7 +57,7 @@ struct cafs_ctx {
   u64* stage = nullptr;  // host-path device staging buffer
   size_t stage_elems = 0;
   u32 epoch = 0;
-  cudaEvent_t ev[4] = {};
+  cudaEvent_t ev[32] = {};
   std::string last_error;
   uint32_t launches = 0;
 };
@@ -233,11 +233,47 @@ void fill_decision(const DevCtl& c, int route, bool has_est, cafs_decision_t* d)
   for (int j = 0; j < d->est.nkeys; ++j) d->est.keys[j] = c.keys[j];
 }
 
+// Non-blocking stage/kernel timer: event pairs are recorded on the stream and
+// read after the call's final synchronize, so timing does not perturb the run.
+enum { L_STAGE_COUNT = 0, L_STAGE_SORT_K = 1, L_STAGE_EMIT = 2, L_K_COUNT = 3, L_K_EMIT = 4,
+       L_K_EST = 5, L_K_PAIR = 6 };
+constexpr int kMaxTimed = 16;
+
+struct StageTimer {
+  cafs_ctx_t* ctx;
+  cudaStream_t st;
+  bool on;
+  cafs_telemetry_t* tel;
+  int n = 0;
+  int label[kMaxTimed] = {};
+  int begin() {
+    if (!on || n >= kMaxTimed) return -1;
+    cudaEventRecord(ctx->ev[2 * n], st);
+    return n++;
+  }
+  void end(int i, int lab) {
+    if (i < 0) return;
+    cudaEventRecord(ctx->ev[2 * i + 1], st);
+    label[i] = lab;
+  }
+  void finish() {  // call after the stream is synchronized
+    for (int i = 0; i < n; ++i) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, ctx->ev[2 * i], ctx->ev[2 * i + 1]) != cudaSuccess) continue;
+      float* slot = label[i] < 3 ? &tel->stage_ms[label[i]] : &tel->kernel_ms[label[i] - 3];
+      *slot = (*slot < 0 ? 0.f : *slot) + ms;
+    }
+    n = 0;
+  }
+};
+
 // K0/K1 (+ the full monotone scan when the prefix is sorted).  Leaves the
 // device control block filled and *monotone / *route set.
 int run_dispatch(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, cudaStream_t st, bool* monotone,
-                 int* route) {
+                 int* route, StageTimer* tm = nullptr) {
+  const int te = tm ? tm->begin() : -1;
   launch_estimate(x, n, flip, 1, ctx->d_ctl, st);
+  if (tm) tm->end(te, L_K_EST);
   ctx->launches++;
   CKL();
   TRY(sync_ctl(ctx, st));
@@ -257,49 +293,35 @@ int run_dispatch(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, cudaStream_t st
   return CAFS_OK;
 }
 
-struct StageTimer {
-  cafs_ctx_t* ctx;
-  cudaStream_t st;
-  bool on;
-  cafs_telemetry_t* tel;
-  void begin() {
-    if (on) cudaEventRecord(ctx->ev[0], st);
-  }
-  void end(int stage) {
-    if (!on) return;
-    cudaEventRecord(ctx->ev[1], st);
-    cudaEventSynchronize(ctx->ev[1]);
-    float ms = 0;
-    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
-    tel->stage_ms[stage] = (tel->stage_ms[stage] < 0 ? 0.f : tel->stage_ms[stage]) + ms;
-  }
-};
-
 // count -> compact -> pair sort -> emit, with the guard (sorter.py:317-332, 254-293)
 int run_main(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
              cafs_telemetry_t* tel, StageTimer& tm, cudaStream_t st) {
   TRY(ensure_main(ctx));
-  tm.begin();
+  int ts = tm.begin(), tk = tm.begin();
   cudaError_t e = launch_hash_count(x, n, flip, mult, ctx->d_ctl, ctx->gkeys, ctx->gcnt,
                                     ctx->glist, (flags & CAFS_FLAG_NO_DIRECT) ? 0 : 1,
                                     ctx->num_sms, st);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
+  tm.end(tk, L_K_COUNT);
   launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
                  ctx->num_sms, st);
   ctx->launches += 2;
   CKL();
-  tm.end(CAFS_STAGE_COUNT);
-  tm.begin();
+  tm.end(ts, L_STAGE_COUNT);
+  const int mark = tm.n;  // timer entries up to the count stage
+  ts = tm.begin();
   e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, n, ctx->pk_b, ctx->pc_b,
                               ctx->poffs, st);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   ctx->launches++;
-  tm.end(CAFS_STAGE_SORT_K);
-  tm.begin();
+  tm.end(ts, L_STAGE_SORT_K);
+  ts = tm.begin();
+  int tk2 = tm.begin();
   launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st);
+  tm.end(tk2, L_K_EMIT);
   ctx->launches++;
   CKL();
-  tm.end(CAFS_STAGE_EMIT);
+  tm.end(ts, L_STAGE_EMIT);
   TRY(sync_ctl(ctx, st));
   DevCtl& c = *ctx->h_ctl;
   if (tel) tel->global_updates = c.g_updates;
@@ -307,18 +329,17 @@ int run_main(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
     // guard: the count is dropped; x is untouched, sort it with the fallback
     CK(cudaMemsetAsync(ctx->gkeys, 0xFF, kGlobalSlots * 8, st));
     CK(cudaMemsetAsync(ctx->gcnt, 0, kGlobalSlots * 8, st));
-    if (tel) {
-      tel->guard_fired = 1;
-      tel->stage_ms[CAFS_STAGE_EMIT] = -1.f;
-    }
-    tm.begin();
+    if (tel) tel->guard_fired = 1;
+    tm.n = mark;  // the dropped pair-sort/emit launches are not reported (sorter.py:264-273)
+    ts = tm.begin();
     TRY(fallback_sort(ctx, x, n, flip, st));
-    tm.end(CAFS_STAGE_SORT_K);
+    tm.end(ts, L_STAGE_SORT_K);
     return CAFS_OK;
   }
   if (c.need_large) {
     const u64 np = c.npairs;
-    tm.begin();
+    tm.n = mark;  // discard the gated (no-op) pair-sort/emit launches of the fast path
+    ts = tm.begin();
     TRY(ensure_radix(ctx, np, false));
     u64 *rk, *rv;
     TRY(radix_sort(ctx, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, np, 0, st, &rk, &rv));
@@ -329,12 +350,14 @@ int run_main(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
     launch_scan(ctx->pc_b, np, ctx->bsum, ctx->poffs, ctx->d_ctl, n, st);
     ctx->launches += 3;
     CKL();
-    tm.end(CAFS_STAGE_SORT_K);
-    tm.begin();
+    tm.end(ts, L_STAGE_SORT_K);
+    ts = tm.begin();
+    int tk3 = tm.begin();
     launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st);
+    tm.end(tk3, L_K_EMIT);
     ctx->launches++;
     CKL();
-    tm.end(CAFS_STAGE_EMIT);
+    tm.end(ts, L_STAGE_EMIT);
     TRY(sync_ctl(ctx, st));
   }
   if (c.sum_error || !c.pairs_ready) return fail(ctx, CAFS_ESUM, "pair counts do not sum to n");
@@ -399,7 +422,7 @@ int cafs_ctx_create(int device, cafs_ctx_t** out) {
     cafs_ctx_destroy(ctx);
     return CAFS_ENOMEM;
   }
-  for (int i = 0; i < 4; ++i) cudaEventCreate(&ctx->ev[i]);
+  for (int i = 0; i < 32; ++i) cudaEventCreate(&ctx->ev[i]);
   *out = ctx;
   return CAFS_OK;
 }
@@ -415,7 +438,7 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
   if (ctx->h_trivial) cudaFreeHost(ctx->h_trivial);
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 32; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   delete ctx;
 }
@@ -433,6 +456,7 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
   memset(tel, 0, sizeof(*tel));
   tel->n = n;
   for (int i = 0; i < 3; ++i) tel->stage_ms[i] = -1.f;
+  for (int i = 0; i < 4; ++i) tel->kernel_ms[i] = -1.f;
   if (n <= 1) {
     tel->decision.route = CAFS_ALREADY_SORTED;
     return CAFS_OK;
@@ -442,39 +466,47 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
   const u64 flip = is_signed ? kSign : 0;
   bool mono;
   int route;
-  TRY(run_dispatch(ctx, x, n, flip, st, &mono, &route));
+  TRY(run_dispatch(ctx, x, n, flip, st, &mono, &route, &tm));
   const DevCtl c = *ctx->h_ctl;
   fill_decision(c, route, !mono && n >= CAFS_SMALL_N_CUTOFF, &tel->decision);
   int rc = CAFS_OK;
+  int ts;
   switch (route) {
     case CAFS_ALREADY_SORTED:
       break;
     case CAFS_FALLBACK_SMALL_N:
     case CAFS_FALLBACK_HIGH_ENTROPY:
-      tm.begin();
+      ts = tm.begin();
       rc = fallback_sort(ctx, x, n, flip, st);
-      tm.end(CAFS_STAGE_SORT_K);
+      tm.end(ts, L_STAGE_SORT_K);
       break;
     case CAFS_TINY_COUNT: {
       TRY(ensure_main(ctx));
-      tm.begin();
+      const int mark = tm.n;
+      ts = tm.begin();
+      int tk = tm.begin();
       launch_tiny_count(x, n, flip, ctx->d_ctl, ctx->num_sms, st);
+      tm.end(tk, L_K_COUNT);
       launch_tiny_finalize(ctx->d_ctl, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st);
       ctx->launches += 2;
       CKL();
-      tm.end(CAFS_STAGE_COUNT);
-      tm.begin();
+      tm.end(ts, L_STAGE_COUNT);
+      ts = tm.begin();
+      tk = tm.begin();
       launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st);
+      tm.end(tk, L_K_EMIT);
+      tm.end(ts, L_STAGE_EMIT);
       ctx->launches++;
       CKL();
       TRY(sync_ctl(ctx, st));
       if (ctx->h_ctl->pairs_ready) {
-        tm.end(CAFS_STAGE_EMIT);
         tel->counted_total = n;
         tel->pairs = (u64)c.nkeys;
         break;
       }
-      // the sample missed a value: MAIN with the same k_hat (sorter.py:378-385)
+      // the sample missed a value: MAIN with the same k_hat (sorter.py:378-385);
+      // the failed tiny pass still counts as a "count" stage
+      tm.n = mark + 2;
       tel->tiny_count_failed = 1;
       tel->decision.route = CAFS_MAIN;
       tel->table_buckets = table_size_for(c.k_hat > 1.0 ? c.k_hat : 1.0, n, 4);
@@ -488,6 +520,7 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
   }
   if (rc != CAFS_OK) return rc;
   CK(cudaStreamSynchronize(st));
+  tm.finish();
   tel->kernels_launched = ctx->launches;
   return CAFS_OK;
 }
@@ -623,6 +656,48 @@ int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, n, ctx->pk_b, ctx->pc_b,
                               ctx->poffs, st);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+  TRY(sync_ctl(ctx, st));
+  DevCtl c = *ctx->h_ctl;
+  if (c.overflow) {
+    CK(cudaMemsetAsync(ctx->gkeys, 0xFF, kGlobalSlots * 8, st));
+    CK(cudaMemsetAsync(ctx->gcnt, 0, kGlobalSlots * 8, st));
+    CK(cudaStreamSynchronize(st));
+    return fail(ctx, CAFS_EINVAL, "more distinct keys than the global table holds");
+  }
+  const u64 np = c.npairs;
+  if (c.need_large) {
+    TRY(ensure_radix(ctx, np, false));
+    u64 *rk, *rv;
+    TRY(radix_sort(ctx, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, np, 0, st, &rk, &rv));
+    if (rk != ctx->pk_b) {
+      CK(cudaMemcpyAsync(ctx->pk_b, rk, np * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(ctx->pc_b, rv, np * 8, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  *h_npairs = np;
+  if (np > cap) return fail(ctx, CAFS_EINVAL, "output capacity too small");
+  CK(cudaMemcpyAsync(d_keys, ctx->pk_b, np * 8, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(d_counts, ctx->pc_b, np * 8, cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  return CAFS_OK;
+}
+
+int cafs_merge_pairs(cafs_ctx_t* ctx, const uint64_t* d_keys_in, const uint64_t* d_counts_in,
+                     uint64_t m, uint64_t* d_keys, uint64_t* d_counts, uint64_t cap,
+                     uint64_t* h_npairs, void* stream) {
+  if (!ctx || !h_npairs || (m && (!d_keys_in || !d_counts_in))) return CAFS_EINVAL;
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  *h_npairs = 0;
+  TRY(ensure_main(ctx));
+  launch_insert_pairs((const u64*)d_keys_in, (const u64*)d_counts_in, m, CAFS_DEFAULT_HASH_MULT,
+                      ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->num_sms, st);
+  launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
+                 ctx->num_sms, st);
+  cudaError_t e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, ~0ull, ctx->pk_b,
+                                          ctx->pc_b, ctx->poffs, st);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+  CKL();
   TRY(sync_ctl(ctx, st));
   DevCtl c = *ctx->h_ctl;
   if (c.overflow) {

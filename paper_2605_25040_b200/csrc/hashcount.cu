@@ -215,6 +215,45 @@ __global__ void compact_kernel(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* gl
   }
 }
 
+// (key, count) pairs -> global table (the merge step of the sharded sort)
+__global__ void insert_pairs_kernel(const u64* __restrict__ keys, const u64* __restrict__ cnts,
+                                    u64 m, u64 mult, DevCtl* ctl, u64* gkeys, u64* gcnt,
+                                    u32* glist) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += stride) {
+    const u64 k = keys[i], c = cnts[i];
+    if (c == 0) continue;
+    if (k == kEmpty) atomicAdd(&ctl->empty_key_count, c);
+    else global_insert(gkeys, gcnt, glist, ctl, k, c, mult);
+  }
+}
+
+// zero the per-call fields of the control block (estimate_kernel does the same)
+__global__ void reset_ctl_kernel(DevCtl* ctl) {
+  if (threadIdx.x == 0) {
+    ctl->g_used = 0;
+    ctl->g_updates = 0;
+    ctl->empty_key_count = 0;
+    ctl->overflow = 0;
+    ctl->need_large = 0;
+    ctl->npairs = 0;
+    ctl->total = 0;
+    ctl->pairs_ready = 0;
+    ctl->sum_error = 0;
+    ctl->range_len = 0;
+  }
+}
+
+void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevCtl* ctl,
+                         u64* gkeys, u64* gcnt, u32* glist, int num_sms, cudaStream_t st) {
+  reset_ctl_kernel<<<1, 32, 0, st>>>(ctl);
+  u64 blocks = (m + 255) / 256;
+  if (blocks > (u64)num_sms * 8) blocks = (u64)num_sms * 8;
+  if (blocks < 1) blocks = 1;
+  insert_pairs_kernel<<<(unsigned)blocks, 256, 0, st>>>(keys, cnts, m, mult, ctl, gkeys, gcnt,
+                                                         glist);
+}
+
 size_t hash_count_smem() { return kHcSmem; }
 
 cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,

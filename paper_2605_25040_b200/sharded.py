@@ -1,0 +1,301 @@
+"""Row-sharded multi-GPU CAFS sort over torch.distributed (NCCL on NVLink/NVSwitch).
+
+One process per GPU.  The global column is the concatenation of every rank's
+``x_local`` in rank order; afterwards rank r's ``x_local`` holds rows
+``[off_r, off_r + n_r)`` of the globally sorted column (same shard sizes), so the
+concatenated result is bit-identical to a single-GPU ``cafs_sort`` (and to the
+reference) on the whole column.
+
+The reference is single-threaded; the paper names a parallel CAFS with
+per-thread tables and a final merge as future work.  Here:
+
+1. dispatch, globally identical on every rank (sorter.py:141-162):
+   * monotone: each shard's full non-decreasing check plus its first/last key,
+     all-gathered (global monotone <=> every shard monotone and the shard
+     boundaries ordered);
+   * samples: the global positions ``i * (N // 1024)`` that fall in a shard
+     are gathered locally and all-gathered (1024 x 8 B in total), then every
+     rank runs the estimate kernel on the same 1024 values and the same
+     float64 Chao1 with the global N;
+2. TINY: local tiny counts, all-reduce of <= 8 counters; a miss anywhere
+   re-enters MAIN on all ranks (sorter.py:378-385);
+3. MAIN: local hash count into sorted (key, count) pairs, all-gather of the
+   pair tables (<= K x 16 B per rank), the merge (union + fold, sorter.py:276-285)
+   on every rank, then each rank emits only its own output slice from the
+   global prefix sum;
+4. FALLBACK / guard: "gather then sort" (every rank sorts the gathered column
+   and keeps its slice).  A distributed radix sort is the next step (SURVEY.md
+   §8(f)2); the high-entropy configs are single-GPU in BASELINE.json.
+
+Local steps go through :class:`DeviceOps` (the C ABI); collectives through
+``torch.distributed``.  Tests inject a CPU ``ops`` object with the same
+interface to check this orchestration under ``gloo``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .sorter import (
+    SAMPLE_TARGET,
+    SMALL_N_CUTOFF,
+    TINY_MAX_KEYS,
+    CardinalityEstimate,
+    DispatchDecision,
+    Route,
+    SortTelemetry,
+    check_hash_mult,
+    chao1,
+    table_size_for,
+)
+
+_SIGN = 1 << 63
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class DeviceOps:
+    """Local pipeline steps on this rank's GPU, through libcafs_b200.so."""
+
+    def __init__(self, device: int, signed: bool = True):
+        self.device = device
+        self.signed = signed
+        self.ctx = _lib.context(device)
+        self.lib = _lib.load()
+
+    def _stream(self):
+        return _torch().cuda.current_stream(self.device).cuda_stream
+
+    def is_monotone(self, x) -> bool:
+        if x.shape[0] < 2:
+            return True
+        out = ctypes.c_int()
+        _lib.check(self.lib.cafs_is_monotone_i64(self.ctx, x.data_ptr(), x.shape[0],
+                                                 int(self.signed), ctypes.byref(out),
+                                                 self._stream()), self.ctx, "is_monotone")
+        return bool(out.value)
+
+    def estimate(self, samples) -> tuple[int, int, int, bool, list[int]]:
+        """(u, f1, f2, saturated, ascending distinct keys if u <= 8) of the samples."""
+        e = _lib.Estimate()
+        _lib.check(self.lib.cafs_estimate_i64(self.ctx, samples.data_ptr(), samples.shape[0],
+                                              int(self.signed), ctypes.byref(e), self._stream()),
+                   self.ctx, "estimate")
+        keys = [int(e.keys[i]) for i in range(e.nkeys)]
+        return int(e.u), int(e.f1), int(e.f2), bool(e.saturated), keys
+
+    def tiny_counts(self, x, keys_u64: list[int]) -> np.ndarray:
+        k = np.array(keys_u64, dtype=np.uint64)
+        out = np.zeros(len(keys_u64), np.int64)
+        if x.shape[0]:
+            _lib.check(self.lib.cafs_tiny_counts_i64(
+                self.ctx, x.data_ptr(), x.shape[0], int(self.signed),
+                k.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(keys_u64),
+                out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), self._stream()),
+                self.ctx, "tiny_counts")
+        return out
+
+    def _pairs_out(self, cap):
+        torch = _torch()
+        dev = torch.device("cuda", self.device)
+        return (torch.empty(cap, dtype=torch.int64, device=dev),
+                torch.empty(cap, dtype=torch.int64, device=dev))
+
+    def count_pairs(self, x, mult: int):
+        """Sorted distinct (key, count) pairs of the shard, or None on table overflow."""
+        cap = 1 << 21
+        k, c = self._pairs_out(cap)
+        if x.shape[0] == 0:
+            return k[:0], c[:0]
+        npairs = ctypes.c_uint64()
+        rc = self.lib.cafs_count_pairs_i64(self.ctx, x.data_ptr(), x.shape[0], int(self.signed),
+                                           mult, k.data_ptr(), c.data_ptr(), cap,
+                                           ctypes.byref(npairs), self._stream())
+        if rc == _lib.EINVAL:
+            return None
+        _lib.check(rc, self.ctx, "count_pairs")
+        return k[:npairs.value], c[:npairs.value]
+
+    def merge_pairs(self, keys, counts):
+        cap = 1 << 21
+        k, c = self._pairs_out(cap)
+        npairs = ctypes.c_uint64()
+        rc = self.lib.cafs_merge_pairs(self.ctx, keys.data_ptr(), counts.data_ptr(), keys.shape[0],
+                                       k.data_ptr(), c.data_ptr(), cap, ctypes.byref(npairs),
+                                       self._stream())
+        if rc == _lib.EINVAL:
+            return None
+        _lib.check(rc, self.ctx, "merge_pairs")
+        return k[:npairs.value], c[:npairs.value]
+
+    def emit_slice(self, keys, counts, out, begin: int, end: int, total: int) -> None:
+        if end <= begin:
+            return
+        _lib.check(self.lib.cafs_emit_i64(self.ctx, keys.data_ptr(), counts.data_ptr(),
+                                          keys.shape[0], out.data_ptr(), begin, end, total,
+                                          int(self.signed), self._stream()), self.ctx, "emit")
+
+    def fallback_sort(self, x) -> None:
+        if x.shape[0] < 2:
+            return
+        _lib.check(self.lib.cafs_fallback_sort_i64(self.ctx, x.data_ptr(), x.shape[0],
+                                                   int(self.signed), self._stream()),
+                   self.ctx, "fallback_sort")
+
+    def keys_tensor(self, keys_u64: list[int], counts: np.ndarray):
+        torch = _torch()
+        dev = torch.device("cuda", self.device)
+        k = torch.from_numpy(np.array(keys_u64, dtype=np.uint64).view(np.int64)).to(dev)
+        c = torch.from_numpy(np.ascontiguousarray(counts, dtype=np.int64)).to(dev)
+        return k, c
+
+
+class Comm:
+    """The few collectives the sharded sort needs, over torch.distributed."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = device  # tensors for the collective live here (cuda for NCCL)
+
+    def _t(self, a, dtype=None):
+        torch = _torch()
+        t = torch.as_tensor(a, dtype=dtype or torch.int64)
+        return t.to(self.device) if self.device is not None else t
+
+    def all_gather_ints(self, vals: list[int]) -> list[list[int]]:
+        torch = _torch()
+        t = self._t(np.array(vals, dtype=np.uint64).view(np.int64))
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.cpu().numpy().view(np.uint64).astype(object).tolist() for o in out]
+
+    def all_reduce_sum(self, a: np.ndarray) -> np.ndarray:
+        t = self._t(np.ascontiguousarray(a, dtype=np.int64))
+        self.dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+    def all_gather_var(self, t):
+        """All-gather 1-D int64 tensors of different lengths (pad to the max)."""
+        torch = _torch()
+        sizes = [s[0] for s in self.all_gather_ints([int(t.shape[0])])]
+        m = max(sizes) if sizes else 0
+        pad = torch.zeros(m, dtype=t.dtype, device=t.device)
+        pad[:t.shape[0]] = t
+        out = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(out, pad, group=self.group)
+        return torch.cat([o[:s] for o, s in zip(out, sizes)])
+
+
+def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTelemetry | None = None,
+                      ops=None, signed: bool | None = None) -> None:
+    """Sort the row-sharded global column in place; see the module docstring."""
+    torch = _torch()
+    mult = check_hash_mult(hash_mult)
+    if ops is None:
+        if signed is None:
+            signed = x_local.dtype == torch.int64
+        dev = x_local.device.index if x_local.device.index is not None else torch.cuda.current_device()
+        ops = DeviceOps(dev, signed)
+    else:
+        signed = ops.signed if signed is None else signed
+    comm = Comm(group, x_local.device if x_local.is_cuda else None)
+    tel = telemetry if telemetry is not None else SortTelemetry()
+    flip = _SIGN if signed else 0
+
+    # ---- global shape ----
+    n_local = int(x_local.shape[0])
+    sizes = [s[0] for s in comm.all_gather_ints([n_local])]
+    N = int(sum(sizes))
+    off = int(sum(sizes[:comm.rank]))
+    tel.n = N
+    if N <= 1:
+        tel.decision = DispatchDecision(Route.ALREADY_SORTED)
+        return
+
+    # ---- monotone (sorter.py:115-129) ----
+    mono = ops.is_monotone(x_local)
+    first = (int(x_local[0].item()) & ((1 << 64) - 1)) ^ flip if n_local else 0
+    last = (int(x_local[-1].item()) & ((1 << 64) - 1)) ^ flip if n_local else 0
+    info = comm.all_gather_ints([int(mono), first, last, int(n_local > 0)])
+    g_mono = all(r[0] for r in info)
+    prev = None
+    for m_, f_, l_, ne in info:
+        if ne:
+            if prev is not None and f_ < prev:
+                g_mono = False
+            prev = l_
+    if g_mono:
+        tel.decision = DispatchDecision(Route.ALREADY_SORTED)
+        return
+
+    def _fallback(route_decision: DispatchDecision, guard: bool = False):
+        tel.decision = route_decision
+        tel.guard_fired = guard
+        full = comm.all_gather_var(x_local)
+        ops.fallback_sort(full)
+        x_local.copy_(full[off:off + n_local])
+
+    if N < SMALL_N_CUTOFF:
+        _fallback(DispatchDecision(Route.FALLBACK_SMALL_N))
+        return
+
+    # ---- strided samples (cardinality.py:99-110), gathered across ranks ----
+    stride = N // SAMPLE_TARGET
+    lo = (off + stride - 1) // stride
+    hi = min(SAMPLE_TARGET, (off + n_local + stride - 1) // stride)
+    if hi > lo:
+        pos = torch.arange(lo, hi, device=x_local.device, dtype=torch.int64) * stride - off
+        local_samples = x_local.index_select(0, pos)
+    else:
+        local_samples = x_local[:0]
+    samples = comm.all_gather_var(local_samples)
+    assert samples.shape[0] == SAMPLE_TARGET
+    u, f1, f2, saturated, keys = ops.estimate(samples)
+    k_hat = chao1(u, f1, f2, N, saturated)
+    est = CardinalityEstimate(k_hat, u, f1, f2, saturated)
+
+    if k_hat <= TINY_MAX_KEYS and u <= TINY_MAX_KEYS:
+        # ---- TINY (sorter.py:367-385) ----
+        cnt = ops.tiny_counts(x_local, keys)
+        tot = comm.all_reduce_sum(cnt)
+        if int(tot.sum()) == N:
+            tel.decision = DispatchDecision(Route.TINY_COUNT, keys=np.array(keys, np.uint64),
+                                            estimate=est)
+            kt, ct = ops.keys_tensor(keys, tot)
+            ops.emit_slice(kt, ct, x_local, off, off + n_local, N)
+            tel.counted_total = N
+            tel.pairs = len(keys)
+            return
+        tel.tiny_count_failed = True
+    elif k_hat * 2 > N:
+        _fallback(DispatchDecision(Route.FALLBACK_HIGH_ENTROPY, estimate=est))
+        return
+
+    # ---- MAIN: local count, all-gather of pair tables, merge, slice emit ----
+    decision = DispatchDecision(Route.MAIN, k_hat=k_hat, estimate=est)
+    tel.table_buckets = table_size_for(max(1.0, k_hat), N, 4)
+    pairs = ops.count_pairs(x_local, mult)
+    overflow = comm.all_reduce_sum(np.array([1 if pairs is None else 0]))[0]
+    merged = None
+    if not overflow:
+        keys_all = comm.all_gather_var(pairs[0])
+        cnts_all = comm.all_gather_var(pairs[1])
+        merged = ops.merge_pairs(keys_all, cnts_all)
+        overflow = comm.all_reduce_sum(np.array([1 if merged is None else 0]))[0]
+    if overflow:
+        _fallback(decision, guard=True)
+        return
+    tel.decision = decision
+    ops.emit_slice(merged[0], merged[1], x_local, off, off + n_local, N)
+    tel.counted_total = N
+    tel.pairs = int(merged[0].shape[0])

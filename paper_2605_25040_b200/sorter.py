@@ -93,6 +93,7 @@ class SortTelemetry:  # sorter.py:60-81
     global_updates: int = 0
     table_buckets: int = 0
     kernels_launched: int = 0
+    kernel_ms: dict[str, float] = field(default_factory=dict)
 
     @property
     def route(self) -> Route | None:
@@ -304,6 +305,9 @@ def _fill_telemetry(tel: SortTelemetry, t: _lib.Telemetry, kind: str, timing: bo
         tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, cap)
     if timing:
         tel.stage_ms = _stage_dict(t)
+        tel.kernel_ms = {name: float(t.kernel_ms[i])
+                         for i, name in enumerate(("count_kernel", "emit_kernel", "estimate_kernel"))
+                         if t.kernel_ms[i] >= 0}
     else:
         # labels of the stages that ran (times not measured without a telemetry object)
         tel.stage_ms = {}
