@@ -100,13 +100,14 @@ class ClockSampler:
                 "samples": len(self.rows), "samples_under_load": len(loaded)}
 
 
-def ncu_traffic(config: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def ncu_traffic(config: str, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the
+    committed `ncu --set full` capture of this config (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get(config)
+            d = json.load(f)[config][kernel]
+        return d["dram_bytes_per_launch"]
     except Exception:
         return None
 
@@ -269,11 +270,15 @@ def main():
             gbs = n_local * 8 / (avg / 1e3) / 1e9
             kernels[name] = {"kernel": kname, "avg_ms": avg, "GB/s": gbs,
                              "share_of_step": avg / (tot_ms / args.steps)}
-    if kernels:
-        dom = max(kernels, key=lambda k: kernels[k]["avg_ms"])
+    k_est = [t.kernel_ms.get("estimate_kernel") for t in tels if "estimate_kernel" in t.kernel_ms]
+    if k_est:
+        kernels["estimate"] = {"kernel": "estimate_kernel", "avg_ms": sum(k_est) / len(k_est),
+                               "share_of_step": sum(k_est) / len(k_est) / (tot_ms / args.steps)}
+    if any("GB/s" in v for v in kernels.values()):
+        dom = max((k for k in kernels if "GB/s" in kernels[k]), key=lambda k: kernels[k]["avg_ms"])
         d = kernels[dom]
         roof = {"bound": "hbm", "kernel": d["kernel"], "achieved": d["GB/s"], "peak": peak,
-                "unit": "GB/s", "frac": d["GB/s"] / peak, "traffic": ncu_traffic(args.config),
+                "unit": "GB/s", "frac": d["GB/s"] / peak, "traffic": ncu_traffic(args.config, d["kernel"]),
                 "algorithmic_bytes_per_launch": n_local * 8, "peak_source": peak_src,
                 "step_frac": (16 * N / (tot_ms / args.steps / 1e3) / 1e9) / world / peak,
                 "kernels": kernels}

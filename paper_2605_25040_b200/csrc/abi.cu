@@ -57,6 +57,7 @@ struct cafs_ctx {
   u64* stage = nullptr;  // host-path device staging buffer
   size_t stage_elems = 0;
   u32 epoch = 0;
+  int32_t* h_scratch = nullptr;  // pinned
   cudaEvent_t ev[32] = {};
   std::string last_error;
   uint32_t launches = 0;
@@ -239,6 +240,10 @@ enum { L_STAGE_COUNT = 0, L_STAGE_SORT_K = 1, L_STAGE_EMIT = 2, L_K_COUNT = 3, L
        L_K_EST = 5, L_K_PAIR = 6 };
 constexpr int kMaxTimed = 16;
 
+// Conditions under which a timed interval is reported (the fused pipeline
+// launches every route's kernels; gated-off ones must not show up as stages).
+enum { C_ALWAYS = 0, C_TINY = 1, C_MAIN = 2, C_EMIT = 3 };
+
 struct StageTimer {
   cafs_ctx_t* ctx;
   cudaStream_t st;
@@ -246,18 +251,25 @@ struct StageTimer {
   cafs_telemetry_t* tel;
   int n = 0;
   int label[kMaxTimed] = {};
+  int cond[kMaxTimed] = {};
   int begin() {
     if (!on || n >= kMaxTimed) return -1;
     cudaEventRecord(ctx->ev[2 * n], st);
     return n++;
   }
-  void end(int i, int lab) {
+  void end(int i, int lab, int c = C_ALWAYS) {
     if (i < 0) return;
     cudaEventRecord(ctx->ev[2 * i + 1], st);
     label[i] = lab;
+    cond[i] = c;
   }
-  void finish() {  // call after the stream is synchronized
+  // call after the stream is synchronized; tiny_ran / main_ran / emitted say
+  // which gated groups actually executed
+  void finish(bool tiny_ran, bool main_ran, bool emitted) {
     for (int i = 0; i < n; ++i) {
+      if ((cond[i] == C_TINY && !tiny_ran) || (cond[i] == C_MAIN && !main_ran) ||
+          (cond[i] == C_EMIT && !emitted))
+        continue;
       float ms = 0;
       if (cudaEventElapsedTime(&ms, ctx->ev[2 * i], ctx->ev[2 * i + 1]) != cudaSuccess) continue;
       float* slot = label[i] < 3 ? &tel->stage_ms[label[i]] : &tel->kernel_ms[label[i] - 3];
@@ -293,53 +305,73 @@ int run_dispatch(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, cudaStream_t st
   return CAFS_OK;
 }
 
-// count -> compact -> pair sort -> emit, with the guard (sorter.py:317-332, 254-293)
-int run_main(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
-             cafs_telemetry_t* tel, StageTimer& tm, cudaStream_t st) {
+// The fused pipeline (sorter.py:357-386 as one stream of gated kernels):
+// tiny count -> tiny finalize -> hash count (dense or queued variant) ->
+// compact -> pair sort -> emit.  Each kernel reads the device decision of the
+// estimate kernel and exits unless its route is active, so the host needs no
+// round trip between the dispatch and the emit.
+int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
+                 StageTimer& tm, cudaStream_t st) {
   TRY(ensure_main(ctx));
+  DevCtl* c = ctx->d_ctl;
   int ts = tm.begin(), tk = tm.begin();
-  cudaError_t e = launch_hash_count(x, n, flip, mult, ctx->d_ctl, ctx->gkeys, ctx->gcnt,
-                                    ctx->glist, (flags & CAFS_FLAG_NO_DIRECT) ? 0 : 1,
-                                    ctx->num_sms, st);
+  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny);
+  tm.end(tk, L_K_COUNT, C_TINY);
+  launch_tiny_finalize(c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st, kGateTiny);
+  tm.end(ts, L_STAGE_COUNT, C_TINY);
+  ts = tm.begin();
+  tk = tm.begin();
+  const bool direct = !(flags & CAFS_FLAG_NO_DIRECT);
+  cudaError_t e;
+  if (direct) {
+    e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
+                          ctx->num_sms, st, 0, kGateMainDense);
+    if (e == cudaSuccess)
+      e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
+                            ctx->num_sms, st, 1, kGateMainHash);
+  } else {
+    e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 0,
+                          ctx->num_sms, st, 1, kGateMain);
+  }
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
-  tm.end(tk, L_K_COUNT);
-  launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
-                 ctx->num_sms, st);
-  ctx->launches += 2;
-  CKL();
-  tm.end(ts, L_STAGE_COUNT);
-  const int mark = tm.n;  // timer entries up to the count stage
+  tm.end(tk, L_K_COUNT, C_MAIN);
+  launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
+                 kGateMain);
+  tm.end(ts, L_STAGE_COUNT, C_MAIN);
   ts = tm.begin();
-  e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, n, ctx->pk_b, ctx->pc_b,
-                              ctx->poffs, st);
+  e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st,
+                              kGateMain);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
-  ctx->launches++;
-  tm.end(ts, L_STAGE_SORT_K);
+  tm.end(ts, L_STAGE_SORT_K, C_MAIN);
   ts = tm.begin();
-  int tk2 = tm.begin();
-  launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st);
-  tm.end(tk2, L_K_EMIT);
-  ctx->launches++;
+  tk = tm.begin();
+  launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, kSmallSortMax);
+  tm.end(tk, L_K_EMIT, C_EMIT);
+  tm.end(ts, L_STAGE_EMIT, C_EMIT);
+  ctx->launches += direct ? 7 : 6;
   CKL();
-  tm.end(ts, L_STAGE_EMIT);
-  TRY(sync_ctl(ctx, st));
+  return CAFS_OK;
+}
+
+// After the fused pipeline: the guard (overflow -> fallback, sorter.py:264-273),
+// the large-pair-set path, and the sum check (sorter.py:247-248).
+int main_finish(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cafs_telemetry_t* tel,
+                StageTimer& tm, cudaStream_t st, bool* emitted) {
   DevCtl& c = *ctx->h_ctl;
-  if (tel) tel->global_updates = c.g_updates;
+  tel->global_updates = c.g_updates;
   if (c.overflow) {
-    // guard: the count is dropped; x is untouched, sort it with the fallback
     CK(cudaMemsetAsync(ctx->gkeys, 0xFF, kGlobalSlots * 8, st));
     CK(cudaMemsetAsync(ctx->gcnt, 0, kGlobalSlots * 8, st));
-    if (tel) tel->guard_fired = 1;
-    tm.n = mark;  // the dropped pair-sort/emit launches are not reported (sorter.py:264-273)
-    ts = tm.begin();
+    tel->guard_fired = 1;
+    *emitted = false;
+    const int ts = tm.begin();
     TRY(fallback_sort(ctx, x, n, flip, st));
     tm.end(ts, L_STAGE_SORT_K);
     return CAFS_OK;
   }
   if (c.need_large) {
     const u64 np = c.npairs;
-    tm.n = mark;  // discard the gated (no-op) pair-sort/emit launches of the fast path
-    ts = tm.begin();
+    int ts = tm.begin();
     TRY(ensure_radix(ctx, np, false));
     u64 *rk, *rv;
     TRY(radix_sort(ctx, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, np, 0, st, &rk, &rv));
@@ -352,19 +384,18 @@ int run_main(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
     CKL();
     tm.end(ts, L_STAGE_SORT_K);
     ts = tm.begin();
-    int tk3 = tm.begin();
-    launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st);
-    tm.end(tk3, L_K_EMIT);
+    const int tk = tm.begin();
+    launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st, np);
+    tm.end(tk, L_K_EMIT);
     ctx->launches++;
     CKL();
     tm.end(ts, L_STAGE_EMIT);
     TRY(sync_ctl(ctx, st));
+    *emitted = true;
   }
   if (c.sum_error || !c.pairs_ready) return fail(ctx, CAFS_ESUM, "pair counts do not sum to n");
-  if (tel) {
-    tel->counted_total = c.total;
-    tel->pairs = c.npairs;
-  }
+  tel->counted_total = c.total;
+  tel->pairs = c.npairs;
   return CAFS_OK;
 }
 
@@ -418,6 +449,7 @@ int cafs_ctx_create(int device, cafs_ctx_t** out) {
   ctx->num_sms = prop.multiProcessorCount;
   if (cudaMalloc(&ctx->d_ctl, sizeof(DevCtl)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_ctl, sizeof(DevCtl)) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_scratch, 64) != cudaSuccess ||
       cudaMemset(ctx->d_ctl, 0, sizeof(DevCtl)) != cudaSuccess) {
     cafs_ctx_destroy(ctx);
     return CAFS_ENOMEM;
@@ -437,6 +469,7 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+  if (ctx->h_scratch) cudaFreeHost(ctx->h_scratch);
   if (ctx->h_trivial) cudaFreeHost(ctx->h_trivial);
   for (int i = 0; i < 32; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
@@ -464,63 +497,72 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
   StageTimer tm{ctx, st, want_tel && (flags & CAFS_FLAG_TIMING), tel};
   u64* x = (u64*)d_x;
   const u64 flip = is_signed ? kSign : 0;
-  bool mono;
-  int route;
-  TRY(run_dispatch(ctx, x, n, flip, st, &mono, &route, &tm));
+  // K0/K1 then every route's kernels, gated on the device decision; one sync
+  const int te = tm.begin();
+  launch_estimate(x, n, flip, 1, ctx->d_ctl, st);
+  tm.end(te, L_K_EST);
+  ctx->launches++;
+  CKL();
+  const int mark = tm.n;
+  TRY(launch_fused(ctx, x, n, flip, hash_mult, flags, tm, st));
+  TRY(sync_ctl(ctx, st));
+  int eff = ctx->h_ctl->eff_route;
+  bool mono = eff == CAFS_ALREADY_SORTED;
+  if (eff == kNeedScan) {
+    // the first 16385 rows are sorted: scan the rest, then rerun the gated
+    // pipeline with the resolved route (the first pass was all no-ops)
+    tm.n = mark;
+    launch_monotone_scan(x, n, flip, ctx->d_ctl, ctx->num_sms, st);
+    ctx->launches++;
+    CKL();
+    TRY(sync_ctl(ctx, st));
+    mono = !ctx->h_ctl->scan_inversion;
+    eff = mono ? CAFS_ALREADY_SORTED : ctx->h_ctl->route;
+    if (!mono && (eff == CAFS_TINY_COUNT || eff == CAFS_MAIN)) {
+      ctx->h_scratch[0] = eff;
+      CK(cudaMemcpyAsync(&ctx->d_ctl->eff_route, ctx->h_scratch, sizeof(int32_t),
+                         cudaMemcpyHostToDevice, st));
+      TRY(launch_fused(ctx, x, n, flip, hash_mult, flags, tm, st));
+      TRY(sync_ctl(ctx, st));
+    }
+  }
   const DevCtl c = *ctx->h_ctl;
-  fill_decision(c, route, !mono && n >= CAFS_SMALL_N_CUTOFF, &tel->decision);
+  fill_decision(c, eff, !mono && n >= CAFS_SMALL_N_CUTOFF, &tel->decision);
+  bool tiny_ran = false, main_ran = false, emitted = false;
   int rc = CAFS_OK;
-  int ts;
-  switch (route) {
+  switch (eff) {
     case CAFS_ALREADY_SORTED:
       break;
     case CAFS_FALLBACK_SMALL_N:
-    case CAFS_FALLBACK_HIGH_ENTROPY:
-      ts = tm.begin();
+    case CAFS_FALLBACK_HIGH_ENTROPY: {
+      const int ts = tm.begin();
       rc = fallback_sort(ctx, x, n, flip, st);
       tm.end(ts, L_STAGE_SORT_K);
       break;
-    case CAFS_TINY_COUNT: {
-      TRY(ensure_main(ctx));
-      const int mark = tm.n;
-      ts = tm.begin();
-      int tk = tm.begin();
-      launch_tiny_count(x, n, flip, ctx->d_ctl, ctx->num_sms, st);
-      tm.end(tk, L_K_COUNT);
-      launch_tiny_finalize(ctx->d_ctl, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st);
-      ctx->launches += 2;
-      CKL();
-      tm.end(ts, L_STAGE_COUNT);
-      ts = tm.begin();
-      tk = tm.begin();
-      launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st);
-      tm.end(tk, L_K_EMIT);
-      tm.end(ts, L_STAGE_EMIT);
-      ctx->launches++;
-      CKL();
-      TRY(sync_ctl(ctx, st));
-      if (ctx->h_ctl->pairs_ready) {
+    }
+    case CAFS_TINY_COUNT:
+      tiny_ran = true;
+      if (!c.tiny_failed) {
+        if (!c.pairs_ready) return fail(ctx, CAFS_ESUM, "tiny counts do not sum to n");
+        emitted = true;
         tel->counted_total = n;
         tel->pairs = (u64)c.nkeys;
         break;
       }
-      // the sample missed a value: MAIN with the same k_hat (sorter.py:378-385);
-      // the failed tiny pass still counts as a "count" stage
-      tm.n = mark + 2;
+      // the sample missed a value: MAIN with the same k_hat (sorter.py:378-385)
       tel->tiny_count_failed = 1;
       tel->decision.route = CAFS_MAIN;
-      tel->table_buckets = table_size_for(c.k_hat > 1.0 ? c.k_hat : 1.0, n, 4);
-      rc = run_main(ctx, x, n, flip, hash_mult, flags, tel, tm, st);
-      break;
-    }
+      /* fall through */
     default:
+      main_ran = true;
+      emitted = true;
       tel->table_buckets = table_size_for(c.k_hat > 1.0 ? c.k_hat : 1.0, n, 4);
-      rc = run_main(ctx, x, n, flip, hash_mult, flags, tel, tm, st);
+      rc = main_finish(ctx, x, n, flip, tel, tm, st, &emitted);
       break;
   }
   if (rc != CAFS_OK) return rc;
   CK(cudaStreamSynchronize(st));
-  tm.finish();
+  tm.finish(tiny_ran, main_ran, emitted);
   tel->kernels_launched = ctx->launches;
   return CAFS_OK;
 }
@@ -628,7 +670,9 @@ int cafs_tiny_counts_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
     }
   }
   CK(cudaMemcpyAsync(ctx->d_ctl, &c, sizeof(DevCtl), cudaMemcpyHostToDevice, st));
-  if (n) launch_tiny_count((const u64*)d_x, n, is_signed ? kSign : 0, ctx->d_ctl, ctx->num_sms, st);
+  if (n)
+    launch_tiny_count((const u64*)d_x, n, is_signed ? kSign : 0, ctx->d_ctl, ctx->num_sms, st,
+                      kGateNone);
   CKL();
   TRY(sync_ctl(ctx, st));
   for (int j = 0; j < nk; ++j) h_counts[j] = (int64_t)ctx->h_ctl->tiny_counts[c.tiny_slot[map[j]]];
@@ -649,12 +693,12 @@ int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   launch_estimate((const u64*)d_x, n, is_signed ? kSign : 0, 0, ctx->d_ctl, st);
   cudaError_t e = launch_hash_count((const u64*)d_x, n, is_signed ? kSign : 0, hash_mult,
                                     ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                                    ctx->num_sms, st);
+                                    ctx->num_sms, st, 1, kGateNone);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
   launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
-                 ctx->num_sms, st);
+                 ctx->num_sms, st, kGateNone);
   e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, n, ctx->pk_b, ctx->pc_b,
-                              ctx->poffs, st);
+                              ctx->poffs, st, kGateNone);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   TRY(sync_ctl(ctx, st));
   DevCtl c = *ctx->h_ctl;
@@ -693,9 +737,9 @@ int cafs_merge_pairs(cafs_ctx_t* ctx, const uint64_t* d_keys_in, const uint64_t*
   launch_insert_pairs((const u64*)d_keys_in, (const u64*)d_counts_in, m, CAFS_DEFAULT_HASH_MULT,
                       ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->num_sms, st);
   launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
-                 ctx->num_sms, st);
+                 ctx->num_sms, st, kGateNone);
   cudaError_t e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, ~0ull, ctx->pk_b,
-                                          ctx->pc_b, ctx->poffs, st);
+                                          ctx->pc_b, ctx->poffs, st, kGateNone);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   CKL();
   TRY(sync_ctl(ctx, st));
@@ -736,7 +780,7 @@ int cafs_pair_sort(cafs_ctx_t* ctx, uint64_t* d_keys, uint64_t* d_counts, uint64
     CK(cudaMemcpyAsync(ctx->pk_a, d_keys, npairs * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(ctx->pc_a, d_counts, npairs * 8, cudaMemcpyDeviceToDevice, st));
     cudaError_t e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, npairs, nullptr, 0, (u64*)d_keys,
-                                            (u64*)d_counts, ctx->poffs, st);
+                                            (u64*)d_counts, ctx->poffs, st, kGateNone);
     if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   } else {
     TRY(ensure_radix(ctx, npairs, false));
@@ -767,7 +811,7 @@ int cafs_emit_i64(cafs_ctx_t* ctx, const uint64_t* d_keys, const uint64_t* d_cou
   launch_scan((const u64*)d_counts, npairs, ctx->bsum, ctx->poffs, ctx->d_ctl, total, st);
   if (npairs && out_end > out_begin)
     launch_emit((const u64*)d_keys, ctx->poffs, 0, ctx->d_ctl, (u64*)d_out, out_begin, out_end,
-                is_signed ? kSign : 0, ctx->num_sms, st);
+                is_signed ? kSign : 0, ctx->num_sms, st, npairs);
   CKL();
   TRY(sync_ctl(ctx, st));
   if (ctx->h_ctl->sum_error)

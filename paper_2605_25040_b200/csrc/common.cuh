@@ -19,7 +19,7 @@ constexpr u64 kSign = 0x8000000000000000ull;
 constexpr u64 kGamma = 0x9E3779B97F4A7C15ull;
 constexpr u64 kEmpty = ~0ull;            // empty-slot sentinel of the hash tables
 constexpr int kSampleTarget = 1024;      // cardinality.py:26
-constexpr u64 kMonoPrefix = 1u << 16;    // rows the dispatch kernel checks for an inversion
+constexpr u64 kMonoPrefix = (1u << 14) + 1;  // rows the dispatch kernel checks (sorter.py:32)
 
 // Global (L2-resident) (key, count) table of the main route.
 constexpr int kGlobalLog2 = 22;                       // 4 Mi slots: 32 MB keys + 32 MB counts
@@ -57,7 +57,27 @@ struct DevCtl {
   u64 total;                     // sum of pair counts
   int32_t pairs_ready;
   int32_t sum_error;
+  // --- fused (sync-free) pipeline ---
+  int32_t eff_route;             // route with the monotone prefix applied (kNeedScan: unknown)
+  int32_t tiny_failed;           // the tiny pass missed a value -> main route runs
 };
+
+// eff_route value when the prefix is sorted but the array is longer than it
+constexpr int32_t kNeedScan = 5;
+
+// Gate modes: the fused pipeline launches every route's kernels back to back and
+// each kernel reads the device decision and exits unless its route is active.
+enum : int { kGateNone = 0, kGateTiny = 1, kGateMain = 2, kGateMainDense = 3, kGateMainHash = 4 };
+
+__device__ __forceinline__ bool gate_open(const DevCtl* ctl, int gate) {
+  if (gate == kGateNone) return true;
+  const int r = ctl->eff_route;
+  if (gate == kGateTiny) return r == CAFS_TINY_COUNT;
+  const bool main = r == CAFS_MAIN || (r == CAFS_TINY_COUNT && ctl->tiny_failed);
+  if (gate == kGateMain) return main;
+  const bool dense = ctl->range_len > 0;
+  return main && (gate == kGateMainDense ? dense : !dense);
+}
 
 __device__ __forceinline__ u64 fmix64(u64 z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -75,6 +95,12 @@ __device__ __forceinline__ ulonglong2 ld_stream_v2(const void* p) {
   asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
                : "=l"(v.x), "=l"(v.y) : "l"(p));
   return v;
+}
+
+// 256-bit streaming load (LDG.E.256 on sm_100a)
+__device__ __forceinline__ void ld_stream_v4(const void* p, u64& a, u64& b, u64& c, u64& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
 }
 
 __device__ __forceinline__ void st_stream_v2(void* p, u64 a, u64 b) {

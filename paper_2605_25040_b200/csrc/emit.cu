@@ -1,44 +1,35 @@
 // emit.cu -- K5: run-length emit of sorted (key, offset) pairs.
 //
 // Replaces emit / emit_fill (sorter.py:244-251, _kernels.py:172-182): the
-// reference walks pairs and fills out[p : p + c] = key.  Here the OUTPUT is
-// partitioned: each CTA owns a contiguous span of 16-byte vectors, finds its
-// first pair once with a 32-ary warp search over the offsets, then walks
-// 8192-element tiles.  A tile covered by a single run (the common case for
-// low-cardinality columns) is a pure streaming fill with 128-bit stores; a
-// fragmented tile gives each thread 16 consecutive positions, one binary
-// search and a forward walk.  The sign-bit flip back to int64 happens in the
-// store.  `begin/end` select a slice of the global sorted order, which is how
-// each GPU of a sharded sort writes only its own output rows.
+// reference walks the pairs and fills out[p : p + c] = key.  Here the OUTPUT
+// is partitioned into warp tiles of 1024 keys (8 KB): every warp works alone
+// (no block-level barrier), finds the pairs covering its tile with a binary
+// search of the offsets (staged once per CTA in shared memory when there are
+// at most kSmemOffs pairs), and writes with 256-bit stores (STG.256, one
+// 1 KB contiguous run per warp instruction).  A tile inside one run -- the
+// common case for low-cardinality columns -- is a pure store stream; a
+// fragmented tile resolves each lane's 4 keys by a search + forward walk.  The
+// bit-63 flip back to int64 happens in the store.  [begin, end) selects a
+// slice of the global sorted order: each GPU of a sharded sort writes only
+// its own rows.
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace cafs {
 
 constexpr int kEmitThreads = 512;
-constexpr u64 kEmitTileV = 4096;  // 16-byte vectors per tile (8192 keys)
+constexpr int kEmitVpl = 8;                       // 32-byte vectors per lane per tile
+constexpr u64 kTileKeys = 32ull * kEmitVpl * 4;  // 1024 keys per warp tile
+constexpr u64 kSmemOffs = 8192;                  // pairs whose offsets fit in smem
 
-// largest p in [lo, hi) with offs[p] <= g (offs non-decreasing, offs[lo] <= g)
-__device__ u64 warp_search(const u64* offs, u64 lo, u64 hi, u64 g) {
-  const int lane = threadIdx.x & 31;
-  while (hi - lo > 32) {
-    const u64 step = (hi - lo + 31) / 32;
-    u64 probe = lo + (u64)lane * step;
-    bool pred = probe < hi && offs[probe] <= g;
-    const u32 b = __ballot_sync(0xffffffffu, pred);
-    const int last = 31 - __clz(b);  // lane 0 always true (offs[lo] <= g)
-    lo = lo + (u64)last * step;
-    const u64 nh = lo + step;
-    hi = nh < hi ? nh : hi;
-  }
-  const u64 probe = lo + lane;
-  const bool pred = probe < hi && offs[probe] <= g;
-  const u32 b = __ballot_sync(0xffffffffu, pred);
-  return lo + (31 - __clz(b));
+__device__ __forceinline__ void st_v4(void* p, u64 a, u64 b, u64 c, u64 d) {
+  asm volatile("st.global.L1::no_allocate.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b),
+               "l"(c), "l"(d)
+               : "memory");
 }
 
-__device__ __forceinline__ u64 bsearch_pair(const u64* offs, u64 lo, u64 hi, u64 g) {
-  // largest p in [lo, hi] with offs[p] <= g
+// largest p in [lo, hi] with offs[p] <= g  (offs non-decreasing, offs[lo] <= g)
+__device__ __forceinline__ u64 find_pair(const u64* offs, u64 lo, u64 hi, u64 g) {
   while (lo < hi) {
     const u64 mid = (lo + hi + 1) >> 1;
     if (offs[mid] <= g) lo = mid; else hi = mid - 1;
@@ -46,89 +37,79 @@ __device__ __forceinline__ u64 bsearch_pair(const u64* offs, u64 lo, u64 hi, u64
   return lo;
 }
 
+template <bool SMEM>
 __global__ void __launch_bounds__(kEmitThreads)
-    emit_kernel(const u64* __restrict__ keys, const u64* __restrict__ offs, u64 npairs_arg,
+    emit_kernel(const u64* __restrict__ keys, const u64* __restrict__ goffs, u64 npairs_arg,
                 const DevCtl* ctl, u64* __restrict__ out, u64 begin, u64 end, u64 flip) {
-  __shared__ u64 sp[2][2];
+  extern __shared__ __align__(16) u64 soffs[];
   u64 npairs = npairs_arg;
   if (ctl) {
     if (!ctl->pairs_ready) return;
     npairs = ctl->npairs;
   }
   if (npairs == 0 || end <= begin) return;
-  const int tid = threadIdx.x, wid = tid >> 5;
+  if (SMEM && npairs > kSmemOffs) return;  // host picks the variant; guard anyway
+  const u64* offs = goffs;
+  if (SMEM) {
+    for (u64 i = threadIdx.x; i <= npairs; i += kEmitThreads) soffs[i] = goffs[i];
+    __syncthreads();
+    offs = soffs;
+  }
+  const int lane = threadIdx.x & 31;
   const u64 L = end - begin;
-  const u64 head = (((uintptr_t)out) & 15) ? 1 : 0;
-  const u64 nvec = L > head ? (L - head) / 2 : 0;
-  // scalar head / tail element
-  if (blockIdx.x == 0 && tid == 0) {
-    if (head) {
-      const u64 p = bsearch_pair(offs, 0, npairs - 1, begin);
-      out[0] = keys[p] ^ flip;
-    }
-    if (L > head && ((L - head) & 1)) {
-      const u64 p = bsearch_pair(offs, 0, npairs - 1, end - 1);
-      out[L - 1] = keys[p] ^ flip;
+  // 32-byte aligned body; up to 3 head and 3 tail keys are scalar
+  const u64 mis = (((uintptr_t)out) >> 3) & 3;
+  const u64 head = mis ? ((4 - mis) < L ? (4 - mis) : L) : 0;
+  const u64 nvec = (L - head) / 4;
+  const u64 body_end = head + nvec * 4;
+  if (blockIdx.x == 0 && threadIdx.x < 8) {
+    const u64 j = threadIdx.x < 4 ? threadIdx.x : body_end + (threadIdx.x - 4);
+    if ((threadIdx.x < 4 && j < head) || (threadIdx.x >= 4 && j < L)) {
+      const u64 p = find_pair(offs, 0, npairs - 1, begin + j);
+      out[j] = keys[p] ^ flip;
     }
   }
   if (nvec == 0) return;
-  // this CTA's vector span, a whole number of tiles
-  const u64 ntiles = (nvec + kEmitTileV - 1) / kEmitTileV;
-  const u64 tpb = (ntiles + gridDim.x - 1) / gridDim.x;
-  const u64 t_begin = (u64)blockIdx.x * tpb;
-  u64 t_end = t_begin + tpb;
-  if (t_end > ntiles) t_end = ntiles;
-  if (t_begin >= t_end) return;
-  ulonglong2* ov = (ulonglong2*)(out + head);
-  const u64 gbase = begin + head;  // global position of vector 0's first element
-
-  u64 p = 0;  // running pair cursor (warp 0)
-  if (wid == 0) p = warp_search(offs, 0, npairs, gbase + t_begin * kEmitTileV * 2);
-  int par = 0;
-  for (u64 t = t_begin; t < t_end; ++t, par ^= 1) {
-    const u64 v0 = t * kEmitTileV;
-    const u64 v1 = (v0 + kEmitTileV) < nvec ? (v0 + kEmitTileV) : nvec;
-    const u64 g0 = gbase + v0 * 2, glast = gbase + v1 * 2 - 1;
-    if (wid == 0) {
-      const int lane = tid & 31;
-      // advance p to the pair containing g0 (offs[npairs] = total > glast stops the scan)
-      while (true) {
-        const u64 q = p + 1 + lane;
-        const bool le = q <= npairs && offs[q] <= g0;
-        const u32 b = __ballot_sync(0xffffffffu, le);
-        p += __popc(b);
-        if (b != 0xffffffffu) break;
-      }
-      u64 p1 = p;
-      while (true) {
-        const u64 q = p1 + 1 + lane;
-        const bool le = q <= npairs && offs[q] <= glast;
-        const u32 b = __ballot_sync(0xffffffffu, le);
-        p1 += __popc(b);
-        if (b != 0xffffffffu) break;
-      }
-      if (lane == 0) { sp[par][0] = p; sp[par][1] = p1; }
-    }
-    __syncthreads();
-    const u64 p0 = sp[par][0], p1 = sp[par][1];
+  u64* ob = out + head;
+  const u64 gb = begin + head;  // global position of ob[0]
+  const u64 ntiles = (nvec * 4 + kTileKeys - 1) / kTileKeys;
+  const u64 nwarps = (u64)gridDim.x * (kEmitThreads / 32);
+  const u64 gw = (u64)blockIdx.x * (kEmitThreads / 32) + (threadIdx.x >> 5);
+  u64 p = 0;  // pair cursor: tiles are visited in increasing order per warp
+  for (u64 t = gw; t < ntiles; t += nwarps) {
+    const u64 e0 = t * kTileKeys;
+    const u64 e1 = (e0 + kTileKeys) < nvec * 4 ? (e0 + kTileKeys) : nvec * 4;
+    u64 p0 = 0, p1 = 0;
+    if (lane == 0) p0 = find_pair(offs, p, npairs - 1, gb + e0);
+    if (lane == 1) p1 = find_pair(offs, p, npairs - 1, gb + e1 - 1);
+    p0 = __shfl_sync(0xffffffffu, p0, 0);
+    p1 = __shfl_sync(0xffffffffu, p1, 1);
+    p = p0;
     if (p0 == p1) {
       const u64 k = keys[p0] ^ flip;
-      for (u64 v = v0 + tid; v < v1; v += kEmitThreads) st_stream_v2(ov + v, k, k);
+#pragma unroll
+      for (int j = 0; j < kEmitVpl; ++j) {
+        const u64 e = e0 + ((u64)j * 32 + lane) * 4;
+        if (e < e1) st_v4(ob + e, k, k, k, k);
+      }
     } else {
-      // 8 vectors (16 keys) per thread: one search, then walk forward
-      const u64 va = v0 + (u64)tid * 8;
-      if (va < v1) {
-        const u64 g = gbase + va * 2;
-        u64 q = bsearch_pair(offs, p0, p1, g);
-        u64 nb = offs[q + 1];
-        u64 kq = keys[q] ^ flip;
-        const int nv = (int)((v1 - va) < 8 ? (v1 - va) : 8);
-        for (int e = 0; e < nv; ++e) {
-          const u64 ga = g + 2 * e;
-          while (ga >= nb) { ++q; nb = offs[q + 1]; kq = keys[q] ^ flip; }
-          const u64 ka = kq;
-          while (ga + 1 >= nb) { ++q; nb = offs[q + 1]; kq = keys[q] ^ flip; }
-          st_stream_v2(ov + va + e, ka, kq);
+      u64 q = p0;
+#pragma unroll 1
+      for (int j = 0; j < kEmitVpl; ++j) {
+        const u64 e = e0 + ((u64)j * 32 + lane) * 4;
+        if (e < e1) {
+          const u64 g = gb + e;
+          q = find_pair(offs, q, p1, g);
+          u64 kv[4];
+          u64 qq = q;
+          u64 nb = offs[qq + 1];
+          kv[0] = keys[qq] ^ flip;
+#pragma unroll
+          for (int r = 1; r < 4; ++r) {
+            while (g + r >= nb) { ++qq; nb = offs[qq + 1]; }
+            kv[r] = keys[qq] ^ flip;
+          }
+          st_v4(ob + e, kv[0], kv[1], kv[2], kv[3]);
         }
       }
     }
@@ -136,13 +117,30 @@ __global__ void __launch_bounds__(kEmitThreads)
 }
 
 void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, u64* out,
-                 u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st) {
+                 u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 npairs_bound) {
   const u64 L = end > begin ? end - begin : 0;
-  u64 tiles = (L / 2 + kEmitTileV - 1) / kEmitTileV;
+  const u64 wtiles = (L + kTileKeys - 1) / kTileKeys;
   u64 grid = (u64)num_sms * 4;
-  if (tiles < grid) grid = tiles ? tiles : 1;
-  emit_kernel<<<(unsigned)grid, kEmitThreads, 0, st>>>(keys, offs, npairs, ctl, out, begin, end,
-                                                       flip);
+  const u64 need = (wtiles + (kEmitThreads / 32) - 1) / (kEmitThreads / 32);
+  if (need < grid) grid = need ? need : 1;
+  // npairs_bound: an upper bound of the pair count known on the host (the device
+  // count may be smaller); smem staging when it fits
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(emit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((kSmemOffs + 1) * 8));
+    attr_dev = dev;
+  }
+  if (npairs_bound <= kSmemOffs) {
+    const size_t sm = (size_t)(npairs_bound + 1) * 8;
+    emit_kernel<true><<<(unsigned)grid, kEmitThreads, sm, st>>>(keys, offs, npairs, ctl, out,
+                                                                begin, end, flip);
+  } else {
+    emit_kernel<false><<<(unsigned)grid, kEmitThreads, 0, st>>>(keys, offs, npairs, ctl, out,
+                                                                 begin, end, flip);
+  }
 }
 
 }  // namespace cafs

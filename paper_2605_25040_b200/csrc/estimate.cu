@@ -6,9 +6,11 @@
 //     here; only a prefix that is already sorted triggers the full-array scan
 //     kernel below (random inputs pay ~0 extra bytes);
 //   * _sample (cardinality.py:99-110): samples x[i * (n // 1024)], i < 1024;
-//   * FreqSet spectrum (cardinality.py:63-73): instead of a 4096-slot linear
-//     probing table the 1024 samples are bitonic-sorted in shared memory and
-//     run lengths counted.  (u, f1, f2) are hash-independent, so this is exact
+//   * FreqSet spectrum (cardinality.py:31-73): a 2048-slot linear
+//     probing table of the multiplicative hash (the reference: 4096), built in smem
+//     by all 1024 samples at once (CAS claims).  Concurrent insertion can place
+//     a key in a different slot than the sequential reference, but
+//     (u, f1, f2) and the sorted distinct keys are hash- and order-independent
 //     (the reference's own test, tests/test_cardinality.py:139-152);
 //   * chao1 (cardinality.py:85-96) in IEEE float64 with explicit _rn ops;
 //   * route chain of sorter.py:153-162 and, for the tiny route, the ascending
@@ -42,18 +44,44 @@ __device__ __forceinline__ int warp_incl_sum(int v) {
   return v;
 }
 
+__device__ __forceinline__ u64 warp_min_u64(u64 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = t < v ? t : v;
+  }
+  return v;
+}
+__device__ __forceinline__ u64 warp_max_u64(u64 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = t > v ? t : v;
+  }
+  return v;
+}
+
+constexpr int kFreqSlots = 2048;  // <= 50% load for 1024 samples (reference: 4096, cardinality.py:27)
+
 __global__ void __launch_bounds__(1024, 1)
     estimate_kernel(const u64* __restrict__ x, u64 n, u64 flip, int check_prefix, DevCtl* ctl) {
-  __shared__ u64 s[kSampleTarget];
-  __shared__ int warp_a[32], warp_b[32];
+  __shared__ u64 fkeys[kFreqSlots];
+  __shared__ u32 fcnt[kFreqSlots];
+  __shared__ u64 rmin[32], rmax[32];
+  __shared__ long long red[3][32];
+  __shared__ u32 n_max_key;  // occurrences of the sentinel value ~0 among the samples
   __shared__ int inv;
   __shared__ int best_t;
-  __shared__ long long red[3][32];
+  __shared__ u32 nlist;
+  __shared__ u64 klist[CAFS_TINY_MAX_KEYS];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
+  for (int i = tid; i < kFreqSlots; i += 1024) { fkeys[i] = kEmpty; fcnt[i] = 0; }
   if (tid == 0) {
     inv = 0;
     best_t = 0x7fffffff;
+    n_max_key = 0;
+    nlist = 0;
     // per-call state of the later stages
     ctl->scan_inversion = 0;
     ctl->tiny_miss = 0;
@@ -66,63 +94,59 @@ __global__ void __launch_bounds__(1024, 1)
     ctl->total = 0;
     ctl->pairs_ready = 0;
     ctl->sum_error = 0;
+    ctl->tiny_failed = 0;
   }
   if (tid < 16) ctl->tiny_counts[tid] = 0;
   __syncthreads();
 
-  // ---- K0: prefix monotone probe (exact: any inversion => not monotone) ----
+  // ---- K0: prefix monotone probe over the reference's first chunk ----
   if (check_prefix) {
+    // 16 coalesced (x[i], x[i+1]) pairs per thread, every load issued before
+    // any compare: one DRAM round trip for the whole 16385-row prefix
     const u64 P = n < kMonoPrefix ? n : kMonoPrefix;
+    u64 a[16], b[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const u64 i = (u64)tid + 1024u * j;
+      a[j] = i + 1 < P ? x[i] : 0;
+      b[j] = i + 1 < P ? x[i + 1] : 0;
+    }
     int found = 0;
-    for (u64 i = tid; i + 1 < P; i += blockDim.x) found |= ((x[i + 1] ^ flip) < (x[i] ^ flip));
+#pragma unroll
+    for (int j = 0; j < 16; ++j) found |= (b[j] ^ flip) < (a[j] ^ flip);
     if (__syncthreads_or(found) && tid == 0) inv = 1;
   }
 
-  // ---- K1: 1024 strided samples (cardinality.py:102-104) ----
+  // ---- K1: 1024 strided samples (cardinality.py:102-104) into a FreqSet ----
   const u64 m = n < (u64)kSampleTarget ? n : (u64)kSampleTarget;
   u64 stride = n / kSampleTarget;
   if (stride < 1) stride = 1;
-  s[tid] = (u64)tid < m ? (x[(u64)tid * stride] ^ flip) : kEmpty;
-  __syncthreads();
-  // bitonic sort, 1024 keys, one per thread
-  for (int k = 2; k <= kSampleTarget; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      int p = tid ^ j;
-      if (p > tid) {
-        u64 a = s[tid], b = s[p];
-        bool up = (tid & k) == 0;
-        if ((a > b) == up) { s[tid] = b; s[p] = a; }
+  const bool valid = (u64)tid < m;
+  const u64 v = valid ? (x[(u64)tid * stride] ^ flip) : 0;
+  if (valid) {
+    if (v == kEmpty) {
+      atomicAdd(&n_max_key, 1u);
+    } else {
+      u32 j = (u32)((v * kGamma) >> 53);  // fast_hash(v, 11); the reference uses 12 bits (cardinality.py:47-61)
+      while (true) {
+        const u64 old = atomicCAS(&fkeys[j], kEmpty, v);
+        if (old == kEmpty || old == v) { atomicAdd(&fcnt[j], 1u); break; }
+        j = (j + 1) & (kFreqSlots - 1);
       }
-      __syncthreads();
     }
   }
-  // ---- spectrum over the first m sorted samples ----
-  const bool valid = (u64)tid < m;
-  const u64 v = s[tid];
-  const bool start = valid && (tid == 0 || s[tid - 1] != v);
-  const bool last = valid && ((u64)tid == m - 1 || s[tid + 1] != v);
-  // run start index (inclusive max-scan of start ? tid : 0)
-  int rs = warp_incl_max(start ? tid : 0);
-  if (lane == 31) warp_a[wid] = rs;
-  // distinct-key rank (inclusive sum of start flags)
-  int rk = warp_incl_sum(start ? 1 : 0);
-  if (lane == 31) warp_b[wid] = rk;
+  u64 lo = warp_min_u64(valid ? v : kEmpty), hi = warp_max_u64(valid ? v : 0ull);
+  if (lane == 0) { rmin[wid] = lo; rmax[wid] = hi; }
   __syncthreads();
-  if (wid == 0) {
-    int a = warp_incl_max(warp_a[lane]);
-    int b = warp_incl_sum(warp_b[lane]);
-    warp_a[lane] = a;  // inclusive
-    warp_b[lane] = b;
+  // ---- spectrum (cardinality.py:63-69): u, f1, f2 ----
+  long long cu = 0, c1 = 0, c2 = 0;
+  for (int i = tid; i < kFreqSlots; i += 1024) {
+    const u32 c = fcnt[i];
+    cu += c > 0;
+    c1 += c == 1;
+    c2 += c == 2;
   }
-  __syncthreads();
-  if (wid > 0) {
-    rs = max(rs, warp_a[wid - 1]);
-    rk += warp_b[wid - 1];
-  }
-  const int len = tid - rs + 1;
-  long long cu = start ? 1 : 0;
-  long long c1 = (last && len == 1) ? 1 : 0;
-  long long c2 = (last && len == 2) ? 1 : 0;
+  if (tid == 0 && n_max_key) { cu += 1; c1 += n_max_key == 1; c2 += n_max_key == 2; }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     cu += __shfl_xor_sync(0xffffffffu, cu, o);
@@ -131,20 +155,24 @@ __global__ void __launch_bounds__(1024, 1)
   }
   if (lane == 0) { red[0][wid] = cu; red[1][wid] = c1; red[2][wid] = c2; }
   __syncthreads();
-  if (wid == 0) {
-    cu = red[0][lane]; c1 = red[1][lane]; c2 = red[2][lane];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      cu += __shfl_xor_sync(0xffffffffu, cu, o);
-      c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-      c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-    }
-    if (lane == 0) { red[0][0] = cu; red[1][0] = c1; red[2][0] = c2; }
+  long long u = 0, f1 = 0, f2 = 0;
+  for (int w = 0; w < 32; ++w) { u += red[0][w]; f1 += red[1][w]; f2 += red[2][w]; }
+  // distinct keys (FreqSet.distinct_keys) when u <= 8: collect, then sort
+  if (u <= CAFS_TINY_MAX_KEYS) {
+    for (int i = tid; i < kFreqSlots; i += 1024)
+      if (fcnt[i]) klist[atomicAdd(&nlist, 1u)] = fkeys[i];
+    if (tid == 0 && n_max_key) klist[atomicAdd(&nlist, 1u)] = kEmpty;
   }
   __syncthreads();
-  const long long u = red[0][0], f1 = red[1][0], f2 = red[2][0];
-  // distinct keys ascending (FreqSet.distinct_keys)
-  if (start && rk - 1 < CAFS_TINY_MAX_KEYS) ctl->keys[rk - 1] = v;
+  if (tid == 0 && u <= CAFS_TINY_MAX_KEYS) {
+    for (int a = 1; a < (int)u; ++a) {  // insertion sort, <= 8 keys
+      const u64 k = klist[a];
+      int b = a - 1;
+      while (b >= 0 && klist[b] > k) { klist[b + 1] = klist[b]; --b; }
+      klist[b + 1] = k;
+    }
+    for (int a = 0; a < (int)u; ++a) ctl->keys[a] = klist[a];
+  }
 
   // ---- chao1 (cardinality.py:85-96), bit-exact float64 ----
   const bool saturated = (u == kSampleTarget);
@@ -165,12 +193,13 @@ __global__ void __launch_bounds__(1024, 1)
 
   // ---- tiny route: perfect hash of the <= 8 keys into 16 slots ----
   if (route == CAFS_TINY_COUNT) {
+    __syncthreads();
     const int nk = (int)u;
     const u64 mult = fmix64((u64)tid + 0x5851F42D4C957F2Dull) | 1ull;
     u32 used = 0;
     bool ok = true;
     for (int j = 0; j < nk; ++j) {
-      u32 sl = (u32)((ctl->keys[j] * mult) >> 60);
+      const u32 sl = (u32)((klist[j] * mult) >> 60);
       ok &= !((used >> sl) & 1u);
       used |= 1u << sl;
     }
@@ -178,13 +207,15 @@ __global__ void __launch_bounds__(1024, 1)
     __syncthreads();
     if (tid == best_t) {
       ctl->tiny_mult = mult;
-      for (int j = 0; j < nk; ++j) ctl->tiny_slot[j] = (int)((ctl->keys[j] * mult) >> 60);
+      for (int j = 0; j < nk; ++j) ctl->tiny_slot[j] = (int)((klist[j] * mult) >> 60);
     }
   }
 
   if (tid == 0) {
     ctl->prefix_sorted = !inv;
     ctl->route = route;
+    ctl->eff_route = (check_prefix && !inv) ? (n <= kMonoPrefix ? CAFS_ALREADY_SORTED : kNeedScan)
+                                            : route;
     ctl->u = u;
     ctl->f1 = f1;
     ctl->f2 = f2;
@@ -192,11 +223,15 @@ __global__ void __launch_bounds__(1024, 1)
     ctl->saturated = saturated;
     ctl->nkeys = (int)(u < CAFS_TINY_MAX_KEYS ? u : CAFS_TINY_MAX_KEYS);
     // dense-range window for the main count: centred on the sample's span
-    const u64 lo = s[0], hi = s[m - 1];
-    const u64 width = hi - lo;
-    if (width < kRangeCap / 2) {
+    u64 smin = kEmpty, smax = 0;
+    for (int w = 0; w < 32; ++w) {
+      smin = rmin[w] < smin ? rmin[w] : smin;
+      smax = rmax[w] > smax ? rmax[w] : smax;
+    }
+    const u64 width = smax - smin;
+    if (m > 0 && smax >= smin && width < kRangeCap / 2) {
       const u64 margin = (kRangeCap - 1 - width) / 2;
-      u64 base = lo >= margin ? lo - margin : 0ull;
+      u64 base = smin >= margin ? smin - margin : 0ull;
       if (base > kEmpty - (kRangeCap - 1)) base = kEmpty - (kRangeCap - 1);
       ctl->range_base = base;
       ctl->range_len = kRangeCap;

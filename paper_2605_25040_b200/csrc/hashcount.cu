@@ -7,9 +7,10 @@
 // (key, count) cell, cells are merged by key, the spill guard re-routes to the
 // fallback -- with a layout for 148 SMs:
 //
-//   * persistent CTAs (one per SM, 1024 threads); warp 0 is a TMA producer
-//     that streams 16 KB chunks of the int64 column into a 6-stage shared
-//     memory ring (cp.async.bulk + mbarrier complete_tx), warps 1..31 consume;
+//   * persistent CTAs (one per SM, 1024 threads); thread 0 doubles as the TMA
+//     producer that streams 32 KB chunks of the int64 column into a 3-stage
+//     shared-memory ring (cp.async.bulk + mbarrier complete_tx); all 32 warps
+//     consume, two 16-byte vectors per thread per stage;
 //   * per element (bit-63 flip in registers):
 //       - dense-range window (dictionary-encoded columns): one shared atomic
 //         into counts[v - base]; the window is set by the estimate kernel from
@@ -17,30 +18,32 @@
 //         the hash path;
 //       - otherwise a per-CTA shared open-addressing (u64 key, u32 count) table,
 //         first probe inline, linear probing + CAS claims on the slow path,
-//         claims capped at 3/4 load;
+//         claims capped at load 1/2;
 //       - keys that find no shared slot go to the global L2-resident table
 //         (global_insert in common.cuh): the analogue of the reference's spill;
 //   * one flush per CTA of its shared cells into the global table;
 //   * the guard: global table overflow (more than kGlobalCap distinct keys or
 //     a probe chain over kGlobalMaxProbe) sets ctl->overflow and the pipeline
 //     re-routes to the fallback radix sort (reference guard: sorter.py:264-273).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace cafs {
 
 constexpr int kHcThreads = 1024;
-constexpr int kHcConsumers = kHcThreads - 32;
 constexpr u32 kRange = 8192;              // dense window (u32 counters, 32 KB)
 constexpr int kSLog2 = 13;                // shared table: 8192 slots (64 KB keys + 32 KB counts)
 constexpr u32 kS = 1u << kSLog2;
-constexpr u32 kSClaimCap = kS * 3 / 4;
-constexpr int kSMaxProbe = 32;
-constexpr int kStages = 6;
-constexpr u32 kStageKeys = 2048;          // 16 KB per stage
-constexpr size_t kHcSmem =
-    (size_t)kRange * 4 + (size_t)kS * 8 + (size_t)kS * 4 + (size_t)kStages * kStageKeys * 8 +
-    (size_t)2 * kStages * 8 + 16;
+constexpr u32 kSClaimCap = kS / 2;        // claims stop at load 1/2 (short miss chains)
+constexpr int kSMaxProbe = 16;
+constexpr size_t kTableSmem = (size_t)kRange * 4 + (size_t)kS * 8 + (size_t)kS * 4;
+template <int STAGES, int STAGE_KEYS, int QCAP>
+constexpr size_t hc_smem() {
+  return kTableSmem + (size_t)STAGES * STAGE_KEYS * 8 + (size_t)32 * QCAP * 8 +
+         (size_t)2 * STAGES * 8 + 16;
+}
 
 struct HcArgs {
   const u64* x;
@@ -52,6 +55,7 @@ struct HcArgs {
   u64* gcnt;
   u32* glist;
   int use_range;
+  int gate;
 };
 
 // key -> global table, keeping the sentinel value out of it
@@ -60,29 +64,65 @@ __device__ __forceinline__ void table_add(const HcArgs& a, u64 key, u64 inc) {
   else global_insert(a.gkeys, a.gcnt, a.glist, a.ctl, key, inc, a.mult);
 }
 
+// Shared-table miss: linear probing with capped claims, else the global table.
+// Returns 1 when the key went to the global table.
+__device__ __noinline__ u32 count_slow(u64 v, u64* skeys, u32* scnt, u32* sclaims,
+                                       const HcArgs& a) {
+  u32 h = mhash(v, a.mult, 64 - kSLog2);
+  for (int p = 0; p < kSMaxProbe; ++p) {
+    const u64 k = *((volatile u64*)&skeys[h]);
+    if (k == v) { atomicAdd(&scnt[h], 1u); return 0; }
+    if (k == kEmpty) {
+      if (*((volatile u32*)sclaims) >= kSClaimCap) break;
+      const u64 old = atomicCAS(&skeys[h], kEmpty, v);
+      if (old == kEmpty) {
+        atomicAdd(sclaims, 1u);
+        atomicAdd(&scnt[h], 1u);
+        return 0;
+      }
+      if (old == v) { atomicAdd(&scnt[h], 1u); return 0; }
+    }
+    h = (h + 1) & (kS - 1);
+  }
+  global_insert(a.gkeys, a.gcnt, a.glist, a.ctl, v, 1, a.mult);
+  return 1;
+}
+
+// STAGES x STAGE_KEYS TMA ring fed by a dedicated producer warp (warp 0);
+// warps 1..31 consume.  STAGE_KEYS / 2 is a multiple of the 992 consumers so
+// every consumer takes the same number of 16-byte vectors per stage.
+// QCAP > 0: first-probe misses are queued per warp and resolved 32 at a time
+// with the whole warp active (the slow path is otherwise run by a few lanes
+// of a diverged warp, leaving its L2 round trips unoverlapped).
+template <int STAGES, int STAGE_KEYS, int QCAP>
 __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
+  if (!gate_open(a.ctl, a.gate)) return;
+  constexpr int kConsumers = kHcThreads - 32;
+  static_assert((STAGE_KEYS / 2) % kConsumers == 0, "balanced stages");
+  constexpr u32 kVpt = STAGE_KEYS / 2 / kConsumers;
   extern __shared__ __align__(128) unsigned char smem[];
-  u64* stage = (u64*)smem;                                        // [kStages][kStageKeys]
-  u64* skeys = stage + (size_t)kStages * kStageKeys;              // [kS]
+  u64* stage = (u64*)smem;                                        // [STAGES][STAGE_KEYS]
+  u64* skeys = stage + (size_t)STAGES * STAGE_KEYS;               // [kS]
   u32* scnt = (u32*)(skeys + kS);                                 // [kS]
   u32* dcnt = scnt + kS;                                          // [kRange]
-  u64* full = (u64*)(dcnt + kRange);                              // [kStages]
-  u64* empty = full + kStages;                                    // [kStages]
+  u64* queue = (u64*)(dcnt + kRange);                             // [32][QCAP]
+  u64* full = queue + 32 * QCAP;                                  // [STAGES]
+  u64* empty = full + STAGES;                                     // [STAGES]
   __shared__ u32 sclaims;
   __shared__ u64 red_empty[32], red_glob[32];
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u64 flip = a.flip, mult = a.mult;
   const u64 base = a.use_range ? a.ctl->range_base : 0ull;
-  const u32 rlen = a.use_range ? a.ctl->range_len : 0u;
+  const u64 rlen = a.use_range ? a.ctl->range_len : 0u;
 
   for (u32 i = tid; i < kS; i += kHcThreads) { skeys[i] = kEmpty; scnt[i] = 0; }
   for (u32 i = tid; i < kRange; i += kHcThreads) dcnt[i] = 0;
   if (tid == 0) {
     sclaims = 0;
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kHcConsumers / 32);
+      mbar_init(&empty[s], kConsumers / 32);
     }
     fence_mbar_init();
   }
@@ -93,84 +133,110 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   const u64 head = (((uintptr_t)a.x) & 15) ? 1 : 0;
   const u64 body = n > head ? ((n - head) & ~1ull) : 0;
   const u64* xb = a.x + head;
-  const u64 nchunks = (body + kStageKeys - 1) / kStageKeys;
+  const u64 nchunks = (body + STAGE_KEYS - 1) / STAGE_KEYS;
+  const u64 my_chunks =
+      nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
-  u64 empty_cnt = 0, glob_cnt = 0;
+  u64 empty_cnt = 0;
+  u32 glob_cnt = 0;
 
-  auto count1 = [&](u64 raw) {
-    const u64 v = raw ^ flip;
+  // direct window or first shared probe; false = unresolved (slow path)
+  auto fast = [&](u64 v) -> bool {
     const u64 d = v - base;
-    if (d < rlen) {
-      atomicAdd(&dcnt[d], 1u);
-      return;
-    }
-    if (v == kEmpty) { empty_cnt++; return; }
-    u32 h = mhash(v, mult, 64 - kSLog2);
-    u64 k = skeys[h];
-    if (k == v) { atomicAdd(&scnt[h], 1u); return; }
-    // slow path: linear probing with capped claims
-    for (int p = 0; p < kSMaxProbe; ++p) {
-      if (k == v) { atomicAdd(&scnt[h], 1u); return; }
-      if (k == kEmpty) {
-        if (*((volatile u32*)&sclaims) >= kSClaimCap) break;
-        u64 old = atomicCAS(&skeys[h], kEmpty, v);
-        if (old == kEmpty) {
-          atomicAdd(&sclaims, 1u);
-          atomicAdd(&scnt[h], 1u);
-          return;
-        }
-        if (old == v) { atomicAdd(&scnt[h], 1u); return; }
-      }
-      h = (h + 1) & (kS - 1);
-      k = *((volatile u64*)&skeys[h]);
-    }
-    glob_cnt++;
-    global_insert(a.gkeys, a.gcnt, a.glist, a.ctl, v, 1, mult);
+    if (d < rlen) { atomicAdd(&dcnt[d], 1u); return true; }
+    if (v == kEmpty) { empty_cnt++; return true; }
+    const u32 h = mhash(v, mult, 64 - kSLog2);
+    if (skeys[h] == v) { atomicAdd(&scnt[h], 1u); return true; }
+    return false;
+  };
+  auto count1 = [&](u64 v) {
+    if (!fast(v)) glob_cnt += count_slow(v, skeys, scnt, &sclaims, a);
   };
 
   if (wid == 0) {
     // ---- TMA producer ----
     if (lane == 0) {
-      u32 it = 0;
-      for (u64 c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
-        const u32 s = it % kStages;
-        const u32 ph = (it / kStages) & 1;
-        if (it >= (u32)kStages) mbar_wait(&empty[s], ph ^ 1);
-        const u64 off = c * kStageKeys;
-        const u64 cnt = (body - off) < kStageKeys ? (body - off) : kStageKeys;
-        const u32 bytes = (u32)(cnt * 8);
+      for (u64 it = 0; it < my_chunks; ++it) {
+        const u32 s = (u32)(it % STAGES);
+        if (it >= (u64)STAGES) mbar_wait(&empty[s], (u32)(((it / STAGES) - 1) & 1));
+        const u64 off = (blockIdx.x + it * gridDim.x) * STAGE_KEYS;
+        const u32 bytes = (u32)(((body - off) < STAGE_KEYS ? (body - off) : STAGE_KEYS) * 8);
         mbar_arrive_expect_tx(&full[s], bytes);
-        tma_load_1d(stage + (size_t)s * kStageKeys, xb + off, bytes, &full[s]);
+        tma_load_1d(stage + (size_t)s * STAGE_KEYS, xb + off, bytes, &full[s]);
       }
     }
   } else {
-    // ---- consumers ----
     const int ctid = tid - 32;
-    u32 it = 0;
-    for (u64 c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
-      const u32 s = it % kStages;
-      const u32 ph = (it / kStages) & 1;
-      mbar_wait(&full[s], ph);
-      const u64 off = c * kStageKeys;
-      const u32 cnt = (u32)((body - off) < kStageKeys ? (body - off) : kStageKeys);
-      const ulonglong2* sv = (const ulonglong2*)(stage + (size_t)s * kStageKeys);
-      for (u32 i = ctid; i < cnt / 2; i += kHcConsumers) {
-        ulonglong2 v = sv[i];
-        count1(v.x);
-        count1(v.y);
+    u64* wq = queue + (size_t)wid * QCAP;
+    u32 qn = 0;  // warp-uniform queue length
+    auto enqueue = [&](bool miss, u64 v) {
+      const u32 m = __ballot_sync(0xffffffffu, miss);
+      if (m == 0) return;
+      if (miss) wq[qn + __popc(m & lanemask_lt())] = v;
+      qn += __popc(m);
+      if (qn >= 32) {
+        __syncwarp();
+        const u64 u = wq[qn - 32 + lane];
+        __syncwarp();
+        qn -= 32;
+        glob_cnt += count_slow(u, skeys, scnt, &sclaims, a);
+      }
+    };
+    for (u64 it = 0; it < my_chunks; ++it) {
+      const u32 s = (u32)(it % STAGES);
+      mbar_wait(&full[s], (u32)((it / STAGES) & 1));
+      const u64 off = (blockIdx.x + it * gridDim.x) * STAGE_KEYS;
+      const u32 nv = (u32)(((body - off) < STAGE_KEYS ? (body - off) : STAGE_KEYS) / 2);
+      const ulonglong2* sv = (const ulonglong2*)(stage + (size_t)s * STAGE_KEYS);
+#pragma unroll
+      for (u32 q = 0; q < kVpt; ++q) {
+        const u32 i = ctid + q * kConsumers;
+        const bool valid = i < nv;
+        ulonglong2 w = make_ulonglong2(0, 0);
+        if (valid) w = sv[i];
+        const u64 v0 = w.x ^ flip, v1 = w.y ^ flip;
+        const u64 d0 = v0 - base, d1 = v1 - base;
+        if (QCAP == 0) {
+          if (valid) {
+            if (d0 < rlen && d1 < rlen) {
+              atomicAdd(&dcnt[d0], 1u);
+              atomicAdd(&dcnt[d1], 1u);
+            } else {
+              count1(v0);
+              count1(v1);
+            }
+          }
+        } else {
+          bool m0 = false, m1 = false;
+          if (valid) {
+            if (d0 < rlen && d1 < rlen) {
+              atomicAdd(&dcnt[d0], 1u);
+              atomicAdd(&dcnt[d1], 1u);
+            } else {
+              m0 = !fast(v0);
+              m1 = !fast(v1);
+            }
+          }
+          enqueue(m0, v0);
+          enqueue(m1, v1);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
+    if (QCAP > 0) {
+      __syncwarp();
+      if ((u32)lane < qn) glob_cnt += count_slow(wq[lane], skeys, scnt, &sclaims, a);
+    }
     if (blockIdx.x == 0 && ctid == 0) {
-      if (head && n > 0) count1(a.x[0]);
-      if (n > head && ((n - head) & 1)) count1(a.x[n - 1]);
+      if (head && n > 0) count1(a.x[0] ^ flip);
+      if (n > head && ((n - head) & 1)) count1(a.x[n - 1] ^ flip);
     }
   }
   __syncthreads();
 
   // ---- flush the CTA's shared cells into the global table ----
-  for (u32 d = tid; d < rlen; d += kHcThreads) {
+  for (u32 d = tid; d < (u32)rlen; d += kHcThreads) {
     const u32 c = dcnt[d];
     if (c) table_add(a, base + d, c);
   }
@@ -178,18 +244,19 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
     const u32 c = scnt[h];
     if (c) table_add(a, skeys[h], c);
   }
+  u64 g = glob_cnt;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     empty_cnt += __shfl_xor_sync(0xffffffffu, empty_cnt, o);
-    glob_cnt += __shfl_xor_sync(0xffffffffu, glob_cnt, o);
+    g += __shfl_xor_sync(0xffffffffu, g, o);
   }
-  if (lane == 0) { red_empty[wid] = empty_cnt; red_glob[wid] = glob_cnt; }
+  if (lane == 0) { red_empty[wid] = empty_cnt; red_glob[wid] = g; }
   __syncthreads();
   if (tid == 0) {
-    u64 e = 0, g = 0;
-    for (int w = 0; w < kHcThreads / 32; ++w) { e += red_empty[w]; g += red_glob[w]; }
+    u64 e = 0, gg = 0;
+    for (int w = 0; w < kHcThreads / 32; ++w) { e += red_empty[w]; gg += red_glob[w]; }
     if (e) atomicAdd(&a.ctl->empty_key_count, e);
-    if (g) atomicAdd(&a.ctl->g_updates, g);
+    if (gg) atomicAdd(&a.ctl->g_updates, gg);
   }
 }
 
@@ -197,8 +264,8 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
 // table is clean for the next call.  The sentinel key's count becomes the last
 // pair.
 __global__ void compact_kernel(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys,
-                               u64* pcnt) {
-  if (ctl->overflow) return;
+                               u64* pcnt, int gate) {
+  if (ctl->overflow || !gate_open(ctl, gate)) return;
   const u64 m = ctl->g_used;
   const u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += stride) {
@@ -254,28 +321,59 @@ void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevC
                                                          glist);
 }
 
-size_t hash_count_smem() { return kHcSmem; }
+size_t hash_count_smem() { return hc_smem<3, 3968, 0>(); }
 
-cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
-                              u64* gcnt, u32* glist, int use_range, int num_sms,
-                              cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(hash_count_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHcSmem);
+template <int ST, int SK, int QC>
+static cudaError_t launch_hc(const HcArgs& a, u64 n, int num_sms, cudaStream_t st) {
+  constexpr size_t sm = hc_smem<ST, SK, QC>();
+  static_assert(sm <= 232448 - 2048, "shared memory budget");
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(hash_count_kernel<ST, SK, QC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    attr_dev = dev;
   }
-  HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range};
-  u64 chunks = (n + kStageKeys - 1) / kStageKeys;
-  int grid = (int)(chunks < (u64)num_sms ? (chunks ? chunks : 1) : (u64)num_sms);
-  hash_count_kernel<<<grid, kHcThreads, kHcSmem, st>>>(a);
+  const u64 chunks = (n + SK - 1) / SK;
+  const int grid = (int)(chunks < (u64)num_sms ? (chunks ? chunks : 1) : (u64)num_sms);
+  hash_count_kernel<ST, SK, QC><<<grid, kHcThreads, sm, st>>>(a);
   return cudaGetLastError();
 }
 
+// Pipeline-shape variants (CAFS_HC_VARIANT, tuning only).  Default: the
+// direct-window shape when the estimate kernel opened a dense window (few
+// misses expected), the queued shape otherwise.
+static int hc_variant() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("CAFS_HC_VARIANT");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+// variant: 0 = dense-window shape (deep TMA ring, inline slow path),
+//          1 = queued shape (smaller ring + per-warp miss queues)
+cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
+                              u64* gcnt, u32* glist, int use_range, int num_sms,
+                              cudaStream_t st, int variant, int gate) {
+  HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate};
+  int v = hc_variant();
+  if (v < 0) v = variant == 0 ? 0 : 2;
+  switch (v) {
+    case 1: return launch_hc<2, 3968, 64>(a, n, num_sms, st);
+    case 2: return launch_hc<3, 1984, 64>(a, n, num_sms, st);  // queued default
+    case 3: return launch_hc<6, 1984, 0>(a, n, num_sms, st);
+    case 4: return launch_hc<4, 1984, 64>(a, n, num_sms, st);
+    default: return launch_hc<3, 3968, 0>(a, n, num_sms, st);
+  }
+}
+
 void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys, u64* pcnt,
-                    int num_sms, cudaStream_t st) {
-  compact_kernel<<<num_sms, 256, 0, st>>>(ctl, gkeys, gcnt, glist, pkeys, pcnt);
+                    int num_sms, cudaStream_t st, int gate) {
+  compact_kernel<<<num_sms, 256, 0, st>>>(ctl, gkeys, gcnt, glist, pkeys, pcnt, gate);
 }
 
 }  // namespace cafs

@@ -13,20 +13,22 @@ void launch_estimate(const u64* x, u64 n, u64 flip, int check_prefix, DevCtl* ct
 void launch_monotone_scan(const u64* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
                           cudaStream_t st);
 // tiny.cu
-void launch_tiny_count(const u64* x, u64 n, u64 flip, DevCtl* ctl, int num_sms, cudaStream_t st);
+void launch_tiny_count(const u64* x, u64 n, u64 flip, DevCtl* ctl, int num_sms, cudaStream_t st,
+                       int gate);
 void launch_tiny_finalize(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,
-                          cudaStream_t st);
+                          cudaStream_t st, int gate);
 // hashcount.cu
 size_t hash_count_smem();
 cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
-                              u64* gcnt, u32* glist, int use_range, int num_sms, cudaStream_t st);
+                              u64* gcnt, u32* glist, int use_range, int num_sms, cudaStream_t st,
+                              int variant, int gate);
 void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevCtl* ctl,
                          u64* gkeys, u64* gcnt, u32* glist, int num_sms, cudaStream_t st);
 void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys, u64* pcnt,
-                    int num_sms, cudaStream_t st);
+                    int num_sms, cudaStream_t st, int gate);
 // emit.cu
 void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, u64* out,
-                 u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st);
+                 u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 npairs_bound);
 // radix.cu
 size_t onesweep_smem(bool has_val);
 u64 onesweep_tiles(u64 n);
@@ -39,7 +41,8 @@ cudaError_t launch_onesweep(const u64* src, const u64* srcv, u64* dst, u64* dstv
 size_t small_sort_smem();
 cudaError_t launch_small_sort_keys(u64* keys, u64 n, u64 flip, cudaStream_t st);
 cudaError_t launch_small_sort_pairs(u64* keys, const u64* cnt, u64 n, DevCtl* ctl, u64 expect,
-                                    u64* out_keys, u64* out_cnt, u64* out_offs, cudaStream_t st);
+                                    u64* out_keys, u64* out_cnt, u64* out_offs, cudaStream_t st,
+                                    int gate);
 void launch_scan(const u64* in, u64 n, u64* bsum, u64* out_offs, DevCtl* ctl, u64 expect,
                  cudaStream_t st);
 // gen.cu

@@ -197,61 +197,132 @@ __global__ void __launch_bounds__(kOsThreads)
 }
 
 // ---------------- single-CTA sorts (<= kSmallSortMax) ----------------
-// Bitonic sort in shared memory of up to 8192 keys (+ optional u64 payload via
-// an index permutation).  Used for the small-n fallback route and for the
-// main route's (key, count) pairs; pairs also get their exclusive offsets.
-__device__ __forceinline__ bool pair_less(u64 ka, u32 ia, u64 kb, u32 ib) {
-  return ka < kb || (ka == kb && ia < ib);
-}
-
+// LSD radix sort of up to 8192 keys in shared memory (the reference's own
+// pair-sort algorithm, _kernels.py:185-214: stable 8-bit digits), carrying a
+// 16-bit index so pairs keep their counts.  Bytes that are equal across all
+// keys (OR == AND) are skipped: dictionary codes need 2 passes, not 8.  Each
+// warp ranks a contiguous segment with the 8-ballot multisplit, so the sort is
+// stable.  Used for the small-n fallback route and the main route's
+// (key, count) pairs, which also get their exclusive offsets (emit's input).
 template <bool PAIRS>
 __global__ void __launch_bounds__(1024, 1)
     small_sort_kernel(u64* keys_io, const u64* in_cnt, u64 n_arg, u64 flip, DevCtl* ctl,
-                      u64 expect_total, u64* out_keys, u64* out_cnt, u64* out_offs) {
+                      u64 expect_total, u64* out_keys, u64* out_cnt, u64* out_offs, int gate) {
   extern __shared__ __align__(16) unsigned char smem[];
-  u64* sk = (u64*)smem;                     // [P]
-  unsigned short* si = (unsigned short*)(sk + kSmallSortMax);  // [P]
+  u64* kb = (u64*)smem;                                       // [2][kSmallSortMax]
+  unsigned short* ib = (unsigned short*)(kb + 2 * kSmallSortMax);  // [2][kSmallSortMax]
+  u32* wcnt = (u32*)(ib + 2 * kSmallSortMax);                 // [32][256]
+  __shared__ u32 dstart[256], wsum8[8];
+  __shared__ u64 red_or[32], red_and[32];
   __shared__ u64 wsum[32];
-  __shared__ u32 P_sh;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   u64 n = n_arg;
   if (PAIRS && ctl) {
-    if (ctl->overflow) return;
+    if (ctl->overflow || !gate_open(ctl, gate)) return;
     n = ctl->npairs;
     if (n > (u64)kSmallSortMax) {
       if (tid == 0) ctl->need_large = 1;
       return;
     }
   }
-  u32 P = 2;
-  while (P < n) P <<= 1;
-  for (u32 i = tid; i < P; i += blockDim.x) {
-    if (i < n) { sk[i] = keys_io[i] ^ flip; si[i] = (unsigned short)i; }
-    else { sk[i] = kEmpty; si[i] = 0xFFFF; }
+  u64 vor = 0, vand = ~0ull;
+  for (u32 i = tid; i < n; i += 1024) {
+    const u64 k = keys_io[i] ^ flip;
+    kb[i] = k;
+    ib[i] = (unsigned short)i;
+    vor |= k;
+    vand &= k;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    vor |= __shfl_xor_sync(0xffffffffu, vor, o);
+    vand &= __shfl_xor_sync(0xffffffffu, vand, o);
+  }
+  if (lane == 0) { red_or[wid] = vor; red_and[wid] = vand; }
   __syncthreads();
-  for (u32 k = 2; k <= P; k <<= 1) {
-    for (u32 j = k >> 1; j > 0; j >>= 1) {
-      for (u32 i = tid; i < P; i += blockDim.x) {
-        const u32 p = i ^ j;
-        if (p > i) {
-          const u64 a = sk[i], b = sk[p];
-          const u32 ia = si[i], ib = si[p];
-          const bool up = (i & k) == 0;
-          if (pair_less(b, ib, a, ia) == up) {
-            sk[i] = b; sk[p] = a; si[i] = (unsigned short)ib; si[p] = (unsigned short)ia;
-          }
-        }
+  vor = 0; vand = ~0ull;
+  for (int w = 0; w < 32; ++w) { vor |= red_or[w]; vand &= red_and[w]; }
+  const u64 vary = vor ^ vand;  // bits that differ between some keys
+
+  // each warp owns a contiguous, 32-aligned segment of at most 8 rounds
+  const u32 seg = (u32)(((n + 31) / 32 + 31) / 32) * 32;  // items per warp (multiple of 32)
+  const u32 w0 = wid * seg;
+  int cur = 0;
+  for (int p = 0; p < 8; ++p) {
+    if (((vary >> (8 * p)) & 0xFF) == 0) continue;
+    const int shift = 8 * p;
+    u64* src = kb + cur * kSmallSortMax;
+    u64* dst = kb + (cur ^ 1) * kSmallSortMax;
+    unsigned short* isrc = ib + cur * kSmallSortMax;
+    unsigned short* idst = ib + (cur ^ 1) * kSmallSortMax;
+    u32* my = wcnt + wid * 256;
+    for (int i = lane; i < 256; i += 32) my[i] = 0;
+    __syncwarp();
+    u32 rank[8], dig[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const u32 idx = w0 + r * 32 + lane;
+      const bool valid = (u32)(r * 32) < seg && idx < n;
+      const u32 d = valid ? (u32)(src[idx] >> shift) & 255u : 0u;
+      u32 peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const u32 bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bb : ~bb;
       }
-      __syncthreads();
+      u32 before = 0;
+      if (valid) before = my[d];
+      __syncwarp();
+      if (valid) {
+        rank[r] = before + __popc(peers & lanemask_lt());
+        if (lane == 31 - __clz(peers)) my[d] = before + __popc(peers);
+      }
+      dig[r] = d;
+      __syncwarp();
     }
+    __syncthreads();
+    if (tid < 256) {  // exclusive prefix over warps, then over digits
+      u32 acc = 0;
+      for (int w = 0; w < 32; ++w) {
+        const u32 c = wcnt[w * 256 + tid];
+        wcnt[w * 256 + tid] = acc;
+        acc += c;
+      }
+      u32 incl = acc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) wsum8[wid] = incl;
+      dstart[tid] = incl - acc;
+    }
+    __syncthreads();
+    if (tid < 256) {
+      u32 pre = 0;
+      for (int w = 0; w < wid; ++w) pre += wsum8[w];
+      dstart[tid] += pre;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const u32 idx = w0 + r * 32 + lane;
+      if ((u32)(r * 32) < seg && idx < n) {
+        const u32 pos = dstart[dig[r]] + wcnt[wid * 256 + dig[r]] + rank[r];
+        dst[pos] = src[idx];
+        idst[pos] = isrc[idx];
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
   }
+  const u64* sk = kb + cur * kSmallSortMax;
+  const unsigned short* si = ib + cur * kSmallSortMax;
   if (!PAIRS) {
-    for (u32 i = tid; i < n; i += blockDim.x) keys_io[i] = sk[i] ^ flip;
+    for (u32 i = tid; i < n; i += 1024) keys_io[i] = sk[i] ^ flip;
     return;
   }
   // gather counts in key order and take the exclusive scan (8 items/thread)
-  const int lane = tid & 31, wid = tid >> 5;
   constexpr int IT = kSmallSortMax / 1024;
   u64 c[IT];
   u64 local = 0;
@@ -393,16 +464,28 @@ cudaError_t launch_onesweep(const u64* src, const u64* srcv, u64* dst, u64* dstv
   const u64 tiles = onesweep_tiles(n);
   cudaError_t e;
   if (hv) {
-    e = cudaFuncSetAttribute(onesweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sm);
-    if (e != cudaSuccess) return e;
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+      e = cudaFuncSetAttribute(onesweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sm);
+      if (e != cudaSuccess) return e;
+      attr_dev = dev;
+    }
     onesweep_kernel<true><<<(unsigned)tiles, kOsThreads, sm, st>>>(
         src, srcv, dst, dstv, n, 8 * pass, flip_in, flip_out, gbase, tile_state, tile_counter,
         epoch);
   } else {
-    e = cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sm);
-    if (e != cudaSuccess) return e;
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+      e = cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sm);
+      if (e != cudaSuccess) return e;
+      attr_dev = dev;
+    }
     onesweep_kernel<false><<<(unsigned)tiles, kOsThreads, sm, st>>>(
         src, nullptr, dst, nullptr, n, 8 * pass, flip_in, flip_out, gbase, tile_state,
         tile_counter, epoch);
@@ -410,26 +493,39 @@ cudaError_t launch_onesweep(const u64* src, const u64* srcv, u64* dst, u64* dstv
   return cudaGetLastError();
 }
 
-size_t small_sort_smem() { return (size_t)kSmallSortMax * (8 + 2); }
+size_t small_sort_smem() { return (size_t)kSmallSortMax * (16 + 4) + 32 * 256 * 4; }
 
 cudaError_t launch_small_sort_keys(u64* keys, u64 n, u64 flip, cudaStream_t st) {
   const size_t sm = small_sort_smem();
-  cudaError_t e = cudaFuncSetAttribute(small_sort_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(small_sort_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
   small_sort_kernel<false><<<1, 1024, sm, st>>>(keys, nullptr, n, flip, nullptr, 0, nullptr,
-                                                nullptr, nullptr);
+                                                nullptr, nullptr, kGateNone);
   return cudaGetLastError();
 }
 
 cudaError_t launch_small_sort_pairs(u64* keys, const u64* cnt, u64 n, DevCtl* ctl, u64 expect,
-                                    u64* out_keys, u64* out_cnt, u64* out_offs, cudaStream_t st) {
+                                    u64* out_keys, u64* out_cnt, u64* out_offs, cudaStream_t st,
+                                    int gate) {
   const size_t sm = small_sort_smem();
-  cudaError_t e = cudaFuncSetAttribute(small_sort_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(small_sort_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
   small_sort_kernel<true><<<1, 1024, sm, st>>>(keys, cnt, n, 0, ctl, expect, out_keys, out_cnt,
-                                               out_offs);
+                                               out_offs, gate);
   return cudaGetLastError();
 }
 

@@ -21,7 +21,8 @@ constexpr int kTinyThreads = 512;
 constexpr int kTinyWarps = kTinyThreads / 32;
 
 __global__ void __launch_bounds__(kTinyThreads)
-    tiny_count_kernel(const u64* __restrict__ x, u64 n, u64 flip, DevCtl* ctl) {
+    tiny_count_kernel(const u64* __restrict__ x, u64 n, u64 flip, DevCtl* ctl, int gate) {
+  if (!gate_open(ctl, gate)) return;
   __shared__ u64 skey[16];
   __shared__ u32 cnt[kTinyWarps][16][32];
   __shared__ u64 wmiss[kTinyWarps];
@@ -90,10 +91,12 @@ __global__ void __launch_bounds__(kTinyThreads)
 }
 
 // Success check (sum == n <=> no miss) and the <= 8 sorted pairs + offsets.
-__global__ void tiny_finalize_kernel(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs) {
-  if (threadIdx.x != 0) return;
+__global__ void tiny_finalize_kernel(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,
+                                     int gate) {
+  if (threadIdx.x != 0 || !gate_open(ctl, gate)) return;
   if (ctl->tiny_miss != 0) {
     ctl->pairs_ready = 0;
+    ctl->tiny_failed = 1;
     return;
   }
   const int nk = ctl->nkeys;
@@ -113,17 +116,17 @@ __global__ void tiny_finalize_kernel(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, 
 }
 
 void launch_tiny_count(const u64* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
-                       cudaStream_t st) {
+                       cudaStream_t st, int gate) {
   u64 blocks = (n / 2 + kTinyThreads * 8 - 1) / (kTinyThreads * 8);
   u64 maxb = (u64)num_sms * 4;
   if (blocks > maxb) blocks = maxb;
   if (blocks < 1) blocks = 1;
-  tiny_count_kernel<<<(unsigned)blocks, kTinyThreads, 0, st>>>(x, n, flip, ctl);
+  tiny_count_kernel<<<(unsigned)blocks, kTinyThreads, 0, st>>>(x, n, flip, ctl, gate);
 }
 
 void launch_tiny_finalize(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,
-                          cudaStream_t st) {
-  tiny_finalize_kernel<<<1, 32, 0, st>>>(ctl, n, pkeys, pcnt, poffs);
+                          cudaStream_t st, int gate) {
+  tiny_finalize_kernel<<<1, 32, 0, st>>>(ctl, n, pkeys, pcnt, poffs, gate);
 }
 
 }  // namespace cafs

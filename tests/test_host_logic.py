@@ -1,0 +1,103 @@
+"""Host-side mirror of the reference API (CPU only): arithmetic pinned to the
+reference's golden values, argument validation with the reference's exception
+types, and the API surface (names, enum values, dataclass fields)."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+import paper_2605_25040_b200 as cafs
+from conftest import load_json
+from oracle import gen as ogen
+from paper_2605_25040_b200 import datagen
+
+
+def test_fast_hash_matches_reference(known_answers):
+    for row in known_answers["fast_hash"]:
+        v, m, want = row[:3]
+        mult = row[3] if len(row) > 3 else None
+        assert cafs.fast_hash(v, m, mult) == want
+    assert cafs.fast_hash(1, 9) == 316  # tests/test_buckets.py:38-40
+    xs = np.arange(4096, dtype=np.uint64)
+    assert cafs.fast_hash(xs, 12).tolist() == [cafs.fast_hash(int(v), 12) for v in xs]
+    for bad in (0, 64, -3):
+        with pytest.raises(ValueError):
+            cafs.fast_hash(1, bad)
+
+
+def test_table_size_matches_reference(known_answers):
+    for k_hat, n, cap, want in known_answers["table_size_for"]:
+        assert cafs.table_size_for(k_hat, n, cap) == want
+    for args in ((0, 10, 4), (1, 0, 4), (1, 10, 5)):
+        with pytest.raises(ValueError):
+            cafs.table_size_for(*args)
+
+
+def test_chao1_matches_reference(known_answers):
+    for u, f1, f2, n, sat, want in known_answers["chao1"]:
+        assert cafs.chao1(u, f1, f2, n, sat) == want
+    with pytest.raises(ValueError):
+        cafs.chao1(0, 0, 0, 10, False)
+
+
+def test_check_hash_mult():
+    assert cafs.check_hash_mult(None) == 0x9E3779B97F4A7C15
+    assert cafs.check_hash_mult(3) == 3
+    for bad in (2, 0, -1, 1 << 64):
+        with pytest.raises(ValueError):
+            cafs.check_hash_mult(bad)
+
+
+def test_validation_errors_match_reference_types():
+    """sorter.py:302-314: raised before any device work."""
+    with pytest.raises(TypeError):
+        cafs.cafs_sort([3, 1, 2])
+    with pytest.raises(TypeError):
+        cafs.cafs_sort(np.zeros(4, np.float64))
+    with pytest.raises(ValueError):
+        cafs.cafs_sort(np.zeros((2, 2), np.uint64))
+    ro = np.zeros(4, np.uint64)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        cafs.cafs_sort(ro)
+    with pytest.raises(ValueError):
+        cafs.cafs_sort(np.zeros(4, np.uint64), hash_mult=4)
+    import torch
+    with pytest.raises(TypeError):
+        cafs.cafs_sort(torch.zeros(4, dtype=torch.float32))
+    with pytest.raises(ValueError):
+        cafs.cafs_sort(torch.zeros((2, 2), dtype=torch.int64))
+
+
+def test_api_surface_mirrors_reference():
+    # sorter.py:44-49 Route values, :52-57 DispatchDecision, :60-81 SortTelemetry,
+    # cardinality.py:76-82 CardinalityEstimate
+    assert [r.value for r in cafs.Route] == [
+        "already_sorted", "fallback_small_n", "tiny_count", "fallback_high_entropy", "main"]
+    assert [f.name for f in dataclasses.fields(cafs.DispatchDecision)] == [
+        "route", "keys", "k_hat", "estimate"]
+    assert [f.name for f in dataclasses.fields(cafs.CardinalityEstimate)] == [
+        "k_hat", "u", "f1", "f2", "saturated"]
+    ref_tel = ["n", "decision", "spill_len", "guard_fired", "stage_ms", "counted_total",
+               "updates", "tiny_count_failed", "table"]
+    assert [f.name for f in dataclasses.fields(cafs.SortTelemetry)][:len(ref_tel)] == ref_tel
+    assert cafs.SortTelemetry().route is None
+    assert (cafs.SMALL_N_CUTOFF, cafs.TINY_MAX_KEYS, cafs.SAMPLE_TARGET) == (2048, 8, 1024)
+    pl = cafs.PairList.from_pairs([(5, 2), (1, 3)])
+    assert pl.to_pairs() == [(5, 2), (1, 3)] and len(pl) == 2
+
+
+def test_package_configs_match_oracle_configs():
+    for name, c in datagen.CONFIGS.items():
+        o = ogen.CONFIGS[name]
+        assert (c.n, c.k, c.dist, c.s, c.palette, c.seed) == (o.n, o.k, o.dist, o.s, o.palette,
+                                                              o.seed)
+        if c.dist == "zipf":
+            assert np.array_equal(datagen.zipf_cdf(c.k, c.s), o.cdf())
+
+
+def test_config_seeds_route_as_intended():
+    rec = {r["name"]: r["route"] for r in load_json("config_cases.json")}
+    assert rec == {"cfg1": "main", "cfg2": "tiny_count", "cfg3": "main",
+                   "cfg5": "fallback_high_entropy", "cfg4": "main"}
