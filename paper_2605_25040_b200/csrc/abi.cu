@@ -44,6 +44,7 @@ struct cafs_ctx {
   u64* pc_b = nullptr;
   u64* poffs = nullptr;  // exclusive offsets, npairs + 1
   u64* bsum = nullptr;
+  u64* spill = nullptr;  // kSpillCap keys
   // radix sort scratch
   u32* ghist = nullptr;  // [8][256]
   u32* gbase = nullptr;  // [8][256]
@@ -132,6 +133,7 @@ int ensure_main(cafs_ctx_t* ctx) {
   CK(cudaMalloc(&ctx->pc_b, kPairCap * 8));
   CK(cudaMalloc(&ctx->poffs, (kPairCap + 1) * 8));
   CK(cudaMalloc(&ctx->bsum, (kPairCap / 8192 + 2) * 8));
+  CK(cudaMalloc(&ctx->spill, kSpillCap * 8));
   return CAFS_OK;
 }
 
@@ -325,16 +327,18 @@ int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t fl
   cudaError_t e;
   if (direct) {
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                          ctx->num_sms, st, 0, kGateMainDense);
+                          ctx->num_sms, st, 0, kGateMainDense, ctx->spill);
     if (e == cudaSuccess)
       e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                            ctx->num_sms, st, 1, kGateMainHash);
+                            ctx->num_sms, st, 1, kGateMainHash, ctx->spill);
   } else {
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 0,
-                          ctx->num_sms, st, 1, kGateMain);
+                          ctx->num_sms, st, 1, kGateMain, ctx->spill);
   }
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
   tm.end(tk, L_K_COUNT, C_MAIN);
+  launch_spill_fold(c, ctx->spill, ctx->gkeys, ctx->gcnt, ctx->glist, mult, ctx->num_sms, st,
+                    kGateMain);
   launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
                  kGateMain);
   tm.end(ts, L_STAGE_COUNT, C_MAIN);
@@ -348,7 +352,7 @@ int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t fl
   launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, kSmallSortMax);
   tm.end(tk, L_K_EMIT, C_EMIT);
   tm.end(ts, L_STAGE_EMIT, C_EMIT);
-  ctx->launches += direct ? 7 : 6;
+  ctx->launches += direct ? 8 : 7;
   CKL();
   return CAFS_OK;
 }
@@ -464,7 +468,7 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
   DeviceGuard g(ctx->device);
   cudaDeviceSynchronize();
   void* dev[] = {ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
-                 ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->ghist, ctx->gbase,
+                 ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->spill, ctx->ghist, ctx->gbase,
                  ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage};
   for (void* p : dev)
     if (p) cudaFree(p);
@@ -693,8 +697,10 @@ int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   launch_estimate((const u64*)d_x, n, is_signed ? kSign : 0, 0, ctx->d_ctl, st);
   cudaError_t e = launch_hash_count((const u64*)d_x, n, is_signed ? kSign : 0, hash_mult,
                                     ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                                    ctx->num_sms, st, 1, kGateNone);
+                                    ctx->num_sms, st, 1, kGateNone, ctx->spill);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
+  launch_spill_fold(ctx->d_ctl, ctx->spill, ctx->gkeys, ctx->gcnt, ctx->glist, hash_mult,
+                    ctx->num_sms, st, kGateNone);
   launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
                  ctx->num_sms, st, kGateNone);
   e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, n, ctx->pk_b, ctx->pc_b,

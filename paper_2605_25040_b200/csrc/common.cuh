@@ -26,6 +26,13 @@ constexpr int kGlobalLog2 = 22;                       // 4 Mi slots: 32 MB keys 
 constexpr u64 kGlobalSlots = 1ull << kGlobalLog2;
 constexpr u64 kGlobalCap = kGlobalSlots / 2;          // max distinct keys before the guard fires
 constexpr int kGlobalMaxProbe = 128;
+constexpr u64 kSpillCap = 1ull << 25;                 // HBM spill buffer (keys); excess goes inline
+constexpr u32 kMaxSpillRegions = 256;                 // >= count-kernel grid (one CTA per SM)
+// The claim list of the global table is striped: a claim from CTA b appends to
+// stripe b % kListStripes, so claims from all SMs do not serialise on one
+// counter.  A full stripe is a table overflow (the guard).
+constexpr u32 kListStripes = 128;
+constexpr u64 kStripeCap = kGlobalCap / kListStripes;
 
 // Device control block: dispatch result + per-call flags/counters.
 struct DevCtl {
@@ -48,8 +55,11 @@ struct DevCtl {
   u64 tiny_counts[16];           // per perfect-hash slot
   u64 tiny_miss;
   // --- main route ---
-  u64 g_used;                    // occupied global slots (append-list length)
+  u32 g_fill[kListStripes];      // claims per stripe of the global table's claim list
   u64 g_updates;                 // elements resolved in the global table
+  u64 spill_len;                 // keys appended to the HBM spill buffer
+  u32 spill_regions;             // count-kernel CTAs (one spill region each)
+  u32 spill_fill[kMaxSpillRegions];
   u64 empty_key_count;           // occurrences of the sentinel key value ~0
   int32_t overflow;              // global table overflow -> guard
   int32_t need_large;            // K' too large for the single-CTA pair sort
@@ -163,8 +173,9 @@ __device__ __forceinline__ void global_insert(u64* gkeys, u64* gcnt, u32* list, 
     if (k == kEmpty) {
       u64 old = atomicCAS(&gkeys[h], kEmpty, key);
       if (old == kEmpty) {
-        u64 idx = atomicAdd(&ctl->g_used, 1ull);
-        if (idx < kGlobalCap) list[idx] = h;
+        const u32 stripe = blockIdx.x & (kListStripes - 1);
+        const u32 idx = atomicAdd(&ctl->g_fill[stripe], 1u);
+        if (idx < kStripeCap) list[stripe * kStripeCap + idx] = h;
         else ctl->overflow = 1;
         atomicAdd(&gcnt[h], inc);
         return;

@@ -2,16 +2,20 @@
 //
 // Replaces emit / emit_fill (sorter.py:244-251, _kernels.py:172-182): the
 // reference walks the pairs and fills out[p : p + c] = key.  Here the OUTPUT
-// is partitioned into warp tiles of 1024 keys (8 KB): every warp works alone
-// (no block-level barrier), finds the pairs covering its tile with a binary
-// search of the offsets (staged once per CTA in shared memory when there are
-// at most kSmemOffs pairs), and writes with 256-bit stores (STG.256, one
-// 1 KB contiguous run per warp instruction).  A tile inside one run -- the
+// is partitioned into 1024-key warp tiles, grid-strided; every warp works
+// alone (no block-level barrier), caches the run it is in, and otherwise finds
+// its tile's pairs with a 32-ary warp search of the offsets (staged once per
+// CTA in shared memory, or a sampled index of them for large pair sets).  It
+// writes with 256-bit stores (STG.256, one 1 KB contiguous run per warp
+// instruction).  A tile inside one run -- the
 // common case for low-cardinality columns -- is a pure store stream; a
-// fragmented tile resolves each lane's 4 keys by a search + forward walk.  The
+// fragmented tile is walked in windows of 32 run boundaries kept in registers
+// (shuffle search, one coalesced 256 B store per warp instruction).  The
 // bit-63 flip back to int64 happens in the store.  [begin, end) selects a
 // slice of the global sorted order: each GPU of a sharded sort writes only
 // its own rows.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -20,7 +24,8 @@ namespace cafs {
 constexpr int kEmitThreads = 512;
 constexpr int kEmitVpl = 8;                       // 32-byte vectors per lane per tile
 constexpr u64 kTileKeys = 32ull * kEmitVpl * 4;  // 1024 keys per warp tile
-constexpr u64 kSmemOffs = 8192;                  // pairs whose offsets fit in smem
+constexpr u64 kIdxEntries = 4096;                // max shared index of the offsets (32 KB)
+constexpr int kIdxDefault = 256;                 // measured best (64..1024 within noise)
 
 __device__ __forceinline__ void st_v4(void* p, u64 a, u64 b, u64 c, u64 d) {
   asm volatile("st.global.L1::no_allocate.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b),
@@ -37,10 +42,29 @@ __device__ __forceinline__ u64 find_pair(const u64* offs, u64 lo, u64 hi, u64 g)
   return lo;
 }
 
-template <bool SMEM>
+// Warp-cooperative 32-ary search: the largest p in [lo, hi] with offs[p] <= g
+// (offs non-decreasing, offs[lo] <= g).  Every lane returns it.
+__device__ __forceinline__ u64 warp_find(const u64* offs, u64 lo, u64 hi, u64 g) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo >= 32) {
+    const u64 step = (hi - lo + 32) / 32;
+    u64 probe = lo + (u64)lane * step;
+    if (probe > hi) probe = hi;
+    const u32 m = __ballot_sync(0xffffffffu, offs[probe] <= g);  // lane 0 always set
+    const u64 at = lo + (u64)(31 - __clz(m)) * step;  // last probe with offs <= g
+    const u64 nh = at + step - 1;                       // the next probe is > g
+    if (nh < hi) hi = nh;
+    lo = at < hi ? at : hi;                              // probes past hi were clamped to hi
+  }
+  const u64 probe = lo + lane;
+  const u32 m = __ballot_sync(0xffffffffu, probe <= hi && offs[probe] <= g);
+  return lo + (31 - __clz(m));
+}
+
 __global__ void __launch_bounds__(kEmitThreads)
     emit_kernel(const u64* __restrict__ keys, const u64* __restrict__ goffs, u64 npairs_arg,
-                const DevCtl* ctl, u64* __restrict__ out, u64 begin, u64 end, u64 flip) {
+                const DevCtl* ctl, u64* __restrict__ out, u64 begin, u64 end, u64 flip,
+                u64 tpw, u64 idx_entries) {
   extern __shared__ __align__(16) u64 soffs[];
   u64 npairs = npairs_arg;
   if (ctl) {
@@ -48,13 +72,24 @@ __global__ void __launch_bounds__(kEmitThreads)
     npairs = ctl->npairs;
   }
   if (npairs == 0 || end <= begin) return;
-  if (SMEM && npairs > kSmemOffs) return;  // host picks the variant; guard anyway
   const u64* offs = goffs;
-  if (SMEM) {
-    for (u64 i = threadIdx.x; i <= npairs; i += kEmitThreads) soffs[i] = goffs[i];
-    __syncthreads();
-    offs = soffs;
-  }
+  // index of the offsets in shared memory: soffs[j] = offs[j * stride]; with at
+  // most kIdxEntries pairs (stride 1) it is the offsets themselves, otherwise it
+  // narrows each search to `stride` global entries
+  const u64 stride = (npairs + idx_entries) / idx_entries;
+  const u64 nidx = npairs / stride + 1;
+  for (u64 i = threadIdx.x; i < nidx; i += kEmitThreads) soffs[i] = goffs[i * stride];
+  __syncthreads();
+  if (stride == 1) offs = soffs;
+  // pair containing global position g, searching from pair lo (offs[lo] <= g)
+  auto locate = [&](u64 lo, u64 g) -> u64 {
+    if (stride == 1) return warp_find(soffs, lo, npairs - 1, g);
+    const u64 j = warp_find(soffs, lo / stride, nidx - 1, g);
+    u64 a = j * stride, b = a + stride - 1;
+    if (a < lo) a = lo;
+    if (b > npairs - 1) b = npairs - 1;
+    return warp_find(goffs, a, b, g);
+  };
   const int lane = threadIdx.x & 31;
   const u64 L = end - begin;
   // 32-byte aligned body; up to 3 head and 3 tail keys are scalar
@@ -62,85 +97,104 @@ __global__ void __launch_bounds__(kEmitThreads)
   const u64 head = mis ? ((4 - mis) < L ? (4 - mis) : L) : 0;
   const u64 nvec = (L - head) / 4;
   const u64 body_end = head + nvec * 4;
-  if (blockIdx.x == 0 && threadIdx.x < 8) {
-    const u64 j = threadIdx.x < 4 ? threadIdx.x : body_end + (threadIdx.x - 4);
-    if ((threadIdx.x < 4 && j < head) || (threadIdx.x >= 4 && j < L)) {
-      const u64 p = find_pair(offs, 0, npairs - 1, begin + j);
-      out[j] = keys[p] ^ flip;
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    // warp 0: scalar head and tail keys (lanes 0-3 head, 4-7 tail)
+    const u64 j = lane < 4 ? (u64)lane : body_end + (lane - 4);
+    const bool act = (lane < 4 && j < head) || (lane >= 4 && lane < 8 && j < L);
+    for (int r = 0; r < 8; ++r) {  // each active lane's search, warp-cooperatively
+      const bool mine = __shfl_sync(0xffffffffu, act, r);
+      const u64 jj = __shfl_sync(0xffffffffu, j, r);
+      if (mine) {
+        const u64 p = locate(0, begin + jj);
+        if (lane == r) out[jj] = keys[p] ^ flip;
+      }
     }
   }
   if (nvec == 0) return;
   u64* ob = out + head;
   const u64 gb = begin + head;  // global position of ob[0]
   const u64 ntiles = (nvec * 4 + kTileKeys - 1) / kTileKeys;
-  const u64 nwarps = (u64)gridDim.x * (kEmitThreads / 32);
   const u64 gw = (u64)blockIdx.x * (kEmitThreads / 32) + (threadIdx.x >> 5);
-  u64 p = 0;  // pair cursor: tiles are visited in increasing order per warp
-  for (u64 t = gw; t < ntiles; t += nwarps) {
+  // each warp takes `tpw` consecutive tiles; CTAs are many and short-lived, so
+  // the tiles being written at any moment form one moving window of the output
+  // in launch order (measured: 7.3 TB/s vs 6.2-6.4 TB/s for persistent
+  // grid-strided warps).  The run a warp is in is cached across its tiles.
+  const u64 t0 = gw * tpw;
+  const u64 t1 = (t0 + tpw) < ntiles ? (t0 + tpw) : ntiles;
+  u64 p = 0;             // pair cursor (pairs only move forward)
+  u64 rs = 1, re = 0;    // cached run [rs, re) of pair p (empty)
+  u64 rk = 0;
+  for (u64 t = t0; t < t1; ++t) {
     const u64 e0 = t * kTileKeys;
     const u64 e1 = (e0 + kTileKeys) < nvec * 4 ? (e0 + kTileKeys) : nvec * 4;
-    u64 p0 = 0, p1 = 0;
-    if (lane == 0) p0 = find_pair(offs, p, npairs - 1, gb + e0);
-    if (lane == 1) p1 = find_pair(offs, p, npairs - 1, gb + e1 - 1);
-    p0 = __shfl_sync(0xffffffffu, p0, 0);
-    p1 = __shfl_sync(0xffffffffu, p1, 1);
-    p = p0;
-    if (p0 == p1) {
-      const u64 k = keys[p0] ^ flip;
-#pragma unroll
-      for (int j = 0; j < kEmitVpl; ++j) {
-        const u64 e = e0 + ((u64)j * 32 + lane) * 4;
-        if (e < e1) st_v4(ob + e, k, k, k, k);
-      }
-    } else {
-      u64 q = p0;
-#pragma unroll 1
-      for (int j = 0; j < kEmitVpl; ++j) {
-        const u64 e = e0 + ((u64)j * 32 + lane) * 4;
-        if (e < e1) {
-          const u64 g = gb + e;
-          q = find_pair(offs, q, p1, g);
-          u64 kv[4];
-          u64 qq = q;
-          u64 nb = offs[qq + 1];
-          kv[0] = keys[qq] ^ flip;
-#pragma unroll
-          for (int r = 1; r < 4; ++r) {
-            while (g + r >= nb) { ++qq; nb = offs[qq + 1]; }
-            kv[r] = keys[qq] ^ flip;
-          }
-          st_v4(ob + e, kv[0], kv[1], kv[2], kv[3]);
-        }
-      }
+    const u64 g0 = gb + e0, glast = gb + e1 - 1;
+    if (!(g0 >= rs && glast < re)) {
+      p = locate(p, g0);
+      rs = offs[p];
+      re = offs[p + 1];
+      rk = keys[p] ^ flip;
     }
+    if (glast < re) {
+#pragma unroll
+      for (int j = 0; j < kEmitVpl; ++j) {
+        const u64 e = e0 + ((u64)j * 32 + lane) * 4;
+        if (e < e1) st_v4(ob + e, rk, rk, rk, rk);
+      }
+      continue;
+    }
+    // fragmented tile: walk its pairs in windows of 32 run boundaries held in
+    // registers; each lane finds its position's pair with a 5-step shuffle
+    // search and the warp writes 32 consecutive keys per store instruction
+    u64 q = p;
+    u64 g = g0;
+    const u64 gend = glast + 1;
+    while (g < gend) {
+      const u64 qi = q + lane;
+      const u64 wb = qi < npairs ? offs[qi + 1] : ~0ull;  // end of pair qi
+      const u64 wk = qi < npairs ? keys[qi] : 0ull;
+      const u64 wtop = __shfl_sync(0xffffffffu, wb, 31);
+      const u64 wend = wtop < gend ? wtop : gend;
+      for (u64 base = g; base < wend; base += 32) {
+        const u64 pos = base + lane;
+        int i = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1) {
+          const u64 b = __shfl_sync(0xffffffffu, wb, i + st - 1);
+          if (b <= pos) i += st;
+        }
+        const u64 k = __shfl_sync(0xffffffffu, wk, i);
+        if (pos < wend) ob[pos - gb] = k ^ flip;
+      }
+      g = wend;
+      if (g < gend) q += 32;
+    }
+    // the last pair touched becomes the cursor for the next tile
+    p = locate(q, glast);
+    rs = offs[p];
+    re = offs[p + 1];
+    rk = keys[p] ^ flip;
   }
 }
 
 void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, u64* out,
-                 u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 npairs_bound) {
+                 u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 /*npairs_bound*/) {
   const u64 L = end > begin ? end - begin : 0;
   const u64 wtiles = (L + kTileKeys - 1) / kTileKeys;
-  u64 grid = (u64)num_sms * 4;
-  const u64 need = (wtiles + (kEmitThreads / 32) - 1) / (kEmitThreads / 32);
-  if (need < grid) grid = need ? need : 1;
-  // npairs_bound: an upper bound of the pair count known on the host (the device
-  // count may be smaller); smem staging when it fits
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    cudaFuncSetAttribute(emit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((kSmemOffs + 1) * 8));
-    attr_dev = dev;
+  static int tpw = -1, idx = -1;  // CAFS_EMIT_TPW / CAFS_EMIT_IDX: tuning knobs
+  if (tpw < 0) {
+    const char* e = getenv("CAFS_EMIT_TPW");
+    tpw = e ? atoi(e) : 2;
+    if (tpw < 1 || tpw > 4096) tpw = 2;
+    e = getenv("CAFS_EMIT_IDX");
+    idx = e ? atoi(e) : kIdxDefault;
+    if (idx < 32 || idx > (int)kIdxEntries) idx = kIdxDefault;
   }
-  if (npairs_bound <= kSmemOffs) {
-    const size_t sm = (size_t)(npairs_bound + 1) * 8;
-    emit_kernel<true><<<(unsigned)grid, kEmitThreads, sm, st>>>(keys, offs, npairs, ctl, out,
-                                                                begin, end, flip);
-  } else {
-    emit_kernel<false><<<(unsigned)grid, kEmitThreads, 0, st>>>(keys, offs, npairs, ctl, out,
-                                                                 begin, end, flip);
-  }
+  const u64 wpb = kEmitThreads / 32;
+  u64 grid = (wtiles + (u64)tpw * wpb - 1) / ((u64)tpw * wpb);
+  if (grid < 1) grid = 1;
+  (void)num_sms;
+  emit_kernel<<<(unsigned)grid, kEmitThreads, ((u64)idx + 1) * 8, st>>>(
+      keys, offs, npairs, ctl, out, begin, end, flip, (u64)tpw, (u64)idx);
 }
 
 }  // namespace cafs

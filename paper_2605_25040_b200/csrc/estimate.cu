@@ -85,8 +85,9 @@ __global__ void __launch_bounds__(1024, 1)
     // per-call state of the later stages
     ctl->scan_inversion = 0;
     ctl->tiny_miss = 0;
-    ctl->g_used = 0;
     ctl->g_updates = 0;
+    ctl->spill_len = 0;
+    ctl->spill_regions = 0;
     ctl->empty_key_count = 0;
     ctl->overflow = 0;
     ctl->need_large = 0;
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(1024, 1)
     ctl->tiny_failed = 0;
   }
   if (tid < 16) ctl->tiny_counts[tid] = 0;
+  if (tid < kListStripes) ctl->g_fill[tid] = 0;
   __syncthreads();
 
   // ---- K0: prefix monotone probe over the reference's first chunk ----

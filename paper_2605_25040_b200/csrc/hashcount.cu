@@ -56,6 +56,7 @@ struct HcArgs {
   u32* glist;
   int use_range;
   int gate;
+  u64* spill;  // HBM spill buffer (queued variant), kSpillCap keys
 };
 
 // key -> global table, keeping the sentinel value out of it
@@ -64,28 +65,56 @@ __device__ __forceinline__ void table_add(const HcArgs& a, u64 key, u64 inc) {
   else global_insert(a.gkeys, a.gcnt, a.glist, a.ctl, key, inc, a.mult);
 }
 
-// Shared-table miss: linear probing with capped claims, else the global table.
-// Returns 1 when the key went to the global table.
-__device__ __noinline__ u32 count_slow(u64 v, u64* skeys, u32* scnt, u32* sclaims,
-                                       const HcArgs& a) {
-  u32 h = mhash(v, a.mult, 64 - kSLog2);
+// Shared-table miss: linear probing with capped claims.  True when resolved.
+__device__ __noinline__ bool probe_smem(u64 v, u64* skeys, u32* scnt, u32* sclaims, u64 mult) {
+  u32 h = mhash(v, mult, 64 - kSLog2);
   for (int p = 0; p < kSMaxProbe; ++p) {
     const u64 k = *((volatile u64*)&skeys[h]);
-    if (k == v) { atomicAdd(&scnt[h], 1u); return 0; }
+    if (k == v) { atomicAdd(&scnt[h], 1u); return true; }
     if (k == kEmpty) {
-      if (*((volatile u32*)sclaims) >= kSClaimCap) break;
+      if (*((volatile u32*)sclaims) >= kSClaimCap) return false;
       const u64 old = atomicCAS(&skeys[h], kEmpty, v);
       if (old == kEmpty) {
         atomicAdd(sclaims, 1u);
         atomicAdd(&scnt[h], 1u);
-        return 0;
+        return true;
       }
-      if (old == v) { atomicAdd(&scnt[h], 1u); return 0; }
+      if (old == v) { atomicAdd(&scnt[h], 1u); return true; }
     }
     h = (h + 1) & (kS - 1);
   }
+  return false;
+}
+
+// Inline slow path (rare misses): shared probe, else the global table.
+__device__ __forceinline__ u32 count_slow(u64 v, u64* skeys, u32* scnt, u32* sclaims,
+                                          const HcArgs& a) {
+  if (probe_smem(v, skeys, scnt, sclaims, a.mult)) return 0;
   global_insert(a.gkeys, a.gcnt, a.glist, a.ctl, v, 1, a.mult);
   return 1;
+}
+
+// Warp-convergent slow path of the queued variant: keys the shared table cannot
+// take are appended to this CTA's region of the HBM spill buffer (a shared
+// cursor, one atomic per warp batch, coalesced stores) -- the reference's spill
+// (buckets.py:273-282) -- and folded into the global table afterwards by
+// spill_fold_kernel with the whole GPU in parallel.  A full region falls back to
+// inline global inserts.
+__device__ __forceinline__ void resolve_or_spill(bool active, u64 v, u64* skeys, u32* scnt,
+                                                 u32* sclaims, u32* sfill, u64* region,
+                                                 u32 region_cap, const HcArgs& a) {
+  const bool miss = active && !probe_smem(v, skeys, scnt, sclaims, a.mult);
+  const u32 m = __ballot_sync(0xffffffffu, miss);
+  if (m == 0) return;
+  const int lane = threadIdx.x & 31;
+  u32 base = 0;
+  if (lane == 0) base = atomicAdd(sfill, (u32)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (miss) {
+    const u32 pos = base + __popc(m & lanemask_lt());
+    if (pos < region_cap) region[pos] = v;
+    else global_insert(a.gkeys, a.gcnt, a.glist, a.ctl, v, 1, a.mult);
+  }
 }
 
 // STAGES x STAGE_KEYS TMA ring fed by a dedicated producer warp (warp 0);
@@ -108,18 +137,22 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   u64* queue = (u64*)(dcnt + kRange);                             // [32][QCAP]
   u64* full = queue + 32 * QCAP;                                  // [STAGES]
   u64* empty = full + STAGES;                                     // [STAGES]
-  __shared__ u32 sclaims;
+  __shared__ u32 sclaims, sfill;
   __shared__ u64 red_empty[32], red_glob[32];
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u64 flip = a.flip, mult = a.mult;
   const u64 base = a.use_range ? a.ctl->range_base : 0ull;
   const u64 rlen = a.use_range ? a.ctl->range_len : 0u;
+  // this CTA's spill region
+  const u32 region_cap = (u32)(kSpillCap / gridDim.x);
+  u64* region = a.spill + (u64)blockIdx.x * region_cap;
 
   for (u32 i = tid; i < kS; i += kHcThreads) { skeys[i] = kEmpty; scnt[i] = 0; }
   for (u32 i = tid; i < kRange; i += kHcThreads) dcnt[i] = 0;
   if (tid == 0) {
     sclaims = 0;
+    sfill = 0;
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers / 32);
@@ -179,7 +212,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
         const u64 u = wq[qn - 32 + lane];
         __syncwarp();
         qn -= 32;
-        glob_cnt += count_slow(u, skeys, scnt, &sclaims, a);
+        resolve_or_spill(true, u, skeys, scnt, &sclaims, &sfill, region, region_cap, a);
       }
     };
     for (u64 it = 0; it < my_chunks; ++it) {
@@ -226,7 +259,8 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
     }
     if (QCAP > 0) {
       __syncwarp();
-      if ((u32)lane < qn) glob_cnt += count_slow(wq[lane], skeys, scnt, &sclaims, a);
+      resolve_or_spill((u32)lane < qn, (u32)lane < qn ? wq[lane] : 0ull, skeys, scnt, &sclaims,
+                       &sfill, region, region_cap, a);
     }
     if (blockIdx.x == 0 && ctid == 0) {
       if (head && n > 0) count1(a.x[0] ^ flip);
@@ -257,29 +291,76 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
     for (int w = 0; w < kHcThreads / 32; ++w) { e += red_empty[w]; gg += red_glob[w]; }
     if (e) atomicAdd(&a.ctl->empty_key_count, e);
     if (gg) atomicAdd(&a.ctl->g_updates, gg);
+    if (QCAP > 0) {
+      const u32 f = sfill < region_cap ? sfill : region_cap;
+      a.ctl->spill_fill[blockIdx.x] = f;
+      atomicAdd(&a.ctl->spill_len, (u64)f);
+      atomicMax(&a.ctl->spill_regions, gridDim.x);
+    }
   }
 }
 
 // Occupied global slots -> dense (key, count) pairs; re-zero the slots so the
-// table is clean for the next call.  The sentinel key's count becomes the last
-// pair.
-__global__ void compact_kernel(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys,
-                               u64* pcnt, int gate) {
+// table is clean for the next call.  Block s compacts claim-list stripe s to
+// the offset of the stripes before it.  The sentinel key's count becomes the
+// last pair.
+__global__ void __launch_bounds__(256) compact_kernel(DevCtl* ctl, u64* gkeys, u64* gcnt,
+                                                      const u32* glist, u64* pkeys, u64* pcnt,
+                                                      int gate) {
   if (ctl->overflow || !gate_open(ctl, gate)) return;
-  const u64 m = ctl->g_used;
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += stride) {
-    const u32 h = glist[i];
-    pkeys[i] = gkeys[h];
-    pcnt[i] = gcnt[h];
+  __shared__ u64 pre_sh, tot_sh;
+  const u32 s = blockIdx.x;
+  if (threadIdx.x < 32) {
+    u64 pre = 0, tot = 0;
+    for (u32 t = threadIdx.x; t < kListStripes; t += 32) {
+      const u64 f = ctl->g_fill[t] < kStripeCap ? ctl->g_fill[t] : kStripeCap;
+      tot += f;
+      if (t < s) pre += f;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      pre += __shfl_xor_sync(0xffffffffu, pre, o);
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    }
+    if (threadIdx.x == 0) { pre_sh = pre; tot_sh = tot; }
+  }
+  __syncthreads();
+  const u64 pre = pre_sh;
+  const u32 m = ctl->g_fill[s] < kStripeCap ? ctl->g_fill[s] : (u32)kStripeCap;
+  const u32* lst = glist + (u64)s * kStripeCap;
+  for (u32 i = threadIdx.x; i < m; i += blockDim.x) {
+    const u32 h = lst[i];
+    pkeys[pre + i] = gkeys[h];
+    pcnt[pre + i] = gcnt[h];
     gkeys[h] = kEmpty;
     gcnt[h] = 0;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (s == 0 && threadIdx.x == 0) {
+    const u64 tot = tot_sh;
     const u64 e = ctl->empty_key_count;
-    if (e) { pkeys[m] = kEmpty; pcnt[m] = e; }
-    ctl->npairs = m + (e ? 1 : 0);
+    if (e) { pkeys[tot] = kEmpty; pcnt[tot] = e; }
+    ctl->npairs = tot + (e ? 1 : 0);
   }
+}
+
+// Fold the spill regions into the global table: block b takes region b (every
+// thread a key: convergent, L2-atomic-throughput bound).
+__global__ void spill_fold_kernel(DevCtl* ctl, const u64* __restrict__ spill, u64* gkeys,
+                                  u64* gcnt, u32* glist, u64 mult, int gate) {
+  if (!gate_open(ctl, gate)) return;
+  const u32 nreg = ctl->spill_regions;
+  if (blockIdx.x >= nreg) return;
+  const u32 cap = (u32)(kSpillCap / nreg);
+  const u64* region = spill + (u64)blockIdx.x * cap;
+  const u32 m = ctl->spill_fill[blockIdx.x];
+  for (u32 i = threadIdx.x; i < m; i += blockDim.x)
+    global_insert(gkeys, gcnt, glist, ctl, region[i], 1, mult);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ctl->g_updates, ctl->spill_len);
+}
+
+void launch_spill_fold(DevCtl* ctl, const u64* spill, u64* gkeys, u64* gcnt, u32* glist, u64 mult,
+                       int num_sms, cudaStream_t st, int gate) {
+  spill_fold_kernel<<<kMaxSpillRegions, 1024, 0, st>>>(ctl, spill, gkeys, gcnt, glist, mult, gate);
 }
 
 // (key, count) pairs -> global table (the merge step of the sharded sort)
@@ -297,9 +378,11 @@ __global__ void insert_pairs_kernel(const u64* __restrict__ keys, const u64* __r
 
 // zero the per-call fields of the control block (estimate_kernel does the same)
 __global__ void reset_ctl_kernel(DevCtl* ctl) {
+  for (u32 t = threadIdx.x; t < kListStripes; t += blockDim.x) ctl->g_fill[t] = 0;
   if (threadIdx.x == 0) {
-    ctl->g_used = 0;
     ctl->g_updates = 0;
+    ctl->spill_len = 0;
+    ctl->spill_regions = 0;
     ctl->empty_key_count = 0;
     ctl->overflow = 0;
     ctl->need_large = 0;
@@ -358,8 +441,8 @@ static int hc_variant() {
 //          1 = queued shape (smaller ring + per-warp miss queues)
 cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms,
-                              cudaStream_t st, int variant, int gate) {
-  HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate};
+                              cudaStream_t st, int variant, int gate, u64* spill) {
+  HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate, spill};
   int v = hc_variant();
   if (v < 0) v = variant == 0 ? 0 : 2;
   switch (v) {
@@ -373,7 +456,7 @@ cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* c
 
 void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys, u64* pcnt,
                     int num_sms, cudaStream_t st, int gate) {
-  compact_kernel<<<num_sms, 256, 0, st>>>(ctl, gkeys, gcnt, glist, pkeys, pcnt, gate);
+  compact_kernel<<<kListStripes, 256, 0, st>>>(ctl, gkeys, gcnt, glist, pkeys, pcnt, gate);
 }
 
 }  // namespace cafs

@@ -21,7 +21,9 @@ void launch_tiny_finalize(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,
 size_t hash_count_smem();
 cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms, cudaStream_t st,
-                              int variant, int gate);
+                              int variant, int gate, u64* spill);
+void launch_spill_fold(DevCtl* ctl, const u64* spill, u64* gkeys, u64* gcnt, u32* glist, u64 mult,
+                       int num_sms, cudaStream_t st, int gate);
 void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevCtl* ctl,
                          u64* gkeys, u64* gcnt, u32* glist, int num_sms, cudaStream_t st);
 void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys, u64* pcnt,
