@@ -55,6 +55,7 @@ struct cafs_ctx {
   size_t tile_state_words = 0;
   u64* tmp = nullptr;
   size_t tmp_elems = 0;
+  void* msd = nullptr;  // MSD bucket-sort state
   u64* stage = nullptr;  // host-path device staging buffer
   size_t stage_elems = 0;
   u32 epoch = 0;
@@ -154,6 +155,7 @@ int ensure_radix(cafs_ctx_t* ctx, u64 n, bool need_tmp) {
     CK(cudaMemset(ctx->tile_state, 0, w * 8));  // epoch 0 is never used
     ctx->tile_state_words = w;
   }
+  if (!ctx->msd) CK(cudaMalloc(&ctx->msd, msd_state_bytes()));
   if (need_tmp && n > ctx->tmp_elems) {
     if (ctx->tmp) CK(cudaFree(ctx->tmp));
     ctx->tmp = nullptr;
@@ -200,6 +202,50 @@ int radix_sort(cafs_ctx_t* ctx, u64* keys, u64* vals, u64* kalt, u64* valt, u64 
   return CAFS_OK;
 }
 
+int try_msd(cafs_ctx_t* ctx, const u64* keys, const u64* vals, u64 n, u64 flip, u64* tk, u64* tv,
+            u64* dk, u64* dv, cudaStream_t st, bool* done);
+
+// More than kSmallSortMax pairs: (pk_a, pc_a) -> (pk_b, pc_b) sorted by key.
+// MSD buckets when they fit (pk_b/pc_b double as the bucket buffers, the result
+// is copied back), else LSD onesweep.
+int sort_pairs_large(cafs_ctx_t* ctx, u64 np, cudaStream_t st) {
+  TRY(ensure_radix(ctx, np, false));
+  bool done;
+  TRY(try_msd(ctx, ctx->pk_a, ctx->pc_a, np, 0, ctx->pk_b, ctx->pc_b, ctx->pk_a, ctx->pc_a, st,
+              &done));
+  if (done) {
+    CK(cudaMemcpyAsync(ctx->pk_b, ctx->pk_a, np * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(ctx->pc_b, ctx->pc_a, np * 8, cudaMemcpyDeviceToDevice, st));
+    return CAFS_OK;
+  }
+  u64 *rk, *rv;
+  TRY(radix_sort(ctx, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, np, 0, st, &rk, &rv));
+  if (rk != ctx->pk_b) {
+    CK(cudaMemcpyAsync(ctx->pk_b, rk, np * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(ctx->pc_b, rv, np * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  return CAFS_OK;
+}
+
+// MSD bucket sort (msd.cu) when every bucket fits a CTA; returns false (nothing
+// written) when some bucket is too large, leaving the LSD path to the caller.
+int try_msd(cafs_ctx_t* ctx, const u64* keys, const u64* vals, u64 n, u64 flip, u64* tk, u64* tv,
+            u64* dk, u64* dv, cudaStream_t st, bool* done) {
+  *done = false;
+  launch_msd_count(keys, n, flip, ctx->msd, ctx->num_sms, st);
+  ctx->launches += 3;
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_scratch, (char*)ctx->msd + msd_maxb_offset(), sizeof(u32),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if ((u32)ctx->h_scratch[0] > msd_bucket_cap()) return CAFS_OK;
+  launch_msd_sort(keys, vals, n, flip, ctx->msd, tk, tv, dk, dv, st);
+  ctx->launches += 2;
+  CKL();
+  *done = true;
+  return CAFS_OK;
+}
+
 // fallback_sort (sorter.py:132-138) on device, in place
 int fallback_sort(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cudaStream_t st) {
   if (n < 2) return CAFS_OK;
@@ -210,6 +256,9 @@ int fallback_sort(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cudaStream_t st) {
     return CAFS_OK;
   }
   TRY(ensure_radix(ctx, n, true));
+  bool done;
+  TRY(try_msd(ctx, x, nullptr, n, flip, ctx->tmp, nullptr, x, nullptr, st, &done));
+  if (done) return CAFS_OK;
   u64 *rk, *rv;
   TRY(radix_sort(ctx, x, nullptr, ctx->tmp, nullptr, n, flip, st, &rk, &rv));
   if (rk != x) CK(cudaMemcpyAsync(x, rk, n * 8, cudaMemcpyDeviceToDevice, st));
@@ -376,13 +425,7 @@ int main_finish(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cafs_telemetry_t* tel,
   if (c.need_large) {
     const u64 np = c.npairs;
     int ts = tm.begin();
-    TRY(ensure_radix(ctx, np, false));
-    u64 *rk, *rv;
-    TRY(radix_sort(ctx, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, np, 0, st, &rk, &rv));
-    if (rk != ctx->pk_b) {
-      CK(cudaMemcpyAsync(ctx->pk_b, rk, np * 8, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(ctx->pc_b, rv, np * 8, cudaMemcpyDeviceToDevice, st));
-    }
+    TRY(sort_pairs_large(ctx, np, st));
     launch_scan(ctx->pc_b, np, ctx->bsum, ctx->poffs, ctx->d_ctl, n, st);
     ctx->launches += 3;
     CKL();
@@ -469,7 +512,7 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
   cudaDeviceSynchronize();
   void* dev[] = {ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
                  ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->spill, ctx->ghist, ctx->gbase,
-                 ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage};
+                 ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage, ctx->msd};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -715,15 +758,7 @@ int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
     return fail(ctx, CAFS_EINVAL, "more distinct keys than the global table holds");
   }
   const u64 np = c.npairs;
-  if (c.need_large) {
-    TRY(ensure_radix(ctx, np, false));
-    u64 *rk, *rv;
-    TRY(radix_sort(ctx, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, np, 0, st, &rk, &rv));
-    if (rk != ctx->pk_b) {
-      CK(cudaMemcpyAsync(ctx->pk_b, rk, np * 8, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(ctx->pc_b, rv, np * 8, cudaMemcpyDeviceToDevice, st));
-    }
-  }
+  if (c.need_large) TRY(sort_pairs_large(ctx, np, st));
   *h_npairs = np;
   if (np > cap) return fail(ctx, CAFS_EINVAL, "output capacity too small");
   CK(cudaMemcpyAsync(d_keys, ctx->pk_b, np * 8, cudaMemcpyDeviceToDevice, st));
@@ -757,15 +792,7 @@ int cafs_merge_pairs(cafs_ctx_t* ctx, const uint64_t* d_keys_in, const uint64_t*
     return fail(ctx, CAFS_EINVAL, "more distinct keys than the global table holds");
   }
   const u64 np = c.npairs;
-  if (c.need_large) {
-    TRY(ensure_radix(ctx, np, false));
-    u64 *rk, *rv;
-    TRY(radix_sort(ctx, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, np, 0, st, &rk, &rv));
-    if (rk != ctx->pk_b) {
-      CK(cudaMemcpyAsync(ctx->pk_b, rk, np * 8, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(ctx->pc_b, rv, np * 8, cudaMemcpyDeviceToDevice, st));
-    }
-  }
+  if (c.need_large) TRY(sort_pairs_large(ctx, np, st));
   *h_npairs = np;
   if (np > cap) return fail(ctx, CAFS_EINVAL, "output capacity too small");
   CK(cudaMemcpyAsync(d_keys, ctx->pk_b, np * 8, cudaMemcpyDeviceToDevice, st));

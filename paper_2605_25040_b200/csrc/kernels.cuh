@@ -47,6 +47,13 @@ cudaError_t launch_small_sort_pairs(u64* keys, const u64* cnt, u64 n, DevCtl* ct
                                     int gate);
 void launch_scan(const u64* in, u64 n, u64* bsum, u64* out_offs, DevCtl* ctl, u64 expect,
                  cudaStream_t st);
+// msd.cu
+size_t msd_state_bytes();
+u32 msd_bucket_cap();
+size_t msd_maxb_offset();
+void launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st);
+void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* state, u64* tk,
+                     u64* tv, u64* dk, u64* dv, cudaStream_t st);
 // gen.cu
 void launch_gen_mix(u64* out, u64 count, u64 seed, u64 skip, int num_sms, cudaStream_t st);
 void launch_gen_draw(u64* out, u64 n, u64 start, u64 seed, const u64* palette, u64 k,

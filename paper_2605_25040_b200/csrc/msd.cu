@@ -1,0 +1,366 @@
+// msd.cu -- MSD bucket sort: the fallback engine and the large pair sort.
+//
+// Replaces fallback_sort (sorter.py:132-138) and, for more than 8192 pairs,
+// radix_sort_pairs (_kernels.py:185-214).  An LSD radix sort of 64-bit keys
+// moves 16 B/key per digit pass (8 passes for random keys); here one pass
+// partitions the keys by the 12 most significant VARYING bits (found from an
+// OR/AND reduction, so dictionary codes and clustered keys still spread), and
+// each of the 4096 buckets is then sorted entirely in shared memory by a
+// 256-thread CTA (stable 8-ballot multisplit LSD over the bytes that vary
+// inside the bucket).  DRAM traffic: 8 (reduce) + 8 (histogram) + 16 (scatter)
+// + 16 (bucket sort) = 48 B/key.  Buckets larger than kBucketCap (skewed keys,
+// or n ~ 2^30) are left to the onesweep LSD path (radix.cu) by the host.
+#include <cstddef>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cafs {
+
+constexpr int kMsdBits = 12;
+constexpr u32 kMsdBuckets = 1u << kMsdBits;
+constexpr int kBsThreads = 256;
+constexpr int kBsWarps = kBsThreads / 32;
+constexpr u32 kBucketCap = 4096;                       // keys per bucket sorted in smem
+constexpr int kBsRounds = kBucketCap / kBsThreads;     // 16 rounds of 32 per warp
+constexpr int kScThreads = 256;
+constexpr int kScItems = 16;                           // keys per thread in the scatter
+constexpr u64 kScChunk = (u64)kScThreads * kScItems;   // 4096
+
+struct MsdState {
+  unsigned long long vor, vand;
+  u32 hist[kMsdBuckets];
+  u32 base[kMsdBuckets + 1];
+  u32 cursor[kMsdBuckets];
+  u32 maxb;
+  int shift;
+};
+
+__device__ __forceinline__ u32 msd_digit(u64 k, int shift) {
+  return (u32)(k >> shift) & (kMsdBuckets - 1);
+}
+
+__global__ void __launch_bounds__(512) msd_reduce_kernel(const u64* __restrict__ keys, u64 n,
+                                                         u64 flip, MsdState* ms) {
+  u64 vor = 0, vand = ~0ull;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u64 k = keys[i] ^ flip;
+    vor |= k;
+    vand &= k;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    vor |= __shfl_xor_sync(0xffffffffu, vor, o);
+    vand &= __shfl_xor_sync(0xffffffffu, vand, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(&ms->vor, vor);
+    atomicAnd(&ms->vand, vand);
+  }
+}
+
+// shift so the bucket digit covers the 12 highest bits that vary
+__device__ __forceinline__ int msd_shift(const MsdState* ms) {
+  const u64 vary = ms->vor ^ ms->vand;
+  if (vary == 0) return 0;
+  const int hb = 63 - __clzll(vary);
+  return hb + 1 > kMsdBits ? hb + 1 - kMsdBits : 0;
+}
+
+__global__ void __launch_bounds__(512) msd_hist_kernel(const u64* __restrict__ keys, u64 n,
+                                                       u64 flip, MsdState* ms) {
+  __shared__ u32 h[kMsdBuckets];
+  for (u32 i = threadIdx.x; i < kMsdBuckets; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int shift = msd_shift(ms);
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += stride)
+    atomicAdd(&h[msd_digit(keys[i] ^ flip, shift)], 1u);
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < kMsdBuckets; i += blockDim.x)
+    if (h[i]) atomicAdd(&ms->hist[i], h[i]);
+}
+
+__global__ void __launch_bounds__(1024) msd_scan_kernel(MsdState* ms) {
+  __shared__ u32 ws[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int IT = kMsdBuckets / 1024;
+  u32 c[IT], local = 0, mx = 0;
+#pragma unroll
+  for (int q = 0; q < IT; ++q) {
+    c[q] = ms->hist[tid * IT + q];
+    local += c[q];
+    mx = c[q] > mx ? c[q] : mx;
+  }
+  u32 incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const u32 t = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = t > mx ? t : mx;
+  }
+  if (lane == 31) ws[wid] = incl;
+  if (lane == 0) atomicMax(&ms->maxb, mx);
+  __syncthreads();
+  if (wid == 0) {
+    u32 w = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    ws[lane] = w;
+  }
+  __syncthreads();
+  u32 run = incl - local + (wid ? ws[wid - 1] : 0);
+#pragma unroll
+  for (int q = 0; q < IT; ++q) {
+    ms->base[tid * IT + q] = run;
+    ms->cursor[tid * IT + q] = run;
+    run += c[q];
+  }
+  if (tid == 1023) ms->base[kMsdBuckets] = run;
+  if (tid == 0) ms->shift = msd_shift(ms);
+}
+
+// Scatter a 4096-key chunk into its buckets: local counts (shared atomics give
+// each key its rank), one global reservation per non-empty bucket, then the
+// writes.  Order inside a bucket is not preserved: keys are sorted afterwards
+// and pair keys are distinct, so stability is not needed.
+template <bool HAS_VAL>
+__global__ void __launch_bounds__(kScThreads)
+    msd_scatter_kernel(const u64* __restrict__ keys, const u64* __restrict__ vals, u64 n, u64 flip,
+                       MsdState* ms, u64* __restrict__ tk, u64* __restrict__ tv) {
+  __shared__ u32 h[kMsdBuckets];
+  __shared__ u32 g[kMsdBuckets];
+  for (u32 i = threadIdx.x; i < kMsdBuckets; i += kScThreads) h[i] = 0;
+  __syncthreads();
+  const int shift = ms->shift;
+  const u64 c0 = (u64)blockIdx.x * kScChunk;
+  u64 k[kScItems];
+  u32 r[kScItems];
+#pragma unroll
+  for (int j = 0; j < kScItems; ++j) {
+    const u64 i = c0 + threadIdx.x + (u64)j * kScThreads;
+    k[j] = i < n ? keys[i] ^ flip : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kScItems; ++j) {
+    const u64 i = c0 + threadIdx.x + (u64)j * kScThreads;
+    if (i < n) r[j] = atomicAdd(&h[msd_digit(k[j], shift)], 1u);
+  }
+  __syncthreads();
+  for (u32 b = threadIdx.x; b < kMsdBuckets; b += kScThreads)
+    if (h[b]) g[b] = atomicAdd(&ms->cursor[b], h[b]);
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kScItems; ++j) {
+    const u64 i = c0 + threadIdx.x + (u64)j * kScThreads;
+    if (i < n) {
+      const u32 pos = g[msd_digit(k[j], shift)] + r[j];
+      tk[pos] = k[j];
+      if (HAS_VAL) tv[pos] = vals[i];
+    }
+  }
+}
+
+// One CTA per bucket: load it into shared memory, LSD radix over the bytes that
+// vary inside the bucket (stable 8-ballot multisplit, warp-contiguous
+// segments), write it back sorted (un-flipping the keys; pairs carry their
+// value through a 16-bit index).
+template <bool HAS_VAL>
+__global__ void __launch_bounds__(kBsThreads)
+    bucket_sort_kernel(const u64* __restrict__ tk, const u64* __restrict__ tv,
+                       const MsdState* ms, u64 flip, u64* __restrict__ dk, u64* __restrict__ dv) {
+  extern __shared__ __align__(16) unsigned char bs_smem[];
+  u64 (*kb)[kBucketCap] = (u64 (*)[kBucketCap])bs_smem;                                // [2]
+  unsigned short (*ib)[kBucketCap] =
+      (unsigned short (*)[kBucketCap])(bs_smem + 2 * kBucketCap * 8);                 // [2]
+  u32 (*wcnt)[256] = (u32 (*)[256])(bs_smem + 2 * kBucketCap * 8 + 2 * kBucketCap * 2);  // [warps]
+  __shared__ u32 dstart[256];
+  __shared__ u32 wsum8[8];
+  __shared__ u64 red_or[kBsWarps], red_and[kBsWarps];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u32 b = blockIdx.x;
+  const u32 base = ms->base[b];
+  const u32 n = ms->base[b + 1] - base;
+  if (n == 0) return;
+  if (n == 1) {
+    if (tid == 0) {
+      dk[base] = tk[base] ^ flip;
+      if (HAS_VAL) dv[base] = tv[base];
+    }
+    return;
+  }
+  u64 vor = 0, vand = ~0ull;
+  {  // all loads in flight before any use (one DRAM round trip, not n/256)
+    u64 lk[kBsRounds];
+#pragma unroll
+    for (int j = 0; j < kBsRounds; ++j) {
+      const u32 i = tid + j * kBsThreads;
+      lk[j] = i < n ? tk[base + i] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kBsRounds; ++j) {
+      const u32 i = tid + j * kBsThreads;
+      if (i < n) {
+        kb[0][i] = lk[j];
+        ib[0][i] = (unsigned short)i;
+        vor |= lk[j];
+        vand &= lk[j];
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    vor |= __shfl_xor_sync(0xffffffffu, vor, o);
+    vand &= __shfl_xor_sync(0xffffffffu, vand, o);
+  }
+  if (lane == 0) { red_or[wid] = vor; red_and[wid] = vand; }
+  __syncthreads();
+  vor = 0; vand = ~0ull;
+  for (int w = 0; w < kBsWarps; ++w) { vor |= red_or[w]; vand &= red_and[w]; }
+  const u64 vary = vor ^ vand;
+  // warp-contiguous segments of whole rounds
+  const u32 rounds = ((n + 31) / 32 + kBsWarps - 1) / kBsWarps;  // rounds per warp
+  const u32 w0 = wid * rounds * 32;
+  int cur = 0;
+  for (int p = 0; p < 8; ++p) {
+    if (((vary >> (8 * p)) & 0xFF) == 0) continue;
+    const int shift = 8 * p;
+    const u64* src = kb[cur];
+    u64* dst = kb[cur ^ 1];
+    const unsigned short* isrc = ib[cur];
+    unsigned short* idst = ib[cur ^ 1];
+    u32* my = wcnt[wid];
+    for (int i = lane; i < 256; i += 32) my[i] = 0;
+    __syncwarp();
+    u32 rank[kBsRounds];
+    u32 dig[kBsRounds];
+#pragma unroll
+    for (int r = 0; r < kBsRounds; ++r) {
+      if ((u32)r >= rounds) break;
+      const u32 idx = w0 + r * 32 + lane;
+      const bool valid = idx < n;
+      const u32 d = valid ? (u32)(src[idx] >> shift) & 255u : 0u;
+      u32 peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+      for (int bb = 0; bb < 8; ++bb) {
+        const u32 bal = __ballot_sync(0xffffffffu, (d >> bb) & 1u);
+        peers &= ((d >> bb) & 1u) ? bal : ~bal;
+      }
+      u32 before = 0;
+      if (valid) before = my[d];
+      __syncwarp();
+      if (valid) {
+        rank[r] = before + __popc(peers & lanemask_lt());
+        if (lane == 31 - __clz(peers)) my[d] = before + __popc(peers);
+      }
+      dig[r] = d;
+      __syncwarp();
+    }
+    __syncthreads();
+    {  // per digit: exclusive prefix over warps, then over digits (256 threads)
+      u32 acc = 0;
+#pragma unroll
+      for (int w = 0; w < kBsWarps; ++w) {
+        const u32 c = wcnt[w][tid];
+        wcnt[w][tid] = acc;
+        acc += c;
+      }
+      u32 incl = acc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) wsum8[wid] = incl;
+      __syncthreads();
+      u32 pre = 0;
+      for (int w = 0; w < wid; ++w) pre += wsum8[w];
+      dstart[tid] = pre + incl - acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kBsRounds; ++r) {
+      if ((u32)r >= rounds) break;
+      const u32 idx = w0 + r * 32 + lane;
+      if (idx < n) {
+        const u32 pos = dstart[dig[r]] + wcnt[wid][dig[r]] + rank[r];
+        dst[pos] = src[idx];
+        idst[pos] = isrc[idx];
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  if (HAS_VAL) {
+    u64 lv[kBsRounds];
+#pragma unroll
+    for (int j = 0; j < kBsRounds; ++j) {
+      const u32 i = tid + j * kBsThreads;
+      lv[j] = i < n ? tv[base + ib[cur][i]] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kBsRounds; ++j) {
+      const u32 i = tid + j * kBsThreads;
+      if (i < n) dv[base + i] = lv[j];
+    }
+  }
+  for (u32 i = tid; i < n; i += kBsThreads) dk[base + i] = kb[cur][i] ^ flip;
+}
+
+// ---------------- host side ----------------
+size_t msd_state_bytes() { return sizeof(MsdState); }
+u32 msd_bucket_cap() { return kBucketCap; }
+
+void launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st) {
+  MsdState* ms = (MsdState*)state;
+  cudaMemsetAsync(ms, 0, sizeof(MsdState), st);
+  cudaMemsetAsync(&ms->vand, 0xFF, sizeof(u64), st);
+  u64 blocks = (n + 512 * 8 - 1) / (512 * 8);
+  if (blocks > (u64)num_sms * 4) blocks = (u64)num_sms * 4;
+  if (blocks < 1) blocks = 1;
+  msd_reduce_kernel<<<(unsigned)blocks, 512, 0, st>>>(keys, n, flip, ms);
+  msd_hist_kernel<<<(unsigned)blocks, 512, 0, st>>>(keys, n, flip, ms);
+  msd_scan_kernel<<<1, 1024, 0, st>>>(ms);
+}
+
+u32 msd_read_max(const void* state_host_copy) { return ((const MsdState*)state_host_copy)->maxb; }
+size_t msd_maxb_offset() { return offsetof(MsdState, maxb); }
+
+// keys (and vals) -> tmp (bucketed) -> dk/dv sorted; dk may equal keys
+constexpr size_t kBsSmem = (size_t)kBucketCap * (16 + 4) + (size_t)kBsWarps * 256 * 4;
+
+void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* state, u64* tk,
+                     u64* tv, u64* dk, u64* dv, cudaStream_t st) {
+  MsdState* ms = (MsdState*)state;
+  const u64 chunks = (n + kScChunk - 1) / kScChunk;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(bucket_sort_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBsSmem);
+    cudaFuncSetAttribute(bucket_sort_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBsSmem);
+    attr_dev = dev;
+  }
+  if (vals) {
+    msd_scatter_kernel<true><<<(unsigned)chunks, kScThreads, 0, st>>>(keys, vals, n, flip, ms, tk,
+                                                                      tv);
+    bucket_sort_kernel<true><<<kMsdBuckets, kBsThreads, kBsSmem, st>>>(tk, tv, ms, flip, dk, dv);
+  } else {
+    msd_scatter_kernel<false><<<(unsigned)chunks, kScThreads, 0, st>>>(keys, nullptr, n, flip, ms,
+                                                                       tk, nullptr);
+    bucket_sort_kernel<false><<<kMsdBuckets, kBsThreads, kBsSmem, st>>>(tk, nullptr, ms, flip, dk,
+                                                                         nullptr);
+  }
+}
+
+}  // namespace cafs

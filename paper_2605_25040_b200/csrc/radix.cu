@@ -157,15 +157,29 @@ __global__ void __launch_bounds__(kOsThreads)
     for (int w = 0; w < wid; ++w) pre += wsum[w];
     dstart[tid] = pre + lane_incl - acc;
     // decoupled look-back over the preceding tiles' digit counts
+    // windowed: the states of 8 predecessors are loaded in one round trip and
+    // consumed nearest-first until an inclusive prefix is found; an unpublished
+    // state stops the window and is polled again
     u32 excl = 0;
     if (tile > 0) {
       int t = (int)tile - 1;
-      while (true) {
-        const u64 s = *((volatile u64*)(tile_state + (u64)t * 256 + tid));
-        if ((u32)(s >> 34) != epoch) continue;  // not yet published in this pass
-        excl += (u32)s;
-        if (((s >> 32) & 3) == kFlagIncl) break;
-        --t;
+      bool done = false;
+      while (!done) {
+        u64 stw[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+          stw[w] = t - w >= 0 ? *((volatile u64*)(tile_state + (u64)(t - w) * 256 + tid)) : 0ull;
+        int used = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          if (done || used != w) break;
+          const u64 sv = stw[w];
+          if ((u32)(sv >> 34) != epoch) break;  // not yet published in this pass
+          excl += (u32)sv;
+          used = w + 1;
+          if (((sv >> 32) & 3) == kFlagIncl) done = true;
+        }
+        t -= used;
       }
       *((volatile u64*)(tile_state + (u64)tile * 256 + tid)) =
           pack_state(epoch, kFlagIncl, excl + acc);
@@ -226,12 +240,23 @@ __global__ void __launch_bounds__(1024, 1)
     }
   }
   u64 vor = 0, vand = ~0ull;
-  for (u32 i = tid; i < n; i += 1024) {
-    const u64 k = keys_io[i] ^ flip;
-    kb[i] = k;
-    ib[i] = (unsigned short)i;
-    vor |= k;
-    vand &= k;
+  {  // all loads in flight before any use (one round trip, not n/1024)
+    u64 lk[kSmallSortMax / 1024];
+#pragma unroll
+    for (int j = 0; j < (int)(kSmallSortMax / 1024); ++j) {
+      const u32 i = tid + j * 1024;
+      lk[j] = i < n ? keys_io[i] ^ flip : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < (int)(kSmallSortMax / 1024); ++j) {
+      const u32 i = tid + j * 1024;
+      if (i < n) {
+        kb[i] = lk[j];
+        ib[i] = (unsigned short)i;
+        vor |= lk[j];
+        vand &= lk[j];
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
