@@ -98,6 +98,12 @@ typedef struct {
   float stage_ms[3];
   float kernel_ms[4];            /* count kernel (hash or tiny), emit kernel, estimate kernel */
   uint32_t kernels_launched;     /* kernels this call put on the stream */
+  /* CAFS_FLAG_EXACT_TELEMETRY: the reference bucket table's statistics
+   * (buckets.py:152-169, sorter.py:326-331), computed exactly on device */
+  int32_t exact;                 /* 1 when the ref_* fields are valid */
+  int32_t ref_guard_fired;       /* 2 * ref_spill_len > n (sorter.py:264) */
+  uint64_t ref_spill_len, ref_updates, ref_hits, ref_claims, ref_spill_pushes;
+  uint64_t ref_counted_total;
 } cafs_telemetry_t;
 
 typedef struct cafs_ctx cafs_ctx_t;
@@ -113,6 +119,9 @@ const char* cafs_last_error(cafs_ctx_t* ctx);
 /* Flags for cafs_sort_i64 */
 #define CAFS_FLAG_TIMING 1u      /* fill stage_ms with CUDA-event timings */
 #define CAFS_FLAG_NO_DIRECT 2u   /* disable the dense-range direct-count path */
+#define CAFS_FLAG_EXACT_TELEMETRY 4u  /* compute the reference's bucket-table statistics */
+#define CAFS_FLAG_DOM_I32 8u     /* keys are widened int32 (reference domain: u32, cap 8) */
+#define CAFS_FLAG_DOM_U32 16u    /* keys are widened uint32 */
 
 /* cafs_sort(x) in place on device memory (sorter.py:335-386).  n < 2^32. */
 int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed,

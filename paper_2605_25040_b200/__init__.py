@@ -20,6 +20,7 @@ from .sorter import (
     PairList,
     Route,
     SortTelemetry,
+    TableSummary,
     cafs_sort,
     chao1,
     check_hash_mult,
@@ -38,7 +39,7 @@ from .sorter import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "CardinalityEstimate", "DispatchDecision", "PairList", "Route", "SortTelemetry",
+    "CardinalityEstimate", "DispatchDecision", "PairList", "Route", "SortTelemetry", "TableSummary",
     "cafs_sort", "chao1", "check_hash_mult", "dispatch", "emit", "fallback_sort", "fast_hash",
     "is_monotone", "pair_sort", "sample_and_estimate", "table_size_for", "tiny_count_sort",
     "tiny_counts", "FREQSET_SLOTS", "HASH_MULT", "PAIR_RADIX_MIN", "SAMPLE_TARGET",

@@ -22,6 +22,9 @@ TINY_MAX = 8
 OK, EINVAL, ECUDA, ENOMEM, ESUM, EINTERNAL = 0, -1, -2, -3, -4, -5
 FLAG_TIMING = 1
 FLAG_NO_DIRECT = 2
+FLAG_EXACT_TELEMETRY = 4
+FLAG_DOM_I32 = 8
+FLAG_DOM_U32 = 16
 
 
 class Estimate(ctypes.Structure):
@@ -40,7 +43,11 @@ class Telemetry(ctypes.Structure):
                 ("counted_total", ctypes.c_uint64), ("pairs", ctypes.c_uint64),
                 ("table_buckets", ctypes.c_uint64), ("global_updates", ctypes.c_uint64),
                 ("stage_ms", ctypes.c_float * 3), ("kernel_ms", ctypes.c_float * 4),
-                ("kernels_launched", ctypes.c_uint32)]
+                ("kernels_launched", ctypes.c_uint32), ("exact", ctypes.c_int32),
+                ("ref_guard_fired", ctypes.c_int32), ("ref_spill_len", ctypes.c_uint64),
+                ("ref_updates", ctypes.c_uint64), ("ref_hits", ctypes.c_uint64),
+                ("ref_claims", ctypes.c_uint64), ("ref_spill_pushes", ctypes.c_uint64),
+                ("ref_counted_total", ctypes.c_uint64)]
 
 
 # every symbol include/cafs_b200.h declares, with its ctypes signature

@@ -56,6 +56,14 @@ struct cafs_ctx {
   u64* tmp = nullptr;
   size_t tmp_elems = 0;
   void* msd = nullptr;  // MSD bucket-sort state
+  // exact-telemetry scratch (telemetry.cu), allocated on first use
+  u64* tl_keys = nullptr;
+  u32* tl_idx = nullptr;
+  u32* tl_first = nullptr;
+  u32* tl_runs = nullptr;
+  u64* tl_comp = nullptr;   // [4][kPairCap]: comp, cidx, comp2, cidx2
+  u64* tl_offs = nullptr;
+  void* tl_acc = nullptr;
   u64* stage = nullptr;  // host-path device staging buffer
   size_t stage_elems = 0;
   u32 epoch = 0;
@@ -362,7 +370,7 @@ int run_dispatch(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, cudaStream_t st
 // estimate kernel and exits unless its route is active, so the host needs no
 // round trip between the dispatch and the emit.
 int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
-                 StageTimer& tm, cudaStream_t st) {
+                 StageTimer& tm, cudaStream_t st, bool with_emit = true) {
   TRY(ensure_main(ctx));
   DevCtl* c = ctx->d_ctl;
   int ts = tm.begin(), tk = tm.begin();
@@ -396,13 +404,79 @@ int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t fl
                               kGateMain);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   tm.end(ts, L_STAGE_SORT_K, C_MAIN);
-  ts = tm.begin();
-  tk = tm.begin();
-  launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, kSmallSortMax);
-  tm.end(tk, L_K_EMIT, C_EMIT);
-  tm.end(ts, L_STAGE_EMIT, C_EMIT);
-  ctx->launches += direct ? 8 : 7;
+  if (with_emit) {
+    ts = tm.begin();
+    tk = tm.begin();
+    launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, kSmallSortMax);
+    tm.end(tk, L_K_EMIT, C_EMIT);
+    tm.end(ts, L_STAGE_EMIT, C_EMIT);
+    ctx->launches++;
+  }
+  ctx->launches += direct ? 7 : 6;
   CKL();
+  return CAFS_OK;
+}
+
+// Reference-exact bucket-table statistics (telemetry.cu), from the compacted
+// pairs (pk_a, pc_a) and the still-unsorted input x.
+int exact_telemetry(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, u64 mult, double k_hat,
+                    uint32_t flags, cafs_telemetry_t* tel, cudaStream_t st) {
+  const DevCtl c = *ctx->h_ctl;
+  const u64 np = c.npairs;
+  if (!ctx->tl_keys) {
+    CK(cudaMalloc(&ctx->tl_keys, (kPairCap * 2) * 8));
+    CK(cudaMalloc(&ctx->tl_idx, (kPairCap * 2) * 4));
+    CK(cudaMalloc(&ctx->tl_first, kPairCap * 4));
+    CK(cudaMalloc(&ctx->tl_runs, kPairCap * 4));
+    CK(cudaMalloc(&ctx->tl_comp, 4 * kPairCap * 8));
+    CK(cudaMalloc(&ctx->tl_offs, (kPairCap + 1) * 8));
+    CK(cudaMalloc(&ctx->tl_acc, tel_accum_bytes()));
+  }
+  TRY(ensure_radix(ctx, np, false));
+  int log2s = 10;
+  while ((1ull << log2s) < 2 * np) ++log2s;
+  CK(cudaMemsetAsync(ctx->tl_acc, 0, tel_accum_bytes(), st));
+  launch_tel_build(ctx->pk_a, np, ctx->tl_keys, ctx->tl_idx, log2s, ctx->tl_first, ctx->tl_runs,
+                   ctx->num_sms, st);
+  const u64 empty_idx = c.empty_key_count ? np - 1 : ~0ull;
+  launch_tel_runs(x, n, flip, ctx->tl_keys, ctx->tl_idx, log2s, empty_idx, ctx->tl_first,
+                  ctx->tl_runs, ctx->tl_acc, ctx->num_sms, st);
+  const bool dom32 = flags & (CAFS_FLAG_DOM_I32 | CAFS_FLAG_DOM_U32);
+  const int cap = dom32 ? 8 : 4;
+  const u64 M = table_size_for(k_hat > 1.0 ? k_hat : 1.0, n, cap);
+  const int m_log2 = 63 - __builtin_clzll(M);
+  const int dom = (flags & CAFS_FLAG_DOM_I32) ? 1 : (flags & CAFS_FLAG_DOM_U32) ? 2 : 0;
+  u64 *comp = ctx->tl_comp, *cidx = comp + kPairCap, *comp2 = cidx + kPairCap,
+      *cidx2 = comp2 + kPairCap;
+  launch_tel_comp(ctx->pk_a, np, ctx->tl_first, mult, m_log2, dom, comp, cidx, ctx->num_sms, st);
+  ctx->launches += 3;
+  u64 *sk = comp, *sv = cidx;
+  if (np <= kSmallSortMax) {
+    cudaError_t e = launch_small_sort_pairs(comp, cidx, np, nullptr, 0, comp2, cidx2, ctx->tl_offs,
+                                            st, kGateNone);
+    if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "telemetry sort", e);
+    sk = comp2;
+    sv = cidx2;
+  } else {
+    bool done;
+    TRY(try_msd(ctx, comp, cidx, np, 0, comp2, cidx2, comp, cidx, st, &done));
+    if (!done) TRY(radix_sort(ctx, comp, cidx, comp2, cidx2, np, 0, st, &sk, &sv));
+  }
+  launch_tel_classify(sk, sv, np, cap, ctx->pc_a, ctx->tl_runs, ctx->tl_acc, ctx->num_sms, st);
+  ctx->launches += 2;
+  CKL();
+  unsigned long long acc[5];
+  CK(cudaMemcpyAsync(acc, ctx->tl_acc, sizeof(acc), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // TelAccum: runs, spill_len, spill_pushes, claims, stored_runs
+  tel->exact = 1;
+  tel->ref_updates = acc[0];
+  tel->ref_spill_len = acc[1];
+  tel->ref_spill_pushes = acc[2];
+  tel->ref_claims = acc[3];
+  tel->ref_hits = acc[4] - acc[3];
+  tel->ref_counted_total = n - acc[1];
+  tel->ref_guard_fired = acc[1] * 2 > n;
   return CAFS_OK;
 }
 
@@ -512,7 +586,9 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
   cudaDeviceSynchronize();
   void* dev[] = {ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
                  ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->spill, ctx->ghist, ctx->gbase,
-                 ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage, ctx->msd};
+                 ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage, ctx->msd,
+                 ctx->tl_keys, ctx->tl_idx, ctx->tl_first, ctx->tl_runs, ctx->tl_comp,
+                 ctx->tl_offs, ctx->tl_acc};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -551,7 +627,8 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
   ctx->launches++;
   CKL();
   const int mark = tm.n;
-  TRY(launch_fused(ctx, x, n, flip, hash_mult, flags, tm, st));
+  const bool exact = want_tel && (flags & CAFS_FLAG_EXACT_TELEMETRY);
+  TRY(launch_fused(ctx, x, n, flip, hash_mult, flags, tm, st, !exact));
   TRY(sync_ctl(ctx, st));
   int eff = ctx->h_ctl->eff_route;
   bool mono = eff == CAFS_ALREADY_SORTED;
@@ -569,8 +646,30 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
       ctx->h_scratch[0] = eff;
       CK(cudaMemcpyAsync(&ctx->d_ctl->eff_route, ctx->h_scratch, sizeof(int32_t),
                          cudaMemcpyHostToDevice, st));
-      TRY(launch_fused(ctx, x, n, flip, hash_mult, flags, tm, st));
+      TRY(launch_fused(ctx, x, n, flip, hash_mult, flags, tm, st, !exact));
       TRY(sync_ctl(ctx, st));
+    }
+  }
+  if (exact) {
+    // the reference's table statistics need the unsorted input: compute them
+    // now, then run the emit the fused pipeline left out
+    const DevCtl& cc = *ctx->h_ctl;
+    const bool main_ran_ = eff == CAFS_MAIN || (eff == CAFS_TINY_COUNT && cc.tiny_failed);
+    if (main_ran_ && !cc.overflow)
+      TRY(exact_telemetry(ctx, x, n, flip, hash_mult, cc.k_hat, flags, tel, st));
+    if ((eff == CAFS_MAIN || eff == CAFS_TINY_COUNT) && cc.pairs_ready) {
+      const int ts = tm.begin();
+      launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st,
+                  kSmallSortMax);
+      tm.end(ts, L_STAGE_EMIT, C_EMIT);
+      ctx->launches++;
+      CKL();
+    }
+    if (main_ran_ && cc.overflow) {
+      // the device guard sorts with the fallback; the reference statistics
+      // still follow from the pairs the count saw -- not available, so report
+      // them as not exact
+      tel->exact = 0;
     }
   }
   const DevCtl c = *ctx->h_ctl;
@@ -610,6 +709,11 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
   if (rc != CAFS_OK) return rc;
   CK(cudaStreamSynchronize(st));
   tm.finish(tiny_ran, main_ran, emitted);
+  if (exact && !main_ran) {
+    // no bucket table in the reference either: all statistics are zero
+    tel->exact = 1;
+    tel->ref_counted_total = tel->counted_total;
+  }
   tel->kernels_launched = ctx->launches;
   return CAFS_OK;
 }

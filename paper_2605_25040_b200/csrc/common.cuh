@@ -28,9 +28,10 @@ constexpr u64 kGlobalCap = kGlobalSlots / 2;          // max distinct keys befor
 constexpr int kGlobalMaxProbe = 128;
 constexpr u64 kSpillCap = 1ull << 25;                 // HBM spill buffer (keys); excess goes inline
 constexpr u32 kMaxSpillRegions = 256;                 // >= count-kernel grid (one CTA per SM)
-// The claim list of the global table is striped: a claim from CTA b appends to
-// stripe b % kListStripes, so claims from all SMs do not serialise on one
-// counter.  A full stripe is a table overflow (the guard).
+// The claim list of the global table is striped: a claim from warp w of CTA b
+// appends to stripe (32 b + w) % kListStripes, so claims from all SMs do not
+// serialise on one counter and the stripes fill evenly.  A full stripe is a
+// table overflow (the guard).
 constexpr u32 kListStripes = 128;
 constexpr u64 kStripeCap = kGlobalCap / kListStripes;
 
@@ -165,15 +166,18 @@ __device__ __forceinline__ u32 lanemask_lt() {
 
 // Insert (key, inc) into the global open-addressing table (linear probing).
 // Claims append the slot to `list` so compaction touches only occupied slots.
+// The slot comes from a full 64-bit mixer, not from the reference's
+// multiplicative hash: inputs built to collide under that hash (the
+// acceptance-c06 guard input, cafs/selftest.py:191-207) must not cluster here.
 __device__ __forceinline__ void global_insert(u64* gkeys, u64* gcnt, u32* list, DevCtl* ctl,
-                                              u64 key, u64 inc, u64 mult) {
-  u32 h = mhash(key, mult, 64 - kGlobalLog2);
+                                              u64 key, u64 inc, u64 /*mult*/) {
+  u32 h = (u32)(fmix64(key) >> (64 - kGlobalLog2));
   for (int p = 0; p < kGlobalMaxProbe; ++p) {
     u64 k = *((volatile u64*)&gkeys[h]);
     if (k == kEmpty) {
       u64 old = atomicCAS(&gkeys[h], kEmpty, key);
       if (old == kEmpty) {
-        const u32 stripe = blockIdx.x & (kListStripes - 1);
+        const u32 stripe = (blockIdx.x * 32u + (threadIdx.x >> 5)) & (kListStripes - 1);
         const u32 idx = atomicAdd(&ctl->g_fill[stripe], 1u);
         if (idx < kStripeCap) list[stripe * kStripeCap + idx] = h;
         else ctl->overflow = 1;

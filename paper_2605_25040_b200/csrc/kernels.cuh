@@ -54,6 +54,17 @@ size_t msd_maxb_offset();
 void launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st);
 void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* state, u64* tk,
                      u64* tv, u64* dk, u64* dv, cudaStream_t st);
+// telemetry.cu
+size_t tel_accum_bytes();
+void launch_tel_build(const u64* keys, u64 np, u64* tkeys, u32* tidx, int log2s, u32* first,
+                      u32* runs, int num_sms, cudaStream_t st);
+void launch_tel_runs(const u64* x, u64 n, u64 flip, const u64* tkeys, const u32* tidx, int log2s,
+                     u64 empty_idx, u32* first, u32* runs, void* acc, int num_sms,
+                     cudaStream_t st);
+void launch_tel_comp(const u64* keys, u64 np, const u32* first, u64 mult, int m_log2, int dom,
+                     u64* comp, u64* cidx, int num_sms, cudaStream_t st);
+void launch_tel_classify(const u64* comp, const u64* cidx, u64 np, int cap, const u64* counts,
+                         const u32* runs, void* acc, int num_sms, cudaStream_t st);
 // gen.cu
 void launch_gen_mix(u64* out, u64 count, u64 seed, u64 skip, int num_sms, cudaStream_t st);
 void launch_gen_draw(u64* out, u64 n, u64 start, u64 seed, const u64* palette, u64 k,

@@ -68,16 +68,32 @@ class DispatchDecision:  # sorter.py:52-57
     estimate: CardinalityEstimate | None = None
 
 
+@dataclass(frozen=True)
+class TableSummary:
+    """The reference BucketTable's shape and statistics (buckets.py:152-192),
+    computed exactly on device when ``exact_telemetry=True``."""
+
+    n_buckets: int
+    cap: int
+    hits: int
+    claims: int
+    spill_pushes: int
+    spill_len: int
+
+
 @dataclass
 class SortTelemetry:  # sorter.py:60-81
     """Read-only view of one cafs_sort invocation.
 
     ``stage_ms`` keys follow the reference's count / sort_k / emit labels and
-    are CUDA-event times.  ``spill_len`` / ``updates`` describe the reference's
-    bucket table, which the device pipeline does not build; they stay 0 (see
-    DESIGN.md, "Telemetry").  ``pairs`` (distinct keys), ``global_updates``
-    (elements resolved in the L2 global table), ``table_buckets`` (the
-    reference's table size M) and ``kernels_launched`` are device extras.
+    are CUDA-event times.  ``spill_len``, ``updates``, ``guard_fired``,
+    ``counted_total`` and ``table`` describe the reference's bucket table, which
+    the device pipeline does not build: with ``cafs_sort(...,
+    exact_telemetry=True)`` they are computed exactly on device (telemetry.cu);
+    otherwise spill_len/updates stay 0 and guard_fired reports the device guard.
+    ``device_guard_fired`` (global-table overflow), ``pairs`` (distinct keys),
+    ``global_updates``, ``table_buckets`` (the reference's table size M) and
+    ``kernels_launched`` are device extras.
     """
 
     n: int = 0
@@ -94,6 +110,8 @@ class SortTelemetry:  # sorter.py:60-81
     table_buckets: int = 0
     kernels_launched: int = 0
     kernel_ms: dict[str, float] = field(default_factory=dict)
+    device_guard_fired: bool = False
+    exact: bool = False
 
     @property
     def route(self) -> Route | None:
@@ -294,6 +312,7 @@ def _fill_telemetry(tel: SortTelemetry, t: _lib.Telemetry, kind: str, timing: bo
     tel.n = int(t.n)
     tel.decision = _decision_from_c(t.decision, tel.n, kind)
     tel.guard_fired = bool(t.guard_fired)
+    tel.device_guard_fired = bool(t.guard_fired)
     tel.tiny_count_failed = bool(t.tiny_count_failed)
     tel.counted_total = int(t.counted_total)
     tel.pairs = int(t.pairs)
@@ -303,6 +322,15 @@ def _fill_telemetry(tel: SortTelemetry, t: _lib.Telemetry, kind: str, timing: bo
     route = tel.decision.route
     if route is Route.MAIN and tel.decision.estimate is not None:
         tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, cap)
+    tel.exact = bool(t.exact)
+    if t.exact:
+        tel.spill_len = int(t.ref_spill_len)
+        tel.updates = int(t.ref_updates)
+        tel.guard_fired = bool(t.ref_guard_fired)
+        tel.counted_total = int(t.ref_counted_total)
+        if route is Route.MAIN:
+            tel.table = TableSummary(tel.table_buckets, cap, int(t.ref_hits), int(t.ref_claims),
+                                     int(t.ref_spill_pushes), int(t.ref_spill_len))
     if timing:
         tel.stage_ms = _stage_dict(t)
         tel.kernel_ms = {name: float(t.kernel_ms[i])
@@ -316,7 +344,7 @@ def _fill_telemetry(tel: SortTelemetry, t: _lib.Telemetry, kind: str, timing: bo
 # ---------------- the API ----------------
 
 def cafs_sort(x, telemetry: SortTelemetry | None = None, hash_mult=None, *,
-              direct_range: bool = True) -> None:
+              direct_range: bool = True, exact_telemetry: bool = False) -> None:
     """Sort a 1-D integer array ascending, in place (sorter.py:335-386).
 
     ``x`` is a torch CUDA tensor (sorted on its device and current stream) or a
@@ -330,6 +358,10 @@ def cafs_sort(x, telemetry: SortTelemetry | None = None, hash_mult=None, *,
     if telemetry is None:
         telemetry = SortTelemetry()
     flags = (_lib.FLAG_TIMING if want else 0) | (0 if direct_range else _lib.FLAG_NO_DIRECT)
+    if want and exact_telemetry:
+        flags |= _lib.FLAG_EXACT_TELEMETRY
+        kind0 = _kind(x)[0]
+        flags |= {"int32": _lib.FLAG_DOM_I32, "uint32": _lib.FLAG_DOM_U32}.get(kind0, 0)
     t = _lib.Telemetry()
     lib = _lib.load()
     if _is_tensor(x) and x.is_cuda:

@@ -50,13 +50,27 @@ def check_decision(tel: SortTelemetry, rec: dict):
         assert tel.table_buckets == rec["table_buckets"]
 
 
-def run_case(x: np.ndarray, rec: dict, mult=None):
+def check_exact(tel: SortTelemetry, rec: dict):
+    """The reference's bucket-table telemetry, computed on device."""
+    assert tel.exact
+    assert (tel.spill_len, tel.guard_fired, tel.updates) == (
+        rec["spill_len"], rec["guard_fired"], rec["updates"])
+    if "table_buckets" in rec:
+        assert tel.counted_total == rec["counted_total"]
+        t = tel.table
+        assert (t.n_buckets, t.hits, t.claims, t.spill_pushes) == (
+            rec["table_buckets"], rec["hits"], rec["claims"], rec["spill_pushes"])
+
+
+def run_case(x: np.ndarray, rec: dict, mult=None, exact=True):
     t = to_dev(x)
     tel = SortTelemetry()
-    cafs.cafs_sort(t, telemetry=tel, hash_mult=mult)
+    cafs.cafs_sort(t, telemetry=tel, hash_mult=mult, exact_telemetry=exact)
     torch.cuda.synchronize()
     assert sha(t) == rec["sha256"], "sorted bytes differ from the reference"
     check_decision(tel, rec)
+    if exact:
+        check_exact(tel, rec)
     if x.shape[0] > 1:
         d = cafs.dispatch(to_dev(x), hash_mult=mult)
         assert d.route.value == rec["dispatch_route"]
@@ -78,8 +92,9 @@ def test_special_cases(rec):
 def test_reference_sweep():
     cases = load_json("sweep_cases.json")
     routes = set()
-    for rec in cases:
-        tel = run_case(sweep_input(rec), rec)
+    for i, rec in enumerate(cases):
+        # alternate: the fused fast path, and the exact-telemetry path
+        tel = run_case(sweep_input(rec), rec, exact=bool(i % 2))
         routes.add(tel.route)
     assert routes == set(Route)
 
@@ -88,8 +103,7 @@ def test_reference_sweep():
 def test_baseline_config(name):
     rec = {r["name"]: r for r in load_json("config_cases.json")}[name]
     x = ogen.CONFIGS[name].generate()
-    tel = run_case(x, rec)
-    assert tel.counted_total in (0, x.shape[0])
+    run_case(x, rec)
 
 
 def _device_config(name, n=None, start=0):
