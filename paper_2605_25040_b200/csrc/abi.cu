@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -71,6 +72,20 @@ struct cafs_ctx {
   cudaEvent_t ev[32] = {};
   std::string last_error;
   uint32_t launches = 0;
+  // CUDA Graphs of the fused pipeline (estimate + gated route kernels), keyed by
+  // the call's arguments; captured on the second call with the same key
+  cudaStream_t cap_stream = nullptr;
+  struct GraphEntry {
+    u64 x = 0, n = 0, flip = 0, mult = 0;
+    uint32_t flags = 0;
+    int timing = 0;
+    int seen = 0;
+    cudaGraphExec_t exec = nullptr;
+    int tn = 0, mark = 0, label[16] = {}, cond[16] = {};
+    uint32_t launches = 0;
+    uint64_t stamp = 0;
+  } graphs[16];
+  uint64_t graph_clock = 0;
 };
 
 namespace {
@@ -311,14 +326,19 @@ struct StageTimer {
   int n = 0;
   int label[kMaxTimed] = {};
   int cond[kMaxTimed] = {};
+  bool capturing = false;  // inside stream capture: record external event nodes
+  void rec(cudaEvent_t e) {
+    if (capturing) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else cudaEventRecord(e, st);
+  }
   int begin() {
     if (!on || n >= kMaxTimed) return -1;
-    cudaEventRecord(ctx->ev[2 * n], st);
+    rec(ctx->ev[2 * n]);
     return n++;
   }
   void end(int i, int lab, int c = C_ALWAYS) {
     if (i < 0) return;
-    cudaEventRecord(ctx->ev[2 * i + 1], st);
+    rec(ctx->ev[2 * i + 1]);
     label[i] = lab;
     cond[i] = c;
   }
@@ -520,6 +540,87 @@ int main_finish(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cafs_telemetry_t* tel,
   return CAFS_OK;
 }
 
+void pipeline_direct(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
+                     StageTimer& tm, cudaStream_t st, bool exact, int* mark, int* rc) {
+  const int te = tm.begin();
+  launch_estimate(x, n, flip, 1, ctx->d_ctl, st);
+  tm.end(te, L_K_EST);
+  ctx->launches++;
+  *mark = tm.n;
+  *rc = launch_fused(ctx, x, n, flip, mult, flags, tm, st, !exact);
+}
+
+// The estimate + fused kernels, replayed from a cached CUDA Graph when the same
+// (buffer, n, flags) was sorted before: one graph launch instead of ~9 kernel
+// launches (the small-input latency).  The graph's kernels are the same; only
+// the launch path differs.
+int launch_pipeline(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
+                    StageTimer& tm, cudaStream_t st, bool exact, int* mark) {
+  static int use_graphs = -1;
+  if (use_graphs < 0) {
+    const char* e = getenv("CAFS_GRAPHS");
+    use_graphs = e ? atoi(e) != 0 : 1;
+  }
+  int rc = CAFS_OK;
+  if (!use_graphs || !ctx->cap_stream) {
+    pipeline_direct(ctx, x, n, flip, mult, flags, tm, st, exact, mark, &rc);
+    CKL();
+    return rc;
+  }
+  const int timing = tm.on ? 1 : 0;
+  cafs_ctx_t::GraphEntry* hit = nullptr;
+  cafs_ctx_t::GraphEntry* lru = &ctx->graphs[0];
+  for (auto& g : ctx->graphs) {
+    if (g.seen && g.x == (u64)x && g.n == n && g.flip == flip && g.mult == mult &&
+        g.flags == flags && g.timing == timing) {
+      hit = &g;
+      break;
+    }
+    if (g.stamp < lru->stamp) lru = &g;
+  }
+  if (hit && hit->exec) {
+    CK(cudaGraphLaunch(hit->exec, st));
+    tm.n = hit->tn;
+    for (int i = 0; i < hit->tn; ++i) { tm.label[i] = hit->label[i]; tm.cond[i] = hit->cond[i]; }
+    *mark = hit->mark;
+    ctx->launches += hit->launches;
+    hit->stamp = ++ctx->graph_clock;
+    return CAFS_OK;
+  }
+  if (!hit) {  // first sighting: run directly, capture next time
+    if (lru->exec) cudaGraphExecDestroy(lru->exec);
+    *lru = cafs_ctx_t::GraphEntry();
+    lru->x = (u64)x; lru->n = n; lru->flip = flip; lru->mult = mult; lru->flags = flags;
+    lru->timing = timing; lru->seen = 1; lru->stamp = ++ctx->graph_clock;
+    pipeline_direct(ctx, x, n, flip, mult, flags, tm, st, exact, mark, &rc);
+    CKL();
+    return rc;
+  }
+  // second sighting: capture on the context's stream, then launch on the caller's
+  const uint32_t l0 = ctx->launches;
+  StageTimer ct = tm;
+  ct.st = ctx->cap_stream;
+  ct.capturing = true;
+  cudaGraph_t graph = nullptr;
+  CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+  pipeline_direct(ctx, x, n, flip, mult, flags, ct, ctx->cap_stream, exact, mark, &rc);
+  cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &graph);
+  if (rc != CAFS_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "graph capture", e);
+  e = cudaGraphInstantiate(&hit->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) { hit->exec = nullptr; return fail(ctx, CAFS_ECUDA, "graph instantiate", e); }
+  hit->tn = ct.n;
+  hit->mark = *mark;
+  for (int i = 0; i < ct.n; ++i) { hit->label[i] = ct.label[i]; hit->cond[i] = ct.cond[i]; }
+  hit->launches = ctx->launches - l0;
+  hit->stamp = ++ctx->graph_clock;
+  CK(cudaGraphLaunch(hit->exec, st));
+  tm.n = ct.n;
+  for (int i = 0; i < ct.n; ++i) { tm.label[i] = ct.label[i]; tm.cond[i] = ct.cond[i]; }
+  return CAFS_OK;
+}
+
 int check_common(cafs_ctx_t* ctx, const void* p, u64 n) {
   if (!ctx) return CAFS_EINVAL;
   if (n >= (1ull << 32)) return fail(ctx, CAFS_EINVAL, "arrays of 2**32 or more elements");
@@ -576,6 +677,7 @@ int cafs_ctx_create(int device, cafs_ctx_t** out) {
     return CAFS_ENOMEM;
   }
   for (int i = 0; i < 32; ++i) cudaEventCreate(&ctx->ev[i]);
+  cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking);
   *out = ctx;
   return CAFS_OK;
 }
@@ -596,6 +698,9 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
   if (ctx->h_trivial) cudaFreeHost(ctx->h_trivial);
   for (int i = 0; i < 32; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  for (auto& g : ctx->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   delete ctx;
 }
 
@@ -621,14 +726,10 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
   u64* x = (u64*)d_x;
   const u64 flip = is_signed ? kSign : 0;
   // K0/K1 then every route's kernels, gated on the device decision; one sync
-  const int te = tm.begin();
-  launch_estimate(x, n, flip, 1, ctx->d_ctl, st);
-  tm.end(te, L_K_EST);
-  ctx->launches++;
-  CKL();
-  const int mark = tm.n;
   const bool exact = want_tel && (flags & CAFS_FLAG_EXACT_TELEMETRY);
-  TRY(launch_fused(ctx, x, n, flip, hash_mult, flags, tm, st, !exact));
+  TRY(ensure_main(ctx));
+  int mark = 0;
+  TRY(launch_pipeline(ctx, x, n, flip, hash_mult, flags, tm, st, exact, &mark));
   TRY(sync_ctl(ctx, st));
   int eff = ctx->h_ctl->eff_route;
   bool mono = eff == CAFS_ALREADY_SORTED;

@@ -5,7 +5,8 @@
 
 namespace cafs {
 
-constexpr u32 kSmallSortMax = 8192;  // single-CTA bitonic sort capacity (keys or pairs)
+constexpr u32 kSmallSortMax = 8192;  // single-CTA sort capacity (keys or pairs)
+constexpr u32 kBitonicMax = 2048;    // below this a bitonic network replaces the radix passes
 
 // estimate.cu
 void launch_estimate(const u64* x, u64 n, u64 flip, int check_prefix, DevCtl* ctl,

@@ -269,11 +269,39 @@ __global__ void __launch_bounds__(1024, 1)
   for (int w = 0; w < 32; ++w) { vor |= red_or[w]; vand &= red_and[w]; }
   const u64 vary = vor ^ vand;  // bits that differ between some keys
 
+  int cur = 0;
+  int nvary = 0;
+  for (int p = 0; p < 8; ++p) nvary += ((vary >> (8 * p)) & 0xFF) != 0;
+  if (n <= kBitonicMax && nvary > 2) {
+    // few keys, many varying bytes: one bitonic network (log2(P)(log2(P)+1)/2
+    // barrier steps) beats up to 8 radix passes of fixed cost each
+    u32 P = 2;
+    while (P < n) P <<= 1;
+    for (u32 i = n + tid; i < P; i += 1024) { kb[i] = kEmpty; ib[i] = 0xFFFF; }
+    __syncthreads();
+    for (u32 k = 2; k <= P; k <<= 1) {
+      for (u32 j = k >> 1; j > 0; j >>= 1) {
+        for (u32 i = tid; i < P; i += 1024) {
+          const u32 q = i ^ j;
+          if (q > i) {
+            const u64 a = kb[i], b = kb[q];
+            const u32 ia = ib[i], iq = ib[q];
+            const bool gt = a > b || (a == b && ia > iq);  // (key, index) order: stable
+            if (gt == ((i & k) == 0)) {
+              kb[i] = b; kb[q] = a;
+              ib[i] = (unsigned short)iq; ib[q] = (unsigned short)ia;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    nvary = 0;  // sorted: skip the radix passes
+  }
   // each warp owns a contiguous, 32-aligned segment of at most 8 rounds
   const u32 seg = (u32)(((n + 31) / 32 + 31) / 32) * 32;  // items per warp (multiple of 32)
   const u32 w0 = wid * seg;
-  int cur = 0;
-  for (int p = 0; p < 8; ++p) {
+  for (int p = 0; p < 8 && nvary > 0; ++p) {
     if (((vary >> (8 * p)) & 0xFF) == 0) continue;
     const int shift = 8 * p;
     u64* src = kb + cur * kSmallSortMax;
@@ -286,6 +314,7 @@ __global__ void __launch_bounds__(1024, 1)
     u32 rank[8], dig[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
+      if ((u32)(r * 32) >= seg) break;  // uniform across the block
       const u32 idx = w0 + r * 32 + lane;
       const bool valid = (u32)(r * 32) < seg && idx < n;
       const u32 d = valid ? (u32)(src[idx] >> shift) & 255u : 0u;
@@ -331,8 +360,9 @@ __global__ void __launch_bounds__(1024, 1)
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
+      if ((u32)(r * 32) >= seg) break;
       const u32 idx = w0 + r * 32 + lane;
-      if ((u32)(r * 32) < seg && idx < n) {
+      if (idx < n) {
         const u32 pos = dstart[dig[r]] + wcnt[wid * 256 + dig[r]] + rank[r];
         dst[pos] = src[idx];
         idst[pos] = isrc[idx];
