@@ -157,7 +157,10 @@ class DeviceOps:
 
 
 class Comm:
-    """The few collectives the sharded sort needs, over torch.distributed."""
+    """The few collectives the sharded sort needs, over torch.distributed.
+
+    With NCCL the collective buffers live on the GPU; with gloo (CPU tests, or
+    several ranks sharing one GPU) they are staged through host memory."""
 
     def __init__(self, group=None, device=None):
         import torch.distributed as dist
@@ -165,7 +168,8 @@ class Comm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        self.device = device  # tensors for the collective live here (cuda for NCCL)
+        host_only = dist.get_backend(group) == "gloo"
+        self.device = None if host_only else device  # where collective buffers live
 
     def _t(self, a, dtype=None):
         torch = _torch()
@@ -189,11 +193,12 @@ class Comm:
         torch = _torch()
         sizes = [s[0] for s in self.all_gather_ints([int(t.shape[0])])]
         m = max(sizes) if sizes else 0
-        pad = torch.zeros(m, dtype=t.dtype, device=t.device)
-        pad[:t.shape[0]] = t
+        dev = t.device if self.device is not None or not t.is_cuda else torch.device("cpu")
+        pad = torch.zeros(m, dtype=t.dtype, device=dev)
+        pad[:t.shape[0]] = t.to(dev)
         out = [torch.empty_like(pad) for _ in range(self.world)]
         self.dist.all_gather(out, pad, group=self.group)
-        return torch.cat([o[:s] for o, s in zip(out, sizes)])
+        return torch.cat([o[:s] for o, s in zip(out, sizes)]).to(t.device)
 
 
 def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTelemetry | None = None,
