@@ -46,6 +46,7 @@ struct cafs_ctx {
   u64* poffs = nullptr;  // exclusive offsets, npairs + 1
   u64* bsum = nullptr;
   u64* spill = nullptr;  // kSpillCap keys
+  u64* dense = nullptr;  // dense-window counts (zero between calls)
   // radix sort scratch
   u32* ghist = nullptr;  // [8][256]
   u32* gbase = nullptr;  // [8][256]
@@ -90,7 +91,8 @@ struct cafs_ctx {
 
 namespace {
 
-constexpr u64 kPairCap = kGlobalCap + 1;
+// hash-table pairs + the ~0 sentinel pair + dense-window pairs appended after them
+constexpr u64 kPairCap = kGlobalCap + 1 + 8192;
 
 int fail(cafs_ctx_t* c, int code, const char* what, cudaError_t e = cudaSuccess) {
   if (c) {
@@ -158,6 +160,8 @@ int ensure_main(cafs_ctx_t* ctx) {
   CK(cudaMalloc(&ctx->poffs, (kPairCap + 1) * 8));
   CK(cudaMalloc(&ctx->bsum, (kPairCap / 8192 + 2) * 8));
   CK(cudaMalloc(&ctx->spill, kSpillCap * 8));
+  CK(cudaMalloc(&ctx->dense, dense_window_len() * 8));
+  CK(cudaMemset(ctx->dense, 0, dense_window_len() * 8));
   return CAFS_OK;
 }
 
@@ -404,13 +408,13 @@ int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t fl
   cudaError_t e;
   if (direct) {
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                          ctx->num_sms, st, 0, kGateMainDense, ctx->spill);
+                          ctx->num_sms, st, 0, kGateMainDense, ctx->spill, ctx->dense);
     if (e == cudaSuccess)
       e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                            ctx->num_sms, st, 1, kGateMainHash, ctx->spill);
+                            ctx->num_sms, st, 1, kGateMainHash, ctx->spill, ctx->dense);
   } else {
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 0,
-                          ctx->num_sms, st, 1, kGateMain, ctx->spill);
+                          ctx->num_sms, st, 1, kGateMain, ctx->spill, ctx->dense);
   }
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
   tm.end(tk, L_K_COUNT, C_MAIN);
@@ -418,6 +422,9 @@ int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t fl
                     kGateMain);
   launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
                  kGateMain);
+  if (direct)
+    launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs, n, st,
+                       kGateMainDense);
   tm.end(ts, L_STAGE_COUNT, C_MAIN);
   ts = tm.begin();
   e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st,
@@ -432,7 +439,7 @@ int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t fl
     tm.end(ts, L_STAGE_EMIT, C_EMIT);
     ctx->launches++;
   }
-  ctx->launches += direct ? 7 : 6;
+  ctx->launches += direct ? 8 : 6;
   CKL();
   return CAFS_OK;
 }
@@ -456,11 +463,14 @@ int exact_telemetry(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, u64 mult, do
   int log2s = 10;
   while ((1ull << log2s) < 2 * np) ++log2s;
   CK(cudaMemsetAsync(ctx->tl_acc, 0, tel_accum_bytes(), st));
-  launch_tel_build(ctx->pk_a, np, ctx->tl_keys, ctx->tl_idx, log2s, ctx->tl_first, ctx->tl_runs,
-                   ctx->num_sms, st);
-  const u64 empty_idx = c.empty_key_count ? np - 1 : ~0ull;
-  launch_tel_runs(x, n, flip, ctx->tl_keys, ctx->tl_idx, log2s, empty_idx, ctx->tl_first,
-                  ctx->tl_runs, ctx->tl_acc, ctx->num_sms, st);
+  // all np pairs: sorted in pk_b when the pair sort (or the dense path)
+  // finished, else the compacted list in pk_a
+  const u64* pk = c.pairs_ready ? ctx->pk_b : ctx->pk_a;
+  const u64* pc = c.pairs_ready ? ctx->pc_b : ctx->pc_a;
+  launch_tel_build(pk, np, ctx->tl_keys, ctx->tl_idx, log2s, ctx->tl_first, ctx->tl_runs,
+                   ctx->tl_acc, ctx->num_sms, st);
+  launch_tel_runs(x, n, flip, ctx->tl_keys, ctx->tl_idx, log2s, ctx->tl_first, ctx->tl_runs,
+                  ctx->tl_acc, ctx->num_sms, st);
   const bool dom32 = flags & (CAFS_FLAG_DOM_I32 | CAFS_FLAG_DOM_U32);
   const int cap = dom32 ? 8 : 4;
   const u64 M = table_size_for(k_hat > 1.0 ? k_hat : 1.0, n, cap);
@@ -468,7 +478,7 @@ int exact_telemetry(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, u64 mult, do
   const int dom = (flags & CAFS_FLAG_DOM_I32) ? 1 : (flags & CAFS_FLAG_DOM_U32) ? 2 : 0;
   u64 *comp = ctx->tl_comp, *cidx = comp + kPairCap, *comp2 = cidx + kPairCap,
       *cidx2 = comp2 + kPairCap;
-  launch_tel_comp(ctx->pk_a, np, ctx->tl_first, mult, m_log2, dom, comp, cidx, ctx->num_sms, st);
+  launch_tel_comp(pk, np, ctx->tl_first, mult, m_log2, dom, comp, cidx, ctx->num_sms, st);
   ctx->launches += 3;
   u64 *sk = comp, *sv = cidx;
   if (np <= kSmallSortMax) {
@@ -482,10 +492,10 @@ int exact_telemetry(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, u64 mult, do
     TRY(try_msd(ctx, comp, cidx, np, 0, comp2, cidx2, comp, cidx, st, &done));
     if (!done) TRY(radix_sort(ctx, comp, cidx, comp2, cidx2, np, 0, st, &sk, &sv));
   }
-  launch_tel_classify(sk, sv, np, cap, ctx->pc_a, ctx->tl_runs, ctx->tl_acc, ctx->num_sms, st);
+  launch_tel_classify(sk, sv, np, cap, pc, ctx->tl_runs, ctx->tl_acc, ctx->num_sms, st);
   ctx->launches += 2;
   CKL();
-  unsigned long long acc[5];
+  unsigned long long acc[6];
   CK(cudaMemcpyAsync(acc, ctx->tl_acc, sizeof(acc), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   // TelAccum: runs, spill_len, spill_pushes, claims, stored_runs
@@ -687,7 +697,7 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
   DeviceGuard g(ctx->device);
   cudaDeviceSynchronize();
   void* dev[] = {ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
-                 ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->spill, ctx->ghist, ctx->gbase,
+                 ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->spill, ctx->dense, ctx->ghist, ctx->gbase,
                  ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage, ctx->msd,
                  ctx->tl_keys, ctx->tl_idx, ctx->tl_first, ctx->tl_runs, ctx->tl_comp,
                  ctx->tl_offs, ctx->tl_acc};
@@ -945,12 +955,14 @@ int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   launch_estimate((const u64*)d_x, n, is_signed ? kSign : 0, 0, ctx->d_ctl, st);
   cudaError_t e = launch_hash_count((const u64*)d_x, n, is_signed ? kSign : 0, hash_mult,
                                     ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                                    ctx->num_sms, st, 1, kGateNone, ctx->spill);
+                                    ctx->num_sms, st, 1, kGateNone, ctx->spill, ctx->dense);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
   launch_spill_fold(ctx->d_ctl, ctx->spill, ctx->gkeys, ctx->gcnt, ctx->glist, hash_mult,
                     ctx->num_sms, st, kGateNone);
   launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
                  ctx->num_sms, st, kGateNone);
+  launch_dense_pairs(ctx->d_ctl, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b,
+                     ctx->poffs, n, st, kGateNone);
   e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, n, ctx->pk_b, ctx->pc_b,
                               ctx->poffs, st, kGateNone);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);

@@ -56,7 +56,8 @@ struct HcArgs {
   u32* glist;
   int use_range;
   int gate;
-  u64* spill;  // HBM spill buffer (queued variant), kSpillCap keys
+  u64* spill;   // HBM spill buffer (queued variant), kSpillCap keys
+  u64* dense;   // global dense-window counts [kRange] (zero on entry)
 };
 
 // key -> global table, keeping the sentinel value out of it
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   // ---- flush the CTA's shared cells into the global table ----
   for (u32 d = tid; d < (u32)rlen; d += kHcThreads) {
     const u32 c = dcnt[d];
-    if (c) table_add(a, base + d, c);
+    if (c) atomicAdd(&a.dense[d], (u64)c);  // key base + d: no hashing, no claims
   }
   for (u32 h = tid; h < kS; h += kHcThreads) {
     const u32 c = scnt[h];
@@ -363,6 +364,101 @@ void launch_spill_fold(DevCtl* ctl, const u64* spill, u64* gkeys, u64* gcnt, u32
   spill_fold_kernel<<<kMaxSpillRegions, 1024, 0, st>>>(ctl, spill, gkeys, gcnt, glist, mult, gate);
 }
 
+// Dense-window counts -> (key, count) pairs in key order (the window is a key
+// range), re-zeroing the array.  When nothing else was counted (no hash-table
+// pairs), these ARE the sorted pairs: offsets are written and the pair sort is
+// skipped; otherwise they are appended to the compacted pairs for the sort.
+__global__ void __launch_bounds__(1024) dense_pairs_kernel(DevCtl* ctl, u64* dense, u64* pkeys,
+                                                           u64* pcnt, u64* skeys, u64* scnt,
+                                                           u64* soffs, u64 n_expect, int gate) {
+  if (!gate_open(ctl, gate)) return;  // the count kernel was gated off too: dense untouched
+  if (ctl->overflow) {  // guard: the fallback sorts; leave the window zeroed for the next call
+    for (u32 d = threadIdx.x; d < ctl->range_len; d += blockDim.x) dense[d] = 0;
+    return;
+  }
+  __shared__ u32 wsum[32];
+  __shared__ unsigned long long csum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u64 base = ctl->range_base;
+  const u32 rlen = ctl->range_len;
+  constexpr int IT = kRange / 1024;
+  u64 c[IT];
+  u32 nz = 0;
+  u64 local = 0;
+#pragma unroll
+  for (int q = 0; q < IT; ++q) {
+    const u32 d = tid * IT + q;
+    c[q] = d < rlen ? dense[d] : 0;
+    nz += c[q] != 0;
+    local += c[q];
+  }
+  // exclusive scans of the non-zero flags (output slot) and counts (offsets)
+  u32 inz = nz;
+  u64 icnt = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 t = __shfl_up_sync(0xffffffffu, inz, o);
+    const u64 t2 = __shfl_up_sync(0xffffffffu, icnt, o);
+    if (lane >= o) { inz += t; icnt += t2; }
+  }
+  if (lane == 31) { wsum[wid] = inz; csum[wid] = icnt; }
+  __syncthreads();
+  if (wid == 0) {
+    u32 w = wsum[lane];
+    u64 w2 = csum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 t = __shfl_up_sync(0xffffffffu, w, o);
+      const u64 t2 = __shfl_up_sync(0xffffffffu, w2, o);
+      if (lane >= o) { w += t; w2 += t2; }
+    }
+    wsum[lane] = w;
+    csum[lane] = w2;
+  }
+  __syncthreads();
+  const u32 ndense = wsum[31];
+  const u64 dtotal = csum[31];
+  const u64 m = ctl->npairs;  // pairs compacted from the hash table
+  const bool direct = (m == 0);
+  u32 slot = inz - nz + (wid ? wsum[wid - 1] : 0);
+  u64 off = icnt - local + (wid ? csum[wid - 1] : 0);
+#pragma unroll
+  for (int q = 0; q < IT; ++q) {
+    const u32 d = tid * IT + q;
+    if (c[q]) {
+      if (direct) {
+        skeys[slot] = base + d;
+        scnt[slot] = c[q];
+        soffs[slot] = off;
+      } else {
+        pkeys[m + slot] = base + d;
+        pcnt[m + slot] = c[q];
+      }
+      dense[d] = 0;
+      ++slot;
+      off += c[q];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    ctl->npairs = m + ndense;
+    if (direct) {
+      soffs[ndense] = dtotal;
+      ctl->total = dtotal;
+      ctl->sum_error = (dtotal != n_expect);
+      ctl->pairs_ready = (dtotal == n_expect);
+    }
+  }
+}
+
+void launch_dense_pairs(DevCtl* ctl, u64* dense, u64* pkeys, u64* pcnt, u64* skeys, u64* scnt,
+                        u64* soffs, u64 n_expect, cudaStream_t st, int gate) {
+  dense_pairs_kernel<<<1, 1024, 0, st>>>(ctl, dense, pkeys, pcnt, skeys, scnt, soffs, n_expect,
+                                         gate);
+}
+
+size_t dense_window_len() { return kRange; }
+
 // (key, count) pairs -> global table (the merge step of the sharded sort)
 __global__ void insert_pairs_kernel(const u64* __restrict__ keys, const u64* __restrict__ cnts,
                                     u64 m, u64 mult, DevCtl* ctl, u64* gkeys, u64* gcnt,
@@ -441,8 +537,8 @@ static int hc_variant() {
 //          1 = queued shape (smaller ring + per-warp miss queues)
 cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms,
-                              cudaStream_t st, int variant, int gate, u64* spill) {
-  HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate, spill};
+                              cudaStream_t st, int variant, int gate, u64* spill, u64* dense) {
+  HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate, spill, dense};
   int v = hc_variant();
   if (v < 0) v = variant == 0 ? 0 : 2;
   switch (v) {

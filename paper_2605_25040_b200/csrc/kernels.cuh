@@ -22,7 +22,10 @@ void launch_tiny_finalize(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,
 size_t hash_count_smem();
 cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms, cudaStream_t st,
-                              int variant, int gate, u64* spill);
+                              int variant, int gate, u64* spill, u64* dense);
+void launch_dense_pairs(DevCtl* ctl, u64* dense, u64* pkeys, u64* pcnt, u64* skeys, u64* scnt,
+                        u64* soffs, u64 n_expect, cudaStream_t st, int gate);
+size_t dense_window_len();
 void launch_spill_fold(DevCtl* ctl, const u64* spill, u64* gkeys, u64* gcnt, u32* glist, u64 mult,
                        int num_sms, cudaStream_t st, int gate);
 void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevCtl* ctl,
@@ -58,10 +61,9 @@ void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* st
 // telemetry.cu
 size_t tel_accum_bytes();
 void launch_tel_build(const u64* keys, u64 np, u64* tkeys, u32* tidx, int log2s, u32* first,
-                      u32* runs, int num_sms, cudaStream_t st);
+                      u32* runs, void* acc, int num_sms, cudaStream_t st);
 void launch_tel_runs(const u64* x, u64 n, u64 flip, const u64* tkeys, const u32* tidx, int log2s,
-                     u64 empty_idx, u32* first, u32* runs, void* acc, int num_sms,
-                     cudaStream_t st);
+                     u32* first, u32* runs, void* acc, int num_sms, cudaStream_t st);
 void launch_tel_comp(const u64* keys, u64 np, const u32* first, u64 mult, int m_log2, int dom,
                      u64* comp, u64* cidx, int num_sms, cudaStream_t st);
 void launch_tel_classify(const u64* comp, const u64* cidx, u64 np, int cap, const u64* counts,

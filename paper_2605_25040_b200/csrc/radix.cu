@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(1024, 1)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   u64 n = n_arg;
   if (PAIRS && ctl) {
-    if (ctl->overflow || !gate_open(ctl, gate)) return;
+    if (ctl->overflow || ctl->pairs_ready || !gate_open(ctl, gate)) return;  // ready: dense path
     n = ctl->npairs;
     if (n > (u64)kSmallSortMax) {
       if (tid == 0) ctl->need_large = 1;

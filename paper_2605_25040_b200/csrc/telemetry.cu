@@ -27,6 +27,7 @@ namespace cafs {
 
 struct TelAccum {
   unsigned long long runs, spill_len, spill_pushes, claims, stored_runs;
+  unsigned long long empty_idx;  // pair index of the sentinel key value ~0, if present
 };
 
 __device__ __forceinline__ u32 tl_hash(u64 k, int log2s) {
@@ -34,14 +35,14 @@ __device__ __forceinline__ u32 tl_hash(u64 k, int log2s) {
 }
 
 __global__ void tl_build_kernel(const u64* __restrict__ keys, u64 np, u64* tkeys, u32* tidx,
-                                int log2s, u32* first, u32* runs) {
+                                int log2s, u32* first, u32* runs, TelAccum* acc) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   const u32 mask = (1u << log2s) - 1;
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < np; j += stride) {
     const u64 k = keys[j];
     first[j] = 0xFFFFFFFFu;
     runs[j] = 0;
-    if (k == kEmpty) continue;  // the sentinel value is looked up by index, not hashed
+    if (k == kEmpty) { acc->empty_idx = j; continue; }  // looked up by index, not hashed
     u32 h = tl_hash(k, log2s);
     while (true) {  // keys are distinct; load <= 1/2
       const u64 old = atomicCAS(&tkeys[h], kEmpty, k);
@@ -62,8 +63,9 @@ __device__ __forceinline__ u32 tl_lookup(const u64* tkeys, const u32* tidx, int 
 
 __global__ void __launch_bounds__(512)
     tl_runs_kernel(const u64* __restrict__ x, u64 n, u64 flip, const u64* tkeys, const u32* tidx,
-                   int log2s, u64 empty_idx, u32* first, u32* runs, TelAccum* acc) {
+                   int log2s, u32* first, u32* runs, TelAccum* acc) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 empty_idx = acc->empty_idx;
   u64 local = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += stride) {
     const u64 v = x[i] ^ flip;
@@ -124,19 +126,18 @@ __global__ void tl_classify_kernel(const u64* __restrict__ comp, const u64* __re
 size_t tel_accum_bytes() { return sizeof(TelAccum); }
 
 void launch_tel_build(const u64* keys, u64 np, u64* tkeys, u32* tidx, int log2s, u32* first,
-                      u32* runs, int num_sms, cudaStream_t st) {
+                      u32* runs, void* acc, int num_sms, cudaStream_t st) {
   cudaMemsetAsync(tkeys, 0xFF, (size_t(1) << log2s) * 8, st);
   u64 blocks = (np + 255) / 256;
   if (blocks > (u64)num_sms * 8) blocks = (u64)num_sms * 8;
   tl_build_kernel<<<(unsigned)(blocks ? blocks : 1), 256, 0, st>>>(keys, np, tkeys, tidx, log2s,
-                                                                   first, runs);
+                                                                   first, runs, (TelAccum*)acc);
 }
 
 void launch_tel_runs(const u64* x, u64 n, u64 flip, const u64* tkeys, const u32* tidx, int log2s,
-                     u64 empty_idx, u32* first, u32* runs, void* acc, int num_sms,
-                     cudaStream_t st) {
-  tl_runs_kernel<<<num_sms * 4, 512, 0, st>>>(x, n, flip, tkeys, tidx, log2s, empty_idx, first,
-                                              runs, (TelAccum*)acc);
+                     u32* first, u32* runs, void* acc, int num_sms, cudaStream_t st) {
+  tl_runs_kernel<<<num_sms * 4, 512, 0, st>>>(x, n, flip, tkeys, tidx, log2s, first, runs,
+                                              (TelAccum*)acc);
 }
 
 void launch_tel_comp(const u64* keys, u64 np, const u32* first, u64 mult, int m_log2, int dom,

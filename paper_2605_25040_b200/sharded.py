@@ -60,6 +60,10 @@ def _torch():
     return torch
 
 
+# the device's pair capacity: global table + the ~0 sentinel + the dense window
+_PAIR_CAP = (1 << 21) + 1 + 8192
+
+
 class DeviceOps:
     """Local pipeline steps on this rank's GPU, through libcafs_b200.so."""
 
@@ -109,7 +113,7 @@ class DeviceOps:
 
     def count_pairs(self, x, mult: int):
         """Sorted distinct (key, count) pairs of the shard, or None on table overflow."""
-        cap = 1 << 21
+        cap = _PAIR_CAP
         k, c = self._pairs_out(cap)
         if x.shape[0] == 0:
             return k[:0], c[:0]
@@ -123,7 +127,7 @@ class DeviceOps:
         return k[:npairs.value], c[:npairs.value]
 
     def merge_pairs(self, keys, counts):
-        cap = 1 << 21
+        cap = _PAIR_CAP
         k, c = self._pairs_out(cap)
         npairs = ctypes.c_uint64()
         rc = self.lib.cafs_merge_pairs(self.ctx, keys.data_ptr(), counts.data_ptr(), keys.shape[0],

@@ -311,3 +311,58 @@ def test_determinism_and_repeat_calls():
         cafs.cafs_sort(t)
         outs.add(sha(t))
     assert len(outs) == 1 and outs == {sha(np.sort(x))}
+
+
+def _dense_mix(kind: str) -> np.ndarray:
+    """Dictionary codes (inside the dense window) plus out-of-window keys."""
+    rng = np.random.default_rng(len(kind))
+    x = rng.integers(-2000, 2000, 1_500_000, dtype=np.int64)
+    if kind == "outliers":  # append mode: hash pairs + dense pairs, one sort
+        x[rng.integers(0, x.shape[0], 3000)] = rng.integers(-(1 << 62), 1 << 62, 3000)
+    elif kind == "sentinel":  # the key whose order-mapped value is ~0
+        x[::1000] = np.iinfo(np.int64).max
+    elif kind == "many_outliers":  # > kSmallSortMax pairs in total: the large sort
+        x[rng.integers(0, x.shape[0], 40_000)] = rng.integers(-(1 << 62), 1 << 62, 40_000)
+    return x
+
+
+@pytest.mark.parametrize("kind", ["codes", "outliers", "sentinel", "many_outliers"])
+@pytest.mark.parametrize("exact", [False, True])
+def test_dense_window_paths(kind, exact):
+    x = _dense_mix(kind)
+    want = x.copy()
+    ot = orc.cafs_sort(want)
+    t = to_dev(x)
+    tel = SortTelemetry()
+    cafs.cafs_sort(t, telemetry=tel, exact_telemetry=exact)
+    assert sha(t) == sha(want)
+    assert tel.route.value == ot.route
+    if exact:
+        assert (tel.spill_len, tel.guard_fired, tel.updates, tel.counted_total) == (
+            ot.spill_len, ot.guard_fired, ot.updates, ot.counted_total)
+        t_ = tel.table
+        assert (t_.hits, t_.claims, t_.spill_pushes) == (ot.hits, ot.claims, ot.spill_pushes)
+    # the stage API the sharded sort uses (count -> pairs) sees the same pairs
+    from paper_2605_25040_b200.sharded import DeviceOps
+    keys, counts = np.unique(x, return_counts=True)
+    k, c = DeviceOps(0).count_pairs(to_dev(x), cafs.HASH_MULT)
+    order_mapped = keys.view(np.uint64) ^ np.uint64(1 << 63)
+    assert np.array_equal(k.cpu().numpy().view(np.uint64), order_mapped)
+    assert np.array_equal(c.cpu().numpy(), counts)
+
+
+def test_guard_then_dense_window():
+    """A guard that fires mid-count must not leave dense-window counts behind."""
+    n = 6_000_000
+    x = ogen.mix_outputs(78, n).view(np.int64).copy()
+    stride = n // 1024
+    x[::stride][:1024] = np.arange(1024, dtype=np.int64) % 100  # low estimate + a window
+    x[:n // 3] = np.arange(n // 3) % 100  # many rows land in the window
+    tel = SortTelemetry()
+    t = to_dev(x)
+    cafs.cafs_sort(t, telemetry=tel)
+    assert tel.guard_fired and np.array_equal(t.cpu().numpy(), np.sort(x))
+    y = ogen.CONFIGS["cfg4"].generate(1_000_000)
+    t = to_dev(y)
+    cafs.cafs_sort(t)
+    assert np.array_equal(t.cpu().numpy(), np.sort(y))
