@@ -40,6 +40,8 @@ struct cafs_ctx {
   u64* gcnt = nullptr;
   u32* glist = nullptr;
   u64* pk_a = nullptr;  // compacted pairs (unsorted)
+  u64* pk_t = nullptr;  // MSD bucket buffers of the large pair sort (lazy)
+  u64* pc_t = nullptr;
   u64* pc_a = nullptr;
   u64* pk_b = nullptr;  // sorted pairs
   u64* pc_b = nullptr;
@@ -237,14 +239,14 @@ int try_msd(cafs_ctx_t* ctx, const u64* keys, const u64* vals, u64 n, u64 flip, 
 // is copied back), else LSD onesweep.
 int sort_pairs_large(cafs_ctx_t* ctx, u64 np, cudaStream_t st) {
   TRY(ensure_radix(ctx, np, false));
-  bool done;
-  TRY(try_msd(ctx, ctx->pk_a, ctx->pc_a, np, 0, ctx->pk_b, ctx->pc_b, ctx->pk_a, ctx->pc_a, st,
-              &done));
-  if (done) {
-    CK(cudaMemcpyAsync(ctx->pk_b, ctx->pk_a, np * 8, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(ctx->pc_b, ctx->pc_a, np * 8, cudaMemcpyDeviceToDevice, st));
-    return CAFS_OK;
+  if (!ctx->pk_t) {
+    CK(cudaMalloc(&ctx->pk_t, kPairCap * 8));
+    CK(cudaMalloc(&ctx->pc_t, kPairCap * 8));
   }
+  bool done;
+  TRY(try_msd(ctx, ctx->pk_a, ctx->pc_a, np, 0, ctx->pk_t, ctx->pc_t, ctx->pk_b, ctx->pc_b, st,
+              &done));
+  if (done) return CAFS_OK;
   u64 *rk, *rv;
   TRY(radix_sort(ctx, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, np, 0, st, &rk, &rv));
   if (rk != ctx->pk_b) {
@@ -265,9 +267,10 @@ int try_msd(cafs_ctx_t* ctx, const u64* keys, const u64* vals, u64 n, u64 flip, 
   CK(cudaMemcpyAsync(ctx->h_scratch, (char*)ctx->msd + msd_maxb_offset(), sizeof(u32),
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  if ((u32)ctx->h_scratch[0] > msd_bucket_cap()) return CAFS_OK;
-  launch_msd_sort(keys, vals, n, flip, ctx->msd, tk, tv, dk, dv, st);
-  ctx->launches += 2;
+  const u32 maxb = (u32)ctx->h_scratch[0];
+  if (maxb > msd_bucket_cap()) return CAFS_OK;
+  launch_msd_sort(keys, vals, n, flip, ctx->msd, tk, tv, dk, dv, maxb, st);
+  ctx->launches += maxb > 128 ? 3 : 2;
   CKL();
   *done = true;
   return CAFS_OK;
@@ -700,7 +703,7 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
                  ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->spill, ctx->dense, ctx->ghist, ctx->gbase,
                  ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage, ctx->msd,
                  ctx->tl_keys, ctx->tl_idx, ctx->tl_first, ctx->tl_runs, ctx->tl_comp,
-                 ctx->tl_offs, ctx->tl_acc};
+                 ctx->tl_offs, ctx->tl_acc, ctx->pk_t, ctx->pc_t};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);

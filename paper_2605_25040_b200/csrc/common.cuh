@@ -173,12 +173,18 @@ __device__ __forceinline__ void global_insert(u64* gkeys, u64* gcnt, u32* list, 
                                               u64 key, u64 inc, u64 /*mult*/) {
   u32 h = (u32)(fmix64(key) >> (64 - kGlobalLog2));
   for (int p = 0; p < kGlobalMaxProbe; ++p) {
-    u64 k = *((volatile u64*)&gkeys[h]);
+    u64 k = __ldcg(&gkeys[h]);  // L2 view; the CAS below arbitrates
     if (k == kEmpty) {
       u64 old = atomicCAS(&gkeys[h], kEmpty, key);
       if (old == kEmpty) {
+        // one claim-list atomic per group of lanes that claimed together (the
+        // stripe is per warp): same-address atomics with return serialise in L2
         const u32 stripe = (blockIdx.x * 32u + (threadIdx.x >> 5)) & (kListStripes - 1);
-        const u32 idx = atomicAdd(&ctl->g_fill[stripe], 1u);
+        const u32 grp = __activemask();
+        const int leader = __ffs(grp) - 1;
+        u32 idx = 0;
+        if ((int)(threadIdx.x & 31) == leader) idx = atomicAdd(&ctl->g_fill[stripe], __popc(grp));
+        idx = __shfl_sync(grp, idx, leader) + __popc(grp & lanemask_lt());
         if (idx < kStripeCap) list[stripe * kStripeCap + idx] = h;
         else ctl->overflow = 1;
         atomicAdd(&gcnt[h], inc);

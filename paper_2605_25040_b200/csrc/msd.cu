@@ -23,6 +23,7 @@ constexpr int kBsThreads = 256;
 constexpr int kBsWarps = kBsThreads / 32;
 constexpr u32 kBucketCap = 4096;                       // keys per bucket sorted in smem
 constexpr int kBsRounds = kBucketCap / kBsThreads;     // 16 rounds of 32 per warp
+constexpr u32 kWarpBucketMax = 128;                    // buckets sorted by one warp
 constexpr int kScThreads = 256;
 constexpr int kScItems = 16;                           // keys per thread in the scatter
 constexpr u64 kScChunk = (u64)kScThreads * kScItems;   // 4096
@@ -169,6 +170,53 @@ __global__ void __launch_bounds__(kScThreads)
   }
 }
 
+// Buckets of at most kWarpBucketMax keys (the common case when the 4096
+// buckets split a few hundred thousand keys): one warp per bucket, a rank sort
+// -- each key's destination is the number of keys that precede it (smaller,
+// or equal and earlier: stable) -- from a broadcast scan of the bucket in
+// shared memory.  No block barriers, no digit passes, 32 buckets per CTA wave.
+template <bool HAS_VAL>
+__global__ void __launch_bounds__(256)
+    bucket_small_kernel(const u64* __restrict__ tk, const u64* __restrict__ tv,
+                        const MsdState* ms, u64 flip, u64* __restrict__ dk,
+                        u64* __restrict__ dv) {
+  constexpr int R = kWarpBucketMax / 32;
+  __shared__ u64 sk[8][kWarpBucketMax];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const u32 b = blockIdx.x * 8 + wid;
+  if (b >= kMsdBuckets) return;
+  const u32 base = ms->base[b];
+  const u32 n = ms->base[b + 1] - base;
+  if (n == 0 || n > kWarpBucketMax) return;
+  u64 k[R], v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const u32 i = lane + 32 * r;
+    k[r] = i < n ? tk[base + i] : ~0ull;
+    v[r] = (HAS_VAL && i < n) ? tv[base + i] : 0;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (lane + 32 * r < n) sk[wid][lane + 32 * r] = k[r];
+  __syncwarp();
+  u32 rank[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) rank[r] = 0;
+  for (u32 j = 0; j < n; ++j) {
+    const u64 kj = sk[wid][j];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      rank[r] += (kj < k[r]) || (kj == k[r] && j < (u32)(lane + 32 * r));
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (lane + 32 * r < n) {
+      dk[base + rank[r]] = k[r] ^ flip;
+      if (HAS_VAL) dv[base + rank[r]] = v[r];
+    }
+  }
+}
+
 // One CTA per bucket: load it into shared memory, LSD radix over the bytes that
 // vary inside the bucket (stable 8-ballot multisplit, warp-contiguous
 // segments), write it back sorted (un-flipping the keys; pairs carry their
@@ -189,14 +237,7 @@ __global__ void __launch_bounds__(kBsThreads)
   const u32 b = blockIdx.x;
   const u32 base = ms->base[b];
   const u32 n = ms->base[b + 1] - base;
-  if (n == 0) return;
-  if (n == 1) {
-    if (tid == 0) {
-      dk[base] = tk[base] ^ flip;
-      if (HAS_VAL) dv[base] = tv[base];
-    }
-    return;
-  }
+  if (n <= kWarpBucketMax) return;  // bucket_small_kernel's
   u64 vor = 0, vand = ~0ull;
   {  // all loads in flight before any use (one DRAM round trip, not n/256)
     u64 lk[kBsRounds];
@@ -338,7 +379,7 @@ size_t msd_maxb_offset() { return offsetof(MsdState, maxb); }
 constexpr size_t kBsSmem = (size_t)kBucketCap * (16 + 4) + (size_t)kBsWarps * 256 * 4;
 
 void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* state, u64* tk,
-                     u64* tv, u64* dk, u64* dv, cudaStream_t st) {
+                     u64* tv, u64* dk, u64* dv, u32 maxb, cudaStream_t st) {
   MsdState* ms = (MsdState*)state;
   const u64 chunks = (n + kScChunk - 1) / kScChunk;
   static int attr_dev = -1;
@@ -351,15 +392,21 @@ void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* st
                          (int)kBsSmem);
     attr_dev = dev;
   }
+  const bool large = maxb > kWarpBucketMax;
   if (vals) {
     msd_scatter_kernel<true><<<(unsigned)chunks, kScThreads, 0, st>>>(keys, vals, n, flip, ms, tk,
                                                                       tv);
-    bucket_sort_kernel<true><<<kMsdBuckets, kBsThreads, kBsSmem, st>>>(tk, tv, ms, flip, dk, dv);
+    bucket_small_kernel<true><<<kMsdBuckets / 8, 256, 0, st>>>(tk, tv, ms, flip, dk, dv);
+    if (large)
+      bucket_sort_kernel<true><<<kMsdBuckets, kBsThreads, kBsSmem, st>>>(tk, tv, ms, flip, dk, dv);
   } else {
     msd_scatter_kernel<false><<<(unsigned)chunks, kScThreads, 0, st>>>(keys, nullptr, n, flip, ms,
                                                                        tk, nullptr);
-    bucket_sort_kernel<false><<<kMsdBuckets, kBsThreads, kBsSmem, st>>>(tk, nullptr, ms, flip, dk,
-                                                                         nullptr);
+    bucket_small_kernel<false><<<kMsdBuckets / 8, 256, 0, st>>>(tk, nullptr, ms, flip, dk,
+                                                               nullptr);
+    if (large)
+      bucket_sort_kernel<false><<<kMsdBuckets, kBsThreads, kBsSmem, st>>>(tk, nullptr, ms, flip,
+                                                                           dk, nullptr);
   }
 }
 
