@@ -22,6 +22,8 @@
  *   cafs_pair_sort           _kernels.py:185-214 radix_sort_pairs / sorter.py:228-241 pair_sort
  *   cafs_emit_i64            sorter.py:244-251 + _kernels.py:172-182  emit / emit_fill
  *   cafs_fallback_sort_i64   sorter.py:132-138   fallback_sort(x)
+ *   cafs_key_span_i64,       (no reference counterpart: the distributed
+ *   cafs_partition_i64        fallback of SURVEY.md §8(f)2, sharded.py)
  *
  * Keys are 64-bit.  `is_signed` = 1 for int64 (order-mapped by flipping bit 63,
  * sorter.py:84-94, folded into the kernels' loads/stores), 0 for uint64.
@@ -179,6 +181,22 @@ int cafs_emit_i64(cafs_ctx_t* ctx, const uint64_t* d_keys, const uint64_t* d_cou
 /* fallback_sort(x): on-device LSD radix sort (sorter.py:132-138 replaced) */
 int cafs_fallback_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed,
                            void* stream);
+
+/* ---- distributed fallback (sharded high-entropy / guard routes) ----
+ * The reference is single-process; its fallback_sort (sorter.py:132-138) is
+ * what a multi-GPU caller replaces with: global span -> one bucket digit ->
+ * local partition -> all-to-all of bucket ranges -> local sort of the received
+ * range.  These two calls are the local steps. */
+/* OR and AND over the order-mapped keys (h_or = 0, h_and = ~0 when n == 0) */
+int cafs_key_span_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                      uint64_t* h_or, uint64_t* h_and, void* stream);
+/* Group x by the 4096-way bucket digit of the 12 highest bits varying over the
+ * GLOBAL span (g_or, g_and): d_out[0..n) = the keys (same representation as x)
+ * in ascending digit order, h_counts[4096] = keys per bucket. */
+#define CAFS_PARTITION_BUCKETS 4096
+int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                       uint64_t g_or, uint64_t g_and, int64_t* d_out, uint64_t* h_counts,
+                       void* stream);
 
 /* ---- synthetic inputs (bench / tests; bit-identical to oracle/gen.py) ---- */
 /* out[i] = fmix64(seed + (skip + i + 1) * 0x9E3779B97F4A7C15) */

@@ -71,7 +71,7 @@ struct cafs_ctx {
   u64* stage = nullptr;  // host-path device staging buffer
   size_t stage_elems = 0;
   u32 epoch = 0;
-  int32_t* h_scratch = nullptr;  // pinned
+  int32_t* h_scratch = nullptr;  // pinned (64 B + a partition histogram)
   cudaEvent_t ev[32] = {};
   std::string last_error;
   uint32_t launches = 0;
@@ -684,7 +684,7 @@ int cafs_ctx_create(int device, cafs_ctx_t** out) {
   ctx->num_sms = prop.multiProcessorCount;
   if (cudaMalloc(&ctx->d_ctl, sizeof(DevCtl)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_ctl, sizeof(DevCtl)) != cudaSuccess ||
-      cudaMallocHost(&ctx->h_scratch, 64) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_scratch, 64 + CAFS_PARTITION_BUCKETS * 4) != cudaSuccess ||
       cudaMemset(ctx->d_ctl, 0, sizeof(DevCtl)) != cudaSuccess) {
     cafs_ctx_destroy(ctx);
     return CAFS_ENOMEM;
@@ -1079,6 +1079,52 @@ int cafs_fallback_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_sig
   cudaStream_t st = (cudaStream_t)stream;
   TRY(fallback_sort(ctx, (u64*)d_x, n, is_signed ? kSign : 0, st));
   CK(cudaStreamSynchronize(st));
+  return CAFS_OK;
+}
+
+int cafs_key_span_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                      uint64_t* h_or, uint64_t* h_and, void* stream) {
+  if (!h_or || !h_and) return CAFS_EINVAL;
+  TRY(check_common(ctx, d_x, n));
+  *h_or = 0;
+  *h_and = ~0ull;
+  if (n == 0) return CAFS_OK;
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(ensure_radix(ctx, n, false));
+  launch_msd_span((const u64*)d_x, n, is_signed ? kSign : 0, ctx->msd, ctx->num_sms, st);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_scratch, (char*)ctx->msd + msd_span_offset(), 16,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const u64* v = (const u64*)ctx->h_scratch;
+  *h_or = v[0];
+  *h_and = v[1];
+  return CAFS_OK;
+}
+
+int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                       uint64_t g_or, uint64_t g_and, int64_t* d_out, uint64_t* h_counts,
+                       void* stream) {
+  if (!h_counts || (n && !d_out)) return CAFS_EINVAL;
+  TRY(check_common(ctx, d_x, n));
+  if (n >> 32) return fail(ctx, CAFS_EINVAL, "partition: more than 2^32 keys per rank");
+  for (int b = 0; b < CAFS_PARTITION_BUCKETS; ++b) h_counts[b] = 0;
+  if (n == 0) return CAFS_OK;
+  const u64 flip = is_signed ? kSign : 0;
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(ensure_radix(ctx, n, false));
+  launch_msd_partition((const u64*)d_x, n, flip, ctx->msd, g_or, g_and, (u64*)d_out,
+                       ctx->num_sms, st);
+  CKL();
+  const u32* hc = (const u32*)ctx->h_scratch;  // pinned, 64 + 4096 x 4 bytes
+  cudaError_t e = cudaMemcpyAsync(ctx->h_scratch, (char*)ctx->msd + msd_hist_offset(),
+                                  CAFS_PARTITION_BUCKETS * 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess)
+    for (int b = 0; b < CAFS_PARTITION_BUCKETS; ++b) h_counts[b] = hc[b];
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "partition", e);
   return CAFS_OK;
 }
 

@@ -29,7 +29,7 @@ constexpr int kGlobalMaxProbe = 128;
 constexpr u64 kSpillCap = 1ull << 25;                 // HBM spill buffer (keys); excess goes inline
 constexpr u32 kMaxSpillRegions = 256;                 // >= count-kernel grid (one CTA per SM)
 // The claim list of the global table is striped: a claim from warp w of CTA b
-// appends to stripe (32 b + w) % kListStripes, so claims from all SMs do not
+// appends to stripe (global warp index) % kListStripes, so claims from all SMs do not
 // serialise on one counter and the stripes fill evenly.  A full stripe is a
 // table overflow (the guard).
 constexpr u32 kListStripes = 128;
@@ -179,7 +179,9 @@ __device__ __forceinline__ void global_insert(u64* gkeys, u64* gcnt, u32* list, 
       if (old == kEmpty) {
         // one claim-list atomic per group of lanes that claimed together (the
         // stripe is per warp): same-address atomics with return serialise in L2
-        const u32 stripe = (blockIdx.x * 32u + (threadIdx.x >> 5)) & (kListStripes - 1);
+        const u32 gwarp = ((blockIdx.y * gridDim.x + blockIdx.x) * (blockDim.x >> 5)) +
+                          (threadIdx.x >> 5);
+        const u32 stripe = gwarp & (kListStripes - 1);
         const u32 grp = __activemask();
         const int leader = __ffs(grp) - 1;
         u32 idx = 0;
@@ -199,6 +201,29 @@ __device__ __forceinline__ void global_insert(u64* gkeys, u64* gcnt, u32* list, 
     h = (h + 1) & (u32)(kGlobalSlots - 1);
   }
   ctl->overflow = 1;
+}
+
+// R independent inserts with their first probes in flight together: a key
+// already in the table (the common case once the hot keys are claimed) costs
+// one L2 round trip shared by all R, instead of R dependent ones.  ok[r] false
+// skips entry r.  The sentinel key value must not be passed.
+template <int R>
+__device__ __forceinline__ void global_insert_batch(u64* gkeys, u64* gcnt, u32* list, DevCtl* ctl,
+                                                    const u64 (&key)[R], const u64 (&inc)[R],
+                                                    const bool (&ok)[R]) {
+  u32 h[R];
+  u64 cur[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    h[r] = (u32)(fmix64(key[r]) >> (64 - kGlobalLog2));
+    cur[r] = ok[r] ? __ldcg(&gkeys[h[r]]) : 0;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (!ok[r]) continue;
+    if (cur[r] == key[r]) atomicAdd(&gcnt[h[r]], inc[r]);
+    else global_insert(gkeys, gcnt, list, ctl, key[r], inc[r], 0);
+  }
 }
 
 }  // namespace cafs

@@ -275,9 +275,24 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
     const u32 c = dcnt[d];
     if (c) atomicAdd(&a.dense[d], (u64)c);  // key base + d: no hashing, no claims
   }
-  for (u32 h = tid; h < kS; h += kHcThreads) {
-    const u32 c = scnt[h];
-    if (c) table_add(a, skeys[h], c);
+  constexpr int kFlushBatch = 2;  // first probes in flight per thread (register budget)
+#pragma unroll 1
+  for (u32 h0 = tid; h0 < kS; h0 += kFlushBatch * kHcThreads) {
+    constexpr int R = kFlushBatch;
+    u64 key[R], inc[R];
+    bool ok[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const u32 h = h0 + r * kHcThreads;
+      inc[r] = scnt[h];
+      key[r] = skeys[h];
+      if (inc[r] && key[r] == kEmpty) {  // cannot happen: the sentinel is counted aside
+        atomicAdd(&a.ctl->empty_key_count, inc[r]);
+        inc[r] = 0;
+      }
+      ok[r] = inc[r] != 0;
+    }
+    global_insert_batch<R>(a.gkeys, a.gcnt, a.glist, a.ctl, key, inc, ok);
   }
   u64 g = glob_cnt;
 #pragma unroll
@@ -354,14 +369,29 @@ __global__ void spill_fold_kernel(DevCtl* ctl, const u64* __restrict__ spill, u6
   const u32 cap = (u32)(kSpillCap / nreg);
   const u64* region = spill + (u64)blockIdx.x * cap;
   const u32 m = ctl->spill_fill[blockIdx.x];
-  for (u32 i = threadIdx.x; i < m; i += blockDim.x)
-    global_insert(gkeys, gcnt, glist, ctl, region[i], 1, mult);
-  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ctl->g_updates, ctl->spill_len);
+  constexpr int R = 8;
+  const u32 step = blockDim.x * R;
+  for (u32 i0 = blockIdx.y * step; i0 < m; i0 += step * gridDim.y) {
+    u64 key[R], inc[R];
+    bool ok[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const u32 i = i0 + r * blockDim.x + threadIdx.x;
+      ok[r] = i < m;
+      key[r] = ok[r] ? __ldcs(&region[i]) : 0;
+      inc[r] = 1;
+    }
+    global_insert_batch<R>(gkeys, gcnt, glist, ctl, key, inc, ok);
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+    atomicAdd(&ctl->g_updates, ctl->spill_len);
 }
 
 void launch_spill_fold(DevCtl* ctl, const u64* spill, u64* gkeys, u64* gcnt, u32* glist, u64 mult,
                        int num_sms, cudaStream_t st, int gate) {
-  spill_fold_kernel<<<kMaxSpillRegions, 1024, 0, st>>>(ctl, spill, gkeys, gcnt, glist, mult, gate);
+  // regions x slices: a few CTAs per region keep every SM's warps issuing
+  spill_fold_kernel<<<dim3(kMaxSpillRegions, 8), 256, 0, st>>>(ctl, spill, gkeys, gcnt, glist,
+                                                              mult, gate);
 }
 
 // Dense-window counts -> (key, count) pairs in key order (the window is a key

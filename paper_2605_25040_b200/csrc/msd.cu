@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(1024) msd_scan_kernel(MsdState* ms) {
 template <bool HAS_VAL>
 __global__ void __launch_bounds__(kScThreads)
     msd_scatter_kernel(const u64* __restrict__ keys, const u64* __restrict__ vals, u64 n, u64 flip,
-                       MsdState* ms, u64* __restrict__ tk, u64* __restrict__ tv) {
+                       MsdState* ms, u64* __restrict__ tk, u64* __restrict__ tv,
+                       u64 out_xor = 0) {
   __shared__ u32 h[kMsdBuckets];
   __shared__ u32 g[kMsdBuckets];
   for (u32 i = threadIdx.x; i < kMsdBuckets; i += kScThreads) h[i] = 0;
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kScThreads)
     const u64 i = c0 + threadIdx.x + (u64)j * kScThreads;
     if (i < n) {
       const u32 pos = g[msd_digit(k[j], shift)] + r[j];
-      tk[pos] = k[j];
+      tk[pos] = k[j] ^ out_xor;
       if (HAS_VAL) tv[pos] = vals[i];
     }
   }
@@ -370,6 +371,43 @@ void launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms
   msd_reduce_kernel<<<(unsigned)blocks, 512, 0, st>>>(keys, n, flip, ms);
   msd_hist_kernel<<<(unsigned)blocks, 512, 0, st>>>(keys, n, flip, ms);
   msd_scan_kernel<<<1, 1024, 0, st>>>(ms);
+}
+
+__global__ void msd_set_span_kernel(MsdState* ms, u64 vor, u64 vand) {
+  ms->vor = vor;
+  ms->vand = vand;
+}
+
+// Local OR/AND of the order-mapped keys (the distributed fallback all-gathers
+// them to fix one bucket digit for every rank).
+void launch_msd_span(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st) {
+  MsdState* ms = (MsdState*)state;
+  cudaMemsetAsync(ms, 0, sizeof(MsdState), st);
+  cudaMemsetAsync(&ms->vand, 0xFF, sizeof(u64), st);
+  u64 blocks = (n + 512 * 8 - 1) / (512 * 8);
+  if (blocks > (u64)num_sms * 4) blocks = (u64)num_sms * 4;
+  if (blocks < 1) blocks = 1;
+  msd_reduce_kernel<<<(unsigned)blocks, 512, 0, st>>>(keys, n, flip, ms);
+}
+size_t msd_span_offset() { return offsetof(MsdState, vor); }  // vor, vand adjacent
+size_t msd_hist_offset() { return offsetof(MsdState, hist); }
+
+// Group keys by the bucket digit of a GLOBAL span (vor, vand): out holds the
+// keys (original representation) in ascending digit order; hist = counts.
+void launch_msd_partition(const u64* keys, u64 n, u64 flip, void* state, u64 vor, u64 vand,
+                          u64* out, int num_sms, cudaStream_t st) {
+  MsdState* ms = (MsdState*)state;
+  cudaMemsetAsync(ms, 0, sizeof(MsdState), st);
+  msd_set_span_kernel<<<1, 1, 0, st>>>(ms, vor, vand);
+  u64 blocks = (n + 512 * 8 - 1) / (512 * 8);
+  if (blocks > (u64)num_sms * 4) blocks = (u64)num_sms * 4;
+  if (blocks < 1) blocks = 1;
+  msd_hist_kernel<<<(unsigned)blocks, 512, 0, st>>>(keys, n, flip, ms);
+  msd_scan_kernel<<<1, 1024, 0, st>>>(ms);
+  const u64 chunks = (n + kScChunk - 1) / kScChunk;
+  if (chunks)
+    msd_scatter_kernel<false><<<(unsigned)chunks, kScThreads, 0, st>>>(keys, nullptr, n, flip, ms,
+                                                                       out, nullptr, flip);
 }
 
 u32 msd_read_max(const void* state_host_copy) { return ((const MsdState*)state_host_copy)->maxb; }

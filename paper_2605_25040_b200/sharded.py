@@ -23,9 +23,10 @@ per-thread tables and a final merge as future work.  Here:
    pair tables (<= K x 16 B per rank), the merge (union + fold, sorter.py:276-285)
    on every rank, then each rank emits only its own output slice from the
    global prefix sum;
-4. FALLBACK / guard: "gather then sort" (every rank sorts the gathered column
-   and keeps its slice).  A distributed radix sort is the next step (SURVEY.md
-   §8(f)2); the high-entropy configs are single-GPU in BASELINE.json.
+4. FALLBACK / guard: a distributed MSD sort (:func:`_exchange_sort`, SURVEY.md
+   §8(f)2): one partition pass on a globally agreed 4096-way digit, an
+   all-to-all of bucket ranges over NCCL, a local sort of the received range;
+   inputs under 2048 rows are gathered and sorted everywhere.
 
 Local steps go through :class:`DeviceOps` (the C ABI); collectives through
 ``torch.distributed``.  Tests inject a CPU ``ops`` object with the same
@@ -53,6 +54,7 @@ from .sorter import (
 )
 
 _SIGN = 1 << 63
+PARTITION_BUCKETS = 4096  # CAFS_PARTITION_BUCKETS
 
 
 def _torch():
@@ -152,6 +154,25 @@ class DeviceOps:
                                                    int(self.signed), self._stream()),
                    self.ctx, "fallback_sort")
 
+    def key_span(self, x) -> tuple[int, int]:
+        """(OR, AND) of the order-mapped keys; (0, 2**64-1) for an empty shard."""
+        vor, vand = ctypes.c_uint64(), ctypes.c_uint64()
+        _lib.check(self.lib.cafs_key_span_i64(self.ctx, x.data_ptr(), x.shape[0], int(self.signed),
+                                              ctypes.byref(vor), ctypes.byref(vand),
+                                              self._stream()), self.ctx, "key_span")
+        return int(vor.value), int(vand.value)
+
+    def partition(self, x, g_or: int, g_and: int):
+        """x grouped by the global bucket digit; (grouped tensor, counts[4096])."""
+        torch = _torch()
+        out = torch.empty_like(x)
+        counts = np.zeros(PARTITION_BUCKETS, np.uint64)
+        _lib.check(self.lib.cafs_partition_i64(
+            self.ctx, x.data_ptr(), x.shape[0], int(self.signed), g_or, g_and, out.data_ptr(),
+            counts.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), self._stream()),
+            self.ctx, "partition")
+        return out, counts.astype(np.int64)
+
     def keys_tensor(self, keys_u64: list[int], counts: np.ndarray):
         torch = _torch()
         dev = torch.device("cuda", self.device)
@@ -188,9 +209,18 @@ class Comm:
         return [o.cpu().numpy().view(np.uint64).astype(object).tolist() for o in out]
 
     def all_reduce_sum(self, a: np.ndarray) -> np.ndarray:
-        t = self._t(np.ascontiguousarray(a, dtype=np.int64))
+        t = self._t(np.array(a, dtype=np.int64))  # a copy: the reduction is in place
         self.dist.all_reduce(t, group=self.group)
         return t.cpu().numpy()
+
+    def all_to_all_var(self, send, in_splits: list[int], out_splits: list[int]):
+        """Variable-size all-to-all of a 1-D int64 tensor (send is split in rank order)."""
+        torch = _torch()
+        stage = self.device is None and send.is_cuda
+        src = send.cpu() if stage else send
+        out = torch.empty(int(sum(out_splits)), dtype=send.dtype, device=src.device)
+        self.dist.all_to_all_single(out, src, out_splits, in_splits, group=self.group)
+        return out.to(send.device) if stage else out
 
     def all_gather_var(self, t):
         """All-gather 1-D int64 tensors of different lengths (pad to the max)."""
@@ -203,6 +233,77 @@ class Comm:
         out = [torch.empty_like(pad) for _ in range(self.world)]
         self.dist.all_gather(out, pad, group=self.group)
         return torch.cat([o[:s] for o, s in zip(out, sizes)]).to(t.device)
+
+
+def msd_shift(g_or: int, g_and: int, bits: int = 12) -> int:
+    """Shift that puts the `bits` highest varying bits of the span in the digit
+    (msd.cu msd_shift)."""
+    vary = g_or ^ g_and
+    if vary == 0:
+        return 0
+    hb = vary.bit_length() - 1
+    return hb + 1 - bits if hb + 1 > bits else 0
+
+
+def bucket_ranges(totals: np.ndarray, sizes: list[int]) -> list[tuple[int, int]]:
+    """Bucket range [lo, hi) each rank needs for its output slice.
+
+    Rank d owns sorted rows [off_d, off_d + n_d); bucket b holds rows
+    [P[b], P[b+1]) of the sorted column.  A bucket straddling two slices goes to
+    both ranks (each sorts it and keeps its part)."""
+    P = np.concatenate([[0], np.cumsum(totals, dtype=np.int64)])
+    out, off = [], 0
+    for n_d in sizes:
+        if n_d == 0:
+            out.append((0, 0))
+        else:
+            lo = int(np.searchsorted(P[1:], off, side="right"))
+            hi = int(np.searchsorted(P[:-1], off + n_d, side="left"))
+            out.append((lo, hi))
+        off += n_d
+    return out
+
+
+def _exchange_sort(x_local, sizes: list[int], comm, ops) -> None:
+    """Distributed fallback sort: one MSD partition pass, an
+    all-to-all of bucket ranges, a local sort of the received range.
+
+    1. global span: all-gather of each shard's OR/AND of the order-mapped keys
+       -> one 4096-way digit on the 12 highest varying bits, the same on every
+       rank (so bucket b precedes bucket b+1 globally);
+    2. local partition by that digit (cafs_partition_i64) and an all-reduce of
+       the bucket counts -> the global row range of every bucket;
+    3. rank d receives, from every rank, the buckets overlapping its output
+       slice (all_to_all_single with per-rank splits), sorts them locally with
+       the single-GPU fallback and keeps its rows.
+    Traffic per key: ~8 B over NVLink plus the local partition and sort; every
+    rank sorts ~1/N of the column (versus all of it when gathering)."""
+    torch = _torch()
+    rank, world = comm.rank, comm.world
+    n_local = int(x_local.shape[0])
+    off = int(sum(sizes[:rank]))
+    spans = comm.all_gather_ints(list(ops.key_span(x_local)))
+    g_or, g_and = 0, (1 << 64) - 1
+    for (o, a), n_r in zip(spans, sizes):
+        if n_r:
+            g_or |= o
+            g_and &= a
+    part, counts = ops.partition(x_local, g_or, g_and)
+    totals = comm.all_reduce_sum(counts)
+    ranges = bucket_ranges(totals, sizes)
+    L = np.concatenate([[0], np.cumsum(counts, dtype=np.int64)])
+    in_splits = [int(L[hi] - L[lo]) for lo, hi in ranges]
+    matrix = comm.all_gather_ints(in_splits)  # matrix[s][d]: rows s sends to d
+    out_splits = [int(matrix[s][rank]) for s in range(world)]
+    pieces = [part[int(L[lo]):int(L[hi])] for lo, hi in ranges]
+    send = torch.cat(pieces) if pieces else part[:0]
+    recv = comm.all_to_all_var(send, in_splits, out_splits)
+    if n_local == 0:
+        return
+    ops.fallback_sort(recv)
+    P = np.concatenate([[0], np.cumsum(totals, dtype=np.int64)])
+    start = off - int(P[ranges[rank][0]])
+    x_local.copy_(recv[start:start + n_local])
 
 
 def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTelemetry | None = None,
@@ -250,9 +351,12 @@ def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTeleme
     def _fallback(route_decision: DispatchDecision, guard: bool = False):
         tel.decision = route_decision
         tel.guard_fired = guard
-        full = comm.all_gather_var(x_local)
-        ops.fallback_sort(full)
-        x_local.copy_(full[off:off + n_local])
+        if N < SMALL_N_CUTOFF:  # a few KB: gather and sort everywhere
+            full = comm.all_gather_var(x_local)
+            ops.fallback_sort(full)
+            x_local.copy_(full[off:off + n_local])
+            return
+        _exchange_sort(x_local, sizes, comm, ops)
 
     if N < SMALL_N_CUTOFF:
         _fallback(DispatchDecision(Route.FALLBACK_SMALL_N))

@@ -101,3 +101,29 @@ def test_config_seeds_route_as_intended():
     rec = {r["name"]: r["route"] for r in load_json("config_cases.json")}
     assert rec == {"cfg1": "main", "cfg2": "tiny_count", "cfg3": "main",
                    "cfg5": "fallback_high_entropy", "cfg4": "main"}
+
+
+def test_distributed_fallback_bucket_ranges():
+    """Bucket ranges of the distributed fallback (sharded._exchange_sort)."""
+    from paper_2605_25040_b200.sharded import bucket_ranges, msd_shift
+    assert msd_shift(0, 0) == 0
+    assert msd_shift(0xFFF, 0) == 0
+    assert msd_shift(0x1FFF, 0) == 1
+    assert msd_shift((1 << 64) - 1, 0) == 52
+    assert msd_shift(0x8000_0000_0000_00FF, 0x8000_0000_0000_0000) == 0
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        totals = rng.integers(0, 5, 16) * rng.integers(0, 2, 16)
+        n = int(totals.sum())
+        cuts = np.sort(rng.integers(0, n + 1, rng.integers(1, 5)))
+        sizes = np.diff(np.concatenate([[0], cuts, [n]])).tolist()
+        P = np.concatenate([[0], np.cumsum(totals)])
+        off = 0
+        for (lo, hi), s in zip(bucket_ranges(totals, sizes), sizes):
+            if s == 0:
+                assert lo == hi
+            else:
+                # the received buckets cover the slice, and no bucket is needless
+                assert P[lo] <= off and P[hi] >= off + s
+                assert totals[lo] > 0 and totals[hi - 1] > 0
+            off += s

@@ -27,6 +27,7 @@ class NumpyOps:
     """Local pipeline steps as numpy (test double of sharded.DeviceOps)."""
 
     signed = True
+    pair_cap = None  # set: count_pairs reports a table overflow above this many keys
 
     def _u(self, x):
         return x.numpy().view(np.uint64) ^ SIGN
@@ -46,6 +47,8 @@ class NumpyOps:
 
     def count_pairs(self, x, mult):
         vals, cnts = np.unique(self._u(x), return_counts=True)
+        if self.pair_cap is not None and vals.shape[0] > self.pair_cap:
+            return None
         return torch.from_numpy(vals.view(np.int64).copy()), torch.from_numpy(cnts.astype(np.int64))
 
     def merge_pairs(self, keys, counts):
@@ -63,6 +66,19 @@ class NumpyOps:
     def fallback_sort(self, x):
         x.copy_(torch.from_numpy(np.sort(x.numpy())))
 
+    def key_span(self, x):
+        u = self._u(x)
+        if u.shape[0] == 0:
+            return 0, (1 << 64) - 1
+        return int(np.bitwise_or.reduce(u)), int(np.bitwise_and.reduce(u))
+
+    def partition(self, x, g_or, g_and):
+        from paper_2605_25040_b200.sharded import PARTITION_BUCKETS, msd_shift
+        d = ((self._u(x) >> np.uint64(msd_shift(g_or, g_and))) & np.uint64(4095)).astype(np.int64)
+        order = np.argsort(d, kind="stable")
+        return (torch.from_numpy(x.numpy()[order].copy()),
+                np.bincount(d, minlength=PARTITION_BUCKETS).astype(np.int64))
+
     def keys_tensor(self, keys, counts):
         return (torch.from_numpy(np.array(keys, np.uint64).view(np.int64)),
                 torch.from_numpy(np.asarray(counts, np.int64)))
@@ -78,11 +94,15 @@ def _cases():
     ramp = np.arange(-50_000, 50_000, dtype=np.int64)
     small = ogen.gen_input(1000, 50, 5).view(np.int64)
     zipf = ogen.CONFIGS["cfg3"].generate(400_000)
+    skew = ogen.distinct_values(100_000, 11).view(np.int64).copy()
+    skew[::2] = 123456789  # one huge bucket across both slices, still high-entropy
     return {"main": (main, [120_003]), "tiny": (tiny, [150_000]), "tiny_fail": (fail, [7]),
             "distinct": (distinct, [60_000]), "ramp": (ramp, [50_000]),
             "small": (small, [400]), "zipf": (zipf, [200_000]),
             "empty_shard": (main[:100_000], [100_000]),
-            "uneven": (rng.permutation(main), [33])}
+            "uneven": (rng.permutation(main), [33]),
+            "distinct_uneven": (distinct, [999]), "distinct_empty": (distinct, [0]),
+            "skew": (skew, [50_001]), "guard": (main, [90_000])}
 
 
 def _worker(rank, world, port, name, q):
@@ -97,9 +117,12 @@ def _worker(rank, world, port, name, q):
         bounds = [0] + cuts + [x.shape[0]]
         local = torch.from_numpy(x[bounds[rank]:bounds[rank + 1]].copy())
         tel = SortTelemetry()
-        cafs_sort_sharded(local, ops=NumpyOps(), telemetry=tel)
+        ops = NumpyOps()
+        if name == "guard":
+            ops.pair_cap = 100  # the device table "overflows": guard -> distributed fallback
+        cafs_sort_sharded(local, ops=ops, telemetry=tel)
         e = tel.decision.estimate
-        q.put((rank, local.numpy(), tel.route.value, tel.tiny_count_failed,
+        q.put((rank, local.numpy(), tel.route.value, tel.tiny_count_failed, tel.guard_fired,
                None if e is None else (e.k_hat, e.u, e.f1, e.f2, e.saturated)))
     finally:
         dist.destroy_process_group()
@@ -132,6 +155,7 @@ def test_sharded_world2_matches_single_process_oracle(name):
     for r in res:
         assert r[2] == otel.route
         assert r[3] == otel.tiny_count_failed
-        if r[4] is not None:
+        assert r[4] == (name == "guard")
+        if r[5] is not None:
             oe = otel.decision.estimate
-            assert r[4] == (oe.k_hat, oe.u, oe.f1, oe.f2, oe.saturated)
+            assert r[5] == (oe.k_hat, oe.u, oe.f1, oe.f2, oe.saturated)

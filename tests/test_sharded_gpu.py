@@ -40,7 +40,24 @@ def _cases():
         "ramp": (np.arange(-100_000, 100_000, dtype=np.int64), [100_000]),
         "small": (ogen.gen_input(1500, 50, 5).view(np.int64), [700]),
         "empty_shard": (main[:50_000], [50_000]),
+        "distinct_uneven": (ogen.distinct_values(300_000, 10).view(np.int64), [1_001]),
+        "skew": (_skew(), [100_001]),
+        "guard": (_guard_input(), [2_500_000]),
     }
+
+
+def _skew():
+    x = ogen.distinct_values(200_000, 11).view(np.int64).copy()
+    x[::2] = 123456789  # one bucket straddles both output slices
+    return x
+
+
+def _guard_input():
+    """More distinct keys than the device table holds, under a low estimate."""
+    n = 5_000_000
+    x = ogen.mix_outputs(77, n).view(np.int64).copy()
+    x[::n // 1024][:1024] = np.arange(1024, dtype=np.int64) % 100
+    return x
 
 
 def _worker(rank, world, port, name, q):
@@ -60,7 +77,7 @@ def _worker(rank, world, port, name, q):
         torch.cuda.synchronize()
         e = tel.decision.estimate
         q.put((rank, local.cpu().numpy(), tel.route.value, tel.tiny_count_failed,
-               None if e is None else (e.k_hat, e.u, e.f1, e.f2, e.saturated)))
+               None if e is None else (e.k_hat, e.u, e.f1, e.f2, e.saturated), tel.guard_fired))
     finally:
         dist.destroy_process_group()
 
@@ -90,6 +107,7 @@ def test_sharded_two_ranks_device_kernels(name):
     otel = orc.cafs_sort(x.copy())
     for r in res:
         assert r[2] == otel.route and r[3] == otel.tiny_count_failed
+        assert r[5] == (name == "guard")  # device guard: the distributed fallback ran
         if r[4] is not None:
             oe = otel.decision.estimate
             assert r[4] == (oe.k_hat, oe.u, oe.f1, oe.f2, oe.saturated)
