@@ -37,12 +37,14 @@ constexpr u32 kRange = 8192;              // dense window (u32 counters, 32 KB)
 constexpr int kSLog2 = 13;                // shared table: 8192 slots (64 KB keys + 32 KB counts)
 constexpr u32 kS = 1u << kSLog2;
 constexpr u32 kSClaimCap = kS / 2;        // claims stop at load 1/2 (short miss chains)
-constexpr int kSMaxProbe = 16;
+constexpr int kSMaxProbe = 4;             // a longer chain spills: the table is only a cache
+                                          // of partial counts, so a key found in two places
+                                          // (or in a slot and the spill) still sums right
 constexpr size_t kTableSmem = (size_t)kRange * 4 + (size_t)kS * 8 + (size_t)kS * 4;
-template <int STAGES, int STAGE_KEYS, int QCAP>
+template <int STAGES, int STAGE_KEYS, int QCAP, bool RANGE>
 constexpr size_t hc_smem() {
-  return kTableSmem + (size_t)STAGES * STAGE_KEYS * 8 + (size_t)32 * QCAP * 8 +
-         (size_t)2 * STAGES * 8 + 16;
+  return kTableSmem - (RANGE ? 0 : (size_t)kRange * 4) + (size_t)STAGES * STAGE_KEYS * 8 +
+         (size_t)32 * QCAP * 8 + (size_t)2 * STAGES * 8 + 16;
 }
 
 struct HcArgs {
@@ -124,7 +126,8 @@ __device__ __forceinline__ void resolve_or_spill(bool active, u64 v, u64* skeys,
 // QCAP > 0: first-probe misses are queued per warp and resolved 32 at a time
 // with the whole warp active (the slow path is otherwise run by a few lanes
 // of a diverged warp, leaving its L2 round trips unoverlapped).
-template <int STAGES, int STAGE_KEYS, int QCAP>
+// RANGE = false: no dense window (launched only when the window is closed).
+template <int STAGES, int STAGE_KEYS, int QCAP, bool RANGE>
 __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   if (!gate_open(a.ctl, a.gate)) return;
   constexpr int kConsumers = kHcThreads - 32;
@@ -134,8 +137,8 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   u64* stage = (u64*)smem;                                        // [STAGES][STAGE_KEYS]
   u64* skeys = stage + (size_t)STAGES * STAGE_KEYS;               // [kS]
   u32* scnt = (u32*)(skeys + kS);                                 // [kS]
-  u32* dcnt = scnt + kS;                                          // [kRange]
-  u64* queue = (u64*)(dcnt + kRange);                             // [32][QCAP]
+  u32* dcnt = scnt + kS;                                          // [kRange] if RANGE
+  u64* queue = (u64*)(dcnt + (RANGE ? kRange : 0));               // [32][QCAP]
   u64* full = queue + 32 * QCAP;                                  // [STAGES]
   u64* empty = full + STAGES;                                     // [STAGES]
   __shared__ u32 sclaims, sfill;
@@ -143,14 +146,15 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u64 flip = a.flip, mult = a.mult;
-  const u64 base = a.use_range ? a.ctl->range_base : 0ull;
-  const u64 rlen = a.use_range ? a.ctl->range_len : 0u;
+  const u64 base = (RANGE && a.use_range) ? a.ctl->range_base : 0ull;
+  const u64 rlen = (RANGE && a.use_range) ? a.ctl->range_len : 0u;
   // this CTA's spill region
   const u32 region_cap = (u32)(kSpillCap / gridDim.x);
   u64* region = a.spill + (u64)blockIdx.x * region_cap;
 
   for (u32 i = tid; i < kS; i += kHcThreads) { skeys[i] = kEmpty; scnt[i] = 0; }
-  for (u32 i = tid; i < kRange; i += kHcThreads) dcnt[i] = 0;
+  if (RANGE)
+    for (u32 i = tid; i < kRange; i += kHcThreads) dcnt[i] = 0;
   if (tid == 0) {
     sclaims = 0;
     sfill = 0;
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   // direct window or first shared probe; false = unresolved (slow path)
   auto fast = [&](u64 v) -> bool {
     const u64 d = v - base;
-    if (d < rlen) { atomicAdd(&dcnt[d], 1u); return true; }
+    if (RANGE && d < rlen) { atomicAdd(&dcnt[d], 1u); return true; }
     if (v == kEmpty) { empty_cnt++; return true; }
     const u32 h = mhash(v, mult, 64 - kSLog2);
     if (skeys[h] == v) { atomicAdd(&scnt[h], 1u); return true; }
@@ -190,13 +194,14 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   if (wid == 0) {
     // ---- TMA producer ----
     if (lane == 0) {
+      u32 s = 0, ph = 0;
       for (u64 it = 0; it < my_chunks; ++it) {
-        const u32 s = (u32)(it % STAGES);
-        if (it >= (u64)STAGES) mbar_wait(&empty[s], (u32)(((it / STAGES) - 1) & 1));
+        if (it >= (u64)STAGES) mbar_wait(&empty[s], ph ^ 1);
         const u64 off = (blockIdx.x + it * gridDim.x) * STAGE_KEYS;
         const u32 bytes = (u32)(((body - off) < STAGE_KEYS ? (body - off) : STAGE_KEYS) * 8);
         mbar_arrive_expect_tx(&full[s], bytes);
         tma_load_1d(stage + (size_t)s * STAGE_KEYS, xb + off, bytes, &full[s]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
   } else {
@@ -216,10 +221,11 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
         resolve_or_spill(true, u, skeys, scnt, &sclaims, &sfill, region, region_cap, a);
       }
     };
-    for (u64 it = 0; it < my_chunks; ++it) {
-      const u32 s = (u32)(it % STAGES);
-      mbar_wait(&full[s], (u32)((it / STAGES) & 1));
-      const u64 off = (blockIdx.x + it * gridDim.x) * STAGE_KEYS;
+    u32 s = 0, ph = 0;
+    u64 off = (u64)blockIdx.x * STAGE_KEYS;
+    const u64 off_step = (u64)gridDim.x * STAGE_KEYS;
+    for (u64 it = 0; it < my_chunks; ++it, off += off_step) {
+      mbar_wait(&full[s], ph);
       const u32 nv = (u32)(((body - off) < STAGE_KEYS ? (body - off) : STAGE_KEYS) / 2);
       const ulonglong2* sv = (const ulonglong2*)(stage + (size_t)s * STAGE_KEYS);
 #pragma unroll
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
         const u64 d0 = v0 - base, d1 = v1 - base;
         if (QCAP == 0) {
           if (valid) {
-            if (d0 < rlen && d1 < rlen) {
+            if (RANGE && d0 < rlen && d1 < rlen) {
               atomicAdd(&dcnt[d0], 1u);
               atomicAdd(&dcnt[d1], 1u);
             } else {
@@ -243,7 +249,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
         } else {
           bool m0 = false, m1 = false;
           if (valid) {
-            if (d0 < rlen && d1 < rlen) {
+            if (RANGE && d0 < rlen && d1 < rlen) {
               atomicAdd(&dcnt[d0], 1u);
               atomicAdd(&dcnt[d1], 1u);
             } else {
@@ -257,6 +263,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == STAGES) { s = 0; ph ^= 1; }
     }
     if (QCAP > 0) {
       __syncwarp();
@@ -271,7 +278,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   __syncthreads();
 
   // ---- flush the CTA's shared cells into the global table ----
-  for (u32 d = tid; d < (u32)rlen; d += kHcThreads) {
+  for (u32 d = tid; RANGE && d < (u32)rlen; d += kHcThreads) {
     const u32 c = dcnt[d];
     if (c) atomicAdd(&a.dense[d], (u64)c);  // key base + d: no hashing, no claims
   }
@@ -530,24 +537,24 @@ void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevC
                                                          glist);
 }
 
-size_t hash_count_smem() { return hc_smem<3, 3968, 0>(); }
+size_t hash_count_smem() { return hc_smem<3, 3968, 0, true>(); }
 
-template <int ST, int SK, int QC>
+template <int ST, int SK, int QC, bool RG>
 static cudaError_t launch_hc(const HcArgs& a, u64 n, int num_sms, cudaStream_t st) {
-  constexpr size_t sm = hc_smem<ST, SK, QC>();
+  constexpr size_t sm = hc_smem<ST, SK, QC, RG>();
   static_assert(sm <= 232448 - 2048, "shared memory budget");
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(hash_count_kernel<ST, SK, QC>,
+    cudaError_t e = cudaFuncSetAttribute(hash_count_kernel<ST, SK, QC, RG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
   const u64 chunks = (n + SK - 1) / SK;
   const int grid = (int)(chunks < (u64)num_sms ? (chunks ? chunks : 1) : (u64)num_sms);
-  hash_count_kernel<ST, SK, QC><<<grid, kHcThreads, sm, st>>>(a);
+  hash_count_kernel<ST, SK, QC, RG><<<grid, kHcThreads, sm, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -564,19 +571,23 @@ static int hc_variant() {
 }
 
 // variant: 0 = dense-window shape (deep TMA ring, inline slow path),
-//          1 = queued shape (smaller ring + per-warp miss queues)
+//          1 = queued shape (per-warp miss queues); without the window when the
+//              caller guarantees it is closed (gate kGateMainHash, or use_range 0)
 cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms,
                               cudaStream_t st, int variant, int gate, u64* spill, u64* dense) {
   HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate, spill, dense};
+  const bool window = use_range && gate != kGateMainHash;
   int v = hc_variant();
-  if (v < 0) v = variant == 0 ? 0 : 2;
+  if (v < 0) v = variant == 0 ? 0 : (window ? 2 : 5);
+  if (!window && v == 0) v = 5;
+  if (window && v == 5) v = 2;
   switch (v) {
-    case 1: return launch_hc<2, 3968, 64>(a, n, num_sms, st);
-    case 2: return launch_hc<3, 1984, 64>(a, n, num_sms, st);  // queued default
-    case 3: return launch_hc<6, 1984, 0>(a, n, num_sms, st);
-    case 4: return launch_hc<4, 1984, 64>(a, n, num_sms, st);
-    default: return launch_hc<3, 3968, 0>(a, n, num_sms, st);
+    case 2: return launch_hc<3, 1984, 64, true>(a, n, num_sms, st);   // queued, window
+    case 3: return launch_hc<2, 5952, 64, false>(a, n, num_sms, st);
+    case 4: return launch_hc<4, 1984, 64, false>(a, n, num_sms, st);
+    case 5: return launch_hc<3, 3968, 64, false>(a, n, num_sms, st);  // queued default
+    default: return launch_hc<3, 3968, 0, true>(a, n, num_sms, st);   // dense window
   }
 }
 

@@ -24,6 +24,10 @@ constexpr int kBsWarps = kBsThreads / 32;
 constexpr u32 kBucketCap = 4096;                       // keys per bucket sorted in smem
 constexpr int kBsRounds = kBucketCap / kBsThreads;     // 16 rounds of 32 per warp
 constexpr u32 kWarpBucketMax = 128;                    // buckets sorted by one warp
+constexpr int kSubBits = 10;                           // second-level split inside a bucket
+constexpr u32 kSubBins = 1u << kSubBits;               // (fits the 8 x 256 warp counters)
+constexpr u32 kSubMax = 64;                            // largest sub-bucket rank-sorted
+static_assert(2 * kSubBins <= kBsWarps * 256, "sub-bucket counters live in the warp counters");
 constexpr int kScThreads = 256;
 constexpr int kScItems = 16;                           // keys per thread in the scatter
 constexpr u64 kScChunk = (u64)kScThreads * kScItems;   // 4096
@@ -268,6 +272,81 @@ __global__ void __launch_bounds__(kBsThreads)
   vor = 0; vand = ~0ull;
   for (int w = 0; w < kBsWarps; ++w) { vor |= red_or[w]; vand &= red_and[w]; }
   const u64 vary = vor ^ vand;
+  // ---- two-level path: split the bucket on its kSubBits highest varying bits
+  // (shared-memory counting sort), then rank-sort each sub-bucket -- a few
+  // keys each when the keys are spread -- instead of up to 7 byte passes.
+  // Buckets with a sub-bucket over kSubMax keys (clustered or repeated keys)
+  // take the LSD passes below.
+  if (vary != 0) {
+    const int hb = 63 - __clzll(vary);
+    const int nbits = hb + 1 < kSubBits ? hb + 1 : kSubBits;
+    const int sh = hb + 1 - nbits;
+    const u32 dmask = (1u << nbits) - 1;
+    u32* h2 = &wcnt[0][0];          // [kSubBins] counts, then sub-bucket starts
+    u32* c2 = h2 + kSubBins;        // [kSubBins] scatter cursors
+    __shared__ u32 maxsub;
+    for (u32 i = tid; i < kSubBins; i += kBsThreads) h2[i] = 0;
+    if (tid == 0) maxsub = 0;
+    __syncthreads();
+    for (u32 i = tid; i < n; i += kBsThreads) atomicAdd(&h2[(u32)(kb[0][i] >> sh) & dmask], 1u);
+    __syncthreads();
+    {  // exclusive scan of the kSubBins counts (kSubBins / kBsThreads per thread)
+      constexpr int PT = kSubBins / kBsThreads;
+      u32 c[PT], loc = 0, mx = 0;
+#pragma unroll
+      for (int q = 0; q < PT; ++q) {
+        c[q] = h2[tid * PT + q];
+        loc += c[q];
+        mx = c[q] > mx ? c[q] : mx;
+      }
+      u32 incl = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const u32 t = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = t > mx ? t : mx;
+      }
+      if (lane == 31) wsum8[wid] = incl;
+      if (lane == 0) atomicMax(&maxsub, mx);
+      __syncthreads();
+      u32 run = incl - loc;
+      for (int w = 0; w < wid; ++w) run += wsum8[w];
+#pragma unroll
+      for (int q = 0; q < PT; ++q) {
+        h2[tid * PT + q] = run;
+        c2[tid * PT + q] = run;
+        run += c[q];
+      }
+    }
+    __syncthreads();
+    if (maxsub <= kSubMax) {
+      for (u32 i = tid; i < n; i += kBsThreads) {
+        const u64 k = kb[0][i];
+        const u32 p = atomicAdd(&c2[(u32)(k >> sh) & dmask], 1u);
+        kb[1][p] = k;
+        if (HAS_VAL) ib[1][p] = ib[0][i];
+      }
+      __syncthreads();
+      for (u32 p = tid; p < n; p += kBsThreads) {
+        const u64 k = kb[1][p];
+        const u32 d = (u32)(k >> sh) & dmask;
+        const u32 s0 = h2[d], e0 = d < dmask ? h2[d + 1] : n;
+        u32 r = 0;
+        for (u32 j = s0; j < e0; ++j) {
+          const u64 kj = kb[1][j];
+          r += (kj < k) || (kj == k && j < p);
+        }
+        dk[base + s0 + r] = k ^ flip;
+        if (HAS_VAL) dv[base + s0 + r] = tv[base + ib[1][p]];
+      }
+      return;
+    }
+    __syncthreads();  // the LSD passes reuse wcnt
+  }
   // warp-contiguous segments of whole rounds
   const u32 rounds = ((n + 31) / 32 + kBsWarps - 1) / kBsWarps;  // rounds per warp
   const u32 w0 = wid * rounds * 32;

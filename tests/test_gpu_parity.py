@@ -246,7 +246,7 @@ def test_tiny_count_sort_semantics():
                              np.zeros(4, np.uint64))
 
 
-@pytest.mark.parametrize("n", [1, 5, 255, 256, 8192, 8193, 100_000])
+@pytest.mark.parametrize("n", [1, 5, 255, 256, 8192, 8193, 100_000, 1_500_000])
 def test_pair_sort_and_emit(n):
     rng = np.random.default_rng(n)
     keys = np.unique(rng.integers(0, 1 << 64, n, dtype=np.uint64))
@@ -263,12 +263,27 @@ def test_pair_sort_and_emit(n):
 
 
 def test_fallback_sort_large_random():
-    for n in (8191, 8192, 8193, 1_000_003):
+    for n in (8191, 8192, 8193, 1_000_003, 12_000_000):
         x = ogen.mix_outputs(n, n).view(np.int64)
         want = np.sort(x)
         t = to_dev(x)
         cafs.fallback_sort(t)
         assert np.array_equal(t.cpu().numpy(), want)
+
+
+def test_fallback_sort_clustered_and_repeated():
+    """Buckets whose sub-buckets are large (repeats, clusters) take the byte passes."""
+    rng = np.random.default_rng(12)
+    n = 4_000_000
+    x = ogen.mix_outputs(21, n).view(np.int64).copy()
+    x[rng.integers(0, n, n // 3)] = 77                      # one heavy key
+    x[rng.integers(0, n, n // 5)] = rng.integers(0, 3000, n // 5) << 20  # low-entropy cluster
+    for arr in (x, x.view(np.uint64)):
+        want = np.sort(arr)
+        t = torch.from_numpy(arr.copy()).cuda() if arr.dtype == np.int64 else arr.copy()
+        cafs.fallback_sort(t)
+        got = t.cpu().numpy() if isinstance(t, torch.Tensor) else t
+        assert np.array_equal(got, want)
 
 
 def test_guard_reroutes_to_fallback():
