@@ -261,7 +261,7 @@ int sort_pairs_large(cafs_ctx_t* ctx, u64 np, cudaStream_t st) {
 int try_msd(cafs_ctx_t* ctx, const u64* keys, const u64* vals, u64 n, u64 flip, u64* tk, u64* tv,
             u64* dk, u64* dv, cudaStream_t st, bool* done) {
   *done = false;
-  launch_msd_count(keys, n, flip, ctx->msd, ctx->num_sms, st);
+  if (!launch_msd_count(keys, n, flip, ctx->msd, ctx->num_sms, st)) return CAFS_OK;  // LSD
   ctx->launches += 3;
   CKL();
   CK(cudaMemcpyAsync(ctx->h_scratch, (char*)ctx->msd + msd_maxb_offset(), sizeof(u32),
@@ -269,7 +269,7 @@ int try_msd(cafs_ctx_t* ctx, const u64* keys, const u64* vals, u64 n, u64 flip, 
   CK(cudaStreamSynchronize(st));
   const u32 maxb = (u32)ctx->h_scratch[0];
   if (maxb > msd_bucket_cap()) return CAFS_OK;
-  launch_msd_sort(keys, vals, n, flip, ctx->msd, tk, tv, dk, dv, maxb, st);
+  launch_msd_sort(keys, vals, n, flip, ctx->msd, tk, tv, dk, dv, maxb, ctx->num_sms, st);
   ctx->launches += maxb > 128 ? 3 : 2;
   CKL();
   *done = true;

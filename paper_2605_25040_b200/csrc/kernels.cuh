@@ -60,9 +60,9 @@ size_t msd_hist_offset();
 void launch_msd_span(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st);
 void launch_msd_partition(const u64* keys, u64 n, u64 flip, void* state, u64 vor, u64 vand,
                           u64* out, int num_sms, cudaStream_t st);
-void launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st);
+bool launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st);
 void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* state, u64* tk,
-                     u64* tv, u64* dk, u64* dv, u32 maxb, cudaStream_t st);
+                     u64* tv, u64* dk, u64* dv, u32 maxb, int num_sms, cudaStream_t st);
 // telemetry.cu
 size_t tel_accum_bytes();
 void launch_tel_build(const u64* keys, u64 np, u64* tkeys, u32* tidx, int log2s, u32* first,

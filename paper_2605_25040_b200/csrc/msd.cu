@@ -32,6 +32,11 @@ constexpr int kScThreads = 256;
 constexpr int kScItems = 16;                           // keys per thread in the scatter
 constexpr u64 kScChunk = (u64)kScThreads * kScItems;   // 4096
 
+// The sort's scatter gives each chunk of keys a fixed slice of every bucket
+// (reserved by the histogram kernel), so it writes without global atomics.
+constexpr u32 kMsdMaxChunks = 512;
+constexpr u64 kMsdMaxN = (u64)kMsdBuckets * kBucketCap;  // beyond: some bucket > kBucketCap
+
 struct MsdState {
   unsigned long long vor, vand;
   u32 hist[kMsdBuckets];
@@ -39,7 +44,18 @@ struct MsdState {
   u32 cursor[kMsdBuckets];
   u32 maxb;
   int shift;
+  u32 offs[kMsdMaxChunks][kMsdBuckets];  // chunk c's offset inside bucket b (not memset)
 };
+constexpr size_t kMsdClear = offsetof(MsdState, offs);
+
+// keys per chunk: about two chunks per SM, a multiple of 4096, at most 64K
+static u64 msd_chunk(u64 n, int num_sms) {
+  u64 c = (n + 2ull * num_sms - 1) / (2ull * num_sms);
+  c = (c + 4095) & ~4095ull;
+  if (c < 4096) c = 4096;
+  if (c > 65536) c = 65536;
+  return c;
+}
 
 __device__ __forceinline__ u32 msd_digit(u64 k, int shift) {
   return (u32)(k >> shift) & (kMsdBuckets - 1);
@@ -49,7 +65,14 @@ __global__ void __launch_bounds__(512) msd_reduce_kernel(const u64* __restrict__
                                                          u64 flip, MsdState* ms) {
   u64 vor = 0, vand = ~0ull;
   const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += stride) {
+  u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {  // four loads in flight per thread
+    const u64 a = keys[i] ^ flip, b = keys[i + stride] ^ flip, c = keys[i + 2 * stride] ^ flip,
+              d = keys[i + 3 * stride] ^ flip;
+    vor |= a | b | c | d;
+    vand &= a & b & c & d;
+  }
+  for (; i < n; i += stride) {
     const u64 k = keys[i] ^ flip;
     vor |= k;
     vand &= k;
@@ -131,6 +154,79 @@ __global__ void __launch_bounds__(1024) msd_scan_kernel(MsdState* ms) {
   }
   if (tid == 1023) ms->base[kMsdBuckets] = run;
   if (tid == 0) ms->shift = msd_shift(ms);
+}
+
+// Chunk histograms (the sort's first pass after the span): chunk c counts its
+// keys per bucket in shared memory, then reserves its slice of every bucket
+// with one atomic per non-empty bucket; offs[c][b] = that slice's offset,
+// hist[b] = the bucket's total.
+__global__ void __launch_bounds__(1024) msd_chunk_hist_kernel(const u64* __restrict__ keys, u64 n,
+                                                              u64 flip, MsdState* ms, u64 chunk) {
+  __shared__ u32 h[kMsdBuckets];
+  for (u32 i = threadIdx.x; i < kMsdBuckets; i += 1024) h[i] = 0;
+  __syncthreads();
+  const int shift = msd_shift(ms);
+  const u64 c0 = blockIdx.x * chunk;
+  const u64 c1 = c0 + chunk < n ? c0 + chunk : n;
+  u64 i = c0 + threadIdx.x;
+  for (; i + 3 * 1024 < c1; i += 4 * 1024) {
+    const u64 a = keys[i], b = keys[i + 1024], c = keys[i + 2048], d = keys[i + 3072];
+    atomicAdd(&h[msd_digit(a ^ flip, shift)], 1u);
+    atomicAdd(&h[msd_digit(b ^ flip, shift)], 1u);
+    atomicAdd(&h[msd_digit(c ^ flip, shift)], 1u);
+    atomicAdd(&h[msd_digit(d ^ flip, shift)], 1u);
+  }
+  for (; i < c1; i += 1024) atomicAdd(&h[msd_digit(keys[i] ^ flip, shift)], 1u);
+  __syncthreads();
+  u32* row = ms->offs[blockIdx.x];
+  for (u32 b = threadIdx.x; b < kMsdBuckets; b += 1024) {
+    const u32 c = h[b];
+    row[b] = c ? atomicAdd(&ms->hist[b], c) : 0u;
+  }
+}
+
+// Scatter with the reserved slices: position = bucket base + chunk offset +
+// the key's rank among the chunk's keys of that bucket (shared atomics; order
+// inside a bucket is not preserved -- the bucket sort follows).
+template <bool HAS_VAL>
+__global__ void __launch_bounds__(1024)
+    msd_scatter_chunk_kernel(const u64* __restrict__ keys, const u64* __restrict__ vals, u64 n,
+                             u64 flip, const MsdState* ms, u64 chunk, u64* __restrict__ tk,
+                             u64* __restrict__ tv) {
+  __shared__ u32 lc[kMsdBuckets];
+  __shared__ u32 gb[kMsdBuckets];
+  const u32* row = ms->offs[blockIdx.x];
+  for (u32 b = threadIdx.x; b < kMsdBuckets; b += 1024) {
+    lc[b] = 0;
+    gb[b] = ms->base[b] + row[b];
+  }
+  __syncthreads();
+  const int shift = ms->shift;
+  const u64 c0 = blockIdx.x * chunk;
+  const u64 c1 = c0 + chunk < n ? c0 + chunk : n;
+  u64 i = c0 + threadIdx.x;
+  for (; i + 3 * 1024 < c1; i += 4 * 1024) {
+    u64 k[4], v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      k[j] = keys[i + j * 1024] ^ flip;
+      if (HAS_VAL) v[j] = vals[i + j * 1024];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const u32 d = msd_digit(k[j], shift);
+      const u32 pos = gb[d] + atomicAdd(&lc[d], 1u);
+      tk[pos] = k[j];
+      if (HAS_VAL) tv[pos] = v[j];
+    }
+  }
+  for (; i < c1; i += 1024) {
+    const u64 k = keys[i] ^ flip;
+    const u32 d = msd_digit(k, shift);
+    const u32 pos = gb[d] + atomicAdd(&lc[d], 1u);
+    tk[pos] = k;
+    if (HAS_VAL) tv[pos] = vals[i];
+  }
 }
 
 // Scatter a 4096-key chunk into its buckets: local counts (shared atomics give
@@ -440,16 +536,23 @@ __global__ void __launch_bounds__(kBsThreads)
 size_t msd_state_bytes() { return sizeof(MsdState); }
 u32 msd_bucket_cap() { return kBucketCap; }
 
-void launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st) {
+// false: the keys cannot all fit kBucketCap-sized buckets (n too large)
+bool launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms,
+                      cudaStream_t st) {
+  if (n > kMsdMaxN) return false;
+  const u64 chunk = msd_chunk(n, num_sms);
+  const u64 nchunks = (n + chunk - 1) / chunk;
+  if (nchunks > kMsdMaxChunks) return false;
   MsdState* ms = (MsdState*)state;
-  cudaMemsetAsync(ms, 0, sizeof(MsdState), st);
+  cudaMemsetAsync(ms, 0, kMsdClear, st);
   cudaMemsetAsync(&ms->vand, 0xFF, sizeof(u64), st);
   u64 blocks = (n + 512 * 8 - 1) / (512 * 8);
   if (blocks > (u64)num_sms * 4) blocks = (u64)num_sms * 4;
   if (blocks < 1) blocks = 1;
   msd_reduce_kernel<<<(unsigned)blocks, 512, 0, st>>>(keys, n, flip, ms);
-  msd_hist_kernel<<<(unsigned)blocks, 512, 0, st>>>(keys, n, flip, ms);
+  msd_chunk_hist_kernel<<<(unsigned)nchunks, 1024, 0, st>>>(keys, n, flip, ms, chunk);
   msd_scan_kernel<<<1, 1024, 0, st>>>(ms);
+  return true;
 }
 
 __global__ void msd_set_span_kernel(MsdState* ms, u64 vor, u64 vand) {
@@ -461,7 +564,7 @@ __global__ void msd_set_span_kernel(MsdState* ms, u64 vor, u64 vand) {
 // them to fix one bucket digit for every rank).
 void launch_msd_span(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st) {
   MsdState* ms = (MsdState*)state;
-  cudaMemsetAsync(ms, 0, sizeof(MsdState), st);
+  cudaMemsetAsync(ms, 0, kMsdClear, st);
   cudaMemsetAsync(&ms->vand, 0xFF, sizeof(u64), st);
   u64 blocks = (n + 512 * 8 - 1) / (512 * 8);
   if (blocks > (u64)num_sms * 4) blocks = (u64)num_sms * 4;
@@ -476,7 +579,7 @@ size_t msd_hist_offset() { return offsetof(MsdState, hist); }
 void launch_msd_partition(const u64* keys, u64 n, u64 flip, void* state, u64 vor, u64 vand,
                           u64* out, int num_sms, cudaStream_t st) {
   MsdState* ms = (MsdState*)state;
-  cudaMemsetAsync(ms, 0, sizeof(MsdState), st);
+  cudaMemsetAsync(ms, 0, kMsdClear, st);
   msd_set_span_kernel<<<1, 1, 0, st>>>(ms, vor, vand);
   u64 blocks = (n + 512 * 8 - 1) / (512 * 8);
   if (blocks > (u64)num_sms * 4) blocks = (u64)num_sms * 4;
@@ -496,9 +599,10 @@ size_t msd_maxb_offset() { return offsetof(MsdState, maxb); }
 constexpr size_t kBsSmem = (size_t)kBucketCap * (16 + 4) + (size_t)kBsWarps * 256 * 4;
 
 void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* state, u64* tk,
-                     u64* tv, u64* dk, u64* dv, u32 maxb, cudaStream_t st) {
+                     u64* tv, u64* dk, u64* dv, u32 maxb, int num_sms, cudaStream_t st) {
   MsdState* ms = (MsdState*)state;
-  const u64 chunks = (n + kScChunk - 1) / kScChunk;
+  const u64 chunk = msd_chunk(n, num_sms);
+  const u64 chunks = (n + chunk - 1) / chunk;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -511,14 +615,14 @@ void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* st
   }
   const bool large = maxb > kWarpBucketMax;
   if (vals) {
-    msd_scatter_kernel<true><<<(unsigned)chunks, kScThreads, 0, st>>>(keys, vals, n, flip, ms, tk,
-                                                                      tv);
+    msd_scatter_chunk_kernel<true><<<(unsigned)chunks, 1024, 0, st>>>(keys, vals, n, flip, ms,
+                                                                      chunk, tk, tv);
     bucket_small_kernel<true><<<kMsdBuckets / 8, 256, 0, st>>>(tk, tv, ms, flip, dk, dv);
     if (large)
       bucket_sort_kernel<true><<<kMsdBuckets, kBsThreads, kBsSmem, st>>>(tk, tv, ms, flip, dk, dv);
   } else {
-    msd_scatter_kernel<false><<<(unsigned)chunks, kScThreads, 0, st>>>(keys, nullptr, n, flip, ms,
-                                                                       tk, nullptr);
+    msd_scatter_chunk_kernel<false><<<(unsigned)chunks, 1024, 0, st>>>(keys, nullptr, n, flip,
+                                                                       ms, chunk, tk, nullptr);
     bucket_small_kernel<false><<<kMsdBuckets / 8, 256, 0, st>>>(tk, nullptr, ms, flip, dk,
                                                                nullptr);
     if (large)

@@ -271,6 +271,16 @@ def test_fallback_sort_large_random():
         assert np.array_equal(t.cpu().numpy(), want)
 
 
+def test_fallback_sort_few_negative_keys():
+    """The key span must see a handful of sign changes among millions of keys."""
+    x = (ogen.mix_outputs(31, 3_000_000) >> np.uint64(1)).view(np.int64).copy()
+    x[[5, 1_000_001, 2_999_998]] = [-1, -(1 << 62), -7]
+    want = np.sort(x)
+    t = to_dev(x)
+    cafs.fallback_sort(t)
+    assert np.array_equal(t.cpu().numpy(), want)
+
+
 def test_fallback_sort_clustered_and_repeated():
     """Buckets whose sub-buckets are large (repeats, clusters) take the byte passes."""
     rng = np.random.default_rng(12)
