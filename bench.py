@@ -282,12 +282,22 @@ def main():
     if k_est:
         kernels["estimate"] = {"kernel": "estimate_kernel", "avg_ms": sum(k_est) / len(k_est),
                                "share_of_step": sum(k_est) / len(k_est) / (tot_ms / args.steps)}
+    if route and route.startswith("fallback"):
+        # the fallback sort is a sequence of kernels (span, chunk histogram,
+        # scatter, bucket sorts); its stage time against one read + one write
+        k_sort = [t.stage_ms.get("sort_k") for t in tels if "sort_k" in t.stage_ms]
+        if k_sort:
+            avg = sum(k_sort) / len(k_sort)
+            kernels["sort"] = {"kernel": "fallback sort stage (msd_* + bucket_*)", "avg_ms": avg,
+                               "GB/s": n_local * 16 / (avg / 1e3) / 1e9,
+                               "share_of_step": avg / (tot_ms / args.steps)}
     if any("GB/s" in v for v in kernels.values()):
         dom = max((k for k in kernels if "GB/s" in kernels[k]), key=lambda k: kernels[k]["avg_ms"])
         d = kernels[dom]
         roof = {"bound": "hbm", "kernel": d["kernel"], "achieved": d["GB/s"], "peak": peak,
                 "unit": "GB/s", "frac": d["GB/s"] / peak, "traffic": ncu_traffic(args.config, d["kernel"]),
-                "algorithmic_bytes_per_launch": n_local * 8, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": n_local * (16 if dom == "sort" else 8),
+                "peak_source": peak_src,
                 "step_frac": (16 * N / (tot_ms / args.steps / 1e3) / 1e9) / world / peak,
                 "kernels": kernels}
 
