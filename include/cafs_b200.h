@@ -198,6 +198,11 @@ int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_s
                        uint64_t g_or, uint64_t g_and, int64_t* d_out, uint64_t* h_counts,
                        void* stream);
 
+/* Kernels this context has launched since it was created (monotone; the
+ * per-call count of cafs_sort_i64 is also in cafs_telemetry_t.kernels_launched).
+ * No reference counterpart: launch accounting for the multi-GPU bench. */
+uint64_t cafs_ctx_kernel_count(const cafs_ctx_t* ctx);
+
 /* ---- synthetic inputs (bench / tests; bit-identical to oracle/gen.py) ---- */
 /* out[i] = fmix64(seed + (skip + i + 1) * 0x9E3779B97F4A7C15) */
 int cafs_gen_mix(uint64_t* d_out, uint64_t count, uint64_t seed, uint64_t skip, void* stream);

@@ -73,6 +73,7 @@ SIGNATURES = {
     "cafs_pair_sort": (_I, [_P, _P, _P, _U64, _P]),
     "cafs_emit_i64": (_I, [_P, _P, _P, _U64, _P, _U64, _U64, _U64, _I, _P]),
     "cafs_fallback_sort_i64": (_I, [_P, _P, _U64, _I, _P]),
+    "cafs_ctx_kernel_count": (_U64, [_P]),
     "cafs_key_span_i64": (_I, [_P, _P, _U64, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), _P]),
     "cafs_partition_i64": (_I, [_P, _P, _U64, _I, _U64, _U64, _P, ctypes.POINTER(_U64), _P]),
     "cafs_gen_mix": (_I, [_P, _U64, _U64, _U64, _P]),

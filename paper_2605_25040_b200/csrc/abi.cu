@@ -74,7 +74,7 @@ struct cafs_ctx {
   int32_t* h_scratch = nullptr;  // pinned (64 B + a partition histogram)
   cudaEvent_t ev[32] = {};
   std::string last_error;
-  uint32_t launches = 0;
+  uint64_t launches = 0;  // kernels this context has launched (monotone)
   // CUDA Graphs of the fused pipeline (estimate + gated route kernels), keyed by
   // the call's arguments; captured on the second call with the same key
   cudaStream_t cap_stream = nullptr;
@@ -85,7 +85,7 @@ struct cafs_ctx {
     int seen = 0;
     cudaGraphExec_t exec = nullptr;
     int tn = 0, mark = 0, label[16] = {}, cond[16] = {};
-    uint32_t launches = 0;
+    uint64_t launches = 0;  // kernels this context has launched (monotone)
     uint64_t stamp = 0;
   } graphs[16];
   uint64_t graph_clock = 0;
@@ -723,7 +723,7 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
   if ((hash_mult & 1) == 0) return fail(ctx, CAFS_EINVAL, "hash multiplier must be odd");
   DeviceGuard g(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
-  ctx->launches = 0;
+  const uint64_t launches0 = ctx->launches;
   cafs_telemetry_t local;
   const bool want_tel = tel != nullptr;
   if (!tel) tel = &local;
@@ -828,7 +828,7 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
     tel->exact = 1;
     tel->ref_counted_total = tel->counted_total;
   }
-  tel->kernels_launched = ctx->launches;
+  tel->kernels_launched = (uint32_t)(ctx->launches - launches0);
   return CAFS_OK;
 }
 
@@ -875,6 +875,7 @@ int cafs_estimate_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_si
   DeviceGuard g(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
   launch_estimate((const u64*)d_x, n, is_signed ? kSign : 0, 0, ctx->d_ctl, st);
+  ctx->launches++;
   CKL();
   TRY(sync_ctl(ctx, st));
   cafs_decision_t d;
@@ -938,6 +939,7 @@ int cafs_tiny_counts_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   if (n)
     launch_tiny_count((const u64*)d_x, n, is_signed ? kSign : 0, ctx->d_ctl, ctx->num_sms, st,
                       kGateNone);
+  ctx->launches += n ? 1 : 0;
   CKL();
   TRY(sync_ctl(ctx, st));
   for (int j = 0; j < nk; ++j) h_counts[j] = (int64_t)ctx->h_ctl->tiny_counts[c.tiny_slot[map[j]]];
@@ -968,6 +970,7 @@ int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
                      ctx->poffs, n, st, kGateNone);
   e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, n, ctx->pk_b, ctx->pc_b,
                               ctx->poffs, st, kGateNone);
+  ctx->launches += 6;
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   TRY(sync_ctl(ctx, st));
   DevCtl c = *ctx->h_ctl;
@@ -1001,6 +1004,7 @@ int cafs_merge_pairs(cafs_ctx_t* ctx, const uint64_t* d_keys_in, const uint64_t*
                  ctx->num_sms, st, kGateNone);
   cudaError_t e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, ~0ull, ctx->pk_b,
                                           ctx->pc_b, ctx->poffs, st, kGateNone);
+  ctx->launches += 4;
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   CKL();
   TRY(sync_ctl(ctx, st));
@@ -1034,6 +1038,7 @@ int cafs_pair_sort(cafs_ctx_t* ctx, uint64_t* d_keys, uint64_t* d_counts, uint64
     CK(cudaMemcpyAsync(ctx->pc_a, d_counts, npairs * 8, cudaMemcpyDeviceToDevice, st));
     cudaError_t e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, npairs, nullptr, 0, (u64*)d_keys,
                                             (u64*)d_counts, ctx->poffs, st, kGateNone);
+    ctx->launches++;
     if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   } else {
     TRY(ensure_radix(ctx, npairs, false));
@@ -1062,9 +1067,12 @@ int cafs_emit_i64(cafs_ctx_t* ctx, const uint64_t* d_keys, const uint64_t* d_cou
   memset(&c, 0, sizeof(c));
   CK(cudaMemcpyAsync(ctx->d_ctl, &c, sizeof(DevCtl), cudaMemcpyHostToDevice, st));
   launch_scan((const u64*)d_counts, npairs, ctx->bsum, ctx->poffs, ctx->d_ctl, total, st);
-  if (npairs && out_end > out_begin)
+  ctx->launches += 3;
+  if (npairs && out_end > out_begin) {
     launch_emit((const u64*)d_keys, ctx->poffs, 0, ctx->d_ctl, (u64*)d_out, out_begin, out_end,
                 is_signed ? kSign : 0, ctx->num_sms, st, npairs);
+    ctx->launches++;
+  }
   CKL();
   TRY(sync_ctl(ctx, st));
   if (ctx->h_ctl->sum_error)
@@ -1093,6 +1101,7 @@ int cafs_key_span_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_si
   cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_radix(ctx, n, false));
   launch_msd_span((const u64*)d_x, n, is_signed ? kSign : 0, ctx->msd, ctx->num_sms, st);
+  ctx->launches++;
   CKL();
   CK(cudaMemcpyAsync(ctx->h_scratch, (char*)ctx->msd + msd_span_offset(), 16,
                      cudaMemcpyDeviceToHost, st));
@@ -1117,6 +1126,7 @@ int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_s
   TRY(ensure_radix(ctx, n, false));
   launch_msd_partition((const u64*)d_x, n, flip, ctx->msd, g_or, g_and, (u64*)d_out,
                        ctx->num_sms, st);
+  ctx->launches += 4;
   CKL();
   const u32* hc = (const u32*)ctx->h_scratch;  // pinned, 64 + 4096 x 4 bytes
   cudaError_t e = cudaMemcpyAsync(ctx->h_scratch, (char*)ctx->msd + msd_hist_offset(),
@@ -1127,6 +1137,8 @@ int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_s
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "partition", e);
   return CAFS_OK;
 }
+
+uint64_t cafs_ctx_kernel_count(const cafs_ctx_t* ctx) { return ctx ? ctx->launches : 0; }
 
 int cafs_gen_mix(uint64_t* d_out, uint64_t count, uint64_t seed, uint64_t skip, void* stream) {
   if (count && !d_out) return CAFS_EINVAL;

@@ -78,6 +78,10 @@ class DeviceOps:
     def _stream(self):
         return _torch().cuda.current_stream(self.device).cuda_stream
 
+    def kernel_count(self) -> int:
+        """Kernels launched so far by this rank's context (C ABI accounting)."""
+        return int(self.lib.cafs_ctx_kernel_count(self.ctx))
+
     def is_monotone(self, x) -> bool:
         if x.shape[0] < 2:
             return True
@@ -320,6 +324,16 @@ def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTeleme
         signed = ops.signed if signed is None else signed
     comm = Comm(group, x_local.device if x_local.is_cuda else None)
     tel = telemetry if telemetry is not None else SortTelemetry()
+    k0 = ops.kernel_count() if hasattr(ops, "kernel_count") else 0
+    try:
+        _sort_sharded(x_local, comm, ops, tel, mult, signed)
+    finally:
+        if hasattr(ops, "kernel_count"):
+            tel.kernels_launched = ops.kernel_count() - k0
+
+
+def _sort_sharded(x_local, comm, ops, tel, mult: int, signed: bool) -> None:
+    torch = _torch()
     flip = _SIGN if signed else 0
 
     # ---- global shape ----

@@ -24,7 +24,7 @@ def lib():
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(cafs_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|uint64_t|const char\*)\s+(cafs_\w+)\(", text, re.M)))
 
 
 def test_header_declares_the_abi():

@@ -75,6 +75,7 @@ def _worker(rank, world, port, name, q):
         tel = SortTelemetry()
         cafs_sort_sharded(local, telemetry=tel)
         torch.cuda.synchronize()
+        assert tel.kernels_launched > 0  # the device kernels ran (C ABI accounting)
         e = tel.decision.estimate
         q.put((rank, local.cpu().numpy(), tel.route.value, tel.tiny_count_failed,
                None if e is None else (e.k_hat, e.u, e.f1, e.f2, e.saturated), tel.guard_fired))
