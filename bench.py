@@ -178,6 +178,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=1 << 24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-direct", action="store_true", help="disable the dense-range count path")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU code path (NCCL) even at one rank")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -194,8 +196,13 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = datagen.CONFIGS[args.config]
     N = cfg.n
@@ -211,7 +218,7 @@ def main():
             dist.barrier()
 
     def one_step(tel):
-        if world == 1:
+        if not sharded:
             cafs.cafs_sort(x, telemetry=tel, direct_range=not args.no_direct)
         else:
             cafs_sort_sharded(x, telemetry=tel)
@@ -342,7 +349,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "int64",
             "data": f"synthetic, device-generated ({cfg.desc}; seed {cfg.seed})",
             "config": {"workload": args.config, "n": N, "k": cfg.k, "dist": cfg.dist, "s": cfg.s,
-                       "route": route, "parallelism": f"rows sharded x{world}",
+                       "route": route, "parallelism": f"rows sharded x{world}" + (" (sharded path)" if sharded else ""),
                        "l2": "input 8 B x N >> 126 MB L2; unsorted input restored by an untimed "
                              "D2D copy before each step",
                        "direct_range": not args.no_direct},

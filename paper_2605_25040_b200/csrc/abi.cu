@@ -958,9 +958,14 @@ int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   TRY(ensure_main(ctx));
   // the estimate kernel resets the per-call control block and sets the range window
   launch_estimate((const u64*)d_x, n, is_signed ? kSign : 0, 0, ctx->d_ctl, st);
+  // both count shapes, each gated on the estimate's window (no host round trip)
   cudaError_t e = launch_hash_count((const u64*)d_x, n, is_signed ? kSign : 0, hash_mult,
                                     ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                                    ctx->num_sms, st, 1, kGateNone, ctx->spill, ctx->dense);
+                                    ctx->num_sms, st, 0, kGateDense, ctx->spill, ctx->dense);
+  if (e == cudaSuccess)
+    e = launch_hash_count((const u64*)d_x, n, is_signed ? kSign : 0, hash_mult, ctx->d_ctl,
+                          ctx->gkeys, ctx->gcnt, ctx->glist, 1, ctx->num_sms, st, 1, kGateHash,
+                          ctx->spill, ctx->dense);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
   launch_spill_fold(ctx->d_ctl, ctx->spill, ctx->gkeys, ctx->gcnt, ctx->glist, hash_mult,
                     ctx->num_sms, st, kGateNone);
@@ -970,7 +975,7 @@ int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
                      ctx->poffs, n, st, kGateNone);
   e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, n, ctx->pk_b, ctx->pc_b,
                               ctx->poffs, st, kGateNone);
-  ctx->launches += 6;
+  ctx->launches += 7;
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   TRY(sync_ctl(ctx, st));
   DevCtl c = *ctx->h_ctl;

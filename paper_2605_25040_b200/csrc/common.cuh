@@ -78,10 +78,15 @@ constexpr int32_t kNeedScan = 5;
 
 // Gate modes: the fused pipeline launches every route's kernels back to back and
 // each kernel reads the device decision and exits unless its route is active.
-enum : int { kGateNone = 0, kGateTiny = 1, kGateMain = 2, kGateMainDense = 3, kGateMainHash = 4 };
+enum : int {
+  kGateNone = 0, kGateTiny = 1, kGateMain = 2, kGateMainDense = 3, kGateMainHash = 4,
+  kGateDense = 5, kGateHash = 6  // window open / closed, whatever the route (stage APIs)
+};
 
 __device__ __forceinline__ bool gate_open(const DevCtl* ctl, int gate) {
   if (gate == kGateNone) return true;
+  if (gate == kGateDense) return ctl->range_len > 0;
+  if (gate == kGateHash) return ctl->range_len == 0;
   const int r = ctl->eff_route;
   if (gate == kGateTiny) return r == CAFS_TINY_COUNT;
   const bool main = r == CAFS_MAIN || (r == CAFS_TINY_COUNT && ctl->tiny_failed);

@@ -577,7 +577,7 @@ cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* c
                               u64* gcnt, u32* glist, int use_range, int num_sms,
                               cudaStream_t st, int variant, int gate, u64* spill, u64* dense) {
   HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate, spill, dense};
-  const bool window = use_range && gate != kGateMainHash;
+  const bool window = use_range && gate != kGateMainHash && gate != kGateHash;
   int v = hc_variant();
   if (v < 0) v = variant == 0 ? 0 : (window ? 2 : 5);
   if (!window && v == 0) v = 5;

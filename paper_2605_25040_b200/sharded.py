@@ -206,11 +206,18 @@ class Comm:
         return t.to(self.device) if self.device is not None else t
 
     def all_gather_ints(self, vals: list[int]) -> list[list[int]]:
+        """u64 values of every rank, rank order; one collective, one copy back."""
         torch = _torch()
         t = self._t(np.array(vals, dtype=np.uint64).view(np.int64))
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(out, t, group=self.group)
-        return [o.cpu().numpy().view(np.uint64).astype(object).tolist() for o in out]
+        if self.device is not None:  # NCCL: one [world, k] device tensor
+            out = torch.empty((self.world, t.shape[0]), dtype=t.dtype, device=t.device)
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+            rows = out.cpu().numpy()
+        else:
+            outs = [torch.empty_like(t) for _ in range(self.world)]
+            self.dist.all_gather(outs, t, group=self.group)
+            rows = torch.stack(outs).numpy()
+        return rows.view(np.uint64).astype(object).tolist()
 
     def all_reduce_sum(self, a: np.ndarray) -> np.ndarray:
         t = self._t(np.array(a, dtype=np.int64))  # a copy: the reduction is in place
@@ -226,10 +233,33 @@ class Comm:
         self.dist.all_to_all_single(out, src, out_splits, in_splits, group=self.group)
         return out.to(send.device) if stage else out
 
-    def all_gather_var(self, t):
+    def all_reduce_tensor(self, t):
+        """Element-wise SUM across ranks of a fixed-shape tensor (a new tensor)."""
+        stage = self.device is None and t.is_cuda
+        w = t.cpu() if stage else t.clone()
+        self.dist.all_reduce(w, group=self.group)
+        return w.to(t.device) if stage else w
+
+    def all_gather_pairs(self, keys, counts, sizes: list[int]):
+        """All-gather every rank's (keys, counts) in rank order, sizes known: one
+        collective of a [2, max] tensor per rank."""
+        torch = _torch()
+        m = max(sizes) if sizes else 0
+        dev = keys.device if self.device is not None or not keys.is_cuda else torch.device("cpu")
+        pack = torch.zeros((2, max(m, 1)), dtype=keys.dtype, device=dev)
+        pack[0, :keys.shape[0]] = keys.to(dev)
+        pack[1, :counts.shape[0]] = counts.to(dev)
+        out = [torch.empty_like(pack) for _ in range(self.world)]
+        self.dist.all_gather(out, pack, group=self.group)
+        k = torch.cat([o[0, :s] for o, s in zip(out, sizes)]).to(keys.device)
+        c = torch.cat([o[1, :s] for o, s in zip(out, sizes)]).to(keys.device)
+        return k, c
+
+    def all_gather_var(self, t, sizes: list[int] | None = None):
         """All-gather 1-D int64 tensors of different lengths (pad to the max)."""
         torch = _torch()
-        sizes = [s[0] for s in self.all_gather_ints([int(t.shape[0])])]
+        if sizes is None:
+            sizes = [s[0] for s in self.all_gather_ints([int(t.shape[0])])]
         m = max(sizes) if sizes else 0
         dev = t.device if self.device is not None or not t.is_cuda else torch.device("cpu")
         pad = torch.zeros(m, dtype=t.dtype, device=dev)
@@ -333,12 +363,20 @@ def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTeleme
 
 
 def _sort_sharded(x_local, comm, ops, tel, mult: int, signed: bool) -> None:
+    """Four collectives on the MAIN route (header, samples, pair sizes, pairs)."""
     torch = _torch()
     flip = _SIGN if signed else 0
+    m64 = (1 << 64) - 1
 
-    # ---- global shape ----
+    # ---- one header all-gather: shard size, local monotone, first/last key ----
     n_local = int(x_local.shape[0])
-    sizes = [s[0] for s in comm.all_gather_ints([n_local])]
+    mono = ops.is_monotone(x_local) if n_local > 1 else True
+    first = last = 0
+    if n_local:
+        fl = torch.stack([x_local[0], x_local[-1]]).cpu().numpy()  # one D2H
+        first, last = ((int(v) & m64) ^ flip for v in fl)
+    hdr = comm.all_gather_ints([n_local, int(mono), first, last])
+    sizes = [int(h[0]) for h in hdr]
     N = int(sum(sizes))
     off = int(sum(sizes[:comm.rank]))
     tel.n = N
@@ -346,15 +384,11 @@ def _sort_sharded(x_local, comm, ops, tel, mult: int, signed: bool) -> None:
         tel.decision = DispatchDecision(Route.ALREADY_SORTED)
         return
 
-    # ---- monotone (sorter.py:115-129) ----
-    mono = ops.is_monotone(x_local)
-    first = (int(x_local[0].item()) & ((1 << 64) - 1)) ^ flip if n_local else 0
-    last = (int(x_local[-1].item()) & ((1 << 64) - 1)) ^ flip if n_local else 0
-    info = comm.all_gather_ints([int(mono), first, last, int(n_local > 0)])
-    g_mono = all(r[0] for r in info)
+    # ---- monotone (sorter.py:115-129): every shard sorted, boundaries ordered ----
+    g_mono = all(h[1] for h in hdr)
     prev = None
-    for m_, f_, l_, ne in info:
-        if ne:
+    for n_r, _, f_, l_ in hdr:
+        if n_r:
             if prev is not None and f_ < prev:
                 g_mono = False
             prev = l_
@@ -366,7 +400,7 @@ def _sort_sharded(x_local, comm, ops, tel, mult: int, signed: bool) -> None:
         tel.decision = route_decision
         tel.guard_fired = guard
         if N < SMALL_N_CUTOFF:  # a few KB: gather and sort everywhere
-            full = comm.all_gather_var(x_local)
+            full = comm.all_gather_var(x_local, sizes)
             ops.fallback_sort(full)
             x_local.copy_(full[off:off + n_local])
             return
@@ -376,17 +410,16 @@ def _sort_sharded(x_local, comm, ops, tel, mult: int, signed: bool) -> None:
         _fallback(DispatchDecision(Route.FALLBACK_SMALL_N))
         return
 
-    # ---- strided samples (cardinality.py:99-110), gathered across ranks ----
+    # ---- strided samples (cardinality.py:99-110): each rank fills the global
+    # positions in its shard, one all-reduce assembles all 1024 ----
     stride = N // SAMPLE_TARGET
     lo = (off + stride - 1) // stride
     hi = min(SAMPLE_TARGET, (off + n_local + stride - 1) // stride)
+    buf = torch.zeros(SAMPLE_TARGET, dtype=x_local.dtype, device=x_local.device)
     if hi > lo:
         pos = torch.arange(lo, hi, device=x_local.device, dtype=torch.int64) * stride - off
-        local_samples = x_local.index_select(0, pos)
-    else:
-        local_samples = x_local[:0]
-    samples = comm.all_gather_var(local_samples)
-    assert samples.shape[0] == SAMPLE_TARGET
+        buf[lo:hi] = x_local.index_select(0, pos)
+    samples = comm.all_reduce_tensor(buf)
     u, f1, f2, saturated, keys = ops.estimate(samples)
     k_hat = chao1(u, f1, f2, N, saturated)
     est = CardinalityEstimate(k_hat, u, f1, f2, saturated)
@@ -412,14 +445,14 @@ def _sort_sharded(x_local, comm, ops, tel, mult: int, signed: bool) -> None:
     decision = DispatchDecision(Route.MAIN, k_hat=k_hat, estimate=est)
     tel.table_buckets = table_size_for(max(1.0, k_hat), N, 4)
     pairs = ops.count_pairs(x_local, mult)
-    overflow = comm.all_reduce_sum(np.array([1 if pairs is None else 0]))[0]
+    meta = comm.all_gather_ints([int(pairs is None), 0 if pairs is None else int(pairs[0].shape[0])])
     merged = None
-    if not overflow:
-        keys_all = comm.all_gather_var(pairs[0])
-        cnts_all = comm.all_gather_var(pairs[1])
+    if not any(m[0] for m in meta):
+        counts = [int(m[1]) for m in meta]
+        keys_all, cnts_all = comm.all_gather_pairs(pairs[0], pairs[1], counts)
+        # every rank merges the same tables: the overflow outcome is the same everywhere
         merged = ops.merge_pairs(keys_all, cnts_all)
-        overflow = comm.all_reduce_sum(np.array([1 if merged is None else 0]))[0]
-    if overflow:
+    if merged is None:
         _fallback(decision, guard=True)
         return
     tel.decision = decision
