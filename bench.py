@@ -178,6 +178,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=1 << 24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-direct", action="store_true", help="disable the dense-range count path")
+    ap.add_argument("--dtype", default="int64", choices=["int64", "int32"],
+                    help="int32: the 4-byte-key path (cfg values truncated to 32 bits)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU code path (NCCL) even at one rank")
     args = ap.parse_args()
@@ -210,6 +212,9 @@ def main():
     start = rank * per
     n_local = per if rank < world - 1 else N - per * (world - 1)
     pristine = datagen.generate(cfg, n_local, start)
+    if args.dtype == "int32":
+        pristine = pristine.to(torch.int32)
+    kb = pristine.element_size()  # bytes per key
     x = torch.empty_like(pristine)
     stream = torch.cuda.current_stream()
 
@@ -282,7 +287,7 @@ def main():
                                else "tiny_count_kernel"), ("emit", k_emit, "emit_kernel")):
         if vals:
             avg = sum(vals) / len(vals)
-            gbs = n_local * 8 / (avg / 1e3) / 1e9
+            gbs = n_local * kb / (avg / 1e3) / 1e9
             kernels[name] = {"kernel": kname, "avg_ms": avg, "GB/s": gbs,
                              "share_of_step": avg / (tot_ms / args.steps)}
     k_est = [t.kernel_ms.get("estimate_kernel") for t in tels if "estimate_kernel" in t.kernel_ms]
@@ -296,46 +301,48 @@ def main():
         if k_sort:
             avg = sum(k_sort) / len(k_sort)
             kernels["sort"] = {"kernel": "fallback sort stage (msd_* + bucket_*)", "avg_ms": avg,
-                               "GB/s": n_local * 16 / (avg / 1e3) / 1e9,
+                               "GB/s": n_local * 2 * kb / (avg / 1e3) / 1e9,
                                "share_of_step": avg / (tot_ms / args.steps)}
     if any("GB/s" in v for v in kernels.values()):
         dom = max((k for k in kernels if "GB/s" in kernels[k]), key=lambda k: kernels[k]["avg_ms"])
         d = kernels[dom]
         roof = {"bound": "hbm", "kernel": d["kernel"], "achieved": d["GB/s"], "peak": peak,
-                "unit": "GB/s", "frac": d["GB/s"] / peak, "traffic": ncu_traffic(args.config, d["kernel"]),
-                "algorithmic_bytes_per_launch": n_local * (16 if dom == "sort" else 8),
+                "unit": "GB/s", "frac": d["GB/s"] / peak, "traffic": ncu_traffic(args.config + ("" if kb == 8 else "_int32"), d["kernel"]),
+                "algorithmic_bytes_per_launch": n_local * kb * (2 if dom == "sort" else 1),
                 "peak_source": peak_src,
-                "step_frac": (16 * N / (tot_ms / args.steps / 1e3) / 1e9) / world / peak,
+                "step_frac": (2 * kb * N / (tot_ms / args.steps / 1e3) / 1e9) / world / peak,
                 "kernels": kernels}
 
     # ---- e2e through the C ABI host entry point (pinned host buffers) ----
     e2e = None
     if world == 1 and args.e2e_steps > 0:
-        h_in = torch.empty(N, dtype=torch.int64, pin_memory=True)
-        h_out = torch.empty(N, dtype=torch.int64, pin_memory=True)
+        h_in = torch.empty(N, dtype=pristine.dtype, pin_memory=True)
+        h_out = torch.empty(N, dtype=pristine.dtype, pin_memory=True)
         h_in.copy_(pristine)
         lib = _lib.load()
         ctx = _lib.context(local)
         tel_c = _lib.Telemetry()
-        lib.cafs_sort_i64_host(ctx, h_in.data_ptr(), h_out.data_ptr(), N, 1, cafs.HASH_MULT, 0,
-                               ctypes.byref(tel_c), stream.cuda_stream)  # warm
+        host_sort = lib.cafs_sort_i32_host if kb == 4 else lib.cafs_sort_i64_host
+        host_name = "cafs_sort_i32_host" if kb == 4 else "cafs_sort_i64_host"
+        host_sort(ctx, h_in.data_ptr(), h_out.data_ptr(), N, 1, cafs.HASH_MULT, 0,
+                  ctypes.byref(tel_c), stream.cuda_stream)  # warm
         torch.cuda.synchronize()
         e_t = []
         for _ in range(args.e2e_steps):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            rc = lib.cafs_sort_i64_host(ctx, h_in.data_ptr(), h_out.data_ptr(), N, 1,
-                                        cafs.HASH_MULT, 0, ctypes.byref(tel_c), stream.cuda_stream)
+            rc = host_sort(ctx, h_in.data_ptr(), h_out.data_ptr(), N, 1,
+                           cafs.HASH_MULT, 0, ctypes.byref(tel_c), stream.cuda_stream)
             b.record(stream)
             b.synchronize()
-            _lib.check(rc, ctx, "cafs_sort_i64_host")
+            _lib.check(rc, ctx, host_name)
             e_t.append(a.elapsed_time(b))
         ok &= bool((h_out[1:] >= h_out[:-1]).all().item())
         e2e = {"value": N * len(e_t) / (sum(e_t) / 1e3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": N * 8, "d2h_bytes_per_step": N * 8,
+               "h2d_bytes_per_step": N * kb, "d2h_bytes_per_step": N * kb,
                "ms_per_step": sum(e_t) / len(e_t),
-               "path": "cafs_sort_i64_host (C ABI), pinned host in/out buffers"}
+               "path": f"{host_name} (C ABI), pinned host in/out buffers"}
         del h_in, h_out
 
     cpu = None
@@ -346,8 +353,9 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-            "data": f"synthetic, device-generated ({cfg.desc}; seed {cfg.seed})",
+            "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+            "data": f"synthetic, device-generated ({cfg.desc}; seed {cfg.seed})"
+                    + ("; values truncated to int32" if kb == 4 else ""),
             "config": {"workload": args.config, "n": N, "k": cfg.k, "dist": cfg.dist, "s": cfg.s,
                        "route": route, "parallelism": f"rows sharded x{world}" + (" (sharded path)" if sharded else ""),
                        "l2": "input 8 B x N >> 126 MB L2; unsorted input restored by an untimed "

@@ -22,6 +22,7 @@
  *   cafs_pair_sort           _kernels.py:185-214 radix_sort_pairs / sorter.py:228-241 pair_sort
  *   cafs_emit_i64            sorter.py:244-251 + _kernels.py:172-182  emit / emit_fill
  *   cafs_fallback_sort_i64   sorter.py:132-138   fallback_sort(x)
+ *   cafs_sort_i32(_host)     sorter.py:335-386   cafs_sort on int32 / uint32 arrays
  *   cafs_key_span_i64,       (no reference counterpart: the distributed
  *   cafs_partition_i64        fallback of SURVEY.md §8(f)2, sharded.py)
  *
@@ -135,6 +136,17 @@ int cafs_sort_i64_host(cafs_ctx_t* ctx, const int64_t* h_in, int64_t* h_out, uin
                        int is_signed, uint64_t hash_mult, uint32_t flags,
                        cafs_telemetry_t* tel, void* stream);
 
+/* cafs_sort for 4-byte keys (SUPPORTED_DTYPES int32 / uint32, sorter.py:34):
+ * is_signed = 1 for int32 (the reference's order map flips bit 31,
+ * sorter.py:84-94), 0 for uint32.  Same routes, estimate and telemetry as the
+ * int64 widening of the column (keys are widened in registers), but the count
+ * reads and the emit writes 4 B per key.  d_x must be 4-byte aligned. */
+int cafs_sort_i32(cafs_ctx_t* ctx, int32_t* d_x, uint64_t n, int is_signed, uint64_t hash_mult,
+                  uint32_t flags, cafs_telemetry_t* tel, void* stream);
+int cafs_sort_i32_host(cafs_ctx_t* ctx, const int32_t* h_in, int32_t* h_out, uint64_t n,
+                       int is_signed, uint64_t hash_mult, uint32_t flags,
+                       cafs_telemetry_t* tel, void* stream);
+
 /* dispatch(x) -> decision (sorter.py:141-162); requires n >= 2 */
 int cafs_dispatch_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
                       uint64_t hash_mult, cafs_decision_t* out, void* stream);
@@ -187,15 +199,16 @@ int cafs_fallback_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_sig
  * what a multi-GPU caller replaces with: global span -> one bucket digit ->
  * local partition -> all-to-all of bucket ranges -> local sort of the received
  * range.  These two calls are the local steps. */
-/* OR and AND over the order-mapped keys (h_or = 0, h_and = ~0 when n == 0) */
+/* min and max of the order-mapped keys (h_min = ~0, h_max = 0 when n == 0) */
 int cafs_key_span_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
-                      uint64_t* h_or, uint64_t* h_and, void* stream);
-/* Group x by the 4096-way bucket digit of the 12 highest bits varying over the
- * GLOBAL span (g_or, g_and): d_out[0..n) = the keys (same representation as x)
- * in ascending digit order, h_counts[4096] = keys per bucket. */
+                      uint64_t* h_min, uint64_t* h_max, void* stream);
+/* Group x into 4096 buckets by ((k - g_min) >> shift), the shift fitting the
+ * GLOBAL span [g_min, g_max] of order-mapped keys into 12 bits:
+ * d_out[0..n) = the keys (same representation as x) in ascending bucket
+ * order, h_counts[4096] = keys per bucket. */
 #define CAFS_PARTITION_BUCKETS 4096
 int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
-                       uint64_t g_or, uint64_t g_and, int64_t* d_out, uint64_t* h_counts,
+                       uint64_t g_min, uint64_t g_max, int64_t* d_out, uint64_t* h_counts,
                        void* stream);
 
 /* Kernels this context has launched since it was created (monotone; the

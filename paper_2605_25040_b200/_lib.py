@@ -63,6 +63,9 @@ SIGNATURES = {
     "cafs_sort_i64": (_I, [_P, _P, _U64, _I, _U64, ctypes.c_uint32, ctypes.POINTER(Telemetry), _P]),
     "cafs_sort_i64_host": (_I, [_P, _P, _P, _U64, _I, _U64, ctypes.c_uint32,
                                 ctypes.POINTER(Telemetry), _P]),
+    "cafs_sort_i32": (_I, [_P, _P, _U64, _I, _U64, ctypes.c_uint32, ctypes.POINTER(Telemetry), _P]),
+    "cafs_sort_i32_host": (_I, [_P, _P, _P, _U64, _I, _U64, ctypes.c_uint32,
+                                ctypes.POINTER(Telemetry), _P]),
     "cafs_dispatch_i64": (_I, [_P, _P, _U64, _I, _U64, ctypes.POINTER(Decision), _P]),
     "cafs_estimate_i64": (_I, [_P, _P, _U64, _I, ctypes.POINTER(Estimate), _P]),
     "cafs_is_monotone_i64": (_I, [_P, _P, _U64, _I, ctypes.POINTER(_I), _P]),

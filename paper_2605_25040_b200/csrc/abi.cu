@@ -75,6 +75,8 @@ struct cafs_ctx {
   cudaEvent_t ev[32] = {};
   std::string last_error;
   uint64_t launches = 0;  // kernels this context has launched (monotone)
+  u64* wide = nullptr;    // int64 copy of a 32-bit column (host-driven fallback routes)
+  u64 wide_elems = 0;
   // CUDA Graphs of the fused pipeline (estimate + gated route kernels), keyed by
   // the call's arguments; captured on the second call with the same key
   cudaStream_t cap_stream = nullptr;
@@ -85,8 +87,9 @@ struct cafs_ctx {
     int seen = 0;
     cudaGraphExec_t exec = nullptr;
     int tn = 0, mark = 0, label[16] = {}, cond[16] = {};
-    uint64_t launches = 0;  // kernels this context has launched (monotone)
+    uint64_t launches = 0;  // kernels in the captured graph
     uint64_t stamp = 0;
+    int kk = 0;             // key kind the graph was captured for
   } graphs[16];
   uint64_t graph_clock = 0;
 };
@@ -295,6 +298,26 @@ int fallback_sort(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cudaStream_t st) {
   return CAFS_OK;
 }
 
+// fallback for any key kind: a 32-bit column is widened to int64, sorted by the
+// 64-bit fallback and narrowed back (rare routes: high entropy, small n, guard)
+int fallback_any(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cudaStream_t st, int kk) {
+  if (kk == 0) return fallback_sort(ctx, (u64*)x, n, flip, st);
+  if (n < 2) return CAFS_OK;
+  if (n > ctx->wide_elems) {
+    if (ctx->wide) CK(cudaFree(ctx->wide));
+    ctx->wide = nullptr;
+    ctx->wide_elems = 0;
+    CK(cudaMalloc(&ctx->wide, n * 8));
+    ctx->wide_elems = n;
+  }
+  launch_widen(x, n, kk, ctx->wide, ctx->num_sms, st);
+  TRY(fallback_sort(ctx, ctx->wide, n, kSign, st));
+  launch_narrow(ctx->wide, n, kk, x, ctx->num_sms, st);
+  ctx->launches += 2;
+  CKL();
+  return CAFS_OK;
+}
+
 int sync_ctl(cafs_ctx_t* ctx, cudaStream_t st) {
   CK(cudaMemcpyAsync(ctx->h_ctl, ctx->d_ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -367,10 +390,10 @@ struct StageTimer {
 
 // K0/K1 (+ the full monotone scan when the prefix is sorted).  Leaves the
 // device control block filled and *monotone / *route set.
-int run_dispatch(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, cudaStream_t st, bool* monotone,
-                 int* route, StageTimer* tm = nullptr) {
+int run_dispatch(cafs_ctx_t* ctx, const void* x, u64 n, u64 flip, cudaStream_t st, bool* monotone,
+                 int* route, StageTimer* tm = nullptr, int kk = 0) {
   const int te = tm ? tm->begin() : -1;
-  launch_estimate(x, n, flip, 1, ctx->d_ctl, st);
+  launch_estimate(x, n, flip, 1, ctx->d_ctl, st, kk);
   if (tm) tm->end(te, L_K_EST);
   ctx->launches++;
   CKL();
@@ -380,7 +403,7 @@ int run_dispatch(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, cudaStream_t st
     if (n <= kMonoPrefix) {
       *monotone = true;
     } else {
-      launch_monotone_scan(x, n, flip, ctx->d_ctl, ctx->num_sms, st);
+      launch_monotone_scan(x, n, flip, ctx->d_ctl, ctx->num_sms, st, kk);
       ctx->launches++;
       CKL();
       TRY(sync_ctl(ctx, st));
@@ -396,12 +419,12 @@ int run_dispatch(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, cudaStream_t st
 // compact -> pair sort -> emit.  Each kernel reads the device decision of the
 // estimate kernel and exits unless its route is active, so the host needs no
 // round trip between the dispatch and the emit.
-int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
-                 StageTimer& tm, cudaStream_t st, bool with_emit = true) {
+int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t flags,
+                 StageTimer& tm, cudaStream_t st, bool with_emit = true, int kk = 0) {
   TRY(ensure_main(ctx));
   DevCtl* c = ctx->d_ctl;
   int ts = tm.begin(), tk = tm.begin();
-  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny);
+  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny, kk);
   tm.end(tk, L_K_COUNT, C_TINY);
   launch_tiny_finalize(c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st, kGateTiny);
   tm.end(ts, L_STAGE_COUNT, C_TINY);
@@ -411,13 +434,13 @@ int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t fl
   cudaError_t e;
   if (direct) {
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                          ctx->num_sms, st, 0, kGateMainDense, ctx->spill, ctx->dense);
+                          ctx->num_sms, st, 0, kGateMainDense, ctx->spill, ctx->dense, kk);
     if (e == cudaSuccess)
       e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                            ctx->num_sms, st, 1, kGateMainHash, ctx->spill, ctx->dense);
+                            ctx->num_sms, st, 1, kGateMainHash, ctx->spill, ctx->dense, kk);
   } else {
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 0,
-                          ctx->num_sms, st, 1, kGateMain, ctx->spill, ctx->dense);
+                          ctx->num_sms, st, 1, kGateMain, ctx->spill, ctx->dense, kk);
   }
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
   tm.end(tk, L_K_COUNT, C_MAIN);
@@ -437,7 +460,7 @@ int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t fl
   if (with_emit) {
     ts = tm.begin();
     tk = tm.begin();
-    launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, kSmallSortMax);
+    launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, kSmallSortMax, kk);
     tm.end(tk, L_K_EMIT, C_EMIT);
     tm.end(ts, L_STAGE_EMIT, C_EMIT);
     ctx->launches++;
@@ -449,8 +472,8 @@ int launch_fused(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t fl
 
 // Reference-exact bucket-table statistics (telemetry.cu), from the compacted
 // pairs (pk_a, pc_a) and the still-unsorted input x.
-int exact_telemetry(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, u64 mult, double k_hat,
-                    uint32_t flags, cafs_telemetry_t* tel, cudaStream_t st) {
+int exact_telemetry(cafs_ctx_t* ctx, const void* x, u64 n, u64 flip, u64 mult, double k_hat,
+                    uint32_t flags, cafs_telemetry_t* tel, cudaStream_t st, int kk = 0) {
   const DevCtl c = *ctx->h_ctl;
   const u64 np = c.npairs;
   if (!ctx->tl_keys) {
@@ -473,12 +496,12 @@ int exact_telemetry(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, u64 mult, do
   launch_tel_build(pk, np, ctx->tl_keys, ctx->tl_idx, log2s, ctx->tl_first, ctx->tl_runs,
                    ctx->tl_acc, ctx->num_sms, st);
   launch_tel_runs(x, n, flip, ctx->tl_keys, ctx->tl_idx, log2s, ctx->tl_first, ctx->tl_runs,
-                  ctx->tl_acc, ctx->num_sms, st);
+                  ctx->tl_acc, ctx->num_sms, st, kk);
   const bool dom32 = flags & (CAFS_FLAG_DOM_I32 | CAFS_FLAG_DOM_U32);
   const int cap = dom32 ? 8 : 4;
   const u64 M = table_size_for(k_hat > 1.0 ? k_hat : 1.0, n, cap);
   const int m_log2 = 63 - __builtin_clzll(M);
-  const int dom = (flags & CAFS_FLAG_DOM_I32) ? 1 : (flags & CAFS_FLAG_DOM_U32) ? 2 : 0;
+  const int dom = kk ? kk : (flags & CAFS_FLAG_DOM_I32) ? 1 : (flags & CAFS_FLAG_DOM_U32) ? 2 : 0;
   u64 *comp = ctx->tl_comp, *cidx = comp + kPairCap, *comp2 = cidx + kPairCap,
       *cidx2 = comp2 + kPairCap;
   launch_tel_comp(pk, np, ctx->tl_first, mult, m_log2, dom, comp, cidx, ctx->num_sms, st);
@@ -515,8 +538,10 @@ int exact_telemetry(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, u64 mult, do
 
 // After the fused pipeline: the guard (overflow -> fallback, sorter.py:264-273),
 // the large-pair-set path, and the sum check (sorter.py:247-248).
-int main_finish(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cafs_telemetry_t* tel,
-                StageTimer& tm, cudaStream_t st, bool* emitted) {
+int fallback_any(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cudaStream_t st, int kk);
+
+int main_finish(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cafs_telemetry_t* tel,
+                StageTimer& tm, cudaStream_t st, bool* emitted, int kk = 0) {
   DevCtl& c = *ctx->h_ctl;
   tel->global_updates = c.g_updates;
   if (c.overflow) {
@@ -525,7 +550,7 @@ int main_finish(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cafs_telemetry_t* tel,
     tel->guard_fired = 1;
     *emitted = false;
     const int ts = tm.begin();
-    TRY(fallback_sort(ctx, x, n, flip, st));
+    TRY(fallback_any(ctx, x, n, flip, st, kk));
     tm.end(ts, L_STAGE_SORT_K);
     return CAFS_OK;
   }
@@ -539,7 +564,7 @@ int main_finish(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cafs_telemetry_t* tel,
     tm.end(ts, L_STAGE_SORT_K);
     ts = tm.begin();
     const int tk = tm.begin();
-    launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st, np);
+    launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st, np, kk);
     tm.end(tk, L_K_EMIT);
     ctx->launches++;
     CKL();
@@ -553,22 +578,22 @@ int main_finish(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cafs_telemetry_t* tel,
   return CAFS_OK;
 }
 
-void pipeline_direct(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
-                     StageTimer& tm, cudaStream_t st, bool exact, int* mark, int* rc) {
+void pipeline_direct(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t flags,
+                     StageTimer& tm, cudaStream_t st, bool exact, int* mark, int* rc, int kk) {
   const int te = tm.begin();
-  launch_estimate(x, n, flip, 1, ctx->d_ctl, st);
+  launch_estimate(x, n, flip, 1, ctx->d_ctl, st, kk);
   tm.end(te, L_K_EST);
   ctx->launches++;
   *mark = tm.n;
-  *rc = launch_fused(ctx, x, n, flip, mult, flags, tm, st, !exact);
+  *rc = launch_fused(ctx, x, n, flip, mult, flags, tm, st, !exact, kk);
 }
 
 // The estimate + fused kernels, replayed from a cached CUDA Graph when the same
 // (buffer, n, flags) was sorted before: one graph launch instead of ~9 kernel
 // launches (the small-input latency).  The graph's kernels are the same; only
 // the launch path differs.
-int launch_pipeline(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t flags,
-                    StageTimer& tm, cudaStream_t st, bool exact, int* mark) {
+int launch_pipeline(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t flags,
+                    StageTimer& tm, cudaStream_t st, bool exact, int* mark, int kk) {
   static int use_graphs = -1;
   if (use_graphs < 0) {
     const char* e = getenv("CAFS_GRAPHS");
@@ -576,7 +601,7 @@ int launch_pipeline(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t
   }
   int rc = CAFS_OK;
   if (!use_graphs || !ctx->cap_stream) {
-    pipeline_direct(ctx, x, n, flip, mult, flags, tm, st, exact, mark, &rc);
+    pipeline_direct(ctx, x, n, flip, mult, flags, tm, st, exact, mark, &rc, kk);
     CKL();
     return rc;
   }
@@ -585,7 +610,7 @@ int launch_pipeline(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t
   cafs_ctx_t::GraphEntry* lru = &ctx->graphs[0];
   for (auto& g : ctx->graphs) {
     if (g.seen && g.x == (u64)x && g.n == n && g.flip == flip && g.mult == mult &&
-        g.flags == flags && g.timing == timing) {
+        g.flags == flags && g.timing == timing && g.kk == kk) {
       hit = &g;
       break;
     }
@@ -604,19 +629,19 @@ int launch_pipeline(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t
     if (lru->exec) cudaGraphExecDestroy(lru->exec);
     *lru = cafs_ctx_t::GraphEntry();
     lru->x = (u64)x; lru->n = n; lru->flip = flip; lru->mult = mult; lru->flags = flags;
-    lru->timing = timing; lru->seen = 1; lru->stamp = ++ctx->graph_clock;
-    pipeline_direct(ctx, x, n, flip, mult, flags, tm, st, exact, mark, &rc);
+    lru->timing = timing; lru->seen = 1; lru->stamp = ++ctx->graph_clock; lru->kk = kk;
+    pipeline_direct(ctx, x, n, flip, mult, flags, tm, st, exact, mark, &rc, kk);
     CKL();
     return rc;
   }
   // second sighting: capture on the context's stream, then launch on the caller's
-  const uint32_t l0 = ctx->launches;
+  const uint64_t l0 = ctx->launches;
   StageTimer ct = tm;
   ct.st = ctx->cap_stream;
   ct.capturing = true;
   cudaGraph_t graph = nullptr;
   CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
-  pipeline_direct(ctx, x, n, flip, mult, flags, ct, ctx->cap_stream, exact, mark, &rc);
+  pipeline_direct(ctx, x, n, flip, mult, flags, ct, ctx->cap_stream, exact, mark, &rc, kk);
   cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &graph);
   if (rc != CAFS_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "graph capture", e);
@@ -634,11 +659,13 @@ int launch_pipeline(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, u64 mult, uint32_t
   return CAFS_OK;
 }
 
-int check_common(cafs_ctx_t* ctx, const void* p, u64 n) {
+int check_common(cafs_ctx_t* ctx, const void* p, u64 n, u64 align = 8) {
   if (!ctx) return CAFS_EINVAL;
   if (n >= (1ull << 32)) return fail(ctx, CAFS_EINVAL, "arrays of 2**32 or more elements");
   if (n > 0 && !p) return fail(ctx, CAFS_EINVAL, "null data pointer");
-  if (((uintptr_t)p) & 7) return fail(ctx, CAFS_EINVAL, "data must be 8-byte aligned");
+  if (((uintptr_t)p) & (align - 1))
+    return fail(ctx, CAFS_EINVAL, align == 8 ? "data must be 8-byte aligned"
+                                             : "data must be 4-byte aligned");
   return CAFS_OK;
 }
 
@@ -703,7 +730,7 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
                  ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->spill, ctx->dense, ctx->ghist, ctx->gbase,
                  ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage, ctx->msd,
                  ctx->tl_keys, ctx->tl_idx, ctx->tl_first, ctx->tl_runs, ctx->tl_comp,
-                 ctx->tl_offs, ctx->tl_acc, ctx->pk_t, ctx->pc_t};
+                 ctx->tl_offs, ctx->tl_acc, ctx->pk_t, ctx->pc_t, ctx->wide};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -717,9 +744,11 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
   delete ctx;
 }
 
-int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint64_t hash_mult,
-                  uint32_t flags, cafs_telemetry_t* tel, void* stream) {
-  TRY(check_common(ctx, d_x, n));
+// The whole sort for key kind kk (0: 64-bit, 1: int32, 2: uint32; the flip of
+// 32-bit kinds is implied).
+static int sort_impl(cafs_ctx_t* ctx, void* d_x, uint64_t n, int is_signed, uint64_t hash_mult,
+                     uint32_t flags, cafs_telemetry_t* tel, void* stream, int kk) {
+  TRY(check_common(ctx, d_x, n, kk ? 4 : 8));
   if ((hash_mult & 1) == 0) return fail(ctx, CAFS_EINVAL, "hash multiplier must be odd");
   DeviceGuard g(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
@@ -736,13 +765,13 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
     return CAFS_OK;
   }
   StageTimer tm{ctx, st, want_tel && (flags & CAFS_FLAG_TIMING), tel};
-  u64* x = (u64*)d_x;
-  const u64 flip = is_signed ? kSign : 0;
+  void* x = d_x;
+  const u64 flip = (is_signed || kk) ? kSign : 0;
   // K0/K1 then every route's kernels, gated on the device decision; one sync
   const bool exact = want_tel && (flags & CAFS_FLAG_EXACT_TELEMETRY);
   TRY(ensure_main(ctx));
   int mark = 0;
-  TRY(launch_pipeline(ctx, x, n, flip, hash_mult, flags, tm, st, exact, &mark));
+  TRY(launch_pipeline(ctx, x, n, flip, hash_mult, flags, tm, st, exact, &mark, kk));
   TRY(sync_ctl(ctx, st));
   int eff = ctx->h_ctl->eff_route;
   bool mono = eff == CAFS_ALREADY_SORTED;
@@ -750,7 +779,7 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
     // the first 16385 rows are sorted: scan the rest, then rerun the gated
     // pipeline with the resolved route (the first pass was all no-ops)
     tm.n = mark;
-    launch_monotone_scan(x, n, flip, ctx->d_ctl, ctx->num_sms, st);
+    launch_monotone_scan(x, n, flip, ctx->d_ctl, ctx->num_sms, st, kk);
     ctx->launches++;
     CKL();
     TRY(sync_ctl(ctx, st));
@@ -760,7 +789,7 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
       ctx->h_scratch[0] = eff;
       CK(cudaMemcpyAsync(&ctx->d_ctl->eff_route, ctx->h_scratch, sizeof(int32_t),
                          cudaMemcpyHostToDevice, st));
-      TRY(launch_fused(ctx, x, n, flip, hash_mult, flags, tm, st, !exact));
+      TRY(launch_fused(ctx, x, n, flip, hash_mult, flags, tm, st, !exact, kk));
       TRY(sync_ctl(ctx, st));
     }
   }
@@ -770,11 +799,11 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
     const DevCtl& cc = *ctx->h_ctl;
     const bool main_ran_ = eff == CAFS_MAIN || (eff == CAFS_TINY_COUNT && cc.tiny_failed);
     if (main_ran_ && !cc.overflow)
-      TRY(exact_telemetry(ctx, x, n, flip, hash_mult, cc.k_hat, flags, tel, st));
+      TRY(exact_telemetry(ctx, x, n, flip, hash_mult, cc.k_hat, flags, tel, st, kk));
     if ((eff == CAFS_MAIN || eff == CAFS_TINY_COUNT) && cc.pairs_ready) {
       const int ts = tm.begin();
       launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st,
-                  kSmallSortMax);
+                  kSmallSortMax, kk);
       tm.end(ts, L_STAGE_EMIT, C_EMIT);
       ctx->launches++;
       CKL();
@@ -796,7 +825,7 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
     case CAFS_FALLBACK_SMALL_N:
     case CAFS_FALLBACK_HIGH_ENTROPY: {
       const int ts = tm.begin();
-      rc = fallback_sort(ctx, x, n, flip, st);
+      rc = fallback_any(ctx, x, n, flip, st, kk);
       tm.end(ts, L_STAGE_SORT_K);
       break;
     }
@@ -817,7 +846,7 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
       main_ran = true;
       emitted = true;
       tel->table_buckets = table_size_for(c.k_hat > 1.0 ? c.k_hat : 1.0, n, 4);
-      rc = main_finish(ctx, x, n, flip, tel, tm, st, &emitted);
+      rc = main_finish(ctx, x, n, flip, tel, tm, st, &emitted, kk);
       break;
   }
   if (rc != CAFS_OK) return rc;
@@ -829,6 +858,38 @@ int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint
     tel->ref_counted_total = tel->counted_total;
   }
   tel->kernels_launched = (uint32_t)(ctx->launches - launches0);
+  return CAFS_OK;
+}
+
+int cafs_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed, uint64_t hash_mult,
+                  uint32_t flags, cafs_telemetry_t* tel, void* stream) {
+  return sort_impl(ctx, d_x, n, is_signed, hash_mult, flags, tel, stream, 0);
+}
+
+int cafs_sort_i32(cafs_ctx_t* ctx, int32_t* d_x, uint64_t n, int is_signed, uint64_t hash_mult,
+                  uint32_t flags, cafs_telemetry_t* tel, void* stream) {
+  return sort_impl(ctx, d_x, n, is_signed, hash_mult, flags, tel, stream, is_signed ? 1 : 2);
+}
+
+int cafs_sort_i32_host(cafs_ctx_t* ctx, const int32_t* h_in, int32_t* h_out, uint64_t n,
+                       int is_signed, uint64_t hash_mult, uint32_t flags, cafs_telemetry_t* tel,
+                       void* stream) {
+  if (!ctx) return CAFS_EINVAL;
+  if (n >= (1ull << 32)) return fail(ctx, CAFS_EINVAL, "arrays of 2**32 or more elements");
+  if (n > 0 && (!h_in || !h_out)) return fail(ctx, CAFS_EINVAL, "null host pointer");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n > ctx->stage_elems) {  // the stage holds n 8-byte words: room for n 4-byte keys
+    if (ctx->stage) CK(cudaFree(ctx->stage));
+    ctx->stage = nullptr;
+    ctx->stage_elems = 0;
+    CK(cudaMalloc(&ctx->stage, (n ? n : 1) * 8));
+    ctx->stage_elems = n;
+  }
+  if (n) CK(cudaMemcpyAsync(ctx->stage, h_in, n * 4, cudaMemcpyHostToDevice, st));
+  TRY(cafs_sort_i32(ctx, (int32_t*)ctx->stage, n, is_signed, hash_mult, flags, tel, stream));
+  if (n) CK(cudaMemcpyAsync(h_out, ctx->stage, n * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   return CAFS_OK;
 }
 
@@ -1096,11 +1157,11 @@ int cafs_fallback_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_sig
 }
 
 int cafs_key_span_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
-                      uint64_t* h_or, uint64_t* h_and, void* stream) {
-  if (!h_or || !h_and) return CAFS_EINVAL;
+                      uint64_t* h_min, uint64_t* h_max, void* stream) {
+  if (!h_min || !h_max) return CAFS_EINVAL;
   TRY(check_common(ctx, d_x, n));
-  *h_or = 0;
-  *h_and = ~0ull;
+  *h_min = ~0ull;
+  *h_max = 0;
   if (n == 0) return CAFS_OK;
   DeviceGuard g(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
@@ -1112,13 +1173,13 @@ int cafs_key_span_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_si
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const u64* v = (const u64*)ctx->h_scratch;
-  *h_or = v[0];
-  *h_and = v[1];
+  *h_min = v[0];
+  *h_max = v[1];
   return CAFS_OK;
 }
 
 int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
-                       uint64_t g_or, uint64_t g_and, int64_t* d_out, uint64_t* h_counts,
+                       uint64_t g_min, uint64_t g_max, int64_t* d_out, uint64_t* h_counts,
                        void* stream) {
   if (!h_counts || (n && !d_out)) return CAFS_EINVAL;
   TRY(check_common(ctx, d_x, n));
@@ -1129,7 +1190,7 @@ int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_s
   DeviceGuard g(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_radix(ctx, n, false));
-  launch_msd_partition((const u64*)d_x, n, flip, ctx->msd, g_or, g_and, (u64*)d_out,
+  launch_msd_partition((const u64*)d_x, n, flip, ctx->msd, g_min, g_max, (u64*)d_out,
                        ctx->num_sms, st);
   ctx->launches += 4;
   CKL();

@@ -106,6 +106,28 @@ __device__ __forceinline__ u32 mhash(u64 v, u64 mult, int shift) {
   return (u32)((v * mult) >> shift);
 }
 
+// ---- key kinds ----
+// 0: 64-bit keys (flip = bit 63 for int64, 0 for uint64); 1: int32; 2: uint32.
+// 32-bit keys are processed in the 64-bit order-mapped domain of their int64
+// widening (v = sign/zero-extended x ^ bit 63), so every table, pair and
+// estimate is the same as for the widened column; loads widen in registers
+// and the emit narrows in the store, moving 4 B per key instead of 8.
+template <int KK> struct KeyT { using T = u64; };
+template <> struct KeyT<1> { using T = u32; };
+template <> struct KeyT<2> { using T = u32; };
+
+template <int KK>
+__device__ __forceinline__ u64 key_map(typename KeyT<KK>::T raw, u64 flip) {
+  if constexpr (KK == 0) return raw ^ flip;
+  else if constexpr (KK == 1) return (u64)(long long)(int)raw ^ kSign;
+  else return (u64)raw ^ kSign;
+}
+template <int KK>
+__device__ __forceinline__ typename KeyT<KK>::T key_unmap(u64 v, u64 flip) {
+  if constexpr (KK == 0) return v ^ flip;
+  else return (u32)(v ^ kSign);
+}
+
 __device__ __forceinline__ ulonglong2 ld_stream_v2(const void* p) {
   ulonglong2 v;
   asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];"

@@ -11,7 +11,8 @@
 // common case for low-cardinality columns -- is a pure store stream; a
 // fragmented tile is walked in windows of 32 run boundaries kept in registers
 // (shuffle search, one coalesced 256 B store per warp instruction).  The
-// bit-63 flip back to int64 happens in the store.  [begin, end) selects a
+// bit-63 flip back to int64 (or the narrowing to 32-bit keys) happens in the
+// store.  [begin, end) selects a
 // slice of the global sorted order: each GPU of a sharded sort writes only
 // its own rows.
 #include <cstdlib>
@@ -23,7 +24,7 @@ namespace cafs {
 
 constexpr int kEmitThreads = 512;
 constexpr int kEmitVpl = 8;                       // 32-byte vectors per lane per tile
-constexpr u64 kTileKeys = 32ull * kEmitVpl * 4;  // 1024 keys per warp tile
+constexpr u64 kTileBytes = 32ull * kEmitVpl * 32;  // 8 KB per warp tile (1024 int64 keys)
 constexpr u64 kIdxEntries = 4096;                // max shared index of the offsets (32 KB)
 constexpr int kIdxDefault = 256;                 // measured best (64..1024 within noise)
 
@@ -61,10 +62,19 @@ __device__ __forceinline__ u64 warp_find(const u64* offs, u64 lo, u64 hi, u64 g)
   return lo + (31 - __clz(m));
 }
 
+template <int KK>
 __global__ void __launch_bounds__(kEmitThreads)
     emit_kernel(const u64* __restrict__ keys, const u64* __restrict__ goffs, u64 npairs_arg,
-                const DevCtl* ctl, u64* __restrict__ out, u64 begin, u64 end, u64 flip,
-                u64 tpw, u64 idx_entries) {
+                const DevCtl* ctl, typename KeyT<KK>::T* __restrict__ out, u64 begin, u64 end,
+                u64 flip, u64 tpw, u64 idx_entries) {
+  using K = typename KeyT<KK>::T;
+  constexpr u64 VK = 32 / sizeof(K);             // keys per 32-byte vector
+  constexpr u64 kTileKeys = kTileBytes / sizeof(K);
+  // a uniform 32-byte vector of key k
+  auto splat = [](K k) -> u64 {
+    if constexpr (sizeof(K) == 8) return (u64)k;
+    else return (u64)k | ((u64)k << 32);
+  };
   extern __shared__ __align__(16) u64 soffs[];
   u64 npairs = npairs_arg;
   if (ctl) {
@@ -92,28 +102,28 @@ __global__ void __launch_bounds__(kEmitThreads)
   };
   const int lane = threadIdx.x & 31;
   const u64 L = end - begin;
-  // 32-byte aligned body; up to 3 head and 3 tail keys are scalar
-  const u64 mis = (((uintptr_t)out) >> 3) & 3;
-  const u64 head = mis ? ((4 - mis) < L ? (4 - mis) : L) : 0;
-  const u64 nvec = (L - head) / 4;
-  const u64 body_end = head + nvec * 4;
+  // 32-byte aligned body; up to VK-1 head and VK-1 tail keys are scalar
+  const u64 mis = (((uintptr_t)out) & 31) / sizeof(K);
+  const u64 head = mis ? ((VK - mis) < L ? (VK - mis) : L) : 0;
+  const u64 nvec = (L - head) / VK;
+  const u64 body_end = head + nvec * VK;
   if (blockIdx.x == 0 && threadIdx.x < 32) {
-    // warp 0: scalar head and tail keys (lanes 0-3 head, 4-7 tail)
-    const u64 j = lane < 4 ? (u64)lane : body_end + (lane - 4);
-    const bool act = (lane < 4 && j < head) || (lane >= 4 && lane < 8 && j < L);
-    for (int r = 0; r < 8; ++r) {  // each active lane's search, warp-cooperatively
+    // warp 0: scalar head and tail keys (lanes [0, VK) head, [VK, 2 VK) tail)
+    const u64 j = (u64)lane < VK ? (u64)lane : body_end + (lane - VK);
+    const bool act = ((u64)lane < VK && j < head) || ((u64)lane >= VK && (u64)lane < 2 * VK && j < L);
+    for (int r = 0; r < (int)(2 * VK); ++r) {  // each active lane's search, warp-cooperatively
       const bool mine = __shfl_sync(0xffffffffu, act, r);
       const u64 jj = __shfl_sync(0xffffffffu, j, r);
       if (mine) {
         const u64 p = locate(0, begin + jj);
-        if (lane == r) out[jj] = keys[p] ^ flip;
+        if (lane == r) out[jj] = key_unmap<KK>(keys[p], flip);
       }
     }
   }
   if (nvec == 0) return;
-  u64* ob = out + head;
+  K* ob = out + head;
   const u64 gb = begin + head;  // global position of ob[0]
-  const u64 ntiles = (nvec * 4 + kTileKeys - 1) / kTileKeys;
+  const u64 ntiles = (nvec * VK + kTileKeys - 1) / kTileKeys;
   const u64 gw = (u64)blockIdx.x * (kEmitThreads / 32) + (threadIdx.x >> 5);
   // each warp takes `tpw` consecutive tiles; CTAs are many and short-lived, so
   // the tiles being written at any moment form one moving window of the output
@@ -123,21 +133,21 @@ __global__ void __launch_bounds__(kEmitThreads)
   const u64 t1 = (t0 + tpw) < ntiles ? (t0 + tpw) : ntiles;
   u64 p = 0;             // pair cursor (pairs only move forward)
   u64 rs = 1, re = 0;    // cached run [rs, re) of pair p (empty)
-  u64 rk = 0;
+  u64 rk = 0;            // the run's key as a uniform 8-byte word
   for (u64 t = t0; t < t1; ++t) {
     const u64 e0 = t * kTileKeys;
-    const u64 e1 = (e0 + kTileKeys) < nvec * 4 ? (e0 + kTileKeys) : nvec * 4;
+    const u64 e1 = (e0 + kTileKeys) < nvec * VK ? (e0 + kTileKeys) : nvec * VK;
     const u64 g0 = gb + e0, glast = gb + e1 - 1;
     if (!(g0 >= rs && glast < re)) {
       p = locate(p, g0);
       rs = offs[p];
       re = offs[p + 1];
-      rk = keys[p] ^ flip;
+      rk = splat(key_unmap<KK>(keys[p], flip));
     }
     if (glast < re) {
 #pragma unroll
       for (int j = 0; j < kEmitVpl; ++j) {
-        const u64 e = e0 + ((u64)j * 32 + lane) * 4;
+        const u64 e = e0 + ((u64)j * 32 + lane) * VK;
         if (e < e1) st_v4(ob + e, rk, rk, rk, rk);
       }
       continue;
@@ -163,7 +173,7 @@ __global__ void __launch_bounds__(kEmitThreads)
           if (b <= pos) i += st;
         }
         const u64 k = __shfl_sync(0xffffffffu, wk, i);
-        if (pos < wend) ob[pos - gb] = k ^ flip;
+        if (pos < wend) ob[pos - gb] = key_unmap<KK>(k, flip);
       }
       g = wend;
       if (g < gend) q += 32;
@@ -172,14 +182,16 @@ __global__ void __launch_bounds__(kEmitThreads)
     p = locate(q, glast);
     rs = offs[p];
     re = offs[p + 1];
-    rk = keys[p] ^ flip;
+    rk = splat(key_unmap<KK>(keys[p], flip));
   }
 }
 
-void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, u64* out,
-                 u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 /*npairs_bound*/) {
+void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, void* out,
+                 u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 /*npairs_bound*/,
+                 int kk) {
   const u64 L = end > begin ? end - begin : 0;
-  const u64 wtiles = (L + kTileKeys - 1) / kTileKeys;
+  const u64 tile_keys = kTileBytes / (kk ? 4 : 8);
+  const u64 wtiles = (L + tile_keys - 1) / tile_keys;
   static int tpw = -1, idx = -1;  // CAFS_EMIT_TPW / CAFS_EMIT_IDX: tuning knobs
   if (tpw < 0) {
     const char* e = getenv("CAFS_EMIT_TPW");
@@ -193,8 +205,20 @@ void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl
   u64 grid = (wtiles + (u64)tpw * wpb - 1) / ((u64)tpw * wpb);
   if (grid < 1) grid = 1;
   (void)num_sms;
-  emit_kernel<<<(unsigned)grid, kEmitThreads, ((u64)idx + 1) * 8, st>>>(
-      keys, offs, npairs, ctl, out, begin, end, flip, (u64)tpw, (u64)idx);
+  const size_t sm = ((u64)idx + 1) * 8;
+  switch (kk) {
+    case 1:
+      emit_kernel<1><<<(unsigned)grid, kEmitThreads, sm, st>>>(
+          keys, offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx);
+      break;
+    case 2:
+      emit_kernel<2><<<(unsigned)grid, kEmitThreads, sm, st>>>(
+          keys, offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx);
+      break;
+    default:
+      emit_kernel<0><<<(unsigned)grid, kEmitThreads, sm, st>>>(
+          keys, offs, npairs, ctl, (u64*)out, begin, end, flip, (u64)tpw, (u64)idx);
+  }
 }
 
 }  // namespace cafs

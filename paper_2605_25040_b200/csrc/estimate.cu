@@ -63,8 +63,11 @@ __device__ __forceinline__ u64 warp_max_u64(u64 v) {
 
 constexpr int kFreqSlots = 2048;  // <= 50% load for 1024 samples (reference: 4096, cardinality.py:27)
 
+template <int KK>
 __global__ void __launch_bounds__(1024, 1)
-    estimate_kernel(const u64* __restrict__ x, u64 n, u64 flip, int check_prefix, DevCtl* ctl) {
+    estimate_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip, int check_prefix,
+                    DevCtl* ctl) {
+  using K = typename KeyT<KK>::T;
   __shared__ u64 fkeys[kFreqSlots];
   __shared__ u32 fcnt[kFreqSlots];
   __shared__ u64 rmin[32], rmax[32];
@@ -108,10 +111,10 @@ __global__ void __launch_bounds__(1024, 1)
   u64 stride = n / kSampleTarget;
   if (stride < 1) stride = 1;
   const bool valid = (u64)tid < m;
-  const u64 v = valid ? (x[(u64)tid * stride] ^ flip) : 0;
+  const u64 v = valid ? key_map<KK>(x[(u64)tid * stride], flip) : 0;
   if (check_prefix) {
     const u64 P = n < kMonoPrefix ? n : kMonoPrefix;
-    u64 a[16], b[16];
+    K a[16], b[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const u64 i = (u64)tid + 1024u * j;
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(1024, 1)
     }
     int found = 0;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) found |= (b[j] ^ flip) < (a[j] ^ flip);
+    for (int j = 0; j < 16; ++j) found |= key_map<KK>(b[j], flip) < key_map<KK>(a[j], flip);
     if (found) inv = 1;  // benign race: any writer sets 1
   }
   // insert the sample into the FreqSet; equal samples of a warp are merged
@@ -250,12 +253,14 @@ __global__ void __launch_bounds__(1024, 1)
 }
 
 // Full-array non-decreasing check; only launched when the prefix was sorted.
-__global__ void monotone_scan_kernel(const u64* __restrict__ x, u64 n, u64 flip, DevCtl* ctl) {
+template <int KK>
+__global__ void monotone_scan_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip,
+                                     DevCtl* ctl) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   int found = 0;
   u64 it = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i + 1 < n; i += stride, ++it) {
-    found |= ((x[i + 1] ^ flip) < (x[i] ^ flip));
+    found |= key_map<KK>(x[i + 1], flip) < key_map<KK>(x[i], flip);
     if ((it & 63) == 63) {
       if (found) break;
       if (*((volatile int*)&ctl->scan_inversion)) return;
@@ -264,14 +269,23 @@ __global__ void monotone_scan_kernel(const u64* __restrict__ x, u64 n, u64 flip,
   if (found) ctl->scan_inversion = 1;
 }
 
-void launch_estimate(const u64* x, u64 n, u64 flip, int check_prefix, DevCtl* ctl,
-                     cudaStream_t st) {
-  estimate_kernel<<<1, 1024, 0, st>>>(x, n, flip, check_prefix, ctl);
+void launch_estimate(const void* x, u64 n, u64 flip, int check_prefix, DevCtl* ctl,
+                     cudaStream_t st, int kk) {
+  switch (kk) {
+    case 1: estimate_kernel<1><<<1, 1024, 0, st>>>((const u32*)x, n, flip, check_prefix, ctl); break;
+    case 2: estimate_kernel<2><<<1, 1024, 0, st>>>((const u32*)x, n, flip, check_prefix, ctl); break;
+    default: estimate_kernel<0><<<1, 1024, 0, st>>>((const u64*)x, n, flip, check_prefix, ctl);
+  }
 }
 
-void launch_monotone_scan(const u64* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
-                          cudaStream_t st) {
-  monotone_scan_kernel<<<num_sms * 4, 512, 0, st>>>(x, n, flip, ctl);
+void launch_monotone_scan(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
+                          cudaStream_t st, int kk) {
+  const dim3 g(num_sms * 4), b(512);
+  switch (kk) {
+    case 1: monotone_scan_kernel<1><<<g, b, 0, st>>>((const u32*)x, n, flip, ctl); break;
+    case 2: monotone_scan_kernel<2><<<g, b, 0, st>>>((const u32*)x, n, flip, ctl); break;
+    default: monotone_scan_kernel<0><<<g, b, 0, st>>>((const u64*)x, n, flip, ctl);
+  }
 }
 
 }  // namespace cafs

@@ -50,4 +50,26 @@ void launch_gen_draw(u64* out, u64 n, u64 start, u64 seed, const u64* palette, u
   gen_draw_kernel<<<num_sms * 8, 256, 0, st>>>(out, n, start, seed, palette, k, cdf);
 }
 
+// 32-bit keys <-> their int64 widening (value-preserving: int32 sign-extends,
+// uint32 zero-extends), for the routes that run on a 64-bit copy
+__global__ void widen_kernel(const void* __restrict__ x, u64 n, int kk, u64* __restrict__ out) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 v = ((const u32*)x)[i];
+    out[i] = kk == 1 ? (u64)(long long)(int)v : (u64)v;
+  }
+}
+__global__ void narrow_kernel(const u64* __restrict__ x, u64 n, void* __restrict__ out) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += stride)
+    ((u32*)out)[i] = (u32)x[i];
+}
+void launch_widen(const void* x, u64 n, int kk, u64* out, int num_sms, cudaStream_t st) {
+  if (n) widen_kernel<<<num_sms * 8, 512, 0, st>>>(x, n, kk, out);
+}
+void launch_narrow(const u64* x, u64 n, int kk, void* out, int num_sms, cudaStream_t st) {
+  (void)kk;
+  if (n) narrow_kernel<<<num_sms * 8, 512, 0, st>>>(x, n, out);
+}
+
 }  // namespace cafs

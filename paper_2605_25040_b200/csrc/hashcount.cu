@@ -48,7 +48,7 @@ constexpr size_t hc_smem() {
 }
 
 struct HcArgs {
-  const u64* x;
+  const void* x;  // keys of kind KK (common.cuh)
   u64 n;
   u64 flip;
   u64 mult;
@@ -127,9 +127,13 @@ __device__ __forceinline__ void resolve_or_spill(bool active, u64 v, u64* skeys,
 // with the whole warp active (the slow path is otherwise run by a few lanes
 // of a diverged warp, leaving its L2 round trips unoverlapped).
 // RANGE = false: no dense window (launched only when the window is closed).
-template <int STAGES, int STAGE_KEYS, int QCAP, bool RANGE>
+// STAGE_KEYS counts 8-byte words; a stage holds STAGE_KEYS * 8 / sizeof(K) keys.
+template <int STAGES, int STAGE_KEYS, int QCAP, bool RANGE, int KK>
 __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   if (!gate_open(a.ctl, a.gate)) return;
+  using K = typename KeyT<KK>::T;
+  constexpr int KPV = 16 / sizeof(K);                         // keys per 16-byte vector
+  constexpr u64 SK = (u64)STAGE_KEYS * 8 / sizeof(K);         // keys per stage
   constexpr int kConsumers = kHcThreads - 32;
   static_assert((STAGE_KEYS / 2) % kConsumers == 0, "balanced stages");
   constexpr u32 kVpt = STAGE_KEYS / 2 / kConsumers;
@@ -166,12 +170,15 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   }
   __syncthreads();
 
-  // body = 16-byte aligned, even-length stretch of x; head/tail elements scalar
+  // body = 16-byte aligned stretch of whole vectors; head/tail keys scalar
   const u64 n = a.n;
-  const u64 head = (((uintptr_t)a.x) & 15) ? 1 : 0;
-  const u64 body = n > head ? ((n - head) & ~1ull) : 0;
-  const u64* xb = a.x + head;
-  const u64 nchunks = (body + STAGE_KEYS - 1) / STAGE_KEYS;
+  const K* xk = (const K*)a.x;
+  const u64 mis = (((uintptr_t)a.x) & 15) / sizeof(K);
+  const u64 head0 = mis ? (u64)KPV - mis : 0;
+  const u64 head = head0 < n ? head0 : n;
+  const u64 body = (n - head) / KPV * KPV;
+  const K* xb = xk + head;
+  const u64 nchunks = (body + SK - 1) / SK;
   const u64 my_chunks =
       nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
@@ -197,8 +204,8 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
       u32 s = 0, ph = 0;
       for (u64 it = 0; it < my_chunks; ++it) {
         if (it >= (u64)STAGES) mbar_wait(&empty[s], ph ^ 1);
-        const u64 off = (blockIdx.x + it * gridDim.x) * STAGE_KEYS;
-        const u32 bytes = (u32)(((body - off) < STAGE_KEYS ? (body - off) : STAGE_KEYS) * 8);
+        const u64 off = (blockIdx.x + it * gridDim.x) * SK;
+        const u32 bytes = (u32)(((body - off) < SK ? (body - off) : SK) * sizeof(K));
         mbar_arrive_expect_tx(&full[s], bytes);
         tma_load_1d(stage + (size_t)s * STAGE_KEYS, xb + off, bytes, &full[s]);
         if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -222,11 +229,11 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
       }
     };
     u32 s = 0, ph = 0;
-    u64 off = (u64)blockIdx.x * STAGE_KEYS;
-    const u64 off_step = (u64)gridDim.x * STAGE_KEYS;
+    u64 off = (u64)blockIdx.x * SK;
+    const u64 off_step = (u64)gridDim.x * SK;
     for (u64 it = 0; it < my_chunks; ++it, off += off_step) {
       mbar_wait(&full[s], ph);
-      const u32 nv = (u32)(((body - off) < STAGE_KEYS ? (body - off) : STAGE_KEYS) / 2);
+      const u32 nv = (u32)(((body - off) < SK ? (body - off) : SK) / KPV);
       const ulonglong2* sv = (const ulonglong2*)(stage + (size_t)s * STAGE_KEYS);
 #pragma unroll
       for (u32 q = 0; q < kVpt; ++q) {
@@ -234,31 +241,46 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
         const bool valid = i < nv;
         ulonglong2 w = make_ulonglong2(0, 0);
         if (valid) w = sv[i];
-        const u64 v0 = w.x ^ flip, v1 = w.y ^ flip;
-        const u64 d0 = v0 - base, d1 = v1 - base;
+        u64 v[KPV];
+        if constexpr (KPV == 2) {
+          v[0] = key_map<KK>((K)w.x, flip);
+          v[1] = key_map<KK>((K)w.y, flip);
+        } else {
+          v[0] = key_map<KK>((K)w.x, flip);
+          v[1] = key_map<KK>((K)(w.x >> 32), flip);
+          v[2] = key_map<KK>((K)w.y, flip);
+          v[3] = key_map<KK>((K)(w.y >> 32), flip);
+        }
+        bool all_in = RANGE;
+        if constexpr (RANGE) {
+#pragma unroll
+          for (int k = 0; k < KPV; ++k) all_in = all_in && (v[k] - base) < rlen;
+        }
         if (QCAP == 0) {
           if (valid) {
-            if (RANGE && d0 < rlen && d1 < rlen) {
-              atomicAdd(&dcnt[d0], 1u);
-              atomicAdd(&dcnt[d1], 1u);
+            if (all_in) {
+#pragma unroll
+              for (int k = 0; k < KPV; ++k) atomicAdd(&dcnt[v[k] - base], 1u);
             } else {
-              count1(v0);
-              count1(v1);
+#pragma unroll
+              for (int k = 0; k < KPV; ++k) count1(v[k]);
             }
           }
         } else {
-          bool m0 = false, m1 = false;
+          bool m[KPV];
+#pragma unroll
+          for (int k = 0; k < KPV; ++k) m[k] = false;
           if (valid) {
-            if (RANGE && d0 < rlen && d1 < rlen) {
-              atomicAdd(&dcnt[d0], 1u);
-              atomicAdd(&dcnt[d1], 1u);
+            if (all_in) {
+#pragma unroll
+              for (int k = 0; k < KPV; ++k) atomicAdd(&dcnt[v[k] - base], 1u);
             } else {
-              m0 = !fast(v0);
-              m1 = !fast(v1);
+#pragma unroll
+              for (int k = 0; k < KPV; ++k) m[k] = !fast(v[k]);
             }
           }
-          enqueue(m0, v0);
-          enqueue(m1, v1);
+#pragma unroll
+          for (int k = 0; k < KPV; ++k) enqueue(m[k], v[k]);
         }
       }
       __syncwarp();
@@ -270,9 +292,10 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
       resolve_or_spill((u32)lane < qn, (u32)lane < qn ? wq[lane] : 0ull, skeys, scnt, &sclaims,
                        &sfill, region, region_cap, a);
     }
-    if (blockIdx.x == 0 && ctid == 0) {
-      if (head && n > 0) count1(a.x[0] ^ flip);
-      if (n > head && ((n - head) & 1)) count1(a.x[n - 1] ^ flip);
+    if (blockIdx.x == 0 && ctid < 32) {  // head and tail keys (< KPV each)
+      const u64 tail0 = head + body;
+      if ((u64)ctid < head) count1(key_map<KK>(xk[ctid], flip));
+      if ((u64)ctid < n - tail0) count1(key_map<KK>(xk[tail0 + ctid], flip));
     }
   }
   __syncthreads();
@@ -539,7 +562,7 @@ void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevC
 
 size_t hash_count_smem() { return hc_smem<3, 3968, 0, true>(); }
 
-template <int ST, int SK, int QC, bool RG>
+template <int ST, int SK, int QC, bool RG, int KK = 0>
 static cudaError_t launch_hc(const HcArgs& a, u64 n, int num_sms, cudaStream_t st) {
   constexpr size_t sm = hc_smem<ST, SK, QC, RG>();
   static_assert(sm <= 232448 - 2048, "shared memory budget");
@@ -547,14 +570,15 @@ static cudaError_t launch_hc(const HcArgs& a, u64 n, int num_sms, cudaStream_t s
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(hash_count_kernel<ST, SK, QC, RG>,
+    cudaError_t e = cudaFuncSetAttribute(hash_count_kernel<ST, SK, QC, RG, KK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  const u64 chunks = (n + SK - 1) / SK;
+  const u64 keys_per_stage = (u64)SK * 8 / (KK ? 4 : 8);
+  const u64 chunks = (n + keys_per_stage - 1) / keys_per_stage;
   const int grid = (int)(chunks < (u64)num_sms ? (chunks ? chunks : 1) : (u64)num_sms);
-  hash_count_kernel<ST, SK, QC, RG><<<grid, kHcThreads, sm, st>>>(a);
+  hash_count_kernel<ST, SK, QC, RG, KK><<<grid, kHcThreads, sm, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -573,11 +597,23 @@ static int hc_variant() {
 // variant: 0 = dense-window shape (deep TMA ring, inline slow path),
 //          1 = queued shape (per-warp miss queues); without the window when the
 //              caller guarantees it is closed (gate kGateMainHash, or use_range 0)
-cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
+cudaError_t launch_hash_count(const void* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms,
-                              cudaStream_t st, int variant, int gate, u64* spill, u64* dense) {
+                              cudaStream_t st, int variant, int gate, u64* spill, u64* dense,
+                              int kk) {
   HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate, spill, dense};
   const bool window = use_range && gate != kGateMainHash && gate != kGateHash;
+  if (kk) {  // 32-bit keys: the three default shapes
+    const int v = variant == 0 && window ? 0 : (window ? 2 : 5);
+#define HC32(K)                                                                        \
+    switch (v) {                                                                       \
+      case 0: return launch_hc<3, 3968, 0, true, K>(a, n, num_sms, st);                \
+      case 2: return launch_hc<3, 1984, 64, true, K>(a, n, num_sms, st);               \
+      default: return launch_hc<3, 3968, 64, false, K>(a, n, num_sms, st);             \
+    }
+    if (kk == 1) { HC32(1) } else { HC32(2) }
+#undef HC32
+  }
   int v = hc_variant();
   if (v < 0) v = variant == 0 ? 0 : (window ? 2 : 5);
   if (!window && v == 0) v = 5;

@@ -9,20 +9,21 @@ constexpr u32 kSmallSortMax = 8192;  // single-CTA sort capacity (keys or pairs)
 constexpr u32 kBitonicMax = 2048;    // below this a bitonic network replaces the radix passes
 
 // estimate.cu
-void launch_estimate(const u64* x, u64 n, u64 flip, int check_prefix, DevCtl* ctl,
-                     cudaStream_t st);
-void launch_monotone_scan(const u64* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
-                          cudaStream_t st);
+// `kk`: key kind (common.cuh): 0 = 64-bit, 1 = int32, 2 = uint32
+void launch_estimate(const void* x, u64 n, u64 flip, int check_prefix, DevCtl* ctl,
+                     cudaStream_t st, int kk = 0);
+void launch_monotone_scan(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
+                          cudaStream_t st, int kk = 0);
 // tiny.cu
-void launch_tiny_count(const u64* x, u64 n, u64 flip, DevCtl* ctl, int num_sms, cudaStream_t st,
-                       int gate);
+void launch_tiny_count(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms, cudaStream_t st,
+                       int gate, int kk = 0);
 void launch_tiny_finalize(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,
                           cudaStream_t st, int gate);
 // hashcount.cu
 size_t hash_count_smem();
-cudaError_t launch_hash_count(const u64* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
+cudaError_t launch_hash_count(const void* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms, cudaStream_t st,
-                              int variant, int gate, u64* spill, u64* dense);
+                              int variant, int gate, u64* spill, u64* dense, int kk = 0);
 void launch_dense_pairs(DevCtl* ctl, u64* dense, u64* pkeys, u64* pcnt, u64* skeys, u64* scnt,
                         u64* soffs, u64 n_expect, cudaStream_t st, int gate);
 size_t dense_window_len();
@@ -33,8 +34,9 @@ void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevC
 void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys, u64* pcnt,
                     int num_sms, cudaStream_t st, int gate);
 // emit.cu
-void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, u64* out,
-                 u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 npairs_bound);
+void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, void* out,
+                 u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 npairs_bound,
+                 int kk = 0);
 // radix.cu
 size_t onesweep_smem(bool has_val);
 u64 onesweep_tiles(u64 n);
@@ -58,7 +60,7 @@ size_t msd_maxb_offset();
 size_t msd_span_offset();
 size_t msd_hist_offset();
 void launch_msd_span(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st);
-void launch_msd_partition(const u64* keys, u64 n, u64 flip, void* state, u64 vor, u64 vand,
+void launch_msd_partition(const u64* keys, u64 n, u64 flip, void* state, u64 kmin, u64 kmax,
                           u64* out, int num_sms, cudaStream_t st);
 bool launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st);
 void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* state, u64* tk,
@@ -67,12 +69,16 @@ void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* st
 size_t tel_accum_bytes();
 void launch_tel_build(const u64* keys, u64 np, u64* tkeys, u32* tidx, int log2s, u32* first,
                       u32* runs, void* acc, int num_sms, cudaStream_t st);
-void launch_tel_runs(const u64* x, u64 n, u64 flip, const u64* tkeys, const u32* tidx, int log2s,
-                     u32* first, u32* runs, void* acc, int num_sms, cudaStream_t st);
+void launch_tel_runs(const void* x, u64 n, u64 flip, const u64* tkeys, const u32* tidx, int log2s,
+                     u32* first, u32* runs, void* acc, int num_sms, cudaStream_t st, int kk = 0);
 void launch_tel_comp(const u64* keys, u64 np, const u32* first, u64 mult, int m_log2, int dom,
                      u64* comp, u64* cidx, int num_sms, cudaStream_t st);
 void launch_tel_classify(const u64* comp, const u64* cidx, u64 np, int cap, const u64* counts,
                          const u32* runs, void* acc, int num_sms, cudaStream_t st);
+// convert (gen.cu): 32-bit keys <-> their int64 widening, for the host-driven
+// fallback routes of a 32-bit column
+void launch_widen(const void* x, u64 n, int kk, u64* out, int num_sms, cudaStream_t st);
+void launch_narrow(const u64* x, u64 n, int kk, void* out, int num_sms, cudaStream_t st);
 // gen.cu
 void launch_gen_mix(u64* out, u64 count, u64 seed, u64 skip, int num_sms, cudaStream_t st);
 void launch_gen_draw(u64* out, u64 n, u64 start, u64 seed, const u64* palette, u64 k,

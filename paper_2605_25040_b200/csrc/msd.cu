@@ -3,13 +3,14 @@
 // Replaces fallback_sort (sorter.py:132-138) and, for more than 8192 pairs,
 // radix_sort_pairs (_kernels.py:185-214).  An LSD radix sort of 64-bit keys
 // moves 16 B/key per digit pass (8 passes for random keys); here one pass
-// partitions the keys by the 12 most significant VARYING bits (found from an
-// OR/AND reduction, so dictionary codes and clustered keys still spread), and
-// each of the 4096 buckets is then sorted entirely in shared memory by a
-// 256-thread CTA (stable 8-ballot multisplit LSD over the bytes that vary
-// inside the bucket).  DRAM traffic: 8 (reduce) + 8 (histogram) + 16 (scatter)
-// + 16 (bucket sort) = 48 B/key.  Buckets larger than kBucketCap (skewed keys,
-// or n ~ 2^30) are left to the onesweep LSD path (radix.cu) by the host.
+// partitions the keys into 4096 buckets by (k - min) >> shift over the keys'
+// numeric span (a min/max reduction, so dictionary codes, clustered and
+// sign-extended 32-bit keys still spread), and each bucket is then sorted in
+// shared memory: one warp for <= 128 keys (rank sort), else a 256-thread CTA
+// (a second split on 10 more bits + rank sort, or stable byte passes).
+// DRAM traffic: 8 (span) + 8 (histogram) + 16 (scatter) + 16 (bucket sort) =
+// 48 B/key.  Buckets larger than kBucketCap (skewed keys, or n ~ 2^30) are
+// left to the onesweep LSD path (radix.cu) by the host.
 #include <cstddef>
 
 #include "common.cuh"
@@ -38,7 +39,7 @@ constexpr u32 kMsdMaxChunks = 512;
 constexpr u64 kMsdMaxN = (u64)kMsdBuckets * kBucketCap;  // beyond: some bucket > kBucketCap
 
 struct MsdState {
-  unsigned long long vor, vand;
+  unsigned long long kmin, kmax;  // span of the order-mapped keys (adjacent: read as a pair)
   u32 hist[kMsdBuckets];
   u32 base[kMsdBuckets + 1];
   u32 cursor[kMsdBuckets];
@@ -57,42 +58,44 @@ static u64 msd_chunk(u64 n, int num_sms) {
   return c;
 }
 
-__device__ __forceinline__ u32 msd_digit(u64 k, int shift) {
-  return (u32)(k >> shift) & (kMsdBuckets - 1);
+__device__ __forceinline__ u32 msd_digit(u64 k, u64 base, int shift) {
+  return (u32)((k - base) >> shift) & (kMsdBuckets - 1);
 }
 
 __global__ void __launch_bounds__(512) msd_reduce_kernel(const u64* __restrict__ keys, u64 n,
                                                          u64 flip, MsdState* ms) {
-  u64 vor = 0, vand = ~0ull;
+  u64 lo = ~0ull, hi = 0;
   const u64 stride = (u64)gridDim.x * blockDim.x;
   u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  auto take = [&](u64 k) {
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
+  };
   for (; i + 3 * stride < n; i += 4 * stride) {  // four loads in flight per thread
     const u64 a = keys[i] ^ flip, b = keys[i + stride] ^ flip, c = keys[i + 2 * stride] ^ flip,
               d = keys[i + 3 * stride] ^ flip;
-    vor |= a | b | c | d;
-    vand &= a & b & c & d;
+    take(a); take(b); take(c); take(d);
   }
-  for (; i < n; i += stride) {
-    const u64 k = keys[i] ^ flip;
-    vor |= k;
-    vand &= k;
-  }
+  for (; i < n; i += stride) take(keys[i] ^ flip);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    vor |= __shfl_xor_sync(0xffffffffu, vor, o);
-    vand &= __shfl_xor_sync(0xffffffffu, vand, o);
+    const u64 l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = l2 < lo ? l2 : lo;
+    hi = h2 > hi ? h2 : hi;
   }
   if ((threadIdx.x & 31) == 0) {
-    atomicOr(&ms->vor, vor);
-    atomicAnd(&ms->vand, vand);
+    atomicMin(&ms->kmin, lo);
+    atomicMax(&ms->kmax, hi);
   }
 }
 
-// shift so the bucket digit covers the 12 highest bits that vary
+// shift so the bucket digit (k - kmin) >> shift covers the span in 4096 steps
+// (the numeric span, not the varying bits: sign-extended 32-bit keys vary in
+// all 32 high bits while spanning only 2^32 values)
 __device__ __forceinline__ int msd_shift(const MsdState* ms) {
-  const u64 vary = ms->vor ^ ms->vand;
-  if (vary == 0) return 0;
-  const int hb = 63 - __clzll(vary);
+  if (ms->kmax <= ms->kmin) return 0;
+  const u64 span = ms->kmax - ms->kmin;
+  const int hb = 63 - __clzll(span);
   return hb + 1 > kMsdBits ? hb + 1 - kMsdBits : 0;
 }
 
@@ -102,9 +105,10 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const u64* __restrict__ k
   for (u32 i = threadIdx.x; i < kMsdBuckets; i += blockDim.x) h[i] = 0;
   __syncthreads();
   const int shift = msd_shift(ms);
+  const u64 kbase = ms->kmin;
   const u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += stride)
-    atomicAdd(&h[msd_digit(keys[i] ^ flip, shift)], 1u);
+    atomicAdd(&h[msd_digit(keys[i] ^ flip, kbase, shift)], 1u);
   __syncthreads();
   for (u32 i = threadIdx.x; i < kMsdBuckets; i += blockDim.x)
     if (h[i]) atomicAdd(&ms->hist[i], h[i]);
@@ -166,17 +170,18 @@ __global__ void __launch_bounds__(1024) msd_chunk_hist_kernel(const u64* __restr
   for (u32 i = threadIdx.x; i < kMsdBuckets; i += 1024) h[i] = 0;
   __syncthreads();
   const int shift = msd_shift(ms);
+  const u64 kbase = ms->kmin;
   const u64 c0 = blockIdx.x * chunk;
   const u64 c1 = c0 + chunk < n ? c0 + chunk : n;
   u64 i = c0 + threadIdx.x;
   for (; i + 3 * 1024 < c1; i += 4 * 1024) {
     const u64 a = keys[i], b = keys[i + 1024], c = keys[i + 2048], d = keys[i + 3072];
-    atomicAdd(&h[msd_digit(a ^ flip, shift)], 1u);
-    atomicAdd(&h[msd_digit(b ^ flip, shift)], 1u);
-    atomicAdd(&h[msd_digit(c ^ flip, shift)], 1u);
-    atomicAdd(&h[msd_digit(d ^ flip, shift)], 1u);
+    atomicAdd(&h[msd_digit(a ^ flip, kbase, shift)], 1u);
+    atomicAdd(&h[msd_digit(b ^ flip, kbase, shift)], 1u);
+    atomicAdd(&h[msd_digit(c ^ flip, kbase, shift)], 1u);
+    atomicAdd(&h[msd_digit(d ^ flip, kbase, shift)], 1u);
   }
-  for (; i < c1; i += 1024) atomicAdd(&h[msd_digit(keys[i] ^ flip, shift)], 1u);
+  for (; i < c1; i += 1024) atomicAdd(&h[msd_digit(keys[i] ^ flip, kbase, shift)], 1u);
   __syncthreads();
   u32* row = ms->offs[blockIdx.x];
   for (u32 b = threadIdx.x; b < kMsdBuckets; b += 1024) {
@@ -202,6 +207,7 @@ __global__ void __launch_bounds__(1024)
   }
   __syncthreads();
   const int shift = ms->shift;
+  const u64 kbase = ms->kmin;
   const u64 c0 = blockIdx.x * chunk;
   const u64 c1 = c0 + chunk < n ? c0 + chunk : n;
   u64 i = c0 + threadIdx.x;
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(1024)
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const u32 d = msd_digit(k[j], shift);
+      const u32 d = msd_digit(k[j], kbase, shift);
       const u32 pos = gb[d] + atomicAdd(&lc[d], 1u);
       tk[pos] = k[j];
       if (HAS_VAL) tv[pos] = v[j];
@@ -222,7 +228,7 @@ __global__ void __launch_bounds__(1024)
   }
   for (; i < c1; i += 1024) {
     const u64 k = keys[i] ^ flip;
-    const u32 d = msd_digit(k, shift);
+    const u32 d = msd_digit(k, kbase, shift);
     const u32 pos = gb[d] + atomicAdd(&lc[d], 1u);
     tk[pos] = k;
     if (HAS_VAL) tv[pos] = vals[i];
@@ -243,6 +249,7 @@ __global__ void __launch_bounds__(kScThreads)
   for (u32 i = threadIdx.x; i < kMsdBuckets; i += kScThreads) h[i] = 0;
   __syncthreads();
   const int shift = ms->shift;
+  const u64 kbase = ms->kmin;
   const u64 c0 = (u64)blockIdx.x * kScChunk;
   u64 k[kScItems];
   u32 r[kScItems];
@@ -254,7 +261,7 @@ __global__ void __launch_bounds__(kScThreads)
 #pragma unroll
   for (int j = 0; j < kScItems; ++j) {
     const u64 i = c0 + threadIdx.x + (u64)j * kScThreads;
-    if (i < n) r[j] = atomicAdd(&h[msd_digit(k[j], shift)], 1u);
+    if (i < n) r[j] = atomicAdd(&h[msd_digit(k[j], kbase, shift)], 1u);
   }
   __syncthreads();
   for (u32 b = threadIdx.x; b < kMsdBuckets; b += kScThreads)
@@ -264,7 +271,7 @@ __global__ void __launch_bounds__(kScThreads)
   for (int j = 0; j < kScItems; ++j) {
     const u64 i = c0 + threadIdx.x + (u64)j * kScThreads;
     if (i < n) {
-      const u32 pos = g[msd_digit(k[j], shift)] + r[j];
+      const u32 pos = g[msd_digit(k[j], kbase, shift)] + r[j];
       tk[pos] = k[j] ^ out_xor;
       if (HAS_VAL) tv[pos] = vals[i];
     }
@@ -545,7 +552,7 @@ bool launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms
   if (nchunks > kMsdMaxChunks) return false;
   MsdState* ms = (MsdState*)state;
   cudaMemsetAsync(ms, 0, kMsdClear, st);
-  cudaMemsetAsync(&ms->vand, 0xFF, sizeof(u64), st);
+  cudaMemsetAsync(&ms->kmin, 0xFF, sizeof(u64), st);
   u64 blocks = (n + 512 * 8 - 1) / (512 * 8);
   if (blocks > (u64)num_sms * 4) blocks = (u64)num_sms * 4;
   if (blocks < 1) blocks = 1;
@@ -555,32 +562,32 @@ bool launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms
   return true;
 }
 
-__global__ void msd_set_span_kernel(MsdState* ms, u64 vor, u64 vand) {
-  ms->vor = vor;
-  ms->vand = vand;
+__global__ void msd_set_span_kernel(MsdState* ms, u64 kmin, u64 kmax) {
+  ms->kmin = kmin;
+  ms->kmax = kmax;
 }
 
-// Local OR/AND of the order-mapped keys (the distributed fallback all-gathers
+// Local min/max of the order-mapped keys (the distributed fallback all-gathers
 // them to fix one bucket digit for every rank).
 void launch_msd_span(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st) {
   MsdState* ms = (MsdState*)state;
   cudaMemsetAsync(ms, 0, kMsdClear, st);
-  cudaMemsetAsync(&ms->vand, 0xFF, sizeof(u64), st);
+  cudaMemsetAsync(&ms->kmin, 0xFF, sizeof(u64), st);
   u64 blocks = (n + 512 * 8 - 1) / (512 * 8);
   if (blocks > (u64)num_sms * 4) blocks = (u64)num_sms * 4;
   if (blocks < 1) blocks = 1;
   msd_reduce_kernel<<<(unsigned)blocks, 512, 0, st>>>(keys, n, flip, ms);
 }
-size_t msd_span_offset() { return offsetof(MsdState, vor); }  // vor, vand adjacent
+size_t msd_span_offset() { return offsetof(MsdState, kmin); }  // kmin, kmax adjacent
 size_t msd_hist_offset() { return offsetof(MsdState, hist); }
 
-// Group keys by the bucket digit of a GLOBAL span (vor, vand): out holds the
+// Group keys by the bucket digit of a GLOBAL span [kmin, kmax]: out holds the
 // keys (original representation) in ascending digit order; hist = counts.
-void launch_msd_partition(const u64* keys, u64 n, u64 flip, void* state, u64 vor, u64 vand,
+void launch_msd_partition(const u64* keys, u64 n, u64 flip, void* state, u64 kmin, u64 kmax,
                           u64* out, int num_sms, cudaStream_t st) {
   MsdState* ms = (MsdState*)state;
   cudaMemsetAsync(ms, 0, kMsdClear, st);
-  msd_set_span_kernel<<<1, 1, 0, st>>>(ms, vor, vand);
+  msd_set_span_kernel<<<1, 1, 0, st>>>(ms, kmin, kmax);
   u64 blocks = (n + 512 * 8 - 1) / (512 * 8);
   if (blocks > (u64)num_sms * 4) blocks = (u64)num_sms * 4;
   if (blocks < 1) blocks = 1;

@@ -61,15 +61,16 @@ __device__ __forceinline__ u32 tl_lookup(const u64* tkeys, const u32* tidx, int 
   return tidx[h];
 }
 
+template <int KK>
 __global__ void __launch_bounds__(512)
-    tl_runs_kernel(const u64* __restrict__ x, u64 n, u64 flip, const u64* tkeys, const u32* tidx,
-                   int log2s, u32* first, u32* runs, TelAccum* acc) {
+    tl_runs_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip, const u64* tkeys,
+                   const u32* tidx, int log2s, u32* first, u32* runs, TelAccum* acc) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   const u64 empty_idx = acc->empty_idx;
   u64 local = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const u64 v = x[i] ^ flip;
-    if (i > 0 && (x[i - 1] ^ flip) == v) continue;
+    const u64 v = key_map<KK>(x[i], flip);
+    if (i > 0 && key_map<KK>(x[i - 1], flip) == v) continue;
     ++local;
     const u32 j = tl_lookup(tkeys, tidx, log2s, v, empty_idx);
     atomicAdd(&runs[j], 1u);
@@ -134,10 +135,20 @@ void launch_tel_build(const u64* keys, u64 np, u64* tkeys, u32* tidx, int log2s,
                                                                    first, runs, (TelAccum*)acc);
 }
 
-void launch_tel_runs(const u64* x, u64 n, u64 flip, const u64* tkeys, const u32* tidx, int log2s,
-                     u32* first, u32* runs, void* acc, int num_sms, cudaStream_t st) {
-  tl_runs_kernel<<<num_sms * 4, 512, 0, st>>>(x, n, flip, tkeys, tidx, log2s, first, runs,
-                                              (TelAccum*)acc);
+void launch_tel_runs(const void* x, u64 n, u64 flip, const u64* tkeys, const u32* tidx, int log2s,
+                     u32* first, u32* runs, void* acc, int num_sms, cudaStream_t st, int kk) {
+  const dim3 g(num_sms * 4), b(512);
+  TelAccum* ac = (TelAccum*)acc;
+  switch (kk) {
+    case 1:
+      tl_runs_kernel<1><<<g, b, 0, st>>>((const u32*)x, n, flip, tkeys, tidx, log2s, first, runs, ac);
+      break;
+    case 2:
+      tl_runs_kernel<2><<<g, b, 0, st>>>((const u32*)x, n, flip, tkeys, tidx, log2s, first, runs, ac);
+      break;
+    default:
+      tl_runs_kernel<0><<<g, b, 0, st>>>((const u64*)x, n, flip, tkeys, tidx, log2s, first, runs, ac);
+  }
 }
 
 void launch_tel_comp(const u64* keys, u64 np, const u32* first, u64 mult, int m_log2, int dom,

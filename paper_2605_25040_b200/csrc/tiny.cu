@@ -20,8 +20,12 @@ namespace cafs {
 constexpr int kTinyThreads = 512;
 constexpr int kTinyWarps = kTinyThreads / 32;
 
+template <int KK>
 __global__ void __launch_bounds__(kTinyThreads)
-    tiny_count_kernel(const u64* __restrict__ x, u64 n, u64 flip, DevCtl* ctl, int gate) {
+    tiny_count_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip, DevCtl* ctl,
+                      int gate) {
+  using K = typename KeyT<KK>::T;
+  constexpr int KPV = 16 / sizeof(K);  // keys per 16-byte vector
   if (!gate_open(ctl, gate)) return;
   __shared__ u64 skey[16];
   __shared__ u32 cnt[kTinyWarps][16][32];
@@ -40,17 +44,27 @@ __global__ void __launch_bounds__(kTinyThreads)
 
   u32* mycnt = &cnt[wid][0][lane];
   u64 miss = 0;
-  auto count1 = [&](u64 raw) {
-    const u64 v = raw ^ flip;
+  auto count1 = [&](K raw) {
+    const u64 v = key_map<KK>(raw, flip);
     const u32 sl = (u32)((v * mult) >> 60);
     const u32 eq = (skey[sl] == v);
     mycnt[sl * 32] += eq;
     miss += 1u - eq;
   };
 
-  // 16-byte aligned body, scalar head/tail (x may be an 8-byte aligned view)
-  const u64 head = (((uintptr_t)x) & 15) ? 1 : 0;
-  const u64 nb = n > head ? (n - head) / 2 : 0;  // 16-byte vectors in the body
+  // a 16-byte vector's keys
+  auto count_vec = [&](ulonglong2 w) {
+    if constexpr (KPV == 2) {
+      count1(w.x); count1(w.y);
+    } else {
+      count1((u32)w.x); count1((u32)(w.x >> 32)); count1((u32)w.y); count1((u32)(w.y >> 32));
+    }
+  };
+  // 16-byte aligned body, scalar head/tail (x may be an element-aligned view)
+  const u64 mis = (((uintptr_t)x) & 15) / sizeof(K);
+  const u64 head0 = mis ? (u64)KPV - mis : 0;
+  const u64 head = head0 < n ? head0 : n;
+  const u64 nb = (n - head) / KPV;  // 16-byte vectors in the body
   const ulonglong2* xv = (const ulonglong2*)(x + head);
   const u64 gtid = blockIdx.x * (u64)blockDim.x + tid;
   const u64 gstride = (u64)gridDim.x * blockDim.x;
@@ -60,17 +74,12 @@ __global__ void __launch_bounds__(kTinyThreads)
     ulonglong2 b = ld_stream_v2(xv + i + gstride);
     ulonglong2 c = ld_stream_v2(xv + i + 2 * gstride);
     ulonglong2 d = ld_stream_v2(xv + i + 3 * gstride);
-    count1(a.x); count1(a.y); count1(b.x); count1(b.y);
-    count1(c.x); count1(c.y); count1(d.x); count1(d.y);
+    count_vec(a); count_vec(b); count_vec(c); count_vec(d);
   }
-  for (; i < nb; i += gstride) {
-    ulonglong2 a = ld_stream_v2(xv + i);
-    count1(a.x); count1(a.y);
-  }
-  if (gtid == 0) {
-    if (head && n > 0) count1(x[0]);
-    if (n > head && ((n - head) & 1)) count1(x[n - 1]);
-  }
+  for (; i < nb; i += gstride) count_vec(ld_stream_v2(xv + i));
+  if (gtid < head) count1(x[gtid]);  // head keys
+  const u64 tail0 = head + nb * KPV;
+  if (gtid < n - tail0) count1(x[tail0 + gtid]);  // tail keys
   // ---- reduce: per slot over warps and lanes ----
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) miss += __shfl_xor_sync(0xffffffffu, miss, o);
@@ -115,13 +124,26 @@ __global__ void tiny_finalize_kernel(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, 
   ctl->pairs_ready = (off == n);
 }
 
-void launch_tiny_count(const u64* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
-                       cudaStream_t st, int gate) {
-  u64 blocks = (n / 2 + kTinyThreads * 8 - 1) / (kTinyThreads * 8);
+void launch_tiny_count(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
+                       cudaStream_t st, int gate, int kk) {
+  const u64 kpv = kk ? 4 : 2;
+  u64 blocks = (n / kpv + kTinyThreads * 8 - 1) / (kTinyThreads * 8);
   u64 maxb = (u64)num_sms * 4;
   if (blocks > maxb) blocks = maxb;
   if (blocks < 1) blocks = 1;
-  tiny_count_kernel<<<(unsigned)blocks, kTinyThreads, 0, st>>>(x, n, flip, ctl, gate);
+  switch (kk) {
+    case 1:
+      tiny_count_kernel<1><<<(unsigned)blocks, kTinyThreads, 0, st>>>((const u32*)x, n, flip, ctl,
+                                                                      gate);
+      break;
+    case 2:
+      tiny_count_kernel<2><<<(unsigned)blocks, kTinyThreads, 0, st>>>((const u32*)x, n, flip, ctl,
+                                                                      gate);
+      break;
+    default:
+      tiny_count_kernel<0><<<(unsigned)blocks, kTinyThreads, 0, st>>>((const u64*)x, n, flip, ctl,
+                                                                      gate);
+  }
 }
 
 void launch_tiny_finalize(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,

@@ -159,20 +159,20 @@ class DeviceOps:
                    self.ctx, "fallback_sort")
 
     def key_span(self, x) -> tuple[int, int]:
-        """(OR, AND) of the order-mapped keys; (0, 2**64-1) for an empty shard."""
-        vor, vand = ctypes.c_uint64(), ctypes.c_uint64()
+        """(min, max) of the order-mapped keys; (2**64-1, 0) for an empty shard."""
+        lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
         _lib.check(self.lib.cafs_key_span_i64(self.ctx, x.data_ptr(), x.shape[0], int(self.signed),
-                                              ctypes.byref(vor), ctypes.byref(vand),
+                                              ctypes.byref(lo), ctypes.byref(hi),
                                               self._stream()), self.ctx, "key_span")
-        return int(vor.value), int(vand.value)
+        return int(lo.value), int(hi.value)
 
-    def partition(self, x, g_or: int, g_and: int):
+    def partition(self, x, g_min: int, g_max: int):
         """x grouped by the global bucket digit; (grouped tensor, counts[4096])."""
         torch = _torch()
         out = torch.empty_like(x)
         counts = np.zeros(PARTITION_BUCKETS, np.uint64)
         _lib.check(self.lib.cafs_partition_i64(
-            self.ctx, x.data_ptr(), x.shape[0], int(self.signed), g_or, g_and, out.data_ptr(),
+            self.ctx, x.data_ptr(), x.shape[0], int(self.signed), g_min, g_max, out.data_ptr(),
             counts.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), self._stream()),
             self.ctx, "partition")
         return out, counts.astype(np.int64)
@@ -269,13 +269,12 @@ class Comm:
         return torch.cat([o[:s] for o, s in zip(out, sizes)]).to(t.device)
 
 
-def msd_shift(g_or: int, g_and: int, bits: int = 12) -> int:
-    """Shift that puts the `bits` highest varying bits of the span in the digit
-    (msd.cu msd_shift)."""
-    vary = g_or ^ g_and
-    if vary == 0:
+def msd_shift(g_min: int, g_max: int, bits: int = 12) -> int:
+    """Shift that fits the span [g_min, g_max] into a `bits`-bit digit
+    (k - g_min) >> shift (msd.cu msd_shift)."""
+    if g_max <= g_min:
         return 0
-    hb = vary.bit_length() - 1
+    hb = (g_max - g_min).bit_length() - 1
     return hb + 1 - bits if hb + 1 > bits else 0
 
 
@@ -302,9 +301,9 @@ def _exchange_sort(x_local, sizes: list[int], comm, ops) -> None:
     """Distributed fallback sort: one MSD partition pass, an
     all-to-all of bucket ranges, a local sort of the received range.
 
-    1. global span: all-gather of each shard's OR/AND of the order-mapped keys
-       -> one 4096-way digit on the 12 highest varying bits, the same on every
-       rank (so bucket b precedes bucket b+1 globally);
+    1. global span: all-gather of each shard's min/max of the order-mapped
+       keys -> one 4096-way digit (k - min) >> shift, the same on every rank
+       (so bucket b precedes bucket b+1 globally);
     2. local partition by that digit (cafs_partition_i64) and an all-reduce of
        the bucket counts -> the global row range of every bucket;
     3. rank d receives, from every rank, the buckets overlapping its output
@@ -317,12 +316,12 @@ def _exchange_sort(x_local, sizes: list[int], comm, ops) -> None:
     n_local = int(x_local.shape[0])
     off = int(sum(sizes[:rank]))
     spans = comm.all_gather_ints(list(ops.key_span(x_local)))
-    g_or, g_and = 0, (1 << 64) - 1
-    for (o, a), n_r in zip(spans, sizes):
+    g_min, g_max = (1 << 64) - 1, 0
+    for (lo, hi), n_r in zip(spans, sizes):
         if n_r:
-            g_or |= o
-            g_and &= a
-    part, counts = ops.partition(x_local, g_or, g_and)
+            g_min = min(g_min, lo)
+            g_max = max(g_max, hi)
+    part, counts = ops.partition(x_local, g_min, g_max)
     totals = comm.all_reduce_sum(counts)
     ranges = bucket_ranges(totals, sizes)
     L = np.concatenate([[0], np.cumsum(counts, dtype=np.int64)])

@@ -251,15 +251,15 @@ class _Device64:
     host entry point instead.
     """
 
-    def __init__(self, x):
+    def __init__(self, x, native32: bool = False):
         torch = _torch()
         self.x = x
         self.kind, self.signed = _TORCH_KIND[str(x.dtype)]
         self.dev = _device_index(x)
-        if self.kind in ("int64", "uint64") and x.is_contiguous():
-            self.t = x
-        elif self.kind in ("int64", "uint64"):
-            self.t = x.contiguous()
+        self.native32 = native32 and self.kind in ("int32", "uint32")
+        if self.native32 or self.kind in ("int64", "uint64"):
+            # cafs_sort_i32 takes 4-byte keys as they are
+            self.t = x if x.is_contiguous() else x.contiguous()
         else:
             # widen to int64: int32 sign-extends, uint32 zero-extends (both < 2^63)
             self.t = x.to(torch.int64)
@@ -365,10 +365,11 @@ def cafs_sort(x, telemetry: SortTelemetry | None = None, hash_mult=None, *,
     t = _lib.Telemetry()
     lib = _lib.load()
     if _is_tensor(x) and x.is_cuda:
-        v = _Device64(x)
+        v = _Device64(x, native32=True)
         ctx = _lib.context(v.dev)
-        rc = lib.cafs_sort_i64(ctx, v.ptr, v.n, int(v.signed), mult, flags, ctypes.byref(t),
-                               _stream_ptr(v.dev))
+        sort = lib.cafs_sort_i32 if v.native32 else lib.cafs_sort_i64
+        rc = sort(ctx, v.ptr, v.n, int(v.signed), mult, flags, ctypes.byref(t),
+                  _stream_ptr(v.dev))
         _lib.check(rc, ctx, "cafs_sort")
         v.write_back()
         kind = v.kind
@@ -382,18 +383,16 @@ def _host_sort(x, mult: int, flags: int, t: _lib.Telemetry) -> str:
     torch = _torch()
     arr = x.numpy() if _is_tensor(x) else x
     kind = arr.dtype.name
-    if kind in ("int32", "uint32"):
-        work = arr.astype(np.int64)
-        signed = 1
-    else:
-        work = arr if arr.flags.c_contiguous else np.ascontiguousarray(arr)
-        signed = int(arr.dtype.kind == "i")
+    work = arr if arr.flags.c_contiguous else np.ascontiguousarray(arr)
+    signed = int(arr.dtype.kind == "i")
     dev = torch.cuda.current_device() if torch.cuda.is_available() else 0
     ctx = _lib.context(dev)
     lib = _lib.load()
     ptr = work.ctypes.data if work.shape[0] else 0
-    rc = lib.cafs_sort_i64_host(ctx, ptr, ptr, work.shape[0], signed, mult, flags,
-                                ctypes.byref(t), _stream_ptr(dev) if torch.cuda.is_available() else 0)
+    # 4-byte keys cross PCIe as 4 bytes (cafs_sort_i32_host)
+    sort = lib.cafs_sort_i32_host if kind in ("int32", "uint32") else lib.cafs_sort_i64_host
+    rc = sort(ctx, ptr, ptr, work.shape[0], signed, mult, flags, ctypes.byref(t),
+              _stream_ptr(dev) if torch.cuda.is_available() else 0)
     _lib.check(rc, ctx, "cafs_sort")
     if work is not arr:
         arr[...] = work.astype(arr.dtype) if work.dtype != arr.dtype else work

@@ -53,3 +53,14 @@ def sweep_input(case):
 @pytest.fixture(scope="session")
 def known_answers():
     return load_json("known_answers.json")
+
+
+_dtype32_arrays = None
+
+
+def dtype32_input(name):
+    """Input array (int32 / uint32) of a golden 32-bit case."""
+    global _dtype32_arrays
+    if _dtype32_arrays is None:
+        _dtype32_arrays = dict(np.load(os.path.join(GOLDEN, "dtype32_inputs.npz")))
+    return _dtype32_arrays[name].copy()

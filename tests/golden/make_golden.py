@@ -213,6 +213,45 @@ def special_cases() -> tuple[list[dict], dict]:
     return recs, arrays
 
 
+def dtype32_cases() -> tuple[list[dict], dict]:
+    """int32 / uint32 columns through the reference (SUPPORTED_DTYPES, sorter.py:34):
+    every route, and bucket-table spills in the 32-bit unsigned domain."""
+    arrays, recs = {}, []
+
+    def add(name, x, mult=None):
+        arrays[name] = x
+        rec = run_ref(x, mult)
+        rec["name"] = name
+        rec["dtype"] = str(x.dtype)
+        if mult is not None:
+            rec["hash_mult"] = mult
+        recs.append(rec)
+
+    i32 = np.iinfo(np.int32)
+    rng = np.random.default_rng(320)
+    add("i32_tiny", np.array([-7, -1, 0, 5, i32.max, i32.min], np.int32)[rng.integers(0, 6, 100_000)])
+    z = np.minimum(rng.zipf(1.3, 500_000), 3000).astype(np.int32) - 1
+    add("i32_main_codes", z)
+    pal = rng.integers(i32.min, i32.max, 30_000, dtype=np.int32)
+    add("i32_main_hash", pal[np.minimum(rng.zipf(1.1, 400_000), 30_000) - 1])
+    pal = np.array([i32.min, i32.min + 1, -2, -1, 0, 1, i32.max - 1, i32.max]
+                   + list(range(1000, 1100)), np.int32)
+    add("i32_extremes_main", pal[rng.integers(0, pal.shape[0], 80_000)])
+    add("i32_distinct", rng.permutation(np.arange(-100_000, 100_000, dtype=np.int32) * 7919))
+    add("i32_small_n", rng.integers(-50, 50, 1500).astype(np.int32))
+    add("i32_sorted", np.arange(-30_000, 30_000, dtype=np.int32))
+    u32 = np.iinfo(np.uint32)
+    pal = np.array([0, 1, 77, u32.max - 1, u32.max] + list(range(5000, 5300)), np.uint32)
+    add("u32_main", pal[rng.integers(0, pal.shape[0], 300_000)])
+    add("u32_tiny", np.array([3, 9, u32.max], np.uint32)[rng.integers(0, 3, 50_000)])
+    cand = np.arange(1, 1 + (64 << (7 + 4)), dtype=np.uint32)
+    colliders = cand[buckets.fast_hash(cand, 7) == 0][:64]
+    add("u32_colliders", colliders[rng.integers(0, 64, 20_000)])
+    add("i32_alt_mult", pal[rng.integers(0, pal.shape[0], 100_000)].astype(np.int32) - 2000,
+        ALT_MULT)
+    return recs, arrays
+
+
 def config_cases() -> list[dict]:
     out = []
     for name in ("cfg1", "cfg2", "cfg3", "cfg5"):
@@ -243,8 +282,19 @@ def config_cases() -> list[dict]:
     return out
 
 
+def write_dtype32() -> None:
+    recs, arrays = dtype32_cases()
+    np.savez_compressed(os.path.join(HERE, "dtype32_inputs.npz"), **arrays)
+    with open(os.path.join(HERE, "dtype32_cases.json"), "w") as f:
+        json.dump(recs, f, indent=0)
+
+
 def main():
     os.makedirs(HERE, exist_ok=True)
+    if "--only-dtype32" in sys.argv:
+        write_dtype32()
+        return
+    write_dtype32()
     with open(os.path.join(HERE, "known_answers.json"), "w") as f:
         json.dump(known_answers(), f)
     recs, arrays = special_cases()

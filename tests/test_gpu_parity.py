@@ -14,7 +14,7 @@ import pytest
 
 torch = pytest.importorskip("torch")
 
-from conftest import load_json, special_input, sweep_input  # noqa: E402
+from conftest import dtype32_input, load_json, special_input, sweep_input  # noqa: E402
 from oracle import cafs_oracle as orc  # noqa: E402
 from oracle import gen as ogen  # noqa: E402
 
@@ -391,3 +391,52 @@ def test_guard_then_dense_window():
     t = to_dev(y)
     cafs.cafs_sort(t)
     assert np.array_equal(t.cpu().numpy(), np.sort(y))
+
+
+@pytest.mark.parametrize("rec", load_json("dtype32_cases.json"), ids=lambda r: r["name"])
+def test_dtype32_native_path(rec):
+    """int32 / uint32 columns on the 4-byte-key path (cafs_sort_i32): sorted
+    bytes, decision and the reference's bucket-table telemetry (hashed in the
+    32-bit unsigned domain) against the reference's own outputs."""
+    x = dtype32_input(rec["name"])
+    mult = rec.get("hash_mult")
+    for exact in (False, True):
+        t = to_dev(x)
+        tel = SortTelemetry()
+        cafs.cafs_sort(t, telemetry=tel, hash_mult=mult, exact_telemetry=exact)
+        torch.cuda.synchronize()
+        assert sha(t) == rec["sha256"]
+        check_decision(tel, rec)
+        if exact:
+            check_exact(tel, rec)
+    y = x.copy()  # numpy: 4 bytes per key over PCIe (cafs_sort_i32_host)
+    cafs.cafs_sort(y, hash_mult=mult)
+    assert sha(y) == rec["sha256"]
+    if x.shape[0] > 4:  # a view 4 bytes past a 16-byte boundary: head/tail paths
+        full = to_dev(np.concatenate([x[:1], x]))
+        v = full[1:]
+        cafs.cafs_sort(v, hash_mult=mult)
+        assert np.array_equal(v.cpu().numpy(), np.sort(x)) and full[0].item() == x[0]
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.uint32])
+def test_dtype32_routes_at_scale(dtype):
+    """Large 32-bit columns through every route, including the guard."""
+    info = np.iinfo(dtype)
+    rng = np.random.default_rng(77)
+    cases = {
+        "tiny": np.array([info.min, 0, 5, info.max], dtype)[rng.integers(0, 4, 8_000_000)],
+        "dense": (np.minimum(rng.zipf(1.2, 6_000_000), 4000) + (0 if dtype == np.uint32 else -2000)).astype(dtype),
+        "hash": rng.integers(info.min, info.max, 200_000, dtype=dtype)[rng.integers(0, 200_000, 5_000_000)],
+        "fallback": rng.integers(info.min, info.max, 3_000_001, dtype=dtype),
+    }
+    g = ogen.mix_outputs(5, 5_000_000).astype(dtype)  # ~all distinct ...
+    g[::5_000_000 // 1024][:1024] = (np.arange(1024) % 100).astype(dtype)  # ... low estimate
+    cases["guard"] = g
+    for name, x in cases.items():
+        t = to_dev(x)
+        tel = SortTelemetry()
+        cafs.cafs_sort(t, telemetry=tel)
+        assert np.array_equal(t.cpu().numpy(), np.sort(x)), name
+        if name == "guard":
+            assert tel.route is Route.MAIN and tel.guard_fired

@@ -107,10 +107,12 @@ def test_distributed_fallback_bucket_ranges():
     """Bucket ranges of the distributed fallback (sharded._exchange_sort)."""
     from paper_2605_25040_b200.sharded import bucket_ranges, msd_shift
     assert msd_shift(0, 0) == 0
-    assert msd_shift(0xFFF, 0) == 0
-    assert msd_shift(0x1FFF, 0) == 1
-    assert msd_shift((1 << 64) - 1, 0) == 52
-    assert msd_shift(0x8000_0000_0000_00FF, 0x8000_0000_0000_0000) == 0
+    assert msd_shift(0, 0xFFF) == 0
+    assert msd_shift(0, 0x1FFF) == 1
+    assert msd_shift(0, (1 << 64) - 1) == 52
+    assert msd_shift(0x8000_0000_0000_0000, 0x8000_0000_0000_00FF) == 0
+    # sign-extended int32 keys: a 2^32 span although all 32 high bits vary
+    assert msd_shift(0x7FFF_FFFF_8000_0000, 0x8000_0000_7FFF_FFFF) == 20
     rng = np.random.default_rng(3)
     for _ in range(200):
         totals = rng.integers(0, 5, 16) * rng.integers(0, 2, 16)

@@ -12,7 +12,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from conftest import load_json, special_input, sweep_input
+from conftest import dtype32_input, load_json, special_input, sweep_input
 from oracle import cafs_oracle as orc
 from oracle import gen as ogen
 
@@ -106,3 +106,22 @@ def test_cfg4_dispatch_sparse():
     assert (k_hat, e.u, e.f1, e.f2, e.saturated) == (
         rec["k_hat"], rec["u"], rec["f1"], rec["f2"], rec["saturated"])
     assert orc.table_size_for(k_hat, c.n, 4) == rec["table_buckets"]
+
+
+@pytest.mark.parametrize("rec", load_json("dtype32_cases.json"), ids=lambda r: r["name"])
+def test_dtype32_cases_match_widened_oracle(rec):
+    """A 32-bit column sorts and dispatches exactly as its int64 widening: the
+    premise of the device's 32-bit path (keys widened in registers).  The
+    bucket-table counters hash in the 32-bit unsigned domain and are checked
+    against these goldens on the GPU (tests/test_gpu_parity.py)."""
+    x = dtype32_input(rec["name"])
+    w = x.astype(np.int64)
+    y = w.copy()
+    tel = orc.cafs_sort(y, rec.get("hash_mult", orc.HASH_MULT))
+    assert _sha(y.astype(x.dtype)) == rec["sha256"]
+    assert tel.route == rec["route"]  # the guard keeps the route MAIN (sorter.py:264-273)
+    if rec["k_hat"] is not None:
+        e = tel.decision.estimate
+        assert (e.k_hat, e.u, e.f1, e.f2, e.saturated) == (
+            rec["k_hat"], rec["u"], rec["f1"], rec["f2"], rec["saturated"])
+    assert tel.tiny_count_failed == rec["tiny_count_failed"]

@@ -69,12 +69,13 @@ class NumpyOps:
     def key_span(self, x):
         u = self._u(x)
         if u.shape[0] == 0:
-            return 0, (1 << 64) - 1
-        return int(np.bitwise_or.reduce(u)), int(np.bitwise_and.reduce(u))
+            return (1 << 64) - 1, 0
+        return int(u.min()), int(u.max())
 
-    def partition(self, x, g_or, g_and):
+    def partition(self, x, g_min, g_max):
         from paper_2605_25040_b200.sharded import PARTITION_BUCKETS, msd_shift
-        d = ((self._u(x) >> np.uint64(msd_shift(g_or, g_and))) & np.uint64(4095)).astype(np.int64)
+        sh = np.uint64(msd_shift(g_min, g_max))
+        d = (((self._u(x) - np.uint64(g_min)) >> sh) & np.uint64(4095)).astype(np.int64)
         order = np.argsort(d, kind="stable")
         return (torch.from_numpy(x.numpy()[order].copy()),
                 np.bincount(d, minlength=PARTITION_BUCKETS).astype(np.int64))
