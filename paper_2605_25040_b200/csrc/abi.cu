@@ -90,6 +90,7 @@ struct cafs_ctx {
     uint64_t launches = 0;  // kernels in the captured graph
     uint64_t stamp = 0;
     int kk = 0;             // key kind the graph was captured for
+    int exact = 0;          // exact-telemetry calls leave the emit out of the graph
   } graphs[16];
   uint64_t graph_clock = 0;
 };
@@ -610,7 +611,7 @@ int launch_pipeline(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_
   cafs_ctx_t::GraphEntry* lru = &ctx->graphs[0];
   for (auto& g : ctx->graphs) {
     if (g.seen && g.x == (u64)x && g.n == n && g.flip == flip && g.mult == mult &&
-        g.flags == flags && g.timing == timing && g.kk == kk) {
+        g.flags == flags && g.timing == timing && g.kk == kk && g.exact == (int)exact) {
       hit = &g;
       break;
     }
@@ -630,6 +631,7 @@ int launch_pipeline(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_
     *lru = cafs_ctx_t::GraphEntry();
     lru->x = (u64)x; lru->n = n; lru->flip = flip; lru->mult = mult; lru->flags = flags;
     lru->timing = timing; lru->seen = 1; lru->stamp = ++ctx->graph_clock; lru->kk = kk;
+    lru->exact = exact ? 1 : 0;
     pipeline_direct(ctx, x, n, flip, mult, flags, tm, st, exact, mark, &rc, kk);
     CKL();
     return rc;

@@ -239,7 +239,9 @@ def _device_index(t) -> int:
 
 
 def _stream_ptr(dev: int) -> int:
-    return _torch().cuda.current_stream(dev).cuda_stream
+    torch = _torch()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # skips the Stream object
+    return raw(dev) if raw is not None else torch.cuda.current_stream(dev).cuda_stream
 
 
 class _Device64:
@@ -355,30 +357,29 @@ def cafs_sort(x, telemetry: SortTelemetry | None = None, hash_mult=None, *,
     _validate(x)
     mult = check_hash_mult(hash_mult)
     want = telemetry is not None
-    if telemetry is None:
-        telemetry = SortTelemetry()
     flags = (_lib.FLAG_TIMING if want else 0) | (0 if direct_range else _lib.FLAG_NO_DIRECT)
     if want and exact_telemetry:
         flags |= _lib.FLAG_EXACT_TELEMETRY
         kind0 = _kind(x)[0]
         flags |= {"int32": _lib.FLAG_DOM_I32, "uint32": _lib.FLAG_DOM_U32}.get(kind0, 0)
-    t = _lib.Telemetry()
+    t = _lib.Telemetry() if want else None  # no telemetry: the C side keeps its own
     lib = _lib.load()
     if _is_tensor(x) and x.is_cuda:
         v = _Device64(x, native32=True)
         ctx = _lib.context(v.dev)
         sort = lib.cafs_sort_i32 if v.native32 else lib.cafs_sort_i64
-        rc = sort(ctx, v.ptr, v.n, int(v.signed), mult, flags, ctypes.byref(t),
-                  _stream_ptr(v.dev))
+        rc = sort(ctx, v.ptr, v.n, int(v.signed), mult, flags,
+                  ctypes.byref(t) if want else None, _stream_ptr(v.dev))
         _lib.check(rc, ctx, "cafs_sort")
         v.write_back()
         kind = v.kind
     else:
         kind = _host_sort(x, mult, flags, t)
-    _fill_telemetry(telemetry, t, kind, want)
+    if want:
+        _fill_telemetry(telemetry, t, kind, want)
 
 
-def _host_sort(x, mult: int, flags: int, t: _lib.Telemetry) -> str:
+def _host_sort(x, mult: int, flags: int, t: _lib.Telemetry | None) -> str:
     """numpy / CPU-tensor input: one H2D, the device pipeline, one D2H."""
     torch = _torch()
     arr = x.numpy() if _is_tensor(x) else x
@@ -391,7 +392,8 @@ def _host_sort(x, mult: int, flags: int, t: _lib.Telemetry) -> str:
     ptr = work.ctypes.data if work.shape[0] else 0
     # 4-byte keys cross PCIe as 4 bytes (cafs_sort_i32_host)
     sort = lib.cafs_sort_i32_host if kind in ("int32", "uint32") else lib.cafs_sort_i64_host
-    rc = sort(ctx, ptr, ptr, work.shape[0], signed, mult, flags, ctypes.byref(t),
+    rc = sort(ctx, ptr, ptr, work.shape[0], signed, mult, flags,
+              ctypes.byref(t) if t is not None else None,
               _stream_ptr(dev) if torch.cuda.is_available() else 0)
     _lib.check(rc, ctx, "cafs_sort")
     if work is not arr:

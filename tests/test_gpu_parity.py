@@ -440,3 +440,36 @@ def test_dtype32_routes_at_scale(dtype):
         assert np.array_equal(t.cpu().numpy(), np.sort(x)), name
         if name == "guard":
             assert tel.route is Route.MAIN and tel.guard_fired
+
+
+@pytest.mark.parametrize("direct", [True, False])
+def test_graph_replay_every_route(direct):
+    """Repeated sorts of one buffer: the 1st call runs the gated pipeline, the
+    2nd captures a CUDA graph with conditional route bodies, later calls replay
+    it -- for every route, including a tiny-count miss and the 32-bit path."""
+    rng = np.random.default_rng(99)
+    tiny = np.array([-5, 3, 1 << 40], np.int64)[rng.integers(0, 3, 500_000)]
+    miss = tiny.copy()
+    miss[7] = 11  # never sampled: the tiny route re-enters MAIN
+    inputs = {
+        "tiny": tiny, "tiny_miss": miss,
+        "dense": (np.minimum(rng.zipf(1.3, 800_000), 3000)).astype(np.int64),
+        "hash": ogen.CONFIGS["cfg3"].generate(600_000),
+        "fallback": ogen.mix_outputs(3, 400_000).view(np.int64).copy(),
+        "sorted": np.arange(-100_000, 100_000, dtype=np.int64),
+        "dense_i32": (np.minimum(rng.zipf(1.3, 800_000), 3000) - 1500).astype(np.int32),
+        "hash_i32": rng.integers(-2**31, 2**31 - 1, 50_000, dtype=np.int32)[rng.integers(0, 50_000, 700_000)],
+    }
+    for name, x in inputs.items():
+        want = np.sort(x)
+        pristine = to_dev(x)
+        t = torch.empty_like(pristine)
+        for it in range(4):
+            t.copy_(pristine)
+            cafs.cafs_sort(t, direct_range=direct)
+            assert np.array_equal(t.cpu().numpy(), want), (name, it)
+        tel = SortTelemetry()  # and a telemetry call on the same buffer (timed graph)
+        t.copy_(pristine)
+        cafs.cafs_sort(t, telemetry=tel, direct_range=direct)
+        assert np.array_equal(t.cpu().numpy(), want), name
+        assert tel.tiny_count_failed == (name == "tiny_miss")
