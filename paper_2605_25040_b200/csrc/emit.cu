@@ -34,15 +34,6 @@ __device__ __forceinline__ void st_v4(void* p, u64 a, u64 b, u64 c, u64 d) {
                : "memory");
 }
 
-// largest p in [lo, hi] with offs[p] <= g  (offs non-decreasing, offs[lo] <= g)
-__device__ __forceinline__ u64 find_pair(const u64* offs, u64 lo, u64 hi, u64 g) {
-  while (lo < hi) {
-    const u64 mid = (lo + hi + 1) >> 1;
-    if (offs[mid] <= g) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
 // Warp-cooperative 32-ary search: the largest p in [lo, hi] with offs[p] <= g
 // (offs non-decreasing, offs[lo] <= g).  Every lane returns it.
 __device__ __forceinline__ u64 warp_find(const u64* offs, u64 lo, u64 hi, u64 g) {

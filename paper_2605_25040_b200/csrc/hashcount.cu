@@ -25,8 +25,6 @@
 //   * the guard: global table overflow (more than kGlobalCap distinct keys or
 //     a probe chain over kGlobalMaxProbe) sets ctl->overflow and the pipeline
 //     re-routes to the fallback radix sort (reference guard: sorter.py:264-273).
-#include <cstdlib>
-
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -560,8 +558,6 @@ void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevC
                                                          glist);
 }
 
-size_t hash_count_smem() { return hc_smem<3, 3968, 0, true>(); }
-
 template <int ST, int SK, int QC, bool RG, int KK = 0>
 static cudaError_t launch_hc(const HcArgs& a, u64 n, int num_sms, cudaStream_t st) {
   constexpr size_t sm = hc_smem<ST, SK, QC, RG>();
@@ -582,49 +578,27 @@ static cudaError_t launch_hc(const HcArgs& a, u64 n, int num_sms, cudaStream_t s
   return cudaGetLastError();
 }
 
-// Pipeline-shape variants (CAFS_HC_VARIANT, tuning only).  Default: the
-// direct-window shape when the estimate kernel opened a dense window (few
-// misses expected), the queued shape otherwise.
-static int hc_variant() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("CAFS_HC_VARIANT");
-    v = e ? atoi(e) : -1;
-  }
-  return v;
-}
-
-// variant: 0 = dense-window shape (deep TMA ring, inline slow path),
-//          1 = queued shape (per-warp miss queues); without the window when the
-//              caller guarantees it is closed (gate kGateMainHash, or use_range 0)
+// shapes: 0 = dense window (deep TMA ring, inline slow path); 1 = queued (per-
+// warp miss queues and the spill), with the window when the caller may have it
+// open, without it (more shared memory for the ring) when the gate guarantees
+// it is closed (kGateMainHash / kGateHash) or use_range is 0
 cudaError_t launch_hash_count(const void* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms,
                               cudaStream_t st, int variant, int gate, u64* spill, u64* dense,
                               int kk) {
   HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate, spill, dense};
   const bool window = use_range && gate != kGateMainHash && gate != kGateHash;
-  if (kk) {  // 32-bit keys: the three default shapes
-    const int v = variant == 0 && window ? 0 : (window ? 2 : 5);
-#define HC32(K)                                                                        \
-    switch (v) {                                                                       \
-      case 0: return launch_hc<3, 3968, 0, true, K>(a, n, num_sms, st);                \
-      case 2: return launch_hc<3, 1984, 64, true, K>(a, n, num_sms, st);               \
-      default: return launch_hc<3, 3968, 64, false, K>(a, n, num_sms, st);             \
-    }
-    if (kk == 1) { HC32(1) } else { HC32(2) }
-#undef HC32
+  const int v = variant == 0 && window ? 0 : (window ? 1 : 2);
+#define HC_SHAPES(K)                                                                   \
+  switch (v) {                                                                         \
+    case 0: return launch_hc<3, 3968, 0, true, K>(a, n, num_sms, st);                  \
+    case 1: return launch_hc<3, 1984, 64, true, K>(a, n, num_sms, st);                 \
+    default: return launch_hc<3, 3968, 64, false, K>(a, n, num_sms, st);               \
   }
-  int v = hc_variant();
-  if (v < 0) v = variant == 0 ? 0 : (window ? 2 : 5);
-  if (!window && v == 0) v = 5;
-  if (window && v == 5) v = 2;
-  switch (v) {
-    case 2: return launch_hc<3, 1984, 64, true>(a, n, num_sms, st);   // queued, window
-    case 3: return launch_hc<2, 5952, 64, false>(a, n, num_sms, st);
-    case 4: return launch_hc<4, 1984, 64, false>(a, n, num_sms, st);
-    case 5: return launch_hc<3, 3968, 64, false>(a, n, num_sms, st);  // queued default
-    default: return launch_hc<3, 3968, 0, true>(a, n, num_sms, st);   // dense window
-  }
+  if (kk == 1) { HC_SHAPES(1) }
+  if (kk == 2) { HC_SHAPES(2) }
+  HC_SHAPES(0)
+#undef HC_SHAPES
 }
 
 void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys, u64* pcnt,

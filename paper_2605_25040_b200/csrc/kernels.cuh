@@ -20,7 +20,6 @@ void launch_tiny_count(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
 void launch_tiny_finalize(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,
                           cudaStream_t st, int gate);
 // hashcount.cu
-size_t hash_count_smem();
 cudaError_t launch_hash_count(const void* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms, cudaStream_t st,
                               int variant, int gate, u64* spill, u64* dense, int kk = 0);

@@ -599,7 +599,6 @@ void launch_msd_partition(const u64* keys, u64 n, u64 flip, void* state, u64 kmi
                                                                        out, nullptr, flip);
 }
 
-u32 msd_read_max(const void* state_host_copy) { return ((const MsdState*)state_host_copy)->maxb; }
 size_t msd_maxb_offset() { return offsetof(MsdState, maxb); }
 
 // keys (and vals) -> tmp (bucketed) -> dk/dv sorted; dk may equal keys
