@@ -211,6 +211,42 @@ int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_s
                        uint64_t g_min, uint64_t g_max, int64_t* d_out, uint64_t* h_counts,
                        void* stream);
 
+/* ---- stream-ordered sharded sort (one process per GPU, row shards) ----
+ * The host-driven sharded path (sharded.py) synchronises between every
+ * collective; these four calls enqueue the local phases on `stream` with the
+ * decisions taken on device, so a rank synchronises once (in finish).  The
+ * caller runs the collectives in between (NCCL, stream-ordered):
+ *   begin(x) -> d_hdr[8]                       all-gather -> d_hdr_all[world*8]
+ *   sample(x, d_hdr_all) -> d_samples[1024]    all-reduce SUM
+ *   count(x, d_samples) -> d_tiny[32], d_send[1+2*cap]
+ *                      all-reduce SUM d_tiny; all-gather d_send -> d_recv
+ *   finish(x, d_tiny, d_recv) -> x = this rank's rows of the sorted column
+ * *h_status = 0: done (route and estimate in tel); 1: this column needs the
+ * host-driven path (fallback routes, tiny miss, table overflow, more than
+ * cap pairs on a rank or 8192 merged) -- every rank returns the same status.
+ * int64 / uint64 only.  The dispatch is sorter.py:141-162 on the global
+ * column. */
+#define CAFS_SHARD_HDR_WORDS 8
+#define CAFS_SHARD_TINY_WORDS 32
+int cafs_shard_begin_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                         uint64_t* d_hdr, void* stream);
+int cafs_shard_sample_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                          const uint64_t* d_hdr_all, int world, int rank, uint64_t* d_samples,
+                          void* stream);
+int cafs_shard_count_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                         uint64_t hash_mult, const uint64_t* d_hdr_all, int world,
+                         const uint64_t* d_samples, uint64_t* d_tiny, uint64_t* d_send,
+                         uint64_t cap, void* stream);
+int cafs_shard_finish_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed,
+                          const uint64_t* d_tiny_sum, const uint64_t* d_recv, int world,
+                          uint64_t cap, cafs_telemetry_t* tel, int* h_status, void* stream);
+
+/* After finish returned status 1 on the main route: this shard's (key, count)
+ * pairs from the count phase, for the host-driven merge; *h_npairs = ~0 when
+ * they were lost to a table overflow (the guard). */
+int cafs_shard_local_pairs_i64(cafs_ctx_t* ctx, uint64_t* d_keys, uint64_t* d_counts,
+                               uint64_t cap, uint64_t* h_npairs, void* stream);
+
 /* Kernels this context has launched since it was created (monotone; the
  * per-call count of cafs_sort_i64 is also in cafs_telemetry_t.kernels_launched).
  * No reference counterpart: launch accounting for the multi-GPU bench. */

@@ -77,6 +77,12 @@ SIGNATURES = {
     "cafs_emit_i64": (_I, [_P, _P, _P, _U64, _P, _U64, _U64, _U64, _I, _P]),
     "cafs_fallback_sort_i64": (_I, [_P, _P, _U64, _I, _P]),
     "cafs_ctx_kernel_count": (_U64, [_P]),
+    "cafs_shard_begin_i64": (_I, [_P, _P, _U64, _I, _P, _P]),
+    "cafs_shard_local_pairs_i64": (_I, [_P, _P, _P, _U64, ctypes.POINTER(_U64), _P]),
+    "cafs_shard_sample_i64": (_I, [_P, _P, _U64, _I, _P, _I, _I, _P, _P]),
+    "cafs_shard_count_i64": (_I, [_P, _P, _U64, _I, _U64, _P, _I, _P, _P, _P, _U64, _P]),
+    "cafs_shard_finish_i64": (_I, [_P, _P, _U64, _I, _P, _P, _I, _U64, ctypes.POINTER(Telemetry),
+                                   ctypes.POINTER(_I), _P]),
     "cafs_key_span_i64": (_I, [_P, _P, _U64, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), _P]),
     "cafs_partition_i64": (_I, [_P, _P, _U64, _I, _U64, _U64, _P, ctypes.POINTER(_U64), _P]),
     "cafs_gen_mix": (_I, [_P, _U64, _U64, _U64, _P]),

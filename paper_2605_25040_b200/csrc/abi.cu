@@ -1208,6 +1208,146 @@ int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_s
 
 uint64_t cafs_ctx_kernel_count(const cafs_ctx_t* ctx) { return ctx ? ctx->launches : 0; }
 
+// After cafs_shard_finish_i64 returned status 1 on the main route: this shard's
+// (key, count) pairs from the count phase, for the host-driven exchange and
+// merge (sorted when they fitted the device pair sort).  *h_npairs = ~0 when
+// they were lost to a global-table overflow (the guard).
+int cafs_shard_local_pairs_i64(cafs_ctx_t* ctx, uint64_t* d_keys, uint64_t* d_counts,
+                               uint64_t cap, uint64_t* h_npairs, void* stream) {
+  if (!ctx || !h_npairs) return CAFS_EINVAL;
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(ensure_main(ctx));
+  TRY(sync_ctl(ctx, st));
+  const DevCtl& c = *ctx->h_ctl;
+  if (c.local_overflow) { *h_npairs = ~0ull; return CAFS_OK; }
+  const u64 np = c.local_npairs;
+  *h_npairs = np;
+  if (np > cap) return fail(ctx, CAFS_EINVAL, "output capacity too small");
+  const u64* k = c.local_sorted ? ctx->pk_b : ctx->pk_a;
+  const u64* v = c.local_sorted ? ctx->pc_b : ctx->pc_a;
+  if (np) {
+    CK(cudaMemcpyAsync(d_keys, k, np * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(d_counts, v, np * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return CAFS_OK;
+}
+
+// ---- stream-ordered sharded pipeline (shard.cu); no host synchronisation
+// until cafs_shard_finish_i64 ----
+int cafs_shard_begin_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                         uint64_t* d_hdr, void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  if (!d_hdr) return fail(ctx, CAFS_EINVAL, "null header buffer");
+  DeviceGuard g(ctx->device);
+  launch_shard_header((const u64*)d_x, n, is_signed ? kSign : 0, (u64*)d_hdr, ctx->num_sms,
+                      (cudaStream_t)stream);
+  ctx->launches += 2;
+  CKL();
+  return CAFS_OK;
+}
+
+int cafs_shard_sample_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                          const uint64_t* d_hdr_all, int world, int rank, uint64_t* d_samples,
+                          void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  if (!d_hdr_all || !d_samples || world < 1 || rank < 0 || rank >= world)
+    return fail(ctx, CAFS_EINVAL, "bad shard arguments");
+  DeviceGuard g(ctx->device);
+  TRY(ensure_main(ctx));
+  launch_shard_samples((const u64*)d_x, n, is_signed ? kSign : 0, (const u64*)d_hdr_all, world,
+                       rank, (u64*)d_samples, ctx->d_ctl, (cudaStream_t)stream);
+  ctx->launches++;
+  CKL();
+  return CAFS_OK;
+}
+
+int cafs_shard_count_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_signed,
+                         uint64_t hash_mult, const uint64_t* d_hdr_all, int world,
+                         const uint64_t* d_samples, uint64_t* d_tiny, uint64_t* d_send,
+                         uint64_t cap, void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  if (!d_hdr_all || !d_samples || !d_tiny || !d_send || world < 1 || (hash_mult & 1) == 0)
+    return fail(ctx, CAFS_EINVAL, "bad shard arguments");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(ensure_main(ctx));
+  DevCtl* c = ctx->d_ctl;
+  const u64* x = (const u64*)d_x;
+  const u64 flip = is_signed ? kSign : 0;
+  launch_estimate_sharded((const u64*)d_samples, (const u64*)d_hdr_all, world, c, st);
+  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny);
+  launch_shard_tiny_pack(c, (u64*)d_tiny, st);
+  cudaError_t e = launch_hash_count(x, n, flip, hash_mult, c, ctx->gkeys, ctx->gcnt, ctx->glist,
+                                    1, ctx->num_sms, st, 0, kGateMainDense, ctx->spill,
+                                    ctx->dense);
+  if (e == cudaSuccess)
+    e = launch_hash_count(x, n, flip, hash_mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
+                          ctx->num_sms, st, 1, kGateMainHash, ctx->spill, ctx->dense);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
+  launch_spill_fold(c, ctx->spill, ctx->gkeys, ctx->gcnt, ctx->glist, hash_mult, ctx->num_sms,
+                    st, kGateMain);
+  launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
+                 kGateMain);
+  launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs, n, st,
+                     kGateMainDense);
+  e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st,
+                              kGateMain);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+  launch_shard_pack_pairs(c, ctx->pk_b, ctx->pc_b, (u64*)d_send, cap, st);
+  ctx->launches += 11;
+  CKL();
+  return CAFS_OK;
+}
+
+int cafs_shard_finish_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed,
+                          const uint64_t* d_tiny_sum, const uint64_t* d_recv, int world,
+                          uint64_t cap, cafs_telemetry_t* tel, int* h_status, void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  if (!d_tiny_sum || !d_recv || !h_status || world < 1)
+    return fail(ctx, CAFS_EINVAL, "bad shard arguments");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(ensure_main(ctx));
+  DevCtl* c = ctx->d_ctl;
+  const u64 flip = is_signed ? kSign : 0;
+  launch_shard_tiny_finish(c, (const u64*)d_tiny_sum, ctx->pk_b, ctx->pc_b, ctx->poffs, st);
+  launch_shard_merge(c, (const u64*)d_recv, world, cap, ctx->gkeys, ctx->gcnt, ctx->glist,
+                     ctx->num_sms, st);
+  launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
+                 kGateMain);
+  cudaError_t e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, kExpectCtlN, ctx->pk_b,
+                                          ctx->pc_b, ctx->poffs, st, kGateMain);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+  launch_emit(ctx->pk_b, ctx->poffs, 0, c, d_x, 0, n, flip, ctx->num_sms, st, 0, 0, true);
+  ctx->launches += 6;
+  CKL();
+  TRY(sync_ctl(ctx, st));
+  const DevCtl& h = *ctx->h_ctl;
+  const int eff = h.eff_route;
+  int status = 1;  // 1: the caller runs the host-driven sharded path
+  if (eff == CAFS_ALREADY_SORTED) status = 0;
+  else if ((eff == CAFS_TINY_COUNT || eff == CAFS_MAIN) && h.pairs_ready && !h.overflow) status = 0;
+  if (eff == CAFS_MAIN && h.overflow) {  // a local overflow left this rank's table dirty
+    CK(cudaMemsetAsync(ctx->gkeys, 0xFF, kGlobalSlots * 8, st));
+    CK(cudaMemsetAsync(ctx->gcnt, 0, kGlobalSlots * 8, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  *h_status = status;
+  if (tel) {
+    memset(tel, 0, sizeof(*tel));
+    tel->n = h.n_global;
+    fill_decision(h, eff, eff != CAFS_ALREADY_SORTED && h.n_global >= CAFS_SMALL_N_CUTOFF,
+                  &tel->decision);
+    tel->counted_total = status == 0 && eff != CAFS_ALREADY_SORTED ? h.n_global : 0;
+    tel->pairs = h.npairs;
+    for (int i = 0; i < 3; ++i) tel->stage_ms[i] = -1.f;
+    for (int i = 0; i < 4; ++i) tel->kernel_ms[i] = -1.f;
+  }
+  return CAFS_OK;
+}
+
 int cafs_gen_mix(uint64_t* d_out, uint64_t count, uint64_t seed, uint64_t skip, void* stream) {
   if (count && !d_out) return CAFS_EINVAL;
   int dev = 0, sms = 148;

@@ -71,7 +71,18 @@ struct DevCtl {
   // --- fused (sync-free) pipeline ---
   int32_t eff_route;             // route with the monotone prefix applied (kNeedScan: unknown)
   int32_t tiny_failed;           // the tiny pass missed a value -> main route runs
+  // --- sharded (stream-ordered) pipeline: this rank's rows of the sorted column ---
+  u64 slice[2];                  // [begin, end) in global positions
+  u64 n_global;
+  u64 local_npairs;              // this shard's pairs (kept for the host-driven merge)
+  int32_t local_sorted;          // ... sorted in the B buffers (else unsorted in A)
+  int32_t local_overflow;        // ... lost to a global-table overflow
 };
+
+// Row-shard header (shard.cu), all-gathered across ranks: rows, local monotone
+// state (0 no, 1 yes, 2 prefix sorted -> see word 4), first and last key
+// (order-mapped), an inversion found by the full scan.
+constexpr int kShardHdrWords = 8;
 
 // eff_route value when the prefix is sorted but the array is longer than it
 constexpr int32_t kNeedScan = 5;

@@ -57,7 +57,7 @@ template <int KK>
 __global__ void __launch_bounds__(kEmitThreads)
     emit_kernel(const u64* __restrict__ keys, const u64* __restrict__ goffs, u64 npairs_arg,
                 const DevCtl* ctl, typename KeyT<KK>::T* __restrict__ out, u64 begin, u64 end,
-                u64 flip, u64 tpw, u64 idx_entries) {
+                u64 flip, u64 tpw, u64 idx_entries, int ctl_slice) {
   using K = typename KeyT<KK>::T;
   constexpr u64 VK = 32 / sizeof(K);             // keys per 32-byte vector
   constexpr u64 kTileKeys = kTileBytes / sizeof(K);
@@ -71,6 +71,10 @@ __global__ void __launch_bounds__(kEmitThreads)
   if (ctl) {
     if (!ctl->pairs_ready) return;
     npairs = ctl->npairs;
+    if (ctl_slice) {  // a sharded rank's rows, known on device only
+      begin = ctl->slice[0];
+      end = ctl->slice[1];
+    }
   }
   if (npairs == 0 || end <= begin) return;
   const u64* offs = goffs;
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(kEmitThreads)
 
 void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, void* out,
                  u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 /*npairs_bound*/,
-                 int kk) {
+                 int kk, bool ctl_slice) {
   const u64 L = end > begin ? end - begin : 0;
   const u64 tile_keys = kTileBytes / (kk ? 4 : 8);
   const u64 wtiles = (L + tile_keys - 1) / tile_keys;
@@ -200,15 +204,15 @@ void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl
   switch (kk) {
     case 1:
       emit_kernel<1><<<(unsigned)grid, kEmitThreads, sm, st>>>(
-          keys, offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx);
+          keys, offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
       break;
     case 2:
       emit_kernel<2><<<(unsigned)grid, kEmitThreads, sm, st>>>(
-          keys, offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx);
+          keys, offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
       break;
     default:
       emit_kernel<0><<<(unsigned)grid, kEmitThreads, sm, st>>>(
-          keys, offs, npairs, ctl, (u64*)out, begin, end, flip, (u64)tpw, (u64)idx);
+          keys, offs, npairs, ctl, (u64*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
   }
 }
 

@@ -66,7 +66,10 @@ constexpr int kFreqSlots = 2048;  // <= 50% load for 1024 samples (reference: 40
 template <int KK>
 __global__ void __launch_bounds__(1024, 1)
     estimate_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip, int check_prefix,
-                    DevCtl* ctl) {
+                    DevCtl* ctl, const u64* __restrict__ ghdr, int world) {
+  // ghdr != null: sharded mode -- x holds the 1024 all-reduced samples
+  // (order-mapped, flip 0) and the column's rows, monotone state and N come
+  // from the all-gathered shard headers (kShardHdrWords words per rank)
   using K = typename KeyT<KK>::T;
   __shared__ u64 fkeys[kFreqSlots];
   __shared__ u32 fcnt[kFreqSlots];
@@ -102,13 +105,18 @@ __global__ void __launch_bounds__(1024, 1)
   }
   if (tid < 16) ctl->tiny_counts[tid] = 0;
   if (tid < kListStripes) ctl->g_fill[tid] = 0;
+  u64 nn = n;  // rows of the column
+  if (ghdr) {
+    nn = 0;
+    for (int r = 0; r < world; ++r) nn += ghdr[r * kShardHdrWords];
+  }
   __syncthreads();
 
   // ---- K0 + K1 loads, all in flight together: the prefix pairs (16 coalesced
   // (x[i], x[i+1]) pairs per thread over the reference's first chunk) and this
   // thread's strided sample (cardinality.py:102-104) ----
-  const u64 m = n < (u64)kSampleTarget ? n : (u64)kSampleTarget;
-  u64 stride = n / kSampleTarget;
+  const u64 m = nn < (u64)kSampleTarget ? nn : (u64)kSampleTarget;
+  u64 stride = ghdr ? 1 : n / kSampleTarget;
   if (stride < 1) stride = 1;
   const bool valid = (u64)tid < m;
   const u64 v = valid ? key_map<KK>(x[(u64)tid * stride], flip) : 0;
@@ -187,17 +195,17 @@ __global__ void __launch_bounds__(1024, 1)
   const bool saturated = (u == kSampleTarget);
   double k_hat;
   if (saturated) {
-    k_hat = (double)n;
+    k_hat = (double)nn;
   } else {
     double q = __ddiv_rn((double)(f1 * f1), __dmul_rn(2.0, (double)(f2 + 1)));
     k_hat = __dadd_rn((double)u, q);
-    if (!(k_hat < (double)n)) k_hat = (double)n;  // min(k_hat, float(n))
+    if (!(k_hat < (double)nn)) k_hat = (double)nn;  // min(k_hat, float(n))
   }
   // ---- route (sorter.py:155-162), assuming not monotone ----
   int route;
-  if (n < CAFS_SMALL_N_CUTOFF) route = CAFS_FALLBACK_SMALL_N;
+  if (nn < CAFS_SMALL_N_CUTOFF) route = CAFS_FALLBACK_SMALL_N;
   else if (k_hat <= 8.0 && u <= 8) route = CAFS_TINY_COUNT;
-  else if (__dmul_rn(k_hat, 2.0) > (double)n) route = CAFS_FALLBACK_HIGH_ENTROPY;
+  else if (__dmul_rn(k_hat, 2.0) > (double)nn) route = CAFS_FALLBACK_HIGH_ENTROPY;
   else route = CAFS_MAIN;
 
   // ---- tiny route: perfect hash of the <= 8 keys into 16 slots ----
@@ -224,8 +232,23 @@ __global__ void __launch_bounds__(1024, 1)
   if (tid == 0) {
     ctl->prefix_sorted = !inv;
     ctl->route = route;
-    ctl->eff_route = (check_prefix && !inv) ? (n <= kMonoPrefix ? CAFS_ALREADY_SORTED : kNeedScan)
-                                            : route;
+    int eff = (check_prefix && !inv) ? (n <= kMonoPrefix ? CAFS_ALREADY_SORTED : kNeedScan)
+                                     : route;
+    if (ghdr) {  // globally sorted iff every shard is and the boundaries are ordered
+      bool mono = true, have = false;
+      u64 prev = 0;
+      for (int r = 0; r < world; ++r) {
+        const u64* h = ghdr + r * kShardHdrWords;
+        if (h[0] == 0) continue;
+        if (!(h[1] == 1 || (h[1] == 2 && h[4] == 0))) mono = false;
+        if (have && h[2] < prev) mono = false;
+        prev = h[3];
+        have = true;
+      }
+      eff = (nn <= 1 || mono) ? CAFS_ALREADY_SORTED : route;
+      ctl->n_global = nn;
+    }
+    ctl->eff_route = eff;
     ctl->u = u;
     ctl->f1 = f1;
     ctl->f2 = f2;
@@ -272,10 +295,20 @@ __global__ void monotone_scan_kernel(const typename KeyT<KK>::T* __restrict__ x,
 void launch_estimate(const void* x, u64 n, u64 flip, int check_prefix, DevCtl* ctl,
                      cudaStream_t st, int kk) {
   switch (kk) {
-    case 1: estimate_kernel<1><<<1, 1024, 0, st>>>((const u32*)x, n, flip, check_prefix, ctl); break;
-    case 2: estimate_kernel<2><<<1, 1024, 0, st>>>((const u32*)x, n, flip, check_prefix, ctl); break;
-    default: estimate_kernel<0><<<1, 1024, 0, st>>>((const u64*)x, n, flip, check_prefix, ctl);
+    case 1:
+      estimate_kernel<1><<<1, 1024, 0, st>>>((const u32*)x, n, flip, check_prefix, ctl, nullptr, 0);
+      break;
+    case 2:
+      estimate_kernel<2><<<1, 1024, 0, st>>>((const u32*)x, n, flip, check_prefix, ctl, nullptr, 0);
+      break;
+    default:
+      estimate_kernel<0><<<1, 1024, 0, st>>>((const u64*)x, n, flip, check_prefix, ctl, nullptr, 0);
   }
+}
+
+void launch_estimate_sharded(const u64* samples, const u64* ghdr, int world, DevCtl* ctl,
+                             cudaStream_t st) {
+  estimate_kernel<0><<<1, 1024, 0, st>>>(samples, kSampleTarget, 0, 0, ctl, ghdr, world);
 }
 
 void launch_monotone_scan(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,

@@ -7,6 +7,7 @@ namespace cafs {
 
 constexpr u32 kSmallSortMax = 8192;  // single-CTA sort capacity (keys or pairs)
 constexpr u32 kBitonicMax = 2048;    // below this a bitonic network replaces the radix passes
+constexpr u64 kExpectCtlN = ~0ull - 1;  // pair-sort `expect`: the sharded column's N (ctl)
 
 // estimate.cu
 // `kk`: key kind (common.cuh): 0 = 64-bit, 1 = int32, 2 = uint32
@@ -14,6 +15,19 @@ void launch_estimate(const void* x, u64 n, u64 flip, int check_prefix, DevCtl* c
                      cudaStream_t st, int kk = 0);
 void launch_monotone_scan(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
                           cudaStream_t st, int kk = 0);
+void launch_estimate_sharded(const u64* samples, const u64* ghdr, int world, DevCtl* ctl,
+                             cudaStream_t st);
+// shard.cu: the stream-ordered sharded pipeline's own kernels
+void launch_shard_header(const u64* x, u64 n, u64 flip, u64* hdr, int num_sms, cudaStream_t st);
+void launch_shard_samples(const u64* x, u64 n, u64 flip, const u64* ghdr, int world, int rank,
+                          u64* samples, DevCtl* ctl, cudaStream_t st);
+void launch_shard_tiny_pack(const DevCtl* ctl, u64* out, cudaStream_t st);
+void launch_shard_pack_pairs(DevCtl* ctl, const u64* keys, const u64* cnts, u64* send,
+                             u64 cap, cudaStream_t st);
+void launch_shard_tiny_finish(DevCtl* ctl, const u64* tiny_sum, u64* pkeys, u64* pcnt, u64* poffs,
+                              cudaStream_t st);
+void launch_shard_merge(DevCtl* ctl, const u64* recv, int world, u64 cap, u64* gkeys, u64* gcnt,
+                        u32* glist, int num_sms, cudaStream_t st);
 // tiny.cu
 void launch_tiny_count(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms, cudaStream_t st,
                        int gate, int kk = 0);
@@ -35,7 +49,7 @@ void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* p
 // emit.cu
 void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, void* out,
                  u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 npairs_bound,
-                 int kk = 0);
+                 int kk = 0, bool ctl_slice = false);
 // radix.cu
 size_t onesweep_smem(bool has_val);
 u64 onesweep_tiles(u64 n);

@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(1024, 1)
   __shared__ u64 wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   u64 n = n_arg;
+  if (ctl && expect_total == kExpectCtlN) expect_total = ctl->n_global;  // sharded merge
   if (PAIRS && ctl) {
     if (ctl->overflow || ctl->pairs_ready || !gate_open(ctl, gate)) return;  // ready: dense path
     n = ctl->npairs;

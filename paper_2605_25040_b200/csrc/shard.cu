@@ -1,0 +1,201 @@
+// shard.cu -- kernels of the stream-ordered sharded pipeline (abi.cu:
+// cafs_shard_*).  One process per GPU holds a row shard of the column; the
+// reference is single-process (the paper leaves a parallel CAFS as future
+// work).  Every decision the host would otherwise make between
+// collectives is taken on device from all-gathered data, so a rank enqueues
+//   header -> all-gather -> samples -> all-reduce -> estimate + local count ->
+//   all-reduce (tiny counts) + all-gather (pair tables) -> merge -> slice emit
+// and synchronises once.  The dispatch is the reference's (sorter.py:141-162)
+// evaluated on the GLOBAL column: N and the monotone test come from the shard
+// headers, the 1024 strided samples from the shards that hold their positions.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cafs {
+
+// Header of this shard (kShardHdrWords words): rows, monotone state of the
+// first kMonoPrefix rows (0 inversion, 1 sorted, 2 sorted prefix of a longer
+// shard -> word 4 holds the full scan's verdict), first and last key.
+__global__ void __launch_bounds__(1024) shard_header_kernel(const u64* __restrict__ x, u64 n,
+                                                            u64 flip, u64* hdr) {
+  __shared__ int inv;
+  if (threadIdx.x == 0) inv = 0;
+  __syncthreads();
+  const u64 P = n < kMonoPrefix ? n : kMonoPrefix;
+  int found = 0;
+  for (u64 i = threadIdx.x; i + 1 < P; i += blockDim.x) found |= (x[i + 1] ^ flip) < (x[i] ^ flip);
+  if (found) inv = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    hdr[0] = n;
+    hdr[1] = n <= 1 ? 1 : (inv ? 0 : (n <= kMonoPrefix ? 1 : 2));
+    hdr[2] = n ? x[0] ^ flip : 0;
+    hdr[3] = n ? x[n - 1] ^ flip : 0;
+    hdr[4] = 0;
+    hdr[5] = hdr[6] = hdr[7] = 0;
+  }
+}
+
+// The rest of a shard whose prefix is sorted (state 2): any inversion -> word 4.
+__global__ void shard_scan_kernel(const u64* __restrict__ x, u64 n, u64 flip, u64* hdr) {
+  if (hdr[1] != 2) return;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  int found = 0;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i + 1 < n; i += stride)
+    found |= (x[i + 1] ^ flip) < (x[i] ^ flip);
+  if (found) hdr[4] = 1;
+}
+
+// The global sample positions i * (N // 1024) (cardinality.py:102-104) that
+// fall in this shard; zeros elsewhere, so an all-reduce SUM assembles the
+// sample.  Also records this rank's slice of the sorted output.
+__global__ void __launch_bounds__(1024) shard_samples_kernel(const u64* __restrict__ x, u64 n,
+                                                             u64 flip, const u64* ghdr, int world,
+                                                             int rank, u64* samples,
+                                                             DevCtl* ctl) {
+  u64 N = 0, off = 0;
+  for (int r = 0; r < world; ++r) {
+    const u64 nr = ghdr[r * kShardHdrWords];
+    if (r < rank) off += nr;
+    N += nr;
+  }
+  const u64 i = threadIdx.x;
+  u64 stride = N / kSampleTarget;
+  if (stride < 1) stride = 1;
+  const u64 m = N < (u64)kSampleTarget ? N : (u64)kSampleTarget;
+  const u64 pos = i * stride;
+  u64 v = 0;
+  if (i < m && pos >= off && pos < off + n) v = x[pos - off] ^ flip;
+  samples[i] = v;
+  if (threadIdx.x == 0) {
+    ctl->slice[0] = off;
+    ctl->slice[1] = off + n;
+  }
+}
+
+// Local tiny counts (per perfect-hash slot) and misses, for the all-reduce.
+__global__ void shard_tiny_pack_kernel(const DevCtl* ctl, u64* out) {
+  const int t = threadIdx.x;
+  if (t < 16) out[t] = ctl->tiny_counts[t];
+  if (t == 16) out[16] = ctl->tiny_miss;
+}
+
+// This rank's sorted (key, count) table for the all-gather: [np, keys[cap],
+// counts[cap]]; np = ~0 when it cannot be exchanged this way (table
+// overflow, more than cap pairs, or pairs not sorted on device).
+__global__ void shard_pack_pairs_kernel(DevCtl* ctl, const u64* keys, const u64* cnts,
+                                        u64* send, u64 cap) {
+  const bool main = gate_open(ctl, kGateMain);
+  const bool ok = main && !ctl->overflow && ctl->pairs_ready && ctl->npairs <= cap;
+  const u64 np = main ? (ok ? ctl->npairs : ~0ull) : 0ull;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    send[0] = np;
+    ctl->local_npairs = main ? ctl->npairs : 0;
+    ctl->local_sorted = main && ctl->pairs_ready;
+    ctl->local_overflow = main && ctl->overflow;
+  }
+  if (!ok) return;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < np; j += stride) {
+    send[1 + j] = keys[j];
+    send[1 + cap + j] = cnts[j];
+  }
+}
+
+// Tiny route on the all-reduced counts: the keys' global counts must sum to N
+// and no rank may have seen another value (sorter.py:367-385); else the
+// caller re-runs the column on the host-driven path.
+__global__ void shard_tiny_finish_kernel(DevCtl* ctl, const u64* tiny_sum, u64* pkeys, u64* pcnt,
+                                         u64* poffs) {
+  if (threadIdx.x != 0 || !gate_open(ctl, kGateTiny)) return;
+  const u64 N = ctl->n_global;
+  const int nk = ctl->nkeys;
+  u64 off = 0;
+  for (int j = 0; j < nk; ++j) {
+    const u64 c = tiny_sum[ctl->tiny_slot[j]];
+    pkeys[j] = ctl->keys[j];
+    pcnt[j] = c;
+    poffs[j] = off;
+    off += c;
+  }
+  poffs[nk] = off;
+  const bool ok = tiny_sum[16] == 0 && off == N;
+  ctl->npairs = nk;
+  ctl->total = off;
+  ctl->pairs_ready = ok;
+  ctl->tiny_failed = !ok;
+}
+
+// Merge: the union of every rank's table (sorter.py:276-285) in the global
+// table -- reset its per-call counters first; a rank that could not exchange
+// its table (np = ~0) or a local overflow skips the merge on this rank (the
+// caller then takes the host-driven path on all ranks: every rank sees the same
+// gathered np values).
+__global__ void shard_merge_reset_kernel(DevCtl* ctl, const u64* recv, int world, u64 cap) {
+  if (!gate_open(ctl, kGateMain)) return;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = ctl->overflow;
+  __syncthreads();
+  for (int r = threadIdx.x; r < world; r += blockDim.x)
+    if (recv[(u64)r * (1 + 2 * cap)] == ~0ull) bad = 1;
+  for (u32 t = threadIdx.x; t < kListStripes; t += blockDim.x) ctl->g_fill[t] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->npairs = 0;
+    ctl->total = 0;
+    ctl->pairs_ready = 0;
+    ctl->sum_error = 0;
+    ctl->need_large = 0;
+    ctl->empty_key_count = 0;
+    ctl->overflow = bad;  // gates the merge kernels below off
+  }
+}
+
+__global__ void shard_merge_insert_kernel(DevCtl* ctl, const u64* recv, int world, u64 cap,
+                                          u64* gkeys, u64* gcnt, u32* glist) {
+  if (!gate_open(ctl, kGateMain) || ctl->overflow) return;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 row = 1 + 2 * cap;
+  for (int r = 0; r < world; ++r) {
+    const u64* t = recv + (u64)r * row;
+    const u64 np = t[0];
+    for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < np; j += stride) {
+      const u64 k = t[1 + j], c = t[1 + cap + j];
+      if (k == kEmpty) atomicAdd(&ctl->empty_key_count, c);
+      else global_insert(gkeys, gcnt, glist, ctl, k, c, 0);
+    }
+  }
+}
+
+void launch_shard_header(const u64* x, u64 n, u64 flip, u64* hdr, int num_sms, cudaStream_t st) {
+  shard_header_kernel<<<1, 1024, 0, st>>>(x, n, flip, hdr);
+  shard_scan_kernel<<<num_sms * 4, 512, 0, st>>>(x, n, flip, hdr);
+}
+
+void launch_shard_samples(const u64* x, u64 n, u64 flip, const u64* ghdr, int world, int rank,
+                          u64* samples, DevCtl* ctl, cudaStream_t st) {
+  shard_samples_kernel<<<1, kSampleTarget, 0, st>>>(x, n, flip, ghdr, world, rank, samples, ctl);
+}
+
+void launch_shard_tiny_pack(const DevCtl* ctl, u64* out, cudaStream_t st) {
+  shard_tiny_pack_kernel<<<1, 32, 0, st>>>(ctl, out);
+}
+
+void launch_shard_pack_pairs(DevCtl* ctl, const u64* keys, const u64* cnts, u64* send,
+                             u64 cap, cudaStream_t st) {
+  shard_pack_pairs_kernel<<<8, 1024, 0, st>>>(ctl, keys, cnts, send, cap);
+}
+
+void launch_shard_tiny_finish(DevCtl* ctl, const u64* tiny_sum, u64* pkeys, u64* pcnt, u64* poffs,
+                              cudaStream_t st) {
+  shard_tiny_finish_kernel<<<1, 32, 0, st>>>(ctl, tiny_sum, pkeys, pcnt, poffs);
+}
+
+void launch_shard_merge(DevCtl* ctl, const u64* recv, int world, u64 cap, u64* gkeys, u64* gcnt,
+                        u32* glist, int num_sms, cudaStream_t st) {
+  shard_merge_reset_kernel<<<1, 256, 0, st>>>(ctl, recv, world, cap);
+  shard_merge_insert_kernel<<<num_sms * 2, 256, 0, st>>>(ctl, recv, world, cap, gkeys, gcnt,
+                                                         glist);
+}
+
+}  // namespace cafs

@@ -177,6 +177,47 @@ class DeviceOps:
             self.ctx, "partition")
         return out, counts.astype(np.int64)
 
+    # ---- the stream-ordered pipeline (cafs_shard_*): no host sync until finish ----
+    def shard_begin(self, x, hdr) -> None:
+        _lib.check(self.lib.cafs_shard_begin_i64(self.ctx, x.data_ptr(), x.shape[0],
+                                                 int(self.signed), hdr.data_ptr(), self._stream()),
+                   self.ctx, "shard_begin")
+
+    def shard_sample(self, x, hdr_all, world: int, rank: int, samples) -> None:
+        _lib.check(self.lib.cafs_shard_sample_i64(self.ctx, x.data_ptr(), x.shape[0],
+                                                  int(self.signed), hdr_all.data_ptr(), world,
+                                                  rank, samples.data_ptr(), self._stream()),
+                   self.ctx, "shard_sample")
+
+    def shard_count(self, x, mult: int, hdr_all, world: int, samples, tiny, send, cap: int):
+        _lib.check(self.lib.cafs_shard_count_i64(self.ctx, x.data_ptr(), x.shape[0],
+                                                 int(self.signed), mult, hdr_all.data_ptr(), world,
+                                                 samples.data_ptr(), tiny.data_ptr(),
+                                                 send.data_ptr(), cap, self._stream()),
+                   self.ctx, "shard_count")
+
+    def shard_finish(self, x, tiny_sum, recv, world: int, cap: int):
+        """(status, telemetry): status 0 = sorted, 1 = needs the host-driven path."""
+        t = _lib.Telemetry()
+        status = ctypes.c_int()
+        _lib.check(self.lib.cafs_shard_finish_i64(self.ctx, x.data_ptr(), x.shape[0],
+                                                  int(self.signed), tiny_sum.data_ptr(),
+                                                  recv.data_ptr(), world, cap, ctypes.byref(t),
+                                                  ctypes.byref(status), self._stream()),
+                   self.ctx, "shard_finish")
+        return int(status.value), t
+
+    def shard_local_pairs(self):
+        """This shard's pairs from the streamed count phase; None on overflow."""
+        k, c = self._pairs_out(_PAIR_CAP)
+        npairs = ctypes.c_uint64()
+        _lib.check(self.lib.cafs_shard_local_pairs_i64(self.ctx, k.data_ptr(), c.data_ptr(),
+                                                       _PAIR_CAP, ctypes.byref(npairs),
+                                                       self._stream()), self.ctx, "shard_pairs")
+        if npairs.value == (1 << 64) - 1:
+            return None
+        return k[:npairs.value], c[:npairs.value]
+
     def keys_tensor(self, keys_u64: list[int], counts: np.ndarray):
         torch = _torch()
         dev = torch.device("cuda", self.device)
@@ -232,6 +273,26 @@ class Comm:
         out = torch.empty(int(sum(out_splits)), dtype=send.dtype, device=src.device)
         self.dist.all_to_all_single(out, src, out_splits, in_splits, group=self.group)
         return out.to(send.device) if stage else out
+
+    def all_gather_into(self, out, t) -> None:
+        """out[world * k] <- every rank's t[k] in rank order (stream-ordered on NCCL)."""
+        if self.device is not None:
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+            return
+        torch = _torch()
+        src = t.cpu()
+        parts = [torch.empty_like(src) for _ in range(self.world)]
+        self.dist.all_gather(parts, src, group=self.group)
+        out.copy_(torch.cat(parts).to(out.device))
+
+    def all_reduce_inplace(self, t) -> None:
+        """t <- SUM over ranks (stream-ordered on NCCL)."""
+        if self.device is not None:
+            self.dist.all_reduce(t, group=self.group)
+            return
+        w = t.cpu()
+        self.dist.all_reduce(w, group=self.group)
+        t.copy_(w.to(t.device))
 
     def all_reduce_tensor(self, t):
         """Element-wise SUM across ranks of a fixed-shape tensor (a new tensor)."""
@@ -355,10 +416,61 @@ def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTeleme
     tel = telemetry if telemetry is not None else SortTelemetry()
     k0 = ops.kernel_count() if hasattr(ops, "kernel_count") else 0
     try:
-        _sort_sharded(x_local, comm, ops, tel, mult, signed)
+        fast = (hasattr(ops, "shard_begin") and x_local.is_cuda and x_local.is_contiguous()
+                and x_local.dtype in (torch.int64, torch.uint64))
+        if fast and _sort_sharded_streamed(x_local, comm, ops, tel, mult):
+            tel.sharded_path = "streamed"
+        else:
+            tel.sharded_path = "host"
+            _sort_sharded(x_local, comm, ops, tel, mult, signed)
     finally:
         if hasattr(ops, "kernel_count"):
             tel.kernels_launched = ops.kernel_count() - k0
+
+
+SHARD_PAIR_CAP = 8192  # pairs per rank in the stream-ordered exchange (the pair sort's capacity)
+
+
+def _sort_sharded_streamed(x_local, comm, ops, tel, mult: int) -> bool:
+    """The stream-ordered path: four local phases (cafs_shard_*) around four
+    stream-ordered collectives, the decisions taken on device, one host sync.
+    False when the column needs the host-driven path (every rank agrees)."""
+    torch = _torch()
+    from .sorter import _decision_from_c
+    dev = x_local.device
+    world, rank = comm.world, comm.rank
+    cap = SHARD_PAIR_CAP
+    i64 = torch.int64
+    hdr = torch.empty(8, dtype=i64, device=dev)
+    hdr_all = torch.empty(world * 8, dtype=i64, device=dev)
+    samples = torch.empty(SAMPLE_TARGET, dtype=i64, device=dev)
+    tiny = torch.empty(32, dtype=i64, device=dev)
+    send = torch.empty(1 + 2 * cap, dtype=i64, device=dev)
+    recv = torch.empty(world * (1 + 2 * cap), dtype=i64, device=dev)
+    ops.shard_begin(x_local, hdr)
+    comm.all_gather_into(hdr_all, hdr)
+    ops.shard_sample(x_local, hdr_all, world, rank, samples)
+    comm.all_reduce_inplace(samples)
+    ops.shard_count(x_local, mult, hdr_all, world, samples, tiny, send, cap)
+    comm.all_reduce_inplace(tiny)
+    comm.all_gather_into(recv, send)
+    status, t = ops.shard_finish(x_local, tiny, recv, world, cap)
+    tel.n = int(t.n)
+    tel.decision = _decision_from_c(t.decision, tel.n, "int64" if ops.signed else "uint64")
+    if status != 0:
+        if tel.decision.route is not Route.MAIN:
+            return False  # fallback routes and tiny misses: the host-driven path
+        # too many pairs for the device merge: continue from this shard's
+        # pairs (the count is not repeated)
+        sizes = [int(v) for v in hdr_all.view(world, 8)[:, 0].cpu().tolist()]
+        tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, 4)
+        _main_exchange(x_local, comm, ops, tel, ops.shard_local_pairs(), sizes, tel.decision)
+        return True
+    tel.counted_total = int(t.counted_total)
+    tel.pairs = int(t.pairs)
+    if tel.decision.route is Route.MAIN:
+        tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, 4)
+    return True
 
 
 def _sort_sharded(x_local, comm, ops, tel, mult: int, signed: bool) -> None:
@@ -443,7 +555,15 @@ def _sort_sharded(x_local, comm, ops, tel, mult: int, signed: bool) -> None:
     # ---- MAIN: local count, all-gather of pair tables, merge, slice emit ----
     decision = DispatchDecision(Route.MAIN, k_hat=k_hat, estimate=est)
     tel.table_buckets = table_size_for(max(1.0, k_hat), N, 4)
-    pairs = ops.count_pairs(x_local, mult)
+    _main_exchange(x_local, comm, ops, tel, ops.count_pairs(x_local, mult), sizes, decision)
+
+
+def _main_exchange(x_local, comm, ops, tel, pairs, sizes: list[int], decision) -> None:
+    """MAIN after the local count: all-gather of the pair tables, merge, slice
+    emit; `pairs` None = this shard's table overflowed (the guard)."""
+    N = int(sum(sizes))
+    off = int(sum(sizes[:comm.rank]))
+    n_local = int(x_local.shape[0])
     meta = comm.all_gather_ints([int(pairs is None), 0 if pairs is None else int(pairs[0].shape[0])])
     merged = None
     if not any(m[0] for m in meta):
@@ -451,8 +571,10 @@ def _sort_sharded(x_local, comm, ops, tel, mult: int, signed: bool) -> None:
         keys_all, cnts_all = comm.all_gather_pairs(pairs[0], pairs[1], counts)
         # every rank merges the same tables: the overflow outcome is the same everywhere
         merged = ops.merge_pairs(keys_all, cnts_all)
-    if merged is None:
-        _fallback(decision, guard=True)
+    if merged is None:  # the guard: the distributed fallback (sorter.py:264-273)
+        tel.decision = decision
+        tel.guard_fired = True
+        _exchange_sort(x_local, sizes, comm, ops)
         return
     tel.decision = decision
     ops.emit_slice(merged[0], merged[1], x_local, off, off + n_local, N)

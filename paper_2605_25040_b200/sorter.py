@@ -112,6 +112,7 @@ class SortTelemetry:  # sorter.py:60-81
     kernel_ms: dict[str, float] = field(default_factory=dict)
     device_guard_fired: bool = False
     exact: bool = False
+    sharded_path: str = ""  # sharded sort: "streamed" (device decisions) or "host"
 
     @property
     def route(self) -> Route | None:

@@ -76,6 +76,9 @@ def _worker(rank, world, port, name, q):
         cafs_sort_sharded(local, telemetry=tel)
         torch.cuda.synchronize()
         assert tel.kernels_launched > 0  # the device kernels ran (C ABI accounting)
+        # columns the stream-ordered path can finish on device must not fall back
+        if name in ("main", "cfg4_slice", "tiny", "ramp", "empty_shard"):
+            assert tel.sharded_path == "streamed", (name, tel.sharded_path)
         e = tel.decision.estimate
         q.put((rank, local.cpu().numpy(), tel.route.value, tel.tiny_count_failed,
                None if e is None else (e.k_hat, e.u, e.f1, e.f2, e.saturated), tel.guard_fired))
