@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kBsThreads)
   const u32 base = ms->base[b];
   const u32 n = ms->base[b + 1] - base;
   if (n <= kWarpBucketMax) return;  // bucket_small_kernel's
-  u64 vor = 0, vand = ~0ull;
+  u64 vor = 0, vand = ~0ull, vmin = ~0ull, vmax = 0;
   {  // all loads in flight before any use (one DRAM round trip, not n/256)
     u64 lk[kBsRounds];
 #pragma unroll
@@ -362,6 +362,8 @@ __global__ void __launch_bounds__(kBsThreads)
         ib[0][i] = (unsigned short)i;
         vor |= lk[j];
         vand &= lk[j];
+        vmin = lk[j] < vmin ? lk[j] : vmin;
+        vmax = lk[j] > vmax ? lk[j] : vmax;
       }
     }
   }
@@ -369,19 +371,28 @@ __global__ void __launch_bounds__(kBsThreads)
   for (int o = 16; o > 0; o >>= 1) {
     vor |= __shfl_xor_sync(0xffffffffu, vor, o);
     vand &= __shfl_xor_sync(0xffffffffu, vand, o);
+    const u64 a = __shfl_xor_sync(0xffffffffu, vmin, o), b = __shfl_xor_sync(0xffffffffu, vmax, o);
+    vmin = a < vmin ? a : vmin;
+    vmax = b > vmax ? b : vmax;
   }
-  if (lane == 0) { red_or[wid] = vor; red_and[wid] = vand; }
+  __shared__ u64 red_min[kBsWarps], red_max[kBsWarps];
+  if (lane == 0) { red_or[wid] = vor; red_and[wid] = vand; red_min[wid] = vmin; red_max[wid] = vmax; }
   __syncthreads();
-  vor = 0; vand = ~0ull;
-  for (int w = 0; w < kBsWarps; ++w) { vor |= red_or[w]; vand &= red_and[w]; }
+  vor = 0; vand = ~0ull; vmin = ~0ull; vmax = 0;
+  for (int w = 0; w < kBsWarps; ++w) {
+    vor |= red_or[w];
+    vand &= red_and[w];
+    vmin = red_min[w] < vmin ? red_min[w] : vmin;
+    vmax = red_max[w] > vmax ? red_max[w] : vmax;
+  }
   const u64 vary = vor ^ vand;
-  // ---- two-level path: split the bucket on its kSubBits highest varying bits
-  // (shared-memory counting sort), then rank-sort each sub-bucket -- a few
-  // keys each when the keys are spread -- instead of up to 7 byte passes.
-  // Buckets with a sub-bucket over kSubMax keys (clustered or repeated keys)
-  // take the LSD passes below.
-  if (vary != 0) {
-    const int hb = 63 - __clzll(vary);
+  // ---- two-level path: split the bucket's numeric span [vmin, vmax] into
+  // 2^kSubBits sub-buckets (shared-memory counting sort), then rank-sort each
+  // sub-bucket -- a few keys each when the keys are spread -- instead of up to
+  // 7 byte passes.  Buckets with a sub-bucket over kSubMax keys (clustered or
+  // repeated keys) take the LSD passes below.
+  if (vmax > vmin) {
+    const int hb = 63 - __clzll(vmax - vmin);
     const int nbits = hb + 1 < kSubBits ? hb + 1 : kSubBits;
     const int sh = hb + 1 - nbits;
     const u32 dmask = (1u << nbits) - 1;
@@ -391,7 +402,8 @@ __global__ void __launch_bounds__(kBsThreads)
     for (u32 i = tid; i < kSubBins; i += kBsThreads) h2[i] = 0;
     if (tid == 0) maxsub = 0;
     __syncthreads();
-    for (u32 i = tid; i < n; i += kBsThreads) atomicAdd(&h2[(u32)(kb[0][i] >> sh) & dmask], 1u);
+    for (u32 i = tid; i < n; i += kBsThreads)
+      atomicAdd(&h2[(u32)((kb[0][i] - vmin) >> sh) & dmask], 1u);
     __syncthreads();
     {  // exclusive scan of the kSubBins counts (kSubBins / kBsThreads per thread)
       constexpr int PT = kSubBins / kBsThreads;
@@ -429,14 +441,14 @@ __global__ void __launch_bounds__(kBsThreads)
     if (maxsub <= kSubMax) {
       for (u32 i = tid; i < n; i += kBsThreads) {
         const u64 k = kb[0][i];
-        const u32 p = atomicAdd(&c2[(u32)(k >> sh) & dmask], 1u);
+        const u32 p = atomicAdd(&c2[(u32)((k - vmin) >> sh) & dmask], 1u);
         kb[1][p] = k;
         if (HAS_VAL) ib[1][p] = ib[0][i];
       }
       __syncthreads();
       for (u32 p = tid; p < n; p += kBsThreads) {
         const u64 k = kb[1][p];
-        const u32 d = (u32)(k >> sh) & dmask;
+        const u32 d = (u32)((k - vmin) >> sh) & dmask;
         const u32 s0 = h2[d], e0 = d < dmask ? h2[d + 1] : n;
         u32 r = 0;
         for (u32 j = s0; j < e0; ++j) {
