@@ -121,17 +121,17 @@ __global__ void __launch_bounds__(1024, 1)
   const bool valid = (u64)tid < m;
   const u64 v = valid ? key_map<KK>(x[(u64)tid * stride], flip) : 0;
   if (check_prefix) {
+    // thread t checks the 16 adjacent pairs of rows [16t, 16t + 16]: 17 keys,
+    // one contiguous run per thread (the warp reads one 4 KB stretch)
     const u64 P = n < kMonoPrefix ? n : kMonoPrefix;
-    K a[16], b[16];
+    const u64 i0 = (u64)tid * 16;
+    K a[17];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const u64 i = (u64)tid + 1024u * j;
-      a[j] = i + 1 < P ? x[i] : 0;
-      b[j] = i + 1 < P ? x[i + 1] : 0;
-    }
+    for (int j = 0; j < 17; ++j) a[j] = i0 + j < P ? x[i0 + j] : 0;
     int found = 0;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) found |= key_map<KK>(b[j], flip) < key_map<KK>(a[j], flip);
+    for (int j = 0; j < 16; ++j)
+      found |= (i0 + j + 1 < P) && key_map<KK>(a[j + 1], flip) < key_map<KK>(a[j], flip);
     if (found) inv = 1;  // benign race: any writer sets 1
   }
   // insert the sample into the FreqSet; equal samples of a warp are merged
@@ -172,8 +172,19 @@ __global__ void __launch_bounds__(1024, 1)
   }
   if (lane == 0) { red[0][wid] = cu; red[1][wid] = c1; red[2][wid] = c2; }
   __syncthreads();
-  long long u = 0, f1 = 0, f2 = 0;
-  for (int w = 0; w < 32; ++w) { u += red[0][w]; f1 += red[1][w]; f2 += red[2][w]; }
+  if (wid == 0) {  // totals by one warp, broadcast through shared memory
+    long long a0 = red[0][lane], a1 = red[1][lane], a2 = red[2][lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    __syncwarp();
+    if (lane == 0) { red[0][0] = a0; red[1][0] = a1; red[2][0] = a2; }
+  }
+  __syncthreads();
+  const long long u = red[0][0], f1 = red[1][0], f2 = red[2][0];
   // distinct keys (FreqSet.distinct_keys) when u <= 8: collect, then sort
   if (u <= CAFS_TINY_MAX_KEYS) {
     for (int i = tid; i < kFreqSlots; i += 1024)
