@@ -34,7 +34,6 @@ constexpr int kHcThreads = 1024;
 constexpr u32 kRange = 8192;              // dense window (u32 counters, 32 KB)
 constexpr int kSLog2 = 13;                // shared table: 8192 slots (64 KB keys + 32 KB counts)
 constexpr u32 kS = 1u << kSLog2;
-constexpr u32 kSClaimCap = kS / 2;        // claims stop at load 1/2 (short miss chains)
 constexpr int kSMaxProbe = 4;             // a longer chain spills: the table is only a cache
                                           // of partial counts, so a key found in two places
                                           // (or in a slot and the spill) still sums right
@@ -66,14 +65,17 @@ __device__ __forceinline__ void table_add(const HcArgs& a, u64 key, u64 inc) {
   else global_insert(a.gkeys, a.gcnt, a.glist, a.ctl, key, inc, a.mult);
 }
 
-// Shared-table miss: linear probing with capped claims.  True when resolved.
+// Shared-table miss: linear probing with claims capped at load 1/2.  True when
+// resolved.  SLOG2: the table's size.
+template <int SLOG2 = kSLog2>
 __device__ __noinline__ bool probe_smem(u64 v, u64* skeys, u32* scnt, u32* sclaims, u64 mult) {
-  u32 h = mhash(v, mult, 64 - kSLog2);
+  constexpr u32 S = 1u << SLOG2;
+  u32 h = mhash(v, mult, 64 - SLOG2);
   for (int p = 0; p < kSMaxProbe; ++p) {
     const u64 k = *((volatile u64*)&skeys[h]);
     if (k == v) { atomicAdd(&scnt[h], 1u); return true; }
     if (k == kEmpty) {
-      if (*((volatile u32*)sclaims) >= kSClaimCap) return false;
+      if (*((volatile u32*)sclaims) >= S / 2) return false;
       const u64 old = atomicCAS(&skeys[h], kEmpty, v);
       if (old == kEmpty) {
         atomicAdd(sclaims, 1u);
@@ -82,15 +84,16 @@ __device__ __noinline__ bool probe_smem(u64 v, u64* skeys, u32* scnt, u32* sclai
       }
       if (old == v) { atomicAdd(&scnt[h], 1u); return true; }
     }
-    h = (h + 1) & (kS - 1);
+    h = (h + 1) & (S - 1);
   }
   return false;
 }
 
 // Inline slow path (rare misses): shared probe, else the global table.
+template <int SLOG2 = kSLog2>
 __device__ __forceinline__ u32 count_slow(u64 v, u64* skeys, u32* scnt, u32* sclaims,
                                           const HcArgs& a) {
-  if (probe_smem(v, skeys, scnt, sclaims, a.mult)) return 0;
+  if (probe_smem<SLOG2>(v, skeys, scnt, sclaims, a.mult)) return 0;
   global_insert(a.gkeys, a.gcnt, a.glist, a.ctl, v, 1, a.mult);
   return 1;
 }
@@ -101,10 +104,11 @@ __device__ __forceinline__ u32 count_slow(u64 v, u64* skeys, u32* scnt, u32* scl
 // (buckets.py:273-282) -- and folded into the global table afterwards by
 // spill_fold_kernel with the whole GPU in parallel.  A full region falls back to
 // inline global inserts.
+template <int SLOG2 = kSLog2>
 __device__ __forceinline__ void resolve_or_spill(bool active, u64 v, u64* skeys, u32* scnt,
                                                  u32* sclaims, u32* sfill, u64* region,
                                                  u32 region_cap, const HcArgs& a) {
-  const bool miss = active && !probe_smem(v, skeys, scnt, sclaims, a.mult);
+  const bool miss = active && !probe_smem<SLOG2>(v, skeys, scnt, sclaims, a.mult);
   const u32 m = __ballot_sync(0xffffffffu, miss);
   if (m == 0) return;
   const int lane = threadIdx.x & 31;
@@ -344,6 +348,168 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   }
 }
 
+// The high-cardinality shape (no dense window): the whole shared memory holds
+// the table -- 16384 slots, twice the TMA shapes' -- and the column is read
+// with direct 16-byte streaming loads (this shape is bound by the table work,
+// ~1.5 TB/s, not by HBM, so the TMA ring buys nothing while taking 93 KB).
+// With twice the slots, a skewed column misses the CTA's table on ~13 % of its
+// keys instead of ~21 % (cfg3), and every miss costs a probe, a spill write
+// and a fold insert.
+constexpr int kBigSLog2 = 14;
+constexpr u32 kBigS = 1u << kBigSLog2;
+constexpr int kBigQcap = 64;
+constexpr size_t kBigSmem = (size_t)kBigS * 12 + (size_t)32 * kBigQcap * 8;
+constexpr int kBigUnroll = 4;  // 16-byte loads in flight per thread
+constexpr u64 kBigMinRows = 1ull << 22;  // below: the 8192-slot queued shape
+
+template <int KK>
+__global__ void __launch_bounds__(kHcThreads, 1) hash_count_big_kernel(HcArgs a) {
+  if (!gate_open(a.ctl, a.gate)) return;
+  using K = typename KeyT<KK>::T;
+  constexpr int KPV = 16 / sizeof(K);
+  extern __shared__ __align__(128) unsigned char smem[];
+  u64* skeys = (u64*)smem;                      // [kBigS]
+  u32* scnt = (u32*)(skeys + kBigS);            // [kBigS]
+  u64* queue = (u64*)(scnt + kBigS);            // [32][kBigQcap]
+  __shared__ u32 sclaims, sfill;
+  __shared__ u64 red_empty[32], red_glob[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u64 flip = a.flip, mult = a.mult;
+  const u32 region_cap = (u32)(kSpillCap / gridDim.x);
+  u64* region = a.spill + (u64)blockIdx.x * region_cap;
+  for (u32 i = tid; i < kBigS; i += kHcThreads) { skeys[i] = kEmpty; scnt[i] = 0; }
+  if (tid == 0) { sclaims = 0; sfill = 0; }
+  __syncthreads();
+
+  const u64 n = a.n;
+  const K* xk = (const K*)a.x;
+  const u64 mis = (((uintptr_t)a.x) & 15) / sizeof(K);
+  const u64 head0 = mis ? (u64)KPV - mis : 0;
+  const u64 head = head0 < n ? head0 : n;
+  const u64 nvec = (n - head) / KPV;
+  const ulonglong2* xv = (const ulonglong2*)(xk + head);
+  // this CTA's contiguous range of vectors
+  const u64 per = (nvec + gridDim.x - 1) / gridDim.x;
+  const u64 v0 = blockIdx.x * per;
+  const u64 v1 = v0 + per < nvec ? v0 + per : nvec;
+
+  u64 empty_cnt = 0;
+  u32 glob_cnt = 0;
+  u64* wq = queue + (size_t)wid * kBigQcap;
+  u32 qn = 0;  // warp-uniform
+  auto enqueue = [&](bool miss, u64 v) {
+    const u32 m = __ballot_sync(0xffffffffu, miss);
+    if (m == 0) return;
+    if (miss) wq[qn + __popc(m & lanemask_lt())] = v;
+    qn += __popc(m);
+    if (qn >= 32) {
+      __syncwarp();
+      const u64 u = wq[qn - 32 + lane];
+      __syncwarp();
+      qn -= 32;
+      resolve_or_spill<kBigSLog2>(true, u, skeys, scnt, &sclaims, &sfill, region, region_cap, a);
+    }
+  };
+  auto fast = [&](u64 v) -> bool {
+    if (v == kEmpty) { empty_cnt++; return true; }
+    const u32 h = mhash(v, mult, 64 - kBigSLog2);
+    if (skeys[h] == v) { atomicAdd(&scnt[h], 1u); return true; }
+    return false;
+  };
+  for (u64 r0 = v0; r0 < v1; r0 += (u64)kBigUnroll * kHcThreads) {  // CTA-uniform rounds
+    ulonglong2 w[kBigUnroll];
+    bool ok[kBigUnroll];
+#pragma unroll
+    for (int q = 0; q < kBigUnroll; ++q) {
+      const u64 i = r0 + (u64)q * kHcThreads + tid;
+      ok[q] = i < v1;
+      w[q] = ok[q] ? ld_stream_v2(xv + i) : make_ulonglong2(0, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < kBigUnroll; ++q) {
+      u64 v[KPV];
+      if constexpr (KPV == 2) {
+        v[0] = key_map<KK>((K)w[q].x, flip);
+        v[1] = key_map<KK>((K)w[q].y, flip);
+      } else {
+        v[0] = key_map<KK>((K)w[q].x, flip);
+        v[1] = key_map<KK>((K)(w[q].x >> 32), flip);
+        v[2] = key_map<KK>((K)w[q].y, flip);
+        v[3] = key_map<KK>((K)(w[q].y >> 32), flip);
+      }
+#pragma unroll
+      for (int k = 0; k < KPV; ++k) enqueue(ok[q] && !fast(v[k]), v[k]);
+    }
+  }
+  __syncwarp();
+  resolve_or_spill<kBigSLog2>((u32)lane < qn, (u32)lane < qn ? wq[lane] : 0ull, skeys, scnt,
+                              &sclaims, &sfill, region, region_cap, a);
+  if (blockIdx.x == 0 && tid < 32) {  // head and tail keys (< KPV each)
+    const u64 tail0 = head + nvec * KPV;
+    if ((u64)tid < head) {
+      const u64 v = key_map<KK>(xk[tid], flip);
+      if (!fast(v)) glob_cnt += count_slow<kBigSLog2>(v, skeys, scnt, &sclaims, a);
+    }
+    if ((u64)tid < n - tail0) {
+      const u64 v = key_map<KK>(xk[tail0 + tid], flip);
+      if (!fast(v)) glob_cnt += count_slow<kBigSLog2>(v, skeys, scnt, &sclaims, a);
+    }
+  }
+  __syncthreads();
+  // ---- flush the CTA's shared cells into the global table ----
+#pragma unroll 1
+  for (u32 h0 = tid; h0 < kBigS; h0 += 2 * kHcThreads) {
+    u64 key[2], inc[2];
+    bool okf[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const u32 h = h0 + r * kHcThreads;
+      inc[r] = scnt[h];
+      key[r] = skeys[h];
+      okf[r] = inc[r] != 0;
+    }
+    global_insert_batch<2>(a.gkeys, a.gcnt, a.glist, a.ctl, key, inc, okf);
+  }
+  u64 g = glob_cnt;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    empty_cnt += __shfl_xor_sync(0xffffffffu, empty_cnt, o);
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+  }
+  if (lane == 0) { red_empty[wid] = empty_cnt; red_glob[wid] = g; }
+  __syncthreads();
+  if (tid == 0) {
+    u64 e = 0, gg = 0;
+    for (int w2 = 0; w2 < kHcThreads / 32; ++w2) { e += red_empty[w2]; gg += red_glob[w2]; }
+    if (e) atomicAdd(&a.ctl->empty_key_count, e);
+    if (gg) atomicAdd(&a.ctl->g_updates, gg);
+    const u32 f = sfill < region_cap ? sfill : region_cap;
+    a.ctl->spill_fill[blockIdx.x] = f;
+    atomicAdd(&a.ctl->spill_len, (u64)f);
+    atomicMax(&a.ctl->spill_regions, gridDim.x);
+  }
+}
+
+template <int KK>
+static cudaError_t launch_hc_big(const HcArgs& a, u64 n, int num_sms, cudaStream_t st) {
+  static_assert(kBigSmem <= 232448 - 2048, "shared memory budget");
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(hash_count_big_kernel<KK>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kBigSmem);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  const u64 kpv = KK ? 4 : 2;
+  const u64 rounds = (n / kpv + (u64)kBigUnroll * kHcThreads - 1) / ((u64)kBigUnroll * kHcThreads);
+  const int grid = (int)(rounds < (u64)num_sms ? (rounds ? rounds : 1) : (u64)num_sms);
+  hash_count_big_kernel<KK><<<grid, kHcThreads, kBigSmem, st>>>(a);
+  return cudaGetLastError();
+}
+
 // Occupied global slots -> dense (key, count) pairs; re-zero the slots so the
 // table is clean for the next call.  Block s compacts claim-list stripe s to
 // the offset of the stripes before it.  The sentinel key's count becomes the
@@ -578,27 +744,31 @@ static cudaError_t launch_hc(const HcArgs& a, u64 n, int num_sms, cudaStream_t s
   return cudaGetLastError();
 }
 
-// shapes: 0 = dense window (deep TMA ring, inline slow path); 1 = queued (per-
-// warp miss queues and the spill), with the window when the caller may have it
-// open, without it (more shared memory for the ring) when the gate guarantees
-// it is closed (kGateMainHash / kGateHash) or use_range is 0
+// shapes: 0 = dense window (deep TMA ring, inline slow path, the window's
+// counters in shared memory); without the window (the gate guarantees it is
+// closed -- kGateMainHash / kGateHash -- or use_range is 0) the big-table
+// shape with per-warp miss queues and the spill (the TMA queued shape for
+// columns under kBigMinRows rows)
 cudaError_t launch_hash_count(const void* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms,
                               cudaStream_t st, int variant, int gate, u64* spill, u64* dense,
                               int kk) {
   HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate, spill, dense};
   const bool window = use_range && gate != kGateMainHash && gate != kGateHash;
-  const int v = variant == 0 && window ? 0 : (window ? 1 : 2);
-#define HC_SHAPES(K)                                                                   \
-  switch (v) {                                                                         \
-    case 0: return launch_hc<3, 3968, 0, true, K>(a, n, num_sms, st);                  \
-    case 1: return launch_hc<3, 1984, 64, true, K>(a, n, num_sms, st);                 \
-    default: return launch_hc<3, 3968, 64, false, K>(a, n, num_sms, st);               \
+  (void)variant;
+  if (window) {
+    if (kk == 1) return launch_hc<3, 3968, 0, true, 1>(a, n, num_sms, st);
+    if (kk == 2) return launch_hc<3, 3968, 0, true, 2>(a, n, num_sms, st);
+    return launch_hc<3, 3968, 0, true, 0>(a, n, num_sms, st);
   }
-  if (kk == 1) { HC_SHAPES(1) }
-  if (kk == 2) { HC_SHAPES(2) }
-  HC_SHAPES(0)
-#undef HC_SHAPES
+  if (n < kBigMinRows) {  // small columns: the table's init and flush would dominate
+    if (kk == 1) return launch_hc<3, 3968, 64, false, 1>(a, n, num_sms, st);
+    if (kk == 2) return launch_hc<3, 3968, 64, false, 2>(a, n, num_sms, st);
+    return launch_hc<3, 3968, 64, false, 0>(a, n, num_sms, st);
+  }
+  if (kk == 1) return launch_hc_big<1>(a, n, num_sms, st);
+  if (kk == 2) return launch_hc_big<2>(a, n, num_sms, st);
+  return launch_hc_big<0>(a, n, num_sms, st);
 }
 
 void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys, u64* pcnt,
