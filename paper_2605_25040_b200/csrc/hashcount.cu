@@ -230,6 +230,17 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
         resolve_or_spill(true, u, skeys, scnt, &sclaims, &sfill, region, region_cap, a);
       }
     };
+    // 32-bit keys: is the dense window inside the 32-bit domain?  Then a key
+    // is in it iff (u32)(x - base) < kRange (no wrap-around false positives)
+    bool w32 = false;
+    u32 base32 = 0;
+    if constexpr (KK != 0 && RANGE) {
+      const long long B = (long long)(base ^ kSign);  // the window's first key, as int64
+      const long long lo = KK == 1 ? -2147483648ll : 0ll;
+      const long long hi = (KK == 1 ? 2147483647ll : 4294967295ll) - (long long)kRange;
+      w32 = rlen == kRange && B >= lo && B <= hi;
+      base32 = (u32)B;
+    }
     u32 s = 0, ph = 0;
     u64 off = (u64)blockIdx.x * SK;
     const u64 off_step = (u64)gridDim.x * SK;
@@ -243,6 +254,21 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
         const bool valid = i < nv;
         ulonglong2 w = make_ulonglong2(0, 0);
         if (valid) w = sv[i];
+        if constexpr (KK != 0 && RANGE && QCAP == 0) {
+          // 32-bit keys inside a window that lies in the 32-bit domain: the
+          // window test in 32-bit arithmetic (exact there), no widening
+          if (w32) {
+            const u32 d0 = (u32)w.x - base32, d1 = (u32)(w.x >> 32) - base32;
+            const u32 d2 = (u32)w.y - base32, d3 = (u32)(w.y >> 32) - base32;
+            if (valid && max(max(d0, d1), max(d2, d3)) < kRange) {
+              atomicAdd(&dcnt[d0], 1u);
+              atomicAdd(&dcnt[d1], 1u);
+              atomicAdd(&dcnt[d2], 1u);
+              atomicAdd(&dcnt[d3], 1u);
+              continue;
+            }
+          }
+        }
         u64 v[KPV];
         if constexpr (KPV == 2) {
           v[0] = key_map<KK>((K)w.x, flip);

@@ -430,6 +430,12 @@ def test_dtype32_routes_at_scale(dtype):
         "hash": rng.integers(info.min, info.max, 200_000, dtype=dtype)[rng.integers(0, 200_000, 5_000_000)],
         "fallback": rng.integers(info.min, info.max, 3_000_001, dtype=dtype),
     }
+    z = np.minimum(rng.zipf(1.2, 3_000_000), 3000).astype(np.int64)
+    # dense windows at the edges of the 32-bit domain (the 32-bit window test
+    # applies only when the window lies inside it)
+    cases["dense_top"] = (int(info.max) - z).astype(dtype)
+    cases["dense_bottom"] = (int(info.min) + z).astype(dtype)
+    cases["dense_mid"] = (z + (1 << 20)).astype(dtype)
     g = ogen.mix_outputs(5, 5_000_000).astype(dtype)  # ~all distinct ...
     g[::5_000_000 // 1024][:1024] = (np.arange(1024) % 100).astype(dtype)  # ... low estimate
     cases["guard"] = g
