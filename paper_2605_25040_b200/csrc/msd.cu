@@ -328,16 +328,24 @@ __global__ void __launch_bounds__(256)
 // One CTA per bucket: load it into shared memory, LSD radix over the bytes that
 // vary inside the bucket (stable 8-ballot multisplit, warp-contiguous
 // segments), write it back sorted (un-flipping the keys; pairs carry their
-// value through a 16-bit index).
+// value through a 16-bit index).  `cap` (>= the largest bucket, a multiple of
+// kBsThreads) sizes the shared buffers, so small buckets leave room for more
+// CTAs per SM.
+__host__ __device__ constexpr size_t bs_smem_bytes(u32 cap, bool has_val) {
+  return (size_t)cap * 16 + (has_val ? (size_t)cap * 4 : 0) + (size_t)kBsWarps * 256 * 4;
+}
+
 template <bool HAS_VAL>
 __global__ void __launch_bounds__(kBsThreads)
     bucket_sort_kernel(const u64* __restrict__ tk, const u64* __restrict__ tv,
-                       const MsdState* ms, u64 flip, u64* __restrict__ dk, u64* __restrict__ dv) {
+                       const MsdState* ms, u64 flip, u64* __restrict__ dk, u64* __restrict__ dv,
+                       u32 cap) {
   extern __shared__ __align__(16) unsigned char bs_smem[];
-  u64 (*kb)[kBucketCap] = (u64 (*)[kBucketCap])bs_smem;                                // [2]
-  unsigned short (*ib)[kBucketCap] =
-      (unsigned short (*)[kBucketCap])(bs_smem + 2 * kBucketCap * 8);                 // [2]
-  u32 (*wcnt)[256] = (u32 (*)[256])(bs_smem + 2 * kBucketCap * 8 + 2 * kBucketCap * 2);  // [warps]
+  u64* kb[2] = {(u64*)bs_smem, (u64*)bs_smem + cap};
+  unsigned short* ib[2] = {(unsigned short*)((u64*)bs_smem + 2 * cap),
+                           (unsigned short*)((u64*)bs_smem + 2 * cap) + cap};
+  u32 (*wcnt)[256] =
+      (u32 (*)[256])(bs_smem + (size_t)cap * 16 + (HAS_VAL ? (size_t)cap * 4 : 0));  // [warps]
   __shared__ u32 dstart[256];
   __shared__ u32 wsum8[8];
   __shared__ u64 red_or[kBsWarps], red_and[kBsWarps];
@@ -359,7 +367,7 @@ __global__ void __launch_bounds__(kBsThreads)
       const u32 i = tid + j * kBsThreads;
       if (i < n) {
         kb[0][i] = lk[j];
-        ib[0][i] = (unsigned short)i;
+        if (HAS_VAL) ib[0][i] = (unsigned short)i;
         vor |= lk[j];
         vand &= lk[j];
         vmin = lk[j] < vmin ? lk[j] : vmin;
@@ -529,7 +537,7 @@ __global__ void __launch_bounds__(kBsThreads)
       if (idx < n) {
         const u32 pos = dstart[dig[r]] + wcnt[wid][dig[r]] + rank[r];
         dst[pos] = src[idx];
-        idst[pos] = isrc[idx];
+        if (HAS_VAL) idst[pos] = isrc[idx];
       }
     }
     __syncthreads();
@@ -614,7 +622,7 @@ void launch_msd_partition(const u64* keys, u64 n, u64 flip, void* state, u64 kmi
 size_t msd_maxb_offset() { return offsetof(MsdState, maxb); }
 
 // keys (and vals) -> tmp (bucketed) -> dk/dv sorted; dk may equal keys
-constexpr size_t kBsSmem = (size_t)kBucketCap * (16 + 4) + (size_t)kBsWarps * 256 * 4;
+constexpr size_t kBsSmem = bs_smem_bytes(kBucketCap, true);
 
 void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* state, u64* tk,
                      u64* tv, u64* dk, u64* dv, u32 maxb, int num_sms, cudaStream_t st) {
@@ -632,20 +640,22 @@ void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* st
     attr_dev = dev;
   }
   const bool large = maxb > kWarpBucketMax;
+  const u32 cap = (maxb + kBsThreads - 1) / kBsThreads * kBsThreads;  // <= kBucketCap
   if (vals) {
     msd_scatter_chunk_kernel<true><<<(unsigned)chunks, 1024, 0, st>>>(keys, vals, n, flip, ms,
                                                                       chunk, tk, tv);
     bucket_small_kernel<true><<<kMsdBuckets / 8, 256, 0, st>>>(tk, tv, ms, flip, dk, dv);
     if (large)
-      bucket_sort_kernel<true><<<kMsdBuckets, kBsThreads, kBsSmem, st>>>(tk, tv, ms, flip, dk, dv);
+      bucket_sort_kernel<true><<<kMsdBuckets, kBsThreads, bs_smem_bytes(cap, true), st>>>(
+          tk, tv, ms, flip, dk, dv, cap);
   } else {
     msd_scatter_chunk_kernel<false><<<(unsigned)chunks, 1024, 0, st>>>(keys, nullptr, n, flip,
                                                                        ms, chunk, tk, nullptr);
     bucket_small_kernel<false><<<kMsdBuckets / 8, 256, 0, st>>>(tk, nullptr, ms, flip, dk,
                                                                nullptr);
     if (large)
-      bucket_sort_kernel<false><<<kMsdBuckets, kBsThreads, kBsSmem, st>>>(tk, nullptr, ms, flip,
-                                                                           dk, nullptr);
+      bucket_sort_kernel<false><<<kMsdBuckets, kBsThreads, bs_smem_bytes(cap, false), st>>>(
+          tk, nullptr, ms, flip, dk, nullptr, cap);
   }
 }
 
