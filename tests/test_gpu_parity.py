@@ -479,3 +479,29 @@ def test_graph_replay_every_route(direct):
         cafs.cafs_sort(t, telemetry=tel, direct_range=direct)
         assert np.array_equal(t.cpu().numpy(), want), name
         assert tel.tiny_count_failed == (name == "tiny_miss")
+
+
+@pytest.mark.parametrize("dtype", [np.int64, np.int32])
+def test_no_writes_outside_the_column(dtype):
+    """Canary rows on both sides of a sorted slice stay untouched, on every
+    route and alignment (no memory checker on the pool: bounds by test)."""
+    rng = np.random.default_rng(2024)
+    info = np.iinfo(dtype)
+    cases = {
+        "tiny": np.array([info.min, 0, 9], dtype)[rng.integers(0, 3, 300_007)],
+        "dense": (np.minimum(rng.zipf(1.3, 300_011), 3000)).astype(dtype),
+        "hash": rng.integers(info.min, info.max, 30_000, dtype=dtype)[rng.integers(0, 30_000, 5_000_003)],
+        "fallback": rng.integers(info.min, info.max, 200_003, dtype=dtype),
+        "small": rng.integers(-50, 50, 1_999).astype(dtype),
+    }
+    canary = np.array(0x5A5A5A5A, dtype=dtype)
+    for name, x in cases.items():
+        for lead in (0, 1, 3):
+            buf = np.full(lead + x.shape[0] + 8, canary, dtype)
+            buf[lead:lead + x.shape[0]] = x
+            full = to_dev(buf)
+            t = full[lead:lead + x.shape[0]]
+            cafs.cafs_sort(t)
+            got = full.cpu().numpy()
+            assert np.array_equal(got[lead:lead + x.shape[0]], np.sort(x)), (name, lead)
+            assert np.all(got[:lead] == canary) and np.all(got[lead + x.shape[0]:] == canary), (name, lead)
