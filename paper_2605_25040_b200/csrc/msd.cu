@@ -25,10 +25,11 @@ constexpr int kBsWarps = kBsThreads / 32;
 constexpr u32 kBucketCap = 4096;                       // keys per bucket sorted in smem
 constexpr int kBsRounds = kBucketCap / kBsThreads;     // 16 rounds of 32 per warp
 constexpr u32 kWarpBucketMax = 128;                    // buckets sorted by one warp
-constexpr int kSubBits = 10;                           // second-level split inside a bucket
-constexpr u32 kSubBins = 1u << kSubBits;               // (fits the 8 x 256 warp counters)
+constexpr int kSubBits = 11;                           // second-level split inside a bucket
+constexpr u32 kSubBins = 1u << kSubBits;               // (overlays the warp counters)
 constexpr u32 kSubMax = 64;                            // largest sub-bucket rank-sorted
-static_assert(2 * kSubBins <= kBsWarps * 256, "sub-bucket counters live in the warp counters");
+constexpr size_t kBsCounterBytes = (size_t)kSubBins * 4 > (size_t)kBsWarps * 256 * 4
+                                       ? (size_t)kSubBins * 4 : (size_t)kBsWarps * 256 * 4;
 constexpr int kScThreads = 256;
 constexpr int kScItems = 16;                           // keys per thread in the scatter
 constexpr u64 kScChunk = (u64)kScThreads * kScItems;   // 4096
@@ -332,11 +333,11 @@ __global__ void __launch_bounds__(256)
 // kBsThreads) sizes the shared buffers, so small buckets leave room for more
 // CTAs per SM.
 __host__ __device__ constexpr size_t bs_smem_bytes(u32 cap, bool has_val) {
-  return (size_t)cap * 16 + (has_val ? (size_t)cap * 4 : 0) + (size_t)kBsWarps * 256 * 4;
+  return (size_t)cap * 16 + (has_val ? (size_t)cap * 4 : 0) + kBsCounterBytes;
 }
 
 template <bool HAS_VAL>
-__global__ void __launch_bounds__(kBsThreads)
+__global__ void __launch_bounds__(kBsThreads, 5)  // latency-bound phases: more CTAs per SM
     bucket_sort_kernel(const u64* __restrict__ tk, const u64* __restrict__ tv,
                        const MsdState* ms, u64 flip, u64* __restrict__ dk, u64* __restrict__ dv,
                        u32 cap) {
@@ -404,21 +405,22 @@ __global__ void __launch_bounds__(kBsThreads)
     const int nbits = hb + 1 < kSubBits ? hb + 1 : kSubBits;
     const int sh = hb + 1 - nbits;
     const u32 dmask = (1u << nbits) - 1;
-    u32* h2 = &wcnt[0][0];          // [kSubBins] counts, then sub-bucket starts
-    u32* c2 = h2 + kSubBins;        // [kSubBins] scatter cursors
+    // one array: counts -> starts (scan) -> ends (the scatter's cursors);
+    // afterwards sub-bucket d is [d ? c2[d-1] : 0, c2[d])
+    u32* c2 = &wcnt[0][0];          // [kSubBins] (overlays the warp counters)
     __shared__ u32 maxsub;
-    for (u32 i = tid; i < kSubBins; i += kBsThreads) h2[i] = 0;
+    for (u32 i = tid; i < kSubBins; i += kBsThreads) c2[i] = 0;
     if (tid == 0) maxsub = 0;
     __syncthreads();
     for (u32 i = tid; i < n; i += kBsThreads)
-      atomicAdd(&h2[(u32)((kb[0][i] - vmin) >> sh) & dmask], 1u);
+      atomicAdd(&c2[(u32)((kb[0][i] - vmin) >> sh) & dmask], 1u);
     __syncthreads();
     {  // exclusive scan of the kSubBins counts (kSubBins / kBsThreads per thread)
       constexpr int PT = kSubBins / kBsThreads;
       u32 c[PT], loc = 0, mx = 0;
 #pragma unroll
       for (int q = 0; q < PT; ++q) {
-        c[q] = h2[tid * PT + q];
+        c[q] = c2[tid * PT + q];
         loc += c[q];
         mx = c[q] > mx ? c[q] : mx;
       }
@@ -440,7 +442,6 @@ __global__ void __launch_bounds__(kBsThreads)
       for (int w = 0; w < wid; ++w) run += wsum8[w];
 #pragma unroll
       for (int q = 0; q < PT; ++q) {
-        h2[tid * PT + q] = run;
         c2[tid * PT + q] = run;
         run += c[q];
       }
@@ -457,7 +458,7 @@ __global__ void __launch_bounds__(kBsThreads)
       for (u32 p = tid; p < n; p += kBsThreads) {
         const u64 k = kb[1][p];
         const u32 d = (u32)((k - vmin) >> sh) & dmask;
-        const u32 s0 = h2[d], e0 = d < dmask ? h2[d + 1] : n;
+        const u32 s0 = d ? c2[d - 1] : 0u, e0 = c2[d];
         u32 r = 0;
         for (u32 j = s0; j < e0; ++j) {
           const u64 kj = kb[1][j];
