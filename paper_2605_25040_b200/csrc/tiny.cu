@@ -21,7 +21,7 @@ constexpr int kTinyThreads = 512;
 constexpr int kTinyWarps = kTinyThreads / 32;
 
 template <int KK>
-__global__ void __launch_bounds__(kTinyThreads)
+__global__ void __launch_bounds__(kTinyThreads, 4)  // 2048 threads per SM: more loads in flight
     tiny_count_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip, DevCtl* ctl,
                       int gate) {
   using K = typename KeyT<KK>::T;
