@@ -425,9 +425,9 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
   TRY(ensure_main(ctx));
   DevCtl* c = ctx->d_ctl;
   int ts = tm.begin(), tk = tm.begin();
-  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny, kk);
+  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny, kk, ctx->pk_b, ctx->pc_b,
+                    ctx->poffs);
   tm.end(tk, L_K_COUNT, C_TINY);
-  launch_tiny_finalize(c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st, kGateTiny);
   tm.end(ts, L_STAGE_COUNT, C_TINY);
   ts = tm.begin();
   tk = tm.begin();
@@ -466,7 +466,7 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
     tm.end(ts, L_STAGE_EMIT, C_EMIT);
     ctx->launches++;
   }
-  ctx->launches += direct ? 8 : 6;
+  ctx->launches += direct ? 7 : 5;
   CKL();
   return CAFS_OK;
 }

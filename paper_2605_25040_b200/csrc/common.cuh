@@ -71,6 +71,8 @@ struct DevCtl {
   // --- fused (sync-free) pipeline ---
   int32_t eff_route;             // route with the monotone prefix applied (kNeedScan: unknown)
   int32_t tiny_failed;           // the tiny pass missed a value -> main route runs
+  u32 tiny_done;                 // CTAs of the tiny count finished (last one finalizes)
+  u32 _pad2;
   // --- sharded (stream-ordered) pipeline: this rank's rows of the sorted column ---
   u64 slice[2];                  // [begin, end) in global positions
   u64 n_global;

@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(1024, 1)
     ctl->pairs_ready = 0;
     ctl->sum_error = 0;
     ctl->tiny_failed = 0;
+    ctl->tiny_done = 0;
   }
   if (tid < 16) ctl->tiny_counts[tid] = 0;
   if (tid < kListStripes) ctl->g_fill[tid] = 0;

@@ -29,10 +29,11 @@ void launch_shard_tiny_finish(DevCtl* ctl, const u64* tiny_sum, u64* pkeys, u64*
 void launch_shard_merge(DevCtl* ctl, const u64* recv, int world, u64 cap, u64* gkeys, u64* gcnt,
                         u32* glist, int num_sms, cudaStream_t st);
 // tiny.cu
+// with pkeys != null the count's last CTA also writes the tiny route's pairs
+// and offsets (or flags the miss): the finalize of sorter.py:367-385
 void launch_tiny_count(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms, cudaStream_t st,
-                       int gate, int kk = 0);
-void launch_tiny_finalize(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,
-                          cudaStream_t st, int gate);
+                       int gate, int kk = 0, u64* pkeys = nullptr, u64* pcnt = nullptr,
+                       u64* poffs = nullptr);
 // hashcount.cu
 cudaError_t launch_hash_count(const void* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms, cudaStream_t st,

@@ -20,10 +20,34 @@ namespace cafs {
 constexpr int kTinyThreads = 512;
 constexpr int kTinyWarps = kTinyThreads / 32;
 
+// Success check (sum == n <=> no miss) and the <= 8 sorted pairs + offsets;
+// run by one thread of the count's last CTA (the counters are read from L2).
+__device__ void tiny_finalize(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs) {
+  if (__ldcg(&ctl->tiny_miss) != 0) {
+    ctl->pairs_ready = 0;
+    ctl->tiny_failed = 1;
+    return;
+  }
+  const int nk = ctl->nkeys;
+  u64 off = 0;
+  for (int j = 0; j < nk; ++j) {
+    const u64 c = __ldcg(&ctl->tiny_counts[ctl->tiny_slot[j]]);
+    pkeys[j] = ctl->keys[j];
+    pcnt[j] = c;
+    poffs[j] = off;
+    off += c;
+  }
+  poffs[nk] = off;
+  ctl->npairs = nk;
+  ctl->total = off;
+  ctl->sum_error = (off != n);
+  ctl->pairs_ready = (off == n);
+}
+
 template <int KK>
 __global__ void __launch_bounds__(kTinyThreads, 4)  // 2048 threads per SM: more loads in flight
     tiny_count_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip, DevCtl* ctl,
-                      int gate) {
+                      int gate, u64* pkeys, u64* pcnt, u64* poffs) {
   using K = typename KeyT<KK>::T;
   constexpr int KPV = 16 / sizeof(K);  // keys per 16-byte vector
   if (!gate_open(ctl, gate)) return;
@@ -97,58 +121,41 @@ __global__ void __launch_bounds__(kTinyThreads, 4)  // 2048 threads per SM: more
     for (int w = 0; w < kTinyWarps; ++w) m += wmiss[w];
     if (m) atomicAdd(&ctl->tiny_miss, m);
   }
-}
-
-// Success check (sum == n <=> no miss) and the <= 8 sorted pairs + offsets.
-__global__ void tiny_finalize_kernel(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,
-                                     int gate) {
-  if (threadIdx.x != 0 || !gate_open(ctl, gate)) return;
-  if (ctl->tiny_miss != 0) {
-    ctl->pairs_ready = 0;
-    ctl->tiny_failed = 1;
-    return;
+  if (pkeys) {  // the last CTA to finish runs the finalize (no separate launch)
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(&ctl->tiny_done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && tid == 0) {
+      __threadfence();
+      tiny_finalize(ctl, n, pkeys, pcnt, poffs);
+      ctl->tiny_done = 0;
+    }
   }
-  const int nk = ctl->nkeys;
-  u64 off = 0;
-  for (int j = 0; j < nk; ++j) {
-    const u64 c = ctl->tiny_counts[ctl->tiny_slot[j]];
-    pkeys[j] = ctl->keys[j];
-    pcnt[j] = c;
-    poffs[j] = off;
-    off += c;
-  }
-  poffs[nk] = off;
-  ctl->npairs = nk;
-  ctl->total = off;
-  ctl->sum_error = (off != n);
-  ctl->pairs_ready = (off == n);
 }
 
 void launch_tiny_count(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
-                       cudaStream_t st, int gate, int kk) {
+                       cudaStream_t st, int gate, int kk, u64* pkeys, u64* pcnt, u64* poffs) {
   const u64 kpv = kk ? 4 : 2;
   u64 blocks = (n / kpv + kTinyThreads * 8 - 1) / (kTinyThreads * 8);
   u64 maxb = (u64)num_sms * 4;
   if (blocks > maxb) blocks = maxb;
   if (blocks < 1) blocks = 1;
+  const unsigned g = (unsigned)blocks;
   switch (kk) {
     case 1:
-      tiny_count_kernel<1><<<(unsigned)blocks, kTinyThreads, 0, st>>>((const u32*)x, n, flip, ctl,
-                                                                      gate);
+      tiny_count_kernel<1><<<g, kTinyThreads, 0, st>>>((const u32*)x, n, flip, ctl, gate, pkeys,
+                                                       pcnt, poffs);
       break;
     case 2:
-      tiny_count_kernel<2><<<(unsigned)blocks, kTinyThreads, 0, st>>>((const u32*)x, n, flip, ctl,
-                                                                      gate);
+      tiny_count_kernel<2><<<g, kTinyThreads, 0, st>>>((const u32*)x, n, flip, ctl, gate, pkeys,
+                                                       pcnt, poffs);
       break;
     default:
-      tiny_count_kernel<0><<<(unsigned)blocks, kTinyThreads, 0, st>>>((const u64*)x, n, flip, ctl,
-                                                                      gate);
+      tiny_count_kernel<0><<<g, kTinyThreads, 0, st>>>((const u64*)x, n, flip, ctl, gate, pkeys,
+                                                       pcnt, poffs);
   }
-}
-
-void launch_tiny_finalize(DevCtl* ctl, u64 n, u64* pkeys, u64* pcnt, u64* poffs,
-                          cudaStream_t st, int gate) {
-  tiny_finalize_kernel<<<1, 32, 0, st>>>(ctl, n, pkeys, pcnt, poffs, gate);
 }
 
 }  // namespace cafs
