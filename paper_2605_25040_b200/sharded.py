@@ -402,9 +402,23 @@ def _exchange_sort(x_local, sizes: list[int], comm, ops) -> None:
 
 def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTelemetry | None = None,
                       ops=None, signed: bool | None = None) -> None:
-    """Sort the row-sharded global column in place; see the module docstring."""
+    """Sort the row-sharded global column in place; see the module docstring.
+
+    int64 / uint64 shards run as they are; int32 / uint32 shards (and strided
+    views) are sorted through a contiguous int64 copy -- widening preserves the
+    order and every rank's decision (the keys' identities are unchanged)."""
     torch = _torch()
     mult = check_hash_mult(hash_mult)
+    if x_local.dim() != 1:
+        raise ValueError("cafs_sort_sharded expects a 1-D shard")
+    if x_local.dtype not in (torch.int64, torch.uint64) or not x_local.is_contiguous():
+        if x_local.dtype not in (torch.int64, torch.uint64, torch.int32, torch.uint32):
+            raise TypeError(f"unsupported dtype {x_local.dtype}")
+        wide = x_local.to(torch.int64) if x_local.dtype != torch.uint64 else x_local.contiguous()
+        cafs_sort_sharded(wide, group, hash_mult, telemetry, ops,
+                          signed if x_local.dtype == torch.uint64 else True)
+        x_local.copy_(wide.to(x_local.dtype) if wide.dtype != x_local.dtype else wide)
+        return
     if ops is None:
         if signed is None:
             signed = x_local.dtype == torch.int64

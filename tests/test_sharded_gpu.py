@@ -43,6 +43,8 @@ def _cases():
         "distinct_uneven": (ogen.distinct_values(300_000, 10).view(np.int64), [1_001]),
         "skew": (_skew(), [100_001]),
         "guard": (_guard_input(), [2_500_000]),
+        "int32": (np.minimum(np.random.default_rng(8).zipf(1.3, 700_000), 3000).astype(np.int32)
+                  - 1500, [250_000]),
     }
 
 
@@ -108,7 +110,7 @@ def test_sharded_two_ranks_device_kernels(name):
         assert p.exitcode == 0
     got = np.concatenate([r[1] for r in res])
     assert np.array_equal(got, np.sort(x))
-    otel = orc.cafs_sort(x.copy())
+    otel = orc.cafs_sort(x.astype(np.int64) if x.dtype == np.int32 else x.copy())
     for r in res:
         assert r[2] == otel.route and r[3] == otel.tiny_count_failed
         assert r[5] == (name == "guard")  # device guard: the distributed fallback ran
