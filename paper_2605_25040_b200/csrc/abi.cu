@@ -24,6 +24,8 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -77,6 +79,10 @@ struct cafs_ctx {
   uint64_t launches = 0;  // kernels this context has launched (monotone)
   u64* wide = nullptr;    // int64 copy of a 32-bit column (host-driven fallback routes)
   u64 wide_elems = 0;
+  // pageable host transfers: per worker thread a stream and two pinned buffers
+  cudaStream_t xfer_stream[16] = {};
+  cudaEvent_t xfer_event[16][2] = {};
+  unsigned char* xfer_buf = nullptr;  // pinned, kXferThreads x 2 x kXferChunk
   // CUDA Graphs of the fused pipeline (estimate + gated route kernels), keyed by
   // the call's arguments; captured on the second call with the same key
   cudaStream_t cap_stream = nullptr;
@@ -316,6 +322,120 @@ int fallback_any(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cudaStream_t st, int
   launch_narrow(ctx->wide, n, kk, x, ctx->num_sms, st);
   ctx->launches += 2;
   CKL();
+  return CAFS_OK;
+}
+
+// ---- host <-> device transfers for pageable (unregistered) host memory ----
+// The driver stages pageable copies through its own pinned buffers at ~7 GB/s
+// per direction on the test host; here kXferThreads host threads each copy a
+// contiguous share through two pinned buffers of their own (host memcpy into
+// one while the DMA of the other runs on the thread's stream): ~PCIe speed.
+constexpr int kXferThreads = 16;
+constexpr size_t kXferChunk = 8u << 20;  // bytes per pinned buffer
+
+bool host_is_pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+int ensure_xfer(cafs_ctx_t* ctx) {
+  if (ctx->xfer_buf) return CAFS_OK;
+  for (int t = 0; t < kXferThreads; ++t) {
+    CK(cudaStreamCreateWithFlags(&ctx->xfer_stream[t], cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b)
+      CK(cudaEventCreateWithFlags(&ctx->xfer_event[t][b], cudaEventDisableTiming));
+  }
+  CK(cudaMallocHost(&ctx->xfer_buf, (size_t)kXferThreads * 2 * kXferChunk));
+  return CAFS_OK;
+}
+
+// bytes from pageable host memory to the device (to_device) or back; returns
+// the first CUDA error of any worker (cudaSuccess otherwise)
+cudaError_t staged_copy(cafs_ctx_t* ctx, void* dev, void* host, size_t bytes, bool to_device) {
+  std::vector<std::thread> workers;
+  cudaError_t errs[kXferThreads] = {};
+  const size_t share = ((bytes + kXferThreads - 1) / kXferThreads + 15) & ~(size_t)15;
+  const int device = ctx->device;
+  for (int t = 0; t < kXferThreads; ++t) {
+    const size_t lo = (size_t)t * share;
+    if (lo >= bytes) break;
+    const size_t hi = lo + share < bytes ? lo + share : bytes;
+    workers.emplace_back([=, &errs]() {
+      cudaError_t e = cudaSetDevice(device);
+      cudaStream_t st = ctx->xfer_stream[t];
+      unsigned char* buf[2] = {ctx->xfer_buf + (size_t)t * 2 * kXferChunk,
+                               ctx->xfer_buf + ((size_t)t * 2 + 1) * kXferChunk};
+      unsigned char* hp = (unsigned char*)host;
+      unsigned char* dp = (unsigned char*)dev;
+      if (to_device) {
+        int k = 0;
+        for (size_t off = lo; off < hi && e == cudaSuccess; off += kXferChunk, k ^= 1) {
+          const size_t len = hi - off < kXferChunk ? hi - off : kXferChunk;
+          if (off >= lo + 2 * kXferChunk) e = cudaEventSynchronize(ctx->xfer_event[t][k]);
+          if (e != cudaSuccess) break;
+          memcpy(buf[k], hp + off, len);
+          e = cudaMemcpyAsync(dp + off, buf[k], len, cudaMemcpyHostToDevice, st);
+          if (e == cudaSuccess) e = cudaEventRecord(ctx->xfer_event[t][k], st);
+        }
+      } else {  // device -> pinned (async, one chunk ahead) -> pageable
+        size_t off = lo;
+        int k = 0;
+        if (off < hi) {
+          const size_t len = hi - off < kXferChunk ? hi - off : kXferChunk;
+          e = cudaMemcpyAsync(buf[0], dp + off, len, cudaMemcpyDeviceToHost, st);
+          if (e == cudaSuccess) e = cudaEventRecord(ctx->xfer_event[t][0], st);
+        }
+        for (; off < hi && e == cudaSuccess; off += kXferChunk, k ^= 1) {
+          const size_t len = hi - off < kXferChunk ? hi - off : kXferChunk;
+          const size_t nxt = off + kXferChunk;
+          if (nxt < hi) {
+            const size_t l2 = hi - nxt < kXferChunk ? hi - nxt : kXferChunk;
+            e = cudaMemcpyAsync(buf[k ^ 1], dp + nxt, l2, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaEventRecord(ctx->xfer_event[t][k ^ 1], st);
+            if (e != cudaSuccess) break;
+          }
+          e = cudaEventSynchronize(ctx->xfer_event[t][k]);
+          if (e == cudaSuccess) memcpy(hp + off, buf[k], len);
+        }
+      }
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      errs[t] = e;
+    });
+  }
+  for (auto& w : workers) w.join();
+  for (int t = 0; t < kXferThreads; ++t)
+    if (errs[t] != cudaSuccess) return errs[t];
+  return cudaSuccess;
+}
+
+// host buffer -> device (the caller's stream waits for it) and back
+int host_to_device(cafs_ctx_t* ctx, void* dev, const void* host, size_t bytes, cudaStream_t st) {
+  if (!bytes) return CAFS_OK;
+  if (bytes >= 4 * kXferChunk && host_is_pageable(host)) {
+    TRY(ensure_xfer(ctx));
+    CK(cudaStreamSynchronize(st));  // the device buffer is free
+    cudaError_t e = staged_copy(ctx, dev, (void*)host, bytes, true);
+    if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "staged host-to-device copy", e);
+    return CAFS_OK;
+  }
+  CK(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, st));
+  return CAFS_OK;
+}
+
+int device_to_host(cafs_ctx_t* ctx, void* host, const void* dev, size_t bytes, cudaStream_t st) {
+  if (!bytes) return CAFS_OK;
+  if (bytes >= 4 * kXferChunk && host_is_pageable(host)) {
+    TRY(ensure_xfer(ctx));
+    CK(cudaStreamSynchronize(st));  // the sort has finished
+    cudaError_t e = staged_copy(ctx, (void*)dev, host, bytes, false);
+    if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "staged device-to-host copy", e);
+    return CAFS_OK;
+  }
+  CK(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st));
   return CAFS_OK;
 }
 
@@ -743,6 +863,12 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
   for (auto& g : ctx->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  for (int t = 0; t < kXferThreads; ++t) {
+    if (ctx->xfer_stream[t]) cudaStreamDestroy(ctx->xfer_stream[t]);
+    for (int b = 0; b < 2; ++b)
+      if (ctx->xfer_event[t][b]) cudaEventDestroy(ctx->xfer_event[t][b]);
+  }
+  if (ctx->xfer_buf) cudaFreeHost(ctx->xfer_buf);
   delete ctx;
 }
 
@@ -888,9 +1014,9 @@ int cafs_sort_i32_host(cafs_ctx_t* ctx, const int32_t* h_in, int32_t* h_out, uin
     CK(cudaMalloc(&ctx->stage, (n ? n : 1) * 8));
     ctx->stage_elems = n;
   }
-  if (n) CK(cudaMemcpyAsync(ctx->stage, h_in, n * 4, cudaMemcpyHostToDevice, st));
+  TRY(host_to_device(ctx, ctx->stage, h_in, n * 4, st));
   TRY(cafs_sort_i32(ctx, (int32_t*)ctx->stage, n, is_signed, hash_mult, flags, tel, stream));
-  if (n) CK(cudaMemcpyAsync(h_out, ctx->stage, n * 4, cudaMemcpyDeviceToHost, st));
+  TRY(device_to_host(ctx, h_out, ctx->stage, n * 4, st));
   CK(cudaStreamSynchronize(st));
   return CAFS_OK;
 }
@@ -910,9 +1036,9 @@ int cafs_sort_i64_host(cafs_ctx_t* ctx, const int64_t* h_in, int64_t* h_out, uin
     CK(cudaMalloc(&ctx->stage, (n ? n : 1) * 8));
     ctx->stage_elems = n;
   }
-  if (n) CK(cudaMemcpyAsync(ctx->stage, h_in, n * 8, cudaMemcpyHostToDevice, st));
+  TRY(host_to_device(ctx, ctx->stage, h_in, n * 8, st));
   TRY(cafs_sort_i64(ctx, (int64_t*)ctx->stage, n, is_signed, hash_mult, flags, tel, stream));
-  if (n) CK(cudaMemcpyAsync(h_out, ctx->stage, n * 8, cudaMemcpyDeviceToHost, st));
+  TRY(device_to_host(ctx, h_out, ctx->stage, n * 8, st));
   CK(cudaStreamSynchronize(st));
   return CAFS_OK;
 }

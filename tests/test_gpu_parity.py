@@ -505,3 +505,15 @@ def test_no_writes_outside_the_column(dtype):
             got = full.cpu().numpy()
             assert np.array_equal(got[lead:lead + x.shape[0]], np.sort(x)), (name, lead)
             assert np.all(got[:lead] == canary) and np.all(got[lead + x.shape[0]:] == canary), (name, lead)
+
+
+def test_large_pageable_numpy_staged_transfers():
+    """Pageable numpy arrays above the staging threshold go through the
+    multi-threaded pinned staging in both directions (int64 and int32)."""
+    rng = np.random.default_rng(77)
+    for x in (rng.integers(-3000, 3000, 40_000_003).astype(np.int64),
+              rng.integers(-2**31, 2**31 - 1, 30_000_001, dtype=np.int32),
+              ogen.mix_outputs(9, 12_000_000).view(np.int64).copy()):
+        want = np.sort(x)
+        cafs.cafs_sort(x)
+        assert np.array_equal(x, want)
