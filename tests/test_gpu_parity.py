@@ -517,3 +517,57 @@ def test_large_pageable_numpy_staged_transfers():
         want = np.sort(x)
         cafs.cafs_sort(x)
         assert np.array_equal(x, want)
+
+
+def _fuzz_input(rng):
+    kind = rng.integers(0, 6)
+    n = int(rng.choice([0, 1, 2, 3, 100, 2047, 2048, 2049, 5000, 16385, 16386, 70_000, 300_000]))
+    if kind == 0:    # tiny alphabet
+        pal = rng.integers(-2**63, 2**63 - 1, int(rng.integers(1, 9)), dtype=np.int64)
+    elif kind == 1:  # dictionary codes around a random base
+        base = int(rng.integers(-2**62, 2**62))
+        pal = base + np.arange(int(rng.integers(2, 6000)), dtype=np.int64)
+    elif kind == 2:  # random palette
+        pal = rng.integers(-2**63, 2**63 - 1, int(rng.integers(9, 50_000)), dtype=np.int64)
+    elif kind == 3:  # all distinct
+        return rng.permutation(rng.integers(-2**63, 2**63 - 1, n, dtype=np.int64))
+    elif kind == 4:  # sorted, with maybe one inversion
+        x = np.sort(rng.integers(-1000, 1000, n).astype(np.int64))
+        if n > 2 and rng.integers(0, 2):
+            i = int(rng.integers(0, n - 1))
+            x[i], x[i + 1] = x[i + 1] + 1, x[i]
+        return x
+    else:            # extremes
+        info = np.iinfo(np.int64)
+        pal = np.array([info.min, info.min + 1, -1, 0, 1, info.max - 1, info.max], np.int64)
+    if n == 0:
+        return np.empty(0, np.int64)
+    w = rng.zipf(1.2, pal.shape[0]).astype(np.float64) if rng.integers(0, 2) else None
+    p = None if w is None else w / w.sum()
+    return pal[rng.choice(pal.shape[0], n, p=p)]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fuzz_against_oracle(seed):
+    """Seeded random columns over every route, size edge and dtype: sorted
+    bytes equal np.sort and the decision equals the C oracle's."""
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(40):
+        x = _fuzz_input(rng)
+        dt = [np.int64, np.uint64, np.int32, np.uint32][int(rng.integers(0, 4))]
+        if dt == np.uint64:
+            x = x.view(np.uint64)
+        elif dt in (np.int32, np.uint32):
+            x = x.astype(dt)  # wraps: a different but valid column
+        want = np.sort(x)
+        t = to_dev(x)
+        tel = SortTelemetry()
+        cafs.cafs_sort(t, telemetry=tel)
+        assert np.array_equal(t.cpu().numpy(), want), (x.dtype, x.shape)
+        if x.shape[0] > 1:
+            xo = x.astype(np.int64) if x.dtype in (np.int32, np.uint32) else x.copy()
+            ot = orc.cafs_sort(xo)
+            assert tel.route.value == ot.route, (x.dtype, x.shape, tel.route, ot.route)
+            if ot.decision.estimate is not None and tel.decision.estimate is not None:
+                e, oe = tel.decision.estimate, ot.decision.estimate
+                assert (e.k_hat, e.u, e.f1, e.f2) == (oe.k_hat, oe.u, oe.f1, oe.f2)
