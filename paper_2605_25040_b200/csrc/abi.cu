@@ -162,7 +162,7 @@ int ensure_main(cafs_ctx_t* ctx) {
   if (ctx->gkeys) return CAFS_OK;
   CK(cudaMalloc(&ctx->gkeys, kGlobalSlots * 8));
   CK(cudaMalloc(&ctx->gcnt, kGlobalSlots * 8));
-  CK(cudaMalloc(&ctx->glist, kGlobalCap * 4));
+  CK(cudaMalloc(&ctx->glist, (size_t)kListStripes * kStripeCap * 4));
   CK(cudaMemset(ctx->gkeys, 0xFF, kGlobalSlots * 8));
   CK(cudaMemset(ctx->gcnt, 0, kGlobalSlots * 8));
   CK(cudaMalloc(&ctx->pk_a, kPairCap * 8));
@@ -597,9 +597,12 @@ int exact_telemetry(cafs_ctx_t* ctx, const void* x, u64 n, u64 flip, u64 mult, d
                     uint32_t flags, cafs_telemetry_t* tel, cudaStream_t st, int kk = 0) {
   const DevCtl c = *ctx->h_ctl;
   const u64 np = c.npairs;
+  // the key -> pair lookup table: a power of two >= 2 x pairs (load <= 1/2)
+  u64 tl_slots = 1024;
+  while (tl_slots < 2 * kPairCap) tl_slots <<= 1;
   if (!ctx->tl_keys) {
-    CK(cudaMalloc(&ctx->tl_keys, (kPairCap * 2) * 8));
-    CK(cudaMalloc(&ctx->tl_idx, (kPairCap * 2) * 4));
+    CK(cudaMalloc(&ctx->tl_keys, tl_slots * 8));
+    CK(cudaMalloc(&ctx->tl_idx, tl_slots * 4));
     CK(cudaMalloc(&ctx->tl_first, kPairCap * 4));
     CK(cudaMalloc(&ctx->tl_runs, kPairCap * 4));
     CK(cudaMalloc(&ctx->tl_comp, 4 * kPairCap * 8));

@@ -22,7 +22,11 @@ constexpr int kSampleTarget = 1024;      // cardinality.py:26
 constexpr u64 kMonoPrefix = (1u << 14) + 1;  // rows the dispatch kernel checks (sorter.py:32)
 
 // Global (L2-resident) (key, count) table of the main route.
-constexpr int kGlobalLog2 = 22;                       // 4 Mi slots: 32 MB keys + 32 MB counts
+// The global table is sized for the B200's memory, not for L2: 32 Mi slots
+// (256 MB keys + 256 MB counts) hold up to 16 Mi distinct keys before the guard
+// fires; only the slots a call claims are touched (claim list), so a small key
+// set still lives in L2.
+constexpr int kGlobalLog2 = 25;
 constexpr u64 kGlobalSlots = 1ull << kGlobalLog2;
 constexpr u64 kGlobalCap = kGlobalSlots / 2;          // max distinct keys before the guard fires
 constexpr int kGlobalMaxProbe = 128;
@@ -33,7 +37,7 @@ constexpr u32 kMaxSpillRegions = 256;                 // >= count-kernel grid (o
 // serialise on one counter and the stripes fill evenly.  A full stripe is a
 // table overflow (the guard).
 constexpr u32 kListStripes = 128;
-constexpr u64 kStripeCap = kGlobalCap / kListStripes;
+constexpr u64 kStripeCap = kGlobalCap / kListStripes * 5 / 4;  // headroom: stripes fill unevenly
 
 // Device control block: dispatch result + per-call flags/counters.
 struct DevCtl {

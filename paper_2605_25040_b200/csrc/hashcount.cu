@@ -561,6 +561,10 @@ __global__ void __launch_bounds__(256) compact_kernel(DevCtl* ctl, u64* gkeys, u
     if (threadIdx.x == 0) { pre_sh = pre; tot_sh = tot; }
   }
   __syncthreads();
+  if (tot_sh > kGlobalCap) {  // stripes have headroom; the table's capacity is the guard
+    if (s == 0 && threadIdx.x == 0) ctl->overflow = 1;
+    return;
+  }
   const u64 pre = pre_sh;
   const u32 m = ctl->g_fill[s] < kStripeCap ? ctl->g_fill[s] : (u32)kStripeCap;
   const u32* lst = glist + (u64)s * kStripeCap;

@@ -63,7 +63,7 @@ def _torch():
 
 
 # the device's pair capacity: global table + the ~0 sentinel + the dense window
-_PAIR_CAP = (1 << 21) + 1 + 8192
+_PAIR_CAP = (1 << 24) + 1 + 8192
 
 
 class DeviceOps:

@@ -297,8 +297,8 @@ def test_fallback_sort_clustered_and_repeated():
 
 
 def test_guard_reroutes_to_fallback():
-    """More distinct keys than the global table holds, under a low estimate."""
-    n = 5_000_000
+    """More distinct keys than the global table holds (16 Mi), under a low estimate."""
+    n = 20_000_000
     x = ogen.mix_outputs(77, n).view(np.int64).copy()
     stride = n // 1024
     x[::stride][:1024] = np.arange(1024, dtype=np.int64) % 100  # sample sees 100 keys
@@ -378,11 +378,11 @@ def test_dense_window_paths(kind, exact):
 
 def test_guard_then_dense_window():
     """A guard that fires mid-count must not leave dense-window counts behind."""
-    n = 6_000_000
+    n = 24_000_000
     x = ogen.mix_outputs(78, n).view(np.int64).copy()
     stride = n // 1024
     x[::stride][:1024] = np.arange(1024, dtype=np.int64) % 100  # low estimate + a window
-    x[:n // 3] = np.arange(n // 3) % 100  # many rows land in the window
+    x[:n // 4] = np.arange(n // 4) % 100  # many rows land in the window
     tel = SortTelemetry()
     t = to_dev(x)
     cafs.cafs_sort(t, telemetry=tel)
@@ -436,8 +436,8 @@ def test_dtype32_routes_at_scale(dtype):
     cases["dense_top"] = (int(info.max) - z).astype(dtype)
     cases["dense_bottom"] = (int(info.min) + z).astype(dtype)
     cases["dense_mid"] = (z + (1 << 20)).astype(dtype)
-    g = ogen.mix_outputs(5, 5_000_000).astype(dtype)  # ~all distinct ...
-    g[::5_000_000 // 1024][:1024] = (np.arange(1024) % 100).astype(dtype)  # ... low estimate
+    g = ogen.mix_outputs(5, 20_000_000).astype(dtype)  # ~all distinct (> 16 Mi) ...
+    g[::20_000_000 // 1024][:1024] = (np.arange(1024) % 100).astype(dtype)  # ... low estimate
     cases["guard"] = g
     for name, x in cases.items():
         t = to_dev(x)
@@ -571,3 +571,23 @@ def test_fuzz_against_oracle(seed):
             if ot.decision.estimate is not None and tel.decision.estimate is not None:
                 e, oe = tel.decision.estimate, ot.decision.estimate
                 assert (e.k_hat, e.u, e.f1, e.f2) == (oe.k_hat, oe.u, oe.f1, oe.f2)
+
+
+def test_main_route_beyond_two_million_keys():
+    """2.3 M distinct keys on the main route (a skewed column the dispatcher
+    sends to MAIN): the 16 Mi-key device table counts them without the guard,
+    and the exact telemetry still matches the oracle's bucket table."""
+    rng = np.random.default_rng(5)
+    K = 6_000_000
+    pal = ogen.mix_outputs(11, K).view(np.int64)
+    x = pal[np.minimum(rng.zipf(1.05, 40_000_000), K) - 1]
+    ot = orc.cafs_sort(x.copy())
+    t = to_dev(x)
+    tel = SortTelemetry()
+    cafs.cafs_sort(t, telemetry=tel, exact_telemetry=True)
+    assert np.array_equal(t.cpu().numpy(), np.sort(x))
+    assert tel.route is Route.MAIN and ot.route == "main"
+    assert not tel.device_guard_fired and tel.pairs == np.unique(x).shape[0] > 2_200_000
+    assert (tel.spill_len, tel.guard_fired, tel.updates) == (ot.spill_len, ot.guard_fired, ot.updates)
+    assert (tel.table.hits, tel.table.claims, tel.table.spill_pushes) == (ot.hits, ot.claims,
+                                                                          ot.spill_pushes)

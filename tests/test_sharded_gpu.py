@@ -42,7 +42,7 @@ def _cases():
         "empty_shard": (main[:50_000], [50_000]),
         "distinct_uneven": (ogen.distinct_values(300_000, 10).view(np.int64), [1_001]),
         "skew": (_skew(), [100_001]),
-        "guard": (_guard_input(), [2_500_000]),
+        "guard": (_guard_input(), [10_000_000]),
         "int32": (np.minimum(np.random.default_rng(8).zipf(1.3, 700_000), 3000).astype(np.int32)
                   - 1500, [250_000]),
     }
@@ -55,8 +55,8 @@ def _skew():
 
 
 def _guard_input():
-    """More distinct keys than the device table holds, under a low estimate."""
-    n = 5_000_000
+    """More distinct keys than the device table holds (16 Mi), under a low estimate."""
+    n = 20_000_000
     x = ogen.mix_outputs(77, n).view(np.int64).copy()
     x[::n // 1024][:1024] = np.arange(1024, dtype=np.int64) % 100
     return x
