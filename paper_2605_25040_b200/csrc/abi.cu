@@ -101,6 +101,18 @@ struct cafs_ctx {
   uint64_t graph_clock = 0;
 };
 
+namespace cafs {
+bool pdl_enabled(unsigned which) {  // programmatic dependent launch (common.cuh)
+  static const unsigned mask = [] {
+    const char* e = getenv("CAFS_PDL");
+    // default: not the spill fold and the compaction -- measured on cfg3, their
+    // early-launched CTAs cost 25 and 45 us (the other kernels gain 2-5 us)
+    return e ? (unsigned)strtoul(e, nullptr, 0) : 0xffu & ~(kPdlSpill | kPdlCompact);
+  }();
+  return (mask & which) != 0;
+}
+}  // namespace cafs
+
 namespace {
 
 // hash-table pairs + the ~0 sentinel pair + dense-window pairs appended after them
@@ -834,10 +846,10 @@ int cafs_ctx_create(int device, cafs_ctx_t** out) {
   if (e != cudaSuccess) { delete ctx; return CAFS_ECUDA; }
   if (prop.major != 10) { delete ctx; return CAFS_EINVAL; }  // sm_100a only
   ctx->num_sms = prop.multiProcessorCount;
-  if (cudaMalloc(&ctx->d_ctl, sizeof(DevCtl)) != cudaSuccess ||
+  if (cudaMalloc(&ctx->d_ctl, kDevCtlAlloc) != cudaSuccess ||
       cudaMallocHost(&ctx->h_ctl, sizeof(DevCtl)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_scratch, 64 + CAFS_PARTITION_BUCKETS * 4) != cudaSuccess ||
-      cudaMemset(ctx->d_ctl, 0, sizeof(DevCtl)) != cudaSuccess) {
+      cudaMemset(ctx->d_ctl, 0, kDevCtlAlloc) != cudaSuccess) {
     cafs_ctx_destroy(ctx);
     return CAFS_ENOMEM;
   }

@@ -85,6 +85,17 @@ struct DevCtl {
   int32_t local_overflow;        // ... lost to a global-table overflow
 };
 
+// Device-only scratch allocated right after the DevCtl (not in its host
+// mirror): the estimate kernel's gathered samples and arrival counter.
+struct EstScratch {
+  u64 samples[kSampleTarget];
+  u32 arrive;  // estimate CTAs done with phase A (low 16 bits) and those that
+               // found an inversion in the monotone prefix (high bits); the last resets
+  u32 _pad;
+};
+__host__ __device__ inline EstScratch* est_scratch(DevCtl* c) { return (EstScratch*)(c + 1); }
+constexpr size_t kDevCtlAlloc = sizeof(DevCtl) + sizeof(EstScratch);
+
 // Row-shard header (shard.cu), all-gathered across ranks: rows, local monotone
 // state (0 no, 1 yes, 2 prefix sorted -> see word 4), first and last key
 // (order-mapped), an inversion found by the full scan.
@@ -99,6 +110,42 @@ enum : int {
   kGateNone = 0, kGateTiny = 1, kGateMain = 2, kGateMainDense = 3, kGateMainHash = 4,
   kGateDense = 5, kGateHash = 6  // window open / closed, whatever the route (stage APIs)
 };
+
+// Programmatic dependent launch (sm_90+).  Pipeline kernels are launched with
+// launch_pdl: the next kernel's CTAs may be scheduled while this one drains,
+// so its launch latency hides behind the predecessor's tail.  Every kernel so
+// launched starts with pdl_begin(): griddepcontrol.wait blocks until the
+// predecessor grid has completed and its writes are visible (unconditionally,
+// so the dependency chain stays transitive), then lets its own dependents
+// launch.  Outside a programmatic dependency both instructions are no-ops.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// which kernels (bit per kernel, kPdl*) launch programmatically; CAFS_PDL
+// overrides the mask (abi.cu)
+enum : unsigned {
+  kPdlEstimate = 1, kPdlTiny = 2, kPdlCount = 4, kPdlSpill = 8, kPdlCompact = 16,
+  kPdlDense = 32, kPdlPairSort = 64, kPdlEmit = 128
+};
+bool pdl_enabled(unsigned which);
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(unsigned which, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                              size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled(which) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 __device__ __forceinline__ bool gate_open(const DevCtl* ctl, int gate) {
   if (gate == kGateNone) return true;

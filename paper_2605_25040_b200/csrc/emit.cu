@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kEmitThreads)
     emit_kernel(const u64* __restrict__ keys, const u64* __restrict__ goffs, u64 npairs_arg,
                 const DevCtl* ctl, typename KeyT<KK>::T* __restrict__ out, u64 begin, u64 end,
                 u64 flip, u64 tpw, u64 idx_entries, int ctl_slice) {
+  pdl_begin();
   using K = typename KeyT<KK>::T;
   constexpr u64 VK = 32 / sizeof(K);             // keys per 32-byte vector
   constexpr u64 kTileKeys = kTileBytes / sizeof(K);
@@ -203,16 +204,16 @@ void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl
   const size_t sm = ((u64)idx + 1) * 8;
   switch (kk) {
     case 1:
-      emit_kernel<1><<<(unsigned)grid, kEmitThreads, sm, st>>>(
-          keys, offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
+      launch_pdl(kPdlEmit, emit_kernel<1>, (unsigned)grid, kEmitThreads, sm, st, keys, offs, npairs, ctl,
+                 (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
       break;
     case 2:
-      emit_kernel<2><<<(unsigned)grid, kEmitThreads, sm, st>>>(
-          keys, offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
+      launch_pdl(kPdlEmit, emit_kernel<2>, (unsigned)grid, kEmitThreads, sm, st, keys, offs, npairs, ctl,
+                 (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
       break;
     default:
-      emit_kernel<0><<<(unsigned)grid, kEmitThreads, sm, st>>>(
-          keys, offs, npairs, ctl, (u64*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
+      launch_pdl(kPdlEmit, emit_kernel<0>, (unsigned)grid, kEmitThreads, sm, st, keys, offs, npairs, ctl,
+                 (u64*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
   }
 }
 

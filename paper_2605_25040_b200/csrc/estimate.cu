@@ -63,6 +63,13 @@ __device__ __forceinline__ u64 warp_max_u64(u64 v) {
 
 constexpr int kFreqSlots = 2048;  // <= 50% load for 1024 samples (reference: 4096, cardinality.py:27)
 
+// Phase A runs on kEstCtas CTAs: each loads its 1024 / kEstCtas samples and
+// checks its stretch of the prefix, so the ~140 KB of scattered reads take one
+// DRAM round trip per SM instead of ~16 on one SM.  The last CTA to arrive
+// (threadfence + arrival counter, self-resetting) runs phase B: FreqSet,
+// spectrum, Chao1, route.
+constexpr int kEstCtas = 16;
+
 template <int KK>
 __global__ void __launch_bounds__(1024, 1)
     estimate_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip, int check_prefix,
@@ -76,15 +83,52 @@ __global__ void __launch_bounds__(1024, 1)
   __shared__ u64 rmin[32], rmax[32];
   __shared__ long long red[3][32];
   __shared__ u32 n_max_key;  // occurrences of the sentinel value ~0 among the samples
-  __shared__ int inv;
+  __shared__ int am_last, inv;
   __shared__ int best_t;
   __shared__ u32 nlist;
   __shared__ u64 klist[CAFS_TINY_MAX_KEYS];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  pdl_begin();
+  EstScratch* es = est_scratch(ctl);
+  u64 nn = n;  // rows of the column
+  if (ghdr) {
+    nn = 0;
+    for (int r = 0; r < world; ++r) nn += ghdr[r * kShardHdrWords];
+  }
+  const u64 m = nn < (u64)kSampleTarget ? nn : (u64)kSampleTarget;
+  u64 stride = ghdr ? 1 : n / kSampleTarget;
+  if (stride < 1) stride = 1;
 
+  // ---- phase A (every CTA): this CTA's strided samples (cardinality.py:102-104)
+  // and its (x[r], x[r+1]) pairs of the reference's first chunk (sorter.py:115-129),
+  // all loads in flight together ----
+  const int G = gridDim.x;
+  const int per = kSampleTarget / G;
+  u64 sv = 0;
+  const u64 si = (u64)blockIdx.x * per + tid;
+  if (tid < per && si < m) sv = key_map<KK>(x[si * stride], flip);
+  int found = 0;
+  if (check_prefix) {
+    const u64 P = n < kMonoPrefix ? n : kMonoPrefix;
+    for (u64 r = (u64)blockIdx.x * 1024 + tid; r + 1 < P; r += (u64)G * 1024)
+      found |= key_map<KK>(x[r + 1], flip) < key_map<KK>(x[r], flip);
+  }
+  if (tid < per) {  // publish (only the writers fence: a fence costs ~1k cycles)
+    __stcg(&es->samples[si], sv);
+    __threadfence();
+  }
+  found = __syncthreads_or(found);
+  if (tid == 0) {  // arrivals in the low 16 bits, CTAs that saw an inversion above
+    const u32 old = atomicAdd(&es->arrive, 1u + (found ? 0x10000u : 0u));
+    am_last = (old & 0xffffu) == (u32)(G - 1);
+    inv = (old >> 16) + (u32)found > 0;
+  }
+  __syncthreads();
+  if (!am_last) return;
+
+  // ---- phase B (the last CTA) ----
   for (int i = tid; i < kFreqSlots; i += 1024) { fkeys[i] = kEmpty; fcnt[i] = 0; }
   if (tid == 0) {
-    inv = 0;
     best_t = 0x7fffffff;
     n_max_key = 0;
     nlist = 0;
@@ -106,35 +150,10 @@ __global__ void __launch_bounds__(1024, 1)
   }
   if (tid < 16) ctl->tiny_counts[tid] = 0;
   if (tid < kListStripes) ctl->g_fill[tid] = 0;
-  u64 nn = n;  // rows of the column
-  if (ghdr) {
-    nn = 0;
-    for (int r = 0; r < world; ++r) nn += ghdr[r * kShardHdrWords];
-  }
-  __syncthreads();
-
-  // ---- K0 + K1 loads, all in flight together: the prefix pairs (16 coalesced
-  // (x[i], x[i+1]) pairs per thread over the reference's first chunk) and this
-  // thread's strided sample (cardinality.py:102-104) ----
-  const u64 m = nn < (u64)kSampleTarget ? nn : (u64)kSampleTarget;
-  u64 stride = ghdr ? 1 : n / kSampleTarget;
-  if (stride < 1) stride = 1;
   const bool valid = (u64)tid < m;
-  const u64 v = valid ? key_map<KK>(x[(u64)tid * stride], flip) : 0;
-  if (check_prefix) {
-    // thread t checks the 16 adjacent pairs of rows [16t, 16t + 16]: 17 keys,
-    // one contiguous run per thread (the warp reads one 4 KB stretch)
-    const u64 P = n < kMonoPrefix ? n : kMonoPrefix;
-    const u64 i0 = (u64)tid * 16;
-    K a[17];
-#pragma unroll
-    for (int j = 0; j < 17; ++j) a[j] = i0 + j < P ? x[i0 + j] : 0;
-    int found = 0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      found |= (i0 + j + 1 < P) && key_map<KK>(a[j + 1], flip) < key_map<KK>(a[j], flip);
-    if (found) inv = 1;  // benign race: any writer sets 1
-  }
+  const u64 v = valid ? __ldcg(&es->samples[tid]) : 0ull;
+  __syncthreads();
+  if (tid == 0) es->arrive = 0;  // ready for the next call (every CTA has arrived)
   // insert the sample into the FreqSet; equal samples of a warp are merged
   // first (one insert of count c instead of c contending atomics -- low
   // cardinality inputs put ~128 samples on one slot)
@@ -308,13 +327,16 @@ void launch_estimate(const void* x, u64 n, u64 flip, int check_prefix, DevCtl* c
                      cudaStream_t st, int kk) {
   switch (kk) {
     case 1:
-      estimate_kernel<1><<<1, 1024, 0, st>>>((const u32*)x, n, flip, check_prefix, ctl, nullptr, 0);
+      launch_pdl(kPdlEstimate, estimate_kernel<1>, kEstCtas, 1024, 0, st, (const u32*)x, n, flip, check_prefix,
+                 ctl, (const u64*)nullptr, 0);
       break;
     case 2:
-      estimate_kernel<2><<<1, 1024, 0, st>>>((const u32*)x, n, flip, check_prefix, ctl, nullptr, 0);
+      launch_pdl(kPdlEstimate, estimate_kernel<2>, kEstCtas, 1024, 0, st, (const u32*)x, n, flip, check_prefix,
+                 ctl, (const u64*)nullptr, 0);
       break;
     default:
-      estimate_kernel<0><<<1, 1024, 0, st>>>((const u64*)x, n, flip, check_prefix, ctl, nullptr, 0);
+      launch_pdl(kPdlEstimate, estimate_kernel<0>, kEstCtas, 1024, 0, st, (const u64*)x, n, flip, check_prefix,
+                 ctl, (const u64*)nullptr, 0);
   }
 }
 

@@ -7,10 +7,10 @@
 // (key, count) cell, cells are merged by key, the spill guard re-routes to the
 // fallback -- with a layout for 148 SMs:
 //
-//   * persistent CTAs (one per SM, 1024 threads); thread 0 doubles as the TMA
-//     producer that streams 32 KB chunks of the int64 column into a 3-stage
-//     shared-memory ring (cp.async.bulk + mbarrier complete_tx); all 32 warps
-//     consume, two 16-byte vectors per thread per stage;
+//   * persistent CTAs (one per SM, 1024 threads); warp 0's lane 0 is the TMA
+//     producer that streams 16-32 KB chunks of the int64 column into a
+//     shared-memory ring (cp.async.bulk + mbarrier complete_tx; 9 x 15.5 KB for
+//     the dense-window shape, 143 KB in flight per SM); warps 1..31 consume;
 //   * per element (bit-63 flip in registers):
 //       - dense-range window (dictionary-encoded columns): one shared atomic
 //         into counts[v - base]; the window is set by the estimate kernel from
@@ -33,15 +33,13 @@ namespace cafs {
 constexpr int kHcThreads = 1024;
 constexpr u32 kRange = 8192;              // dense window (u32 counters, 32 KB)
 constexpr int kSLog2 = 13;                // shared table: 8192 slots (64 KB keys + 32 KB counts)
-constexpr u32 kS = 1u << kSLog2;
 constexpr int kSMaxProbe = 4;             // a longer chain spills: the table is only a cache
                                           // of partial counts, so a key found in two places
                                           // (or in a slot and the spill) still sums right
-constexpr size_t kTableSmem = (size_t)kRange * 4 + (size_t)kS * 8 + (size_t)kS * 4;
-template <int STAGES, int STAGE_KEYS, int QCAP, bool RANGE>
+template <int STAGES, int STAGE_KEYS, int QCAP, bool RANGE, int SLOG2 = kSLog2>
 constexpr size_t hc_smem() {
-  return kTableSmem - (RANGE ? 0 : (size_t)kRange * 4) + (size_t)STAGES * STAGE_KEYS * 8 +
-         (size_t)32 * QCAP * 8 + (size_t)2 * STAGES * 8 + 16;
+  return (RANGE ? (size_t)kRange * 4 : 0) + ((size_t)12 << SLOG2) +
+         (size_t)STAGES * STAGE_KEYS * 8 + (size_t)32 * QCAP * 8 + (size_t)2 * STAGES * 8 + 16;
 }
 
 struct HcArgs {
@@ -130,8 +128,12 @@ __device__ __forceinline__ void resolve_or_spill(bool active, u64 v, u64* skeys,
 // of a diverged warp, leaving its L2 round trips unoverlapped).
 // RANGE = false: no dense window (launched only when the window is closed).
 // STAGE_KEYS counts 8-byte words; a stage holds STAGE_KEYS * 8 / sizeof(K) keys.
-template <int STAGES, int STAGE_KEYS, int QCAP, bool RANGE, int KK>
+// SLOG2: log2 of the shared table's slots (the dense-window shape gives some
+// of them to a deeper ring: its keys rarely reach the table).
+template <int STAGES, int STAGE_KEYS, int QCAP, bool RANGE, int KK, int SLOG2 = kSLog2>
 __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
+  constexpr u32 kS = 1u << SLOG2;
+  pdl_begin();
   if (!gate_open(a.ctl, a.gate)) return;
   using K = typename KeyT<KK>::T;
   constexpr int KPV = 16 / sizeof(K);                         // keys per 16-byte vector
@@ -192,12 +194,12 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
     const u64 d = v - base;
     if (RANGE && d < rlen) { atomicAdd(&dcnt[d], 1u); return true; }
     if (v == kEmpty) { empty_cnt++; return true; }
-    const u32 h = mhash(v, mult, 64 - kSLog2);
+    const u32 h = mhash(v, mult, 64 - SLOG2);
     if (skeys[h] == v) { atomicAdd(&scnt[h], 1u); return true; }
     return false;
   };
   auto count1 = [&](u64 v) {
-    if (!fast(v)) glob_cnt += count_slow(v, skeys, scnt, &sclaims, a);
+    if (!fast(v)) glob_cnt += count_slow<SLOG2>(v, skeys, scnt, &sclaims, a);
   };
 
   if (wid == 0) {
@@ -227,7 +229,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
         const u64 u = wq[qn - 32 + lane];
         __syncwarp();
         qn -= 32;
-        resolve_or_spill(true, u, skeys, scnt, &sclaims, &sfill, region, region_cap, a);
+        resolve_or_spill<SLOG2>(true, u, skeys, scnt, &sclaims, &sfill, region, region_cap, a);
       }
     };
     // 32-bit keys: is the dense window inside the 32-bit domain?  Then a key
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
     }
     if (QCAP > 0) {
       __syncwarp();
-      resolve_or_spill((u32)lane < qn, (u32)lane < qn ? wq[lane] : 0ull, skeys, scnt, &sclaims,
+      resolve_or_spill<SLOG2>((u32)lane < qn, (u32)lane < qn ? wq[lane] : 0ull, skeys, scnt, &sclaims,
                        &sfill, region, region_cap, a);
     }
     if (blockIdx.x == 0 && ctid < 32) {  // head and tail keys (< KPV each)
@@ -390,6 +392,7 @@ constexpr u64 kBigMinRows = 1ull << 22;  // below: the 8192-slot queued shape
 
 template <int KK>
 __global__ void __launch_bounds__(kHcThreads, 1) hash_count_big_kernel(HcArgs a) {
+  pdl_begin();
   if (!gate_open(a.ctl, a.gate)) return;
   using K = typename KeyT<KK>::T;
   constexpr int KPV = 16 / sizeof(K);
@@ -532,7 +535,7 @@ static cudaError_t launch_hc_big(const HcArgs& a, u64 n, int num_sms, cudaStream
   const u64 kpv = KK ? 4 : 2;
   const u64 rounds = (n / kpv + (u64)kBigUnroll * kHcThreads - 1) / ((u64)kBigUnroll * kHcThreads);
   const int grid = (int)(rounds < (u64)num_sms ? (rounds ? rounds : 1) : (u64)num_sms);
-  hash_count_big_kernel<KK><<<grid, kHcThreads, kBigSmem, st>>>(a);
+  return launch_pdl(kPdlCount, hash_count_big_kernel<KK>, grid, kHcThreads, kBigSmem, st, a);
   return cudaGetLastError();
 }
 
@@ -543,6 +546,7 @@ static cudaError_t launch_hc_big(const HcArgs& a, u64 n, int num_sms, cudaStream
 __global__ void __launch_bounds__(256) compact_kernel(DevCtl* ctl, u64* gkeys, u64* gcnt,
                                                       const u32* glist, u64* pkeys, u64* pcnt,
                                                       int gate) {
+  pdl_begin();
   if (ctl->overflow || !gate_open(ctl, gate)) return;
   __shared__ u64 pre_sh, tot_sh;
   const u32 s = blockIdx.x;
@@ -587,6 +591,7 @@ __global__ void __launch_bounds__(256) compact_kernel(DevCtl* ctl, u64* gkeys, u
 // thread a key: convergent, L2-atomic-throughput bound).
 __global__ void spill_fold_kernel(DevCtl* ctl, const u64* __restrict__ spill, u64* gkeys,
                                   u64* gcnt, u32* glist, u64 mult, int gate) {
+  pdl_begin();
   if (!gate_open(ctl, gate)) return;
   const u32 nreg = ctl->spill_regions;
   if (blockIdx.x >= nreg) return;
@@ -614,8 +619,8 @@ __global__ void spill_fold_kernel(DevCtl* ctl, const u64* __restrict__ spill, u6
 void launch_spill_fold(DevCtl* ctl, const u64* spill, u64* gkeys, u64* gcnt, u32* glist, u64 mult,
                        int num_sms, cudaStream_t st, int gate) {
   // regions x slices: a few CTAs per region keep every SM's warps issuing
-  spill_fold_kernel<<<dim3(kMaxSpillRegions, 8), 256, 0, st>>>(ctl, spill, gkeys, gcnt, glist,
-                                                              mult, gate);
+  launch_pdl(kPdlSpill, spill_fold_kernel, dim3(kMaxSpillRegions, 8), 256, 0, st, ctl, spill, gkeys, gcnt,
+             glist, mult, gate);
 }
 
 // Dense-window counts -> (key, count) pairs in key order (the window is a key
@@ -625,6 +630,7 @@ void launch_spill_fold(DevCtl* ctl, const u64* spill, u64* gkeys, u64* gcnt, u32
 __global__ void __launch_bounds__(1024) dense_pairs_kernel(DevCtl* ctl, u64* dense, u64* pkeys,
                                                            u64* pcnt, u64* skeys, u64* scnt,
                                                            u64* soffs, u64 n_expect, int gate) {
+  pdl_begin();
   if (!gate_open(ctl, gate)) return;  // the count kernel was gated off too: dense untouched
   if (ctl->overflow) {  // guard: the fallback sorts; leave the window zeroed for the next call
     for (u32 d = threadIdx.x; d < ctl->range_len; d += blockDim.x) dense[d] = 0;
@@ -707,8 +713,8 @@ __global__ void __launch_bounds__(1024) dense_pairs_kernel(DevCtl* ctl, u64* den
 
 void launch_dense_pairs(DevCtl* ctl, u64* dense, u64* pkeys, u64* pcnt, u64* skeys, u64* scnt,
                         u64* soffs, u64 n_expect, cudaStream_t st, int gate) {
-  dense_pairs_kernel<<<1, 1024, 0, st>>>(ctl, dense, pkeys, pcnt, skeys, scnt, soffs, n_expect,
-                                         gate);
+  launch_pdl(kPdlDense, dense_pairs_kernel, 1, 1024, 0, st, ctl, dense, pkeys, pcnt, skeys, scnt, soffs,
+             n_expect, gate);
 }
 
 size_t dense_window_len() { return kRange; }
@@ -754,15 +760,15 @@ void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevC
                                                          glist);
 }
 
-template <int ST, int SK, int QC, bool RG, int KK = 0>
+template <int ST, int SK, int QC, bool RG, int KK = 0, int SL = kSLog2>
 static cudaError_t launch_hc(const HcArgs& a, u64 n, int num_sms, cudaStream_t st) {
-  constexpr size_t sm = hc_smem<ST, SK, QC, RG>();
+  constexpr size_t sm = hc_smem<ST, SK, QC, RG, SL>();
   static_assert(sm <= 232448 - 2048, "shared memory budget");
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(hash_count_kernel<ST, SK, QC, RG, KK>,
+    cudaError_t e = cudaFuncSetAttribute(hash_count_kernel<ST, SK, QC, RG, KK, SL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     attr_dev = dev;
@@ -770,7 +776,7 @@ static cudaError_t launch_hc(const HcArgs& a, u64 n, int num_sms, cudaStream_t s
   const u64 keys_per_stage = (u64)SK * 8 / (KK ? 4 : 8);
   const u64 chunks = (n + keys_per_stage - 1) / keys_per_stage;
   const int grid = (int)(chunks < (u64)num_sms ? (chunks ? chunks : 1) : (u64)num_sms);
-  hash_count_kernel<ST, SK, QC, RG, KK><<<grid, kHcThreads, sm, st>>>(a);
+  return launch_pdl(kPdlCount, hash_count_kernel<ST, SK, QC, RG, KK, SL>, grid, kHcThreads, sm, st, a);
   return cudaGetLastError();
 }
 
@@ -787,9 +793,11 @@ cudaError_t launch_hash_count(const void* x, u64 n, u64 flip, u64 mult, DevCtl* 
   const bool window = use_range && gate != kGateMainHash && gate != kGateHash;
   (void)variant;
   if (window) {
-    if (kk == 1) return launch_hc<3, 3968, 0, true, 1>(a, n, num_sms, st);
-    if (kk == 2) return launch_hc<3, 3968, 0, true, 2>(a, n, num_sms, st);
-    return launch_hc<3, 3968, 0, true, 0>(a, n, num_sms, st);
+    // 9 x 15.5 KB ring, 4096-slot table: 143 KB in flight per SM (3 x 31 KB
+    // with 8192 slots left the cfg4 count at 6.85 TB/s; this shape 7.19)
+    if (kk == 1) return launch_hc<9, 1984, 0, true, 1, 12>(a, n, num_sms, st);
+    if (kk == 2) return launch_hc<9, 1984, 0, true, 2, 12>(a, n, num_sms, st);
+    return launch_hc<9, 1984, 0, true, 0, 12>(a, n, num_sms, st);
   }
   if (n < kBigMinRows) {  // small columns: the table's init and flush would dominate
     if (kk == 1) return launch_hc<3, 3968, 64, false, 1>(a, n, num_sms, st);
@@ -803,7 +811,7 @@ cudaError_t launch_hash_count(const void* x, u64 n, u64 flip, u64 mult, DevCtl* 
 
 void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys, u64* pcnt,
                     int num_sms, cudaStream_t st, int gate) {
-  compact_kernel<<<kListStripes, 256, 0, st>>>(ctl, gkeys, gcnt, glist, pkeys, pcnt, gate);
+  launch_pdl(kPdlCompact, compact_kernel, kListStripes, 256, 0, st, ctl, gkeys, gcnt, glist, pkeys, pcnt, gate);
 }
 
 }  // namespace cafs

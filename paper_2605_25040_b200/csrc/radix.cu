@@ -222,6 +222,7 @@ template <bool PAIRS>
 __global__ void __launch_bounds__(1024, 1)
     small_sort_kernel(u64* keys_io, const u64* in_cnt, u64 n_arg, u64 flip, DevCtl* ctl,
                       u64 expect_total, u64* out_keys, u64* out_cnt, u64* out_offs, int gate) {
+  pdl_begin();
   extern __shared__ __align__(16) unsigned char smem[];
   u64* kb = (u64*)smem;                                       // [2][kSmallSortMax]
   unsigned short* ib = (unsigned short*)(kb + 2 * kSmallSortMax);  // [2][kSmallSortMax]
@@ -580,9 +581,8 @@ cudaError_t launch_small_sort_pairs(u64* keys, const u64* cnt, u64 n, DevCtl* ct
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  small_sort_kernel<true><<<1, 1024, sm, st>>>(keys, cnt, n, 0, ctl, expect, out_keys, out_cnt,
-                                               out_offs, gate);
-  return cudaGetLastError();
+  return launch_pdl(kPdlPairSort, small_sort_kernel<true>, 1, 1024, sm, st, keys, cnt, n, (u64)0, ctl, expect,
+                    out_keys, out_cnt, out_offs, gate);
 }
 
 void launch_scan(const u64* in, u64 n, u64* bsum, u64* out_offs, DevCtl* ctl, u64 expect,

@@ -48,6 +48,7 @@ template <int KK>
 __global__ void __launch_bounds__(kTinyThreads, 4)  // 2048 threads per SM: more loads in flight
     tiny_count_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip, DevCtl* ctl,
                       int gate, u64* pkeys, u64* pcnt, u64* poffs) {
+  pdl_begin();
   using K = typename KeyT<KK>::T;
   constexpr int KPV = 16 / sizeof(K);  // keys per 16-byte vector
   if (!gate_open(ctl, gate)) return;
@@ -145,16 +146,16 @@ void launch_tiny_count(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
   const unsigned g = (unsigned)blocks;
   switch (kk) {
     case 1:
-      tiny_count_kernel<1><<<g, kTinyThreads, 0, st>>>((const u32*)x, n, flip, ctl, gate, pkeys,
-                                                       pcnt, poffs);
+      launch_pdl(kPdlTiny, tiny_count_kernel<1>, g, kTinyThreads, 0, st, (const u32*)x, n, flip, ctl, gate,
+                 pkeys, pcnt, poffs);
       break;
     case 2:
-      tiny_count_kernel<2><<<g, kTinyThreads, 0, st>>>((const u32*)x, n, flip, ctl, gate, pkeys,
-                                                       pcnt, poffs);
+      launch_pdl(kPdlTiny, tiny_count_kernel<2>, g, kTinyThreads, 0, st, (const u32*)x, n, flip, ctl, gate,
+                 pkeys, pcnt, poffs);
       break;
     default:
-      tiny_count_kernel<0><<<g, kTinyThreads, 0, st>>>((const u64*)x, n, flip, ctl, gate, pkeys,
-                                                       pcnt, poffs);
+      launch_pdl(kPdlTiny, tiny_count_kernel<0>, g, kTinyThreads, 0, st, (const u64*)x, n, flip, ctl, gate,
+                 pkeys, pcnt, poffs);
   }
 }
 
