@@ -49,7 +49,6 @@ struct cafs_ctx {
   u64* pc_b = nullptr;
   u64* poffs = nullptr;  // exclusive offsets, npairs + 1
   u64* bsum = nullptr;
-  u64* spill = nullptr;  // kSpillCap keys
   u64* dense = nullptr;  // dense-window counts (zero between calls)
   // radix sort scratch
   u32* ghist = nullptr;  // [8][256]
@@ -105,9 +104,9 @@ namespace cafs {
 bool pdl_enabled(unsigned which) {  // programmatic dependent launch (common.cuh)
   static const unsigned mask = [] {
     const char* e = getenv("CAFS_PDL");
-    // default: not the spill fold and the compaction -- measured on cfg3, their
-    // early-launched CTAs cost 25 and 45 us (the other kernels gain 2-5 us)
-    return e ? (unsigned)strtoul(e, nullptr, 0) : 0xffu & ~(kPdlSpill | kPdlCompact);
+    // default: not the compaction -- measured on cfg3, its early-launched CTAs
+    // cost 45 us (the other kernels gain 2-5 us)
+    return e ? (unsigned)strtoul(e, nullptr, 0) : 0xffu & ~kPdlCompact;
   }();
   return (mask & which) != 0;
 }
@@ -183,7 +182,6 @@ int ensure_main(cafs_ctx_t* ctx) {
   CK(cudaMalloc(&ctx->pc_b, kPairCap * 8));
   CK(cudaMalloc(&ctx->poffs, (kPairCap + 1) * 8));
   CK(cudaMalloc(&ctx->bsum, (kPairCap / 8192 + 2) * 8));
-  CK(cudaMalloc(&ctx->spill, kSpillCap * 8));
   CK(cudaMalloc(&ctx->dense, dense_window_len() * 8));
   CK(cudaMemset(ctx->dense, 0, dense_window_len() * 8));
   return CAFS_OK;
@@ -567,18 +565,16 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
   cudaError_t e;
   if (direct) {
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                          ctx->num_sms, st, 0, kGateMainDense, ctx->spill, ctx->dense, kk);
+                          ctx->num_sms, st, 0, kGateMainDense, ctx->dense, kk);
     if (e == cudaSuccess)
       e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                            ctx->num_sms, st, 1, kGateMainHash, ctx->spill, ctx->dense, kk);
+                            ctx->num_sms, st, 1, kGateMainHash, ctx->dense, kk);
   } else {
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 0,
-                          ctx->num_sms, st, 1, kGateMain, ctx->spill, ctx->dense, kk);
+                          ctx->num_sms, st, 1, kGateMain, ctx->dense, kk);
   }
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
   tm.end(tk, L_K_COUNT, C_MAIN);
-  launch_spill_fold(c, ctx->spill, ctx->gkeys, ctx->gcnt, ctx->glist, mult, ctx->num_sms, st,
-                    kGateMain);
   launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
                  kGateMain);
   if (direct)
@@ -598,7 +594,7 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
     tm.end(ts, L_STAGE_EMIT, C_EMIT);
     ctx->launches++;
   }
-  ctx->launches += direct ? 7 : 5;
+  ctx->launches += direct ? 6 : 4;
   CKL();
   return CAFS_OK;
 }
@@ -864,7 +860,7 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
   DeviceGuard g(ctx->device);
   cudaDeviceSynchronize();
   void* dev[] = {ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
-                 ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->spill, ctx->dense, ctx->ghist, ctx->gbase,
+                 ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->dense, ctx->ghist, ctx->gbase,
                  ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage, ctx->msd,
                  ctx->tl_keys, ctx->tl_idx, ctx->tl_first, ctx->tl_runs, ctx->tl_comp,
                  ctx->tl_offs, ctx->tl_acc, ctx->pk_t, ctx->pc_t, ctx->wide};
@@ -1165,21 +1161,19 @@ int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   // both count shapes, each gated on the estimate's window (no host round trip)
   cudaError_t e = launch_hash_count((const u64*)d_x, n, is_signed ? kSign : 0, hash_mult,
                                     ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                                    ctx->num_sms, st, 0, kGateDense, ctx->spill, ctx->dense);
+                                    ctx->num_sms, st, 0, kGateDense, ctx->dense);
   if (e == cudaSuccess)
     e = launch_hash_count((const u64*)d_x, n, is_signed ? kSign : 0, hash_mult, ctx->d_ctl,
                           ctx->gkeys, ctx->gcnt, ctx->glist, 1, ctx->num_sms, st, 1, kGateHash,
-                          ctx->spill, ctx->dense);
+                          ctx->dense);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
-  launch_spill_fold(ctx->d_ctl, ctx->spill, ctx->gkeys, ctx->gcnt, ctx->glist, hash_mult,
-                    ctx->num_sms, st, kGateNone);
   launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
                  ctx->num_sms, st, kGateNone);
   launch_dense_pairs(ctx->d_ctl, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b,
                      ctx->poffs, n, st, kGateNone);
   e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, ctx->d_ctl, n, ctx->pk_b, ctx->pc_b,
                               ctx->poffs, st, kGateNone);
-  ctx->launches += 7;
+  ctx->launches += 6;
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   TRY(sync_ctl(ctx, st));
   DevCtl c = *ctx->h_ctl;
@@ -1421,14 +1415,11 @@ int cafs_shard_count_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny);
   launch_shard_tiny_pack(c, (u64*)d_tiny, st);
   cudaError_t e = launch_hash_count(x, n, flip, hash_mult, c, ctx->gkeys, ctx->gcnt, ctx->glist,
-                                    1, ctx->num_sms, st, 0, kGateMainDense, ctx->spill,
-                                    ctx->dense);
+                                    1, ctx->num_sms, st, 0, kGateMainDense, ctx->dense);
   if (e == cudaSuccess)
     e = launch_hash_count(x, n, flip, hash_mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                          ctx->num_sms, st, 1, kGateMainHash, ctx->spill, ctx->dense);
+                          ctx->num_sms, st, 1, kGateMainHash, ctx->dense);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
-  launch_spill_fold(c, ctx->spill, ctx->gkeys, ctx->gcnt, ctx->glist, hash_mult, ctx->num_sms,
-                    st, kGateMain);
   launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
                  kGateMain);
   launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs, n, st,
@@ -1437,7 +1428,7 @@ int cafs_shard_count_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
                               kGateMain);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   launch_shard_pack_pairs(c, ctx->pk_b, ctx->pc_b, (u64*)d_send, cap, st);
-  ctx->launches += 11;
+  ctx->launches += 10;
   CKL();
   return CAFS_OK;
 }

@@ -30,8 +30,6 @@ constexpr int kGlobalLog2 = 25;
 constexpr u64 kGlobalSlots = 1ull << kGlobalLog2;
 constexpr u64 kGlobalCap = kGlobalSlots / 2;          // max distinct keys before the guard fires
 constexpr int kGlobalMaxProbe = 128;
-constexpr u64 kSpillCap = 1ull << 25;                 // HBM spill buffer (keys); excess goes inline
-constexpr u32 kMaxSpillRegions = 256;                 // >= count-kernel grid (one CTA per SM)
 // The claim list of the global table is striped: a claim from warp w of CTA b
 // appends to stripe (global warp index) % kListStripes, so claims from all SMs do not
 // serialise on one counter and the stripes fill evenly.  A full stripe is a
@@ -62,9 +60,6 @@ struct DevCtl {
   // --- main route ---
   u32 g_fill[kListStripes];      // claims per stripe of the global table's claim list
   u64 g_updates;                 // elements resolved in the global table
-  u64 spill_len;                 // keys appended to the HBM spill buffer
-  u32 spill_regions;             // count-kernel CTAs (one spill region each)
-  u32 spill_fill[kMaxSpillRegions];
   u64 empty_key_count;           // occurrences of the sentinel key value ~0
   int32_t overflow;              // global table overflow -> guard
   int32_t need_large;            // K' too large for the single-CTA pair sort
@@ -126,7 +121,7 @@ __device__ __forceinline__ void pdl_begin() {
 // which kernels (bit per kernel, kPdl*) launch programmatically; CAFS_PDL
 // overrides the mask (abi.cu)
 enum : unsigned {
-  kPdlEstimate = 1, kPdlTiny = 2, kPdlCount = 4, kPdlSpill = 8, kPdlCompact = 16,
+  kPdlEstimate = 1, kPdlTiny = 2, kPdlCount = 4, kPdlCompact = 16,
   kPdlDense = 32, kPdlPairSort = 64, kPdlEmit = 128
 };
 bool pdl_enabled(unsigned which);

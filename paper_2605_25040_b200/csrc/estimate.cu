@@ -136,8 +136,6 @@ __global__ void __launch_bounds__(1024, 1)
     ctl->scan_inversion = 0;
     ctl->tiny_miss = 0;
     ctl->g_updates = 0;
-    ctl->spill_len = 0;
-    ctl->spill_regions = 0;
     ctl->empty_key_count = 0;
     ctl->overflow = 0;
     ctl->need_large = 0;

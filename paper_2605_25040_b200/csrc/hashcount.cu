@@ -53,7 +53,6 @@ struct HcArgs {
   u32* glist;
   int use_range;
   int gate;
-  u64* spill;   // HBM spill buffer (queued variant), kSpillCap keys
   u64* dense;   // global dense-window counts [kRange] (zero on entry)
 };
 
@@ -96,28 +95,18 @@ __device__ __forceinline__ u32 count_slow(u64 v, u64* skeys, u32* scnt, u32* scl
   return 1;
 }
 
-// Warp-convergent slow path of the queued variant: keys the shared table cannot
-// take are appended to this CTA's region of the HBM spill buffer (a shared
-// cursor, one atomic per warp batch, coalesced stores) -- the reference's spill
-// (buckets.py:273-282) -- and folded into the global table afterwards by
-// spill_fold_kernel with the whole GPU in parallel.  A full region falls back to
-// inline global inserts.
+// Warp-convergent slow path of the queued shapes: the warp's queued misses are
+// probed in the CTA's table 32 at a time, and those it cannot take go straight
+// to the L2-resident global table -- the reference's spill (buckets.py:273-282)
+// without the spill buffer: a fold pass over spilled keys cost more (cfg3:
+// +100 us) than the inline L2 round trips it saves in the count (+45 us).
+// Returns 1 on the lanes whose key went to the global table.
 template <int SLOG2 = kSLog2>
-__device__ __forceinline__ void resolve_or_spill(bool active, u64 v, u64* skeys, u32* scnt,
-                                                 u32* sclaims, u32* sfill, u64* region,
-                                                 u32 region_cap, const HcArgs& a) {
+__device__ __forceinline__ u32 resolve_miss(bool active, u64 v, u64* skeys, u32* scnt, u32* sclaims,
+                                            const HcArgs& a) {
   const bool miss = active && !probe_smem<SLOG2>(v, skeys, scnt, sclaims, a.mult);
-  const u32 m = __ballot_sync(0xffffffffu, miss);
-  if (m == 0) return;
-  const int lane = threadIdx.x & 31;
-  u32 base = 0;
-  if (lane == 0) base = atomicAdd(sfill, (u32)__popc(m));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (miss) {
-    const u32 pos = base + __popc(m & lanemask_lt());
-    if (pos < region_cap) region[pos] = v;
-    else global_insert(a.gkeys, a.gcnt, a.glist, a.ctl, v, 1, a.mult);
-  }
+  if (miss) global_insert(a.gkeys, a.gcnt, a.glist, a.ctl, v, 1, a.mult);
+  return miss ? 1u : 0u;
 }
 
 // STAGES x STAGE_KEYS TMA ring fed by a dedicated producer warp (warp 0);
@@ -149,23 +138,19 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   u64* queue = (u64*)(dcnt + (RANGE ? kRange : 0));               // [32][QCAP]
   u64* full = queue + 32 * QCAP;                                  // [STAGES]
   u64* empty = full + STAGES;                                     // [STAGES]
-  __shared__ u32 sclaims, sfill;
+  __shared__ u32 sclaims;
   __shared__ u64 red_empty[32], red_glob[32];
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u64 flip = a.flip, mult = a.mult;
   const u64 base = (RANGE && a.use_range) ? a.ctl->range_base : 0ull;
   const u64 rlen = (RANGE && a.use_range) ? a.ctl->range_len : 0u;
-  // this CTA's spill region
-  const u32 region_cap = (u32)(kSpillCap / gridDim.x);
-  u64* region = a.spill + (u64)blockIdx.x * region_cap;
 
   for (u32 i = tid; i < kS; i += kHcThreads) { skeys[i] = kEmpty; scnt[i] = 0; }
   if (RANGE)
     for (u32 i = tid; i < kRange; i += kHcThreads) dcnt[i] = 0;
   if (tid == 0) {
     sclaims = 0;
-    sfill = 0;
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers / 32);
@@ -229,7 +214,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
         const u64 u = wq[qn - 32 + lane];
         __syncwarp();
         qn -= 32;
-        resolve_or_spill<SLOG2>(true, u, skeys, scnt, &sclaims, &sfill, region, region_cap, a);
+        glob_cnt += resolve_miss<SLOG2>(true, u, skeys, scnt, &sclaims, a);
       }
     };
     // 32-bit keys: is the dense window inside the 32-bit domain?  Then a key
@@ -319,8 +304,8 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
     }
     if (QCAP > 0) {
       __syncwarp();
-      resolve_or_spill<SLOG2>((u32)lane < qn, (u32)lane < qn ? wq[lane] : 0ull, skeys, scnt, &sclaims,
-                       &sfill, region, region_cap, a);
+      glob_cnt += resolve_miss<SLOG2>((u32)lane < qn, (u32)lane < qn ? wq[lane] : 0ull, skeys, scnt,
+                                      &sclaims, a);
     }
     if (blockIdx.x == 0 && ctid < 32) {  // head and tail keys (< KPV each)
       const u64 tail0 = head + body;
@@ -367,12 +352,6 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
     for (int w = 0; w < kHcThreads / 32; ++w) { e += red_empty[w]; gg += red_glob[w]; }
     if (e) atomicAdd(&a.ctl->empty_key_count, e);
     if (gg) atomicAdd(&a.ctl->g_updates, gg);
-    if (QCAP > 0) {
-      const u32 f = sfill < region_cap ? sfill : region_cap;
-      a.ctl->spill_fill[blockIdx.x] = f;
-      atomicAdd(&a.ctl->spill_len, (u64)f);
-      atomicMax(&a.ctl->spill_regions, gridDim.x);
-    }
   }
 }
 
@@ -381,8 +360,8 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
 // with direct 16-byte streaming loads (this shape is bound by the table work,
 // ~1.5 TB/s, not by HBM, so the TMA ring buys nothing while taking 93 KB).
 // With twice the slots, a skewed column misses the CTA's table on ~13 % of its
-// keys instead of ~21 % (cfg3), and every miss costs a probe, a spill write
-// and a fold insert.
+// keys instead of ~21 % (cfg3), and every miss costs a probe and an L2
+// round trip into the global table.
 constexpr int kBigSLog2 = 14;
 constexpr u32 kBigS = 1u << kBigSLog2;
 constexpr int kBigQcap = 64;
@@ -400,14 +379,12 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_big_kernel(HcArgs a)
   u64* skeys = (u64*)smem;                      // [kBigS]
   u32* scnt = (u32*)(skeys + kBigS);            // [kBigS]
   u64* queue = (u64*)(scnt + kBigS);            // [32][kBigQcap]
-  __shared__ u32 sclaims, sfill;
+  __shared__ u32 sclaims;
   __shared__ u64 red_empty[32], red_glob[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u64 flip = a.flip, mult = a.mult;
-  const u32 region_cap = (u32)(kSpillCap / gridDim.x);
-  u64* region = a.spill + (u64)blockIdx.x * region_cap;
   for (u32 i = tid; i < kBigS; i += kHcThreads) { skeys[i] = kEmpty; scnt[i] = 0; }
-  if (tid == 0) { sclaims = 0; sfill = 0; }
+  if (tid == 0) sclaims = 0;
   __syncthreads();
 
   const u64 n = a.n;
@@ -436,7 +413,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_big_kernel(HcArgs a)
       const u64 u = wq[qn - 32 + lane];
       __syncwarp();
       qn -= 32;
-      resolve_or_spill<kBigSLog2>(true, u, skeys, scnt, &sclaims, &sfill, region, region_cap, a);
+      glob_cnt += resolve_miss<kBigSLog2>(true, u, skeys, scnt, &sclaims, a);
     }
   };
   auto fast = [&](u64 v) -> bool {
@@ -471,8 +448,8 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_big_kernel(HcArgs a)
     }
   }
   __syncwarp();
-  resolve_or_spill<kBigSLog2>((u32)lane < qn, (u32)lane < qn ? wq[lane] : 0ull, skeys, scnt,
-                              &sclaims, &sfill, region, region_cap, a);
+  glob_cnt += resolve_miss<kBigSLog2>((u32)lane < qn, (u32)lane < qn ? wq[lane] : 0ull, skeys,
+                                      scnt, &sclaims, a);
   if (blockIdx.x == 0 && tid < 32) {  // head and tail keys (< KPV each)
     const u64 tail0 = head + nvec * KPV;
     if ((u64)tid < head) {
@@ -512,10 +489,6 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_big_kernel(HcArgs a)
     for (int w2 = 0; w2 < kHcThreads / 32; ++w2) { e += red_empty[w2]; gg += red_glob[w2]; }
     if (e) atomicAdd(&a.ctl->empty_key_count, e);
     if (gg) atomicAdd(&a.ctl->g_updates, gg);
-    const u32 f = sfill < region_cap ? sfill : region_cap;
-    a.ctl->spill_fill[blockIdx.x] = f;
-    atomicAdd(&a.ctl->spill_len, (u64)f);
-    atomicMax(&a.ctl->spill_regions, gridDim.x);
   }
 }
 
@@ -585,42 +558,6 @@ __global__ void __launch_bounds__(256) compact_kernel(DevCtl* ctl, u64* gkeys, u
     if (e) { pkeys[tot] = kEmpty; pcnt[tot] = e; }
     ctl->npairs = tot + (e ? 1 : 0);
   }
-}
-
-// Fold the spill regions into the global table: block b takes region b (every
-// thread a key: convergent, L2-atomic-throughput bound).
-__global__ void spill_fold_kernel(DevCtl* ctl, const u64* __restrict__ spill, u64* gkeys,
-                                  u64* gcnt, u32* glist, u64 mult, int gate) {
-  pdl_begin();
-  if (!gate_open(ctl, gate)) return;
-  const u32 nreg = ctl->spill_regions;
-  if (blockIdx.x >= nreg) return;
-  const u32 cap = (u32)(kSpillCap / nreg);
-  const u64* region = spill + (u64)blockIdx.x * cap;
-  const u32 m = ctl->spill_fill[blockIdx.x];
-  constexpr int R = 8;
-  const u32 step = blockDim.x * R;
-  for (u32 i0 = blockIdx.y * step; i0 < m; i0 += step * gridDim.y) {
-    u64 key[R], inc[R];
-    bool ok[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const u32 i = i0 + r * blockDim.x + threadIdx.x;
-      ok[r] = i < m;
-      key[r] = ok[r] ? __ldcs(&region[i]) : 0;
-      inc[r] = 1;
-    }
-    global_insert_batch<R>(gkeys, gcnt, glist, ctl, key, inc, ok);
-  }
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
-    atomicAdd(&ctl->g_updates, ctl->spill_len);
-}
-
-void launch_spill_fold(DevCtl* ctl, const u64* spill, u64* gkeys, u64* gcnt, u32* glist, u64 mult,
-                       int num_sms, cudaStream_t st, int gate) {
-  // regions x slices: a few CTAs per region keep every SM's warps issuing
-  launch_pdl(kPdlSpill, spill_fold_kernel, dim3(kMaxSpillRegions, 8), 256, 0, st, ctl, spill, gkeys, gcnt,
-             glist, mult, gate);
 }
 
 // Dense-window counts -> (key, count) pairs in key order (the window is a key
@@ -737,8 +674,6 @@ __global__ void reset_ctl_kernel(DevCtl* ctl) {
   for (u32 t = threadIdx.x; t < kListStripes; t += blockDim.x) ctl->g_fill[t] = 0;
   if (threadIdx.x == 0) {
     ctl->g_updates = 0;
-    ctl->spill_len = 0;
-    ctl->spill_regions = 0;
     ctl->empty_key_count = 0;
     ctl->overflow = 0;
     ctl->need_large = 0;
@@ -783,13 +718,13 @@ static cudaError_t launch_hc(const HcArgs& a, u64 n, int num_sms, cudaStream_t s
 // shapes: 0 = dense window (deep TMA ring, inline slow path, the window's
 // counters in shared memory); without the window (the gate guarantees it is
 // closed -- kGateMainHash / kGateHash -- or use_range is 0) the big-table
-// shape with per-warp miss queues and the spill (the TMA queued shape for
+// shape with per-warp miss queues (the TMA queued shape for
 // columns under kBigMinRows rows)
 cudaError_t launch_hash_count(const void* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms,
-                              cudaStream_t st, int variant, int gate, u64* spill, u64* dense,
+                              cudaStream_t st, int variant, int gate, u64* dense,
                               int kk) {
-  HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate, spill, dense};
+  HcArgs a{x, n, flip, mult, ctl, gkeys, gcnt, glist, use_range, gate, dense};
   const bool window = use_range && gate != kGateMainHash && gate != kGateHash;
   (void)variant;
   if (window) {

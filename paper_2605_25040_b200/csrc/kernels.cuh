@@ -37,12 +37,10 @@ void launch_tiny_count(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
 // hashcount.cu
 cudaError_t launch_hash_count(const void* x, u64 n, u64 flip, u64 mult, DevCtl* ctl, u64* gkeys,
                               u64* gcnt, u32* glist, int use_range, int num_sms, cudaStream_t st,
-                              int variant, int gate, u64* spill, u64* dense, int kk = 0);
+                              int variant, int gate, u64* dense, int kk = 0);
 void launch_dense_pairs(DevCtl* ctl, u64* dense, u64* pkeys, u64* pcnt, u64* skeys, u64* scnt,
                         u64* soffs, u64 n_expect, cudaStream_t st, int gate);
 size_t dense_window_len();
-void launch_spill_fold(DevCtl* ctl, const u64* spill, u64* gkeys, u64* gcnt, u32* glist, u64 mult,
-                       int num_sms, cudaStream_t st, int gate);
 void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevCtl* ctl,
                          u64* gkeys, u64* gcnt, u32* glist, int num_sms, cudaStream_t st);
 void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys, u64* pcnt,
