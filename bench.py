@@ -106,8 +106,11 @@ def ncu_traffic(config: str, kernel: str):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)[config][kernel]
-        return d["dram_bytes_per_launch"]
+            t = json.load(f)[config]
+        if kernel.startswith("fallback sort stage"):  # the stage's kernels together
+            return sum(v["dram_bytes_per_launch"] for k, v in t.items()
+                       if k.startswith(("msd_", "bucket_")))
+        return t[kernel]["dram_bytes_per_launch"]
     except Exception:
         return None
 
