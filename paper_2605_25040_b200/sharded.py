@@ -330,6 +330,32 @@ class Comm:
         return torch.cat([o[:s] for o, s in zip(out, sizes)]).to(t.device)
 
 
+_OPS: dict = {}
+_COMMS: dict = {}
+
+
+def _device_ops(device: int, signed: bool) -> DeviceOps:
+    """One DeviceOps per (device, signedness): the context and library handles
+    are per process anyway, and building them costs host time on every call."""
+    ops = _OPS.get((device, signed))
+    if ops is None:
+        ops = _OPS[(device, signed)] = DeviceOps(device, signed)
+    return ops
+
+
+def _comm(group, device) -> Comm:
+    """One Comm per (process group, device); a destroyed default group is
+    replaced by a new object, so the key includes the group's identity."""
+    import torch.distributed as dist
+    g = group if group is not None else dist.group.WORLD
+    key = (id(g), str(device))
+    c = _COMMS.get(key)
+    if (c is None or c.group is not group or c.world != dist.get_world_size(group)
+            or c.rank != dist.get_rank(group)):
+        c = _COMMS[key] = Comm(group, device)
+    return c
+
+
 def msd_shift(g_min: int, g_max: int, bits: int = 12) -> int:
     """Shift that fits the span [g_min, g_max] into a `bits`-bit digit
     (k - g_min) >> shift (msd.cu msd_shift)."""
@@ -423,10 +449,10 @@ def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTeleme
         if signed is None:
             signed = x_local.dtype == torch.int64
         dev = x_local.device.index if x_local.device.index is not None else torch.cuda.current_device()
-        ops = DeviceOps(dev, signed)
+        ops = _device_ops(dev, signed)
     else:
         signed = ops.signed if signed is None else signed
-    comm = Comm(group, x_local.device if x_local.is_cuda else None)
+    comm = _comm(group, x_local.device if x_local.is_cuda else None)
     tel = telemetry if telemetry is not None else SortTelemetry()
     k0 = ops.kernel_count() if hasattr(ops, "kernel_count") else 0
     try:
@@ -445,6 +471,29 @@ def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTeleme
 SHARD_PAIR_CAP = 8192  # pairs per rank in the stream-ordered exchange (the pair sort's capacity)
 
 
+_SHARD_BUFS: dict = {}
+
+
+def _shard_buffers(dev, world: int, cap: int):
+    """The stream-ordered path's exchange buffers, allocated once per (device,
+    world size, stream): header, gathered headers, samples, tiny counters, the
+    send row and the gathered rows.  Every phase fully rewrites what it reads
+    next, and calls on one stream are ordered, so reuse across them is safe."""
+    torch = _torch()
+    key = (str(dev), world, cap, torch.cuda.current_stream(dev).cuda_stream)
+    bufs = _SHARD_BUFS.get(key)
+    if bufs is None:
+        i64 = torch.int64
+        bufs = (torch.empty(8, dtype=i64, device=dev),
+                torch.empty(world * 8, dtype=i64, device=dev),
+                torch.empty(SAMPLE_TARGET, dtype=i64, device=dev),
+                torch.empty(32, dtype=i64, device=dev),
+                torch.empty(1 + 2 * cap, dtype=i64, device=dev),
+                torch.empty(world * (1 + 2 * cap), dtype=i64, device=dev))
+        _SHARD_BUFS[key] = bufs
+    return bufs
+
+
 def _sort_sharded_streamed(x_local, comm, ops, tel, mult: int) -> bool:
     """The stream-ordered path: four local phases (cafs_shard_*) around four
     stream-ordered collectives, the decisions taken on device, one host sync.
@@ -454,13 +503,7 @@ def _sort_sharded_streamed(x_local, comm, ops, tel, mult: int) -> bool:
     dev = x_local.device
     world, rank = comm.world, comm.rank
     cap = SHARD_PAIR_CAP
-    i64 = torch.int64
-    hdr = torch.empty(8, dtype=i64, device=dev)
-    hdr_all = torch.empty(world * 8, dtype=i64, device=dev)
-    samples = torch.empty(SAMPLE_TARGET, dtype=i64, device=dev)
-    tiny = torch.empty(32, dtype=i64, device=dev)
-    send = torch.empty(1 + 2 * cap, dtype=i64, device=dev)
-    recv = torch.empty(world * (1 + 2 * cap), dtype=i64, device=dev)
+    hdr, hdr_all, samples, tiny, send, recv = _shard_buffers(dev, world, cap)
     ops.shard_begin(x_local, hdr)
     comm.all_gather_into(hdr_all, hdr)
     ops.shard_sample(x_local, hdr_all, world, rank, samples)
