@@ -366,11 +366,15 @@ constexpr int kBigSLog2 = 14;
 constexpr u32 kBigS = 1u << kBigSLog2;
 constexpr int kBigQcap = 64;
 constexpr size_t kBigSmem = (size_t)kBigS * 12 + (size_t)32 * kBigQcap * 8;
+constexpr int kBigThreads = kHcThreads;  // 32 warps: the shape is latency-bound per warp
+                                         // (512 threads with 8 loads each: 1.4x slower)
 constexpr int kBigUnroll = 4;  // 16-byte loads in flight per thread
+constexpr int kBigBatchVecs = 1;  // vectors whose first probes are issued together (2 or 4:
+                                  // register spills at the 64-register cap, 5-30 % slower)
 constexpr u64 kBigMinRows = 1ull << 22;  // below: the 8192-slot queued shape
 
 template <int KK>
-__global__ void __launch_bounds__(kHcThreads, 1) hash_count_big_kernel(HcArgs a) {
+__global__ void __launch_bounds__(kBigThreads, 1) hash_count_big_kernel(HcArgs a) {
   pdl_begin();
   if (!gate_open(a.ctl, a.gate)) return;
   using K = typename KeyT<KK>::T;
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_big_kernel(HcArgs a)
   __shared__ u64 red_empty[32], red_glob[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u64 flip = a.flip, mult = a.mult;
-  for (u32 i = tid; i < kBigS; i += kHcThreads) { skeys[i] = kEmpty; scnt[i] = 0; }
+  for (u32 i = tid; i < kBigS; i += kBigThreads) { skeys[i] = kEmpty; scnt[i] = 0; }
   if (tid == 0) sclaims = 0;
   __syncthreads();
 
@@ -422,29 +426,58 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_big_kernel(HcArgs a)
     if (skeys[h] == v) { atomicAdd(&scnt[h], 1u); return true; }
     return false;
   };
-  for (u64 r0 = v0; r0 < v1; r0 += (u64)kBigUnroll * kHcThreads) {  // CTA-uniform rounds
+  for (u64 r0 = v0; r0 < v1; r0 += (u64)kBigUnroll * kBigThreads) {  // CTA-uniform rounds
     ulonglong2 w[kBigUnroll];
     bool ok[kBigUnroll];
 #pragma unroll
     for (int q = 0; q < kBigUnroll; ++q) {
-      const u64 i = r0 + (u64)q * kHcThreads + tid;
+      const u64 i = r0 + (u64)q * kBigThreads + tid;
       ok[q] = i < v1;
       w[q] = ok[q] ? ld_stream_v2(xv + i) : make_ulonglong2(0, 0);
     }
+    // branch-free first probes, BATCH keys at a time: hashes, then the shared
+    // loads, then predicated increments; the miss queue (a ballot per key)
+    // only when some lane of the warp missed (the per-key branchy form: +2 %)
+    constexpr int BV = kBigBatchVecs;          // vectors per batch
+    constexpr int BATCH = BV * KPV;            // keys per batch
 #pragma unroll
-    for (int q = 0; q < kBigUnroll; ++q) {
-      u64 v[KPV];
-      if constexpr (KPV == 2) {
-        v[0] = key_map<KK>((K)w[q].x, flip);
-        v[1] = key_map<KK>((K)w[q].y, flip);
-      } else {
-        v[0] = key_map<KK>((K)w[q].x, flip);
-        v[1] = key_map<KK>((K)(w[q].x >> 32), flip);
-        v[2] = key_map<KK>((K)w[q].y, flip);
-        v[3] = key_map<KK>((K)(w[q].y >> 32), flip);
+    for (int q0 = 0; q0 < kBigUnroll; q0 += BV) {
+      u64 v[BATCH];
+      bool act[BATCH];
+#pragma unroll
+      for (int b = 0; b < BV; ++b) {
+        const ulonglong2 ww = w[q0 + b];
+        if constexpr (KPV == 2) {
+          v[b * 2] = key_map<KK>((K)ww.x, flip);
+          v[b * 2 + 1] = key_map<KK>((K)ww.y, flip);
+        } else {
+          v[b * 4] = key_map<KK>((K)ww.x, flip);
+          v[b * 4 + 1] = key_map<KK>((K)(ww.x >> 32), flip);
+          v[b * 4 + 2] = key_map<KK>((K)ww.y, flip);
+          v[b * 4 + 3] = key_map<KK>((K)(ww.y >> 32), flip);
+        }
+#pragma unroll
+        for (int k = 0; k < KPV; ++k) act[b * KPV + k] = ok[q0 + b];
       }
+      u32 h[BATCH];
+      u64 sk[BATCH];
 #pragma unroll
-      for (int k = 0; k < KPV; ++k) enqueue(ok[q] && !fast(v[k]), v[k]);
+      for (int j = 0; j < BATCH; ++j) h[j] = mhash(v[j], mult, 64 - kBigSLog2);
+#pragma unroll
+      for (int j = 0; j < BATCH; ++j) sk[j] = skeys[h[j]];
+      u32 mm = 0;
+#pragma unroll
+      for (int j = 0; j < BATCH; ++j) {
+        const bool sentinel = v[j] == kEmpty;  // counted aside (never a table key)
+        const bool hit = act[j] && !sentinel && sk[j] == v[j];
+        if (hit) atomicAdd(&scnt[h[j]], 1u);
+        empty_cnt += (act[j] && sentinel) ? 1u : 0u;
+        mm |= (act[j] && !sentinel && !hit) ? (1u << j) : 0u;
+      }
+      if (__any_sync(0xffffffffu, mm != 0)) {
+#pragma unroll
+        for (int j = 0; j < BATCH; ++j) enqueue((mm >> j) & 1u, v[j]);
+      }
     }
   }
   __syncwarp();
@@ -464,12 +497,12 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_big_kernel(HcArgs a)
   __syncthreads();
   // ---- flush the CTA's shared cells into the global table ----
 #pragma unroll 1
-  for (u32 h0 = tid; h0 < kBigS; h0 += 2 * kHcThreads) {
+  for (u32 h0 = tid; h0 < kBigS; h0 += 2 * kBigThreads) {
     u64 key[2], inc[2];
     bool okf[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      const u32 h = h0 + r * kHcThreads;
+      const u32 h = h0 + r * kBigThreads;
       inc[r] = scnt[h];
       key[r] = skeys[h];
       okf[r] = inc[r] != 0;
@@ -486,7 +519,7 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_big_kernel(HcArgs a)
   __syncthreads();
   if (tid == 0) {
     u64 e = 0, gg = 0;
-    for (int w2 = 0; w2 < kHcThreads / 32; ++w2) { e += red_empty[w2]; gg += red_glob[w2]; }
+    for (int w2 = 0; w2 < kBigThreads / 32; ++w2) { e += red_empty[w2]; gg += red_glob[w2]; }
     if (e) atomicAdd(&a.ctl->empty_key_count, e);
     if (gg) atomicAdd(&a.ctl->g_updates, gg);
   }
@@ -506,9 +539,9 @@ static cudaError_t launch_hc_big(const HcArgs& a, u64 n, int num_sms, cudaStream
     attr_dev = dev;
   }
   const u64 kpv = KK ? 4 : 2;
-  const u64 rounds = (n / kpv + (u64)kBigUnroll * kHcThreads - 1) / ((u64)kBigUnroll * kHcThreads);
+  const u64 rounds = (n / kpv + (u64)kBigUnroll * kBigThreads - 1) / ((u64)kBigUnroll * kBigThreads);
   const int grid = (int)(rounds < (u64)num_sms ? (rounds ? rounds : 1) : (u64)num_sms);
-  return launch_pdl(kPdlCount, hash_count_big_kernel<KK>, grid, kHcThreads, kBigSmem, st, a);
+  return launch_pdl(kPdlCount, hash_count_big_kernel<KK>, grid, kBigThreads, kBigSmem, st, a);
   return cudaGetLastError();
 }
 
