@@ -68,6 +68,9 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        t0 = time.time()  # nvidia-smi can take a second to print its first row
+        while not self.rows and time.time() - t0 < 5.0:
+            time.sleep(0.05)
 
     def _read(self):
         for line in self.proc.stdout:
