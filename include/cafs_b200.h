@@ -241,6 +241,29 @@ int cafs_shard_finish_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_sign
                           const uint64_t* d_tiny_sum, const uint64_t* d_recv, int world,
                           uint64_t cap, cafs_telemetry_t* tel, int* h_status, void* stream);
 
+/* ---- native multi-GPU sort (the library's own NCCL communicator) ----
+ * The stream-ordered sharded sort above with the collectives inside the
+ * library: cafs_sort_i64_sharded enqueues header -> ncclAllGather -> samples
+ * -> ncclAllReduce -> estimate + local count -> ncclAllGather of the pair
+ * tables (the tiny counters ride in the same rows) -> merge -> slice emit,
+ * captured as one CUDA graph per (column, rows, flags) and replayed, and
+ * synchronises once.  Same results and *h_status as cafs_shard_finish_i64
+ * (1: the caller continues on the host-driven path; the column is untouched).
+ * Replaces the per-phase torch.distributed orchestration of sharded.py for
+ * NCCL process groups; the reference has no multi-GPU sort.
+ * Communicator setup: rank 0 calls cafs_nccl_unique_id, the caller
+ * broadcasts the bytes, every rank calls cafs_comm_create (collective). */
+#define CAFS_NCCL_ID_BYTES 128
+#define CAFS_SHARD_PAIR_CAP 8192 /* pairs per rank in the exchange (as sharded.py) */
+typedef struct cafs_comm_t cafs_comm_t;
+int cafs_nccl_unique_id(unsigned char* out /* CAFS_NCCL_ID_BYTES */);
+int cafs_comm_create(int device, const unsigned char* id, int world, int rank,
+                     cafs_comm_t** out);
+int cafs_comm_destroy(cafs_comm_t* comm);
+int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint64_t n,
+                          int is_signed, uint64_t hash_mult, cafs_telemetry_t* tel, int* h_status,
+                          void* stream);
+
 /* After finish returned status 1 on the main route: this shard's (key, count)
  * pairs from the count phase, for the host-driven merge; *h_npairs = ~0 when
  * they were lost to a table overflow (the guard). */

@@ -79,6 +79,11 @@ SIGNATURES = {
     "cafs_ctx_kernel_count": (_U64, [_P]),
     "cafs_shard_begin_i64": (_I, [_P, _P, _U64, _I, _P, _P]),
     "cafs_shard_local_pairs_i64": (_I, [_P, _P, _P, _U64, ctypes.POINTER(_U64), _P]),
+    "cafs_nccl_unique_id": (_I, [ctypes.c_char_p]),
+    "cafs_comm_create": (_I, [_I, ctypes.c_char_p, _I, _I, ctypes.POINTER(_P)]),
+    "cafs_comm_destroy": (_I, [_P]),
+    "cafs_sort_i64_sharded": (_I, [_P, _P, _P, _U64, _I, _U64, ctypes.POINTER(Telemetry),
+                                   ctypes.POINTER(_I), _P]),
     "cafs_shard_sample_i64": (_I, [_P, _P, _U64, _I, _P, _I, _I, _P, _P]),
     "cafs_shard_count_i64": (_I, [_P, _P, _U64, _I, _U64, _P, _I, _P, _P, _P, _U64, _P]),
     "cafs_shard_finish_i64": (_I, [_P, _P, _U64, _I, _P, _P, _I, _U64, ctypes.POINTER(Telemetry),

@@ -24,6 +24,24 @@ LIB = os.path.join(PKG, "libcafs_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir() -> str:
+    """The NCCL that torch ships (nvidia-nccl wheel): headers and libnccl.so.2."""
+    try:
+        import nvidia.nccl
+        d = list(nvidia.nccl.__path__)[0]
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    except ImportError:
+        pass
+    return ""
+
+
+NCCL = _nccl_dir()
+NCCL_INC = ["-I", os.path.join(NCCL, "include")] if NCCL else []
+NCCL_LINK = (["-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker",
+              "-rpath=" + os.path.join(NCCL, "lib")] if NCCL else ["-lnccl"])
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
 
@@ -37,7 +55,7 @@ def _compile(src: str, force: bool) -> str:
     newest = max(os.path.getmtime(p) for p in [src] + _deps())
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest:
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *NCCL_INC, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -53,7 +71,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, force), srcs))
     newest = max(os.path.getmtime(o) for o in objs)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", *NCCL_LINK]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

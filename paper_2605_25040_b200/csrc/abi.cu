@@ -16,6 +16,7 @@
 // kernels exist) and one at the end of the call (telemetry, guard).  Every
 // stage in between is stream-ordered and gated on the device control block.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdlib>
@@ -809,6 +810,83 @@ u64 host_fmix64(u64 z) {
   return z ^ (z >> 31);
 }
 
+// ---- the sharded pipeline's device phases (shard.cu), shared by the
+// cafs_shard_* calls (collectives by the caller) and cafs_sort_i64_sharded
+// (collectives here, over the library's own NCCL communicator) ----
+
+// estimate on the gathered samples -> route; tiny count or local hash count ->
+// sorted local pairs -> this rank's send row [np, keys[cap], counts[cap]]
+int shard_count_enqueue(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, u64 mult,
+                        const u64* hdr_all, int world, const u64* samples, u64* tiny, u64* send,
+                        u64 cap, cudaStream_t st) {
+  DevCtl* c = ctx->d_ctl;
+  launch_estimate_sharded(samples, hdr_all, world, c, st);
+  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny);
+  launch_shard_tiny_pack(c, tiny, st);
+  cudaError_t e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
+                                    ctx->num_sms, st, 0, kGateMainDense, ctx->dense);
+  if (e == cudaSuccess)
+    e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
+                          ctx->num_sms, st, 1, kGateMainHash, ctx->dense);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
+  launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
+                 kGateMain);
+  launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs, n, st,
+                     kGateMainDense);
+  e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st,
+                              kGateMain);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+  launch_shard_pack_pairs(c, ctx->pk_b, ctx->pc_b, send, cap, st);
+  ctx->launches += 10;
+  CKL();
+  return CAFS_OK;
+}
+
+// tiny totals or the merge of every rank's row -> sorted global pairs -> this
+// rank's slice emit (every kernel gated on the device decision)
+int shard_finish_enqueue(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, const u64* tiny_sum,
+                         const u64* recv, int world, u64 cap, u64 row, cudaStream_t st) {
+  DevCtl* c = ctx->d_ctl;
+  launch_shard_tiny_finish(c, tiny_sum, ctx->pk_b, ctx->pc_b, ctx->poffs, st);
+  launch_shard_merge(c, recv, world, cap, row, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->num_sms, st);
+  launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
+                 kGateMain);
+  cudaError_t e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, kExpectCtlN, ctx->pk_b,
+                                          ctx->pc_b, ctx->poffs, st, kGateMain);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+  launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, 0, 0, true);
+  ctx->launches += 6;
+  CKL();
+  return CAFS_OK;
+}
+
+// after the control block reached the host mirror: the status every rank agrees
+// on (same gathered data) and the telemetry
+int shard_result(cafs_ctx_t* ctx, cafs_telemetry_t* tel, int* h_status, cudaStream_t st) {
+  const DevCtl& h = *ctx->h_ctl;
+  const int eff = h.eff_route;
+  int status = 1;  // 1: the caller runs the host-driven sharded path
+  if (eff == CAFS_ALREADY_SORTED) status = 0;
+  else if ((eff == CAFS_TINY_COUNT || eff == CAFS_MAIN) && h.pairs_ready && !h.overflow) status = 0;
+  if (eff == CAFS_MAIN && h.overflow) {  // a local overflow left this rank's table dirty
+    CK(cudaMemsetAsync(ctx->gkeys, 0xFF, kGlobalSlots * 8, st));
+    CK(cudaMemsetAsync(ctx->gcnt, 0, kGlobalSlots * 8, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  *h_status = status;
+  if (tel) {
+    memset(tel, 0, sizeof(*tel));
+    tel->n = h.n_global;
+    fill_decision(h, eff, eff != CAFS_ALREADY_SORTED && h.n_global >= CAFS_SMALL_N_CUTOFF,
+                  &tel->decision);
+    tel->counted_total = status == 0 && eff != CAFS_ALREADY_SORTED ? h.n_global : 0;
+    tel->pairs = h.npairs;
+    for (int i = 0; i < 3; ++i) tel->stage_ms[i] = -1.f;
+    for (int i = 0; i < 4; ++i) tel->kernel_ms[i] = -1.f;
+  }
+  return CAFS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1406,31 +1484,10 @@ int cafs_shard_count_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   if (!d_hdr_all || !d_samples || !d_tiny || !d_send || world < 1 || (hash_mult & 1) == 0)
     return fail(ctx, CAFS_EINVAL, "bad shard arguments");
   DeviceGuard g(ctx->device);
-  cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_main(ctx));
-  DevCtl* c = ctx->d_ctl;
-  const u64* x = (const u64*)d_x;
-  const u64 flip = is_signed ? kSign : 0;
-  launch_estimate_sharded((const u64*)d_samples, (const u64*)d_hdr_all, world, c, st);
-  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny);
-  launch_shard_tiny_pack(c, (u64*)d_tiny, st);
-  cudaError_t e = launch_hash_count(x, n, flip, hash_mult, c, ctx->gkeys, ctx->gcnt, ctx->glist,
-                                    1, ctx->num_sms, st, 0, kGateMainDense, ctx->dense);
-  if (e == cudaSuccess)
-    e = launch_hash_count(x, n, flip, hash_mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                          ctx->num_sms, st, 1, kGateMainHash, ctx->dense);
-  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
-  launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
-                 kGateMain);
-  launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs, n, st,
-                     kGateMainDense);
-  e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st,
-                              kGateMain);
-  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
-  launch_shard_pack_pairs(c, ctx->pk_b, ctx->pc_b, (u64*)d_send, cap, st);
-  ctx->launches += 10;
-  CKL();
-  return CAFS_OK;
+  return shard_count_enqueue(ctx, (const u64*)d_x, n, is_signed ? kSign : 0, hash_mult,
+                             (const u64*)d_hdr_all, world, (const u64*)d_samples, (u64*)d_tiny,
+                             (u64*)d_send, cap, (cudaStream_t)stream);
 }
 
 int cafs_shard_finish_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_signed,
@@ -1442,42 +1499,10 @@ int cafs_shard_finish_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_sign
   DeviceGuard g(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_main(ctx));
-  DevCtl* c = ctx->d_ctl;
-  const u64 flip = is_signed ? kSign : 0;
-  launch_shard_tiny_finish(c, (const u64*)d_tiny_sum, ctx->pk_b, ctx->pc_b, ctx->poffs, st);
-  launch_shard_merge(c, (const u64*)d_recv, world, cap, ctx->gkeys, ctx->gcnt, ctx->glist,
-                     ctx->num_sms, st);
-  launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
-                 kGateMain);
-  cudaError_t e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, kExpectCtlN, ctx->pk_b,
-                                          ctx->pc_b, ctx->poffs, st, kGateMain);
-  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
-  launch_emit(ctx->pk_b, ctx->poffs, 0, c, d_x, 0, n, flip, ctx->num_sms, st, 0, 0, true);
-  ctx->launches += 6;
-  CKL();
+  TRY(shard_finish_enqueue(ctx, (u64*)d_x, n, is_signed ? kSign : 0, (const u64*)d_tiny_sum,
+                           (const u64*)d_recv, world, cap, 1 + 2 * cap, st));
   TRY(sync_ctl(ctx, st));
-  const DevCtl& h = *ctx->h_ctl;
-  const int eff = h.eff_route;
-  int status = 1;  // 1: the caller runs the host-driven sharded path
-  if (eff == CAFS_ALREADY_SORTED) status = 0;
-  else if ((eff == CAFS_TINY_COUNT || eff == CAFS_MAIN) && h.pairs_ready && !h.overflow) status = 0;
-  if (eff == CAFS_MAIN && h.overflow) {  // a local overflow left this rank's table dirty
-    CK(cudaMemsetAsync(ctx->gkeys, 0xFF, kGlobalSlots * 8, st));
-    CK(cudaMemsetAsync(ctx->gcnt, 0, kGlobalSlots * 8, st));
-    CK(cudaStreamSynchronize(st));
-  }
-  *h_status = status;
-  if (tel) {
-    memset(tel, 0, sizeof(*tel));
-    tel->n = h.n_global;
-    fill_decision(h, eff, eff != CAFS_ALREADY_SORTED && h.n_global >= CAFS_SMALL_N_CUTOFF,
-                  &tel->decision);
-    tel->counted_total = status == 0 && eff != CAFS_ALREADY_SORTED ? h.n_global : 0;
-    tel->pairs = h.npairs;
-    for (int i = 0; i < 3; ++i) tel->stage_ms[i] = -1.f;
-    for (int i = 0; i < 4; ++i) tel->kernel_ms[i] = -1.f;
-  }
-  return CAFS_OK;
+  return shard_result(ctx, tel, h_status, st);
 }
 
 int cafs_gen_mix(uint64_t* d_out, uint64_t count, uint64_t seed, uint64_t skip, void* stream) {
@@ -1499,6 +1524,167 @@ int cafs_gen_draw(int64_t* d_out, uint64_t n, uint64_t start, uint64_t seed,
     launch_gen_draw((u64*)d_out, n, start, seed, (const u64*)d_palette, k, d_cdf, sms,
                     (cudaStream_t)stream);
   return cudaGetLastError() == cudaSuccess ? CAFS_OK : CAFS_ECUDA;
+}
+
+
+// ---- native multi-GPU sort: the library's own NCCL communicator ----
+// One call enqueues the whole stream-ordered sharded pipeline (shard.cu
+// phases + three NCCL collectives over NVLink/NVSwitch), captured once per
+// (column, rows, flags) as a CUDA graph with the collectives inside, then
+// replayed: one graph launch and one host synchronisation per call.
+
+struct cafs_comm_t {
+  ncclComm_t nc = nullptr;
+  int world = 0, rank = 0, device = 0;
+  u64 cap = 0, row = 0;  // pairs per rank in the exchange; words per gathered row
+  u64 *hdr = nullptr, *hdr_all = nullptr, *samples = nullptr, *send = nullptr, *recv = nullptr,
+      *tiny_sum = nullptr;
+  struct Graph {
+    u64 x = 0, n = 0, flip = 0, mult = 0;
+    int seen = 0;
+    uint64_t launches = 0, stamp = 0;
+    cudaGraphExec_t exec = nullptr;
+  } graphs[8];
+  uint64_t clock = 0;
+};
+
+int cafs_nccl_unique_id(unsigned char* out) {
+  if (!out) return CAFS_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return CAFS_ECUDA;
+  static_assert(sizeof(id) == CAFS_NCCL_ID_BYTES, "ncclUniqueId size");
+  memcpy(out, &id, sizeof(id));
+  return CAFS_OK;
+}
+
+int cafs_comm_destroy(cafs_comm_t* comm) {
+  if (!comm) return CAFS_OK;
+  cudaSetDevice(comm->device);
+  for (auto& g : comm->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (comm->nc) ncclCommDestroy(comm->nc);
+  for (u64* p : {comm->hdr, comm->hdr_all, comm->samples, comm->send, comm->recv, comm->tiny_sum})
+    if (p) cudaFree(p);
+  delete comm;
+  return CAFS_OK;
+}
+
+int cafs_comm_create(int device, const unsigned char* id, int world, int rank,
+                     cafs_comm_t** out) {
+  if (!id || !out || world < 1 || rank < 0 || rank >= world) return CAFS_EINVAL;
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return CAFS_ECUDA;
+  cafs_comm_t* c = new (std::nothrow) cafs_comm_t();
+  if (!c) return CAFS_ENOMEM;
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  c->cap = CAFS_SHARD_PAIR_CAP;
+  c->row = 1 + 2 * c->cap + CAFS_SHARD_TINY_WORDS;
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  if (ncclCommInitRank(&c->nc, world, uid, rank) != ncclSuccess) {
+    c->nc = nullptr;
+    cafs_comm_destroy(c);
+    return CAFS_ECUDA;
+  }
+  if (cudaMalloc(&c->hdr, kShardHdrWords * 8) != cudaSuccess ||
+      cudaMalloc(&c->hdr_all, (size_t)world * kShardHdrWords * 8) != cudaSuccess ||
+      cudaMalloc(&c->samples, kSampleTarget * 8) != cudaSuccess ||
+      cudaMalloc(&c->send, c->row * 8) != cudaSuccess ||
+      cudaMalloc(&c->recv, (size_t)world * c->row * 8) != cudaSuccess ||
+      cudaMalloc(&c->tiny_sum, CAFS_SHARD_TINY_WORDS * 8) != cudaSuccess) {
+    cafs_comm_destroy(c);
+    return CAFS_ENOMEM;
+  }
+  *out = c;
+  return CAFS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int sharded_enqueue(cafs_ctx_t* ctx, cafs_comm_t* cm, u64* x, u64 n, u64 flip, u64 mult,
+                    cudaStream_t st) {
+  const u64 cap = cm->cap, row = cm->row, tiny_off = 1 + 2 * cap;
+  launch_shard_header(x, n, flip, cm->hdr, ctx->num_sms, st);
+  if (ncclAllGather(cm->hdr, cm->hdr_all, kShardHdrWords, ncclUint64, cm->nc, st) != ncclSuccess)
+    return fail(ctx, CAFS_ECUDA, "ncclAllGather (headers)");
+  launch_shard_samples(x, n, flip, cm->hdr_all, cm->world, cm->rank, cm->samples, ctx->d_ctl, st);
+  if (ncclAllReduce(cm->samples, cm->samples, kSampleTarget, ncclUint64, ncclSum, cm->nc, st) !=
+      ncclSuccess)
+    return fail(ctx, CAFS_ECUDA, "ncclAllReduce (samples)");
+  TRY(shard_count_enqueue(ctx, x, n, flip, mult, cm->hdr_all, cm->world, cm->samples,
+                          cm->send + tiny_off, cm->send, cap, st));
+  if (ncclAllGather(cm->send, cm->recv, row, ncclUint64, cm->nc, st) != ncclSuccess)
+    return fail(ctx, CAFS_ECUDA, "ncclAllGather (pair tables)");
+  launch_shard_tiny_gather(cm->recv, cm->world, row, tiny_off, cm->tiny_sum, st);
+  TRY(shard_finish_enqueue(ctx, x, n, flip, cm->tiny_sum, cm->recv, cm->world, cap, row, st));
+  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->d_ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
+  ctx->launches += 4;  // header (2), samples, tiny gather
+  CKL();
+  return CAFS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint64_t n,
+                          int is_signed, uint64_t hash_mult, cafs_telemetry_t* tel, int* h_status,
+                          void* stream) {
+  TRY(check_common(ctx, d_x, n));
+  if (!comm || !h_status || (hash_mult & 1) == 0) return fail(ctx, CAFS_EINVAL, "bad arguments");
+  if (comm->device != ctx->device) return fail(ctx, CAFS_EINVAL, "comm and context devices differ");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(ensure_main(ctx));
+  const u64 flip = is_signed ? kSign : 0;
+  u64* x = (u64*)d_x;
+  static int use_graphs = -1;
+  if (use_graphs < 0) {
+    const char* e = getenv("CAFS_GRAPHS");
+    use_graphs = e ? atoi(e) != 0 : 1;
+  }
+  cafs_comm_t::Graph* hit = nullptr;
+  cafs_comm_t::Graph* lru = &comm->graphs[0];
+  for (auto& gr : comm->graphs) {
+    if (gr.seen && gr.x == (u64)x && gr.n == n && gr.flip == flip && gr.mult == hash_mult) {
+      hit = &gr;
+      break;
+    }
+    if (gr.stamp < lru->stamp) lru = &gr;
+  }
+  if (!use_graphs || !ctx->cap_stream) {
+    TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st));
+  } else if (hit && hit->exec) {  // replay
+    CK(cudaGraphLaunch(hit->exec, st));
+    ctx->launches += hit->launches;
+    hit->stamp = ++comm->clock;
+  } else if (!hit) {  // first sighting: direct, capture next time
+    if (lru->exec) cudaGraphExecDestroy(lru->exec);
+    *lru = cafs_comm_t::Graph();
+    lru->x = (u64)x; lru->n = n; lru->flip = flip; lru->mult = hash_mult;
+    lru->seen = 1; lru->stamp = ++comm->clock;
+    TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st));
+  } else {  // second sighting: capture on the context's stream, launch on the caller's
+    const uint64_t l0 = ctx->launches;
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = sharded_enqueue(ctx, comm, x, n, flip, hash_mult, ctx->cap_stream);
+    cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &graph);
+    if (rc != CAFS_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
+    if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "graph capture (sharded)", e);
+    e = cudaGraphInstantiate(&hit->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) { hit->exec = nullptr; return fail(ctx, CAFS_ECUDA, "graph instantiate", e); }
+    hit->launches = ctx->launches - l0;
+    hit->stamp = ++comm->clock;
+    CK(cudaGraphLaunch(hit->exec, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return shard_result(ctx, tel, h_status, st);
 }
 
 }  // extern "C"

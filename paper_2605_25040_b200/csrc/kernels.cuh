@@ -26,8 +26,10 @@ void launch_shard_pack_pairs(DevCtl* ctl, const u64* keys, const u64* cnts, u64*
                              u64 cap, cudaStream_t st);
 void launch_shard_tiny_finish(DevCtl* ctl, const u64* tiny_sum, u64* pkeys, u64* pcnt, u64* poffs,
                               cudaStream_t st);
-void launch_shard_merge(DevCtl* ctl, const u64* recv, int world, u64 cap, u64* gkeys, u64* gcnt,
-                        u32* glist, int num_sms, cudaStream_t st);
+void launch_shard_merge(DevCtl* ctl, const u64* recv, int world, u64 cap, u64 row, u64* gkeys,
+                        u64* gcnt, u32* glist, int num_sms, cudaStream_t st);
+void launch_shard_tiny_gather(const u64* recv, int world, u64 row, u64 tiny_off, u64* tiny_sum,
+                              cudaStream_t st);
 // tiny.cu
 // with pkeys != null the count's last CTA also writes the tiny route's pairs
 // and offsets (or flags the miss): the finalize of sorter.py:367-385

@@ -131,13 +131,13 @@ __global__ void shard_tiny_finish_kernel(DevCtl* ctl, const u64* tiny_sum, u64* 
 // its table (np = ~0) or a local overflow skips the merge on this rank (the
 // caller then takes the host-driven path on all ranks: every rank sees the same
 // gathered np values).
-__global__ void shard_merge_reset_kernel(DevCtl* ctl, const u64* recv, int world, u64 cap) {
+__global__ void shard_merge_reset_kernel(DevCtl* ctl, const u64* recv, int world, u64 row) {
   if (!gate_open(ctl, kGateMain)) return;
   __shared__ int bad;
   if (threadIdx.x == 0) bad = ctl->overflow;
   __syncthreads();
   for (int r = threadIdx.x; r < world; r += blockDim.x)
-    if (recv[(u64)r * (1 + 2 * cap)] == ~0ull) bad = 1;
+    if (recv[(u64)r * row] == ~0ull) bad = 1;
   for (u32 t = threadIdx.x; t < kListStripes; t += blockDim.x) ctl->g_fill[t] = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -152,10 +152,9 @@ __global__ void shard_merge_reset_kernel(DevCtl* ctl, const u64* recv, int world
 }
 
 __global__ void shard_merge_insert_kernel(DevCtl* ctl, const u64* recv, int world, u64 cap,
-                                          u64* gkeys, u64* gcnt, u32* glist) {
+                                          u64 row, u64* gkeys, u64* gcnt, u32* glist) {
   if (!gate_open(ctl, kGateMain) || ctl->overflow) return;
   const u64 stride = (u64)gridDim.x * blockDim.x;
-  const u64 row = 1 + 2 * cap;
   for (int r = 0; r < world; ++r) {
     const u64* t = recv + (u64)r * row;
     const u64 np = t[0];
@@ -191,11 +190,28 @@ void launch_shard_tiny_finish(DevCtl* ctl, const u64* tiny_sum, u64* pkeys, u64*
   shard_tiny_finish_kernel<<<1, 32, 0, st>>>(ctl, tiny_sum, pkeys, pcnt, poffs);
 }
 
-void launch_shard_merge(DevCtl* ctl, const u64* recv, int world, u64 cap, u64* gkeys, u64* gcnt,
-                        u32* glist, int num_sms, cudaStream_t st) {
-  shard_merge_reset_kernel<<<1, 256, 0, st>>>(ctl, recv, world, cap);
-  shard_merge_insert_kernel<<<num_sms * 2, 256, 0, st>>>(ctl, recv, world, cap, gkeys, gcnt,
+void launch_shard_merge(DevCtl* ctl, const u64* recv, int world, u64 cap, u64 row, u64* gkeys,
+                        u64* gcnt, u32* glist, int num_sms, cudaStream_t st) {
+  shard_merge_reset_kernel<<<1, 256, 0, st>>>(ctl, recv, world, row);
+  shard_merge_insert_kernel<<<num_sms * 2, 256, 0, st>>>(ctl, recv, world, cap, row, gkeys, gcnt,
                                                          glist);
+}
+
+// The tiny counters every rank packed at `tiny_off` of its gathered row, summed
+// (the native sharded path carries them in the pair-table all-gather instead
+// of a separate all-reduce).
+__global__ void shard_tiny_gather_kernel(const u64* recv, int world, u64 row, u64 tiny_off,
+                                         u64* tiny_sum) {
+  const int t = threadIdx.x;
+  u64 s = 0;
+  for (int r = 0; r < world; ++r) s += recv[(u64)r * row + tiny_off + t];
+  tiny_sum[t] = s;
+}
+
+void launch_shard_tiny_gather(const u64* recv, int world, u64 row, u64 tiny_off, u64* tiny_sum,
+                              cudaStream_t st) {
+  shard_tiny_gather_kernel<<<1, CAFS_SHARD_TINY_WORDS, 0, st>>>(recv, world, row, tiny_off,
+                                                                tiny_sum);
 }
 
 }  // namespace cafs

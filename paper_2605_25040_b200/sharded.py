@@ -207,6 +207,17 @@ class DeviceOps:
                    self.ctx, "shard_finish")
         return int(status.value), t
 
+    def sort_native(self, x, ncomm: int, mult: int):
+        """The whole stream-ordered sharded sort with the library's own NCCL
+        communicator (cafs_sort_i64_sharded): (status, telemetry)."""
+        t = _lib.Telemetry()
+        status = ctypes.c_int()
+        _lib.check(self.lib.cafs_sort_i64_sharded(self.ctx, ncomm, x.data_ptr(), x.shape[0],
+                                                  int(self.signed), mult, ctypes.byref(t),
+                                                  ctypes.byref(status), self._stream()),
+                   self.ctx, "sort_sharded")
+        return int(status.value), t
+
     def shard_local_pairs(self):
         """This shard's pairs from the streamed count phase; None on overflow."""
         k, c = self._pairs_out(_PAIR_CAP)
@@ -458,7 +469,11 @@ def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTeleme
     try:
         fast = (hasattr(ops, "shard_begin") and x_local.is_cuda and x_local.is_contiguous()
                 and x_local.dtype in (torch.int64, torch.uint64))
-        if fast and _sort_sharded_streamed(x_local, comm, ops, tel, mult):
+        native = (fast and comm.device is not None and hasattr(ops, "sort_native")
+                  and _native_enabled())
+        if native and _sort_sharded_native(x_local, comm, ops, tel, mult):
+            tel.sharded_path = "native"
+        elif not native and fast and _sort_sharded_streamed(x_local, comm, ops, tel, mult):
             tel.sharded_path = "streamed"
         else:
             tel.sharded_path = "host"
@@ -469,6 +484,59 @@ def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTeleme
 
 
 SHARD_PAIR_CAP = 8192  # pairs per rank in the stream-ordered exchange (the pair sort's capacity)
+
+_NATIVE_COMMS: dict = {}
+
+
+def _native_enabled() -> bool:
+    import os
+    return os.environ.get("CAFS_SHARD_NATIVE", "1") != "0"
+
+
+def _native_comm(comm, device: int):
+    """The library's NCCL communicator for this process group (cafs_comm_create),
+    made once: rank 0's unique id is broadcast over the group itself."""
+    torch = _torch()
+    dist = comm.dist
+    key = (id(comm.group if comm.group is not None else dist.group.WORLD), device, comm.world)
+    h = _NATIVE_COMMS.get(key)
+    if h is not None:
+        return h
+    lib = _lib.load()
+    buf = ctypes.create_string_buffer(128)
+    if comm.rank == 0:
+        _lib.check(lib.cafs_nccl_unique_id(buf), None, "nccl_unique_id")
+    idt = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).to(comm.device)
+    src = 0 if comm.group is None else dist.get_global_rank(comm.group, 0)
+    dist.broadcast(idt, src=src, group=comm.group)
+    out = ctypes.c_void_p()
+    _lib.check(lib.cafs_comm_create(device, bytes(idt.cpu().numpy().tobytes()), comm.world,
+                                    comm.rank, ctypes.byref(out)), None, "comm_create")
+    _NATIVE_COMMS[key] = out.value
+    return out.value
+
+
+def _sort_sharded_native(x_local, comm, ops, tel, mult: int) -> bool:
+    """cafs_sort_i64_sharded: every phase and the three NCCL collectives in one
+    graph-replayed enqueue.  False when the column needs the host-driven path
+    (every rank agrees; the column is untouched)."""
+    from .sorter import _decision_from_c
+    ncomm = _native_comm(comm, ops.device)
+    status, t = ops.sort_native(x_local, ncomm, mult)
+    tel.n = int(t.n)
+    tel.decision = _decision_from_c(t.decision, tel.n, "int64" if ops.signed else "uint64")
+    if status != 0:
+        if tel.decision.route is not Route.MAIN:
+            return False
+        sizes = [int(v[0]) for v in comm.all_gather_ints([int(x_local.shape[0])])]
+        tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, 4)
+        _main_exchange(x_local, comm, ops, tel, ops.shard_local_pairs(), sizes, tel.decision)
+        return True
+    tel.counted_total = int(t.counted_total)
+    tel.pairs = int(t.pairs)
+    if tel.decision.route is Route.MAIN:
+        tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, 4)
+    return True
 
 
 _SHARD_BUFS: dict = {}

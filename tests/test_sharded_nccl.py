@@ -1,0 +1,74 @@
+"""The native multi-GPU sort (cafs_sort_i64_sharded: the library's own NCCL
+communicator, collectives inside one graph-replayed enqueue) at one NCCL rank
+on the GPU: bit-exact against np.sort and the oracle's decision on every route,
+across direct, captured and replayed calls; columns the device cannot finish
+continue on the host-driven path (> 8192 pairs: from the already-counted
+pairs, still labelled "native"; fallback routes: "host").  (More ranks need more GPUs than this pool
+gives: the 2-rank tests in test_sharded_gpu.py share one GPU over gloo.)"""
+
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_CHILD = r"""
+import os, sys
+import numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, sys.argv[1])
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=sys.argv[2], RANK="0", WORLD_SIZE="1")
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+import paper_2605_25040_b200 as cafs
+from paper_2605_25040_b200.sharded import cafs_sort_sharded
+from oracle import cafs_oracle as orc
+rng = np.random.default_rng(3)
+cols = {
+    "tiny": (rng.choice(rng.integers(-2**62, 2**62, 6), 400_000), "native"),
+    "codes": (rng.integers(0, 4000, 2_000_000), "native"),
+    "main_hash": (rng.choice(rng.integers(-2**62, 2**62, 3000), 1_000_000), "native"),
+    "many_pairs": (rng.choice(rng.integers(-2**62, 2**62, 50_000), 2_000_000), "native"),
+    "fallback": (rng.integers(-2**62, 2**62, 300_000), "host"),
+    "sorted": (np.arange(-50_000, 50_000, dtype=np.int64), "native"),
+}
+bad = []
+for name, (x, path) in cols.items():
+    x = x.astype(np.int64)
+    want = np.sort(x)
+    route = orc.cafs_sort(x.copy()).route
+    t = torch.empty(x.shape[0], dtype=torch.int64, device="cuda")
+    for rep in range(3):  # direct, captured, replayed
+        t.copy_(torch.from_numpy(x))
+        tel = cafs.SortTelemetry()
+        cafs_sort_sharded(t, telemetry=tel)
+        torch.cuda.synchronize()
+        got_path = tel.sharded_path
+        if (not np.array_equal(t.cpu().numpy(), want) or tel.route.value != route
+                or got_path != path):
+            bad.append((name, rep, tel.route.value, route, got_path, path))
+dist.destroy_process_group()
+print("BAD", bad)
+sys.exit(1 if bad else 0)
+"""
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_native_sharded_sort_one_nccl_rank():
+    r = subprocess.run([sys.executable, "-c", _CHILD, ROOT, str(_port())], cwd=ROOT,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
