@@ -336,6 +336,15 @@ def main():
                 "step_frac": (2 * kb * N / (tot_ms / args.steps / 1e3) / 1e9) / world / peak,
                 "kernels": kernels}
 
+    if roof is None:  # sharded path: no per-kernel events; the whole step per rank
+        step_s = tot_ms / args.steps / 1e3
+        ach = 2 * kb * n_local / step_s / 1e9
+        roof = {"bound": "hbm", "kernel": "whole step per rank (count + emit passes; the sharded "
+                "path records no per-kernel events)", "achieved": ach, "peak": peak,
+                "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                "algorithmic_bytes_per_launch": 2 * kb * n_local, "peak_source": peak_src,
+                "step_frac": ach / peak, "kernels": kernels}
+
     # ---- e2e through the C ABI host entry point (pinned host buffers) ----
     e2e = None
     if world == 1 and args.e2e_steps > 0:
