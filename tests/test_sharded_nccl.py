@@ -40,13 +40,15 @@ cols = {
     "many_pairs": (rng.choice(rng.integers(-2**62, 2**62, 50_000), 2_000_000), "native"),
     "fallback": (rng.integers(-2**62, 2**62, 300_000), "host"),
     "sorted": (np.arange(-50_000, 50_000, dtype=np.int64), "native"),
+    "uint64": (rng.choice(rng.integers(0, 2**63, 500, dtype=np.uint64) * 2, 600_000), "native"),
 }
 bad = []
 for name, (x, path) in cols.items():
-    x = x.astype(np.int64)
+    x = x if x.dtype == np.uint64 else x.astype(np.int64)
     want = np.sort(x)
     route = orc.cafs_sort(x.copy()).route
-    t = torch.empty(x.shape[0], dtype=torch.int64, device="cuda")
+    t = torch.empty(x.shape[0], dtype=torch.uint64 if x.dtype == np.uint64 else torch.int64,
+                    device="cuda")
     for rep in range(3):  # direct, captured, replayed
         t.copy_(torch.from_numpy(x))
         tel = cafs.SortTelemetry()
