@@ -1559,7 +1559,7 @@ int cafs_nccl_unique_id(unsigned char* out) {
 
 int cafs_comm_destroy(cafs_comm_t* comm) {
   if (!comm) return CAFS_OK;
-  cudaSetDevice(comm->device);
+  DeviceGuard g(comm->device);
   for (auto& g : comm->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (comm->nc) ncclCommDestroy(comm->nc);
@@ -1573,7 +1573,7 @@ int cafs_comm_create(int device, const unsigned char* id, int world, int rank,
                      cafs_comm_t** out) {
   if (!id || !out || world < 1 || rank < 0 || rank >= world) return CAFS_EINVAL;
   *out = nullptr;
-  if (cudaSetDevice(device) != cudaSuccess) return CAFS_ECUDA;
+  DeviceGuard g(device);
   cafs_comm_t* c = new (std::nothrow) cafs_comm_t();
   if (!c) return CAFS_ENOMEM;
   c->world = world;
@@ -1593,7 +1593,8 @@ int cafs_comm_create(int device, const unsigned char* id, int world, int rank,
       cudaMalloc(&c->samples, kSampleTarget * 8) != cudaSuccess ||
       cudaMalloc(&c->send, c->row * 8) != cudaSuccess ||
       cudaMalloc(&c->recv, (size_t)world * c->row * 8) != cudaSuccess ||
-      cudaMalloc(&c->tiny_sum, CAFS_SHARD_TINY_WORDS * 8) != cudaSuccess) {
+      cudaMalloc(&c->tiny_sum, CAFS_SHARD_TINY_WORDS * 8) != cudaSuccess ||
+      cudaMemset(c->send, 0, c->row * 8) != cudaSuccess) {  // unused tiny words stay 0
     cafs_comm_destroy(c);
     return CAFS_ENOMEM;
   }

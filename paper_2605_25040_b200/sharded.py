@@ -498,7 +498,8 @@ def _native_comm(comm, device: int):
     made once: rank 0's unique id is broadcast over the group itself."""
     torch = _torch()
     dist = comm.dist
-    key = (id(comm.group if comm.group is not None else dist.group.WORLD), device, comm.world)
+    key = (id(comm.group if comm.group is not None else dist.group.WORLD), device, comm.world,
+           comm.rank)
     h = _NATIVE_COMMS.get(key)
     if h is not None:
         return h
