@@ -22,8 +22,15 @@ __global__ void __launch_bounds__(1024) shard_header_kernel(const u64* __restric
   if (threadIdx.x == 0) inv = 0;
   __syncthreads();
   const u64 P = n < kMonoPrefix ? n : kMonoPrefix;
+  // thread t checks rows [16t, 16t + 16]: 17 loads in flight at once (one
+  // DRAM round trip for the reference's first chunk, not 16)
+  const u64 i0 = (u64)threadIdx.x * 16;
+  u64 a[17];
+#pragma unroll
+  for (int j = 0; j < 17; ++j) a[j] = i0 + j < P ? x[i0 + j] ^ flip : 0;
   int found = 0;
-  for (u64 i = threadIdx.x; i + 1 < P; i += blockDim.x) found |= (x[i + 1] ^ flip) < (x[i] ^ flip);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) found |= (i0 + j + 1 < P) && a[j + 1] < a[j];
   if (found) inv = 1;
   __syncthreads();
   if (threadIdx.x == 0) {
