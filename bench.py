@@ -56,38 +56,48 @@ class ClockSampler:
         self.gpu = gpu
         self.rows = []
         self.proc = None
-        self.thread = None
+        self.path = None
 
     def start(self):
+        # nvidia-smi writes straight to a file: no reader thread in this process,
+        # so the timed host loop never waits on the GIL (a reader thread cost a
+        # 5-10 ms switch-interval stall inside a step)
+        import tempfile
+        fd, self.path = tempfile.mkstemp(prefix="cafs_clocks_", suffix=".csv")
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                stdout=fd, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
-            return
-        self.thread = threading.Thread(target=self._read, daemon=True)
-        self.thread.start()
+            self.proc = None
+        finally:
+            os.close(fd)
         t0 = time.time()  # nvidia-smi can take a second to print its first row
-        while not self.rows and time.time() - t0 < 5.0:
+        while self.proc is not None and os.path.getsize(self.path) == 0 and time.time() - t0 < 5.0:
             time.sleep(0.05)
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                self.rows.append(parts)
+    def _parse(self):
+        try:
+            with open(self.path) as f:
+                for line in f:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) >= 9:
+                        self.rows.append(parts)
+        finally:
+            os.unlink(self.path)
 
     def stop(self) -> dict:
         if self.proc is None:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        if self.thread:
-            self.thread.join(timeout=2)
+        self._parse()
         def num(v):
             try:
                 return float(v)
