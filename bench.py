@@ -20,6 +20,7 @@ The input (8 GiB for cfg4) is far larger than the 126 MB L2.
 from __future__ import annotations
 
 import argparse
+import gc
 import ctypes
 import json
 import os
@@ -274,6 +275,10 @@ def main():
         ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         tels = []
+        # no garbage-collector pause inside a step (a full collection in this
+        # process takes ~10 ms; timeit does the same)
+        gc.collect()
+        gc.disable()
         barrier()
         torch.cuda.synchronize()
         wall0 = time.perf_counter()
@@ -287,6 +292,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         wall = time.perf_counter() - wall0
+        gc.enable()
         return [a.elapsed_time(b) for a, b in zip(ev0, ev1)], tels, wall
 
     # the timed region: plain API calls (no per-call instrumentation)
