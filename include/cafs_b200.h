@@ -3,7 +3,9 @@
  *
  * Plain pointers, sizes and status codes; no torch or CUDA types in the
  * signatures (streams travel as `void*` = cudaStream_t).  Every call is
- * stream-ordered on the given stream and thread-safe across distinct contexts.
+ * stream-ordered on the given stream and thread-safe: calls on distinct contexts run
+ * concurrently; calls sharing a context are serialised (a per-context lock, and a
+ * call on a different stream than the previous one first waits for that stream).
  *
  * Each entry point replaces one interface of the reference package
  * (paths relative to /root/reference/pkg/src/cafs):

@@ -36,6 +36,12 @@ using namespace cafs;
 struct cafs_ctx {
   int device = 0;
   int num_sms = 148;
+  // calls on one context are serialised: a host lock, and a call on a stream
+  // other than the previous call's first waits for that stream (the control
+  // block, tables and scratch are per context)
+  std::recursive_mutex mu;
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
   DevCtl* d_ctl = nullptr;
   DevCtl* h_ctl = nullptr;  // pinned mirror
   // main route: global table + pair buffers
@@ -157,6 +163,22 @@ struct DeviceGuard {
     int cur = -1;
     cudaGetDevice(&cur);
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// One per entry-point call (see cafs_ctx::mu).
+// A stream switch waits (on the host) for the previous stream's work: nothing
+// is recorded on the common same-stream path.
+struct CallGuard {
+  cafs_ctx_t* c;
+  cudaStream_t st;
+  std::unique_lock<std::recursive_mutex> lk;
+  CallGuard(cafs_ctx_t* ctx, void* stream) : c(ctx), st((cudaStream_t)stream), lk(ctx->mu) {
+    if (c->has_last && c->last_stream != st) cudaStreamSynchronize(c->last_stream);
+  }
+  ~CallGuard() {
+    c->last_stream = st;
+    c->has_last = true;
   }
 };
 
@@ -936,6 +958,7 @@ int cafs_ctx_create(int device, cafs_ctx_t** out) {
 void cafs_ctx_destroy(cafs_ctx_t* ctx) {
   if (!ctx) return;
   DeviceGuard g(ctx->device);
+  { std::lock_guard<std::recursive_mutex> lk(ctx->mu); }  // no call in flight on the host
   cudaDeviceSynchronize();
   void* dev[] = {ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
                  ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->dense, ctx->ghist, ctx->gbase,
@@ -968,6 +991,7 @@ static int sort_impl(cafs_ctx_t* ctx, void* d_x, uint64_t n, int is_signed, uint
   TRY(check_common(ctx, d_x, n, kk ? 4 : 8));
   if ((hash_mult & 1) == 0) return fail(ctx, CAFS_EINVAL, "hash multiplier must be odd");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   const uint64_t launches0 = ctx->launches;
   cafs_telemetry_t local;
@@ -1095,6 +1119,7 @@ int cafs_sort_i32_host(cafs_ctx_t* ctx, const int32_t* h_in, int32_t* h_out, uin
   if (n >= (1ull << 32)) return fail(ctx, CAFS_EINVAL, "arrays of 2**32 or more elements");
   if (n > 0 && (!h_in || !h_out)) return fail(ctx, CAFS_EINVAL, "null host pointer");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   if (n > ctx->stage_elems) {  // the stage holds n 8-byte words: room for n 4-byte keys
     if (ctx->stage) CK(cudaFree(ctx->stage));
@@ -1117,6 +1142,7 @@ int cafs_sort_i64_host(cafs_ctx_t* ctx, const int64_t* h_in, int64_t* h_out, uin
   if (n >= (1ull << 32)) return fail(ctx, CAFS_EINVAL, "arrays of 2**32 or more elements");
   if (n > 0 && (!h_in || !h_out)) return fail(ctx, CAFS_EINVAL, "null host pointer");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   if (n > ctx->stage_elems) {
     if (ctx->stage) CK(cudaFree(ctx->stage));
@@ -1138,6 +1164,7 @@ int cafs_dispatch_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_si
   if (!out || n < 2) return fail(ctx, CAFS_EINVAL, "dispatch needs n >= 2");
   if ((hash_mult & 1) == 0) return fail(ctx, CAFS_EINVAL, "hash multiplier must be odd");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   bool mono;
   int route;
   TRY(run_dispatch(ctx, (const u64*)d_x, n, is_signed ? kSign : 0, (cudaStream_t)stream, &mono,
@@ -1151,6 +1178,7 @@ int cafs_estimate_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_si
   TRY(check_common(ctx, d_x, n));
   if (!out || n < 1) return fail(ctx, CAFS_EINVAL, "n must be >= 1");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   launch_estimate((const u64*)d_x, n, is_signed ? kSign : 0, 0, ctx->d_ctl, st);
   ctx->launches++;
@@ -1168,6 +1196,7 @@ int cafs_is_monotone_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   if (!out) return CAFS_EINVAL;
   if (n < 2) { *out = 1; return CAFS_OK; }
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   bool mono;
   int route;
   TRY(run_dispatch(ctx, (const u64*)d_x, n, is_signed ? kSign : 0, (cudaStream_t)stream, &mono,
@@ -1183,6 +1212,7 @@ int cafs_tiny_counts_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
     return fail(ctx, CAFS_EINVAL, "tiny-count takes at most 8 keys");
   if (nk == 0) return CAFS_OK;
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   // distinct keys -> perfect hash into 16 slots
   u64 uk[CAFS_TINY_MAX_KEYS];
@@ -1230,6 +1260,7 @@ int cafs_count_pairs_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   TRY(check_common(ctx, d_x, n));
   if (!h_npairs || (hash_mult & 1) == 0) return fail(ctx, CAFS_EINVAL, "bad arguments");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   *h_npairs = 0;
   if (n == 0) return CAFS_OK;
@@ -1276,6 +1307,7 @@ int cafs_merge_pairs(cafs_ctx_t* ctx, const uint64_t* d_keys_in, const uint64_t*
                      uint64_t* h_npairs, void* stream) {
   if (!ctx || !h_npairs || (m && (!d_keys_in || !d_counts_in))) return CAFS_EINVAL;
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   *h_npairs = 0;
   TRY(ensure_main(ctx));
@@ -1312,6 +1344,7 @@ int cafs_pair_sort(cafs_ctx_t* ctx, uint64_t* d_keys, uint64_t* d_counts, uint64
   if (npairs > kGlobalCap) return fail(ctx, CAFS_EINVAL, "too many pairs");
   if (npairs < 2) return CAFS_OK;
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_main(ctx));
   if (npairs <= kSmallSortMax) {
@@ -1342,6 +1375,7 @@ int cafs_emit_i64(cafs_ctx_t* ctx, const uint64_t* d_keys, const uint64_t* d_cou
   if (out_begin > out_end || out_end > total || npairs > kGlobalCap)
     return fail(ctx, CAFS_EINVAL, "bad output slice");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_main(ctx));
   DevCtl& c = *ctx->h_ctl;
@@ -1365,6 +1399,7 @@ int cafs_fallback_sort_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_sig
                            void* stream) {
   TRY(check_common(ctx, d_x, n));
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   TRY(fallback_sort(ctx, (u64*)d_x, n, is_signed ? kSign : 0, st));
   CK(cudaStreamSynchronize(st));
@@ -1379,6 +1414,7 @@ int cafs_key_span_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_si
   *h_max = 0;
   if (n == 0) return CAFS_OK;
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_radix(ctx, n, false));
   launch_msd_span((const u64*)d_x, n, is_signed ? kSign : 0, ctx->msd, ctx->num_sms, st);
@@ -1403,6 +1439,7 @@ int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_s
   if (n == 0) return CAFS_OK;
   const u64 flip = is_signed ? kSign : 0;
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_radix(ctx, n, false));
   launch_msd_partition((const u64*)d_x, n, flip, ctx->msd, g_min, g_max, (u64*)d_out,
@@ -1429,6 +1466,7 @@ int cafs_shard_local_pairs_i64(cafs_ctx_t* ctx, uint64_t* d_keys, uint64_t* d_co
                                uint64_t cap, uint64_t* h_npairs, void* stream) {
   if (!ctx || !h_npairs) return CAFS_EINVAL;
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_main(ctx));
   TRY(sync_ctl(ctx, st));
@@ -1454,6 +1492,7 @@ int cafs_shard_begin_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   TRY(check_common(ctx, d_x, n));
   if (!d_hdr) return fail(ctx, CAFS_EINVAL, "null header buffer");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   launch_shard_header((const u64*)d_x, n, is_signed ? kSign : 0, (u64*)d_hdr, ctx->num_sms,
                       (cudaStream_t)stream);
   ctx->launches += 2;
@@ -1468,6 +1507,7 @@ int cafs_shard_sample_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int i
   if (!d_hdr_all || !d_samples || world < 1 || rank < 0 || rank >= world)
     return fail(ctx, CAFS_EINVAL, "bad shard arguments");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   TRY(ensure_main(ctx));
   launch_shard_samples((const u64*)d_x, n, is_signed ? kSign : 0, (const u64*)d_hdr_all, world,
                        rank, (u64*)d_samples, ctx->d_ctl, (cudaStream_t)stream);
@@ -1484,6 +1524,7 @@ int cafs_shard_count_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is
   if (!d_hdr_all || !d_samples || !d_tiny || !d_send || world < 1 || (hash_mult & 1) == 0)
     return fail(ctx, CAFS_EINVAL, "bad shard arguments");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   TRY(ensure_main(ctx));
   return shard_count_enqueue(ctx, (const u64*)d_x, n, is_signed ? kSign : 0, hash_mult,
                              (const u64*)d_hdr_all, world, (const u64*)d_samples, (u64*)d_tiny,
@@ -1497,6 +1538,7 @@ int cafs_shard_finish_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_sign
   if (!d_tiny_sum || !d_recv || !h_status || world < 1)
     return fail(ctx, CAFS_EINVAL, "bad shard arguments");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_main(ctx));
   TRY(shard_finish_enqueue(ctx, (u64*)d_x, n, is_signed ? kSign : 0, (const u64*)d_tiny_sum,
@@ -1639,6 +1681,7 @@ int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint
   if (!comm || !h_status || (hash_mult & 1) == 0) return fail(ctx, CAFS_EINVAL, "bad arguments");
   if (comm->device != ctx->device) return fail(ctx, CAFS_EINVAL, "comm and context devices differ");
   DeviceGuard g(ctx->device);
+  CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_main(ctx));
   const u64 flip = is_signed ? kSign : 0;

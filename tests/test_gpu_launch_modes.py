@@ -94,3 +94,39 @@ def test_estimate_interleaved_shapes_against_oracle():
             if oe is not None:
                 assert (e.k_hat, e.u, e.f1, e.f2) == (oe.k_hat, oe.u, oe.f1, oe.f2)
             assert np.array_equal(t.cpu().numpy(), np.sort(x))
+
+
+def test_concurrent_threads_on_two_streams_share_one_context():
+    """Two host threads, each sorting on its own CUDA stream through the one
+    per-device context: the context serialises the calls (host lock plus a
+    wait for the previous stream on a switch), so both threads get exact results."""
+    import threading
+
+    import paper_2605_25040_b200 as cafs
+
+    rng = np.random.default_rng(9)
+    cols = [rng.choice(rng.integers(-2**62, 2**62, k), n).astype(np.int64)
+            for k, n in ((5, 700_000), (3000, 900_000), (60_000, 1_200_000), (4, 500_000))]
+    want = [np.sort(c) for c in cols]
+    errors = []
+
+    def worker(idx):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(6):
+                    c = idx * 2 + rep % 2
+                    t = torch.from_numpy(cols[c]).cuda(non_blocking=False)
+                    cafs.cafs_sort(t)
+                    s.synchronize()
+                    if not np.array_equal(t.cpu().numpy(), want[c]):
+                        errors.append((idx, rep))
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    ths = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errors, errors
