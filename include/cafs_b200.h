@@ -27,6 +27,10 @@
  *   cafs_sort_i32(_host)     sorter.py:335-386   cafs_sort on int32 / uint32 arrays
  *   cafs_key_span_i64,       (no reference counterpart: the distributed
  *   cafs_partition_i64        fallback of SURVEY.md §8(f)2, sharded.py)
+ *   cafs_shard_*_i64,        (no reference counterpart: the reference is single-process,
+ *   cafs_sort_i64_sharded,    PAPER.md:714 names a parallel CAFS as future work) the
+ *   cafs_comm_create          row-sharded multi-GPU sort of SURVEY.md §8(e); the native
+ *                             call runs its collectives on the library's NCCL communicator
  *
  * Keys are 64-bit.  `is_signed` = 1 for int64 (order-mapped by flipping bit 63,
  * sorter.py:84-94, folded into the kernels' loads/stores), 0 for uint64.
