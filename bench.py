@@ -363,7 +363,7 @@ def main():
 
     # ---- e2e through the C ABI host entry point (pinned host buffers) ----
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
+    if not sharded and args.e2e_steps > 0:
         h_in = torch.empty(N, dtype=pristine.dtype, pin_memory=True)
         h_out = torch.empty(N, dtype=pristine.dtype, pin_memory=True)
         h_in.copy_(pristine)
@@ -391,6 +391,38 @@ def main():
                "h2d_bytes_per_step": N * kb, "d2h_bytes_per_step": N * kb,
                "ms_per_step": sum(e_t) / len(e_t),
                "path": f"{host_name} (C ABI), pinned host in/out buffers"}
+        del h_in, h_out
+    elif sharded and args.e2e_steps > 0:
+        # every rank: its pinned host shard -> device -> cafs_sort_sharded -> its
+        # rows of the sorted column back to pinned host memory; max over ranks
+        h_in = torch.empty(n_local, dtype=pristine.dtype, pin_memory=True)
+        h_out = torch.empty(n_local, dtype=pristine.dtype, pin_memory=True)
+        h_in.copy_(pristine)
+        e_t = []
+        for i in range(args.e2e_steps + 1):  # the first call is a warm-up
+            barrier()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            x.copy_(h_in, non_blocking=True)
+            cafs_sort_sharded(x)
+            h_out.copy_(x, non_blocking=True)
+            b.record(stream)
+            b.synchronize()
+            if i:
+                e_t.append(a.elapsed_time(b))
+        ok &= bool((h_out[1:] >= h_out[:-1]).all().item())
+        tot_e = sum(e_t)
+        if dist is not None:
+            t = torch.tensor([tot_e], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot_e = float(t.item())
+        e2e = {"value": N * len(e_t) / (tot_e / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": N * kb, "d2h_bytes_per_step": N * kb,
+               "ms_per_step": tot_e / len(e_t),
+               "path": "cafs_sort_sharded per rank (public API), pinned host shards in/out; "
+                       "max over ranks"}
         del h_in, h_out
 
     cpu = None
