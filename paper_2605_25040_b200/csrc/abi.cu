@@ -113,7 +113,7 @@ bool pdl_enabled(unsigned which) {  // programmatic dependent launch (common.cuh
     const char* e = getenv("CAFS_PDL");
     // default: not the compaction -- measured on cfg3, its early-launched CTAs
     // cost 45 us (the other kernels gain 2-5 us)
-    return e ? (unsigned)strtoul(e, nullptr, 0) : 0xffu & ~kPdlCompact;
+    return e ? (unsigned)strtoul(e, nullptr, 0) : 0x1ffu & ~kPdlCompact;
   }();
   return (mask & which) != 0;
 }

@@ -122,7 +122,8 @@ __device__ __forceinline__ void pdl_begin() {
 // overrides the mask (abi.cu)
 enum : unsigned {
   kPdlEstimate = 1, kPdlTiny = 2, kPdlCount = 4, kPdlCompact = 16,
-  kPdlDense = 32, kPdlPairSort = 64, kPdlEmit = 128
+  kPdlDense = 32, kPdlPairSort = 64, kPdlEmit = 128,
+  kPdlMsd = 256  // the MSD / scan kernels of the large pair sort and the fallback
 };
 bool pdl_enabled(unsigned which);
 

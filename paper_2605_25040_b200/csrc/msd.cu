@@ -65,6 +65,7 @@ __device__ __forceinline__ u32 msd_digit(u64 k, u64 base, int shift) {
 
 __global__ void __launch_bounds__(512) msd_reduce_kernel(const u64* __restrict__ keys, u64 n,
                                                          u64 flip, MsdState* ms) {
+  pdl_begin();
   u64 lo = ~0ull, hi = 0;
   const u64 stride = (u64)gridDim.x * blockDim.x;
   u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const u64* __restrict__ k
 }
 
 __global__ void __launch_bounds__(1024) msd_scan_kernel(MsdState* ms) {
+  pdl_begin();
   __shared__ u32 ws[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int IT = kMsdBuckets / 1024;
@@ -167,6 +169,7 @@ __global__ void __launch_bounds__(1024) msd_scan_kernel(MsdState* ms) {
 // hist[b] = the bucket's total.
 __global__ void __launch_bounds__(1024) msd_chunk_hist_kernel(const u64* __restrict__ keys, u64 n,
                                                               u64 flip, MsdState* ms, u64 chunk) {
+  pdl_begin();
   __shared__ u32 h[kMsdBuckets];
   for (u32 i = threadIdx.x; i < kMsdBuckets; i += 1024) h[i] = 0;
   __syncthreads();
@@ -199,6 +202,7 @@ __global__ void __launch_bounds__(1024)
     msd_scatter_chunk_kernel(const u64* __restrict__ keys, const u64* __restrict__ vals, u64 n,
                              u64 flip, const MsdState* ms, u64 chunk, u64* __restrict__ tk,
                              u64* __restrict__ tv) {
+  pdl_begin();
   __shared__ u32 lc[kMsdBuckets];
   __shared__ u32 gb[kMsdBuckets];
   const u32* row = ms->offs[blockIdx.x];
@@ -247,6 +251,7 @@ constexpr size_t kStSmem = (size_t)kStTile * 8 + (size_t)kMsdBuckets * 4 * 3;
 __global__ void __launch_bounds__(1024, 1)
     msd_scatter_staged_kernel(const u64* __restrict__ keys, u64 n, u64 flip, const MsdState* ms,
                               u64 chunk, u64* __restrict__ tk) {
+  pdl_begin();
   extern __shared__ __align__(16) unsigned char st_smem[];
   u64* stage = (u64*)st_smem;                    // [kStTile] keys in bucket order
   u32* gpos = (u32*)(stage + kStTile);           // [4096] next global position per bucket
@@ -386,6 +391,7 @@ __global__ void __launch_bounds__(256)
     bucket_small_kernel(const u64* __restrict__ tk, const u64* __restrict__ tv,
                         const MsdState* ms, u64 flip, u64* __restrict__ dk,
                         u64* __restrict__ dv) {
+  pdl_begin();
   constexpr int R = kWarpBucketMax / 32;
   __shared__ u64 sk[8][kWarpBucketMax];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -438,6 +444,7 @@ __global__ void __launch_bounds__(kBsThreads, 5)  // latency-bound phases: more 
     bucket_sort_kernel(const u64* __restrict__ tk, const u64* __restrict__ tv,
                        const MsdState* ms, u64 flip, u64* __restrict__ dk, u64* __restrict__ dv,
                        u32 cap) {
+  pdl_begin();
   extern __shared__ __align__(16) unsigned char bs_smem[];
   u64* kb[2] = {(u64*)bs_smem, (u64*)bs_smem + cap};
   unsigned short* ib[2] = {(unsigned short*)((u64*)bs_smem + 2 * cap),
@@ -675,8 +682,8 @@ bool launch_msd_count(const u64* keys, u64 n, u64 flip, void* state, int num_sms
   if (blocks > (u64)num_sms * 4) blocks = (u64)num_sms * 4;
   if (blocks < 1) blocks = 1;
   msd_reduce_kernel<<<(unsigned)blocks, 512, 0, st>>>(keys, n, flip, ms);
-  msd_chunk_hist_kernel<<<(unsigned)nchunks, 1024, 0, st>>>(keys, n, flip, ms, chunk);
-  msd_scan_kernel<<<1, 1024, 0, st>>>(ms);
+  launch_pdl(kPdlMsd, msd_chunk_hist_kernel, (unsigned)nchunks, 1024, 0, st, keys, n, flip, ms, chunk);
+  launch_pdl(kPdlMsd, msd_scan_kernel, 1, 1024, 0, st, ms);
   return true;
 }
 
@@ -742,20 +749,23 @@ void launch_msd_sort(const u64* keys, const u64* vals, u64 n, u64 flip, void* st
   const bool large = maxb > kWarpBucketMax;
   const u32 cap = (maxb + kBsThreads - 1) / kBsThreads * kBsThreads;  // <= kBucketCap
   if (vals) {
-    msd_scatter_chunk_kernel<true><<<(unsigned)chunks, 1024, 0, st>>>(keys, vals, n, flip, ms,
-                                                                      chunk, tk, tv);
-    bucket_small_kernel<true><<<kMsdBuckets / 8, 256, 0, st>>>(tk, tv, ms, flip, dk, dv);
+    launch_pdl(kPdlMsd, msd_scatter_chunk_kernel<true>, (unsigned)chunks, 1024, 0, st, keys, vals,
+               n, flip, (const MsdState*)ms, chunk, tk, tv);
+    launch_pdl(kPdlMsd, bucket_small_kernel<true>, kMsdBuckets / 8, 256, 0, st, (const u64*)tk,
+               (const u64*)tv, (const MsdState*)ms, flip, dk, dv);
     if (large)
-      bucket_sort_kernel<true><<<kMsdBuckets, kBsThreads, bs_smem_bytes(cap, true), st>>>(
-          tk, tv, ms, flip, dk, dv, cap);
+      launch_pdl(kPdlMsd, bucket_sort_kernel<true>, kMsdBuckets, kBsThreads,
+                 bs_smem_bytes(cap, true), st, (const u64*)tk, (const u64*)tv,
+                 (const MsdState*)ms, flip, dk, dv, cap);
   } else {
-    msd_scatter_staged_kernel<<<(unsigned)chunks, 1024, kStSmem, st>>>(keys, n, flip, ms, chunk,
-                                                                       tk);
-    bucket_small_kernel<false><<<kMsdBuckets / 8, 256, 0, st>>>(tk, nullptr, ms, flip, dk,
-                                                               nullptr);
+    launch_pdl(kPdlMsd, msd_scatter_staged_kernel, (unsigned)chunks, 1024, kStSmem, st, keys, n,
+               flip, (const MsdState*)ms, chunk, tk);
+    launch_pdl(kPdlMsd, bucket_small_kernel<false>, kMsdBuckets / 8, 256, 0, st, (const u64*)tk,
+               (const u64*)nullptr, (const MsdState*)ms, flip, dk, (u64*)nullptr);
     if (large)
-      bucket_sort_kernel<false><<<kMsdBuckets, kBsThreads, bs_smem_bytes(cap, false), st>>>(
-          tk, nullptr, ms, flip, dk, nullptr, cap);
+      launch_pdl(kPdlMsd, bucket_sort_kernel<false>, kMsdBuckets, kBsThreads,
+                 bs_smem_bytes(cap, false), st, (const u64*)tk, (const u64*)nullptr,
+                 (const MsdState*)ms, flip, dk, (u64*)nullptr, cap);
   }
 }
 

@@ -434,6 +434,7 @@ __global__ void __launch_bounds__(1024, 1)
 constexpr int kScanItems = 8192;  // per block: 1024 threads x 8
 
 __global__ void __launch_bounds__(1024) scan_reduce_kernel(const u64* in, u64 n, u64* bsum) {
+  pdl_begin();
   __shared__ u64 w[32];
   const u64 b0 = (u64)blockIdx.x * kScanItems;
   u64 s = 0;
@@ -453,6 +454,7 @@ __global__ void __launch_bounds__(1024) scan_reduce_kernel(const u64* in, u64 n,
 
 __global__ void scan_top_kernel(u64* bsum, u64 nb, u64 n, u64* offs_end, DevCtl* ctl,
                                 u64 expect_total) {
+  pdl_begin();
   if (threadIdx.x != 0) return;
   u64 run = 0;
   for (u64 b = 0; b < nb; ++b) { const u64 c = bsum[b]; bsum[b] = run; run += c; }
@@ -467,6 +469,7 @@ __global__ void scan_top_kernel(u64* bsum, u64 nb, u64 n, u64* offs_end, DevCtl*
 
 __global__ void __launch_bounds__(1024)
     scan_apply_kernel(const u64* in, u64 n, const u64* bsum, u64* out) {
+  pdl_begin();
   __shared__ u64 w[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u64 b0 = (u64)blockIdx.x * kScanItems + (u64)tid * 8;
@@ -588,9 +591,10 @@ cudaError_t launch_small_sort_pairs(u64* keys, const u64* cnt, u64 n, DevCtl* ct
 void launch_scan(const u64* in, u64 n, u64* bsum, u64* out_offs, DevCtl* ctl, u64 expect,
                  cudaStream_t st) {
   const u64 nb = (n + kScanItems - 1) / kScanItems;
-  scan_reduce_kernel<<<(unsigned)(nb ? nb : 1), 1024, 0, st>>>(in, n, bsum);
-  scan_top_kernel<<<1, 32, 0, st>>>(bsum, nb, n, out_offs + n, ctl, expect);
-  scan_apply_kernel<<<(unsigned)(nb ? nb : 1), 1024, 0, st>>>(in, n, bsum, out_offs);
+  launch_pdl(kPdlMsd, scan_reduce_kernel, (unsigned)(nb ? nb : 1), 1024, 0, st, in, n, bsum);
+  launch_pdl(kPdlMsd, scan_top_kernel, 1, 32, 0, st, bsum, nb, n, out_offs + n, ctl, expect);
+  launch_pdl(kPdlMsd, scan_apply_kernel, (unsigned)(nb ? nb : 1), 1024, 0, st, in, n,
+             (const u64*)bsum, out_offs);
 }
 
 }  // namespace cafs

@@ -57,7 +57,7 @@ sys.exit(1 if bad else 0)
 """
 
 
-@pytest.mark.parametrize("env", [{"CAFS_PDL": "0"}, {"CAFS_PDL": "0xff"},
+@pytest.mark.parametrize("env", [{"CAFS_PDL": "0"}, {"CAFS_PDL": "0x1ff"},
                                  {"CAFS_PDL": "0", "CAFS_GRAPHS": "0"},
                                  {"CAFS_GRAPHS": "0"}])
 def test_launch_modes_sort_identically(env):
