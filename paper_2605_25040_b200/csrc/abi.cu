@@ -299,6 +299,28 @@ int sort_pairs_large(cafs_ctx_t* ctx, u64 np, cudaStream_t st) {
   return CAFS_OK;
 }
 
+// The main route's > kSmallSortMax pairs without the host's bucket-size round
+// trip: the MSD bucket sorts go out with the largest cap, and a bucket above it
+// raises MsdState::overflow, checked after the call's final synchronisation
+// (then the pairs are re-sorted by LSD and re-emitted).  *check: such an
+// unchecked MSD sort was enqueued.
+int sort_pairs_large_unchecked(cafs_ctx_t* ctx, u64 np, cudaStream_t st, bool* check) {
+  *check = false;
+  TRY(ensure_radix(ctx, np, false));
+  if (!ctx->pk_t) {
+    CK(cudaMalloc(&ctx->pk_t, kPairCap * 8));
+    CK(cudaMalloc(&ctx->pc_t, kPairCap * 8));
+  }
+  if (!launch_msd_count(ctx->pk_a, np, 0, ctx->msd, ctx->num_sms, st))
+    return sort_pairs_large(ctx, np, st);  // too many pairs for MSD buckets: LSD
+  launch_msd_sort(ctx->pk_a, ctx->pc_a, np, 0, ctx->msd, ctx->pk_t, ctx->pc_t, ctx->pk_b,
+                  ctx->pc_b, msd_bucket_cap(), ctx->num_sms, st);
+  ctx->launches += 6;
+  CKL();
+  *check = true;
+  return CAFS_OK;
+}
+
 // MSD bucket sort (msd.cu) when every bucket fits a CTA; returns false (nothing
 // written) when some bucket is too large, leaving the LSD path to the caller.
 int try_msd(cafs_ctx_t* ctx, const u64* keys, const u64* vals, u64 n, u64 flip, u64* tk, u64* tv,
@@ -711,20 +733,37 @@ int main_finish(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cafs_telemetry_t* tel
   }
   if (c.need_large) {
     const u64 np = c.npairs;
-    int ts = tm.begin();
-    TRY(sort_pairs_large(ctx, np, st));
-    launch_scan(ctx->pc_b, np, ctx->bsum, ctx->poffs, ctx->d_ctl, n, st);
-    ctx->launches += 3;
-    CKL();
-    tm.end(ts, L_STAGE_SORT_K);
-    ts = tm.begin();
-    const int tk = tm.begin();
-    launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st, np, kk);
-    tm.end(tk, L_K_EMIT);
-    ctx->launches++;
-    CKL();
-    tm.end(ts, L_STAGE_EMIT);
-    TRY(sync_ctl(ctx, st));
+    bool check = false;
+    for (int pass = 0; pass < 2; ++pass) {
+      int ts = tm.begin();
+      if (pass == 0) {
+        TRY(sort_pairs_large_unchecked(ctx, np, st, &check));
+      } else {  // a bucket overflowed the unchecked MSD sort: LSD, then the same scan + emit
+        u64 *rk, *rv;
+        TRY(radix_sort(ctx, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, np, 0, st, &rk, &rv));
+        if (rk != ctx->pk_b) {
+          CK(cudaMemcpyAsync(ctx->pk_b, rk, np * 8, cudaMemcpyDeviceToDevice, st));
+          CK(cudaMemcpyAsync(ctx->pc_b, rv, np * 8, cudaMemcpyDeviceToDevice, st));
+        }
+        check = false;
+      }
+      launch_scan(ctx->pc_b, np, ctx->bsum, ctx->poffs, ctx->d_ctl, n, st);
+      ctx->launches += 3;
+      CKL();
+      tm.end(ts, L_STAGE_SORT_K);
+      ts = tm.begin();
+      const int tk = tm.begin();
+      launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st, np, kk);
+      tm.end(tk, L_K_EMIT);
+      ctx->launches++;
+      CKL();
+      tm.end(ts, L_STAGE_EMIT);
+      if (check)
+        CK(cudaMemcpyAsync(ctx->h_scratch, (char*)ctx->msd + msd_overflow_offset(), sizeof(u32),
+                           cudaMemcpyDeviceToHost, st));
+      TRY(sync_ctl(ctx, st));
+      if (!check || ctx->h_scratch[0] == 0) break;
+    }
     *emitted = true;
   }
   if (c.sum_error || !c.pairs_ready) return fail(ctx, CAFS_ESUM, "pair counts do not sum to n");

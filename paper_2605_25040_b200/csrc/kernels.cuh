@@ -71,6 +71,7 @@ void launch_scan(const u64* in, u64 n, u64* bsum, u64* out_offs, DevCtl* ctl, u6
 size_t msd_state_bytes();
 u32 msd_bucket_cap();
 size_t msd_maxb_offset();
+size_t msd_overflow_offset();
 size_t msd_span_offset();
 size_t msd_hist_offset();
 void launch_msd_span(const u64* keys, u64 n, u64 flip, void* state, int num_sms, cudaStream_t st);

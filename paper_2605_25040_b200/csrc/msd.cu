@@ -46,6 +46,7 @@ struct MsdState {
   u32 cursor[kMsdBuckets];
   u32 maxb;
   int shift;
+  u32 overflow;  // a bucket larger than the bucket sort's cap (unchecked launches)
   u32 offs[kMsdMaxChunks][kMsdBuckets];  // chunk c's offset inside bucket b (not memset)
 };
 constexpr size_t kMsdClear = offsetof(MsdState, offs);
@@ -459,6 +460,10 @@ __global__ void __launch_bounds__(kBsThreads, 5)  // latency-bound phases: more 
   const u32 base = ms->base[b];
   const u32 n = ms->base[b + 1] - base;
   if (n <= kWarpBucketMax) return;  // bucket_small_kernel's
+  if (n > cap) {  // launched without the host's maxb check: the caller redoes the sort
+    if (tid == 0) atomicOr(&((MsdState*)ms)->overflow, 1u);
+    return;
+  }
   u64 vor = 0, vand = ~0ull, vmin = ~0ull, vmax = 0;
   {  // all loads in flight before any use (one DRAM round trip, not n/256)
     u64 lk[kBsRounds];
@@ -725,6 +730,7 @@ void launch_msd_partition(const u64* keys, u64 n, u64 flip, void* state, u64 kmi
 }
 
 size_t msd_maxb_offset() { return offsetof(MsdState, maxb); }
+size_t msd_overflow_offset() { return offsetof(MsdState, overflow); }
 
 // keys (and vals) -> tmp (bucketed) -> dk/dv sorted; dk may equal keys
 constexpr size_t kBsSmem = bs_smem_bytes(kBucketCap, true);

@@ -130,3 +130,27 @@ def test_concurrent_threads_on_two_streams_share_one_context():
     for t in ths:
         t.join()
     assert not errors, errors
+
+
+def test_large_pair_sort_bucket_overflow_recovers():
+    """> 8192 pairs whose keys cluster in one MSD bucket of the pair span: the
+    unchecked bucket sort flags the overflow and the call re-sorts the pairs
+    by LSD and re-emits (abi.cu sort_pairs_large_unchecked); the output and the
+    route still match the oracle."""
+    import paper_2605_25040_b200 as cafs
+    from oracle import cafs_oracle as orc
+
+    rng = np.random.default_rng(21)
+    hot = rng.integers(-2**62, 2**62, 300)
+    n_hot, n_cold = 2_700_000, 300_000
+    x = np.concatenate([rng.choice(hot, n_hot), rng.integers(0, 60_000, n_cold)]).astype(np.int64)
+    rng.shuffle(x)
+    otel = orc.cafs_sort(x.copy())
+    assert otel.route == "main"
+    for _ in range(2):  # direct and graph-replayed pipelines
+        t = torch.from_numpy(x).cuda()
+        tel = cafs.SortTelemetry()
+        cafs.cafs_sort(t, telemetry=tel)
+        torch.cuda.synchronize()
+        assert tel.route.value == "main" and tel.pairs > 8192
+        assert np.array_equal(t.cpu().numpy(), np.sort(x))
