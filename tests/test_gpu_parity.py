@@ -591,3 +591,21 @@ def test_main_route_beyond_two_million_keys():
     assert (tel.spill_len, tel.guard_fired, tel.updates) == (ot.spill_len, ot.guard_fired, ot.updates)
     assert (tel.table.hits, tel.table.claims, tel.table.spill_pushes) == (ot.hits, ot.claims,
                                                                           ot.spill_pushes)
+
+
+def test_parity_checks_catch_an_injected_fault():
+    """Negative control for the GPU checks (the reference's fault_point pattern,
+    selftest.py:84-105): a device result with one flipped bit, or a golden
+    record with a wrong route / estimate / spill count, must fail run_case."""
+    rec = next(r for r in load_json("special_cases.json")
+               if r["route"] == "main" and "table_buckets" in r)
+    x = special_input(rec["name"])
+    run_case(x, rec)  # clean
+    t = to_dev(x)
+    cafs.cafs_sort(t)
+    t[t.shape[0] // 2] ^= 1
+    assert sha(t) != rec["sha256"]
+    for field, bad in (("route", "tiny_count"), ("u", rec["u"] + 1),
+                       ("spill_len", rec["spill_len"] + 1)):
+        with pytest.raises(AssertionError):
+            run_case(x, dict(rec, **{field: bad}))

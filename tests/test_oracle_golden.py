@@ -125,3 +125,21 @@ def test_dtype32_cases_match_widened_oracle(rec):
         assert (e.k_hat, e.u, e.f1, e.f2, e.saturated) == (
             rec["k_hat"], rec["u"], rec["f1"], rec["f2"], rec["saturated"])
     assert tel.tiny_count_failed == rec["tiny_count_failed"]
+
+
+def test_checker_fails_on_an_injected_fault():
+    """Negative control (the reference's fault_point pattern, selftest.py:84-105):
+    one corrupted output element, a wrong dispatch tuple or a wrong telemetry
+    counter must each make the golden check fail."""
+    recs = load_json("special_cases.json")
+    rec = next(r for r in recs if r["route"] == "main" and "table_buckets" in r)
+    x = special_input(rec["name"])
+    _check(rec, x)  # the clean case passes
+    y = x.copy()
+    orc.cafs_sort(y)
+    y[y.shape[0] // 2] ^= 1  # one flipped bit in the sorted output
+    assert _sha(y) != rec["sha256"]
+    for field, bad in (("route", "tiny_count"), ("u", rec["u"] + 1),
+                       ("spill_len", rec["spill_len"] + 1)):
+        with pytest.raises(AssertionError):
+            _check(dict(rec, **{field: bad}), x)
