@@ -50,6 +50,8 @@ struct cafs_ctx {
   u32* glist = nullptr;
   u64* pk_a = nullptr;  // compacted pairs (unsorted)
   u64* pk_t = nullptr;  // MSD bucket buffers of the large pair sort (lazy)
+  u32* tile_map = nullptr;  // emit tile -> pair map for large pair sets (lazy)
+  u64 tile_map_len = 0;
   u64* pc_t = nullptr;
   u64* pc_a = nullptr;
   u64* pk_b = nullptr;  // sorted pairs
@@ -752,10 +754,20 @@ int main_finish(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cafs_telemetry_t* tel
       CKL();
       tm.end(ts, L_STAGE_SORT_K);
       ts = tm.begin();
+      const u64 tiles = emit_tiles(n, kk);
+      if (tiles > ctx->tile_map_len) {
+        if (ctx->tile_map) CK(cudaFree(ctx->tile_map));
+        ctx->tile_map = nullptr;
+        ctx->tile_map_len = 0;
+        CK(cudaMalloc(&ctx->tile_map, tiles * sizeof(u32)));
+        ctx->tile_map_len = tiles;
+      }
+      launch_emit_map(ctx->poffs, ctx->d_ctl, x, 0, n, ctx->tile_map, np, ctx->num_sms, st, kk);
       const int tk = tm.begin();
-      launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st, np, kk);
+      launch_emit(ctx->pk_b, ctx->poffs, 0, ctx->d_ctl, x, 0, n, flip, ctx->num_sms, st, np, kk,
+                  false, ctx->tile_map);
       tm.end(tk, L_K_EMIT);
-      ctx->launches++;
+      ctx->launches += 2;
       CKL();
       tm.end(ts, L_STAGE_EMIT);
       if (check)
@@ -1003,7 +1015,7 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
                  ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->dense, ctx->ghist, ctx->gbase,
                  ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage, ctx->msd,
                  ctx->tl_keys, ctx->tl_idx, ctx->tl_first, ctx->tl_runs, ctx->tl_comp,
-                 ctx->tl_offs, ctx->tl_acc, ctx->pk_t, ctx->pc_t, ctx->wide};
+                 ctx->tl_offs, ctx->tl_acc, ctx->pk_t, ctx->pc_t, ctx->wide, ctx->tile_map};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);

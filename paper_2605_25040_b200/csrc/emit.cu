@@ -57,7 +57,8 @@ template <int KK>
 __global__ void __launch_bounds__(kEmitThreads)
     emit_kernel(const u64* __restrict__ keys, const u64* __restrict__ goffs, u64 npairs_arg,
                 const DevCtl* ctl, typename KeyT<KK>::T* __restrict__ out, u64 begin, u64 end,
-                u64 flip, u64 tpw, u64 idx_entries, int ctl_slice) {
+                u64 flip, u64 tpw, u64 idx_entries, int ctl_slice,
+                const u32* __restrict__ tile_pair) {
   pdl_begin();
   using K = typename KeyT<KK>::T;
   constexpr u64 VK = 32 / sizeof(K);             // keys per 32-byte vector
@@ -82,13 +83,15 @@ __global__ void __launch_bounds__(kEmitThreads)
   // index of the offsets in shared memory: soffs[j] = offs[j * stride]; with at
   // most kIdxEntries pairs (stride 1) it is the offsets themselves, otherwise it
   // narrows each search to `stride` global entries
-  const u64 stride = (npairs + idx_entries) / idx_entries;
-  const u64 nidx = npairs / stride + 1;
+  // (with a tile map the tiles' pairs are looked up, not searched: no index)
+  const u64 stride = tile_pair ? 0 : (npairs + idx_entries) / idx_entries;
+  const u64 nidx = tile_pair ? 0 : npairs / stride + 1;
   for (u64 i = threadIdx.x; i < nidx; i += kEmitThreads) soffs[i] = goffs[i * stride];
-  __syncthreads();
+  if (!tile_pair) __syncthreads();
   if (stride == 1) offs = soffs;
   // pair containing global position g, searching from pair lo (offs[lo] <= g)
   auto locate = [&](u64 lo, u64 g) -> u64 {
+    if (tile_pair) return warp_find(goffs, lo, npairs - 1, g);  // head / tail keys only
     if (stride == 1) return warp_find(soffs, lo, npairs - 1, g);
     const u64 j = warp_find(soffs, lo / stride, nidx - 1, g);
     u64 a = j * stride, b = a + stride - 1;
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(kEmitThreads)
     const u64 e1 = (e0 + kTileKeys) < nvec * VK ? (e0 + kTileKeys) : nvec * VK;
     const u64 g0 = gb + e0, glast = gb + e1 - 1;
     if (!(g0 >= rs && glast < re)) {
-      p = locate(p, g0);
+      p = tile_pair ? (u64)tile_pair[t] : locate(p, g0);
       rs = offs[p];
       re = offs[p + 1];
       rk = splat(key_unmap<KK>(keys[p], flip));
@@ -175,16 +178,87 @@ __global__ void __launch_bounds__(kEmitThreads)
       if (g < gend) q += 32;
     }
     // the last pair touched becomes the cursor for the next tile
-    p = locate(q, glast);
+    if (tile_pair) {
+      if (t + 1 >= t1) break;  // the warp's last tile: no cursor needed
+      p = tile_pair[t + 1];    // the pair holding glast + 1; glast is in it or just before
+      if (offs[p] > glast) --p;
+    } else {
+      p = locate(q, glast);
+    }
     rs = offs[p];
     re = offs[p + 1];
     rk = splat(key_unmap<KK>(keys[p], flip));
   }
 }
 
+// Tile -> pair map for large pair sets: tile_pair[t] = the pair holding the
+// first key of emit tile t.  One warp per pair writes the tiles that start
+// inside its run (long runs: 32 tiles per store instruction), so the emit's
+// warps look their tiles' pairs up instead of searching the offsets (a search
+// costs ~4 dependent L2 round trips per tile: 27 % of the emit's warp time on
+// cfg3, plus 7 % for each CTA's shared index of the offsets).
+template <int KK>
+__global__ void __launch_bounds__(256)
+    emit_map_kernel(const u64* __restrict__ goffs, const DevCtl* ctl, const void* out, u64 begin,
+                    u64 end, u32* __restrict__ tile_pair) {
+  pdl_begin();
+  using K = typename KeyT<KK>::T;
+  constexpr u64 VK = 32 / sizeof(K);
+  constexpr u64 kTileKeys = kTileBytes / sizeof(K);
+  if (!ctl->pairs_ready) return;
+  const u64 npairs = ctl->npairs;
+  const u64 L = end - begin;
+  const u64 mis = (((uintptr_t)out) & 31) / sizeof(K);  // the emit's head (same formula)
+  const u64 head = mis ? ((VK - mis) < L ? (VK - mis) : L) : 0;
+  const u64 nkeys = (L - head) / VK * VK;
+  const u64 ntiles = (nkeys + kTileKeys - 1) / kTileKeys;
+  const u64 gb = begin + head;
+  // a thread per pair writes its (usually 0 or 1) tiles; a run covering more
+  // than 32 tiles is written by its whole warp, 32 entries per instruction
+  const int lane = threadIdx.x & 31;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 p0 = (u64)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); p0 < npairs;
+       p0 += stride) {  // warp-uniform: p0 is the warp's first pair
+    const u64 p = p0 + lane;
+    u64 t_lo = 0, t_hi = 0;
+    if (p < npairs) {
+      const u64 s = goffs[p], e = goffs[p + 1];
+      // tiles whose first position gb + t * TK lies in [s, e)
+      t_lo = s <= gb ? 0 : (s - gb + kTileKeys - 1) / kTileKeys;
+      t_hi = e <= gb ? 0 : (e - gb + kTileKeys - 1) / kTileKeys;
+      if (t_hi > ntiles) t_hi = ntiles;
+    }
+    const bool longrun = t_hi > t_lo + 32;
+    if (!longrun)
+      for (u64 t = t_lo; t < t_hi; ++t) tile_pair[t] = (u32)p;
+    for (u32 m = __ballot_sync(0xffffffffu, longrun); m; m &= m - 1) {
+      const int r = __ffs(m) - 1;
+      const u64 lo = __shfl_sync(0xffffffffu, t_lo, r), hi = __shfl_sync(0xffffffffu, t_hi, r);
+      const u32 pr = (u32)(p0 + r);
+      for (u64 t = lo + lane; t < hi; t += 32) tile_pair[t] = pr;
+    }
+  }
+}
+
+u64 emit_tiles(u64 L, int kk) { return (L + kTileBytes / (kk ? 4 : 8) - 1) / (kTileBytes / (kk ? 4 : 8)); }
+
+void launch_emit_map(const u64* offs, const DevCtl* ctl, const void* out, u64 begin, u64 end,
+                     u32* tile_pair, u64 npairs_bound, int num_sms, cudaStream_t st, int kk) {
+  u64 grid = (npairs_bound + 255) / 256;  // a thread per pair
+  const u64 maxg = (u64)num_sms * 8;
+  if (grid > maxg) grid = maxg;
+  if (grid < 1) grid = 1;
+  if (kk)
+    launch_pdl(kPdlEmit, emit_map_kernel<1>, (unsigned)grid, 256, 0, st, offs, ctl, out, begin,
+               end, tile_pair);
+  else
+    launch_pdl(kPdlEmit, emit_map_kernel<0>, (unsigned)grid, 256, 0, st, offs, ctl, out, begin,
+               end, tile_pair);
+}
+
 void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, void* out,
                  u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 /*npairs_bound*/,
-                 int kk, bool ctl_slice) {
+                 int kk, bool ctl_slice, const u32* tile_pair) {
   const u64 L = end > begin ? end - begin : 0;
   const u64 tile_keys = kTileBytes / (kk ? 4 : 8);
   const u64 wtiles = (L + tile_keys - 1) / tile_keys;
@@ -205,15 +279,15 @@ void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl
   switch (kk) {
     case 1:
       launch_pdl(kPdlEmit, emit_kernel<1>, (unsigned)grid, kEmitThreads, sm, st, keys, offs, npairs, ctl,
-                 (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
+                 (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0, tile_pair);
       break;
     case 2:
       launch_pdl(kPdlEmit, emit_kernel<2>, (unsigned)grid, kEmitThreads, sm, st, keys, offs, npairs, ctl,
-                 (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
+                 (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0, tile_pair);
       break;
     default:
       launch_pdl(kPdlEmit, emit_kernel<0>, (unsigned)grid, kEmitThreads, sm, st, keys, offs, npairs, ctl,
-                 (u64*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0);
+                 (u64*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0, tile_pair);
   }
 }
 

@@ -50,7 +50,10 @@ void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* p
 // emit.cu
 void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, void* out,
                  u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 npairs_bound,
-                 int kk = 0, bool ctl_slice = false);
+                 int kk = 0, bool ctl_slice = false, const u32* tile_pair = nullptr);
+u64 emit_tiles(u64 L, int kk);
+void launch_emit_map(const u64* offs, const DevCtl* ctl, const void* out, u64 begin, u64 end,
+                     u32* tile_pair, u64 npairs_bound, int num_sms, cudaStream_t st, int kk);
 // radix.cu
 size_t onesweep_smem(bool has_val);
 u64 onesweep_tiles(u64 n);
