@@ -41,7 +41,9 @@ cols = {
     "fallback": (rng.integers(-2**62, 2**62, 300_000), "host"),
     "sorted": (np.arange(-50_000, 50_000, dtype=np.int64), "native"),
     "uint64": (rng.choice(rng.integers(0, 2**63, 500, dtype=np.uint64) * 2, 600_000), "native"),
+    "small_n": (rng.integers(-9, 9, 1500), "host"),
 }
+MULTS = {"main_hash": 0x2545F4914F6CDD1D}  # a caller's odd hash multiplier (buckets.py:54-67)
 bad = []
 for name, (x, path) in cols.items():
     x = x if x.dtype == np.uint64 else x.astype(np.int64)
@@ -52,7 +54,7 @@ for name, (x, path) in cols.items():
     for rep in range(3):  # direct, captured, replayed
         t.copy_(torch.from_numpy(x))
         tel = cafs.SortTelemetry()
-        cafs_sort_sharded(t, telemetry=tel)
+        cafs_sort_sharded(t, telemetry=tel, hash_mult=MULTS.get(name))
         torch.cuda.synchronize()
         got_path = tel.sharded_path
         if (not np.array_equal(t.cpu().numpy(), want) or tel.route.value != route
