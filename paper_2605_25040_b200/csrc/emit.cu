@@ -53,7 +53,10 @@ __device__ __forceinline__ u64 warp_find(const u64* offs, u64 lo, u64 hi, u64 g)
   return lo + (31 - __clz(m));
 }
 
-template <int KK>
+// MAP: tiles find their pairs in a tile -> pair map (large pair sets) instead
+// of searching the offsets; a template flag so the common path's code (and its
+// 48 registers) is unchanged -- a runtime flag cost cfg4 70 us (60 registers).
+template <int KK, bool MAP>
 __global__ void __launch_bounds__(kEmitThreads)
     emit_kernel(const u64* __restrict__ keys, const u64* __restrict__ goffs, u64 npairs_arg,
                 const DevCtl* ctl, typename KeyT<KK>::T* __restrict__ out, u64 begin, u64 end,
@@ -84,14 +87,14 @@ __global__ void __launch_bounds__(kEmitThreads)
   // most kIdxEntries pairs (stride 1) it is the offsets themselves, otherwise it
   // narrows each search to `stride` global entries
   // (with a tile map the tiles' pairs are looked up, not searched: no index)
-  const u64 stride = tile_pair ? 0 : (npairs + idx_entries) / idx_entries;
-  const u64 nidx = tile_pair ? 0 : npairs / stride + 1;
+  const u64 stride = MAP ? 0 : (npairs + idx_entries) / idx_entries;
+  const u64 nidx = MAP ? 0 : npairs / stride + 1;
   for (u64 i = threadIdx.x; i < nidx; i += kEmitThreads) soffs[i] = goffs[i * stride];
-  if (!tile_pair) __syncthreads();
+  if (!MAP) __syncthreads();
   if (stride == 1) offs = soffs;
   // pair containing global position g, searching from pair lo (offs[lo] <= g)
   auto locate = [&](u64 lo, u64 g) -> u64 {
-    if (tile_pair) return warp_find(goffs, lo, npairs - 1, g);  // head / tail keys only
+    if (MAP) return warp_find(goffs, lo, npairs - 1, g);  // head / tail keys only
     if (stride == 1) return warp_find(soffs, lo, npairs - 1, g);
     const u64 j = warp_find(soffs, lo / stride, nidx - 1, g);
     u64 a = j * stride, b = a + stride - 1;
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(kEmitThreads)
     const u64 e1 = (e0 + kTileKeys) < nvec * VK ? (e0 + kTileKeys) : nvec * VK;
     const u64 g0 = gb + e0, glast = gb + e1 - 1;
     if (!(g0 >= rs && glast < re)) {
-      p = tile_pair ? (u64)tile_pair[t] : locate(p, g0);
+      p = MAP ? (u64)tile_pair[t] : locate(p, g0);
       rs = offs[p];
       re = offs[p + 1];
       rk = splat(key_unmap<KK>(keys[p], flip));
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(kEmitThreads)
       if (g < gend) q += 32;
     }
     // the last pair touched becomes the cursor for the next tile
-    if (tile_pair) {
+    if (MAP) {
       if (t + 1 >= t1) break;  // the warp's last tile: no cursor needed
       p = tile_pair[t + 1];    // the pair holding glast + 1; glast is in it or just before
       if (offs[p] > glast) --p;
@@ -278,16 +281,34 @@ void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl
   const size_t sm = ((u64)idx + 1) * 8;
   switch (kk) {
     case 1:
-      launch_pdl(kPdlEmit, emit_kernel<1>, (unsigned)grid, kEmitThreads, sm, st, keys, offs, npairs, ctl,
-                 (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0, tile_pair);
+      if (tile_pair)
+        launch_pdl(kPdlEmit, emit_kernel<1, true>, (unsigned)grid, kEmitThreads, sm, st, keys,
+                   offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx,
+                   ctl_slice ? 1 : 0, tile_pair);
+      else
+        launch_pdl(kPdlEmit, emit_kernel<1, false>, (unsigned)grid, kEmitThreads, sm, st, keys,
+                   offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx,
+                   ctl_slice ? 1 : 0, tile_pair);
       break;
     case 2:
-      launch_pdl(kPdlEmit, emit_kernel<2>, (unsigned)grid, kEmitThreads, sm, st, keys, offs, npairs, ctl,
-                 (u32*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0, tile_pair);
+      if (tile_pair)
+        launch_pdl(kPdlEmit, emit_kernel<2, true>, (unsigned)grid, kEmitThreads, sm, st, keys,
+                   offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx,
+                   ctl_slice ? 1 : 0, tile_pair);
+      else
+        launch_pdl(kPdlEmit, emit_kernel<2, false>, (unsigned)grid, kEmitThreads, sm, st, keys,
+                   offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx,
+                   ctl_slice ? 1 : 0, tile_pair);
       break;
     default:
-      launch_pdl(kPdlEmit, emit_kernel<0>, (unsigned)grid, kEmitThreads, sm, st, keys, offs, npairs, ctl,
-                 (u64*)out, begin, end, flip, (u64)tpw, (u64)idx, ctl_slice ? 1 : 0, tile_pair);
+      if (tile_pair)
+        launch_pdl(kPdlEmit, emit_kernel<0, true>, (unsigned)grid, kEmitThreads, sm, st, keys,
+                   offs, npairs, ctl, (u64*)out, begin, end, flip, (u64)tpw, (u64)idx,
+                   ctl_slice ? 1 : 0, tile_pair);
+      else
+        launch_pdl(kPdlEmit, emit_kernel<0, false>, (unsigned)grid, kEmitThreads, sm, st, keys,
+                   offs, npairs, ctl, (u64*)out, begin, end, flip, (u64)tpw, (u64)idx,
+                   ctl_slice ? 1 : 0, tile_pair);
   }
 }
 
