@@ -49,7 +49,10 @@ def full(rep, config, out):
     t = json.load(open(tpath)) if os.path.exists(tpath) else {}
     t[config] = {}
     for d in res:  # per kernel family: the launch that did the work
-        fam = "hash_count_kernel" if "hash_count" in d["kernel"] else d["kernel"].split()[-1].split("<")[0]
+        # family: the function name without return type or template arguments
+        # ("void emit_kernel<0, 1>" -> "emit_kernel")
+        fam = ("hash_count_kernel" if "hash_count" in d["kernel"]
+               else d["kernel"].split("<")[0].split()[-1])
         if d["dram_bytes"] > t[config].get(fam, {}).get("dram_bytes_per_launch", -1):
             t[config][fam] = {"kernel": d["kernel"], "dram_bytes_per_launch": d["dram_bytes"],
                               "duration_s": d["duration_s"], "source": os.path.basename(out)}
