@@ -609,3 +609,42 @@ def test_parity_checks_catch_an_injected_fault():
                        ("spill_len", rec["spill_len"] + 1)):
         with pytest.raises(AssertionError):
             run_case(x, dict(rec, **{field: bad}))
+
+
+def _checksums(t):
+    """Permutation-invariant fingerprints of an int64 column (sum and sum of
+    squares mod 2^64), computed on the device in 2^28-row slices."""
+    s = q = 0
+    for i in range(0, t.shape[0], 1 << 28):
+        c = t[i:i + (1 << 28)]
+        s = (s + int(c.sum().item())) % (1 << 64)
+        q = (q + int((c * c).sum().item())) % (1 << 64)
+    return s, q
+
+
+@pytest.mark.parametrize("route", ["main", "fallback"])
+def test_beyond_two_billion_rows(route):
+    """Maximum-size edge: 2^31 + 12345 rows (past every 32-bit row index), on the
+    dense-window main route and on the fallback route (LSD onesweep: more rows
+    than the MSD buckets take); sortedness plus permutation-invariant checksums
+    (and the per-code histogram for the codes) at full size."""
+    n = (1 << 31) + 12345
+    lib = cafs.sorter._lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    x = torch.empty(n, dtype=torch.int64, device="cuda")
+    if route == "main":  # dictionary codes 0..999, uniform
+        assert lib.cafs_gen_draw(x.data_ptr(), n, 0, 77, 0, 1000, 0, st) == 0
+        hist_in = torch.bincount(x, minlength=1000)
+    else:  # random 64-bit keys
+        assert lib.cafs_gen_mix(x.data_ptr(), n, 78, 0, st) == 0
+    sums = _checksums(x)
+    tel = SortTelemetry()
+    cafs.cafs_sort(x, telemetry=tel)
+    torch.cuda.synchronize()
+    assert tel.route.value == ("main" if route == "main" else "fallback_high_entropy")
+    assert bool((x[1:] >= x[:-1]).all())
+    assert _checksums(x) == sums
+    if route == "main":
+        assert torch.equal(torch.bincount(x, minlength=1000), hist_in)
+    del x
+    torch.cuda.empty_cache()
