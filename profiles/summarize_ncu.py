@@ -72,11 +72,19 @@ def launches(path, out):
         if len(r) > mi:
             agg.setdefault(r[ki].split("(")[0][:60], []).append(float(r[mi].replace(",", "")))
     tot = sum(sum(v) for v in agg.values())
+    # the sort's own kernels (the library's, not the generator's or torch's
+    # checks): their shares are the ones to set beside the bench line's
+    # roofline.kernels[*].share_of_step
+    own = {k: v for k, v in agg.items() if "cafs::" in k and "gen_" not in k}
+    tot_own = sum(sum(v) for v in own.values()) or 1.0
     with open(out, "w") as f:
         f.write(f"# per-kernel device time from `ncu --metrics gpu__time_duration.sum` ({os.path.basename(path)})\n")
         f.write("# cold-cache, serialised launches: compare shares, not absolutes\n")
         for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
             f.write(f"{k:60s} n={len(v):3d} avg={sum(v)/len(v)/1e3:10.3f} us  share={sum(v)/tot*100:5.1f}%\n")
+        f.write("#\n# shares among the sort pipeline's kernels only (all calls of the command)\n")
+        for k, v in sorted(own.items(), key=lambda kv: -sum(kv[1])):
+            f.write(f"{k:60s} n={len(v):3d} share_of_sort={sum(v)/tot_own*100:5.1f}%\n")
     print(open(out).read())
 
 
