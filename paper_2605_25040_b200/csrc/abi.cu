@@ -88,8 +88,8 @@ struct cafs_ctx {
   u64* wide = nullptr;    // int64 copy of a 32-bit column (host-driven fallback routes)
   u64 wide_elems = 0;
   // pageable host transfers: per worker thread a stream and two pinned buffers
-  cudaStream_t xfer_stream[16] = {};
-  cudaEvent_t xfer_event[16][2] = {};
+  cudaStream_t xfer_stream[32] = {};
+  cudaEvent_t xfer_event[32][4] = {};
   unsigned char* xfer_buf = nullptr;  // pinned, kXferThreads x 2 x kXferChunk
   // CUDA Graphs of the fused pipeline (estimate + gated route kernels), keyed by
   // the call's arguments; captured on the second call with the same key
@@ -384,11 +384,32 @@ int fallback_any(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cudaStream_t st, int
 
 // ---- host <-> device transfers for pageable (unregistered) host memory ----
 // The driver stages pageable copies through its own pinned buffers at ~7 GB/s
-// per direction on the test host; here kXferThreads host threads each copy a
-// contiguous share through two pinned buffers of their own (host memcpy into
-// one while the DMA of the other runs on the thread's stream): ~PCIe speed.
-constexpr int kXferThreads = 16;
-constexpr size_t kXferChunk = 8u << 20;  // bytes per pinned buffer
+// per direction on the test host; here host threads each copy a contiguous
+// share through a small ring of pinned buffers of their own (host memcpy into
+// one while the DMAs of the others run on the thread's stream).
+constexpr int kXferMax = 32;
+static int xfer_threads() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("CAFS_XFER_T"); v = e ? atoi(e) : 16; if (v < 1 || v > 32) v = 16; }
+  return v;
+}
+static size_t xfer_chunk() {
+  static size_t v = 0;
+  if (!v) {
+    const char* e = getenv("CAFS_XFER_MB");
+    const int mb = e ? atoi(e) : 4;
+    v = (size_t)(mb >= 1 && mb <= 64 ? mb : 4) << 20;
+  }
+  return v;
+}
+static int xfer_bufs() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("CAFS_XFER_NB"); v = e ? atoi(e) : 3; if (v < 2 || v > 4) v = 3; }
+  return v;
+}
+#define kXferThreads xfer_threads()
+#define kXferChunk xfer_chunk()
+#define kXferBufs xfer_bufs()
 
 bool host_is_pageable(const void* p) {
   cudaPointerAttributes a;
@@ -403,10 +424,10 @@ int ensure_xfer(cafs_ctx_t* ctx) {
   if (ctx->xfer_buf) return CAFS_OK;
   for (int t = 0; t < kXferThreads; ++t) {
     CK(cudaStreamCreateWithFlags(&ctx->xfer_stream[t], cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < 4; ++b)
       CK(cudaEventCreateWithFlags(&ctx->xfer_event[t][b], cudaEventDisableTiming));
   }
-  CK(cudaMallocHost(&ctx->xfer_buf, (size_t)kXferThreads * 2 * kXferChunk));
+  CK(cudaMallocHost(&ctx->xfer_buf, (size_t)kXferThreads * kXferBufs * kXferChunk));
   return CAFS_OK;
 }
 
@@ -414,49 +435,47 @@ int ensure_xfer(cafs_ctx_t* ctx) {
 // the first CUDA error of any worker (cudaSuccess otherwise)
 cudaError_t staged_copy(cafs_ctx_t* ctx, void* dev, void* host, size_t bytes, bool to_device) {
   std::vector<std::thread> workers;
-  cudaError_t errs[kXferThreads] = {};
-  const size_t share = ((bytes + kXferThreads - 1) / kXferThreads + 15) & ~(size_t)15;
+  cudaError_t errs[kXferMax] = {};
+  const int T = kXferThreads, NB = kXferBufs;
+  const size_t C = kXferChunk;
+  const size_t share = ((bytes + T - 1) / T + 15) & ~(size_t)15;
   const int device = ctx->device;
-  for (int t = 0; t < kXferThreads; ++t) {
+  for (int t = 0; t < T; ++t) {
     const size_t lo = (size_t)t * share;
     if (lo >= bytes) break;
     const size_t hi = lo + share < bytes ? lo + share : bytes;
     workers.emplace_back([=, &errs]() {
       cudaError_t e = cudaSetDevice(device);
       cudaStream_t st = ctx->xfer_stream[t];
-      unsigned char* buf[2] = {ctx->xfer_buf + (size_t)t * 2 * kXferChunk,
-                               ctx->xfer_buf + ((size_t)t * 2 + 1) * kXferChunk};
+      unsigned char* base = ctx->xfer_buf + (size_t)t * NB * C;  // NB pinned buffers, a ring
       unsigned char* hp = (unsigned char*)host;
       unsigned char* dp = (unsigned char*)dev;
-      if (to_device) {
-        int k = 0;
-        for (size_t off = lo; off < hi && e == cudaSuccess; off += kXferChunk, k ^= 1) {
-          const size_t len = hi - off < kXferChunk ? hi - off : kXferChunk;
-          if (off >= lo + 2 * kXferChunk) e = cudaEventSynchronize(ctx->xfer_event[t][k]);
+      const size_t nch = (hi - lo + C - 1) / C;
+      auto len_of = [&](size_t c) { const size_t o = lo + c * C; return hi - o < C ? hi - o : C; };
+      if (to_device) {  // memcpy into buffer c % NB once its previous DMA is done, then DMA it
+        for (size_t c = 0; c < nch && e == cudaSuccess; ++c) {
+          const int k = (int)(c % NB);
+          if (c >= (size_t)NB) e = cudaEventSynchronize(ctx->xfer_event[t][k]);
           if (e != cudaSuccess) break;
-          memcpy(buf[k], hp + off, len);
-          e = cudaMemcpyAsync(dp + off, buf[k], len, cudaMemcpyHostToDevice, st);
+          memcpy(base + k * C, hp + lo + c * C, len_of(c));
+          e = cudaMemcpyAsync(dp + lo + c * C, base + k * C, len_of(c), cudaMemcpyHostToDevice, st);
           if (e == cudaSuccess) e = cudaEventRecord(ctx->xfer_event[t][k], st);
         }
-      } else {  // device -> pinned (async, one chunk ahead) -> pageable
-        size_t off = lo;
-        int k = 0;
-        if (off < hi) {
-          const size_t len = hi - off < kXferChunk ? hi - off : kXferChunk;
-          e = cudaMemcpyAsync(buf[0], dp + off, len, cudaMemcpyDeviceToHost, st);
-          if (e == cudaSuccess) e = cudaEventRecord(ctx->xfer_event[t][0], st);
+      } else {  // DMAs run NB - 1 chunks ahead of the memcpy out of the pinned ring
+        for (size_t c = 0; c < nch && c < (size_t)NB - 1 && e == cudaSuccess; ++c) {
+          e = cudaMemcpyAsync(base + (c % NB) * C, dp + lo + c * C, len_of(c), cudaMemcpyDeviceToHost, st);
+          if (e == cudaSuccess) e = cudaEventRecord(ctx->xfer_event[t][c % NB], st);
         }
-        for (; off < hi && e == cudaSuccess; off += kXferChunk, k ^= 1) {
-          const size_t len = hi - off < kXferChunk ? hi - off : kXferChunk;
-          const size_t nxt = off + kXferChunk;
-          if (nxt < hi) {
-            const size_t l2 = hi - nxt < kXferChunk ? hi - nxt : kXferChunk;
-            e = cudaMemcpyAsync(buf[k ^ 1], dp + nxt, l2, cudaMemcpyDeviceToHost, st);
-            if (e == cudaSuccess) e = cudaEventRecord(ctx->xfer_event[t][k ^ 1], st);
+        for (size_t c = 0; c < nch && e == cudaSuccess; ++c) {
+          const size_t nx = c + NB - 1;
+          if (nx < nch) {
+            e = cudaMemcpyAsync(base + (nx % NB) * C, dp + lo + nx * C, len_of(nx),
+                                cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaEventRecord(ctx->xfer_event[t][nx % NB], st);
             if (e != cudaSuccess) break;
           }
-          e = cudaEventSynchronize(ctx->xfer_event[t][k]);
-          if (e == cudaSuccess) memcpy(hp + off, buf[k], len);
+          e = cudaEventSynchronize(ctx->xfer_event[t][c % NB]);
+          if (e == cudaSuccess) memcpy(hp + lo + c * C, base + (c % NB) * C, len_of(c));
         }
       }
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -464,7 +483,7 @@ cudaError_t staged_copy(cafs_ctx_t* ctx, void* dev, void* host, size_t bytes, bo
     });
   }
   for (auto& w : workers) w.join();
-  for (int t = 0; t < kXferThreads; ++t)
+  for (int t = 0; t < T; ++t)
     if (errs[t] != cudaSuccess) return errs[t];
   return cudaSuccess;
 }
@@ -1028,7 +1047,7 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   for (int t = 0; t < kXferThreads; ++t) {
     if (ctx->xfer_stream[t]) cudaStreamDestroy(ctx->xfer_stream[t]);
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < 4; ++b)
       if (ctx->xfer_event[t][b]) cudaEventDestroy(ctx->xfer_event[t][b]);
   }
   if (ctx->xfer_buf) cudaFreeHost(ctx->xfer_buf);
