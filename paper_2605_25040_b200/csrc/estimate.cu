@@ -258,6 +258,12 @@ __global__ void __launch_bounds__(1024, 1)
     }
   }
 
+  // the sample's span by warp 0's shuffles (a 32-step loop on thread 0 cost ~1 us)
+  u64 span_lo = kEmpty, span_hi = 0;
+  if (wid == 0) {
+    span_lo = warp_min_u64(rmin[lane]);
+    span_hi = warp_max_u64(rmax[lane]);
+  }
   if (tid == 0) {
     ctl->prefix_sorted = !inv;
     ctl->route = route;
@@ -285,11 +291,7 @@ __global__ void __launch_bounds__(1024, 1)
     ctl->saturated = saturated;
     ctl->nkeys = (int)(u < CAFS_TINY_MAX_KEYS ? u : CAFS_TINY_MAX_KEYS);
     // dense-range window for the main count: centred on the sample's span
-    u64 smin = kEmpty, smax = 0;
-    for (int w = 0; w < 32; ++w) {
-      smin = rmin[w] < smin ? rmin[w] : smin;
-      smax = rmax[w] > smax ? rmax[w] : smax;
-    }
+    const u64 smin = span_lo, smax = span_hi;
     const u64 width = smax - smin;
     if (m > 0 && smax >= smin && width < kRangeCap / 2) {
       const u64 margin = (kRangeCap - 1 - width) / 2;
