@@ -30,6 +30,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -129,27 +131,35 @@ def ncu_traffic(config: str, kernel: str):
         return None
 
 
-def cpu_baseline(config: str, rows: int) -> dict:
+def cpu_baseline(config: str, column=None) -> dict:
     """The C oracle (a restatement of the reference algorithm; 1 thread, like the
-    reference) timed on a bounded sample of the same workload."""
+    reference) timed on the config's whole column: `column` is the device
+    column copied to host (same bits as the GPU sorted), else it is generated
+    on the host."""
     from oracle import cafs_oracle as orc
     from oracle import gen as ogen
 
     c = ogen.CONFIGS[config]
-    rows = min(rows, c.n)
-    x = c.generate(rows, 0)
+    x = column if column is not None else orc.generate(c)
+    rows = x.shape[0]
     best = float("inf")
+    y = np.empty_like(x)
     for _ in range(2):
-        y = x.copy()
+        np.copyto(y, x)
         t0 = time.perf_counter()
         orc.cafs_sort(y)
         best = min(best, time.perf_counter() - t0)
     return {"value": rows / best / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"first {rows} rows of {config} (C restatement of the reference, "
-                      f"min of 2, {best * 1e3:.1f} ms; nproc={os.cpu_count()})"}
+            "same_config": rows == c.n,
+            "sample": f"all {rows} rows of {config} (C restatement of the reference, "
+                      f"single-threaded like the reference; min of 2, {best * 1e3:.1f} ms; "
+                      f"nproc={os.cpu_count()})"}
 
 
 def run_reference(args) -> None:
+    """The reference algorithm on the host (the C restatement in oracle/,
+    single-threaded like the reference): every step sorts the
+    config's whole column (2^30 rows for cfg4, ~3-4 s per step)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -157,48 +167,65 @@ def run_reference(args) -> None:
     from oracle import gen as ogen
 
     c = ogen.CONFIGS[args.config]
-    rows = min(args.cpu_rows, c.n)
-    x = c.generate(rows, 0)
+    rows = min(args.cpu_rows, c.n) if args.cpu_rows else c.n
+    x = orc.generate(c, rows)
+    y = np.empty_like(x)
     for _ in range(args.warmup):
-        orc.cafs_sort(x.copy())
+        np.copyto(y, x)
+        orc.cafs_sort(y)
     times = []
     for _ in range(args.steps):
-        y = x.copy()
+        np.copyto(y, x)  # restore the unsorted column (untimed)
         t0 = time.perf_counter()
         orc.cafs_sort(y)
         times.append(time.perf_counter() - t0)
+    assert bool((y[1:] >= y[:-1]).all())
     tot = sum(times)
     value = rows * args.steps / tot / 1e9
-    # the reference sorts one column on one thread ("a single
-    # invocation is single-threaded; concurrent invocations on disjoint arrays
-    # are safe"); for scale, the box's aggregate: one invocation per host core
-    # on disjoint slices of the sample (ctypes releases the GIL)
-    import threading
+    # for scale, the box's aggregate: one invocation per host core on disjoint
+    # slices of the column (ctypes releases the GIL) -- not one column's sort
     nthr = os.cpu_count() or 1
-    slices = [x[i * (rows // nthr):(i + 1) * (rows // nthr)].copy() for i in range(nthr)]
+    np.copyto(y, x)
+    per = rows // nthr
     t0 = time.perf_counter()
-    ths = [threading.Thread(target=orc.cafs_sort, args=(sl,)) for sl in slices]
+    ths = [threading.Thread(target=orc.cafs_sort, args=(y[i * per:(i + 1) * per],))
+           for i in range(nthr)]
     for th in ths:
         th.start()
     for th in ths:
         th.join()
-    agg = (rows // nthr) * nthr / (time.perf_counter() - t0) / 1e9
+    agg = per * nthr / (time.perf_counter() - t0) / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": args.config, "n": rows, "k": c.k, "sample_of_n": c.n},
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic (host-generated, same bits as "
+        "the device generator)",
+        "config": {"workload": args.config, "n": rows, "k": c.k, "same_config": rows == c.n},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"first {rows} rows of {args.config}; C restatement of the "
-                                   "reference (single-threaded by design, SPEC.md:284); "
+                         "sample": f"all {rows} rows of {args.config} per step; C restatement of "
+                                   "the reference (single-threaded by design, SPEC.md:284); "
                                    f"nproc={os.cpu_count()}",
                          "all_cores": {"value": agg, "cores": nthr,
                                        "sample": f"{nthr} concurrent invocations on disjoint "
-                                                 f"{rows // nthr}-row slices (not one column)"}},
+                                                 f"{per}-row slices (not one column)"}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _relaunch(n: int) -> None:
+    """Re-execute this command under torch.distributed.run with N local ranks."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc:
+        raise SystemExit(rc)
 
 
 def main():
@@ -209,7 +236,8 @@ def main():
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-rows", type=int, default=1 << 24)
+    ap.add_argument("--cpu-rows", type=int, default=0,
+                    help="reference arm: rows per step (0 = the whole config column)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-direct", action="store_true", help="disable the dense-range count path")
     ap.add_argument("--dtype", default="int64", choices=["int64", "int32"],
@@ -217,6 +245,16 @@ def main():
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU code path (NCCL) even at one rank")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `bench.py --gpus N` outside torchrun: start the N ranks ourselves (one
+        # process per GPU, the same launch the driver uses) and pass their exit
+        # code through; rank 0 prints the line
+        _relaunch(args.gpus)
+        return
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}; "
+                         "launch N ranks with torchrun --nproc-per-node N (or drop WORLD_SIZE)")
     if args.impl == "reference":
         run_reference(args)
         return
@@ -258,7 +296,8 @@ def main():
 
     def one_step(tel):
         if not sharded:
-            cafs.cafs_sort(x, telemetry=tel, direct_range=not args.no_direct)
+            cafs.cafs_sort(x, telemetry=tel, direct_range=not args.no_direct,
+                           exact_telemetry=False)
         else:
             cafs_sort_sharded(x, telemetry=tel)
 
@@ -427,7 +466,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.config, args.cpu_rows)
+        col = pristine if kb == 8 else pristine.to(torch.int64)
+        cpu = cpu_baseline(args.config, col.cpu().numpy())
 
     if rank == 0:
         line = {

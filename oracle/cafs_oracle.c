@@ -338,3 +338,31 @@ void orc_mix_outputs(uint64_t seed, uint64_t count, uint64_t skip, uint64_t* out
   for (uint64_t i = 0; i < count; ++i)
     out[i] = orc_fmix64(seed + (skip + i + 1) * 0x9E3779B97F4A7C15ull);
 }
+
+/* The config generator of oracle/gen.py (Config.generate) in C, for the CPU
+ * baseline at full size (numpy takes ~2 min for 2^30 rows).  Rows
+ * [start, start + n): uniform draws by multiply-high (cdf == NULL) or Zipf draws
+ * by searchsorted(cdf, u, 'right') over k entries; palette == NULL means the
+ * dictionary codes 0..k-1.  Bit-identical to gen.py (tests/test_oracle_golden.py). */
+void orc_gen_draw(uint64_t seed, uint64_t n, uint64_t start, const int64_t* palette, uint64_t k,
+                  const double* cdf, int64_t* out) {
+  const uint64_t s = seed ^ 0xD1B54A32D192ED03ull;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t r = orc_fmix64(s + (start + i + 1) * 0x9E3779B97F4A7C15ull);
+    uint64_t idx;
+    if (!cdf) {
+      const uint64_t hi = r >> 32, lo = r & 0xFFFFFFFFull;
+      idx = (hi * k + ((lo * k) >> 32)) >> 32;
+    } else {
+      const double u = (double)(r >> 11) * (1.0 / 9007199254740992.0);
+      uint64_t lo = 0, len = k; /* first j with cdf[j] > u */
+      while (len > 0) {
+        const uint64_t half = len >> 1;
+        if (cdf[lo + half] <= u) { lo += half + 1; len -= half + 1; }
+        else len = half;
+      }
+      idx = lo;
+    }
+    out[i] = palette ? palette[idx] : (int64_t)idx;
+  }
+}

@@ -55,5 +55,7 @@ void orc_fallback_sort(int64_t* x, uint64_t n, int is_signed);
 int orc_cafs_sort(int64_t* x, uint64_t n, int is_signed, uint64_t mult, orc_telemetry_t* tel);
 uint64_t orc_fmix64(uint64_t z);
 void orc_mix_outputs(uint64_t seed, uint64_t count, uint64_t skip, uint64_t* out);
+void orc_gen_draw(uint64_t seed, uint64_t n, uint64_t start, const int64_t* palette, uint64_t k,
+                  const double* cdf, int64_t* out);
 
 #endif

@@ -79,6 +79,9 @@ def lib():
         L.orc_cafs_sort.restype = ctypes.c_int
         L.orc_cafs_sort.argtypes = [p64, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64,
                                     ctypes.POINTER(_Telemetry)]
+        L.orc_gen_draw.restype = None
+        L.orc_gen_draw.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, p64,
+                                   ctypes.c_uint64, ctypes.POINTER(ctypes.c_double), p64]
         _lib = L
     return _lib
 
@@ -213,3 +216,33 @@ def cafs_sort(x: np.ndarray, mult: int = HASH_MULT) -> Telemetry:
 def fallback_sort(x: np.ndarray) -> None:
     xi, signed = _as_i64(x)
     lib().orc_fallback_sort(_ptr(xi), xi.shape[0], signed)
+
+
+def generate(config, n: int | None = None, start: int = 0, threads: int | None = None) -> np.ndarray:
+    """Rows [start, start+n) of a BASELINE config (oracle/gen.py Config) by the C
+    generator, split over host threads (ctypes releases the GIL); bit-identical
+    to ``config.generate`` (tests/test_oracle_golden.py)."""
+    import threading
+
+    n = config.n - start if n is None else n
+    out = np.empty(n, np.int64)
+    pal = None if config.palette == "codes" else np.ascontiguousarray(config.palette_values())
+    cdf = config.cdf()
+    cdf_p = None if cdf is None else cdf.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    pal_p = None if pal is None else _ptr(pal)
+    T = max(1, min(threads or os.cpu_count() or 1, (n >> 16) or 1))
+    share = (n + T - 1) // T
+
+    def work(t):
+        lo = t * share
+        hi = min(n, lo + share)
+        if hi > lo:
+            lib().orc_gen_draw(config.seed, hi - lo, start + lo, pal_p, config.k, cdf_p,
+                               _ptr(out[lo:hi]))
+
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(T)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    return out

@@ -20,6 +20,7 @@ from .sorter import (
     PairList,
     Route,
     SortTelemetry,
+    TableStats,
     TableSummary,
     cafs_sort,
     chao1,
@@ -36,9 +37,12 @@ from .sorter import (
     tiny_counts,
 )
 
+from .tables import Bucket, BucketTable, FreqSet, bucket_update
+
 __version__ = "0.1.0"
 
 __all__ = [
+    "Bucket", "BucketTable", "FreqSet", "TableStats", "bucket_update",
     "CardinalityEstimate", "DispatchDecision", "PairList", "Route", "SortTelemetry", "TableSummary",
     "cafs_sort", "chao1", "check_hash_mult", "dispatch", "emit", "fallback_sort", "fast_hash",
     "is_monotone", "pair_sort", "sample_and_estimate", "table_size_for", "tiny_count_sort",

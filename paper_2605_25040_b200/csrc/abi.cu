@@ -1159,7 +1159,7 @@ static int sort_impl(cafs_ctx_t* ctx, void* d_x, uint64_t n, int is_signed, uint
     default:
       main_ran = true;
       emitted = true;
-      tel->table_buckets = table_size_for(c.k_hat > 1.0 ? c.k_hat : 1.0, n, 4);
+      tel->table_buckets = table_size_for(c.k_hat > 1.0 ? c.k_hat : 1.0, n, kk ? 8 : 4);  // bucket_cap, buckets.py:33-43
       rc = main_finish(ctx, x, n, flip, tel, tm, st, &emitted, kk);
       break;
   }

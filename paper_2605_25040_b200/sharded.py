@@ -455,6 +455,11 @@ def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTeleme
         cafs_sort_sharded(wide, group, hash_mult, telemetry, ops,
                           signed if x_local.dtype == torch.uint64 else True)
         x_local.copy_(wide.to(x_local.dtype) if wide.dtype != x_local.dtype else wide)
+        if (telemetry is not None and x_local.dtype in (torch.int32, torch.uint32)
+                and telemetry.route is Route.MAIN and telemetry.decision.estimate is not None):
+            # the reference's table for 4-byte keys has 8-slot buckets (buckets.py:33-43)
+            telemetry.table_buckets = table_size_for(
+                max(1.0, telemetry.decision.estimate.k_hat), telemetry.n, 8)
         return
     if ops is None:
         if signed is None:

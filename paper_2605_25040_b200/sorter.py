@@ -68,17 +68,57 @@ class DispatchDecision:  # sorter.py:52-57
     estimate: CardinalityEstimate | None = None
 
 
-@dataclass(frozen=True)
-class TableSummary:
-    """The reference BucketTable's shape and statistics (buckets.py:152-192),
-    computed exactly on device when ``exact_telemetry=True``."""
+class TableStats:
+    """The reference's TableStats (buckets.py:152-169): named update counters."""
 
-    n_buckets: int
-    cap: int
-    hits: int
-    claims: int
-    spill_pushes: int
-    spill_len: int
+    __slots__ = ("updates", "hits", "claims", "spill_pushes", "spill_len")
+
+    def __init__(self, updates=0, hits=0, claims=0, spill_pushes=0, spill_len=0):
+        self.updates, self.hits, self.claims = int(updates), int(hits), int(claims)
+        self.spill_pushes, self.spill_len = int(spill_pushes), int(spill_len)
+
+    def __repr__(self):
+        return (f"TableStats(updates={self.updates}, hits={self.hits}, claims={self.claims}, "
+                f"spill_pushes={self.spill_pushes}, spill_len={self.spill_len})")
+
+
+class TableSummary:
+    """``SortTelemetry.table``: a read-only view with the reference BucketTable's
+    observable surface (buckets.py:172-292) -- ``n_buckets``, ``cap``,
+    ``m_log2``, ``dtype``, ``hash_mult``, ``stats``, ``spill_len``,
+    ``counted_total()`` -- for the table the reference would have built on the
+    same input.  The device computes these exactly (telemetry.cu) without
+    building the table; its slot arrays and spill buffer are not materialised
+    (``keys`` / ``counts`` / ``spill`` raise)."""
+
+    def __init__(self, n_buckets: int, cap: int, hits: int, claims: int, spill_pushes: int,
+                 spill_len: int, updates: int = 0, counted_total: int = 0,
+                 dtype=np.uint64, hash_mult: int = HASH_MULT):
+        self.n_buckets = int(n_buckets)
+        self.cap = int(cap)
+        self.m_log2 = self.n_buckets.bit_length() - 1
+        self.dtype = np.dtype(dtype)
+        self.hash_mult = int(hash_mult)
+        self.stats = TableStats(updates, hits, claims, spill_pushes, spill_len)
+        self._counted = int(counted_total)
+
+    hits = property(lambda self: self.stats.hits)
+    claims = property(lambda self: self.stats.claims)
+    spill_pushes = property(lambda self: self.stats.spill_pushes)
+    spill_len = property(lambda self: self.stats.spill_len)
+
+    def counted_total(self) -> int:
+        """Sum of the bucket counters (excludes the spill), buckets.py:290-292."""
+        return self._counted
+
+    def _absent(self, *_):
+        raise AttributeError("the device pipeline does not materialise the reference's "
+                             "bucket slots or spill buffer; see stats / spill_len")
+
+    keys = property(_absent)
+    counts = property(_absent)
+    spill = property(_absent)
+    occupied_pairs = _absent
 
 
 @dataclass
@@ -88,9 +128,11 @@ class SortTelemetry:  # sorter.py:60-81
     ``stage_ms`` keys follow the reference's count / sort_k / emit labels and
     are CUDA-event times.  ``spill_len``, ``updates``, ``guard_fired``,
     ``counted_total`` and ``table`` describe the reference's bucket table, which
-    the device pipeline does not build: with ``cafs_sort(...,
-    exact_telemetry=True)`` they are computed exactly on device (telemetry.cu);
-    otherwise spill_len/updates stay 0 and guard_fired reports the device guard.
+    the device pipeline does not build; whenever a telemetry object is passed
+    they are computed exactly on device (telemetry.cu), as the reference fills
+    them (sorter.py:326-331).  ``cafs_sort(..., exact_telemetry=False)`` skips
+    that extra pass: spill_len / updates / table are then None (not computed)
+    and guard_fired reports the device guard.
     ``device_guard_fired`` (global-table overflow), ``pairs`` (distinct keys),
     ``global_updates``, ``table_buckets`` (the reference's table size M) and
     ``kernels_launched`` are device extras.
@@ -98,11 +140,11 @@ class SortTelemetry:  # sorter.py:60-81
 
     n: int = 0
     decision: DispatchDecision | None = None
-    spill_len: int = 0
+    spill_len: int | None = 0
     guard_fired: bool = False
     stage_ms: dict[str, float] = field(default_factory=dict)
     counted_total: int = 0
-    updates: int = 0
+    updates: int | None = 0
     tiny_count_failed: bool = False
     table: object | None = None
     pairs: int = 0
@@ -311,7 +353,12 @@ def _stage_dict(t: _lib.Telemetry) -> dict[str, float]:
     return out
 
 
-def _fill_telemetry(tel: SortTelemetry, t: _lib.Telemetry, kind: str, timing: bool) -> None:
+# the reference's table key dtype per input dtype (to_unsigned, sorter.py:84-94)
+_REF_DTYPE = {"int64": np.uint64, "uint64": np.uint64, "int32": np.uint32, "uint32": np.uint32}
+
+
+def _fill_telemetry(tel: SortTelemetry, t: _lib.Telemetry, kind: str, timing: bool,
+                    mult: int = HASH_MULT) -> None:
     tel.n = int(t.n)
     tel.decision = _decision_from_c(t.decision, tel.n, kind)
     tel.guard_fired = bool(t.guard_fired)
@@ -333,7 +380,16 @@ def _fill_telemetry(tel: SortTelemetry, t: _lib.Telemetry, kind: str, timing: bo
         tel.counted_total = int(t.ref_counted_total)
         if route is Route.MAIN:
             tel.table = TableSummary(tel.table_buckets, cap, int(t.ref_hits), int(t.ref_claims),
-                                     int(t.ref_spill_pushes), int(t.ref_spill_len))
+                                     int(t.ref_spill_pushes), int(t.ref_spill_len),
+                                     int(t.ref_updates), int(t.ref_counted_total),
+                                     _REF_DTYPE[kind], mult)
+        else:
+            tel.table = None
+    elif route is Route.MAIN:
+        # the reference's table statistics were not computed (exact_telemetry=False)
+        tel.spill_len = None
+        tel.updates = None
+        tel.table = None
     if timing:
         tel.stage_ms = _stage_dict(t)
         tel.kernel_ms = {name: float(t.kernel_ms[i])
@@ -347,17 +403,20 @@ def _fill_telemetry(tel: SortTelemetry, t: _lib.Telemetry, kind: str, timing: bo
 # ---------------- the API ----------------
 
 def cafs_sort(x, telemetry: SortTelemetry | None = None, hash_mult=None, *,
-              direct_range: bool = True, exact_telemetry: bool = False) -> None:
+              direct_range: bool = True, exact_telemetry: bool | None = None) -> None:
     """Sort a 1-D integer array ascending, in place (sorter.py:335-386).
 
     ``x`` is a torch CUDA tensor (sorted on its device and current stream) or a
     numpy array / CPU tensor (sorted through the host entry point).  Pass a
-    :class:`SortTelemetry` to observe the route, estimate, guard and per-stage
-    CUDA-event timings.
+    :class:`SortTelemetry` to observe the route, estimate, guard, the
+    reference's bucket-table statistics and per-stage CUDA-event timings;
+    ``exact_telemetry=False`` skips the statistics' extra input pass.
     """
     _validate(x)
     mult = check_hash_mult(hash_mult)
     want = telemetry is not None
+    if exact_telemetry is None:
+        exact_telemetry = want
     flags = (_lib.FLAG_TIMING if want else 0) | (0 if direct_range else _lib.FLAG_NO_DIRECT)
     if want and exact_telemetry:
         flags |= _lib.FLAG_EXACT_TELEMETRY
@@ -377,7 +436,7 @@ def cafs_sort(x, telemetry: SortTelemetry | None = None, hash_mult=None, *,
     else:
         kind = _host_sort(x, mult, flags, t)
     if want:
-        _fill_telemetry(telemetry, t, kind, want)
+        _fill_telemetry(telemetry, t, kind, want, mult)
 
 
 def _host_sort(x, mult: int, flags: int, t: _lib.Telemetry | None) -> str:
@@ -422,9 +481,13 @@ def _as_device(x):
 
 
 def dispatch(x, n: int | None = None, hash_mult=None) -> DispatchDecision:
-    """sorter.py:141-162.  The reference expects x already in the unsigned
-    domain; here x is the caller's array (any supported dtype) and the
-    order map is applied on device, so the decision is the one cafs_sort takes."""
+    """sorter.py:141-162, with the reference's input semantics: x's values are
+    taken as they are (cafs_sort passes the unsigned-domain copy, sorter.py:357);
+    the monotone test uses x's own order and the tiny keys are the sampled
+    values' 64-bit patterns (signed 32-bit values sign-extended, as the
+    reference's uint64 FreqSet stores them, cardinality.py:71-73), ascending as
+    unsigned integers.  Unsigned input -- what cafs_sort itself dispatches on --
+    gives exactly cafs_sort's decision."""
     mult = check_hash_mult(hash_mult)
     if n is not None and n != x.shape[0]:
         x = x[:n]
@@ -437,7 +500,11 @@ def dispatch(x, n: int | None = None, hash_mult=None) -> DispatchDecision:
     rc = _lib.load().cafs_dispatch_i64(ctx, v.ptr, v.n, int(v.signed), mult, ctypes.byref(d),
                                        _stream_ptr(v.dev))
     _lib.check(rc, ctx, "dispatch")
-    return _decision_from_c(d, n, v.kind)
+    dec = _decision_from_c(d, n, "uint64")
+    if dec.keys is not None and v.signed:
+        # device keys are order-mapped (bit 63 flipped): back to the raw bits
+        dec.keys = np.sort(dec.keys ^ np.uint64(1 << 63))
+    return dec
 
 
 def sample_and_estimate(x, n: int | None = None, hash_mult=None) -> CardinalityEstimate:

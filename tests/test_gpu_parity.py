@@ -72,10 +72,18 @@ def run_case(x: np.ndarray, rec: dict, mult=None, exact=True):
     if exact:
         check_exact(tel, rec)
     if x.shape[0] > 1:
-        d = cafs.dispatch(to_dev(x), hash_mult=mult)
+        # the reference's dispatch takes the unsigned-domain copy (sorter.py:357)
+        xu = x.view(np.uint64) ^ np.uint64(1 << 63) if x.dtype == np.int64 else x
+        d = cafs.dispatch(to_dev(xu), hash_mult=mult)
         assert d.route.value == rec["dispatch_route"]
         if rec.get("tiny_keys") is not None:
             assert d.keys.tolist() == rec["tiny_keys"]
+            if x.dtype == np.int64:
+                # signed input as it is: the keys are the values' raw bits,
+                # ascending as unsigned (the reference's uint64 FreqSet)
+                ds = cafs.dispatch(to_dev(x), hash_mult=mult)
+                want = sorted(int(k) ^ (1 << 63) for k in rec["tiny_keys"])
+                assert ds.keys.tolist() == want
     assert set(tel.stage_ms) <= {"count", "sort_k", "emit"}
     return tel
 

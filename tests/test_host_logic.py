@@ -129,3 +129,47 @@ def test_distributed_fallback_bucket_ranges():
                 assert P[lo] <= off and P[hi] >= off + s
                 assert totals[lo] > 0 and totals[hi - 1] > 0
             off += s
+
+
+def test_host_tables_match_oracle_telemetry():
+    """The exported host BucketTable / FreqSet (the reference API's counting
+    structures) reproduce the oracle's (= the reference's) table statistics and
+    estimate on the same inputs."""
+    from oracle import cafs_oracle as orc
+    from oracle import gen as ogen
+
+    for n, k, seed in ((20_000, 300, 1), (30_000, 3000, 2), (9_000, 40, 3)):
+        x = ogen.gen_input(n, k, seed).view(np.int64)
+        ot = orc.cafs_sort(x.copy())
+        assert ot.route == "main"
+        xu = x.view(np.uint64) ^ np.uint64(1 << 63)
+        t = cafs.BucketTable(int(ot.table_buckets).bit_length() - 1)
+        t.count_sequence(xu)
+        s = t.stats
+        assert (s.updates, s.hits, s.claims, s.spill_pushes, s.spill_len) == (
+            ot.updates, ot.hits, ot.claims, ot.spill_pushes, ot.spill_len)
+        assert t.counted_total() == ot.counted_total
+        assert t.spill.shape[0] == ot.spill_len
+        keys, counts = t.occupied_pairs()
+        assert int(counts.sum()) + ot.spill_len == n
+        fs = cafs.FreqSet()
+        stride = n // 1024
+        for v in xu[: 1024 * stride: stride]:
+            fs.insert(int(v))
+        e = ot.decision.estimate
+        assert fs.spectrum() == (e.u, e.f1, e.f2)
+
+
+def test_bucket_update_rules():
+    b = cafs.Bucket.empty()
+    assert b.cap == 4
+    assert cafs.bucket_update(b, 0)          # a zero key matches the empty slot 0
+    assert b.counts.tolist() == [1, 0, 0, 0]
+    for v in (5, 6, 7):
+        assert cafs.bucket_update(b, v, 2)
+    assert not cafs.bucket_update(b, 8)       # full: the caller spills
+    assert cafs.bucket_update(b, 6)
+    assert b.keys.tolist() == [0, 5, 6, 7] and b.counts.tolist() == [1, 2, 3, 2]
+    with pytest.raises(ValueError):
+        cafs.bucket_update(b, 5, 0)
+    assert cafs.Bucket.empty(np.uint32).cap == 8

@@ -143,3 +143,14 @@ def test_checker_fails_on_an_injected_fault():
                        ("spill_len", rec["spill_len"] + 1)):
         with pytest.raises(AssertionError):
             _check(dict(rec, **{field: bad}), x)
+
+
+def test_c_generator_matches_numpy_generator():
+    """oracle.cafs_oracle.generate (the C generator the CPU baseline uses at full
+    size) is bit-identical to oracle/gen.py on every config, threaded and not."""
+    from oracle import cafs_oracle as orc
+    from oracle import gen as ogen
+
+    for c in ogen.CONFIGS.values():
+        for start, n, thr in ((0, 70_000, 1), (987_654, 200_001, 5)):
+            assert np.array_equal(orc.generate(c, n, start, threads=thr), c.generate(n, start)), c.name
