@@ -87,6 +87,10 @@ struct cafs_ctx {
   uint64_t launches = 0;  // kernels this context has launched (monotone)
   u64* wide = nullptr;    // int64 copy of a 32-bit column (host-driven fallback routes)
   u64 wide_elems = 0;
+  // partitioned count (hashpart.cu): the partitioned spill (n keys) and its scratch
+  void* hp_part = nullptr;
+  size_t hp_part_bytes = 0;
+  void* hp_scratch = nullptr;
   // pageable host transfers: per worker thread a stream and two pinned buffers
   cudaStream_t xfer_stream[32] = {};
   cudaEvent_t xfer_event[32][4] = {};
@@ -211,6 +215,37 @@ int ensure_main(cafs_ctx_t* ctx) {
   CK(cudaMemset(ctx->dense, 0, dense_window_len() * 8));
   return CAFS_OK;
 }
+
+// Drop every captured pipeline graph (a buffer they reference was reallocated).
+void drop_graphs(cafs_ctx_t* ctx) {
+  for (auto& g : ctx->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g = cafs_ctx_t::GraphEntry();
+  }
+}
+
+// Columns from this many rows take the partitioned count when the sample shows
+// no dense window (smaller ones: the TMA queued shape of hashcount.cu).
+constexpr u64 kHpMinRows = 1ull << 20;
+
+bool hp_allowed(u64 n, bool exact) { return !exact && n >= kHpMinRows; }
+
+int ensure_hp(cafs_ctx_t* ctx, u64 n, int kk) {
+  const size_t bytes = (size_t)n * (kk ? 4 : 8) + 64;
+  if (bytes > ctx->hp_part_bytes) {
+    CK(cudaDeviceSynchronize());
+    if (ctx->hp_part) CK(cudaFree(ctx->hp_part));
+    ctx->hp_part = nullptr;
+    ctx->hp_part_bytes = 0;
+    drop_graphs(ctx);
+    CK(cudaMalloc(&ctx->hp_part, bytes));
+    ctx->hp_part_bytes = bytes;
+  }
+  if (!ctx->hp_scratch) CK(cudaMalloc(&ctx->hp_scratch, hp_scratch_bytes(ctx->num_sms)));
+  return CAFS_OK;
+}
+
+HpBufs hp_bufs(cafs_ctx_t* ctx) { return HpBufs{ctx->hp_part, ctx->hp_scratch, ctx->pk_a, ctx->pc_a}; }
 
 int ensure_radix(cafs_ctx_t* ctx, u64 n, bool need_tmp) {
   if (!ctx->ghist) {
@@ -631,28 +666,32 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
   ts = tm.begin();
   tk = tm.begin();
   const bool direct = !(flags & CAFS_FLAG_NO_DIRECT);
-  cudaError_t e;
-  if (direct) {
+  const bool hp = hp_allowed(n, !with_emit);
+  if (hp) TRY(ensure_hp(ctx, n, kk));
+  cudaError_t e = cudaSuccess;
+  if (direct)
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
                           ctx->num_sms, st, 0, kGateMainDense, ctx->dense, kk);
-    if (e == cudaSuccess)
-      e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                            ctx->num_sms, st, 1, kGateMainHash, ctx->dense, kk);
-  } else {
-    e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 0,
-                          ctx->num_sms, st, 1, kGateMain, ctx->dense, kk);
+  if (hp && e == cudaSuccess) {  // the partitioned count: the sorted pairs, no pair sort
+    e = launch_hp_count(hp_bufs(ctx), x, n, flip, c, ctx->pk_b, ctx->pc_b, ctx->poffs,
+                        ctx->num_sms, st, kGateMainHP, kk);
+    ctx->launches += 3;
   }
+  if (e == cudaSuccess)
+    e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, direct ? 1 : 0,
+                          ctx->num_sms, st, 1, direct ? kGateMainHash : kGateMainOld,
+                          ctx->dense, kk);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
   tm.end(tk, L_K_COUNT, C_MAIN);
   launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
-                 kGateMain);
+                 kGateMainOld);
   if (direct)
     launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs, n, st,
                        kGateMainDense);
   tm.end(ts, L_STAGE_COUNT, C_MAIN);
   ts = tm.begin();
   e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st,
-                              kGateMain);
+                              kGateMainOld);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   tm.end(ts, L_STAGE_SORT_K, C_MAIN);
   if (with_emit) {
@@ -745,6 +784,24 @@ int main_finish(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cafs_telemetry_t* tel
                 StageTimer& tm, cudaStream_t st, bool* emitted, int kk = 0) {
   DevCtl& c = *ctx->h_ctl;
   tel->global_updates = c.g_updates;
+  if (getenv("CAFS_DEBUG"))
+    fprintf(stderr, "[cafs] route=%d eff=%d hp_ok=%d hp_ovf=%u range_len=%u npairs=%llu total=%llu ready=%d need_large=%d ovf=%d k_hat=%f\n",
+            c.route, c.eff_route, c.hp_ok, c.hp_overflow, c.range_len, (unsigned long long)c.npairs,
+            (unsigned long long)c.total, c.pairs_ready, c.need_large, c.overflow, c.k_hat);
+  if (c.hp_overflow) {
+    // a partition of the partitioned count held more distinct keys than its
+    // table: put the column back together from the cells and the spill (its
+    // streamed part was overwritten by the spill), then sort it like the guard
+    launch_hp_restore(hp_bufs(ctx), x, n, flip, ctx->num_sms, st, kk);
+    ctx->launches++;
+    CKL();
+    tel->guard_fired = 1;
+    *emitted = false;
+    const int ts = tm.begin();
+    TRY(fallback_any(ctx, x, n, flip, st, kk));
+    tm.end(ts, L_STAGE_SORT_K);
+    return CAFS_OK;
+  }
   if (c.overflow) {
     CK(cudaMemsetAsync(ctx->gkeys, 0xFF, kGlobalSlots * 8, st));
     CK(cudaMemsetAsync(ctx->gcnt, 0, kGlobalSlots * 8, st));
@@ -809,7 +866,9 @@ int main_finish(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cafs_telemetry_t* tel
 void pipeline_direct(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t flags,
                      StageTimer& tm, cudaStream_t st, bool exact, int* mark, int* rc, int kk) {
   const int te = tm.begin();
-  launch_estimate(x, n, flip, 1, ctx->d_ctl, st, kk);
+  launch_estimate(x, n, flip, 1, ctx->d_ctl, st, kk,
+                  (hp_allowed(n, exact) ? kEstHp : 0) |
+                      ((flags & CAFS_FLAG_NO_DIRECT) ? kEstNoWindow : 0));
   tm.end(te, L_K_EST);
   ctx->launches++;
   *mark = tm.n;
@@ -1037,7 +1096,8 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
                  ctx->pk_b, ctx->pc_b, ctx->poffs, ctx->bsum, ctx->dense, ctx->ghist, ctx->gbase,
                  ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage, ctx->msd,
                  ctx->tl_keys, ctx->tl_idx, ctx->tl_first, ctx->tl_runs, ctx->tl_comp,
-                 ctx->tl_offs, ctx->tl_acc, ctx->pk_t, ctx->pc_t, ctx->wide, ctx->tile_map};
+                 ctx->tl_offs, ctx->tl_acc, ctx->pk_t, ctx->pc_t, ctx->wide, ctx->tile_map,
+                 ctx->hp_part, ctx->hp_scratch};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);

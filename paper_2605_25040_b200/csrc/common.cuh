@@ -78,6 +78,9 @@ struct DevCtl {
   u64 local_npairs;              // this shard's pairs (kept for the host-driven merge)
   int32_t local_sorted;          // ... sorted in the B buffers (else unsorted in A)
   int32_t local_overflow;        // ... lost to a global-table overflow
+  // --- partitioned count (hashpart.cu) ---
+  int32_t hp_ok;                 // the estimate chose the partitioned count for this call
+  u32 hp_overflow;               // a partition held more distinct keys than its table
 };
 
 // Device-only scratch allocated right after the DevCtl (not in its host
@@ -103,8 +106,12 @@ constexpr int32_t kNeedScan = 5;
 // each kernel reads the device decision and exits unless its route is active.
 enum : int {
   kGateNone = 0, kGateTiny = 1, kGateMain = 2, kGateMainDense = 3, kGateMainHash = 4,
-  kGateDense = 5, kGateHash = 6  // window open / closed, whatever the route (stage APIs)
+  kGateDense = 5, kGateHash = 6,  // window open / closed, whatever the route (stage APIs)
+  kGateMainHP = 7,    // main route, no window, partitioned count (hashpart.cu)
+  kGateMainOld = 8    // main route on the global-table path (window, or not partitioned)
 };
+constexpr int kHpParts = 512;      // key-range partitions of the partitioned count
+constexpr double kHpMaxKhat = 524288.0;  // above: the global-table count
 
 // Programmatic dependent launch (sm_90+).  Pipeline kernels are launched with
 // launch_pdl: the next kernel's CTAs may be scheduled while this one drains,
@@ -152,7 +159,10 @@ __device__ __forceinline__ bool gate_open(const DevCtl* ctl, int gate) {
   const bool main = r == CAFS_MAIN || (r == CAFS_TINY_COUNT && ctl->tiny_failed);
   if (gate == kGateMain) return main;
   const bool dense = ctl->range_len > 0;
-  return main && (gate == kGateMainDense ? dense : !dense);
+  const bool hp = !dense && ctl->hp_ok;
+  if (gate == kGateMainHP) return main && hp;
+  if (gate == kGateMainOld) return main && !hp;
+  return main && (gate == kGateMainDense ? dense : (!dense && !hp));
 }
 
 __device__ __forceinline__ u64 fmix64(u64 z) {

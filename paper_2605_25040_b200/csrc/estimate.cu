@@ -73,7 +73,7 @@ constexpr int kEstCtas = 16;
 template <int KK>
 __global__ void __launch_bounds__(1024, 1)
     estimate_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip, int check_prefix,
-                    DevCtl* ctl, const u64* __restrict__ ghdr, int world) {
+                    DevCtl* ctl, const u64* __restrict__ ghdr, int world, int opts) {
   // ghdr != null: sharded mode -- x holds the 1024 all-reduced samples
   // (order-mapped, flip 0) and the column's rows, monotone state and N come
   // from the all-gathered shard headers (kShardHdrWords words per rank)
@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(1024, 1)
     ctl->sum_error = 0;
     ctl->tiny_failed = 0;
     ctl->tiny_done = 0;
+    ctl->hp_overflow = 0;
   }
   if (tid < 16) ctl->tiny_counts[tid] = 0;
   if (tid < kListStripes) ctl->g_fill[tid] = 0;
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(1024, 1)
     // dense-range window for the main count: centred on the sample's span
     const u64 smin = span_lo, smax = span_hi;
     const u64 width = smax - smin;
-    if (m > 0 && smax >= smin && width < kRangeCap / 2) {
+    if (!(opts & kEstNoWindow) && m > 0 && smax >= smin && width < kRangeCap / 2) {
       const u64 margin = (kRangeCap - 1 - width) / 2;
       u64 base = smin >= margin ? smin - margin : 0ull;
       if (base > kEmpty - (kRangeCap - 1)) base = kEmpty - (kRangeCap - 1);
@@ -303,6 +304,10 @@ __global__ void __launch_bounds__(1024, 1)
       ctl->range_base = 0;
       ctl->range_len = 0;
     }
+    // the partitioned count (hashpart.cu): columns without a window whose
+    // estimated key count fits its 256 partitions of <= 4096 keys
+    ctl->hp_ok = (opts & kEstHp) && m == kSampleTarget && ctl->range_len == 0 &&
+                 k_hat <= kHpMaxKhat;
   }
 }
 
@@ -324,25 +329,25 @@ __global__ void monotone_scan_kernel(const typename KeyT<KK>::T* __restrict__ x,
 }
 
 void launch_estimate(const void* x, u64 n, u64 flip, int check_prefix, DevCtl* ctl,
-                     cudaStream_t st, int kk) {
+                     cudaStream_t st, int kk, int opts) {
   switch (kk) {
     case 1:
       launch_pdl(kPdlEstimate, estimate_kernel<1>, kEstCtas, 1024, 0, st, (const u32*)x, n, flip, check_prefix,
-                 ctl, (const u64*)nullptr, 0);
+                 ctl, (const u64*)nullptr, 0, opts);
       break;
     case 2:
       launch_pdl(kPdlEstimate, estimate_kernel<2>, kEstCtas, 1024, 0, st, (const u32*)x, n, flip, check_prefix,
-                 ctl, (const u64*)nullptr, 0);
+                 ctl, (const u64*)nullptr, 0, opts);
       break;
     default:
       launch_pdl(kPdlEstimate, estimate_kernel<0>, kEstCtas, 1024, 0, st, (const u64*)x, n, flip, check_prefix,
-                 ctl, (const u64*)nullptr, 0);
+                 ctl, (const u64*)nullptr, 0, opts);
   }
 }
 
 void launch_estimate_sharded(const u64* samples, const u64* ghdr, int world, DevCtl* ctl,
                              cudaStream_t st) {
-  estimate_kernel<0><<<1, 1024, 0, st>>>(samples, kSampleTarget, 0, 0, ctl, ghdr, world);
+  estimate_kernel<0><<<1, 1024, 0, st>>>(samples, kSampleTarget, 0, 0, ctl, ghdr, world, 0);
 }
 
 void launch_monotone_scan(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,

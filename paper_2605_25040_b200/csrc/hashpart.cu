@@ -1,0 +1,931 @@
+// hashpart.cu -- K3 for columns without a dense window: a partitioned count
+// whose output is the sorted (key, count) pairs, with no global hash table and
+// no pair sort.
+//
+// Replaces count_sequence + BucketTable (_kernels.py:25-81, buckets.py:172-292)
+// and reconstruct's pair sort (sorter.py:228-241, 276-285) on the MAIN route
+// when the sample saw no dense key window.  The reference folds runs into a
+// 4-slot bucket cache and spills what does not fit; this path keeps that
+// contract (every element lands in exactly one partial (key, count) cell or
+// in the spill) and then finishes the spill exactly, on chip:
+//
+//   hp_count_kernel, one persistent CTA per SM, 1024 threads
+//     * warp 0 streams the CTA's contiguous row range through a 3 x 31 KB TMA
+//       ring (cp.async.bulk + mbarrier complete_tx);
+//     * 31 consumer warps look every key up in a two-choice table of 2-slot
+//       buckets in shared memory (8192 slots): two independent LDS.128, four
+//       compares, one shared atomic per hit.  No sentinel test: an empty slot
+//       holds a marker that is never one of the probing key's two buckets'
+//       keys (the marker of E0's buckets is E1, E1's buckets are disjoint);
+//     * a miss goes to the warp's queue.  While the table has room, 32 queued
+//       misses are resolved together (CAS claims); once it is nearly full a
+//       miss is spilled without probing: 32 keys at a time, coalesced, into the
+//       part of the CTA's own input range it has already streamed (the emit
+//       overwrites the input anyway) -- no extra memory, no global atomics;
+//     * tail: the CTA's cells (occupied slots) and its spill are counting-sorted
+//       by key-range partition (512 partitions, monotone in the key) into its
+//       region of the cell buffer and of `part` (laid out like x).
+//   hp_reduce_kernel, one CTA per partition (two per SM)
+//     * gathers the partition's segments of every CTA's cells and spill into an
+//       exact shared-memory table and sorts its distinct keys (bitonic) -- in
+//       global key order, since partitions are key ranges;
+//   hp_place_kernel, one CTA per partition
+//     * prefix of the partitions' (pairs, rows), then the pairs at their global
+//       positions with their emit offsets; the last one publishes npairs /
+//       total / pairs_ready for the emit.
+//   A partition with more than kHpPartCap distinct keys sets hp_overflow; the
+//   host then writes the column back from the (intact) cells and spill and
+//   sorts it with the fallback (abi.cu: main_finish).
+//
+// Partition map: 4096 fine bins over the sample's span [min, max] (keys
+// outside clamp to the end bins), bin -> partition = half the sample mass
+// before the bin + half the bin's position in the span, so that a partition
+// holds at most ~2x its share of the rows (heavy keys) or of the value range
+// (spread-out distinct keys).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cafs {
+
+constexpr int kHpThreads = 1024;
+constexpr int kHpConsumers = kHpThreads - 32;
+constexpr int kHpStages = 3;
+constexpr int kHpStageWords = 3968;  // 31 KB per stage; 2 vectors per consumer thread
+constexpr int kHpVpt = kHpStageWords / 2 / kHpConsumers;
+static_assert(kHpVpt * kHpConsumers * 2 == kHpStageWords, "balanced stages");
+constexpr int kHpSLog2 = 13;
+constexpr u32 kHpS = 1u << kHpSLog2;      // table slots
+constexpr int kHpNBLog2 = kHpSLog2 - 1;
+constexpr u32 kHpNB = 1u << kHpNBLog2;    // 2-slot buckets
+constexpr u32 kHpFullClaims = kHpS - kHpS / 16;  // from here on a miss spills without probing
+constexpr int kHpQ = 64;                  // per-warp claim queue
+constexpr int kHpP = kHpParts;            // key-range partitions
+constexpr int kHpFine = 4096;             // fine bins of the partition map
+constexpr u32 kHpCellCap = kHpS + 16;     // cells per CTA (+ CTA 0's head / tail keys)
+constexpr int kHpChunk = 8192;            // tail scatter chunk (spilled keys)
+constexpr u32 kHpPartSlots = 4096;        // hp_reduce exact table
+constexpr u32 kHpPartCap = 2048;          // distinct keys per partition (load <= 1/2)
+constexpr u32 kHpListCap = kHpPartCap + kHpThreads;  // claims may overshoot by one per thread
+constexpr u32 kHpStage = kHpPartCap + 1;  // staged pairs per partition (+ the ~0 sentinel)
+static_assert(kHpP == 512, "scans below are written for 512 partitions");
+
+constexpr size_t kHpRingBytes = (size_t)kHpStages * kHpStageWords * 8;
+constexpr size_t kHpQueueBytes = (size_t)32 * kHpQ * 8;
+constexpr size_t kHpStagingBytes = kHpRingBytes + kHpQueueBytes;  // tail staging (ring + queues)
+constexpr size_t kHpCountSmem =
+    kHpStagingBytes + (size_t)kHpS * 12 + 2 * kHpStages * 8 + (size_t)kHpFine * 2;
+static_assert((size_t)kHpCellCap * 12 <= kHpStagingBytes, "cell staging");
+static_assert((size_t)kHpChunk * 10 <= kHpStagingBytes, "spill staging");
+static_assert(kHpCountSmem + 12288 <= 232448, "shared memory budget");
+constexpr size_t kHpReduceSmem = (size_t)kHpPartSlots * 12 + (size_t)kHpListCap * 16;
+
+// the two candidate buckets of a key (a cache of partial counts: a weak hash
+// costs spills, never correctness)
+__host__ __device__ __forceinline__ u32 hp_t(u64 v) {
+  return (u32)(v >> 32) * 0x9E3779B1u + (u32)v;
+}
+__host__ __device__ __forceinline__ u32 hp_b1(u32 t) { return (t * 0x85EBCA77u) >> (32 - kHpNBLog2); }
+__host__ __device__ __forceinline__ u32 hp_b2(u32 t) { return (t * 0xC2B2AE3Du) >> (32 - kHpNBLog2); }
+
+struct HpArgs {
+  const void* x;   // column (keys of kind KK); its streamed part receives the spill
+  u64 n;
+  u64 flip;
+  DevCtl* ctl;
+  void* part;      // partitioned spill, same layout and key type as x
+  u64* cellk;      // [grid][kHpCellCap]
+  u32* cellw;
+  u32* cpofs;      // [grid][kHpP + 1] cell segment starts per partition
+  u32* spofs;      // [grid][kHpP + 1] spill segment starts per partition
+  u64* pd;         // [kHpP] pairs of each partition (hp_reduce -> hp_place)
+  u64* pr;         // [kHpP] rows of each partition
+  u64* pk_stage;   // [kHpP][kHpStage] each partition's sorted pairs (hp_reduce)
+  u64* pc_stage;
+  u64* pk;         // sorted pairs: keys, counts, offsets (npairs + 1)
+  u64* pc;
+  u64* poffs;
+  u64 e0, e1;      // empty-slot markers: e1 in E0's two buckets ma, mb, e0 elsewhere
+  u32 ma, mb;
+  int gate;
+};
+
+__device__ __forceinline__ u64 hp_marker(const HpArgs& a, u32 b) {
+  return (b == a.ma || b == a.mb) ? a.e1 : a.e0;
+}
+
+// Partition of a key: its fine bin over the sample span, mapped (pmap).
+__device__ __forceinline__ u32 hp_part(u64 v, u64 lo, int sh, const unsigned short* pmap) {
+  const u64 d = (v - lo) >> sh;
+  const u32 f = v < lo ? 0u : (d < (u64)kHpFine ? (u32)d : (u32)(kHpFine - 1));
+  return pmap[f];
+}
+
+// CTA c's rows: a contiguous range of whole stages of the 16-byte-aligned body.
+__device__ __forceinline__ void hp_range(u64 body_keys, u64 skk, u32 c, u32 G, u64* k0, u64* k1) {
+  const u64 chunks = (body_keys + skk - 1) / skk;
+  const u64 per = (chunks + G - 1) / G;
+  const u64 a = (u64)c * per * skk, b = a + per * skk;
+  *k0 = a < body_keys ? a : body_keys;
+  *k1 = b < body_keys ? b : body_keys;
+}
+
+// Exclusive scan of 512 u32 counters by one warp (16 per lane); out[512] = total.
+__device__ __forceinline__ void hp_scan512(const u32* in, u32* out) {
+  const int lane = threadIdx.x & 31;
+  u32 v[16], s = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) { v[j] = in[lane * 16 + j]; s += v[j]; }
+  u32 inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  u32 run = inc - s;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) { out[lane * 16 + j] = run; run += v[j]; }
+  if (lane == 31) out[512] = run;
+}
+
+template <int KK>
+__global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
+  pdl_begin();
+  if (!gate_open(a.ctl, a.gate)) return;
+  using K = typename KeyT<KK>::T;
+  constexpr int KPV = 16 / sizeof(K);                    // keys per 16-byte vector
+  constexpr u64 SKK = (u64)kHpStageWords * 8 / sizeof(K);  // keys per stage
+  extern __shared__ __align__(128) unsigned char smem[];
+  u64* ring = (u64*)smem;                                    // [stages][stage words]
+  u64* queue = (u64*)(smem + kHpRingBytes);                  // [32][kHpQ]
+  u64* tkeys = (u64*)(smem + kHpStagingBytes);               // [kHpS]
+  u32* tcnt = (u32*)(tkeys + kHpS);                          // [kHpS]
+  u64* full = (u64*)(tcnt + kHpS);
+  u64* empty = full + kHpStages;
+  unsigned short* pmap = (unsigned short*)(empty + kHpStages);  // [kHpFine]
+  __shared__ u32 shist[kHpP + 1], hstart[kHpP + 1], lhist[kHpP + 1], lstart[kHpP + 1];
+  __shared__ u32 written[kHpP];
+  __shared__ u32 sfill, ncell_extra, sclaims;
+  __shared__ u64 extra_k[16];
+  __shared__ u64 s_lo;
+  __shared__ int s_sh;
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u32 c = blockIdx.x, G = gridDim.x;
+  const u64 flip = a.flip, n = a.n;
+  const K* xk = (const K*)a.x;
+  const u64 mis = (((uintptr_t)a.x) & 15) / sizeof(K);
+  const u64 head0 = mis ? (u64)KPV - mis : 0;
+  const u64 head = head0 < n ? head0 : n;
+  const u64 body = (n - head) / KPV * KPV;
+  K* xb = (K*)(xk + head);
+  u64 r0, r1;
+  hp_range(body, SKK, c, G, &r0, &r1);
+  const u64 nst = (r1 - r0 + SKK - 1) / SKK;
+
+  if (tid == 0) {
+    for (int s = 0; s < kHpStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kHpConsumers / 32);
+    }
+    fence_mbar_init();
+    // the first stages go out before the prologue (the ring fills meanwhile)
+    for (u64 it = 0; it < nst && it < (u64)kHpStages; ++it) {
+      const u64 off = r0 + it * SKK;
+      const u32 bytes = (u32)(((r1 - off) < SKK ? (r1 - off) : SKK) * sizeof(K));
+      mbar_arrive_expect_tx(&full[it], bytes);
+      tma_load_1d(ring + it * kHpStageWords, xb + off, bytes, &full[it]);
+    }
+    sfill = 0;
+    ncell_extra = 0;
+    sclaims = 0;
+  }
+  // ---- prologue: partition map from the estimate's 1024 samples ----
+  {
+    const u64* samp = est_scratch(a.ctl)->samples;
+    u32* fh = tcnt;  // fine histogram (the counts are zeroed below)
+    for (u32 i = tid; i < kHpFine; i += kHpThreads) fh[i] = 0;
+    const u64 sv = __ldcg(&samp[tid]);
+    u64 lo = sv, hi = sv;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+      lo = l2 < lo ? l2 : lo;
+      hi = h2 > hi ? h2 : hi;
+    }
+    u64* rl = queue;  // per-warp partials
+    if (lane == 0) { rl[wid] = lo; rl[32 + wid] = hi; }
+    __syncthreads();
+    if (wid == 0) {
+      lo = rl[lane];
+      hi = rl[32 + lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const u64 l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+      }
+      if (lane == 0) {
+        int sh = 0;
+        while (sh < 63 && ((hi - lo) >> sh) >= (u64)kHpFine) ++sh;
+        s_lo = lo;
+        s_sh = sh;
+      }
+    }
+    __syncthreads();
+    const u64 d = (sv - s_lo) >> s_sh;
+    atomicAdd(&fh[d < (u64)kHpFine ? (u32)d : kHpFine - 1], 1u);
+    __syncthreads();
+    // exclusive scan of the 4096 bins: 4 per thread
+    u32 v4[4], s = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { v4[j] = fh[tid * 4 + j]; s += v4[j]; }
+    u32 inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    u32* ws = (u32*)(queue + 64);
+    if (lane == 31) ws[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      u32 w = ws[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += t;
+      }
+      ws[32 + lane] = w;
+    }
+    __syncthreads();
+    u32 run = inc - s + (wid ? ws[32 + wid - 1] : 0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const u32 f = tid * 4 + j;
+      // half sample mass, half span position (both monotone in f)
+      const u32 p = (run * (kHpP / 2)) / kSampleTarget + (f * (kHpP / 2)) / kHpFine;
+      pmap[f] = (unsigned short)(p < (u32)kHpP ? p : kHpP - 1);
+      run += v4[j];
+    }
+    __syncthreads();
+  }
+  for (u32 i = tid; i < kHpS; i += kHpThreads) {
+    tkeys[i] = hp_marker(a, i >> 1);
+    tcnt[i] = 0;
+  }
+  for (u32 i = tid; i <= kHpP; i += kHpThreads) shist[i] = 0;
+  __syncthreads();
+  const u64 plo = s_lo;
+  const int psh = s_sh;
+  const u32 tbase = smem_u32(tkeys), cbase = smem_u32(tcnt);
+
+  // 32 queued misses (one per active lane) with the whole warp: while the
+  // table has room, look again and claim an empty slot of either bucket;
+  // what remains is spilled into the streamed range
+  auto resolve = [&](bool active, u64 u) {
+    bool done = !active;
+    if (*((volatile u32*)&sclaims) < kHpFullClaims && __any_sync(0xffffffffu, active)) {
+      if (active) {
+        const u32 t = hp_t(u);
+        const u32 bk[2] = {hp_b1(t), hp_b2(t)};
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          if (!done) {
+            const u32 bb = bk[r];
+            u64 t0, t1;
+            asm volatile("ld.volatile.shared.v2.u64 {%0,%1}, [%2];"
+                         : "=l"(t0), "=l"(t1) : "r"(smem_u32(&tkeys[2 * bb])));
+            const u64 mk = hp_marker(a, bb);
+            int hit = t0 == u ? 0 : (t1 == u ? 1 : -1);
+            if (hit < 0 && t0 == mk) {
+              const u64 o = atomicCAS(&tkeys[2 * bb], mk, u);
+              if (o == mk) atomicAdd(&sclaims, 1u);
+              if (o == mk || o == u) hit = 0;
+            }
+            if (hit < 0 && t1 == mk) {
+              const u64 o = atomicCAS(&tkeys[2 * bb + 1], mk, u);
+              if (o == mk) atomicAdd(&sclaims, 1u);
+              if (o == mk || o == u) hit = 1;
+            }
+            if (hit >= 0) { atomicAdd(&tcnt[2 * bb + hit], 1u); done = true; }
+          }
+        }
+      }
+    }
+    const bool sp = !done;
+    const u32 m = __ballot_sync(0xffffffffu, sp);
+    if (m) {
+      u32 base = 0;
+      if (lane == 0) base = atomicAdd(&sfill, (u32)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (sp) {
+        xb[r0 + base + __popc(m & lanemask_lt())] = key_unmap<KK>(u, flip);
+        atomicAdd(&shist[hp_part(u, plo, psh, pmap)], 1u);
+      }
+    }
+  };
+
+  if (wid == 0) {
+    // ---- TMA producer (stages past the first kHpStages) ----
+    if (lane == 0) {
+      for (u64 it = kHpStages; it < nst; ++it) {
+        const u32 s = (u32)(it % kHpStages);
+        const u32 ph = (u32)((it / kHpStages) & 1);
+        mbar_wait(&empty[s], ph ^ 1);
+        const u64 off = r0 + it * SKK;
+        const u32 bytes = (u32)(((r1 - off) < SKK ? (r1 - off) : SKK) * sizeof(K));
+        mbar_arrive_expect_tx(&full[s], bytes);
+        tma_load_1d(ring + (size_t)s * kHpStageWords, xb + off, bytes, &full[s]);
+      }
+    }
+  } else {
+    const int ctid = tid - 32;
+    u64* wq = queue + (size_t)wid * kHpQ;
+    u32 qn = 0;  // warp-uniform
+    u32 s = 0, ph = 0;
+    constexpr int KPT = kHpVpt * KPV;  // keys per thread per stage
+    for (u64 it = 0; it < nst; ++it) {
+      const u64 off = r0 + it * SKK;
+      const u32 nv = (u32)(((r1 - off) < SKK ? (r1 - off) : SKK) / KPV);
+      mbar_wait(&full[s], ph);
+      const ulonglong2* sv = (const ulonglong2*)(ring + (size_t)s * kHpStageWords);
+      u64 v[KPT];
+      u32 vmask = 0;  // valid keys of this thread
+#pragma unroll
+      for (int q = 0; q < kHpVpt; ++q) {
+        const u32 i = ctid + q * kHpConsumers;
+        ulonglong2 w = make_ulonglong2(0, 0);
+        if (i < nv) { w = sv[i]; vmask |= ((1u << KPV) - 1) << (q * KPV); }
+        if constexpr (KPV == 2) {
+          v[q * 2] = key_map<KK>((K)w.x, flip);
+          v[q * 2 + 1] = key_map<KK>((K)w.y, flip);
+        } else {
+          v[q * 4] = key_map<KK>((K)w.x, flip);
+          v[q * 4 + 1] = key_map<KK>((K)(w.x >> 32), flip);
+          v[q * 4 + 2] = key_map<KK>((K)w.y, flip);
+          v[q * 4 + 3] = key_map<KK>((K)(w.y >> 32), flip);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == kHpStages) { s = 0; ph ^= 1; }
+      u32 mm = 0;  // this thread's misses
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        // shared-space loads and a predicated RED: no generic addressing, no
+        // branch, and both buckets' loads issued before any compare
+        const u32 t = hp_t(v[k]);
+        const u32 b1 = hp_b1(t), b2 = hp_b2(t);
+        u64 a0, a1, c0, c1;
+        asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(a0), "=l"(a1) : "r"(tbase + b1 * 16));
+        asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(c0), "=l"(c1) : "r"(tbase + b2 * 16));
+        const bool h1x = a0 == v[k], h1y = a1 == v[k], h2x = c0 == v[k], h2y = c1 == v[k];
+        const bool h1 = h1x | h1y;
+        const bool hit = h1 | h2x | h2y;
+        const u32 slot = h1 ? 2 * b1 + (u32)h1y : 2 * b2 + (u32)h2y;
+        const u32 live = (vmask >> k) & 1u;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
+                     ::"r"(cbase + slot * 4), "r"((u32)hit & live) : "memory");
+        mm |= (((u32)!hit) & live) << k;
+      }
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        const bool miss = (mm >> k) & 1u;
+        const u32 m = __ballot_sync(0xffffffffu, miss);
+        if (m) {
+          if (miss) wq[qn + __popc(m & lanemask_lt())] = v[k];
+          qn += __popc(m);
+          if (qn >= 32) {
+            __syncwarp();
+            const u64 u = wq[qn - 32 + lane];
+            __syncwarp();
+            qn -= 32;
+            resolve(true, u);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    const u64 u = (u32)lane < qn ? wq[lane] : 0ull;
+    __syncwarp();
+    resolve((u32)lane < qn, u);
+  }
+  __syncthreads();
+  // head and tail keys (< KPV each, CTA 0): the table, else extra cells
+  if (c == 0 && wid == 1) {
+    const u64 tail0 = head + body;
+    const bool hv = (u64)lane < head, tv = (u64)lane < n - tail0;
+    for (int r = 0; r < 2; ++r) {
+      const bool act = r == 0 ? hv : tv;
+      const u64 u = act ? key_map<KK>(xk[r == 0 ? lane : tail0 + lane], flip) : 0ull;
+      bool done = !act;
+      const u32 t = hp_t(u);
+      const u32 bk[2] = {hp_b1(t), hp_b2(t)};
+      for (int d = 0; d < 2 && !done; ++d) {
+        const u64 mk = hp_marker(a, bk[d]);
+        for (int s2 = 0; s2 < 2 && !done; ++s2) {
+          const u32 slot = 2 * bk[d] + s2;
+          u64 k = atomicCAS(&tkeys[slot], mk, u);
+          if (k == mk) k = u;
+          if (k == u) { atomicAdd(&tcnt[slot], 1u); done = true; }
+        }
+      }
+      if (!done) extra_k[atomicAdd(&ncell_extra, 1u)] = u;
+    }
+  }
+  __syncthreads();
+
+  // ---- tail 1: the cells, counting-sorted by partition into this CTA's region ----
+  u64* stk = (u64*)smem;                                   // staging keys [kHpCellCap]
+  u32* stw = (u32*)(smem + (size_t)kHpCellCap * 8);        // staging counts
+  for (u32 i = tid; i <= kHpP; i += kHpThreads) lhist[i] = 0;
+  __syncthreads();
+  constexpr int kCpt = kHpS / kHpThreads;  // slots per thread
+  u32 cp[kCpt + 1], cr[kCpt + 1];
+#pragma unroll
+  for (int j = 0; j < kCpt; ++j) {
+    const u32 slot = tid + j * kHpThreads;
+    const u64 k = tkeys[slot];
+    cp[j] = kHpP;
+    if (k != hp_marker(a, slot >> 1)) {
+      cp[j] = hp_part(k, plo, psh, pmap);
+      cr[j] = atomicAdd(&lhist[cp[j]], 1u);
+    }
+  }
+  cp[kCpt] = kHpP;
+  if ((u32)tid < ncell_extra) {
+    cp[kCpt] = hp_part(extra_k[tid], plo, psh, pmap);
+    cr[kCpt] = atomicAdd(&lhist[cp[kCpt]], 1u);
+  }
+  __syncthreads();
+  if (wid == 0) hp_scan512(lhist, lstart);
+  else if (wid == 1) hp_scan512(shist, hstart);  // the spill's histogram, taken while spilling
+  __syncthreads();
+  const u32 ncells = lstart[kHpP];
+#pragma unroll
+  for (int j = 0; j <= kCpt; ++j) {
+    if (cp[j] < (u32)kHpP) {
+      const u32 pos = lstart[cp[j]] + cr[j];
+      if (j < kCpt) {
+        const u32 slot = tid + j * kHpThreads;
+        stk[pos] = tkeys[slot];
+        stw[pos] = tcnt[slot];
+      } else {
+        stk[pos] = extra_k[tid];
+        stw[pos] = 1;
+      }
+    }
+  }
+  for (u32 i = tid; i <= kHpP; i += kHpThreads) {
+    a.cpofs[(size_t)c * (kHpP + 1) + i] = lstart[i];
+    a.spofs[(size_t)c * (kHpP + 1) + i] = hstart[i];
+  }
+  for (u32 i = tid; i < kHpP; i += kHpThreads) written[i] = 0;
+  __syncthreads();
+  for (u32 i = tid; i < ncells; i += kHpThreads) {
+    a.cellk[(size_t)c * kHpCellCap + i] = stk[i];
+    a.cellw[(size_t)c * kHpCellCap + i] = stw[i];
+  }
+  // ---- tail 2: the spill, chunk by chunk ----
+  const u32 ns = sfill;
+  K* stv = (K*)smem;                                                     // staged keys
+  unsigned short* stp = (unsigned short*)(smem + (size_t)kHpChunk * 8);  // their partitions
+  K* outp = (K*)a.part + head + r0;
+  for (u32 ch = 0; ch < ns; ch += kHpChunk) {
+    const u32 cn = ns - ch < (u32)kHpChunk ? ns - ch : (u32)kHpChunk;
+    __syncthreads();
+    for (u32 i = tid; i <= kHpP; i += kHpThreads) lhist[i] = 0;
+    __syncthreads();
+    constexpr int kSpt = kHpChunk / kHpThreads;
+    K kv[kSpt];
+    u32 pp[kSpt], rr[kSpt];
+#pragma unroll
+    for (int j = 0; j < kSpt; ++j) {
+      const u32 i = tid + j * kHpThreads;
+      pp[j] = kHpP;
+      if (i < cn) {
+        kv[j] = *((volatile K*)&xb[r0 + ch + i]);
+        pp[j] = hp_part(key_map<KK>(kv[j], flip), plo, psh, pmap);
+        rr[j] = atomicAdd(&lhist[pp[j]], 1u);
+      }
+    }
+    __syncthreads();
+    if (wid == 0) hp_scan512(lhist, lstart);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSpt; ++j) {
+      if (pp[j] < (u32)kHpP) {
+        const u32 pos = lstart[pp[j]] + rr[j];
+        stv[pos] = kv[j];
+        stp[pos] = (unsigned short)pp[j];
+      }
+    }
+    __syncthreads();
+    for (u32 i = tid; i < cn; i += kHpThreads) {
+      const u32 p = stp[i];
+      outp[hstart[p] + written[p] + (i - lstart[p])] = stv[i];
+    }
+    __syncthreads();
+    for (u32 i = tid; i < kHpP; i += kHpThreads) written[i] += lhist[i];
+  }
+  if (tid == 0 && ns) atomicAdd(&a.ctl->g_updates, (u64)ns);
+}
+
+// ---- hp_reduce: one CTA per partition ----
+// The partition's items are the segments [cpofs[c][p], cpofs[c][p+1]) of every
+// CTA c's cells and [spofs[c][p], spofs[c][p+1]) of its spill, read as one flat
+// list (a segment table in shared memory), a warp per segment with kRdUnroll
+// loads per lane in flight.  Output:
+// the partition's sorted distinct keys and counts in its staging slot, and its
+// (pairs, rows) in pd / pr for hp_place.
+constexpr int kRdUnroll = 4;
+template <int KK>
+__global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 G) {
+  pdl_begin();
+  if (!gate_open(a.ctl, a.gate)) return;
+  using K = typename KeyT<KK>::T;
+  constexpr int KPV = 16 / sizeof(K);
+  constexpr u64 SKK = (u64)kHpStageWords * 8 / sizeof(K);
+  extern __shared__ __align__(128) unsigned char smem[];
+  u64* hk = (u64*)smem;                        // [kHpPartSlots]
+  u32* hc = (u32*)(hk + kHpPartSlots);         // [kHpPartSlots]
+  u64* lk = (u64*)(hc + kHpPartSlots);         // [kHpListCap]
+  u64* lc = lk + kHpListCap;                   // [kHpListCap]
+  __shared__ u32 segs[2 * 160 + 1];            // flat start of segment j (cells, then spill)
+  __shared__ u32 sbeg[2 * 160];                // its first index in the source array
+  __shared__ u32 claims, nd, ovf;
+  __shared__ unsigned long long sent;
+  __shared__ u64 wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u32 p = blockIdx.x;
+  for (u32 i = tid; i < kHpPartSlots; i += kHpThreads) { hk[i] = kEmpty; hc[i] = 0; }
+  if (tid == 0) { claims = 0; nd = 0; ovf = 0; sent = 0; }
+  const u64 n = a.n;
+  const u64 mis = (((uintptr_t)a.x) & 15) / sizeof(K);
+  const u64 head0 = mis ? (u64)KPV - mis : 0;
+  const u64 head = head0 < n ? head0 : n;
+  const u64 body = (n - head) / KPV * KPV;
+  const K* part = (const K*)a.part + head;
+  // segment table: j < G cells of CTA j, G <= j < 2G spill of CTA j - G
+  u32 len = 0;
+  if ((u32)tid < 2 * G) {
+    const bool cell = (u32)tid < G;
+    const u32 c = cell ? tid : tid - G;
+    const u32* o = (cell ? a.cpofs : a.spofs) + (size_t)c * (kHpP + 1);
+    const u32 b0 = o[p], b1 = o[p + 1];
+    len = b1 - b0;
+    u64 r0 = 0, r1;
+    if (!cell) hp_range(body, SKK, c, G, &r0, &r1);
+    sbeg[tid] = cell ? b0 : (u32)(r0 + b0);  // spill: index into part (CTA range + segment)
+  }
+  u32 inc = len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    u64 w = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u64 t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    wsum[lane] = w;
+  }
+  __syncthreads();
+  if ((u32)tid <= 2 * G) segs[tid] = inc - len + (wid ? (u32)wsum[wid - 1] : 0u);
+  __syncthreads();
+  const u32 nseg = 2 * G, total = segs[nseg];
+
+  auto insert = [&](u64 k, u32 w) {
+    if (k == kEmpty) { atomicAdd(&sent, (unsigned long long)w); return; }
+    u32 h = (u32)((k * kGamma) >> (64 - 12));
+    for (u32 pr = 0; pr < kHpPartSlots; ++pr) {
+      u64 cur = *((volatile u64*)&hk[h]);
+      if (cur == kEmpty) {
+        if (*((volatile u32*)&claims) >= kHpPartCap) { ovf = 1; return; }
+        cur = atomicCAS(&hk[h], kEmpty, k);
+        if (cur == kEmpty) { atomicAdd(&claims, 1u); cur = k; }
+      }
+      if (cur == k) { atomicAdd(&hc[h], w); return; }
+      h = (h + 1) & (kHpPartSlots - 1);
+    }
+    ovf = 1;
+  };
+  // warp per segment: lanes read consecutive items, kRdUnroll per lane in flight
+  for (u32 j = wid; j < nseg; j += 32) {
+    const u32 len_j = segs[j + 1] - segs[j], b = sbeg[j];
+    const bool cell = j < G;
+    for (u32 i0 = lane; i0 < len_j; i0 += 32 * kRdUnroll) {
+      u64 k[kRdUnroll];
+      u32 w[kRdUnroll];
+#pragma unroll
+      for (int r = 0; r < kRdUnroll; ++r) {
+        const u32 i = i0 + r * 32;
+        w[r] = 0;
+        if (i < len_j) {
+          if (cell) {
+            k[r] = a.cellk[(size_t)j * kHpCellCap + b + i];
+            w[r] = a.cellw[(size_t)j * kHpCellCap + b + i];
+          } else {
+            k[r] = key_map<KK>(part[b + i], a.flip);
+            w[r] = 1;
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kRdUnroll; ++r)
+        if (w[r]) insert(k[r], w[r]);
+    }
+  }
+  __syncthreads();
+  // compact the distinct keys (order is irrelevant: they are sorted next)
+  for (u32 j = tid; j < kHpPartSlots; j += kHpThreads) {
+    const u64 kk = hk[j];
+    if (kk != kEmpty) {
+      const u32 q = atomicAdd(&nd, 1u);
+      if (q < kHpListCap) { lk[q] = kk; lc[q] = hc[j]; }
+    }
+  }
+  __syncthreads();
+  const bool bad = ovf || nd > kHpPartCap;
+  const u32 d = bad ? 0u : nd;
+  if (d <= kHpThreads) {
+    // rank sort (the keys are distinct): thread t moves key t to the number
+    // of keys below it; every step reads one key by broadcast
+    u64 mk = 0, mc = 0;
+    u32 rank = 0;
+    if ((u32)tid < d) {
+      mk = lk[tid];
+      mc = lc[tid];
+#pragma unroll 8
+      for (u32 j = 0; j < d; ++j) rank += lk[j] < mk ? 1u : 0u;
+    }
+    __syncthreads();
+    if ((u32)tid < d) { lk[rank] = mk; lc[rank] = mc; }
+    __syncthreads();
+  } else {
+    // bitonic sort (padded to a power of two with ~0)
+    u32 np2 = 1;
+    while (np2 < d) np2 <<= 1;
+    for (u32 j = d + tid; j < np2; j += kHpThreads) { lk[j] = kEmpty; lc[j] = 0; }
+    __syncthreads();
+    for (u32 k2 = 2; k2 <= np2; k2 <<= 1) {
+      for (u32 j = k2 >> 1; j > 0; j >>= 1) {
+        for (u32 q = tid; q < np2; q += kHpThreads) {
+          const u32 l = q ^ j;
+          if (l > q) {
+            const u64 ki = lk[q], kl = lk[l];
+            const bool up = (q & k2) == 0;
+            if ((ki > kl) == up) {
+              lk[q] = kl; lk[l] = ki;
+              const u64 t = lc[q]; lc[q] = lc[l]; lc[l] = t;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // the sentinel key ~0 (the largest) goes last
+  const u64 snt = bad ? 0ull : (u64)sent;
+  const u32 dd = d + (snt ? 1u : 0u);
+  if (tid == 0 && snt) { lk[d] = kEmpty; lc[d] = snt; }
+  __syncthreads();
+  u64 rows = 0;
+  u64* sk = a.pk_stage + (size_t)p * kHpStage;
+  u64* sc = a.pc_stage + (size_t)p * kHpStage;
+  for (u32 j = tid; j < dd; j += kHpThreads) {
+    sk[j] = lk[j];
+    sc[j] = lc[j];
+    rows += lc[j];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rows += __shfl_xor_sync(0xffffffffu, rows, o);
+  __syncthreads();
+  if (lane == 0) wsum[wid] = rows;
+  __syncthreads();
+  if (tid == 0) {
+    u64 r = 0;
+    for (int w2 = 0; w2 < 32; ++w2) r += wsum[w2];
+    a.pd[p] = dd;
+    a.pr[p] = r;
+    if (bad) atomicExch((unsigned*)&a.ctl->hp_overflow, 1u);
+  }
+}
+
+// ---- hp_place: the partitions' staged pairs -> their global positions ----
+// Block p sums (pairs, rows) of the partitions before it, copies its pairs to
+// pk / pc and writes their emit offsets; the last block publishes the totals.
+__global__ void __launch_bounds__(256) hp_place_kernel(HpArgs a) {
+  pdl_begin();
+  if (!gate_open(a.ctl, a.gate)) return;
+  __shared__ u64 wd[8], wr[8], wsc[8];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u32 p = blockIdx.x;
+  u64 d0 = 0, r0 = 0;
+  for (u32 q = tid; q < p; q += 256) { d0 += a.pd[q]; r0 += a.pr[q]; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+    r0 += __shfl_xor_sync(0xffffffffu, r0, o);
+  }
+  if (lane == 0) { wd[wid] = d0; wr[wid] = r0; }
+  __syncthreads();
+  u64 D = 0, R = 0;
+#pragma unroll
+  for (int w2 = 0; w2 < 8; ++w2) { D += wd[w2]; R += wr[w2]; }
+  const u32 dd = (u32)a.pd[p];
+  const u64* sk = a.pk_stage + (size_t)p * kHpStage;
+  const u64* sc = a.pc_stage + (size_t)p * kHpStage;
+  u64 run = R;
+  for (u32 b0 = 0; b0 < dd; b0 += 256) {
+    const u32 i = b0 + tid;
+    const u64 cnt = i < dd ? sc[i] : 0;
+    u64 inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u64 t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsc[wid] = inc;
+    __syncthreads();
+    u64 before = 0, all = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < 8; ++w2) {
+      before += w2 < wid ? wsc[w2] : 0;
+      all += wsc[w2];
+    }
+    if (i < dd) {
+      a.pk[D + i] = sk[i];
+      a.pc[D + i] = cnt;
+      a.poffs[D + i] = run + before + inc - cnt;
+    }
+    run += all;
+    __syncthreads();
+  }
+  if (p == gridDim.x - 1 && tid == 0) {
+    const u64 tot_d = D + dd, tot_r = run;
+    const bool bad = *((volatile u32*)&a.ctl->hp_overflow) != 0;
+    a.poffs[tot_d] = tot_r;
+    a.ctl->npairs = tot_d;
+    a.ctl->total = tot_r;
+    a.ctl->sum_error = !bad && tot_r != a.n;
+    a.ctl->pairs_ready = !bad && tot_r == a.n;
+  }
+}
+
+// The recovery after a partition overflow: every CTA's rows are exactly its
+// spill plus its cells (CTA 0's also hold the unaligned head and tail keys),
+// so each CTA writes them back over its own range of the column, which the
+// general fallback sort then sorts.
+template <int KK>
+__global__ void __launch_bounds__(1024) hp_restore_kernel(HpArgs a, u32 G) {
+  using K = typename KeyT<KK>::T;
+  constexpr int KPV = 16 / sizeof(K);
+  constexpr u64 SKK = (u64)kHpStageWords * 8 / sizeof(K);
+  __shared__ u64 woff[1025];
+  const u32 c = blockIdx.x;
+  const int tid = threadIdx.x;
+  const u64 n = a.n;
+  const u64 mis = (((uintptr_t)a.x) & 15) / sizeof(K);
+  const u64 head0 = mis ? (u64)KPV - mis : 0;
+  const u64 head = head0 < n ? head0 : n;
+  const u64 body = (n - head) / KPV * KPV;
+  const u64 tail0 = head + body;
+  u64 r0, r1;
+  hp_range(body, SKK, c, G, &r0, &r1);
+  K* x = (K*)a.x;
+  const u64 span = r1 - r0;
+  auto pos = [&](u64 q) -> u64 {  // q-th row of this CTA -> its index in the column
+    if (q < span) return head + r0 + q;
+    q -= span;
+    return q < head ? q : tail0 + (q - head);
+  };
+  const u32 ns = a.spofs[(size_t)c * (kHpP + 1) + kHpP];
+  const u32 nc = a.cpofs[(size_t)c * (kHpP + 1) + kHpP];
+  const K* src = (const K*)a.part + head + r0;
+  for (u32 i = tid; i < ns; i += blockDim.x) x[pos(i)] = src[i];
+  const u64* ck = a.cellk + (size_t)c * kHpCellCap;
+  const u32* cw = a.cellw + (size_t)c * kHpCellCap;
+  u64 base = ns;
+  for (u32 c0 = 0; c0 < nc; c0 += 1024) {
+    const u32 m = nc - c0 < 1024u ? nc - c0 : 1024u;
+    if (tid == 0) {
+      u64 run = base;
+      for (u32 j = 0; j < m; ++j) { woff[j] = run; run += cw[c0 + j]; }
+      woff[m] = run;
+    }
+    __syncthreads();
+    for (u32 j = 0; j < m; ++j) {
+      const K k = key_unmap<KK>(ck[c0 + j], a.flip);
+      for (u64 q = woff[j] + tid; q < woff[j + 1]; q += blockDim.x) x[pos(q)] = k;
+    }
+    base = woff[m];
+    __syncthreads();
+  }
+}
+
+// ---- host side ----
+static void hp_markers(u64* e0, u64* e1, u32* ma, u32* mb) {
+  const u64 E0 = 0x5DEECE66D1234567ull;
+  const u32 t0 = hp_t(E0), a0 = hp_b1(t0), b0 = hp_b2(t0);
+  u64 E1 = E0;
+  for (u64 t = 1;; ++t) {
+    E1 = E0 + t * 0x9E3779B97F4A7C15ull;
+    const u32 t1 = hp_t(E1), a1 = hp_b1(t1), b1 = hp_b2(t1);
+    if (a1 != a0 && a1 != b0 && b1 != a0 && b1 != b0) break;
+  }
+  *e0 = E0;
+  *e1 = E1;
+  *ma = a0;
+  *mb = b0;
+}
+
+int hp_grid(u64 n, int kk, int num_sms) {
+  const u64 skk = (u64)kHpStageWords * 8 / (kk ? 4 : 8);
+  const u64 chunks = (n + skk - 1) / skk;
+  const u64 g = num_sms < 160 ? (u64)num_sms : 160;  // hp_reduce's segment table holds 2 x 160
+  return (int)(chunks < g ? (chunks ? chunks : 1) : g);
+}
+
+size_t hp_scratch_bytes(int num_sms) {
+  return (size_t)num_sms * kHpCellCap * 12 + (size_t)num_sms * (kHpP + 1) * 8 + kHpP * 16 + 16;
+}
+
+// G: the count's grid (the scratch is laid out per CTA of it)
+static HpArgs hp_args(const HpBufs& b, const void* x, u64 n, u64 flip, DevCtl* ctl, u64* pk,
+                      u64* pc, u64* poffs, int gate, int G) {
+  HpArgs a{};
+  a.x = x;
+  a.n = n;
+  a.flip = flip;
+  a.ctl = ctl;
+  a.part = b.part;
+  char* s = (char*)b.scratch;
+  a.cellk = (u64*)s;
+  s += (size_t)G * kHpCellCap * 8;
+  a.cellw = (u32*)s;
+  s += (size_t)G * kHpCellCap * 4;
+  a.cpofs = (u32*)s;
+  s += (size_t)G * (kHpP + 1) * 4;
+  a.spofs = (u32*)s;
+  s += (size_t)G * (kHpP + 1) * 4;
+  a.pd = (u64*)(((uintptr_t)s + 7) & ~(uintptr_t)7);
+  a.pr = a.pd + kHpP;
+  a.pk_stage = b.pk_stage;
+  a.pc_stage = b.pc_stage;
+  a.pk = pk;
+  a.pc = pc;
+  a.poffs = poffs;
+  hp_markers(&a.e0, &a.e1, &a.ma, &a.mb);
+  a.gate = gate;
+  return a;
+}
+
+template <typename F>
+static cudaError_t hp_attr(F* f, size_t smem) {
+  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <int KK>
+static cudaError_t hp_launch_t(const HpArgs& a, int G, cudaStream_t st) {
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = hp_attr(hp_count_kernel<KK>, kHpCountSmem);
+    if (e == cudaSuccess) e = hp_attr(hp_reduce_kernel<KK>, kHpReduceSmem);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  cudaError_t e = launch_pdl(kPdlCount, hp_count_kernel<KK>, G, kHpThreads, kHpCountSmem, st, a);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(kPdlCount, hp_reduce_kernel<KK>, kHpP, kHpThreads, kHpReduceSmem, st, a, (u32)G);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(kPdlCount, hp_place_kernel, kHpP, 256, 0, st, a);
+}
+
+cudaError_t launch_hp_count(const HpBufs& b, const void* x, u64 n, u64 flip, DevCtl* ctl,
+                            u64* pk, u64* pc, u64* poffs, int num_sms, cudaStream_t st, int gate,
+                            int kk) {
+  const int G = hp_grid(n, kk, num_sms);
+  const HpArgs a = hp_args(b, x, n, flip, ctl, pk, pc, poffs, gate, G);
+  if (kk == 1) return hp_launch_t<1>(a, G, st);
+  if (kk == 2) return hp_launch_t<2>(a, G, st);
+  return hp_launch_t<0>(a, G, st);
+}
+
+void launch_hp_restore(const HpBufs& b, void* x, u64 n, u64 flip, int num_sms, cudaStream_t st,
+                       int kk) {
+  const int G = hp_grid(n, kk, num_sms);
+  const HpArgs a = hp_args(b, x, n, flip, nullptr, nullptr, nullptr, nullptr, kGateNone, G);
+  if (kk == 1) hp_restore_kernel<1><<<G, 1024, 0, st>>>(a, (u32)G);
+  else if (kk == 2) hp_restore_kernel<2><<<G, 1024, 0, st>>>(a, (u32)G);
+  else hp_restore_kernel<0><<<G, 1024, 0, st>>>(a, (u32)G);
+}
+
+}  // namespace cafs

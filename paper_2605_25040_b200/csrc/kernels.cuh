@@ -11,8 +11,10 @@ constexpr u64 kExpectCtlN = ~0ull - 1;  // pair-sort `expect`: the sharded colum
 
 // estimate.cu
 // `kk`: key kind (common.cuh): 0 = 64-bit, 1 = int32, 2 = uint32
+// opts: kEstHp (the partitioned count may run), kEstNoWindow (no dense window)
+enum : int { kEstHp = 1, kEstNoWindow = 2 };
 void launch_estimate(const void* x, u64 n, u64 flip, int check_prefix, DevCtl* ctl,
-                     cudaStream_t st, int kk = 0);
+                     cudaStream_t st, int kk = 0, int opts = 0);
 void launch_monotone_scan(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
                           cudaStream_t st, int kk = 0);
 void launch_estimate_sharded(const u64* samples, const u64* ghdr, int world, DevCtl* ctl,
@@ -47,6 +49,18 @@ void launch_insert_pairs(const u64* keys, const u64* cnts, u64 m, u64 mult, DevC
                          u64* gkeys, u64* gcnt, u32* glist, int num_sms, cudaStream_t st);
 void launch_compact(DevCtl* ctl, u64* gkeys, u64* gcnt, const u32* glist, u64* pkeys, u64* pcnt,
                     int num_sms, cudaStream_t st, int gate);
+// hashpart.cu: the partitioned count (no dense window) -> sorted pairs
+struct HpBufs {
+  void* part;     // partitioned spill: n keys of the column's type
+  void* scratch;  // hp_scratch_bytes(num_sms): cells, segment tables, partition totals
+  u64* pk_stage;  // kHpParts x 4097 staged pairs (keys, counts)
+  u64* pc_stage;
+};
+size_t hp_scratch_bytes(int num_sms);
+cudaError_t launch_hp_count(const HpBufs& b, const void* x, u64 n, u64 flip, DevCtl* ctl, u64* pk,
+                            u64* pc, u64* poffs, int num_sms, cudaStream_t st, int gate, int kk);
+void launch_hp_restore(const HpBufs& b, void* x, u64 n, u64 flip, int num_sms, cudaStream_t st,
+                       int kk);
 // emit.cu
 void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl, void* out,
                  u64 begin, u64 end, u64 flip, int num_sms, cudaStream_t st, u64 npairs_bound,
