@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define CAFS_ABI_VERSION 1
+#define CAFS_ABI_VERSION 2
 #define CAFS_TINY_MAX_KEYS 8      /* sorter.py:30  TINY_MAX_KEYS */
 #define CAFS_SMALL_N_CUTOFF 2048  /* sorter.py:29  SMALL_N_CUTOFF */
 #define CAFS_SAMPLE_TARGET 1024   /* cardinality.py:26 */
@@ -113,7 +113,18 @@ typedef struct {
   int32_t ref_guard_fired;       /* 2 * ref_spill_len > n (sorter.py:264) */
   uint64_t ref_spill_len, ref_updates, ref_hits, ref_claims, ref_spill_pushes;
   uint64_t ref_counted_total;
+  int32_t count_path;            /* cafs_count_path_t: how the column was counted */
+  int32_t _reserved;
 } cafs_telemetry_t;
+
+/* cafs_telemetry_t.count_path (B200-side; the reference has one bucket table) */
+typedef enum {
+  CAFS_COUNT_NONE = 0,         /* no count: sorted input or a fallback route */
+  CAFS_COUNT_TINY = 1,         /* tiny route: <= 8 sampled keys, one pass */
+  CAFS_COUNT_DENSE = 2,        /* main route: dense key window (dictionary codes) */
+  CAFS_COUNT_TABLE = 3,        /* main route: CTA tables + the global (L2) hash table */
+  CAFS_COUNT_PARTITIONED = 4   /* main route: CTA tables + key-range partitions (hashpart.cu) */
+} cafs_count_path_t;
 
 typedef struct cafs_ctx cafs_ctx_t;
 

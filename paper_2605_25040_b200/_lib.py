@@ -47,7 +47,8 @@ class Telemetry(ctypes.Structure):
                 ("ref_guard_fired", ctypes.c_int32), ("ref_spill_len", ctypes.c_uint64),
                 ("ref_updates", ctypes.c_uint64), ("ref_hits", ctypes.c_uint64),
                 ("ref_claims", ctypes.c_uint64), ("ref_spill_pushes", ctypes.c_uint64),
-                ("ref_counted_total", ctypes.c_uint64)]
+                ("ref_counted_total", ctypes.c_uint64), ("count_path", ctypes.c_int32),
+                ("_reserved", ctypes.c_int32)]
 
 
 # every symbol include/cafs_b200.h declares, with its ctypes signature

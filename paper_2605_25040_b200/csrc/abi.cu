@@ -784,7 +784,8 @@ int main_finish(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cafs_telemetry_t* tel
                 StageTimer& tm, cudaStream_t st, bool* emitted, int kk = 0) {
   DevCtl& c = *ctx->h_ctl;
   tel->global_updates = c.g_updates;
-  if (getenv("CAFS_DEBUG"))
+  static const bool debug = getenv("CAFS_DEBUG") != nullptr;
+  if (debug)
     fprintf(stderr, "[cafs] route=%d eff=%d hp_ok=%d hp_ovf=%u range_len=%u npairs=%llu total=%llu ready=%d need_large=%d ovf=%d k_hat=%f\n",
             c.route, c.eff_route, c.hp_ok, c.hp_overflow, c.range_len, (unsigned long long)c.npairs,
             (unsigned long long)c.total, c.pairs_ready, c.need_large, c.overflow, c.k_hat);
@@ -1224,6 +1225,11 @@ static int sort_impl(cafs_ctx_t* ctx, void* d_x, uint64_t n, int is_signed, uint
       break;
   }
   if (rc != CAFS_OK) return rc;
+  if (tiny_ran && !c.tiny_failed) tel->count_path = CAFS_COUNT_TINY;
+  else if (main_ran)
+    tel->count_path = c.range_len > 0 ? CAFS_COUNT_DENSE
+                      : c.hp_ok       ? CAFS_COUNT_PARTITIONED
+                                      : CAFS_COUNT_TABLE;
   CK(cudaStreamSynchronize(st));
   tm.finish(tiny_ran, main_ran, emitted);
   if (exact && !main_ran) {

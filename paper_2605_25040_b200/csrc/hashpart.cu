@@ -48,44 +48,37 @@
 namespace cafs {
 
 constexpr int kHpThreads = 1024;
-constexpr int kHpConsumers = kHpThreads - 32;
-constexpr int kHpStages = 3;
-constexpr int kHpStageWords = 3968;  // 31 KB per stage; 2 vectors per consumer thread
-constexpr int kHpVpt = kHpStageWords / 2 / kHpConsumers;
-static_assert(kHpVpt * kHpConsumers * 2 == kHpStageWords, "balanced stages");
-constexpr int kHpSLog2 = 13;
-constexpr u32 kHpS = 1u << kHpSLog2;      // table slots
+constexpr int kHpUnroll = 4;                 // 16-byte loads in flight per thread
+constexpr u64 kHpRound = (u64)kHpUnroll * kHpThreads;  // vectors per CTA round
+constexpr int kHpSLog2 = 14;
+constexpr u32 kHpS = 1u << kHpSLog2;         // table slots
+constexpr u32 kHpNB = kHpS / 2;              // 2-slot buckets
 constexpr int kHpNBLog2 = kHpSLog2 - 1;
-constexpr u32 kHpNB = 1u << kHpNBLog2;    // 2-slot buckets
+constexpr int kHpD = 2;                      // buckets a key may sit in (home + 1)
 constexpr u32 kHpFullClaims = kHpS - kHpS / 16;  // from here on a miss spills without probing
-constexpr int kHpQ = 64;                  // per-warp claim queue
-constexpr int kHpP = kHpParts;            // key-range partitions
-constexpr int kHpFine = 4096;             // fine bins of the partition map
-constexpr u32 kHpCellCap = kHpS + 16;     // cells per CTA (+ CTA 0's head / tail keys)
-constexpr int kHpChunk = 8192;            // tail scatter chunk (spilled keys)
-constexpr u32 kHpPartSlots = 4096;        // hp_reduce exact table
-constexpr u32 kHpPartCap = 2048;          // distinct keys per partition (load <= 1/2)
+constexpr int kHpQ = 64;                     // per-warp miss queue
+constexpr int kHpP = kHpParts;               // key-range partitions
+constexpr int kHpFine = 2048;                // fine bins of the partition map
+constexpr u32 kHpCellCap = kHpS + 16;        // cells per CTA (+ CTA 0's head / tail keys)
+constexpr int kHpChunk = 8192;               // tail scatter chunk (spilled keys)
+constexpr u32 kHpPartSlots = 4096;           // hp_reduce exact table
+constexpr u32 kHpPartCap = 2048;             // distinct keys per partition (load <= 1/2)
 constexpr u32 kHpListCap = kHpPartCap + kHpThreads;  // claims may overshoot by one per thread
-constexpr u32 kHpStage = kHpPartCap + 1;  // staged pairs per partition (+ the ~0 sentinel)
+constexpr u32 kHpStage = kHpPartCap + 1;     // staged pairs per partition (+ the ~0 sentinel)
 static_assert(kHpP == 512, "scans below are written for 512 partitions");
 
-constexpr size_t kHpRingBytes = (size_t)kHpStages * kHpStageWords * 8;
 constexpr size_t kHpQueueBytes = (size_t)32 * kHpQ * 8;
-constexpr size_t kHpStagingBytes = kHpRingBytes + kHpQueueBytes;  // tail staging (ring + queues)
-constexpr size_t kHpCountSmem =
-    kHpStagingBytes + (size_t)kHpS * 12 + 2 * kHpStages * 8 + (size_t)kHpFine * 2;
-static_assert((size_t)kHpCellCap * 12 <= kHpStagingBytes, "cell staging");
-static_assert((size_t)kHpChunk * 10 <= kHpStagingBytes, "spill staging");
-static_assert(kHpCountSmem + 12288 <= 232448, "shared memory budget");
+constexpr size_t kHpCountSmem = (size_t)kHpS * 12 + kHpQueueBytes + (size_t)kHpFine * 2;
+static_assert((size_t)kHpChunk * 10 + kHpP * 4 <= (size_t)kHpS * 12, "spill staging");
+static_assert(kHpCountSmem + 11 * 1024 <= 232448, "shared memory budget");
 constexpr size_t kHpReduceSmem = (size_t)kHpPartSlots * 12 + (size_t)kHpListCap * 16;
 
-// the two candidate buckets of a key (a cache of partial counts: a weak hash
-// costs spills, never correctness)
+// the home bucket of a key (a cache of partial counts: a weak hash costs
+// spills, never correctness)
 __host__ __device__ __forceinline__ u32 hp_t(u64 v) {
   return (u32)(v >> 32) * 0x9E3779B1u + (u32)v;
 }
 __host__ __device__ __forceinline__ u32 hp_b1(u32 t) { return (t * 0x85EBCA77u) >> (32 - kHpNBLog2); }
-__host__ __device__ __forceinline__ u32 hp_b2(u32 t) { return (t * 0xC2B2AE3Du) >> (32 - kHpNBLog2); }
 
 struct HpArgs {
   const void* x;   // column (keys of kind KK); its streamed part receives the spill
@@ -104,13 +97,13 @@ struct HpArgs {
   u64* pk;         // sorted pairs: keys, counts, offsets (npairs + 1)
   u64* pc;
   u64* poffs;
-  u64 e0, e1;      // empty-slot markers: e1 in E0's two buckets ma, mb, e0 elsewhere
-  u32 ma, mb;
+  u64 e0, e1;      // empty-slot markers: e1 in E0's kHpD buckets from ma, e0 elsewhere
+  u32 ma;
   int gate;
 };
 
 __device__ __forceinline__ u64 hp_marker(const HpArgs& a, u32 b) {
-  return (b == a.ma || b == a.mb) ? a.e1 : a.e0;
+  return ((b - a.ma) % kHpNB) < (u32)kHpD ? a.e1 : a.e0;
 }
 
 // Partition of a key: its fine bin over the sample span, mapped (pmap).
@@ -147,24 +140,30 @@ __device__ __forceinline__ void hp_scan512(const u32* in, u32* out) {
   if (lane == 31) out[512] = run;
 }
 
+// The spill of warp w lives in the vectors w itself has streamed: its j-th
+// spilled key goes to chunk j / (32 * KPV) of its own (round, unroll) chunks.
+template <int KPV>
+__device__ __forceinline__ u64 hp_spill_pos(u64 v0, u32 w, u32 j) {
+  const u32 ci = j / (32 * KPV), within = j % (32 * KPV);
+  const u32 r = ci / kHpUnroll, q = ci % kHpUnroll;
+  return (v0 + (u64)r * kHpRound + (u64)q * kHpThreads + (u64)w * 32) * KPV + within;
+}
+
 template <int KK>
 __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
   pdl_begin();
   if (!gate_open(a.ctl, a.gate)) return;
   using K = typename KeyT<KK>::T;
-  constexpr int KPV = 16 / sizeof(K);                    // keys per 16-byte vector
-  constexpr u64 SKK = (u64)kHpStageWords * 8 / sizeof(K);  // keys per stage
+  constexpr int KPV = 16 / sizeof(K);  // keys per 16-byte vector
+  constexpr int KPT = kHpUnroll * KPV;  // keys per thread per round
   extern __shared__ __align__(128) unsigned char smem[];
-  u64* ring = (u64*)smem;                                    // [stages][stage words]
-  u64* queue = (u64*)(smem + kHpRingBytes);                  // [32][kHpQ]
-  u64* tkeys = (u64*)(smem + kHpStagingBytes);               // [kHpS]
-  u32* tcnt = (u32*)(tkeys + kHpS);                          // [kHpS]
-  u64* full = (u64*)(tcnt + kHpS);
-  u64* empty = full + kHpStages;
-  unsigned short* pmap = (unsigned short*)(empty + kHpStages);  // [kHpFine]
+  u64* tkeys = (u64*)smem;                              // [kHpS]
+  u32* tcnt = (u32*)(tkeys + kHpS);                     // [kHpS]
+  u64* queue = (u64*)(tcnt + kHpS);                     // [32][kHpQ]
+  unsigned short* pmap = (unsigned short*)(queue + 32 * kHpQ);  // [kHpFine]
   __shared__ u32 shist[kHpP + 1], hstart[kHpP + 1], lhist[kHpP + 1], lstart[kHpP + 1];
-  __shared__ u32 written[kHpP];
-  __shared__ u32 sfill, ncell_extra, sclaims;
+  __shared__ u32 wsp[33];  // spilled keys per warp, then their prefix
+  __shared__ u32 ncell_extra, sclaims;
   __shared__ u64 extra_k[16];
   __shared__ u64 s_lo;
   __shared__ int s_sh;
@@ -178,27 +177,12 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
   const u64 head = head0 < n ? head0 : n;
   const u64 body = (n - head) / KPV * KPV;
   K* xb = (K*)(xk + head);
-  u64 r0, r1;
-  hp_range(body, SKK, c, G, &r0, &r1);
-  const u64 nst = (r1 - r0 + SKK - 1) / SKK;
+  const ulonglong2* xv = (const ulonglong2*)xb;
+  u64 v0, v1;  // this CTA's vectors (whole rounds)
+  hp_range(body / KPV, kHpRound, c, G, &v0, &v1);
 
-  if (tid == 0) {
-    for (int s = 0; s < kHpStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kHpConsumers / 32);
-    }
-    fence_mbar_init();
-    // the first stages go out before the prologue (the ring fills meanwhile)
-    for (u64 it = 0; it < nst && it < (u64)kHpStages; ++it) {
-      const u64 off = r0 + it * SKK;
-      const u32 bytes = (u32)(((r1 - off) < SKK ? (r1 - off) : SKK) * sizeof(K));
-      mbar_arrive_expect_tx(&full[it], bytes);
-      tma_load_1d(ring + it * kHpStageWords, xb + off, bytes, &full[it]);
-    }
-    sfill = 0;
-    ncell_extra = 0;
-    sclaims = 0;
-  }
+  if (tid == 0) { ncell_extra = 0; sclaims = 0; }
+  if (tid < 33) wsp[tid] = 0;
   // ---- prologue: partition map from the estimate's 1024 samples ----
   {
     const u64* samp = est_scratch(a.ctl)->samples;
@@ -235,10 +219,11 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
     const u64 d = (sv - s_lo) >> s_sh;
     atomicAdd(&fh[d < (u64)kHpFine ? (u32)d : kHpFine - 1], 1u);
     __syncthreads();
-    // exclusive scan of the 4096 bins: 4 per thread
-    u32 v4[4], s = 0;
+    // exclusive scan of the fine bins: kHpFine / 1024 per thread
+    constexpr int FPT = kHpFine / kHpThreads;
+    u32 vf[FPT], s = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) { v4[j] = fh[tid * 4 + j]; s += v4[j]; }
+    for (int j = 0; j < FPT; ++j) { vf[j] = fh[tid * FPT + j]; s += vf[j]; }
     u32 inc = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -260,12 +245,12 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
     __syncthreads();
     u32 run = inc - s + (wid ? ws[32 + wid - 1] : 0);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const u32 f = tid * 4 + j;
+    for (int j = 0; j < FPT; ++j) {
+      const u32 f = tid * FPT + j;
       // half sample mass, half span position (both monotone in f)
       const u32 p = (run * (kHpP / 2)) / kSampleTarget + (f * (kHpP / 2)) / kHpFine;
       pmap[f] = (unsigned short)(p < (u32)kHpP ? p : kHpP - 1);
-      run += v4[j];
+      run += vf[j];
     }
     __syncthreads();
   }
@@ -278,138 +263,110 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
   const u64 plo = s_lo;
   const int psh = s_sh;
   const u32 tbase = smem_u32(tkeys), cbase = smem_u32(tcnt);
+  u64* wq = queue + (size_t)wid * kHpQ;
+  u32 qn = 0;   // warp-uniform queue length
+  u32 nsw = 0;  // warp-uniform: keys this warp has spilled
 
   // 32 queued misses (one per active lane) with the whole warp: while the
-  // table has room, look again and claim an empty slot of either bucket;
-  // what remains is spilled into the streamed range
+  // table has room, look again in the key's kHpD buckets and claim an empty
+  // slot; what remains is spilled into vectors this warp has streamed
   auto resolve = [&](bool active, u64 u) {
     bool done = !active;
     if (*((volatile u32*)&sclaims) < kHpFullClaims && __any_sync(0xffffffffu, active)) {
-      if (active) {
-        const u32 t = hp_t(u);
-        const u32 bk[2] = {hp_b1(t), hp_b2(t)};
+      const u32 b = hp_b1(hp_t(u));
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          if (!done) {
-            const u32 bb = bk[r];
-            u64 t0, t1;
-            asm volatile("ld.volatile.shared.v2.u64 {%0,%1}, [%2];"
-                         : "=l"(t0), "=l"(t1) : "r"(smem_u32(&tkeys[2 * bb])));
-            const u64 mk = hp_marker(a, bb);
-            int hit = t0 == u ? 0 : (t1 == u ? 1 : -1);
-            if (hit < 0 && t0 == mk) {
-              const u64 o = atomicCAS(&tkeys[2 * bb], mk, u);
-              if (o == mk) atomicAdd(&sclaims, 1u);
-              if (o == mk || o == u) hit = 0;
-            }
-            if (hit < 0 && t1 == mk) {
-              const u64 o = atomicCAS(&tkeys[2 * bb + 1], mk, u);
-              if (o == mk) atomicAdd(&sclaims, 1u);
-              if (o == mk || o == u) hit = 1;
-            }
-            if (hit >= 0) { atomicAdd(&tcnt[2 * bb + hit], 1u); done = true; }
+      for (int d = 0; d < kHpD; ++d) {
+        if (!done) {
+          const u32 bb = (b + d) % kHpNB;
+          u64 t0, t1;
+          asm volatile("ld.volatile.shared.v2.u64 {%0,%1}, [%2];"
+                       : "=l"(t0), "=l"(t1) : "r"(tbase + bb * 16));
+          const u64 mk = hp_marker(a, bb);
+          int hit = t0 == u ? 0 : (t1 == u ? 1 : -1);
+          if (hit < 0 && t0 == mk) {
+            const u64 o = atomicCAS(&tkeys[2 * bb], mk, u);
+            if (o == mk) atomicAdd(&sclaims, 1u);
+            if (o == mk || o == u) hit = 0;
           }
+          if (hit < 0 && t1 == mk) {
+            const u64 o = atomicCAS(&tkeys[2 * bb + 1], mk, u);
+            if (o == mk) atomicAdd(&sclaims, 1u);
+            if (o == mk || o == u) hit = 1;
+          }
+          if (hit >= 0) { atomicAdd(&tcnt[2 * bb + hit], 1u); done = true; }
         }
       }
     }
     const bool sp = !done;
     const u32 m = __ballot_sync(0xffffffffu, sp);
     if (m) {
-      u32 base = 0;
-      if (lane == 0) base = atomicAdd(&sfill, (u32)__popc(m));
-      base = __shfl_sync(0xffffffffu, base, 0);
       if (sp) {
-        xb[r0 + base + __popc(m & lanemask_lt())] = key_unmap<KK>(u, flip);
+        xb[hp_spill_pos<KPV>(v0, wid, nsw + __popc(m & lanemask_lt()))] = key_unmap<KK>(u, flip);
         atomicAdd(&shist[hp_part(u, plo, psh, pmap)], 1u);
       }
+      nsw += __popc(m);
     }
   };
 
-  if (wid == 0) {
-    // ---- TMA producer (stages past the first kHpStages) ----
-    if (lane == 0) {
-      for (u64 it = kHpStages; it < nst; ++it) {
-        const u32 s = (u32)(it % kHpStages);
-        const u32 ph = (u32)((it / kHpStages) & 1);
-        mbar_wait(&empty[s], ph ^ 1);
-        const u64 off = r0 + it * SKK;
-        const u32 bytes = (u32)(((r1 - off) < SKK ? (r1 - off) : SKK) * sizeof(K));
-        mbar_arrive_expect_tx(&full[s], bytes);
-        tma_load_1d(ring + (size_t)s * kHpStageWords, xb + off, bytes, &full[s]);
+  for (u64 r0v = v0; r0v < v1; r0v += kHpRound) {  // CTA-uniform rounds
+    ulonglong2 w[kHpUnroll];
+    u32 vmask = 0;
+#pragma unroll
+    for (int q = 0; q < kHpUnroll; ++q) {
+      const u64 i = r0v + (u64)q * kHpThreads + tid;
+      w[q] = make_ulonglong2(0, 0);
+      if (i < v1) { w[q] = ld_stream_v2(xv + i); vmask |= ((1u << KPV) - 1) << (q * KPV); }
+    }
+    u64 v[KPT];
+#pragma unroll
+    for (int q = 0; q < kHpUnroll; ++q) {
+      if constexpr (KPV == 2) {
+        v[q * 2] = key_map<KK>((K)w[q].x, flip);
+        v[q * 2 + 1] = key_map<KK>((K)w[q].y, flip);
+      } else {
+        v[q * 4] = key_map<KK>((K)w[q].x, flip);
+        v[q * 4 + 1] = key_map<KK>((K)(w[q].x >> 32), flip);
+        v[q * 4 + 2] = key_map<KK>((K)w[q].y, flip);
+        v[q * 4 + 3] = key_map<KK>((K)(w[q].y >> 32), flip);
       }
     }
-  } else {
-    const int ctid = tid - 32;
-    u64* wq = queue + (size_t)wid * kHpQ;
-    u32 qn = 0;  // warp-uniform
-    u32 s = 0, ph = 0;
-    constexpr int KPT = kHpVpt * KPV;  // keys per thread per stage
-    for (u64 it = 0; it < nst; ++it) {
-      const u64 off = r0 + it * SKK;
-      const u32 nv = (u32)(((r1 - off) < SKK ? (r1 - off) : SKK) / KPV);
-      mbar_wait(&full[s], ph);
-      const ulonglong2* sv = (const ulonglong2*)(ring + (size_t)s * kHpStageWords);
-      u64 v[KPT];
-      u32 vmask = 0;  // valid keys of this thread
+    u32 mm = 0;  // this thread's misses
 #pragma unroll
-      for (int q = 0; q < kHpVpt; ++q) {
-        const u32 i = ctid + q * kHpConsumers;
-        ulonglong2 w = make_ulonglong2(0, 0);
-        if (i < nv) { w = sv[i]; vmask |= ((1u << KPV) - 1) << (q * KPV); }
-        if constexpr (KPV == 2) {
-          v[q * 2] = key_map<KK>((K)w.x, flip);
-          v[q * 2 + 1] = key_map<KK>((K)w.y, flip);
-        } else {
-          v[q * 4] = key_map<KK>((K)w.x, flip);
-          v[q * 4 + 1] = key_map<KK>((K)(w.x >> 32), flip);
-          v[q * 4 + 2] = key_map<KK>((K)w.y, flip);
-          v[q * 4 + 3] = key_map<KK>((K)(w.y >> 32), flip);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (++s == kHpStages) { s = 0; ph ^= 1; }
-      u32 mm = 0;  // this thread's misses
+    for (int k = 0; k < KPT; ++k) {
+      // one LDS.128 of the home bucket, a predicated RED on a hit
+      const u32 b = hp_b1(hp_t(v[k]));
+      u64 a0, a1;
+      asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(a0), "=l"(a1) : "r"(tbase + b * 16));
+      const bool hx = a0 == v[k], hy = a1 == v[k];
+      const u32 live = (vmask >> k) & 1u;
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
+                   ::"r"(cbase + (2 * b + (u32)hy) * 4), "r"((u32)(hx | hy) & live) : "memory");
+      mm |= (((u32)!(hx | hy)) & live) << k;
+    }
 #pragma unroll
-      for (int k = 0; k < KPT; ++k) {
-        // shared-space loads and a predicated RED: no generic addressing, no
-        // branch, and both buckets' loads issued before any compare
-        const u32 t = hp_t(v[k]);
-        const u32 b1 = hp_b1(t), b2 = hp_b2(t);
-        u64 a0, a1, c0, c1;
-        asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(a0), "=l"(a1) : "r"(tbase + b1 * 16));
-        asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(c0), "=l"(c1) : "r"(tbase + b2 * 16));
-        const bool h1x = a0 == v[k], h1y = a1 == v[k], h2x = c0 == v[k], h2y = c1 == v[k];
-        const bool h1 = h1x | h1y;
-        const bool hit = h1 | h2x | h2y;
-        const u32 slot = h1 ? 2 * b1 + (u32)h1y : 2 * b2 + (u32)h2y;
-        const u32 live = (vmask >> k) & 1u;
-        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
-                     ::"r"(cbase + slot * 4), "r"((u32)hit & live) : "memory");
-        mm |= (((u32)!hit) & live) << k;
-      }
-#pragma unroll
-      for (int k = 0; k < KPT; ++k) {
-        const bool miss = (mm >> k) & 1u;
-        const u32 m = __ballot_sync(0xffffffffu, miss);
-        if (m) {
-          if (miss) wq[qn + __popc(m & lanemask_lt())] = v[k];
-          qn += __popc(m);
-          if (qn >= 32) {
-            __syncwarp();
-            const u64 u = wq[qn - 32 + lane];
-            __syncwarp();
-            qn -= 32;
-            resolve(true, u);
-          }
+    for (int k = 0; k < KPT; ++k) {
+      const bool miss = (mm >> k) & 1u;
+      const u32 m = __ballot_sync(0xffffffffu, miss);
+      if (m) {
+        if (miss) wq[qn + __popc(m & lanemask_lt())] = v[k];
+        qn += __popc(m);
+        if (qn >= 32) {
+          __syncwarp();
+          const u64 u = wq[qn - 32 + lane];
+          __syncwarp();
+          qn -= 32;
+          resolve(true, u);
         }
       }
     }
-    __syncwarp();
+  }
+  __syncwarp();
+  {
     const u64 u = (u32)lane < qn ? wq[lane] : 0ull;
     __syncwarp();
     resolve((u32)lane < qn, u);
   }
+  if (lane == 0) wsp[wid] = nsw;
   __syncthreads();
   // head and tail keys (< KPV each, CTA 0): the table, else extra cells
   if (c == 0 && wid == 1) {
@@ -419,12 +376,12 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
       const bool act = r == 0 ? hv : tv;
       const u64 u = act ? key_map<KK>(xk[r == 0 ? lane : tail0 + lane], flip) : 0ull;
       bool done = !act;
-      const u32 t = hp_t(u);
-      const u32 bk[2] = {hp_b1(t), hp_b2(t)};
-      for (int d = 0; d < 2 && !done; ++d) {
-        const u64 mk = hp_marker(a, bk[d]);
+      const u32 b = hp_b1(hp_t(u));
+      for (int d = 0; d < kHpD && !done; ++d) {
+        const u32 bb = (b + d) % kHpNB;
+        const u64 mk = hp_marker(a, bb);
         for (int s2 = 0; s2 < 2 && !done; ++s2) {
-          const u32 slot = 2 * bk[d] + s2;
+          const u32 slot = 2 * bb + s2;
           u64 k = atomicCAS(&tkeys[slot], mk, u);
           if (k == mk) k = u;
           if (k == u) { atomicAdd(&tcnt[slot], 1u); done = true; }
@@ -433,14 +390,25 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
       if (!done) extra_k[atomicAdd(&ncell_extra, 1u)] = u;
     }
   }
-  __syncthreads();
-
-  // ---- tail 1: the cells, counting-sorted by partition into this CTA's region ----
-  u64* stk = (u64*)smem;                                   // staging keys [kHpCellCap]
-  u32* stw = (u32*)(smem + (size_t)kHpCellCap * 8);        // staging counts
+  if (wid == 0) {  // prefix of the warps' spills
+    const u32 x = wsp[lane];
+    u32 inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    __syncwarp();
+    wsp[lane] = inc - x;
+    if (lane == 31) wsp[32] = inc;
+  }
   for (u32 i = tid; i <= kHpP; i += kHpThreads) lhist[i] = 0;
   __syncthreads();
+
+  // ---- tail 1: the cells, counting-sorted by partition in passes that fit
+  // the staging area (the queues), written to this CTA's region ----
   constexpr int kCpt = kHpS / kHpThreads;  // slots per thread
+  constexpr u32 kStage = (u32)(kHpQueueBytes / 12);  // cells per pass
   u32 cp[kCpt + 1], cr[kCpt + 1];
 #pragma unroll
   for (int j = 0; j < kCpt; ++j) {
@@ -461,36 +429,47 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
   if (wid == 0) hp_scan512(lhist, lstart);
   else if (wid == 1) hp_scan512(shist, hstart);  // the spill's histogram, taken while spilling
   __syncthreads();
-  const u32 ncells = lstart[kHpP];
-#pragma unroll
-  for (int j = 0; j <= kCpt; ++j) {
-    if (cp[j] < (u32)kHpP) {
-      const u32 pos = lstart[cp[j]] + cr[j];
-      if (j < kCpt) {
-        const u32 slot = tid + j * kHpThreads;
-        stk[pos] = tkeys[slot];
-        stw[pos] = tcnt[slot];
-      } else {
-        stk[pos] = extra_k[tid];
-        stw[pos] = 1;
-      }
-    }
-  }
   for (u32 i = tid; i <= kHpP; i += kHpThreads) {
     a.cpofs[(size_t)c * (kHpP + 1) + i] = lstart[i];
     a.spofs[(size_t)c * (kHpP + 1) + i] = hstart[i];
   }
-  for (u32 i = tid; i < kHpP; i += kHpThreads) written[i] = 0;
-  __syncthreads();
-  for (u32 i = tid; i < ncells; i += kHpThreads) {
-    a.cellk[(size_t)c * kHpCellCap + i] = stk[i];
-    a.cellw[(size_t)c * kHpCellCap + i] = stw[i];
+  const u32 ncells = lstart[kHpP];
+  u64* stk = queue;                                  // staging keys [kStage]
+  u32* stw = (u32*)(queue + kStage);                 // staging counts
+  u64* gck = a.cellk + (size_t)c * kHpCellCap;
+  u32* gcw = a.cellw + (size_t)c * kHpCellCap;
+  for (u32 lo = 0; lo < ncells; lo += kStage) {      // cells [lo, lo + kStage) of the sorted order
+    const u32 hi = lo + kStage < ncells ? lo + kStage : ncells;
+#pragma unroll
+    for (int j = 0; j <= kCpt; ++j) {
+      if (cp[j] < (u32)kHpP) {
+        const u32 pos = lstart[cp[j]] + cr[j];
+        if (pos >= lo && pos < hi) {
+          if (j < kCpt) {
+            const u32 slot = tid + j * kHpThreads;
+            stk[pos - lo] = tkeys[slot];
+            stw[pos - lo] = tcnt[slot];
+          } else {
+            stk[pos - lo] = extra_k[tid];
+            stw[pos - lo] = 1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (u32 i = lo + tid; i < hi; i += kHpThreads) {
+      gck[i] = stk[i - lo];
+      gcw[i] = stw[i - lo];
+    }
+    __syncthreads();
   }
-  // ---- tail 2: the spill, chunk by chunk ----
-  const u32 ns = sfill;
+  // ---- tail 2: the spill (the table's space is free now), chunk by chunk ----
+  const u32 ns = wsp[32];
   K* stv = (K*)smem;                                                     // staged keys
   unsigned short* stp = (unsigned short*)(smem + (size_t)kHpChunk * 8);  // their partitions
-  K* outp = (K*)a.part + head + r0;
+  u32* written = (u32*)(smem + (size_t)kHpChunk * 10);                   // [kHpP]
+  for (u32 i = tid; i < kHpP; i += kHpThreads) written[i] = 0;
+  K* outp = (K*)a.part + head + v0 * KPV;
   for (u32 ch = 0; ch < ns; ch += kHpChunk) {
     const u32 cn = ns - ch < (u32)kHpChunk ? ns - ch : (u32)kHpChunk;
     __syncthreads();
@@ -504,7 +483,12 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
       const u32 i = tid + j * kHpThreads;
       pp[j] = kHpP;
       if (i < cn) {
-        kv[j] = *((volatile K*)&xb[r0 + ch + i]);
+        const u32 g = ch + i;  // spilled key g: warp ww, its index g - wsp[ww]
+        u32 ww = 0;
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1)
+          if (ww + st < 32 && wsp[ww + st] <= g) ww += st;
+        kv[j] = *((volatile K*)&xb[hp_spill_pos<KPV>(v0, ww, g - wsp[ww])]);
         pp[j] = hp_part(key_map<KK>(kv[j], flip), plo, psh, pmap);
         rr[j] = atomicAdd(&lhist[pp[j]], 1u);
       }
@@ -545,7 +529,6 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
   if (!gate_open(a.ctl, a.gate)) return;
   using K = typename KeyT<KK>::T;
   constexpr int KPV = 16 / sizeof(K);
-  constexpr u64 SKK = (u64)kHpStageWords * 8 / sizeof(K);
   extern __shared__ __align__(128) unsigned char smem[];
   u64* hk = (u64*)smem;                        // [kHpPartSlots]
   u32* hc = (u32*)(hk + kHpPartSlots);         // [kHpPartSlots]
@@ -574,9 +557,9 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
     const u32* o = (cell ? a.cpofs : a.spofs) + (size_t)c * (kHpP + 1);
     const u32 b0 = o[p], b1 = o[p + 1];
     len = b1 - b0;
-    u64 r0 = 0, r1;
-    if (!cell) hp_range(body, SKK, c, G, &r0, &r1);
-    sbeg[tid] = cell ? b0 : (u32)(r0 + b0);  // spill: index into part (CTA range + segment)
+    u64 v0 = 0, v1;
+    if (!cell) hp_range(body / KPV, kHpRound, c, G, &v0, &v1);
+    sbeg[tid] = cell ? b0 : (u32)(v0 * KPV + b0);  // spill: index into part (CTA range + segment)
   }
   u32 inc = len;
 #pragma unroll
@@ -653,7 +636,7 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
   __syncthreads();
   const bool bad = ovf || nd > kHpPartCap;
   const u32 d = bad ? 0u : nd;
-  if (d <= kHpThreads) {
+  if (d <= 192) {
     // rank sort (the keys are distinct): thread t moves key t to the number
     // of keys below it; every step reads one key by broadcast
     u64 mk = 0, mc = 0;
@@ -786,7 +769,6 @@ template <int KK>
 __global__ void __launch_bounds__(1024) hp_restore_kernel(HpArgs a, u32 G) {
   using K = typename KeyT<KK>::T;
   constexpr int KPV = 16 / sizeof(K);
-  constexpr u64 SKK = (u64)kHpStageWords * 8 / sizeof(K);
   __shared__ u64 woff[1025];
   const u32 c = blockIdx.x;
   const int tid = threadIdx.x;
@@ -796,8 +778,9 @@ __global__ void __launch_bounds__(1024) hp_restore_kernel(HpArgs a, u32 G) {
   const u64 head = head0 < n ? head0 : n;
   const u64 body = (n - head) / KPV * KPV;
   const u64 tail0 = head + body;
-  u64 r0, r1;
-  hp_range(body, SKK, c, G, &r0, &r1);
+  u64 v0, v1;
+  hp_range(body / KPV, kHpRound, c, G, &v0, &v1);
+  const u64 r0 = v0 * KPV, r1 = v1 * KPV;
   K* x = (K*)a.x;
   const u64 span = r1 - r0;
   auto pos = [&](u64 q) -> u64 {  // q-th row of this CTA -> its index in the column
@@ -830,24 +813,22 @@ __global__ void __launch_bounds__(1024) hp_restore_kernel(HpArgs a, u32 G) {
 }
 
 // ---- host side ----
-static void hp_markers(u64* e0, u64* e1, u32* ma, u32* mb) {
+static void hp_markers(u64* e0, u64* e1, u32* ma) {
   const u64 E0 = 0x5DEECE66D1234567ull;
-  const u32 t0 = hp_t(E0), a0 = hp_b1(t0), b0 = hp_b2(t0);
+  const u32 a0 = hp_b1(hp_t(E0));
   u64 E1 = E0;
   for (u64 t = 1;; ++t) {
     E1 = E0 + t * 0x9E3779B97F4A7C15ull;
-    const u32 t1 = hp_t(E1), a1 = hp_b1(t1), b1 = hp_b2(t1);
-    if (a1 != a0 && a1 != b0 && b1 != a0 && b1 != b0) break;
+    const u32 dist = (hp_b1(hp_t(E1)) - a0) % kHpNB;  // E1's buckets clear of E0's
+    if (dist >= 2 * kHpD && dist <= kHpNB - 2 * kHpD) break;
   }
   *e0 = E0;
   *e1 = E1;
   *ma = a0;
-  *mb = b0;
 }
 
 int hp_grid(u64 n, int kk, int num_sms) {
-  const u64 skk = (u64)kHpStageWords * 8 / (kk ? 4 : 8);
-  const u64 chunks = (n + skk - 1) / skk;
+  const u64 chunks = (n / (kk ? 4 : 2) + kHpRound - 1) / kHpRound;
   const u64 g = num_sms < 160 ? (u64)num_sms : 160;  // hp_reduce's segment table holds 2 x 160
   return (int)(chunks < g ? (chunks ? chunks : 1) : g);
 }
@@ -881,7 +862,7 @@ static HpArgs hp_args(const HpBufs& b, const void* x, u64 n, u64 flip, DevCtl* c
   a.pk = pk;
   a.pc = pc;
   a.poffs = poffs;
-  hp_markers(&a.e0, &a.e1, &a.ma, &a.mb);
+  hp_markers(&a.e0, &a.e1, &a.ma);
   a.gate = gate;
   return a;
 }

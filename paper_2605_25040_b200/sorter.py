@@ -134,8 +134,10 @@ class SortTelemetry:  # sorter.py:60-81
     that extra pass: spill_len / updates / table are then None (not computed)
     and guard_fired reports the device guard.
     ``device_guard_fired`` (global-table overflow), ``pairs`` (distinct keys),
-    ``global_updates``, ``table_buckets`` (the reference's table size M) and
-    ``kernels_launched`` are device extras.
+    ``global_updates``, ``table_buckets`` (the reference's table size M),
+    ``kernels_launched`` and ``count_path`` (how the column was counted: "tiny",
+    "dense" window, global "table" or "partitioned", include/cafs_b200.h) are
+    device extras.
     """
 
     n: int = 0
@@ -155,6 +157,7 @@ class SortTelemetry:  # sorter.py:60-81
     device_guard_fired: bool = False
     exact: bool = False
     sharded_path: str = ""  # sharded sort: "streamed" (device decisions) or "host"
+    count_path: str = ""    # "", "tiny", "dense", "table" or "partitioned"
 
     @property
     def route(self) -> Route | None:
@@ -357,6 +360,9 @@ def _stage_dict(t: _lib.Telemetry) -> dict[str, float]:
 _REF_DTYPE = {"int64": np.uint64, "uint64": np.uint64, "int32": np.uint32, "uint32": np.uint32}
 
 
+_COUNT_PATHS = {1: "tiny", 2: "dense", 3: "table", 4: "partitioned"}  # cafs_count_path_t
+
+
 def _fill_telemetry(tel: SortTelemetry, t: _lib.Telemetry, kind: str, timing: bool,
                     mult: int = HASH_MULT) -> None:
     tel.n = int(t.n)
@@ -368,6 +374,7 @@ def _fill_telemetry(tel: SortTelemetry, t: _lib.Telemetry, kind: str, timing: bo
     tel.pairs = int(t.pairs)
     tel.global_updates = int(t.global_updates)
     tel.kernels_launched = int(t.kernels_launched)
+    tel.count_path = _COUNT_PATHS.get(int(t.count_path), "")
     cap = 8 if kind in ("int32", "uint32") else 4
     route = tel.decision.route
     if route is Route.MAIN and tel.decision.estimate is not None:

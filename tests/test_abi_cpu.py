@@ -44,7 +44,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.cafs_abi_version() == 1
+    assert lib.cafs_abi_version() == 2
     assert lib.cafs_status_string(0) == b"ok"
     assert b"invalid" in lib.cafs_status_string(-1)
 
