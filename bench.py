@@ -361,8 +361,11 @@ def main():
     k_emit = [t.kernel_ms.get("emit_kernel") for t in tels if "emit_kernel" in t.kernel_ms]
     roof = None
     kernels = {}
-    for name, vals, kname in (("count", k_count, "hash_count_kernel" if route == "main"
-                               else "tiny_count_kernel"), ("emit", k_emit, "emit_kernel")):
+    count_name = {"tiny": "tiny_count_kernel", "dense": "hash_count_kernel",
+                  "table": "hash_count_big_kernel",
+                  "partitioned": "hp_count_kernel + hp_reduce_kernel + hp_place_kernel"}.get(
+                      t0.count_path, "hash_count_kernel")
+    for name, vals, kname in (("count", k_count, count_name), ("emit", k_emit, "emit_kernel")):
         if vals:
             avg = sum(vals) / len(vals)
             gbs = n_local * kb / (avg / 1e3) / 1e9
@@ -477,7 +480,7 @@ def main():
             "data": f"synthetic, device-generated ({cfg.desc}; seed {cfg.seed})"
                     + ("; values truncated to int32" if kb == 4 else ""),
             "config": {"workload": args.config, "n": N, "k": cfg.k, "dist": cfg.dist, "s": cfg.s,
-                       "route": route, "parallelism": f"rows sharded x{world}" + (" (sharded path)" if sharded else ""),
+                       "route": route, "count_path": t0.count_path, "parallelism": f"rows sharded x{world}" + (" (sharded path)" if sharded else ""),
                        "l2": "input 8 B x N >> 126 MB L2; unsorted input restored by an untimed "
                              "D2D copy before each step",
                        "direct_range": not args.no_direct},

@@ -41,6 +41,9 @@ CONFIGS = {
                    desc="N=2^30 int64 dictionary codes 0..4095, Zipf s=0.8"),
     "cfg5": Config("cfg5", 10_000_000, 6_000_000, "uniform", seed=5,
                    desc="N=1e7 int64, K=6e6 random keys, i.i.d. uniform (fallback route)"),
+    # cfg4's shape over random int64 keys: no dense window (the hash paths)
+    "cfg4r": Config("cfg4r", 1 << 30, 4096, "zipf", s=0.8, seed=6,
+                    desc="N=2^30 int64, K=4096 random keys, Zipf s=0.8 (no dense window)"),
 }
 
 
