@@ -126,7 +126,8 @@ def ncu_traffic(config: str, kernel: str):
         if kernel.startswith("fallback sort stage"):  # the stage's kernels together
             return sum(v["dram_bytes_per_launch"] for k, v in t.items()
                        if k.startswith(("msd_", "bucket_")))
-        return t[kernel]["dram_bytes_per_launch"]
+        # "a + b + c": the kernels of one count stage together
+        return sum(t[k.strip()]["dram_bytes_per_launch"] for k in kernel.split("+"))
     except Exception:
         return None
 
