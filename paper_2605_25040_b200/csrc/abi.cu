@@ -109,6 +109,7 @@ struct cafs_ctx {
     uint64_t stamp = 0;
     int kk = 0;             // key kind the graph was captured for
     int exact = 0;          // exact-telemetry calls leave the emit out of the graph
+    uint32_t groups = ~0u;  // kernel groups the graph holds (the route the last call took)
   } graphs[16];
   uint64_t graph_clock = 0;
 };
@@ -649,52 +650,94 @@ int run_dispatch(cafs_ctx_t* ctx, const void* x, u64 n, u64 flip, cudaStream_t s
   return CAFS_OK;
 }
 
+// Kernel groups of the fused pipeline.  Every group's kernels check the device
+// decision, so launching all of them is always correct; a call whose buffer
+// and shape were sorted before launches only the groups the previous call's
+// route used (its captured graph holds just those), and the host re-runs the
+// full pipeline when the device decision needs a group that was left out
+// (the left-out kernels never touch the column, so nothing is lost).
+enum : uint32_t {
+  kGrpTiny = 1, kGrpDense = 2, kGrpHp = 4, kGrpTable = 8, kGrpOld = 16, kGrpDensePairs = 32,
+  kGrpAll = 63
+};
+
+uint32_t groups_needed(const DevCtl& c) {
+  const int r = c.eff_route;
+  uint32_t main = c.range_len > 0 ? (kGrpDense | kGrpOld | kGrpDensePairs)
+                  : c.hp_ok       ? kGrpHp
+                                  : (kGrpTable | kGrpOld);
+  if (r == CAFS_TINY_COUNT) return kGrpTiny | (c.tiny_failed ? main : 0u);
+  if (r == CAFS_MAIN) return main;
+  return 0;  // sorted input (or its scan), fallback routes: the host's
+}
+
 // The fused pipeline (sorter.py:357-386 as one stream of gated kernels):
 // tiny count -> tiny finalize -> hash count (dense or queued variant) ->
 // compact -> pair sort -> emit.  Each kernel reads the device decision of the
 // estimate kernel and exits unless its route is active, so the host needs no
 // round trip between the dispatch and the emit.
 int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t flags,
-                 StageTimer& tm, cudaStream_t st, bool with_emit = true, int kk = 0) {
+                 StageTimer& tm, cudaStream_t st, bool with_emit = true, int kk = 0,
+                 uint32_t groups = kGrpAll) {
   TRY(ensure_main(ctx));
   DevCtl* c = ctx->d_ctl;
-  int ts = tm.begin(), tk = tm.begin();
-  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny, kk, ctx->pk_b, ctx->pc_b,
-                    ctx->poffs);
-  tm.end(tk, L_K_COUNT, C_TINY);
-  tm.end(ts, L_STAGE_COUNT, C_TINY);
-  ts = tm.begin();
-  tk = tm.begin();
-  const bool direct = !(flags & CAFS_FLAG_NO_DIRECT);
-  const bool hp = hp_allowed(n, !with_emit);
-  if (hp) TRY(ensure_hp(ctx, n, kk));
-  cudaError_t e = cudaSuccess;
-  if (direct)
-    e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                          ctx->num_sms, st, 0, kGateMainDense, ctx->dense, kk);
-  if (hp && e == cudaSuccess) {  // the partitioned count: the sorted pairs, no pair sort
-    e = launch_hp_count(hp_bufs(ctx), x, n, flip, c, ctx->pk_b, ctx->pc_b, ctx->poffs,
-                        ctx->num_sms, st, kGateMainHP, kk);
-    ctx->launches += 3;
+  int ts, tk;
+  if (groups & kGrpTiny) {
+    ts = tm.begin();
+    tk = tm.begin();
+    launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny, kk, ctx->pk_b, ctx->pc_b,
+                      ctx->poffs);
+    tm.end(tk, L_K_COUNT, C_TINY);
+    tm.end(ts, L_STAGE_COUNT, C_TINY);
+    ctx->launches++;
   }
-  if (e == cudaSuccess)
-    e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, direct ? 1 : 0,
-                          ctx->num_sms, st, 1, direct ? kGateMainHash : kGateMainOld,
-                          ctx->dense, kk);
-  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
-  tm.end(tk, L_K_COUNT, C_MAIN);
-  launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
-                 kGateMainOld);
-  if (direct)
-    launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs, n, st,
-                       kGateMainDense);
-  tm.end(ts, L_STAGE_COUNT, C_MAIN);
-  ts = tm.begin();
-  e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st,
-                              kGateMainOld);
-  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
-  tm.end(ts, L_STAGE_SORT_K, C_MAIN);
-  if (with_emit) {
+  const bool direct = !(flags & CAFS_FLAG_NO_DIRECT);
+  const bool hp = hp_allowed(n, !with_emit) && (groups & kGrpHp);
+  const bool any_main = groups & (kGrpDense | kGrpHp | kGrpTable | kGrpOld);
+  if (any_main) {
+    ts = tm.begin();
+    tk = tm.begin();
+    if (hp) TRY(ensure_hp(ctx, n, kk));
+    cudaError_t e = cudaSuccess;
+    if (direct && (groups & kGrpDense)) {
+      e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
+                            ctx->num_sms, st, 0, kGateMainDense, ctx->dense, kk);
+      ctx->launches++;
+    }
+    if (hp && e == cudaSuccess) {  // the partitioned count: the sorted pairs, no pair sort
+      e = launch_hp_count(hp_bufs(ctx), x, n, flip, c, ctx->pk_b, ctx->pc_b, ctx->poffs,
+                          ctx->num_sms, st, kGateMainHP, kk);
+      ctx->launches += 3;
+    }
+    if (e == cudaSuccess && (groups & kGrpTable)) {
+      e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist,
+                            direct ? 1 : 0, ctx->num_sms, st, 1,
+                            direct ? kGateMainHash : kGateMainOld, ctx->dense, kk);
+      ctx->launches++;
+    }
+    if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
+    tm.end(tk, L_K_COUNT, C_MAIN);
+    if (groups & kGrpOld) {
+      launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
+                     kGateMainOld);
+      ctx->launches++;
+    }
+    if (direct && (groups & kGrpDensePairs)) {
+      launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs, n,
+                         st, kGateMainDense);
+      ctx->launches++;
+    }
+    tm.end(ts, L_STAGE_COUNT, C_MAIN);
+    if (groups & kGrpOld) {
+      ts = tm.begin();
+      e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs,
+                                  st, kGateMainOld);
+      if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+      tm.end(ts, L_STAGE_SORT_K, C_MAIN);
+      ctx->launches++;
+    }
+  }
+  if (with_emit && (groups & ~(uint32_t)0) != 0) {
     ts = tm.begin();
     tk = tm.begin();
     launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, kSmallSortMax, kk);
@@ -702,7 +745,6 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
     tm.end(ts, L_STAGE_EMIT, C_EMIT);
     ctx->launches++;
   }
-  ctx->launches += direct ? 6 : 4;
   CKL();
   return CAFS_OK;
 }
@@ -865,7 +907,8 @@ int main_finish(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cafs_telemetry_t* tel
 }
 
 void pipeline_direct(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t flags,
-                     StageTimer& tm, cudaStream_t st, bool exact, int* mark, int* rc, int kk) {
+                     StageTimer& tm, cudaStream_t st, bool exact, int* mark, int* rc, int kk,
+                     uint32_t groups = kGrpAll) {
   const int te = tm.begin();
   launch_estimate(x, n, flip, 1, ctx->d_ctl, st, kk,
                   (hp_allowed(n, exact) ? kEstHp : 0) |
@@ -873,7 +916,7 @@ void pipeline_direct(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32
   tm.end(te, L_K_EST);
   ctx->launches++;
   *mark = tm.n;
-  *rc = launch_fused(ctx, x, n, flip, mult, flags, tm, st, !exact, kk);
+  *rc = launch_fused(ctx, x, n, flip, mult, flags, tm, st, !exact, kk, groups);
 }
 
 // The estimate + fused kernels, replayed from a cached CUDA Graph when the same
@@ -881,7 +924,10 @@ void pipeline_direct(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32
 // launches (the small-input latency).  The graph's kernels are the same; only
 // the launch path differs.
 int launch_pipeline(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t flags,
-                    StageTimer& tm, cudaStream_t st, bool exact, int* mark, int kk) {
+                    StageTimer& tm, cudaStream_t st, bool exact, int* mark, int kk,
+                    uint32_t* used, cafs_ctx_t::GraphEntry** entry) {
+  *used = kGrpAll;
+  *entry = nullptr;
   static int use_graphs = -1;
   if (use_graphs < 0) {
     const char* e = getenv("CAFS_GRAPHS");
@@ -905,6 +951,8 @@ int launch_pipeline(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_
     if (g.stamp < lru->stamp) lru = &g;
   }
   if (hit && hit->exec) {
+    *used = hit->groups;
+    *entry = hit;
     CK(cudaGraphLaunch(hit->exec, st));
     tm.n = hit->tn;
     for (int i = 0; i < hit->tn; ++i) { tm.label[i] = hit->label[i]; tm.cond[i] = hit->cond[i]; }
@@ -919,6 +967,7 @@ int launch_pipeline(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_
     lru->x = (u64)x; lru->n = n; lru->flip = flip; lru->mult = mult; lru->flags = flags;
     lru->timing = timing; lru->seen = 1; lru->stamp = ++ctx->graph_clock; lru->kk = kk;
     lru->exact = exact ? 1 : 0;
+    *entry = lru;
     pipeline_direct(ctx, x, n, flip, mult, flags, tm, st, exact, mark, &rc, kk);
     CKL();
     return rc;
@@ -929,8 +978,11 @@ int launch_pipeline(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_
   ct.st = ctx->cap_stream;
   ct.capturing = true;
   cudaGraph_t graph = nullptr;
+  *used = hit->groups;
+  *entry = hit;
   CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
-  pipeline_direct(ctx, x, n, flip, mult, flags, ct, ctx->cap_stream, exact, mark, &rc, kk);
+  pipeline_direct(ctx, x, n, flip, mult, flags, ct, ctx->cap_stream, exact, mark, &rc, kk,
+                  hit->groups);
   cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &graph);
   if (rc != CAFS_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "graph capture", e);
@@ -1146,8 +1198,30 @@ static int sort_impl(cafs_ctx_t* ctx, void* d_x, uint64_t n, int is_signed, uint
   const bool exact = want_tel && (flags & CAFS_FLAG_EXACT_TELEMETRY);
   TRY(ensure_main(ctx));
   int mark = 0;
-  TRY(launch_pipeline(ctx, x, n, flip, hash_mult, flags, tm, st, exact, &mark, kk));
+  uint32_t used = kGrpAll;
+  cafs_ctx_t::GraphEntry* entry = nullptr;
+  TRY(launch_pipeline(ctx, x, n, flip, hash_mult, flags, tm, st, exact, &mark, kk, &used, &entry));
   TRY(sync_ctl(ctx, st));
+  {
+    const uint32_t need = groups_needed(*ctx->h_ctl);
+    if (need & ~used) {
+      // the cached pipeline left out a group this input's route needs: run
+      // the whole pipeline (nothing was written to the column)
+      tm.n = 0;
+      int rc2 = CAFS_OK;
+      pipeline_direct(ctx, x, n, flip, hash_mult, flags, tm, st, exact, &mark, &rc2, kk);
+      TRY(rc2);
+      CKL();
+      TRY(sync_ctl(ctx, st));
+    }
+    // the next call on this buffer and shape launches what this route used
+    const uint32_t next = groups_needed(*ctx->h_ctl);
+    if (entry && entry->groups != next && ctx->h_ctl->eff_route != kNeedScan) {
+      if (entry->exec) cudaGraphExecDestroy(entry->exec);
+      entry->exec = nullptr;
+      entry->groups = next;
+    }
+  }
   int eff = ctx->h_ctl->eff_route;
   bool mono = eff == CAFS_ALREADY_SORTED;
   if (eff == kNeedScan) {

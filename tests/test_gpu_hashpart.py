@@ -175,3 +175,31 @@ def test_host_numpy_column():
     y = xn.copy()
     cafs.cafs_sort(y)
     assert np.array_equal(y, np.sort(xn))
+
+
+def test_route_changes_on_one_buffer():
+    """The graph cached for a buffer holds only the kernels of the route its
+    last call took; a call whose data needs another route must notice and run
+    the whole pipeline.  One buffer, same length, data cycling through every
+    route and count path, several times (direct, captured, replayed)."""
+    n = 2_100_000
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    cols = {
+        "tiny": datagen.generate(datagen.Config("t1", n, 5, "uniform", seed=41)),
+        "dense": datagen.generate(datagen.Config("t2", n, 3000, "zipf", s=0.9,
+                                                 palette="codes", seed=42)),
+        "partitioned": datagen.generate(datagen.Config("t3", n, 20_000, "zipf", s=1.1, seed=43)),
+        "fallback": torch.randint(-2**62, 2**62, (n,), device="cuda", generator=g),
+        "sorted": torch.arange(n, device="cuda", dtype=torch.int64) * 3 - n,
+    }
+    want = {k: np.sort(v.cpu().numpy()) for k, v in cols.items()}
+    buf = torch.empty(n, dtype=torch.int64, device="cuda")
+    order = ["tiny", "dense", "dense", "partitioned", "partitioned", "tiny", "fallback",
+             "dense", "sorted", "partitioned", "tiny", "tiny", "fallback", "dense"]
+    for rep in range(2):
+        for name in order:
+            buf.copy_(cols[name])
+            cafs.cafs_sort(buf)
+            torch.cuda.synchronize()
+            assert np.array_equal(buf.cpu().numpy(), want[name]), (rep, name)
