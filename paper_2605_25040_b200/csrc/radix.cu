@@ -274,7 +274,26 @@ __global__ void __launch_bounds__(1024, 1)
   int cur = 0;
   int nvary = 0;
   for (int p = 0; p < 8; ++p) nvary += ((vary >> (8 * p)) & 0xFF) != 0;
-  if (n <= kBitonicMax && nvary > 2) {
+  if (n <= 1024 && nvary > 0) {
+    // up to 1024 keys: a rank sort -- thread i counts the keys before its own
+    // (smaller, or equal and earlier: stable) with broadcast reads, then
+    // writes it to the other buffer; one barrier instead of a bitonic network
+    u64 k = 0;
+    u32 r = 0;
+    if ((u64)tid < n) {
+      k = kb[tid];
+#pragma unroll 8
+      for (u32 j = 0; j < (u32)n; ++j) {
+        const u64 kj = kb[j];
+        r += (kj < k || (kj == k && j < (u32)tid)) ? 1u : 0u;
+      }
+      kb[kSmallSortMax + r] = k;
+      ib[kSmallSortMax + r] = ib[tid];
+    }
+    __syncthreads();
+    cur = 1;
+    nvary = 0;
+  } else if (n <= kBitonicMax && nvary > 2) {
     // few keys, many varying bytes: one bitonic network (log2(P)(log2(P)+1)/2
     // barrier steps) beats up to 8 radix passes of fixed cost each
     u32 P = 2;
