@@ -243,6 +243,16 @@ int ensure_hp(cafs_ctx_t* ctx, u64 n, int kk) {
     ctx->hp_part_bytes = bytes;
   }
   if (!ctx->hp_scratch) CK(cudaMalloc(&ctx->hp_scratch, hp_scratch_bytes(ctx->num_sms)));
+  const u64 tiles = emit_tiles(n, kk);  // the emit's tile -> pair map (hp_place's pairs)
+  if (tiles > ctx->tile_map_len) {
+    CK(cudaDeviceSynchronize());
+    if (ctx->tile_map) CK(cudaFree(ctx->tile_map));
+    ctx->tile_map = nullptr;
+    ctx->tile_map_len = 0;
+    drop_graphs(ctx);
+    CK(cudaMalloc(&ctx->tile_map, tiles * sizeof(u32)));
+    ctx->tile_map_len = tiles;
+  }
   return CAFS_OK;
 }
 
@@ -737,10 +747,19 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
       ctx->launches++;
     }
   }
-  if (with_emit && (groups & ~(uint32_t)0) != 0) {
+  // a pipeline that holds only the partitioned count (its route predicted)
+  // also writes the emit's tile -> pair map: its pair sets are large
+  const bool map = hp && groups == kGrpHp;
+  if (with_emit && map) {
+    launch_emit_map(ctx->poffs, c, x, 0, n, ctx->tile_map, (u64)ctx->num_sms * 8 * 256,
+                    ctx->num_sms, st, kk);
+    ctx->launches++;
+  }
+  if (with_emit && groups != 0) {
     ts = tm.begin();
     tk = tm.begin();
-    launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, kSmallSortMax, kk);
+    launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, kSmallSortMax, kk,
+                false, map ? ctx->tile_map : nullptr);
     tm.end(tk, L_K_EMIT, C_EMIT);
     tm.end(ts, L_STAGE_EMIT, C_EMIT);
     ctx->launches++;
