@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kEmitThreads)
   // (with a tile map the tiles' pairs are looked up, not searched: no index)
   const u64 stride = MAP ? 0 : (npairs + idx_entries) / idx_entries;
   const u64 nidx = MAP ? 0 : npairs / stride + 1;
-  for (u64 i = threadIdx.x; i < nidx; i += kEmitThreads) soffs[i] = goffs[i * stride];
+  for (u64 i = threadIdx.x; i < nidx; i += blockDim.x) soffs[i] = goffs[i * stride];
   if (!MAP) __syncthreads();
   if (stride == 1) offs = soffs;
   // pair containing global position g, searching from pair lo (offs[lo] <= g)
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kEmitThreads)
   K* ob = out + head;
   const u64 gb = begin + head;  // global position of ob[0]
   const u64 ntiles = (nvec * VK + kTileKeys - 1) / kTileKeys;
-  const u64 gw = (u64)blockIdx.x * (kEmitThreads / 32) + (threadIdx.x >> 5);
+  const u64 gw = (u64)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   // each warp takes `tpw` consecutive tiles; CTAs are many and short-lived, so
   // the tiles being written at any moment form one moving window of the output
   // in launch order (measured: 7.3 TB/s vs 6.2-6.4 TB/s for persistent
@@ -274,40 +274,45 @@ void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl
     idx = e ? atoi(e) : kIdxDefault;
     if (idx < 32 || idx > (int)kIdxEntries) idx = kIdxDefault;
   }
-  const u64 wpb = kEmitThreads / 32;
-  u64 grid = (wtiles + (u64)tpw * wpb - 1) / ((u64)tpw * wpb);
+  // small outputs: one tile per warp and smaller CTAs, so the work still
+  // spreads over every SM (1M keys = 977 tiles: 31 CTAs of 16 warps x 2 tiles)
+  u64 tpw_use = (u64)tpw, threads = kEmitThreads;
+  const u64 spread = (u64)num_sms * 4;
+  if ((wtiles + tpw_use * 16 - 1) / (tpw_use * 16) < spread) tpw_use = 1;
+  if ((wtiles + 15) / 16 < spread) threads = 128;
+  const u64 wpb = threads / 32;
+  u64 grid = (wtiles + tpw_use * wpb - 1) / (tpw_use * wpb);
   if (grid < 1) grid = 1;
-  (void)num_sms;
   const size_t sm = ((u64)idx + 1) * 8;
   switch (kk) {
     case 1:
       if (tile_pair)
-        launch_pdl(kPdlEmit, emit_kernel<1, true>, (unsigned)grid, kEmitThreads, sm, st, keys,
-                   offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx,
+        launch_pdl(kPdlEmit, emit_kernel<1, true>, (unsigned)grid, (unsigned)threads, sm, st, keys,
+                   offs, npairs, ctl, (u32*)out, begin, end, flip, tpw_use, (u64)idx,
                    ctl_slice ? 1 : 0, tile_pair);
       else
-        launch_pdl(kPdlEmit, emit_kernel<1, false>, (unsigned)grid, kEmitThreads, sm, st, keys,
-                   offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx,
+        launch_pdl(kPdlEmit, emit_kernel<1, false>, (unsigned)grid, (unsigned)threads, sm, st, keys,
+                   offs, npairs, ctl, (u32*)out, begin, end, flip, tpw_use, (u64)idx,
                    ctl_slice ? 1 : 0, tile_pair);
       break;
     case 2:
       if (tile_pair)
-        launch_pdl(kPdlEmit, emit_kernel<2, true>, (unsigned)grid, kEmitThreads, sm, st, keys,
-                   offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx,
+        launch_pdl(kPdlEmit, emit_kernel<2, true>, (unsigned)grid, (unsigned)threads, sm, st, keys,
+                   offs, npairs, ctl, (u32*)out, begin, end, flip, tpw_use, (u64)idx,
                    ctl_slice ? 1 : 0, tile_pair);
       else
-        launch_pdl(kPdlEmit, emit_kernel<2, false>, (unsigned)grid, kEmitThreads, sm, st, keys,
-                   offs, npairs, ctl, (u32*)out, begin, end, flip, (u64)tpw, (u64)idx,
+        launch_pdl(kPdlEmit, emit_kernel<2, false>, (unsigned)grid, (unsigned)threads, sm, st, keys,
+                   offs, npairs, ctl, (u32*)out, begin, end, flip, tpw_use, (u64)idx,
                    ctl_slice ? 1 : 0, tile_pair);
       break;
     default:
       if (tile_pair)
-        launch_pdl(kPdlEmit, emit_kernel<0, true>, (unsigned)grid, kEmitThreads, sm, st, keys,
-                   offs, npairs, ctl, (u64*)out, begin, end, flip, (u64)tpw, (u64)idx,
+        launch_pdl(kPdlEmit, emit_kernel<0, true>, (unsigned)grid, (unsigned)threads, sm, st, keys,
+                   offs, npairs, ctl, (u64*)out, begin, end, flip, tpw_use, (u64)idx,
                    ctl_slice ? 1 : 0, tile_pair);
       else
-        launch_pdl(kPdlEmit, emit_kernel<0, false>, (unsigned)grid, kEmitThreads, sm, st, keys,
-                   offs, npairs, ctl, (u64*)out, begin, end, flip, (u64)tpw, (u64)idx,
+        launch_pdl(kPdlEmit, emit_kernel<0, false>, (unsigned)grid, (unsigned)threads, sm, st, keys,
+                   offs, npairs, ctl, (u64*)out, begin, end, flip, tpw_use, (u64)idx,
                    ctl_slice ? 1 : 0, tile_pair);
   }
 }

@@ -54,7 +54,7 @@ constexpr int kHpSLog2 = 14;
 constexpr u32 kHpS = 1u << kHpSLog2;         // table slots
 constexpr u32 kHpNB = kHpS / 2;              // 2-slot buckets
 constexpr int kHpNBLog2 = kHpSLog2 - 1;
-constexpr int kHpD = 2;                      // buckets a key may sit in (home + 1)
+constexpr int kHpD = 2;                      // buckets a key may sit in (home, second choice)
 constexpr u32 kHpFullClaims = kHpS - kHpS / 16;  // from here on a miss spills without probing
 constexpr int kHpQ = 64;                     // per-warp miss queue
 constexpr int kHpP = kHpParts;               // key-range partitions
@@ -79,6 +79,9 @@ __host__ __device__ __forceinline__ u32 hp_t(u64 v) {
   return (u32)(v >> 32) * 0x9E3779B1u + (u32)v;
 }
 __host__ __device__ __forceinline__ u32 hp_b1(u32 t) { return (t * 0x85EBCA77u) >> (32 - kHpNBLog2); }
+// the second choice: an independent bucket (adjacent buckets would make the
+// same few keys overflow in every CTA, piling their rows into one partition)
+__host__ __device__ __forceinline__ u32 hp_b2(u32 t) { return (t * 0xC2B2AE3Du) >> (32 - kHpNBLog2); }
 
 struct HpArgs {
   const void* x;   // column (keys of kind KK); its streamed part receives the spill
@@ -97,13 +100,13 @@ struct HpArgs {
   u64* pk;         // sorted pairs: keys, counts, offsets (npairs + 1)
   u64* pc;
   u64* poffs;
-  u64 e0, e1;      // empty-slot markers: e1 in E0's kHpD buckets from ma, e0 elsewhere
-  u32 ma;
+  u64 e0, e1;      // empty-slot markers: e1 in E0's two buckets ma, mb, e0 elsewhere
+  u32 ma, mb;
   int gate;
 };
 
 __device__ __forceinline__ u64 hp_marker(const HpArgs& a, u32 b) {
-  return ((b - a.ma) % kHpNB) < (u32)kHpD ? a.e1 : a.e0;
+  return (b == a.ma || b == a.mb) ? a.e1 : a.e0;
 }
 
 // Partition of a key: its fine bin over the sample span, mapped (pmap).
@@ -273,11 +276,11 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
   auto resolve = [&](bool active, u64 u) {
     bool done = !active;
     if (*((volatile u32*)&sclaims) < kHpFullClaims && __any_sync(0xffffffffu, active)) {
-      const u32 b = hp_b1(hp_t(u));
+      const u32 t = hp_t(u);
 #pragma unroll
       for (int d = 0; d < kHpD; ++d) {
         if (!done) {
-          const u32 bb = (b + d) % kHpNB;
+          const u32 bb = d ? hp_b2(t) : hp_b1(t);
           u64 t0, t1;
           asm volatile("ld.volatile.shared.v2.u64 {%0,%1}, [%2];"
                        : "=l"(t0), "=l"(t1) : "r"(tbase + bb * 16));
@@ -376,9 +379,9 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
       const bool act = r == 0 ? hv : tv;
       const u64 u = act ? key_map<KK>(xk[r == 0 ? lane : tail0 + lane], flip) : 0ull;
       bool done = !act;
-      const u32 b = hp_b1(hp_t(u));
+      const u32 t = hp_t(u);
       for (int d = 0; d < kHpD && !done; ++d) {
-        const u32 bb = (b + d) % kHpNB;
+        const u32 bb = d ? hp_b2(t) : hp_b1(t);
         const u64 mk = hp_marker(a, bb);
         for (int s2 = 0; s2 < 2 && !done; ++s2) {
           const u32 slot = 2 * bb + s2;
@@ -813,18 +816,19 @@ __global__ void __launch_bounds__(1024) hp_restore_kernel(HpArgs a, u32 G) {
 }
 
 // ---- host side ----
-static void hp_markers(u64* e0, u64* e1, u32* ma) {
+static void hp_markers(u64* e0, u64* e1, u32* ma, u32* mb) {
   const u64 E0 = 0x5DEECE66D1234567ull;
-  const u32 a0 = hp_b1(hp_t(E0));
+  const u32 t0 = hp_t(E0), a0 = hp_b1(t0), b0 = hp_b2(t0);
   u64 E1 = E0;
-  for (u64 t = 1;; ++t) {
+  for (u64 t = 1;; ++t) {  // E1's two buckets clear of E0's
     E1 = E0 + t * 0x9E3779B97F4A7C15ull;
-    const u32 dist = (hp_b1(hp_t(E1)) - a0) % kHpNB;  // E1's buckets clear of E0's
-    if (dist >= 2 * kHpD && dist <= kHpNB - 2 * kHpD) break;
+    const u32 t1 = hp_t(E1), a1 = hp_b1(t1), b1 = hp_b2(t1);
+    if (a1 != a0 && a1 != b0 && b1 != a0 && b1 != b0) break;
   }
   *e0 = E0;
   *e1 = E1;
   *ma = a0;
+  *mb = b0;
 }
 
 int hp_grid(u64 n, int kk, int num_sms) {
@@ -862,7 +866,7 @@ static HpArgs hp_args(const HpBufs& b, const void* x, u64 n, u64 flip, DevCtl* c
   a.pk = pk;
   a.pc = pc;
   a.poffs = poffs;
-  hp_markers(&a.e0, &a.e1, &a.ma);
+  hp_markers(&a.e0, &a.e1, &a.ma, &a.mb);
   a.gate = gate;
   return a;
 }
