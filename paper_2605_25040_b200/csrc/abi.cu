@@ -91,6 +91,7 @@ struct cafs_ctx {
   void* hp_part = nullptr;
   size_t hp_part_bytes = 0;
   void* hp_scratch = nullptr;
+  void* hp_mscratch = nullptr;  // the sharded merge's (the local count's stays for a restore)
   // pageable host transfers: per worker thread a stream and two pinned buffers
   cudaStream_t xfer_stream[32] = {};
   cudaEvent_t xfer_event[32][4] = {};
@@ -112,6 +113,7 @@ struct cafs_ctx {
     uint32_t groups = ~0u;  // kernel groups the graph holds (the route the last call took)
   } graphs[16];
   uint64_t graph_clock = 0;
+  uint64_t buf_gen = 0;  // bumped when a buffer captured graphs point to is reallocated
 };
 
 namespace cafs {
@@ -219,6 +221,7 @@ int ensure_main(cafs_ctx_t* ctx) {
 
 // Drop every captured pipeline graph (a buffer they reference was reallocated).
 void drop_graphs(cafs_ctx_t* ctx) {
+  ++ctx->buf_gen;  // the sharded calls' graphs (per communicator) check it
   for (auto& g : ctx->graphs) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
     g = cafs_ctx_t::GraphEntry();
@@ -1046,21 +1049,30 @@ int shard_count_enqueue(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, u64 mult
                         const u64* hdr_all, int world, const u64* samples, u64* tiny, u64* send,
                         u64 cap, cudaStream_t st) {
   DevCtl* c = ctx->d_ctl;
-  launch_estimate_sharded(samples, hdr_all, world, c, st);
+  // the partitioned count gives this shard's pairs sorted on device for any
+  // number of keys (the table path's pair sort stops at 8192)
+  const bool hp = hp_allowed(n, false);
+  if (hp) TRY(ensure_hp(ctx, n, 0));
+  launch_estimate_sharded(samples, hdr_all, world, c, st, hp ? kEstHp : 0);
   launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny);
   launch_shard_tiny_pack(c, tiny, st);
   cudaError_t e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
                                     ctx->num_sms, st, 0, kGateMainDense, ctx->dense);
+  if (hp && e == cudaSuccess) {
+    e = launch_hp_count(hp_bufs(ctx), x, n, flip, c, ctx->pk_b, ctx->pc_b, ctx->poffs,
+                        ctx->num_sms, st, kGateMainHP, 0);
+    ctx->launches += 3;
+  }
   if (e == cudaSuccess)
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
                           ctx->num_sms, st, 1, kGateMainHash, ctx->dense);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
   launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
-                 kGateMain);
+                 kGateMainOld);
   launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs, n, st,
                      kGateMainDense);
   e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st,
-                              kGateMain);
+                              kGateMainOld);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
   launch_shard_pack_pairs(c, ctx->pk_b, ctx->pc_b, send, cap, st);
   ctx->launches += 10;
@@ -1074,12 +1086,16 @@ int shard_finish_enqueue(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, const u64* ti
                          const u64* recv, int world, u64 cap, u64 row, cudaStream_t st) {
   DevCtl* c = ctx->d_ctl;
   launch_shard_tiny_finish(c, tiny_sum, ctx->pk_b, ctx->pc_b, ctx->poffs, st);
-  launch_shard_merge(c, recv, world, cap, row, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->num_sms, st);
-  launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
-                 kGateMain);
-  cudaError_t e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, kExpectCtlN, ctx->pk_b,
-                                          ctx->pc_b, ctx->poffs, st, kGateMain);
-  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+  // the union of every rank's sorted list (sorter.py:276-285): key-range
+  // partitions of the gathered lists reduced on device into the global sorted
+  // pairs and offsets -- no hash table, no pair sort, any number of pairs
+  if (!ctx->hp_mscratch) CK(cudaMalloc(&ctx->hp_mscratch, hp_scratch_bytes(ctx->num_sms)));
+  launch_shard_merge_check(c, recv, world, cap, row, st);
+  HpBufs mb = hp_bufs(ctx);
+  mb.scratch = ctx->hp_mscratch;
+  cudaError_t e = launch_hp_shard_merge(mb, recv, world, cap, row, c, ctx->pk_b, ctx->pc_b,
+                                        ctx->poffs, st);
+  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "sharded merge", e);
   launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, 0, 0, true);
   ctx->launches += 6;
   CKL();
@@ -1088,12 +1104,28 @@ int shard_finish_enqueue(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, const u64* ti
 
 // after the control block reached the host mirror: the status every rank agrees
 // on (same gathered data) and the telemetry
-int shard_result(cafs_ctx_t* ctx, cafs_telemetry_t* tel, int* h_status, cudaStream_t st) {
+int shard_result(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cafs_telemetry_t* tel, int* h_status,
+                 cudaStream_t st) {
   const DevCtl& h = *ctx->h_ctl;
   const int eff = h.eff_route;
   int status = 1;  // 1: the caller runs the host-driven sharded path
   if (eff == CAFS_ALREADY_SORTED) status = 0;
   else if ((eff == CAFS_TINY_COUNT || eff == CAFS_MAIN) && h.pairs_ready && !h.overflow) status = 0;
+  if (status != 0 && eff == CAFS_MAIN && h.local_hp) {
+    // the partitioned count spilled into this shard: rebuild it from the cells
+    // and the spill for the host-driven path (which may sort the rows again)
+    launch_hp_restore(hp_bufs(ctx), x, n, flip, ctx->num_sms, st, 0);
+    ctx->launches++;
+    CKL();
+    CK(cudaStreamSynchronize(st));
+  }
+  if (status != 0 && eff == CAFS_MAIN && !h.merge_bad && h.hp_overflow) {
+    // the merge itself overflowed over this shard's sorted pairs: they are gone
+    ctx->h_ctl->local_overflow = 1;
+    CK(cudaMemcpyAsync(&ctx->d_ctl->local_overflow, &ctx->h_ctl->local_overflow,
+                       sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
   if (eff == CAFS_MAIN && h.overflow) {  // a local overflow left this rank's table dirty
     CK(cudaMemsetAsync(ctx->gkeys, 0xFF, kGlobalSlots * 8, st));
     CK(cudaMemsetAsync(ctx->gcnt, 0, kGlobalSlots * 8, st));
@@ -1169,7 +1201,7 @@ void cafs_ctx_destroy(cafs_ctx_t* ctx) {
                  ctx->trivial, ctx->tile_counters, ctx->tile_state, ctx->tmp, ctx->stage, ctx->msd,
                  ctx->tl_keys, ctx->tl_idx, ctx->tl_first, ctx->tl_runs, ctx->tl_comp,
                  ctx->tl_offs, ctx->tl_acc, ctx->pk_t, ctx->pc_t, ctx->wide, ctx->tile_map,
-                 ctx->hp_part, ctx->hp_scratch};
+                 ctx->hp_part, ctx->hp_scratch, ctx->hp_mscratch};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -1776,7 +1808,7 @@ int cafs_shard_finish_i64(cafs_ctx_t* ctx, int64_t* d_x, uint64_t n, int is_sign
   TRY(shard_finish_enqueue(ctx, (u64*)d_x, n, is_signed ? kSign : 0, (const u64*)d_tiny_sum,
                            (const u64*)d_recv, world, cap, 1 + 2 * cap, st));
   TRY(sync_ctl(ctx, st));
-  return shard_result(ctx, tel, h_status, st);
+  return shard_result(ctx, (u64*)d_x, n, is_signed ? kSign : 0, tel, h_status, st);
 }
 
 int cafs_gen_mix(uint64_t* d_out, uint64_t count, uint64_t seed, uint64_t skip, void* stream) {
@@ -1817,6 +1849,7 @@ struct cafs_comm_t {
     u64 x = 0, n = 0, flip = 0, mult = 0;
     int seen = 0;
     uint64_t launches = 0, stamp = 0;
+    uint64_t gen = 0;  // the context's buf_gen at capture
     cudaGraphExec_t exec = nullptr;
   } graphs[8];
   uint64_t clock = 0;
@@ -1880,6 +1913,47 @@ int cafs_comm_create(int device, const unsigned char* id, int world, int rank,
 
 namespace {
 
+// largest exchange row (pairs per rank) the native sharded sort grows to; a
+// longer list continues on the host-driven path
+constexpr u64 kShardCapMax = 1ull << 20;
+
+// the pair tables' all-gather, the merge and this rank's slice emit; again
+// (from_local) after the row grew: the rows are re-packed from the count's pairs
+int sharded_exchange(cafs_ctx_t* ctx, cafs_comm_t* cm, u64* x, u64 n, u64 flip, cudaStream_t st,
+                     int from_local) {
+  const u64 cap = cm->cap, row = cm->row, tiny_off = 1 + 2 * cap;
+  if (from_local) {
+    launch_shard_pack_pairs(ctx->d_ctl, ctx->pk_b, ctx->pc_b, cm->send, cap, st, 1);
+    ctx->launches++;
+  }
+  if (ncclAllGather(cm->send, cm->recv, row, ncclUint64, cm->nc, st) != ncclSuccess)
+    return fail(ctx, CAFS_ECUDA, "ncclAllGather (pair tables)");
+  launch_shard_tiny_gather(cm->recv, cm->world, row, tiny_off, cm->tiny_sum, st);
+  TRY(shard_finish_enqueue(ctx, x, n, flip, cm->tiny_sum, cm->recv, cm->world, cap, row, st));
+  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->d_ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
+  ctx->launches += 1;  // tiny gather
+  CKL();
+  return CAFS_OK;
+}
+
+// a larger exchange row for this communicator (the captured graphs go)
+int comm_resize(cafs_ctx_t* ctx, cafs_comm_t* c, u64 cap) {
+  CK(cudaDeviceSynchronize());
+  for (auto& g : c->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g = cafs_comm_t::Graph();
+  }
+  if (c->send) CK(cudaFree(c->send));
+  if (c->recv) CK(cudaFree(c->recv));
+  c->send = c->recv = nullptr;
+  c->cap = cap;
+  c->row = 1 + 2 * cap + CAFS_SHARD_TINY_WORDS;
+  CK(cudaMalloc(&c->send, c->row * 8));
+  CK(cudaMalloc(&c->recv, (size_t)c->world * c->row * 8));
+  CK(cudaMemset(c->send, 0, c->row * 8));
+  return CAFS_OK;
+}
+
 int sharded_enqueue(cafs_ctx_t* ctx, cafs_comm_t* cm, u64* x, u64 n, u64 flip, u64 mult,
                     cudaStream_t st) {
   const u64 cap = cm->cap, row = cm->row, tiny_off = 1 + 2 * cap;
@@ -1892,14 +1966,8 @@ int sharded_enqueue(cafs_ctx_t* ctx, cafs_comm_t* cm, u64* x, u64 n, u64 flip, u
     return fail(ctx, CAFS_ECUDA, "ncclAllReduce (samples)");
   TRY(shard_count_enqueue(ctx, x, n, flip, mult, cm->hdr_all, cm->world, cm->samples,
                           cm->send + tiny_off, cm->send, cap, st));
-  if (ncclAllGather(cm->send, cm->recv, row, ncclUint64, cm->nc, st) != ncclSuccess)
-    return fail(ctx, CAFS_ECUDA, "ncclAllGather (pair tables)");
-  launch_shard_tiny_gather(cm->recv, cm->world, row, tiny_off, cm->tiny_sum, st);
-  TRY(shard_finish_enqueue(ctx, x, n, flip, cm->tiny_sum, cm->recv, cm->world, cap, row, st));
-  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->d_ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
-  ctx->launches += 4;  // header (2), samples, tiny gather
-  CKL();
-  return CAFS_OK;
+  ctx->launches += 3;  // header (2), samples
+  return sharded_exchange(ctx, cm, x, n, flip, st, 0);
 }
 
 }  // namespace
@@ -1928,6 +1996,10 @@ int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint
   for (auto& gr : comm->graphs) {
     if (gr.seen && gr.x == (u64)x && gr.n == n && gr.flip == flip && gr.mult == hash_mult) {
       hit = &gr;
+      if (gr.exec && gr.gen != ctx->buf_gen) {  // captured before a buffer moved
+        cudaGraphExecDestroy(gr.exec);
+        gr.exec = nullptr;
+      }
       break;
     }
     if (gr.stamp < lru->stamp) lru = &gr;
@@ -1957,10 +2029,23 @@ int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint
     if (e != cudaSuccess) { hit->exec = nullptr; return fail(ctx, CAFS_ECUDA, "graph instantiate", e); }
     hit->launches = ctx->launches - l0;
     hit->stamp = ++comm->clock;
+    hit->gen = ctx->buf_gen;
     CK(cudaGraphLaunch(hit->exec, st));
   }
   CK(cudaStreamSynchronize(st));
-  return shard_result(ctx, tel, h_status, st);
+  const DevCtl& h = *ctx->h_ctl;
+  if (h.eff_route == CAFS_MAIN && h.merge_bad && h.shard_grow > comm->cap &&
+      h.shard_grow <= kShardCapMax) {
+    // some rank's sorted pairs did not fit the exchange row: every rank saw it
+    // in the same gathered rows, so all grow the row and exchange again from
+    // the pairs their count left on device (later calls use the larger row)
+    u64 cap = comm->cap;
+    while (cap < h.shard_grow) cap <<= 1;
+    TRY(comm_resize(ctx, comm, cap));
+    TRY(sharded_exchange(ctx, comm, x, n, flip, st, 1));
+    CK(cudaStreamSynchronize(st));
+  }
+  return shard_result(ctx, x, n, flip, tel, h_status, st);
 }
 
 }  // extern "C"

@@ -81,6 +81,10 @@ struct DevCtl {
   // --- partitioned count (hashpart.cu) ---
   int32_t hp_ok;                 // the estimate chose the partitioned count for this call
   u32 hp_overflow;               // a partition held more distinct keys than its table
+  // --- sharded merge of the gathered sorted lists ---
+  u32 merge_bad;                 // some rank's list is missing or too long: merge gated off
+  u32 local_hp;                  // this rank counted with the partitioned count (input spilled)
+  u64 shard_grow;                // the longest list a rank could not send (> the exchange cap)
 };
 
 // Device-only scratch allocated right after the DevCtl (not in its host

@@ -146,6 +146,9 @@ __global__ void __launch_bounds__(1024, 1)
     ctl->tiny_failed = 0;
     ctl->tiny_done = 0;
     ctl->hp_overflow = 0;
+    ctl->merge_bad = 0;
+    ctl->local_hp = 0;
+    ctl->shard_grow = 0;
   }
   if (tid < 16) ctl->tiny_counts[tid] = 0;
   if (tid < kListStripes) ctl->g_fill[tid] = 0;
@@ -346,8 +349,8 @@ void launch_estimate(const void* x, u64 n, u64 flip, int check_prefix, DevCtl* c
 }
 
 void launch_estimate_sharded(const u64* samples, const u64* ghdr, int world, DevCtl* ctl,
-                             cudaStream_t st) {
-  estimate_kernel<0><<<1, 1024, 0, st>>>(samples, kSampleTarget, 0, 0, ctl, ghdr, world, 0);
+                             cudaStream_t st, int opts) {
+  estimate_kernel<0><<<1, 1024, 0, st>>>(samples, kSampleTarget, 0, 0, ctl, ghdr, world, opts);
 }
 
 void launch_monotone_scan(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,

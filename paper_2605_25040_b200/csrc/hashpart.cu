@@ -103,6 +103,11 @@ struct HpArgs {
   u64 e0, e1;      // empty-slot markers: e1 in E0's two buckets ma, mb, e0 elsewhere
   u32 ma, mb;
   int gate;
+  // the sharded merge (hp_reduce<KK, true>): every rank's sorted (key, count)
+  // list gathered in rows [np, keys[cap], counts[cap]] of `row` words
+  const u64* recv;
+  u64 row, cap;
+  int shard;
 };
 
 __device__ __forceinline__ u64 hp_marker(const HpArgs& a, u32 b) {
@@ -152,6 +157,79 @@ __device__ __forceinline__ u64 hp_spill_pos(u64 v0, u32 w, u32 j) {
   return (v0 + (u64)r * kHpRound + (u64)q * kHpThreads + (u64)w * 32) * KPV + within;
 }
 
+// The partition map from the estimate's 1024 order-mapped samples, by a whole
+// 1024-thread CTA: span [lo, hi] -> shift sh (2^sh-wide fine bins), fine-bin
+// histogram, bin -> partition (half sample mass before the bin, half its
+// position in the span).  `fh` is kHpFine u32 of scratch, `rl` 128 u64.
+__device__ void hp_build_pmap(const u64* samp, unsigned short* pmap, u32* fh, u64* rl, u64* s_lo,
+                              int* s_sh) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (u32 i = tid; i < kHpFine; i += kHpThreads) fh[i] = 0;
+  const u64 sv = __ldcg(&samp[tid]);
+  u64 lo = sv, hi = sv;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = l2 < lo ? l2 : lo;
+    hi = h2 > hi ? h2 : hi;
+  }
+  if (lane == 0) { rl[wid] = lo; rl[32 + wid] = hi; }
+  __syncthreads();
+  if (wid == 0) {
+    lo = rl[lane];
+    hi = rl[32 + lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+      lo = l2 < lo ? l2 : lo;
+      hi = h2 > hi ? h2 : hi;
+    }
+    if (lane == 0) {
+      int sh = 0;
+      while (sh < 63 && ((hi - lo) >> sh) >= (u64)kHpFine) ++sh;
+      *s_lo = lo;
+      *s_sh = sh;
+    }
+  }
+  __syncthreads();
+  const u64 d = (sv - *s_lo) >> *s_sh;
+  atomicAdd(&fh[d < (u64)kHpFine ? (u32)d : kHpFine - 1], 1u);
+  __syncthreads();
+  // exclusive scan of the fine bins: kHpFine / 1024 per thread
+  constexpr int FPT = kHpFine / kHpThreads;
+  u32 vf[FPT], s = 0;
+#pragma unroll
+  for (int j = 0; j < FPT; ++j) { vf[j] = fh[tid * FPT + j]; s += vf[j]; }
+  u32 inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  u32* ws = (u32*)(rl + 64);
+  if (lane == 31) ws[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    u32 w = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    ws[32 + lane] = w;
+  }
+  __syncthreads();
+  u32 run = inc - s + (wid ? ws[32 + wid - 1] : 0);
+#pragma unroll
+  for (int j = 0; j < FPT; ++j) {
+    const u32 f = tid * FPT + j;
+    const u32 p = (run * (kHpP / 2)) / kSampleTarget + (f * (kHpP / 2)) / kHpFine;
+    pmap[f] = (unsigned short)(p < (u32)kHpP ? p : kHpP - 1);
+    run += vf[j];
+  }
+  __syncthreads();
+}
+
 template <int KK>
 __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
   pdl_begin();
@@ -187,76 +265,7 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
   if (tid == 0) { ncell_extra = 0; sclaims = 0; }
   if (tid < 33) wsp[tid] = 0;
   // ---- prologue: partition map from the estimate's 1024 samples ----
-  {
-    const u64* samp = est_scratch(a.ctl)->samples;
-    u32* fh = tcnt;  // fine histogram (the counts are zeroed below)
-    for (u32 i = tid; i < kHpFine; i += kHpThreads) fh[i] = 0;
-    const u64 sv = __ldcg(&samp[tid]);
-    u64 lo = sv, hi = sv;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const u64 l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
-      lo = l2 < lo ? l2 : lo;
-      hi = h2 > hi ? h2 : hi;
-    }
-    u64* rl = queue;  // per-warp partials
-    if (lane == 0) { rl[wid] = lo; rl[32 + wid] = hi; }
-    __syncthreads();
-    if (wid == 0) {
-      lo = rl[lane];
-      hi = rl[32 + lane];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const u64 l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
-        lo = l2 < lo ? l2 : lo;
-        hi = h2 > hi ? h2 : hi;
-      }
-      if (lane == 0) {
-        int sh = 0;
-        while (sh < 63 && ((hi - lo) >> sh) >= (u64)kHpFine) ++sh;
-        s_lo = lo;
-        s_sh = sh;
-      }
-    }
-    __syncthreads();
-    const u64 d = (sv - s_lo) >> s_sh;
-    atomicAdd(&fh[d < (u64)kHpFine ? (u32)d : kHpFine - 1], 1u);
-    __syncthreads();
-    // exclusive scan of the fine bins: kHpFine / 1024 per thread
-    constexpr int FPT = kHpFine / kHpThreads;
-    u32 vf[FPT], s = 0;
-#pragma unroll
-    for (int j = 0; j < FPT; ++j) { vf[j] = fh[tid * FPT + j]; s += vf[j]; }
-    u32 inc = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += t;
-    }
-    u32* ws = (u32*)(queue + 64);
-    if (lane == 31) ws[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      u32 w = ws[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const u32 t = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += t;
-      }
-      ws[32 + lane] = w;
-    }
-    __syncthreads();
-    u32 run = inc - s + (wid ? ws[32 + wid - 1] : 0);
-#pragma unroll
-    for (int j = 0; j < FPT; ++j) {
-      const u32 f = tid * FPT + j;
-      // half sample mass, half span position (both monotone in f)
-      const u32 p = (run * (kHpP / 2)) / kSampleTarget + (f * (kHpP / 2)) / kHpFine;
-      pmap[f] = (unsigned short)(p < (u32)kHpP ? p : kHpP - 1);
-      run += vf[j];
-    }
-    __syncthreads();
-  }
+  hp_build_pmap(est_scratch(a.ctl)->samples, pmap, tcnt, queue, &s_lo, &s_sh);
   for (u32 i = tid; i < kHpS; i += kHpThreads) {
     tkeys[i] = hp_marker(a, i >> 1);
     tcnt[i] = 0;
@@ -526,10 +535,11 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
 // the partition's sorted distinct keys and counts in its staging slot, and its
 // (pairs, rows) in pd / pr for hp_place.
 constexpr int kRdUnroll = 4;
-template <int KK>
+template <int KK, bool SH>
 __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 G) {
   pdl_begin();
   if (!gate_open(a.ctl, a.gate)) return;
+  if (SH && a.ctl->merge_bad) return;
   using K = typename KeyT<KK>::T;
   constexpr int KPV = 16 / sizeof(K);
   extern __shared__ __align__(128) unsigned char smem[];
@@ -554,7 +564,8 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
   const K* part = (const K*)a.part + head;
   // segment table: j < G cells of CTA j, G <= j < 2G spill of CTA j - G
   u32 len = 0;
-  if ((u32)tid < 2 * G) {
+  const u32 nseg = SH ? G : 2 * G;  // sharded merge: one segment per rank's list
+  if ((u32)tid < nseg) {
     const bool cell = (u32)tid < G;
     const u32 c = cell ? tid : tid - G;
     const u32* o = (cell ? a.cpofs : a.spofs) + (size_t)c * (kHpP + 1);
@@ -582,9 +593,8 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
     wsum[lane] = w;
   }
   __syncthreads();
-  if ((u32)tid <= 2 * G) segs[tid] = inc - len + (wid ? (u32)wsum[wid - 1] : 0u);
+  if ((u32)tid <= nseg) segs[tid] = inc - len + (wid ? (u32)wsum[wid - 1] : 0u);
   __syncthreads();
-  const u32 nseg = 2 * G, total = segs[nseg];
 
   auto insert = [&](u64 k, u32 w) {
     if (k == kEmpty) { atomicAdd(&sent, (unsigned long long)w); return; }
@@ -613,7 +623,11 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
         const u32 i = i0 + r * 32;
         w[r] = 0;
         if (i < len_j) {
-          if (cell) {
+          if (SH) {
+            const u64* L = a.recv + (size_t)j * a.row;
+            k[r] = L[1 + b + i];
+            w[r] = (u32)L[1 + a.cap + b + i];
+          } else if (cell) {
             k[r] = a.cellk[(size_t)j * kHpCellCap + b + i];
             w[r] = a.cellw[(size_t)j * kHpCellCap + b + i];
           } else {
@@ -709,6 +723,7 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
 __global__ void __launch_bounds__(256) hp_place_kernel(HpArgs a) {
   pdl_begin();
   if (!gate_open(a.ctl, a.gate)) return;
+  if (a.shard && a.ctl->merge_bad) return;
   __shared__ u64 wd[8], wr[8], wsc[8];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u32 p = blockIdx.x;
@@ -756,11 +771,12 @@ __global__ void __launch_bounds__(256) hp_place_kernel(HpArgs a) {
   if (p == gridDim.x - 1 && tid == 0) {
     const u64 tot_d = D + dd, tot_r = run;
     const bool bad = *((volatile u32*)&a.ctl->hp_overflow) != 0;
+    const u64 expect = a.shard ? a.ctl->n_global : a.n;  // sharded merge: the column's N
     a.poffs[tot_d] = tot_r;
     a.ctl->npairs = tot_d;
     a.ctl->total = tot_r;
-    a.ctl->sum_error = !bad && tot_r != a.n;
-    a.ctl->pairs_ready = !bad && tot_r == a.n;
+    a.ctl->sum_error = !bad && tot_r != expect;
+    a.ctl->pairs_ready = !bad && tot_r == expect;
   }
 }
 
@@ -812,6 +828,54 @@ __global__ void __launch_bounds__(1024) hp_restore_kernel(HpArgs a, u32 G) {
     }
     base = woff[m];
     __syncthreads();
+  }
+}
+
+// The sharded merge's segment table: every rank's gathered list (sorted,
+// order-mapped keys) cut at the partitions' key boundaries, which follow
+// from the partition map of the (identical, all-reduced) samples: partition
+// p starts at the first fine bin mapped to p or above.  CTA r: list r.
+__global__ void __launch_bounds__(kHpThreads, 1) hp_shard_bounds_kernel(HpArgs a) {
+  pdl_begin();
+  if (!gate_open(a.ctl, kGateMain) || a.ctl->merge_bad) return;
+  __shared__ unsigned short pmap[kHpFine];
+  __shared__ u32 fh[kHpFine];
+  __shared__ u64 rl[128];
+  __shared__ u64 bound[kHpP + 1];
+  __shared__ unsigned char has[kHpP + 1];  // a bin starts partition p (else: past every key)
+  __shared__ u64 s_lo;
+  __shared__ int s_sh;
+  const int tid = threadIdx.x;
+  const u32 r = blockIdx.x;
+  if (r == 0 && tid == 0) a.ctl->hp_overflow = 0;  // the merge's own overflow flag
+  hp_build_pmap(est_scratch(a.ctl)->samples, pmap, fh, rl, &s_lo, &s_sh);
+  for (u32 p = tid; p <= kHpP; p += kHpThreads) has[p] = 0;
+  __syncthreads();
+  const u64 lo = s_lo;
+  const int sh = s_sh;
+  if (tid == 0) { bound[0] = 0; has[0] = 1; }
+  for (u32 f = 1 + tid; f < (u32)kHpFine; f += kHpThreads) {
+    const u32 p0 = pmap[f - 1], p1 = pmap[f];
+    const u64 off = (u64)f << sh;
+    if (off > ~0ull - lo) continue;  // the bin starts past the largest key: holds none
+    for (u32 q = p0 + 1; q <= p1; ++q) { bound[q] = lo + off; has[q] = 1; }
+  }
+  __syncthreads();
+  const u64* L = a.recv + (size_t)r * a.row;
+  const u64 np = L[0];
+  u32* out = a.cpofs + (size_t)r * (kHpP + 1);
+  for (u32 p = tid; p <= kHpP; p += kHpThreads) {
+    u64 pos = np;
+    if (p < (u32)kHpP && has[p]) {  // the first index with key >= bound[p]
+      u64 lo2 = 0, hi2 = np;
+      const u64 kb = bound[p];
+      while (lo2 < hi2) {
+        const u64 mid = (lo2 + hi2) >> 1;
+        if (L[1 + mid] < kb) lo2 = mid + 1; else hi2 = mid;
+      }
+      pos = lo2;
+    }
+    out[p] = (u32)pos;
   }
 }
 
@@ -883,13 +947,14 @@ static cudaError_t hp_launch_t(const HpArgs& a, int G, cudaStream_t st) {
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
     cudaError_t e = hp_attr(hp_count_kernel<KK>, kHpCountSmem);
-    if (e == cudaSuccess) e = hp_attr(hp_reduce_kernel<KK>, kHpReduceSmem);
+    if (e == cudaSuccess) e = hp_attr(hp_reduce_kernel<KK, false>, kHpReduceSmem);
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
   cudaError_t e = launch_pdl(kPdlCount, hp_count_kernel<KK>, G, kHpThreads, kHpCountSmem, st, a);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kPdlCount, hp_reduce_kernel<KK>, kHpP, kHpThreads, kHpReduceSmem, st, a, (u32)G);
+  e = launch_pdl(kPdlCount, hp_reduce_kernel<KK, false>, kHpP, kHpThreads, kHpReduceSmem, st, a,
+                 (u32)G);
   if (e != cudaSuccess) return e;
   return launch_pdl(kPdlCount, hp_place_kernel, kHpP, 256, 0, st, a);
 }
@@ -902,6 +967,31 @@ cudaError_t launch_hp_count(const HpBufs& b, const void* x, u64 n, u64 flip, Dev
   if (kk == 1) return hp_launch_t<1>(a, G, st);
   if (kk == 2) return hp_launch_t<2>(a, G, st);
   return hp_launch_t<0>(a, G, st);
+}
+
+// The sharded merge: the gathered sorted lists -> the global sorted pairs and
+// their offsets in pk / pc / poffs (every rank, the same result).
+cudaError_t launch_hp_shard_merge(const HpBufs& b, const u64* recv, int world, u64 cap, u64 row,
+                                  DevCtl* ctl, u64* pk, u64* pc, u64* poffs, cudaStream_t st) {
+  HpArgs a = hp_args(b, nullptr, 0, 0, ctl, pk, pc, poffs, kGateMain, world);
+  a.recv = recv;
+  a.row = row;
+  a.cap = cap;
+  a.shard = 1;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = hp_attr(hp_reduce_kernel<0, true>, kHpReduceSmem);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  cudaError_t e = launch_pdl(kPdlCount, hp_shard_bounds_kernel, world, kHpThreads, 0, st, a);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(kPdlCount, hp_reduce_kernel<0, true>, kHpP, kHpThreads, kHpReduceSmem, st, a,
+                 (u32)world);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(kPdlCount, hp_place_kernel, kHpP, 256, 0, st, a);
 }
 
 void launch_hp_restore(const HpBufs& b, void* x, u64 n, u64 flip, int num_sms, cudaStream_t st,

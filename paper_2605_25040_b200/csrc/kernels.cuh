@@ -18,14 +18,16 @@ void launch_estimate(const void* x, u64 n, u64 flip, int check_prefix, DevCtl* c
 void launch_monotone_scan(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,
                           cudaStream_t st, int kk = 0);
 void launch_estimate_sharded(const u64* samples, const u64* ghdr, int world, DevCtl* ctl,
-                             cudaStream_t st);
+                             cudaStream_t st, int opts = 0);
 // shard.cu: the stream-ordered sharded pipeline's own kernels
 void launch_shard_header(const u64* x, u64 n, u64 flip, u64* hdr, int num_sms, cudaStream_t st);
 void launch_shard_samples(const u64* x, u64 n, u64 flip, const u64* ghdr, int world, int rank,
                           u64* samples, DevCtl* ctl, cudaStream_t st);
 void launch_shard_tiny_pack(const DevCtl* ctl, u64* out, cudaStream_t st);
 void launch_shard_pack_pairs(DevCtl* ctl, const u64* keys, const u64* cnts, u64* send,
-                             u64 cap, cudaStream_t st);
+                             u64 cap, cudaStream_t st, int from_local = 0);
+void launch_shard_merge_check(DevCtl* ctl, const u64* recv, int world, u64 cap, u64 row,
+                              cudaStream_t st);
 void launch_shard_tiny_finish(DevCtl* ctl, const u64* tiny_sum, u64* pkeys, u64* pcnt, u64* poffs,
                               cudaStream_t st);
 void launch_shard_merge(DevCtl* ctl, const u64* recv, int world, u64 cap, u64 row, u64* gkeys,
@@ -59,6 +61,8 @@ struct HpBufs {
 size_t hp_scratch_bytes(int num_sms);
 cudaError_t launch_hp_count(const HpBufs& b, const void* x, u64 n, u64 flip, DevCtl* ctl, u64* pk,
                             u64* pc, u64* poffs, int num_sms, cudaStream_t st, int gate, int kk);
+cudaError_t launch_hp_shard_merge(const HpBufs& b, const u64* recv, int world, u64 cap, u64 row,
+                                  DevCtl* ctl, u64* pk, u64* pc, u64* poffs, cudaStream_t st);
 void launch_hp_restore(const HpBufs& b, void* x, u64 n, u64 flip, int num_sms, cudaStream_t st,
                        int kk);
 // emit.cu

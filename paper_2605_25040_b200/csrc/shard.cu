@@ -88,18 +88,30 @@ __global__ void shard_tiny_pack_kernel(const DevCtl* ctl, u64* out) {
 }
 
 // This rank's sorted (key, count) table for the all-gather: [np, keys[cap],
-// counts[cap]]; np = ~0 when it cannot be exchanged this way (table
-// overflow, more than cap pairs, or pairs not sorted on device).
+// counts[cap]]; np = ~0 when the pairs are lost or unsorted (table overflow);
+// np > cap: sorted, but too many for this exchange row (the pairs are not
+// sent; the caller may grow the row and exchange again, from_local).
 __global__ void shard_pack_pairs_kernel(DevCtl* ctl, const u64* keys, const u64* cnts,
-                                        u64* send, u64 cap) {
+                                        u64* send, u64 cap, int from_local) {
   const bool main = gate_open(ctl, kGateMain);
-  const bool ok = main && !ctl->overflow && ctl->pairs_ready && ctl->npairs <= cap;
-  const u64 np = main ? (ok ? ctl->npairs : ~0ull) : 0ull;
+  bool sorted;
+  u64 np;
+  if (from_local) {  // a second exchange: the count's state was saved by the first
+    sorted = ctl->local_sorted && !ctl->local_overflow;
+    np = ctl->local_npairs;
+  } else {
+    sorted = main && !ctl->overflow && !ctl->hp_overflow && ctl->pairs_ready;
+    np = ctl->npairs;
+  }
+  const bool ok = main && sorted && np <= cap;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    send[0] = np;
-    ctl->local_npairs = main ? ctl->npairs : 0;
-    ctl->local_sorted = main && ctl->pairs_ready;
-    ctl->local_overflow = main && ctl->overflow;
+    send[0] = main ? (sorted ? np : ~0ull) : 0ull;
+    if (!from_local) {
+      ctl->local_npairs = main ? ctl->npairs : 0;
+      ctl->local_sorted = main && ctl->pairs_ready && !ctl->hp_overflow;
+      ctl->local_overflow = main && (ctl->overflow || ctl->hp_overflow);
+      ctl->local_hp = main && ctl->hp_ok && ctl->range_len == 0;
+    }
   }
   if (!ok) return;
   const u64 stride = (u64)gridDim.x * blockDim.x;
@@ -158,6 +170,38 @@ __global__ void shard_merge_reset_kernel(DevCtl* ctl, const u64* recv, int world
   }
 }
 
+// Before the sorted merge: reset the per-call merge state; a rank whose list
+// is missing (np = ~0) or longer than the row (np > cap) gates the merge off
+// on every rank (they all see the same rows); shard_grow = the longest list
+// that did not fit, for the caller to grow the row.
+__global__ void shard_merge_check_kernel(DevCtl* ctl, const u64* recv, int world, u64 cap, u64 row) {
+  if (!gate_open(ctl, kGateMain)) return;
+  __shared__ int bad;
+  __shared__ unsigned long long grow;
+  if (threadIdx.x == 0) { bad = 0; grow = 0; }
+  __syncthreads();
+  for (int r = threadIdx.x; r < world; r += blockDim.x) {
+    const u64 np = recv[(u64)r * row];
+    if (np == ~0ull || np > cap) atomicOr(&bad, 1);
+    if (np != ~0ull && np > cap) atomicMax(&grow, (unsigned long long)np);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->npairs = 0;
+    ctl->total = 0;
+    ctl->pairs_ready = 0;
+    ctl->sum_error = 0;
+    ctl->need_large = 0;
+    ctl->merge_bad = bad;
+    ctl->shard_grow = grow;
+  }
+}
+
+void launch_shard_merge_check(DevCtl* ctl, const u64* recv, int world, u64 cap, u64 row,
+                              cudaStream_t st) {
+  shard_merge_check_kernel<<<1, 256, 0, st>>>(ctl, recv, world, cap, row);
+}
+
 __global__ void shard_merge_insert_kernel(DevCtl* ctl, const u64* recv, int world, u64 cap,
                                           u64 row, u64* gkeys, u64* gcnt, u32* glist) {
   if (!gate_open(ctl, kGateMain) || ctl->overflow) return;
@@ -188,8 +232,10 @@ void launch_shard_tiny_pack(const DevCtl* ctl, u64* out, cudaStream_t st) {
 }
 
 void launch_shard_pack_pairs(DevCtl* ctl, const u64* keys, const u64* cnts, u64* send,
-                             u64 cap, cudaStream_t st) {
-  shard_pack_pairs_kernel<<<8, 1024, 0, st>>>(ctl, keys, cnts, send, cap);
+                             u64 cap, cudaStream_t st, int from_local) {
+  const u64 g = cap / 8192 + 1;
+  shard_pack_pairs_kernel<<<(unsigned)(g < 148 ? g : 148), 1024, 0, st>>>(ctl, keys, cnts, send,
+                                                                          cap, from_local);
 }
 
 void launch_shard_tiny_finish(DevCtl* ctl, const u64* tiny_sum, u64* pkeys, u64* pcnt, u64* poffs,

@@ -477,7 +477,7 @@ def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTeleme
         native = (fast and comm.device is not None and hasattr(ops, "sort_native")
                   and _native_enabled())
         if native and _sort_sharded_native(x_local, comm, ops, tel, mult):
-            tel.sharded_path = "native"
+            pass  # "native", or "native+host" when the merge continued on the host
         elif not native and fast and _sort_sharded_streamed(x_local, comm, ops, tel, mult):
             tel.sharded_path = "streamed"
         else:
@@ -537,7 +537,9 @@ def _sort_sharded_native(x_local, comm, ops, tel, mult: int) -> bool:
         sizes = [int(v[0]) for v in comm.all_gather_ints([int(x_local.shape[0])])]
         tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, 4)
         _main_exchange(x_local, comm, ops, tel, ops.shard_local_pairs(), sizes, tel.decision)
+        tel.sharded_path = "native+host"  # counted natively, merged on the host-driven path
         return True
+    tel.sharded_path = "native"
     tel.counted_total = int(t.counted_total)
     tel.pairs = int(t.pairs)
     if tel.decision.route is Route.MAIN:
@@ -596,7 +598,9 @@ def _sort_sharded_streamed(x_local, comm, ops, tel, mult: int) -> bool:
         sizes = [int(v) for v in hdr_all.view(world, 8)[:, 0].cpu().tolist()]
         tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, 4)
         _main_exchange(x_local, comm, ops, tel, ops.shard_local_pairs(), sizes, tel.decision)
+        tel.sharded_path = "native+host"  # counted natively, merged on the host-driven path
         return True
+    tel.sharded_path = "native"
     tel.counted_total = int(t.counted_total)
     tel.pairs = int(t.pairs)
     if tel.decision.route is Route.MAIN:

@@ -2,8 +2,9 @@
 communicator, collectives inside one graph-replayed enqueue) at one NCCL rank
 on the GPU: bit-exact against np.sort and the oracle's decision on every route,
 across direct, captured and replayed calls; columns the device cannot finish
-continue on the host-driven path (> 8192 pairs: from the already-counted
-pairs, still labelled "native"; fallback routes: "host").  (More ranks need more GPUs than this pool
+finish natively too (> 8192 pairs per rank: the partitioned count sorts each
+shard's pairs, the library grows its exchange row once and merges the
+gathered lists on device); fallback routes take the host-driven path ("host").  (More ranks need more GPUs than this pool
 gives: the 2-rank tests in test_sharded_gpu.py share one GPU over gloo.)"""
 
 import os
@@ -38,6 +39,8 @@ cols = {
     "codes": (rng.integers(0, 4000, 2_000_000), "native"),
     "main_hash": (rng.choice(rng.integers(-2**62, 2**62, 3000), 1_000_000), "native"),
     "many_pairs": (rng.choice(rng.integers(-2**62, 2**62, 50_000), 2_000_000), "native"),
+    "many_pairs_zipf": (rng.integers(-2**62, 2**62, 300_000)[
+        np.minimum(rng.zipf(1.2, 6_000_000), 300_000) - 1], "native"),
     "fallback": (rng.integers(-2**62, 2**62, 300_000), "host"),
     "sorted": (np.arange(-50_000, 50_000, dtype=np.int64), "native"),
     "uint64": (rng.choice(rng.integers(0, 2**63, 500, dtype=np.uint64) * 2, 600_000), "native"),
