@@ -280,6 +280,12 @@ int cafs_comm_destroy(cafs_comm_t* comm);
 int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint64_t n,
                           int is_signed, uint64_t hash_mult, cafs_telemetry_t* tel, int* h_status,
                           void* stream);
+/* The same for int32 (is_signed = 1) / uint32 (is_signed = 0) shards: 4 bytes
+ * per key read and written on every rank (the tables and the exchange hold
+ * the keys' 64-bit order-mapped widening, as cafs_sort_i32 does). */
+int cafs_sort_i32_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int32_t* d_x, uint64_t n,
+                          int is_signed, uint64_t hash_mult, cafs_telemetry_t* tel, int* h_status,
+                          void* stream);
 
 /* After finish returned status 1 on the main route: this shard's (key, count)
  * pairs from the count phase, for the host-driven merge; *h_npairs = ~0 when

@@ -85,6 +85,8 @@ SIGNATURES = {
     "cafs_comm_destroy": (_I, [_P]),
     "cafs_sort_i64_sharded": (_I, [_P, _P, _P, _U64, _I, _U64, ctypes.POINTER(Telemetry),
                                    ctypes.POINTER(_I), _P]),
+    "cafs_sort_i32_sharded": (_I, [_P, _P, _P, _U64, _I, _U64, ctypes.POINTER(Telemetry),
+                                   ctypes.POINTER(_I), _P]),
     "cafs_shard_sample_i64": (_I, [_P, _P, _U64, _I, _P, _I, _I, _P, _P]),
     "cafs_shard_count_i64": (_I, [_P, _P, _U64, _I, _U64, _P, _I, _P, _P, _P, _U64, _P]),
     "cafs_shard_finish_i64": (_I, [_P, _P, _U64, _I, _P, _P, _I, _U64, ctypes.POINTER(Telemetry),

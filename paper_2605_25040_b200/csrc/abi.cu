@@ -1045,27 +1045,27 @@ u64 host_fmix64(u64 z) {
 
 // estimate on the gathered samples -> route; tiny count or local hash count ->
 // sorted local pairs -> this rank's send row [np, keys[cap], counts[cap]]
-int shard_count_enqueue(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, u64 mult,
+int shard_count_enqueue(cafs_ctx_t* ctx, const void* x, u64 n, u64 flip, u64 mult,
                         const u64* hdr_all, int world, const u64* samples, u64* tiny, u64* send,
-                        u64 cap, cudaStream_t st) {
+                        u64 cap, cudaStream_t st, int kk = 0) {
   DevCtl* c = ctx->d_ctl;
   // the partitioned count gives this shard's pairs sorted on device for any
   // number of keys (the table path's pair sort stops at 8192)
   const bool hp = hp_allowed(n, false);
-  if (hp) TRY(ensure_hp(ctx, n, 0));
+  if (hp) TRY(ensure_hp(ctx, n, kk));
   launch_estimate_sharded(samples, hdr_all, world, c, st, hp ? kEstHp : 0);
-  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny);
+  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny, kk);
   launch_shard_tiny_pack(c, tiny, st);
   cudaError_t e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                                    ctx->num_sms, st, 0, kGateMainDense, ctx->dense);
+                                    ctx->num_sms, st, 0, kGateMainDense, ctx->dense, kk);
   if (hp && e == cudaSuccess) {
     e = launch_hp_count(hp_bufs(ctx), x, n, flip, c, ctx->pk_b, ctx->pc_b, ctx->poffs,
-                        ctx->num_sms, st, kGateMainHP, 0);
+                        ctx->num_sms, st, kGateMainHP, kk);
     ctx->launches += 3;
   }
   if (e == cudaSuccess)
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                          ctx->num_sms, st, 1, kGateMainHash, ctx->dense);
+                          ctx->num_sms, st, 1, kGateMainHash, ctx->dense, kk);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
   launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
                  kGateMainOld);
@@ -1082,8 +1082,9 @@ int shard_count_enqueue(cafs_ctx_t* ctx, const u64* x, u64 n, u64 flip, u64 mult
 
 // tiny totals or the merge of every rank's row -> sorted global pairs -> this
 // rank's slice emit (every kernel gated on the device decision)
-int shard_finish_enqueue(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, const u64* tiny_sum,
-                         const u64* recv, int world, u64 cap, u64 row, cudaStream_t st) {
+int shard_finish_enqueue(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, const u64* tiny_sum,
+                         const u64* recv, int world, u64 cap, u64 row, cudaStream_t st,
+                         int kk = 0) {
   DevCtl* c = ctx->d_ctl;
   launch_shard_tiny_finish(c, tiny_sum, ctx->pk_b, ctx->pc_b, ctx->poffs, st);
   // the union of every rank's sorted list (sorter.py:276-285): key-range
@@ -1096,7 +1097,7 @@ int shard_finish_enqueue(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, const u64* ti
   cudaError_t e = launch_hp_shard_merge(mb, recv, world, cap, row, c, ctx->pk_b, ctx->pc_b,
                                         ctx->poffs, st);
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "sharded merge", e);
-  launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, 0, 0, true);
+  launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, 0, kk, true);
   ctx->launches += 6;
   CKL();
   return CAFS_OK;
@@ -1104,8 +1105,8 @@ int shard_finish_enqueue(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, const u64* ti
 
 // after the control block reached the host mirror: the status every rank agrees
 // on (same gathered data) and the telemetry
-int shard_result(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cafs_telemetry_t* tel, int* h_status,
-                 cudaStream_t st) {
+int shard_result(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cafs_telemetry_t* tel, int* h_status,
+                 cudaStream_t st, int kk = 0) {
   const DevCtl& h = *ctx->h_ctl;
   const int eff = h.eff_route;
   int status = 1;  // 1: the caller runs the host-driven sharded path
@@ -1114,7 +1115,7 @@ int shard_result(cafs_ctx_t* ctx, u64* x, u64 n, u64 flip, cafs_telemetry_t* tel
   if (status != 0 && eff == CAFS_MAIN && h.local_hp) {
     // the partitioned count spilled into this shard: rebuild it from the cells
     // and the spill for the host-driven path (which may sort the rows again)
-    launch_hp_restore(hp_bufs(ctx), x, n, flip, ctx->num_sms, st, 0);
+    launch_hp_restore(hp_bufs(ctx), x, n, flip, ctx->num_sms, st, kk);
     ctx->launches++;
     CKL();
     CK(cudaStreamSynchronize(st));
@@ -1850,6 +1851,7 @@ struct cafs_comm_t {
     int seen = 0;
     uint64_t launches = 0, stamp = 0;
     uint64_t gen = 0;  // the context's buf_gen at capture
+    int kk = 0;        // key kind
     cudaGraphExec_t exec = nullptr;
   } graphs[8];
   uint64_t clock = 0;
@@ -1919,8 +1921,8 @@ constexpr u64 kShardCapMax = 1ull << 20;
 
 // the pair tables' all-gather, the merge and this rank's slice emit; again
 // (from_local) after the row grew: the rows are re-packed from the count's pairs
-int sharded_exchange(cafs_ctx_t* ctx, cafs_comm_t* cm, u64* x, u64 n, u64 flip, cudaStream_t st,
-                     int from_local) {
+int sharded_exchange(cafs_ctx_t* ctx, cafs_comm_t* cm, void* x, u64 n, u64 flip, cudaStream_t st,
+                     int from_local, int kk) {
   const u64 cap = cm->cap, row = cm->row, tiny_off = 1 + 2 * cap;
   if (from_local) {
     launch_shard_pack_pairs(ctx->d_ctl, ctx->pk_b, ctx->pc_b, cm->send, cap, st, 1);
@@ -1929,7 +1931,7 @@ int sharded_exchange(cafs_ctx_t* ctx, cafs_comm_t* cm, u64* x, u64 n, u64 flip, 
   if (ncclAllGather(cm->send, cm->recv, row, ncclUint64, cm->nc, st) != ncclSuccess)
     return fail(ctx, CAFS_ECUDA, "ncclAllGather (pair tables)");
   launch_shard_tiny_gather(cm->recv, cm->world, row, tiny_off, cm->tiny_sum, st);
-  TRY(shard_finish_enqueue(ctx, x, n, flip, cm->tiny_sum, cm->recv, cm->world, cap, row, st));
+  TRY(shard_finish_enqueue(ctx, x, n, flip, cm->tiny_sum, cm->recv, cm->world, cap, row, st, kk));
   CK(cudaMemcpyAsync(ctx->h_ctl, ctx->d_ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
   ctx->launches += 1;  // tiny gather
   CKL();
@@ -1954,38 +1956,43 @@ int comm_resize(cafs_ctx_t* ctx, cafs_comm_t* c, u64 cap) {
   return CAFS_OK;
 }
 
-int sharded_enqueue(cafs_ctx_t* ctx, cafs_comm_t* cm, u64* x, u64 n, u64 flip, u64 mult,
-                    cudaStream_t st) {
+int sharded_enqueue(cafs_ctx_t* ctx, cafs_comm_t* cm, void* x, u64 n, u64 flip, u64 mult,
+                    cudaStream_t st, int kk) {
   const u64 cap = cm->cap, row = cm->row, tiny_off = 1 + 2 * cap;
-  launch_shard_header(x, n, flip, cm->hdr, ctx->num_sms, st);
+  launch_shard_header(x, n, flip, cm->hdr, ctx->num_sms, st, kk);
   if (ncclAllGather(cm->hdr, cm->hdr_all, kShardHdrWords, ncclUint64, cm->nc, st) != ncclSuccess)
     return fail(ctx, CAFS_ECUDA, "ncclAllGather (headers)");
-  launch_shard_samples(x, n, flip, cm->hdr_all, cm->world, cm->rank, cm->samples, ctx->d_ctl, st);
+  launch_shard_samples(x, n, flip, cm->hdr_all, cm->world, cm->rank, cm->samples, ctx->d_ctl, st,
+                       kk);
   if (ncclAllReduce(cm->samples, cm->samples, kSampleTarget, ncclUint64, ncclSum, cm->nc, st) !=
       ncclSuccess)
     return fail(ctx, CAFS_ECUDA, "ncclAllReduce (samples)");
   TRY(shard_count_enqueue(ctx, x, n, flip, mult, cm->hdr_all, cm->world, cm->samples,
-                          cm->send + tiny_off, cm->send, cap, st));
+                          cm->send + tiny_off, cm->send, cap, st, kk));
   ctx->launches += 3;  // header (2), samples
-  return sharded_exchange(ctx, cm, x, n, flip, st, 0);
+  return sharded_exchange(ctx, cm, x, n, flip, st, 0, kk);
 }
 
 }  // namespace
 
 extern "C" {
 
-int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint64_t n,
-                          int is_signed, uint64_t hash_mult, cafs_telemetry_t* tel, int* h_status,
-                          void* stream) {
-  TRY(check_common(ctx, d_x, n));
+}  // extern "C"
+
+namespace {
+
+static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t n, int is_signed,
+                        uint64_t hash_mult, cafs_telemetry_t* tel, int* h_status, void* stream,
+                        int kk) {
+  TRY(check_common(ctx, d_x, n, kk ? 4 : 8));
   if (!comm || !h_status || (hash_mult & 1) == 0) return fail(ctx, CAFS_EINVAL, "bad arguments");
   if (comm->device != ctx->device) return fail(ctx, CAFS_EINVAL, "comm and context devices differ");
   DeviceGuard g(ctx->device);
   CallGuard cg(ctx, stream);
   cudaStream_t st = (cudaStream_t)stream;
   TRY(ensure_main(ctx));
-  const u64 flip = is_signed ? kSign : 0;
-  u64* x = (u64*)d_x;
+  const u64 flip = (is_signed || kk) ? kSign : 0;
+  void* x = d_x;
   static int use_graphs = -1;
   if (use_graphs < 0) {
     const char* e = getenv("CAFS_GRAPHS");
@@ -1994,7 +2001,8 @@ int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint
   cafs_comm_t::Graph* hit = nullptr;
   cafs_comm_t::Graph* lru = &comm->graphs[0];
   for (auto& gr : comm->graphs) {
-    if (gr.seen && gr.x == (u64)x && gr.n == n && gr.flip == flip && gr.mult == hash_mult) {
+    if (gr.seen && gr.x == (u64)x && gr.n == n && gr.flip == flip && gr.mult == hash_mult &&
+        gr.kk == kk) {
       hit = &gr;
       if (gr.exec && gr.gen != ctx->buf_gen) {  // captured before a buffer moved
         cudaGraphExecDestroy(gr.exec);
@@ -2005,7 +2013,7 @@ int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint
     if (gr.stamp < lru->stamp) lru = &gr;
   }
   if (!use_graphs || !ctx->cap_stream) {
-    TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st));
+    TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st, kk));
   } else if (hit && hit->exec) {  // replay
     CK(cudaGraphLaunch(hit->exec, st));
     ctx->launches += hit->launches;
@@ -2014,13 +2022,13 @@ int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint
     if (lru->exec) cudaGraphExecDestroy(lru->exec);
     *lru = cafs_comm_t::Graph();
     lru->x = (u64)x; lru->n = n; lru->flip = flip; lru->mult = hash_mult;
-    lru->seen = 1; lru->stamp = ++comm->clock;
-    TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st));
+    lru->seen = 1; lru->stamp = ++comm->clock; lru->kk = kk;
+    TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st, kk));
   } else {  // second sighting: capture on the context's stream, launch on the caller's
     const uint64_t l0 = ctx->launches;
     cudaGraph_t graph = nullptr;
     CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
-    const int rc = sharded_enqueue(ctx, comm, x, n, flip, hash_mult, ctx->cap_stream);
+    const int rc = sharded_enqueue(ctx, comm, x, n, flip, hash_mult, ctx->cap_stream, kk);
     cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &graph);
     if (rc != CAFS_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "graph capture (sharded)", e);
@@ -2042,10 +2050,27 @@ int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint
     u64 cap = comm->cap;
     while (cap < h.shard_grow) cap <<= 1;
     TRY(comm_resize(ctx, comm, cap));
-    TRY(sharded_exchange(ctx, comm, x, n, flip, st, 1));
+    TRY(sharded_exchange(ctx, comm, x, n, flip, st, 1, kk));
     CK(cudaStreamSynchronize(st));
   }
-  return shard_result(ctx, x, n, flip, tel, h_status, st);
+  return shard_result(ctx, x, n, flip, tel, h_status, st, kk);
+}
+
+}  // namespace
+
+extern "C" {
+
+int cafs_sort_i64_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int64_t* d_x, uint64_t n,
+                          int is_signed, uint64_t hash_mult, cafs_telemetry_t* tel, int* h_status,
+                          void* stream) {
+  return sharded_impl(ctx, comm, d_x, n, is_signed, hash_mult, tel, h_status, stream, 0);
+}
+
+int cafs_sort_i32_sharded(cafs_ctx_t* ctx, cafs_comm_t* comm, int32_t* d_x, uint64_t n,
+                          int is_signed, uint64_t hash_mult, cafs_telemetry_t* tel, int* h_status,
+                          void* stream) {
+  return sharded_impl(ctx, comm, d_x, n, is_signed, hash_mult, tel, h_status, stream,
+                      is_signed ? 1 : 2);
 }
 
 }  // extern "C"

@@ -20,9 +20,10 @@ void launch_monotone_scan(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_s
 void launch_estimate_sharded(const u64* samples, const u64* ghdr, int world, DevCtl* ctl,
                              cudaStream_t st, int opts = 0);
 // shard.cu: the stream-ordered sharded pipeline's own kernels
-void launch_shard_header(const u64* x, u64 n, u64 flip, u64* hdr, int num_sms, cudaStream_t st);
-void launch_shard_samples(const u64* x, u64 n, u64 flip, const u64* ghdr, int world, int rank,
-                          u64* samples, DevCtl* ctl, cudaStream_t st);
+void launch_shard_header(const void* x, u64 n, u64 flip, u64* hdr, int num_sms, cudaStream_t st,
+                         int kk = 0);
+void launch_shard_samples(const void* x, u64 n, u64 flip, const u64* ghdr, int world, int rank,
+                          u64* samples, DevCtl* ctl, cudaStream_t st, int kk = 0);
 void launch_shard_tiny_pack(const DevCtl* ctl, u64* out, cudaStream_t st);
 void launch_shard_pack_pairs(DevCtl* ctl, const u64* keys, const u64* cnts, u64* send,
                              u64 cap, cudaStream_t st, int from_local = 0);

@@ -16,8 +16,9 @@ namespace cafs {
 // Header of this shard (kShardHdrWords words): rows, monotone state of the
 // first kMonoPrefix rows (0 inversion, 1 sorted, 2 sorted prefix of a longer
 // shard -> word 4 holds the full scan's verdict), first and last key.
-__global__ void __launch_bounds__(1024) shard_header_kernel(const u64* __restrict__ x, u64 n,
-                                                            u64 flip, u64* hdr) {
+template <int KK>
+__global__ void __launch_bounds__(1024) shard_header_kernel(const typename KeyT<KK>::T* __restrict__ x,
+                                                            u64 n, u64 flip, u64* hdr) {
   __shared__ int inv;
   if (threadIdx.x == 0) inv = 0;
   __syncthreads();
@@ -27,7 +28,7 @@ __global__ void __launch_bounds__(1024) shard_header_kernel(const u64* __restric
   const u64 i0 = (u64)threadIdx.x * 16;
   u64 a[17];
 #pragma unroll
-  for (int j = 0; j < 17; ++j) a[j] = i0 + j < P ? x[i0 + j] ^ flip : 0;
+  for (int j = 0; j < 17; ++j) a[j] = i0 + j < P ? key_map<KK>(x[i0 + j], flip) : 0;
   int found = 0;
 #pragma unroll
   for (int j = 0; j < 16; ++j) found |= (i0 + j + 1 < P) && a[j + 1] < a[j];
@@ -36,28 +37,31 @@ __global__ void __launch_bounds__(1024) shard_header_kernel(const u64* __restric
   if (threadIdx.x == 0) {
     hdr[0] = n;
     hdr[1] = n <= 1 ? 1 : (inv ? 0 : (n <= kMonoPrefix ? 1 : 2));
-    hdr[2] = n ? x[0] ^ flip : 0;
-    hdr[3] = n ? x[n - 1] ^ flip : 0;
+    hdr[2] = n ? key_map<KK>(x[0], flip) : 0;
+    hdr[3] = n ? key_map<KK>(x[n - 1], flip) : 0;
     hdr[4] = 0;
     hdr[5] = hdr[6] = hdr[7] = 0;
   }
 }
 
 // The rest of a shard whose prefix is sorted (state 2): any inversion -> word 4.
-__global__ void shard_scan_kernel(const u64* __restrict__ x, u64 n, u64 flip, u64* hdr) {
+template <int KK>
+__global__ void shard_scan_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip,
+                                  u64* hdr) {
   if (hdr[1] != 2) return;
   const u64 stride = (u64)gridDim.x * blockDim.x;
   int found = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i + 1 < n; i += stride)
-    found |= (x[i + 1] ^ flip) < (x[i] ^ flip);
+    found |= key_map<KK>(x[i + 1], flip) < key_map<KK>(x[i], flip);
   if (found) hdr[4] = 1;
 }
 
 // The global sample positions i * (N // 1024) (cardinality.py:102-104) that
 // fall in this shard; zeros elsewhere, so an all-reduce SUM assembles the
 // sample.  Also records this rank's slice of the sorted output.
-__global__ void __launch_bounds__(1024) shard_samples_kernel(const u64* __restrict__ x, u64 n,
-                                                             u64 flip, const u64* ghdr, int world,
+template <int KK>
+__global__ void __launch_bounds__(1024) shard_samples_kernel(const typename KeyT<KK>::T* __restrict__ x,
+                                                             u64 n, u64 flip, const u64* ghdr, int world,
                                                              int rank, u64* samples,
                                                              DevCtl* ctl) {
   u64 N = 0, off = 0;
@@ -72,7 +76,7 @@ __global__ void __launch_bounds__(1024) shard_samples_kernel(const u64* __restri
   const u64 m = N < (u64)kSampleTarget ? N : (u64)kSampleTarget;
   const u64 pos = i * stride;
   u64 v = 0;
-  if (i < m && pos >= off && pos < off + n) v = x[pos - off] ^ flip;
+  if (i < m && pos >= off && pos < off + n) v = key_map<KK>(x[pos - off], flip);
   samples[i] = v;
   if (threadIdx.x == 0) {
     ctl->slice[0] = off;
@@ -217,14 +221,31 @@ __global__ void shard_merge_insert_kernel(DevCtl* ctl, const u64* recv, int worl
   }
 }
 
-void launch_shard_header(const u64* x, u64 n, u64 flip, u64* hdr, int num_sms, cudaStream_t st) {
-  shard_header_kernel<<<1, 1024, 0, st>>>(x, n, flip, hdr);
-  shard_scan_kernel<<<num_sms * 4, 512, 0, st>>>(x, n, flip, hdr);
+void launch_shard_header(const void* x, u64 n, u64 flip, u64* hdr, int num_sms, cudaStream_t st,
+                         int kk) {
+  if (kk == 1) {
+    shard_header_kernel<1><<<1, 1024, 0, st>>>((const u32*)x, n, flip, hdr);
+    shard_scan_kernel<1><<<num_sms * 4, 512, 0, st>>>((const u32*)x, n, flip, hdr);
+  } else if (kk == 2) {
+    shard_header_kernel<2><<<1, 1024, 0, st>>>((const u32*)x, n, flip, hdr);
+    shard_scan_kernel<2><<<num_sms * 4, 512, 0, st>>>((const u32*)x, n, flip, hdr);
+  } else {
+    shard_header_kernel<0><<<1, 1024, 0, st>>>((const u64*)x, n, flip, hdr);
+    shard_scan_kernel<0><<<num_sms * 4, 512, 0, st>>>((const u64*)x, n, flip, hdr);
+  }
 }
 
-void launch_shard_samples(const u64* x, u64 n, u64 flip, const u64* ghdr, int world, int rank,
-                          u64* samples, DevCtl* ctl, cudaStream_t st) {
-  shard_samples_kernel<<<1, kSampleTarget, 0, st>>>(x, n, flip, ghdr, world, rank, samples, ctl);
+void launch_shard_samples(const void* x, u64 n, u64 flip, const u64* ghdr, int world, int rank,
+                          u64* samples, DevCtl* ctl, cudaStream_t st, int kk) {
+  if (kk == 1)
+    shard_samples_kernel<1><<<1, kSampleTarget, 0, st>>>((const u32*)x, n, flip, ghdr, world, rank,
+                                                         samples, ctl);
+  else if (kk == 2)
+    shard_samples_kernel<2><<<1, kSampleTarget, 0, st>>>((const u32*)x, n, flip, ghdr, world, rank,
+                                                         samples, ctl);
+  else
+    shard_samples_kernel<0><<<1, kSampleTarget, 0, st>>>((const u64*)x, n, flip, ghdr, world, rank,
+                                                         samples, ctl);
 }
 
 void launch_shard_tiny_pack(const DevCtl* ctl, u64* out, cudaStream_t st) {

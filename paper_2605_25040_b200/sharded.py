@@ -209,12 +209,17 @@ class DeviceOps:
 
     def sort_native(self, x, ncomm: int, mult: int):
         """The whole stream-ordered sharded sort with the library's own NCCL
-        communicator (cafs_sort_i64_sharded): (status, telemetry)."""
+        communicator (cafs_sort_i64_sharded, or cafs_sort_i32_sharded for
+        4-byte shards): (status, telemetry)."""
         t = _lib.Telemetry()
         status = ctypes.c_int()
-        _lib.check(self.lib.cafs_sort_i64_sharded(self.ctx, ncomm, x.data_ptr(), x.shape[0],
-                                                  int(self.signed), mult, ctypes.byref(t),
-                                                  ctypes.byref(status), self._stream()),
+        torch = _torch()
+        if x.dtype in (torch.int32, torch.uint32):
+            fn, signed = self.lib.cafs_sort_i32_sharded, x.dtype == torch.int32
+        else:
+            fn, signed = self.lib.cafs_sort_i64_sharded, self.signed
+        _lib.check(fn(self.ctx, ncomm, x.data_ptr(), x.shape[0], int(signed), mult,
+                      ctypes.byref(t), ctypes.byref(status), self._stream()),
                    self.ctx, "sort_sharded")
         return int(status.value), t
 
@@ -441,13 +446,19 @@ def cafs_sort_sharded(x_local, group=None, hash_mult=None, telemetry: SortTeleme
                       ops=None, signed: bool | None = None) -> None:
     """Sort the row-sharded global column in place; see the module docstring.
 
-    int64 / uint64 shards run as they are; int32 / uint32 shards (and strided
-    views) are sorted through a contiguous int64 copy -- widening preserves the
-    order and every rank's decision (the keys' identities are unchanged)."""
+    int64 / uint64 shards run as they are; contiguous int32 / uint32 CUDA
+    shards run natively at 4 bytes per key (cafs_sort_i32_sharded); other
+    4-byte shards (strided views, the host-driven continuation) are sorted
+    through a contiguous int64 copy -- widening preserves the order and every
+    rank's decision (the keys' identities are unchanged)."""
     torch = _torch()
     mult = check_hash_mult(hash_mult)
     if x_local.dim() != 1:
         raise ValueError("cafs_sort_sharded expects a 1-D shard")
+    if (x_local.dtype in (torch.int32, torch.uint32) and x_local.is_cuda
+            and x_local.is_contiguous() and ops is None and _native_enabled()
+            and _sort_sharded_native32(x_local, group, mult, telemetry)):
+        return
     if x_local.dtype not in (torch.int64, torch.uint64) or not x_local.is_contiguous():
         if x_local.dtype not in (torch.int64, torch.uint64, torch.int32, torch.uint32):
             raise TypeError(f"unsupported dtype {x_local.dtype}")
@@ -544,6 +555,35 @@ def _sort_sharded_native(x_local, comm, ops, tel, mult: int) -> bool:
     tel.pairs = int(t.pairs)
     if tel.decision.route is Route.MAIN:
         tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, 4)
+    return True
+
+
+def _sort_sharded_native32(x_local, group, mult: int, telemetry) -> bool:
+    """A 4-byte shard through cafs_sort_i32_sharded.  False (column untouched,
+    every rank agrees) when the column needs the host-driven continuation; the
+    caller then sorts it through the widened int64 copy."""
+    from .sorter import _decision_from_c
+    torch = _torch()
+    dev = x_local.device.index if x_local.device.index is not None else torch.cuda.current_device()
+    signed = x_local.dtype == torch.int32
+    ops = _device_ops(dev, signed)
+    comm = _comm(group, x_local.device)
+    if comm.device is None:
+        return False
+    k0 = ops.kernel_count()
+    status, t = ops.sort_native(x_local, _native_comm(comm, ops.device), mult)
+    if status != 0:
+        return False
+    tel = telemetry if telemetry is not None else SortTelemetry()
+    tel.n = int(t.n)
+    tel.decision = _decision_from_c(t.decision, tel.n, "int32" if signed else "uint32")
+    tel.sharded_path = "native"
+    tel.counted_total = int(t.counted_total)
+    tel.pairs = int(t.pairs)
+    if tel.decision.route is Route.MAIN:
+        # the reference's table for 4-byte keys has 8-slot buckets (buckets.py:33-43)
+        tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, 8)
+    tel.kernels_launched = ops.kernel_count() - k0
     return True
 
 

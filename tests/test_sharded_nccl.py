@@ -4,7 +4,8 @@ on the GPU: bit-exact against np.sort and the oracle's decision on every route,
 across direct, captured and replayed calls; columns the device cannot finish
 finish natively too (> 8192 pairs per rank: the partitioned count sorts each
 shard's pairs, the library grows its exchange row once and merges the
-gathered lists on device); fallback routes take the host-driven path ("host").  (More ranks need more GPUs than this pool
+gathered lists on device); int32 / uint32 shards run natively at 4 bytes per
+key (cafs_sort_i32_sharded); fallback routes take the host-driven path ("host").  (More ranks need more GPUs than this pool
 gives: the 2-rank tests in test_sharded_gpu.py share one GPU over gloo.)"""
 
 import os
@@ -45,15 +46,24 @@ cols = {
     "sorted": (np.arange(-50_000, 50_000, dtype=np.int64), "native"),
     "uint64": (rng.choice(rng.integers(0, 2**63, 500, dtype=np.uint64) * 2, 600_000), "native"),
     "small_n": (rng.integers(-9, 9, 1500), "host"),
+    # 4-byte shards: cafs_sort_i32_sharded, 4 bytes per key read and written
+    "i32_codes": (rng.integers(-2000, 2000, 1_500_000).astype(np.int32), "native"),
+    "i32_many_pairs": (rng.integers(-2**31, 2**31, 40_000)[
+        rng.integers(0, 40_000, 2_000_000)].astype(np.int32), "native"),
+    "i32_extremes": (rng.choice(np.array([-2**31, 2**31 - 1, -1, 0, 7], np.int64),
+                                900_001).astype(np.int32), "native"),
+    "u32_main": (rng.choice(rng.integers(0, 2**32, 3000, dtype=np.uint64), 1_000_000)
+                 .astype(np.uint32), "native"),
 }
+TDT = {np.dtype(np.uint64): torch.uint64, np.dtype(np.int64): torch.int64,
+       np.dtype(np.int32): torch.int32, np.dtype(np.uint32): torch.uint32}
 MULTS = {"main_hash": 0x2545F4914F6CDD1D}  # a caller's odd hash multiplier (buckets.py:54-67)
 bad = []
 for name, (x, path) in cols.items():
-    x = x if x.dtype == np.uint64 else x.astype(np.int64)
+    x = x if x.dtype in (np.uint64, np.int32, np.uint32) else x.astype(np.int64)
     want = np.sort(x)
-    route = orc.cafs_sort(x.copy()).route
-    t = torch.empty(x.shape[0], dtype=torch.uint64 if x.dtype == np.uint64 else torch.int64,
-                    device="cuda")
+    route = orc.cafs_sort(x.astype(np.int64) if x.itemsize == 4 else x.copy()).route
+    t = torch.empty(x.shape[0], dtype=TDT[x.dtype], device="cuda")
     for rep in range(3):  # direct, captured, replayed
         t.copy_(torch.from_numpy(x))
         tel = cafs.SortTelemetry()
