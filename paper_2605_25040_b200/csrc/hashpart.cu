@@ -60,7 +60,6 @@ constexpr int kHpQ = 64;                     // per-warp miss queue
 constexpr int kHpP = kHpParts;               // key-range partitions
 constexpr int kHpFine = 2048;                // fine bins of the partition map
 constexpr u32 kHpCellCap = kHpS + 16;        // cells per CTA (+ CTA 0's head / tail keys)
-constexpr int kHpChunk = 8192;               // tail scatter chunk (spilled keys)
 constexpr u32 kHpPartSlots = 4096;           // hp_reduce exact table
 constexpr u32 kHpPartCap = 2048;             // distinct keys per partition (load <= 1/2)
 constexpr u32 kHpListCap = kHpPartCap + kHpThreads;  // claims may overshoot by one per thread
@@ -69,7 +68,6 @@ static_assert(kHpP == 512, "scans below are written for 512 partitions");
 
 constexpr size_t kHpQueueBytes = (size_t)32 * kHpQ * 8;
 constexpr size_t kHpCountSmem = (size_t)kHpS * 12 + kHpQueueBytes + (size_t)kHpFine * 2;
-static_assert((size_t)kHpChunk * 10 + kHpP * 4 <= (size_t)kHpS * 12, "spill staging");
 static_assert(kHpCountSmem + 11 * 1024 <= 232448, "shared memory budget");
 constexpr size_t kHpReduceSmem = (size_t)kHpPartSlots * 12 + (size_t)kHpListCap * 16;
 
@@ -89,7 +87,7 @@ struct HpArgs {
   u64 flip;
   DevCtl* ctl;
   void* part;      // partitioned spill, same layout and key type as x
-  u64* cellk;      // [grid][kHpCellCap]
+  u64* cellk;      // [grid][kHpCellCap] cells (key, count), grouped by partition
   u32* cellw;
   u32* cpofs;      // [grid][kHpP + 1] cell segment starts per partition
   u32* spofs;      // [grid][kHpP + 1] spill segment starts per partition
@@ -417,25 +415,27 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
   for (u32 i = tid; i <= kHpP; i += kHpThreads) lhist[i] = 0;
   __syncthreads();
 
-  // ---- tail 1: the cells, counting-sorted by partition in passes that fit
-  // the staging area (the queues), written to this CTA's region ----
+  // ---- tail 1: the cells, counting-sorted by partition into this CTA's region.
+  // A thread keeps its slots' destinations and counts in registers, which
+  // frees the count array as the staging area: the keys go through it in two
+  // passes, the counts in one, every global store coalesced ----
   constexpr int kCpt = kHpS / kHpThreads;  // slots per thread
-  constexpr u32 kStage = (u32)(kHpQueueBytes / 12);  // cells per pass
-  u32 cp[kCpt + 1], cr[kCpt + 1];
+  u32 cpos[kCpt + 1], ccnt[kCpt];  // destination (partition | rank << 16, then the position)
 #pragma unroll
   for (int j = 0; j < kCpt; ++j) {
     const u32 slot = tid + j * kHpThreads;
     const u64 k = tkeys[slot];
-    cp[j] = kHpP;
+    ccnt[j] = tcnt[slot];
+    cpos[j] = ~0u;
     if (k != hp_marker(a, slot >> 1)) {
-      cp[j] = hp_part(k, plo, psh, pmap);
-      cr[j] = atomicAdd(&lhist[cp[j]], 1u);
+      const u32 pp = hp_part(k, plo, psh, pmap);
+      cpos[j] = pp | (atomicAdd(&lhist[pp], 1u) << 16);
     }
   }
-  cp[kCpt] = kHpP;
+  cpos[kCpt] = ~0u;
   if ((u32)tid < ncell_extra) {
-    cp[kCpt] = hp_part(extra_k[tid], plo, psh, pmap);
-    cr[kCpt] = atomicAdd(&lhist[cp[kCpt]], 1u);
+    const u32 pp = hp_part(extra_k[tid], plo, psh, pmap);
+    cpos[kCpt] = pp | (atomicAdd(&lhist[pp], 1u) << 16);
   }
   __syncthreads();
   if (wid == 0) hp_scan512(lhist, lstart);
@@ -445,85 +445,60 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
     a.cpofs[(size_t)c * (kHpP + 1) + i] = lstart[i];
     a.spofs[(size_t)c * (kHpP + 1) + i] = hstart[i];
   }
+#pragma unroll
+  for (int j = 0; j <= kCpt; ++j)
+    if (cpos[j] != ~0u) cpos[j] = lstart[cpos[j] & 0xffffu] + (cpos[j] >> 16);
   const u32 ncells = lstart[kHpP];
-  u64* stk = queue;                                  // staging keys [kStage]
-  u32* stw = (u32*)(queue + kStage);                 // staging counts
   u64* gck = a.cellk + (size_t)c * kHpCellCap;
   u32* gcw = a.cellw + (size_t)c * kHpCellCap;
-  for (u32 lo = 0; lo < ncells; lo += kStage) {      // cells [lo, lo + kStage) of the sorted order
-    const u32 hi = lo + kStage < ncells ? lo + kStage : ncells;
+  u64* stk = (u64*)tcnt;  // staging: kHpS / 2 keys, or kHpS counts
+  for (u32 lo = 0; lo < ncells; lo += kHpS / 2) {
+    const u32 hi = lo + kHpS / 2 < ncells ? lo + kHpS / 2 : ncells;
 #pragma unroll
-    for (int j = 0; j <= kCpt; ++j) {
-      if (cp[j] < (u32)kHpP) {
-        const u32 pos = lstart[cp[j]] + cr[j];
-        if (pos >= lo && pos < hi) {
-          if (j < kCpt) {
-            const u32 slot = tid + j * kHpThreads;
-            stk[pos - lo] = tkeys[slot];
-            stw[pos - lo] = tcnt[slot];
-          } else {
-            stk[pos - lo] = extra_k[tid];
-            stw[pos - lo] = 1;
-          }
-        }
-      }
-    }
+    for (int j = 0; j <= kCpt; ++j)
+      if (cpos[j] >= lo && cpos[j] < hi)
+        stk[cpos[j] - lo] = j < kCpt ? tkeys[tid + j * kHpThreads] : extra_k[tid];
     __syncthreads();
-    for (u32 i = lo + tid; i < hi; i += kHpThreads) {
-      gck[i] = stk[i - lo];
-      gcw[i] = stw[i - lo];
-    }
+    for (u32 i = lo + tid; i < hi; i += kHpThreads) gck[i] = stk[i - lo];
     __syncthreads();
   }
-  // ---- tail 2: the spill (the table's space is free now), chunk by chunk ----
-  const u32 ns = wsp[32];
-  K* stv = (K*)smem;                                                     // staged keys
-  unsigned short* stp = (unsigned short*)(smem + (size_t)kHpChunk * 8);  // their partitions
-  u32* written = (u32*)(smem + (size_t)kHpChunk * 10);                   // [kHpP]
-  for (u32 i = tid; i < kHpP; i += kHpThreads) written[i] = 0;
+  {
+    const u32 lo = 0, hi = ncells < kHpS ? ncells : kHpS;  // the (<= 16) cells past kHpS below
+#pragma unroll
+    for (int j = 0; j <= kCpt; ++j)
+      if (cpos[j] < hi) tcnt[cpos[j]] = j < kCpt ? ccnt[j] : 1u;
+    __syncthreads();
+    for (u32 i = lo + tid; i < hi; i += kHpThreads) gcw[i] = tcnt[i];
+#pragma unroll
+    for (int j = 0; j <= kCpt; ++j)
+      if (cpos[j] != ~0u && cpos[j] >= kHpS) gcw[cpos[j]] = j < kCpt ? ccnt[j] : 1u;
+  }
+  // ---- tail 2: the spill, grouped by partition in this CTA's rows of `part`:
+  // a key's place is its partition's start (the histogram taken while
+  // spilling) + its arrival rank (the order inside a partition is free); a
+  // warp moves the keys it spilled itself ----
+  __syncthreads();
+  for (u32 i = tid; i < kHpP; i += kHpThreads) lhist[i] = 0;
+  __syncthreads();
   K* outp = (K*)a.part + head + v0 * KPV;
-  for (u32 ch = 0; ch < ns; ch += kHpChunk) {
-    const u32 cn = ns - ch < (u32)kHpChunk ? ns - ch : (u32)kHpChunk;
-    __syncthreads();
-    for (u32 i = tid; i <= kHpP; i += kHpThreads) lhist[i] = 0;
-    __syncthreads();
-    constexpr int kSpt = kHpChunk / kHpThreads;
-    K kv[kSpt];
-    u32 pp[kSpt], rr[kSpt];
+  constexpr int kSpU = 4;
+  for (u32 g0 = 0; g0 < nsw; g0 += 32 * kSpU) {
+    K kv[kSpU];
 #pragma unroll
-    for (int j = 0; j < kSpt; ++j) {
-      const u32 i = tid + j * kHpThreads;
-      pp[j] = kHpP;
-      if (i < cn) {
-        const u32 g = ch + i;  // spilled key g: warp ww, its index g - wsp[ww]
-        u32 ww = 0;
+    for (int j = 0; j < kSpU; ++j) {
+      const u32 g = g0 + j * 32 + lane;
+      if (g < nsw) kv[j] = *((volatile K*)&xb[hp_spill_pos<KPV>(v0, wid, g)]);
+    }
 #pragma unroll
-        for (int st = 16; st > 0; st >>= 1)
-          if (ww + st < 32 && wsp[ww + st] <= g) ww += st;
-        kv[j] = *((volatile K*)&xb[hp_spill_pos<KPV>(v0, ww, g - wsp[ww])]);
-        pp[j] = hp_part(key_map<KK>(kv[j], flip), plo, psh, pmap);
-        rr[j] = atomicAdd(&lhist[pp[j]], 1u);
+    for (int j = 0; j < kSpU; ++j) {
+      const u32 g = g0 + j * 32 + lane;
+      if (g < nsw) {
+        const u32 pp = hp_part(key_map<KK>(kv[j], flip), plo, psh, pmap);
+        outp[hstart[pp] + atomicAdd(&lhist[pp], 1u)] = kv[j];
       }
     }
-    __syncthreads();
-    if (wid == 0) hp_scan512(lhist, lstart);
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kSpt; ++j) {
-      if (pp[j] < (u32)kHpP) {
-        const u32 pos = lstart[pp[j]] + rr[j];
-        stv[pos] = kv[j];
-        stp[pos] = (unsigned short)pp[j];
-      }
-    }
-    __syncthreads();
-    for (u32 i = tid; i < cn; i += kHpThreads) {
-      const u32 p = stp[i];
-      outp[hstart[p] + written[p] + (i - lstart[p])] = stv[i];
-    }
-    __syncthreads();
-    for (u32 i = tid; i < kHpP; i += kHpThreads) written[i] += lhist[i];
   }
+  const u32 ns = wsp[32];
   if (tid == 0 && ns) atomicAdd(&a.ctl->g_updates, (u64)ns);
 }
 
@@ -549,6 +524,7 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
   u64* lc = lk + kHpListCap;                   // [kHpListCap]
   __shared__ u32 segs[2 * 160 + 1];            // flat start of segment j (cells, then spill)
   __shared__ u32 sbeg[2 * 160];                // its first index in the source array
+  __shared__ u32 rk[512];                      // rank sort: a key's rank
   __shared__ u32 claims, nd, ovf;
   __shared__ unsigned long long sent;
   __shared__ u64 wsum[32];
@@ -563,8 +539,9 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
   const u64 body = (n - head) / KPV * KPV;
   const K* part = (const K*)a.part + head;
   // segment table: j < G cells of CTA j, G <= j < 2G spill of CTA j - G
+  // (sharded merge: one segment per rank's list); segs = their flat starts
+  const u32 nseg = SH ? G : 2 * G;
   u32 len = 0;
-  const u32 nseg = SH ? G : 2 * G;  // sharded merge: one segment per rank's list
   if ((u32)tid < nseg) {
     const bool cell = (u32)tid < G;
     const u32 c = cell ? tid : tid - G;
@@ -573,7 +550,8 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
     len = b1 - b0;
     u64 v0 = 0, v1;
     if (!cell) hp_range(body / KPV, kHpRound, c, G, &v0, &v1);
-    sbeg[tid] = cell ? b0 : (u32)(v0 * KPV + b0);  // spill: index into part (CTA range + segment)
+    // cells: index into cellk / cellw; spill: index into part (CTA range + segment)
+    sbeg[tid] = cell ? (SH ? b0 : c * kHpCellCap + b0) : (u32)(v0 * KPV + b0);
   }
   u32 inc = len;
 #pragma unroll
@@ -611,35 +589,54 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
     }
     ovf = 1;
   };
-  // warp per segment: lanes read consecutive items, kRdUnroll per lane in flight
-  for (u32 j = wid; j < nseg; j += 32) {
-    const u32 len_j = segs[j + 1] - segs[j], b = sbeg[j];
-    const bool cell = j < G;
-    for (u32 i0 = lane; i0 < len_j; i0 += 32 * kRdUnroll) {
-      u64 k[kRdUnroll];
-      u32 w[kRdUnroll];
+  // Equal single-row items in a warp (a spilled heavy key fills whole
+  // segments) are added once by their first lane instead of 32 serialised
+  // shared atomics on one address.
+  auto insert_agg = [&](u64 k, u32 w) {
+    const bool one = w == 1;
+    const u32 m1 = __ballot_sync(0xffffffffu, one);
+    if (m1) {
+      const int ld = __ffs(m1) - 1;
+      const u64 kl = __shfl_sync(0xffffffffu, k, ld);
+      const u32 me = __ballot_sync(0xffffffffu, one && k == kl);
+      if (one && k == kl) w = lane == ld ? (u32)__popc(me) : 0u;
+    }
+    if (w) insert(k, w);
+  };
+  // The segments as one flat list: thread t takes items t, t + 1024, ... with
+  // kRdUnroll loads in flight (an item's segment by binary search of the
+  // table, mostly a broadcast: neighbours share a segment), so a partition
+  // costs a few global round trips however its rows are spread over segments.
+  const u32 total = segs[nseg];
+  for (u32 i0 = 0; i0 < total; i0 += kHpThreads * kRdUnroll) {  // CTA-uniform
+    u64 k[kRdUnroll];
+    u32 w[kRdUnroll];
 #pragma unroll
-      for (int r = 0; r < kRdUnroll; ++r) {
-        const u32 i = i0 + r * 32;
-        w[r] = 0;
-        if (i < len_j) {
-          if (SH) {
-            const u64* L = a.recv + (size_t)j * a.row;
-            k[r] = L[1 + b + i];
-            w[r] = (u32)L[1 + a.cap + b + i];
-          } else if (cell) {
-            k[r] = a.cellk[(size_t)j * kHpCellCap + b + i];
-            w[r] = a.cellw[(size_t)j * kHpCellCap + b + i];
-          } else {
-            k[r] = key_map<KK>(part[b + i], a.flip);
-            w[r] = 1;
-          }
+    for (int r = 0; r < kRdUnroll; ++r) {
+      const u32 i = i0 + r * kHpThreads + tid;
+      w[r] = 0;
+      k[r] = 0;
+      if (i < total) {
+        u32 j = 0;
+#pragma unroll
+        for (u32 st = SH ? 16 : 256; st > 0; st >>= 1)  // sharded: nseg < 32 ranks
+          if (j + st < nseg && segs[j + st] <= i) j += st;
+        const u32 off = sbeg[j] + (i - segs[j]);
+        if (SH) {
+          const u64* L = a.recv + (size_t)j * a.row;
+          k[r] = L[1 + off];
+          w[r] = (u32)L[1 + a.cap + off];
+        } else if (j < G) {
+          k[r] = a.cellk[off];
+          w[r] = a.cellw[off];
+        } else {
+          k[r] = key_map<KK>(part[off], a.flip);
+          w[r] = 1;
         }
       }
-#pragma unroll
-      for (int r = 0; r < kRdUnroll; ++r)
-        if (w[r]) insert(k[r], w[r]);
     }
+#pragma unroll
+    for (int r = 0; r < kRdUnroll; ++r) insert_agg(k[r], w[r]);
   }
   __syncthreads();
   // compact the distinct keys (order is irrelevant: they are sorted next)
@@ -653,19 +650,29 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
   __syncthreads();
   const bool bad = ovf || nd > kHpPartCap;
   const u32 d = bad ? 0u : nd;
-  if (d <= 192) {
-    // rank sort (the keys are distinct): thread t moves key t to the number
-    // of keys below it; every step reads one key by broadcast
+  if (d <= 512) {
+    // rank sort (the keys are distinct): key q moves to the number of keys
+    // below it.  1024 / dpad threads share a key, each counting over its
+    // slice of the list (every step reads one key by broadcast: a warp's
+    // lanes hold consecutive keys and the same slice); no barrier per step,
+    // where the bitonic network needs 36-45
+    u32 dpad = 32;
+    while (dpad < d) dpad <<= 1;
+    const u32 T = kHpThreads / dpad, q = tid & (dpad - 1), sl = tid / dpad;
+    if ((u32)tid < 512) rk[tid] = 0;
+    __syncthreads();
     u64 mk = 0, mc = 0;
-    u32 rank = 0;
-    if ((u32)tid < d) {
-      mk = lk[tid];
-      mc = lc[tid];
+    if (q < d) {
+      mk = lk[q];
+      if (sl == 0) mc = lc[q];
+      const u32 j0 = (u32)(((u64)d * sl) / T), j1 = (u32)(((u64)d * (sl + 1)) / T);
+      u32 rank = 0;
 #pragma unroll 8
-      for (u32 j = 0; j < d; ++j) rank += lk[j] < mk ? 1u : 0u;
+      for (u32 j = j0; j < j1; ++j) rank += lk[j] < mk ? 1u : 0u;
+      if (rank) atomicAdd(&rk[q], rank);
     }
     __syncthreads();
-    if ((u32)tid < d) { lk[rank] = mk; lc[rank] = mc; }
+    if (q < d && sl == 0) { const u32 r = rk[q]; lk[r] = mk; lc[r] = mc; }
     __syncthreads();
   } else {
     // bitonic sort (padded to a power of two with ~0)
