@@ -234,6 +234,21 @@ constexpr u64 kHpMinRows = 1ull << 20;
 
 bool hp_allowed(u64 n, bool exact) { return !exact && n >= kHpMinRows; }
 
+// The emit's tile -> pair map (emit.cu): one u32 per 8 KB output tile.
+int ensure_tile_map(cafs_ctx_t* ctx, u64 n, int kk) {
+  const u64 tiles = emit_tiles(n, kk);
+  if (tiles > ctx->tile_map_len) {
+    CK(cudaDeviceSynchronize());
+    if (ctx->tile_map) CK(cudaFree(ctx->tile_map));
+    ctx->tile_map = nullptr;
+    ctx->tile_map_len = 0;
+    drop_graphs(ctx);
+    CK(cudaMalloc(&ctx->tile_map, tiles * sizeof(u32)));
+    ctx->tile_map_len = tiles;
+  }
+  return CAFS_OK;
+}
+
 int ensure_hp(cafs_ctx_t* ctx, u64 n, int kk) {
   const size_t bytes = (size_t)n * (kk ? 4 : 8) + 64;
   if (bytes > ctx->hp_part_bytes) {
@@ -246,17 +261,7 @@ int ensure_hp(cafs_ctx_t* ctx, u64 n, int kk) {
     ctx->hp_part_bytes = bytes;
   }
   if (!ctx->hp_scratch) CK(cudaMalloc(&ctx->hp_scratch, hp_scratch_bytes(ctx->num_sms)));
-  const u64 tiles = emit_tiles(n, kk);  // the emit's tile -> pair map (hp_place's pairs)
-  if (tiles > ctx->tile_map_len) {
-    CK(cudaDeviceSynchronize());
-    if (ctx->tile_map) CK(cudaFree(ctx->tile_map));
-    ctx->tile_map = nullptr;
-    ctx->tile_map_len = 0;
-    drop_graphs(ctx);
-    CK(cudaMalloc(&ctx->tile_map, tiles * sizeof(u32)));
-    ctx->tile_map_len = tiles;
-  }
-  return CAFS_OK;
+  return ensure_tile_map(ctx, n, kk);  // the emit's tile -> pair map (hp_place's pairs)
 }
 
 HpBufs hp_bufs(cafs_ctx_t* ctx) { return HpBufs{ctx->hp_part, ctx->hp_scratch, ctx->pk_a, ctx->pc_a}; }
@@ -752,7 +757,12 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
   }
   // a pipeline that holds only the partitioned count (its route predicted)
   // also writes the emit's tile -> pair map: its pair sets are large
-  const bool map = hp && groups == kGrpHp;
+  static const int force_map = getenv("CAFS_EMIT_MAP") ? atoi(getenv("CAFS_EMIT_MAP")) : 0;
+  bool map = hp && groups == kGrpHp;
+  if (force_map && with_emit && groups != kGrpAll && groups != 0 && !(groups & kGrpTiny)) {
+    TRY(ensure_tile_map(ctx, n, kk));
+    map = true;
+  }
   if (with_emit && map) {
     launch_emit_map(ctx->poffs, c, x, 0, n, ctx->tile_map, (u64)ctx->num_sms * 8 * 256,
                     ctx->num_sms, st, kk);

@@ -22,7 +22,9 @@
 
 namespace cafs {
 
-constexpr int kEmitThreads = 512;
+constexpr int kEmitThreads = 128;                 // a CTA lives as long as its slowest warp (one
+                                                  // fragmented tile): 4 warps, not 16 (cfg4 / 8:
+                                                  // emit 178 -> 160 us; cfg4: 1163 -> 1153 us)
 constexpr int kEmitVpl = 8;                       // 32-byte vectors per lane per tile
 constexpr u64 kTileBytes = 32ull * kEmitVpl * 32;  // 8 KB per warp tile (1024 int64 keys)
 constexpr u64 kIdxEntries = 4096;                // max shared index of the offsets (32 KB)
@@ -155,39 +157,84 @@ __global__ void __launch_bounds__(kEmitThreads)
       continue;
     }
     // fragmented tile: walk its pairs in windows of 32 run boundaries held in
-    // registers; each lane finds its position's pair with a 5-step shuffle
-    // search and the warp writes 32 consecutive keys per store instruction
+    // registers (as 32-bit positions relative to the tile).  Each lane takes a
+    // whole 32-byte vector: one 5-step shuffle search for the vector's first
+    // key; a chunk of 32 vectors no boundary cuts through is written like a
+    // uniform tile, otherwise the remaining keys of each vector are searched
+    // too -- either way the warp writes 1 KB per store instruction
     u64 q = p;
-    u64 g = g0;
-    const u64 gend = glast + 1;
-    while (g < gend) {
+    u32 g = 0;
+    const u32 gend = (u32)(glast + 1 - g0);
+    K* ot = ob + e0;  // the tile's first key (32-byte aligned)
+    while (true) {
       const u64 qi = q + lane;
-      const u64 wb = qi < npairs ? offs[qi + 1] : ~0ull;  // end of pair qi
-      const u64 wk = qi < npairs ? keys[qi] : 0ull;
-      const u64 wtop = __shfl_sync(0xffffffffu, wb, 31);
-      const u64 wend = wtop < gend ? wtop : gend;
-      for (u64 base = g; base < wend; base += 32) {
-        const u64 pos = base + lane;
+      u32 wr = 0xffffffffu;  // end of pair qi, relative to the tile
+      K wk = 0;
+      if (qi < npairs) {
+        const u64 d = offs[qi + 1] - g0;
+        wr = d > 0xfffffffeull ? 0xffffffffu : (u32)d;
+        wk = key_unmap<KK>(keys[qi], flip);
+      }
+      const u32 wtop = __shfl_sync(0xffffffffu, wr, 31);
+      const u32 wend = wtop < gend ? wtop : gend;
+      // number of the window's boundaries <= pos (pos < wtop): the pair of pos
+      auto find = [&](u32 pos) -> int {
         int i = 0;
 #pragma unroll
         for (int st = 16; st >= 1; st >>= 1) {
-          const u64 b = __shfl_sync(0xffffffffu, wb, i + st - 1);
+          const u32 b = __shfl_sync(0xffffffffu, wr, i + st - 1);
           if (b <= pos) i += st;
         }
-        const u64 k = __shfl_sync(0xffffffffu, wk, i);
-        if (pos < wend) ob[pos - gb] = key_unmap<KK>(k, flip);
+        return i;
+      };
+      u32 a = g;
+      // keys before the first whole vector (only after a window change)
+      u32 ha = (a + (u32)VK - 1) / (u32)VK * (u32)VK;
+      if (ha > wend) ha = wend;
+      if (a < ha) {
+        const u32 pos = a + lane;
+        const K k = __shfl_sync(0xffffffffu, wk, find(pos));
+        if (pos < ha) ot[pos] = k;
+        a = ha;
+      }
+      const u32 vend = a + (wend - a) / (u32)VK * (u32)VK;
+      for (; a < vend; a += 32 * (u32)VK) {
+        const u32 pos = a + lane * (u32)VK;
+        const bool act = pos < vend;
+        const int i = find(pos);
+        const u32 b = __shfl_sync(0xffffffffu, wr, i);
+        K kv[VK];
+        kv[0] = __shfl_sync(0xffffffffu, wk, i);
+        if (__any_sync(0xffffffffu, act && b < pos + (u32)VK)) {
+#pragma unroll
+          for (int e = 1; e < (int)VK; ++e) kv[e] = __shfl_sync(0xffffffffu, wk, find(pos + e));
+        } else {
+#pragma unroll
+          for (int e = 1; e < (int)VK; ++e) kv[e] = kv[0];
+        }
+        if (act) {
+          if constexpr (sizeof(K) == 8)
+            st_v4(ot + pos, (u64)kv[0], (u64)kv[1], (u64)kv[2], (u64)kv[3]);
+          else
+            st_v4(ot + pos, (u64)kv[0] | ((u64)kv[1] << 32), (u64)kv[2] | ((u64)kv[3] << 32),
+                  (u64)kv[4] | ((u64)kv[5] << 32), (u64)kv[6] | ((u64)kv[7] << 32));
+        }
+      }
+      a = vend;
+      if (a < wend) {  // keys after the last whole vector (the window ends inside one)
+        const u32 pos = a + lane;
+        const K k = __shfl_sync(0xffffffffu, wk, find(pos));
+        if (pos < wend) ot[pos] = k;
       }
       g = wend;
-      if (g < gend) q += 32;
+      if (g >= gend) {
+        // the tile's last key is in the window: its pair is the next tile's cursor
+        p = q + (u64)find(gend - 1);
+        break;
+      }
+      q += 32;
     }
-    // the last pair touched becomes the cursor for the next tile
-    if (MAP) {
-      if (t + 1 >= t1) break;  // the warp's last tile: no cursor needed
-      p = tile_pair[t + 1];    // the pair holding glast + 1; glast is in it or just before
-      if (offs[p] > glast) --p;
-    } else {
-      p = locate(q, glast);
-    }
+    if (t + 1 >= t1) break;  // the warp's last tile: no cursor needed
     rs = offs[p];
     re = offs[p + 1];
     rk = splat(key_unmap<KK>(keys[p], flip));
@@ -265,9 +312,11 @@ void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl
   const u64 L = end > begin ? end - begin : 0;
   const u64 tile_keys = kTileBytes / (kk ? 4 : 8);
   const u64 wtiles = (L + tile_keys - 1) / tile_keys;
-  static int tpw = -1, idx = -1;  // CAFS_EMIT_TPW / CAFS_EMIT_IDX: tuning knobs
+  static int tpw = -1, idx = -1, thr = 0;  // CAFS_EMIT_TPW / CAFS_EMIT_IDX / CAFS_EMIT_THREADS: tuning knobs
   if (tpw < 0) {
-    const char* e = getenv("CAFS_EMIT_TPW");
+    const char* e = getenv("CAFS_EMIT_THREADS");
+    thr = e ? atoi(e) : 0;
+    e = getenv("CAFS_EMIT_TPW");
     tpw = e ? atoi(e) : 2;
     if (tpw < 1 || tpw > 4096) tpw = 2;
     e = getenv("CAFS_EMIT_IDX");
@@ -278,8 +327,8 @@ void launch_emit(const u64* keys, const u64* offs, u64 npairs, const DevCtl* ctl
   // spreads over every SM (1M keys = 977 tiles: 31 CTAs of 16 warps x 2 tiles)
   u64 tpw_use = (u64)tpw, threads = kEmitThreads;
   const u64 spread = (u64)num_sms * 4;
-  if ((wtiles + tpw_use * 16 - 1) / (tpw_use * 16) < spread) tpw_use = 1;
-  if ((wtiles + 15) / 16 < spread) threads = 128;
+  if ((wtiles + tpw_use * 4 - 1) / (tpw_use * 4) < spread * 4) tpw_use = 1;
+  if (thr == 64 || thr == 128) threads = thr;
   const u64 wpb = threads / 32;
   u64 grid = (wtiles + tpw_use * wpb - 1) / (tpw_use * wpb);
   if (grid < 1) grid = 1;

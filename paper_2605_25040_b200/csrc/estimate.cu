@@ -156,13 +156,11 @@ __global__ void __launch_bounds__(1024, 1)
   const u64 v = valid ? __ldcg(&es->samples[tid]) : 0ull;
   __syncthreads();
   if (tid == 0) es->arrive = 0;  // ready for the next call (every CTA has arrived)
-  // insert the sample into the FreqSet; equal samples of a warp are merged
-  // first (one insert of count c instead of c contending atomics -- low
-  // cardinality inputs put ~128 samples on one slot)
-  const u32 peers = __match_any_sync(0xffffffffu, valid ? v : kEmpty);
-  const bool leader = valid && lane == __ffs(peers) - 1;
-  if (leader) {
-    const u32 c = __popc(peers);
+  // insert the sample into the FreqSet
+  // (merging a warp's equal samples first with __match_any_sync cost 2 us:
+  // 0.26 lanes/clk/SM; 128 contending shared atomics per slot are cheaper)
+  if (valid) {
+    const u32 c = 1;
     if (v == kEmpty) {
       atomicAdd(&n_max_key, c);
     } else {
