@@ -1053,39 +1053,73 @@ u64 host_fmix64(u64 z) {
 // cafs_shard_* calls (collectives by the caller) and cafs_sort_i64_sharded
 // (collectives here, over the library's own NCCL communicator) ----
 
+// Route classes of the sharded pipeline.  The route, the dense window and so
+// the class of a column are the same on every rank (all decide from the same
+// all-reduced samples and gathered headers), so a communicator can predict the
+// next column's class from the last ones and leave the other classes' kernels
+// out of its graph -- the collectives stay the same three on every rank; a
+// wrong prediction is seen by every rank alike and all re-run the full
+// pipeline (the left-out kernels never touch the column).
+enum : uint32_t { kClsTiny = 1, kClsWindow = 2, kClsNoWindow = 4, kClsAll = 7 };
+
+uint32_t shard_class(const DevCtl& h) {
+  if (h.eff_route == CAFS_TINY_COUNT) return kClsTiny;
+  if (h.eff_route == CAFS_MAIN) return h.range_len > 0 ? kClsWindow : kClsNoWindow;
+  return 0;  // sorted, fallback routes: no device count
+}
+
 // estimate on the gathered samples -> route; tiny count or local hash count ->
 // sorted local pairs -> this rank's send row [np, keys[cap], counts[cap]]
 int shard_count_enqueue(cafs_ctx_t* ctx, const void* x, u64 n, u64 flip, u64 mult,
                         const u64* hdr_all, int world, const u64* samples, u64* tiny, u64* send,
-                        u64 cap, cudaStream_t st, int kk = 0) {
+                        u64 cap, cudaStream_t st, int kk = 0, uint32_t cls = kClsAll) {
   DevCtl* c = ctx->d_ctl;
   // the partitioned count gives this shard's pairs sorted on device for any
   // number of keys (the table path's pair sort stops at 8192)
   const bool hp = hp_allowed(n, false);
   if (hp) TRY(ensure_hp(ctx, n, kk));
   launch_estimate_sharded(samples, hdr_all, world, c, st, hp ? kEstHp : 0);
-  launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny, kk);
-  launch_shard_tiny_pack(c, tiny, st);
-  cudaError_t e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
-                                    ctx->num_sms, st, 0, kGateMainDense, ctx->dense, kk);
-  if (hp && e == cudaSuccess) {
+  ctx->launches++;
+  if (cls & kClsTiny) {
+    launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny, kk);
+    launch_shard_tiny_pack(c, tiny, st);
+    ctx->launches += 2;
+  }
+  const bool any_main = cls & (kClsWindow | kClsNoWindow);
+  cudaError_t e = cudaSuccess;
+  if (cls & kClsWindow) {
+    e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1, ctx->num_sms,
+                          st, 0, kGateMainDense, ctx->dense, kk);
+    ctx->launches++;
+  }
+  if (hp && (cls & kClsNoWindow) && e == cudaSuccess) {
     e = launch_hp_count(hp_bufs(ctx), x, n, flip, c, ctx->pk_b, ctx->pc_b, ctx->poffs,
                         ctx->num_sms, st, kGateMainHP, kk);
     ctx->launches += 3;
   }
-  if (e == cudaSuccess)
+  if ((cls & kClsNoWindow) && e == cudaSuccess) {
     e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
                           ctx->num_sms, st, 1, kGateMainHash, ctx->dense, kk);
+    ctx->launches++;
+  }
   if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
-  launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
-                 kGateMainOld);
-  launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs, n, st,
-                     kGateMainDense);
-  e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs, st,
-                              kGateMainOld);
-  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
-  launch_shard_pack_pairs(c, ctx->pk_b, ctx->pc_b, send, cap, st);
-  ctx->launches += 10;
+  if (any_main) {
+    launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
+                   kGateMainOld);
+    ctx->launches++;
+  }
+  if (cls & kClsWindow) {
+    launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs, n,
+                       st, kGateMainDense);
+    ctx->launches++;
+  }
+  if (any_main) {
+    e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs,
+                                st, kGateMainOld);
+    if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
+    launch_shard_pack_pairs(c, ctx->pk_b, ctx->pc_b, send, cap, st);
+    ctx->launches += 2;
+  }
   CKL();
   return CAFS_OK;
 }
@@ -1094,21 +1128,27 @@ int shard_count_enqueue(cafs_ctx_t* ctx, const void* x, u64 n, u64 flip, u64 mul
 // rank's slice emit (every kernel gated on the device decision)
 int shard_finish_enqueue(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, const u64* tiny_sum,
                          const u64* recv, int world, u64 cap, u64 row, cudaStream_t st,
-                         int kk = 0) {
+                         int kk = 0, uint32_t cls = kClsAll) {
   DevCtl* c = ctx->d_ctl;
-  launch_shard_tiny_finish(c, tiny_sum, ctx->pk_b, ctx->pc_b, ctx->poffs, st);
-  // the union of every rank's sorted list (sorter.py:276-285): key-range
-  // partitions of the gathered lists reduced on device into the global sorted
-  // pairs and offsets -- no hash table, no pair sort, any number of pairs
-  if (!ctx->hp_mscratch) CK(cudaMalloc(&ctx->hp_mscratch, hp_scratch_bytes(ctx->num_sms)));
-  launch_shard_merge_check(c, recv, world, cap, row, st);
-  HpBufs mb = hp_bufs(ctx);
-  mb.scratch = ctx->hp_mscratch;
-  cudaError_t e = launch_hp_shard_merge(mb, recv, world, cap, row, c, ctx->pk_b, ctx->pc_b,
-                                        ctx->poffs, st);
-  if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "sharded merge", e);
+  if (cls & kClsTiny) {
+    launch_shard_tiny_finish(c, tiny_sum, ctx->pk_b, ctx->pc_b, ctx->poffs, st);
+    ctx->launches++;
+  }
+  if (cls & (kClsWindow | kClsNoWindow)) {
+    // the union of every rank's sorted list (sorter.py:276-285): key-range
+    // partitions of the gathered lists reduced on device into the global sorted
+    // pairs and offsets -- no hash table, no pair sort, any number of pairs
+    if (!ctx->hp_mscratch) CK(cudaMalloc(&ctx->hp_mscratch, hp_scratch_bytes(ctx->num_sms)));
+    launch_shard_merge_check(c, recv, world, cap, row, st);
+    HpBufs mb = hp_bufs(ctx);
+    mb.scratch = ctx->hp_mscratch;
+    cudaError_t e = launch_hp_shard_merge(mb, recv, world, cap, row, c, ctx->pk_b, ctx->pc_b,
+                                          ctx->poffs, st);
+    if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "sharded merge", e);
+    ctx->launches += 4;
+  }
   launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, 0, kk, true);
-  ctx->launches += 6;
+  ctx->launches++;
   CKL();
   return CAFS_OK;
 }
@@ -1862,9 +1902,13 @@ struct cafs_comm_t {
     uint64_t launches = 0, stamp = 0;
     uint64_t gen = 0;  // the context's buf_gen at capture
     int kk = 0;        // key kind
+    uint32_t cls = 0;  // route classes whose kernels the graph holds
     cudaGraphExec_t exec = nullptr;
   } graphs[8];
   uint64_t clock = 0;
+  // the route classes the next call's pipeline holds: one class after two
+  // columns of that class in a row, else all (the same on every rank)
+  uint32_t pred = 7, last_cls = 0;
 };
 
 int cafs_nccl_unique_id(unsigned char* out) {
@@ -1932,7 +1976,7 @@ constexpr u64 kShardCapMax = 1ull << 20;
 // the pair tables' all-gather, the merge and this rank's slice emit; again
 // (from_local) after the row grew: the rows are re-packed from the count's pairs
 int sharded_exchange(cafs_ctx_t* ctx, cafs_comm_t* cm, void* x, u64 n, u64 flip, cudaStream_t st,
-                     int from_local, int kk) {
+                     int from_local, int kk, uint32_t cls) {
   const u64 cap = cm->cap, row = cm->row, tiny_off = 1 + 2 * cap;
   if (from_local) {
     launch_shard_pack_pairs(ctx->d_ctl, ctx->pk_b, ctx->pc_b, cm->send, cap, st, 1);
@@ -1940,10 +1984,13 @@ int sharded_exchange(cafs_ctx_t* ctx, cafs_comm_t* cm, void* x, u64 n, u64 flip,
   }
   if (ncclAllGather(cm->send, cm->recv, row, ncclUint64, cm->nc, st) != ncclSuccess)
     return fail(ctx, CAFS_ECUDA, "ncclAllGather (pair tables)");
-  launch_shard_tiny_gather(cm->recv, cm->world, row, tiny_off, cm->tiny_sum, st);
-  TRY(shard_finish_enqueue(ctx, x, n, flip, cm->tiny_sum, cm->recv, cm->world, cap, row, st, kk));
+  if (cls & kClsTiny) {
+    launch_shard_tiny_gather(cm->recv, cm->world, row, tiny_off, cm->tiny_sum, st);
+    ctx->launches++;
+  }
+  TRY(shard_finish_enqueue(ctx, x, n, flip, cm->tiny_sum, cm->recv, cm->world, cap, row, st, kk,
+                           cls));
   CK(cudaMemcpyAsync(ctx->h_ctl, ctx->d_ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
-  ctx->launches += 1;  // tiny gather
   CKL();
   return CAFS_OK;
 }
@@ -1967,7 +2014,7 @@ int comm_resize(cafs_ctx_t* ctx, cafs_comm_t* c, u64 cap) {
 }
 
 int sharded_enqueue(cafs_ctx_t* ctx, cafs_comm_t* cm, void* x, u64 n, u64 flip, u64 mult,
-                    cudaStream_t st, int kk) {
+                    cudaStream_t st, int kk, uint32_t cls) {
   const u64 cap = cm->cap, row = cm->row, tiny_off = 1 + 2 * cap;
   launch_shard_header(x, n, flip, cm->hdr, ctx->num_sms, st, kk);
   if (ncclAllGather(cm->hdr, cm->hdr_all, kShardHdrWords, ncclUint64, cm->nc, st) != ncclSuccess)
@@ -1978,9 +2025,9 @@ int sharded_enqueue(cafs_ctx_t* ctx, cafs_comm_t* cm, void* x, u64 n, u64 flip, 
       ncclSuccess)
     return fail(ctx, CAFS_ECUDA, "ncclAllReduce (samples)");
   TRY(shard_count_enqueue(ctx, x, n, flip, mult, cm->hdr_all, cm->world, cm->samples,
-                          cm->send + tiny_off, cm->send, cap, st, kk));
+                          cm->send + tiny_off, cm->send, cap, st, kk, cls));
   ctx->launches += 3;  // header (2), samples
-  return sharded_exchange(ctx, cm, x, n, flip, st, 0, kk);
+  return sharded_exchange(ctx, cm, x, n, flip, st, 0, kk, cls);
 }
 
 }  // namespace
@@ -2008,11 +2055,17 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
     const char* e = getenv("CAFS_GRAPHS");
     use_graphs = e ? atoi(e) != 0 : 1;
   }
+  static int predict = -1;  // CAFS_SHARD_PREDICT=0: every call holds every class's kernels
+  if (predict < 0) {
+    const char* e = getenv("CAFS_SHARD_PREDICT");
+    predict = e ? atoi(e) != 0 : 1;
+  }
+  uint32_t used = predict ? comm->pred : (uint32_t)kClsAll;
   cafs_comm_t::Graph* hit = nullptr;
   cafs_comm_t::Graph* lru = &comm->graphs[0];
   for (auto& gr : comm->graphs) {
     if (gr.seen && gr.x == (u64)x && gr.n == n && gr.flip == flip && gr.mult == hash_mult &&
-        gr.kk == kk) {
+        gr.kk == kk && gr.cls == used) {
       hit = &gr;
       if (gr.exec && gr.gen != ctx->buf_gen) {  // captured before a buffer moved
         cudaGraphExecDestroy(gr.exec);
@@ -2023,7 +2076,7 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
     if (gr.stamp < lru->stamp) lru = &gr;
   }
   if (!use_graphs || !ctx->cap_stream) {
-    TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st, kk));
+    TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st, kk, used));
   } else if (hit && hit->exec) {  // replay
     CK(cudaGraphLaunch(hit->exec, st));
     ctx->launches += hit->launches;
@@ -2032,13 +2085,13 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
     if (lru->exec) cudaGraphExecDestroy(lru->exec);
     *lru = cafs_comm_t::Graph();
     lru->x = (u64)x; lru->n = n; lru->flip = flip; lru->mult = hash_mult;
-    lru->seen = 1; lru->stamp = ++comm->clock; lru->kk = kk;
-    TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st, kk));
+    lru->seen = 1; lru->stamp = ++comm->clock; lru->kk = kk; lru->cls = used;
+    TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st, kk, used));
   } else {  // second sighting: capture on the context's stream, launch on the caller's
     const uint64_t l0 = ctx->launches;
     cudaGraph_t graph = nullptr;
     CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
-    const int rc = sharded_enqueue(ctx, comm, x, n, flip, hash_mult, ctx->cap_stream, kk);
+    const int rc = sharded_enqueue(ctx, comm, x, n, flip, hash_mult, ctx->cap_stream, kk, used);
     cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &graph);
     if (rc != CAFS_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "graph capture (sharded)", e);
@@ -2052,6 +2105,21 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
   }
   CK(cudaStreamSynchronize(st));
   const DevCtl& h = *ctx->h_ctl;
+  {
+    uint32_t now = shard_class(h);
+    if (now & ~used) {
+      // the prediction left this column's class out (on every rank alike):
+      // all re-run the full pipeline, collectives included
+      used = kClsAll;
+      TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st, kk, used));
+      CK(cudaStreamSynchronize(st));
+      now = shard_class(h);
+    }
+    if (now) {
+      comm->pred = now == comm->last_cls ? now : (uint32_t)kClsAll;
+      comm->last_cls = now;
+    }
+  }
   if (h.eff_route == CAFS_MAIN && h.merge_bad && h.shard_grow > comm->cap &&
       h.shard_grow <= kShardCapMax) {
     // some rank's sorted pairs did not fit the exchange row: every rank saw it
@@ -2060,7 +2128,7 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
     u64 cap = comm->cap;
     while (cap < h.shard_grow) cap <<= 1;
     TRY(comm_resize(ctx, comm, cap));
-    TRY(sharded_exchange(ctx, comm, x, n, flip, st, 1, kk));
+    TRY(sharded_exchange(ctx, comm, x, n, flip, st, 1, kk, used));
     CK(cudaStreamSynchronize(st));
   }
   return shard_result(ctx, x, n, flip, tel, h_status, st, kk);

@@ -64,7 +64,10 @@ for name, (x, path) in cols.items():
     want = np.sort(x)
     route = orc.cafs_sort(x.astype(np.int64) if x.itemsize == 4 else x.copy()).route
     t = torch.empty(x.shape[0], dtype=TDT[x.dtype], device="cuda")
-    for rep in range(3):  # direct, captured, replayed
+    # direct, captured, replayed with every route class's kernels, then (the
+    # communicator predicts the class after two columns of it) the same three
+    # with only this class's kernels
+    for rep in range(6):
         t.copy_(torch.from_numpy(x))
         tel = cafs.SortTelemetry()
         cafs_sort_sharded(t, telemetry=tel, hash_mult=MULTS.get(name))
@@ -73,6 +76,19 @@ for name, (x, path) in cols.items():
         if (not np.array_equal(t.cpu().numpy(), want) or tel.route.value != route
                 or got_path != path):
             bad.append((name, rep, tel.route.value, route, got_path, path))
+# columns of changing route classes on one communicator: a prediction that
+# left the column's class out is re-run with the full pipeline
+order = ["tiny", "tiny", "tiny", "codes", "main_hash", "main_hash", "main_hash", "tiny",
+         "sorted", "codes", "codes", "codes", "many_pairs", "fallback", "codes", "tiny"]
+for i, name in enumerate(order):
+    x, path = cols[name]
+    x = x if x.dtype in (np.uint64, np.int32, np.uint32) else x.astype(np.int64)
+    t = torch.from_numpy(x).to("cuda")
+    tel = cafs.SortTelemetry()
+    cafs_sort_sharded(t, telemetry=tel, hash_mult=MULTS.get(name))
+    torch.cuda.synchronize()
+    if not np.array_equal(t.cpu().numpy(), np.sort(x)) or tel.sharded_path != path:
+        bad.append(("cycle", i, name, tel.sharded_path, path))
 dist.destroy_process_group()
 print("BAD", bad)
 sys.exit(1 if bad else 0)
