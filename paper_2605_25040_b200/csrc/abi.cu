@@ -1060,7 +1060,13 @@ u64 host_fmix64(u64 z) {
 // out of its graph -- the collectives stay the same three on every rank; a
 // wrong prediction is seen by every rank alike and all re-run the full
 // pipeline (the left-out kernels never touch the column).
-enum : uint32_t { kClsTiny = 1, kClsWindow = 2, kClsNoWindow = 4, kClsAll = 7 };
+// kClsWindowSum: the window class's own pipeline -- every rank counts into the
+// same dense window (its base comes from the all-reduced samples), so the
+// merge is the element-wise sum of the count arrays: one all-reduce of 64 KB
+// in place of the pair tables' all-gather and the merge of the gathered lists.
+// A key outside the window on any rank leaves the summed counts short of the
+// column's rows on every rank: all re-run the full pipeline.
+enum : uint32_t { kClsTiny = 1, kClsWindow = 2, kClsNoWindow = 4, kClsAll = 7, kClsWindowSum = 8 };
 
 uint32_t shard_class(const DevCtl& h) {
   if (h.eff_route == CAFS_TINY_COUNT) return kClsTiny;
@@ -1909,6 +1915,7 @@ struct cafs_comm_t {
   // the route classes the next call's pipeline holds: one class after two
   // columns of that class in a row, else all (the same on every rank)
   uint32_t pred = 7, last_cls = 0;
+  int sum_penalty = 0;  // calls left before the window class's sum pipeline is tried again
 };
 
 int cafs_nccl_unique_id(unsigned char* out) {
@@ -2024,6 +2031,24 @@ int sharded_enqueue(cafs_ctx_t* ctx, cafs_comm_t* cm, void* x, u64 n, u64 flip, 
   if (ncclAllReduce(cm->samples, cm->samples, kSampleTarget, ncclUint64, ncclSum, cm->nc, st) !=
       ncclSuccess)
     return fail(ctx, CAFS_ECUDA, "ncclAllReduce (samples)");
+  if (cls == kClsWindowSum) {
+    DevCtl* c = ctx->d_ctl;
+    launch_estimate_sharded(cm->samples, cm->hdr_all, cm->world, c, st, 0);
+    cudaError_t e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
+                                      ctx->num_sms, st, 0, kGateMainDense, ctx->dense, kk);
+    if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
+    if (ncclAllReduce(ctx->dense, ctx->dense, dense_window_len(), ncclUint64, ncclSum, cm->nc,
+                      st) != ncclSuccess)
+      return fail(ctx, CAFS_ECUDA, "ncclAllReduce (window counts)");
+    // the summed counts -> the column's sorted pairs and offsets on every rank
+    launch_dense_pairs(c, ctx->dense, ctx->pk_a, ctx->pc_a, ctx->pk_b, ctx->pc_b, ctx->poffs,
+                       ~0ull, st, kGateMainDense);
+    launch_emit(ctx->pk_b, ctx->poffs, 0, c, x, 0, n, flip, ctx->num_sms, st, 0, kk, true);
+    CK(cudaMemcpyAsync(ctx->h_ctl, c, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
+    ctx->launches += 7;  // header (2), samples, estimate, count, pairs, emit
+    CKL();
+    return CAFS_OK;
+  }
   TRY(shard_count_enqueue(ctx, x, n, flip, mult, cm->hdr_all, cm->world, cm->samples,
                           cm->send + tiny_off, cm->send, cap, st, kk, cls));
   ctx->launches += 3;  // header (2), samples
@@ -2061,6 +2086,8 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
     predict = e ? atoi(e) != 0 : 1;
   }
   uint32_t used = predict ? comm->pred : (uint32_t)kClsAll;
+  if (used == kClsWindow && comm->sum_penalty == 0) used = kClsWindowSum;
+  if (comm->sum_penalty > 0) --comm->sum_penalty;
   cafs_comm_t::Graph* hit = nullptr;
   cafs_comm_t::Graph* lru = &comm->graphs[0];
   for (auto& gr : comm->graphs) {
@@ -2107,7 +2134,23 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
   const DevCtl& h = *ctx->h_ctl;
   {
     uint32_t now = shard_class(h);
-    if (now & ~used) {
+    bool redo = now & ~(used == kClsWindowSum ? (uint32_t)kClsWindow : used);
+    if (used == kClsWindowSum && now == kClsWindow && !h.pairs_ready) {
+      // the summed window counts are short: a rank met keys outside the window
+      // (they sit in its global table) or lost its table -- clean up, and use
+      // the pair-table pipeline for this communicator's next columns
+      if (h.overflow) {
+        CK(cudaMemsetAsync(ctx->gkeys, 0xFF, kGlobalSlots * 8, st));
+        CK(cudaMemsetAsync(ctx->gcnt, 0, kGlobalSlots * 8, st));
+      } else {
+        launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
+                       ctx->num_sms, st, kGateNone);
+        ctx->launches++;
+      }
+      comm->sum_penalty = 32;
+      redo = true;
+    }
+    if (redo) {
       // the prediction left this column's class out (on every rank alike):
       // all re-run the full pipeline, collectives included
       used = kClsAll;

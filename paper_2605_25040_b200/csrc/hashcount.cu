@@ -611,6 +611,9 @@ __global__ void __launch_bounds__(1024) dense_pairs_kernel(DevCtl* ctl, u64* den
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u64 base = ctl->range_base;
   const u32 rlen = ctl->range_len;
+  // ~0: the counts were all-reduced over the ranks of a sharded sort and must
+  // sum to the whole column
+  if (n_expect == ~0ull) n_expect = ctl->n_global;
   constexpr int IT = kRange / 1024;
   u64 c[IT];
   u32 nz = 0;

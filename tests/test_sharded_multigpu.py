@@ -45,8 +45,11 @@ rng = np.random.default_rng(11)
 codes = ogen.Config("c", 3_000_000, 4096, "zipf", s=0.8, palette="codes", seed=4).generate()
 skew = rng.integers(-2**62, 2**62, 5_000_000)
 skew[: 3_000_000] = rng.integers(0, 3, 3_000_000)
+outl = codes.copy()
+outl[7::600_000] = 2**50 + np.arange(outl[7::600_000].shape[0])  # keys outside the dense window
 cols = {
     "codes": codes,
+    "codes_outliers": outl,  # on one or two ranks only: every rank must re-run alike
     "tiny": rng.choice(rng.integers(-2**62, 2**62, 6), 1_000_003),
     "many_pairs": rng.choice(rng.integers(-2**62, 2**62, 50_000), 3_000_000),
     "skew_guard": rng.permutation(skew),
@@ -63,7 +66,9 @@ for name, x in cols.items():
     lo = rank * per
     hi = n if rank == world - 1 else lo + per
     t = torch.from_numpy(x[lo:hi].copy()).cuda()
-    for rep in range(3):  # direct, captured, replayed
+    # direct, captured, replayed with every route class's kernels, then with the
+    # predicted class's only (dictionary codes: the all-reduce of the window counts)
+    for rep in range(6):
         t.copy_(torch.from_numpy(x[lo:hi]))
         tel = cafs.SortTelemetry()
         cafs_sort_sharded(t, telemetry=tel)

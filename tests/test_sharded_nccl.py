@@ -38,6 +38,11 @@ rng = np.random.default_rng(3)
 cols = {
     "tiny": (rng.choice(rng.integers(-2**62, 2**62, 6), 400_000), "native"),
     "codes": (rng.integers(0, 4000, 2_000_000), "native"),
+    # a few keys outside the dense window the sample opens: the window class's
+    # all-reduce of the count arrays comes up short and the column is re-run
+    # with the pair-table exchange
+    "codes_outliers": (np.where(np.arange(2_000_000) % 399_999 == 7, 2**50 + np.arange(2_000_000),
+                                rng.integers(0, 4000, 2_000_000)), "native"),
     "main_hash": (rng.choice(rng.integers(-2**62, 2**62, 3000), 1_000_000), "native"),
     "many_pairs": (rng.choice(rng.integers(-2**62, 2**62, 50_000), 2_000_000), "native"),
     "many_pairs_zipf": (rng.integers(-2**62, 2**62, 300_000)[
@@ -79,7 +84,8 @@ for name, (x, path) in cols.items():
 # columns of changing route classes on one communicator: a prediction that
 # left the column's class out is re-run with the full pipeline
 order = ["tiny", "tiny", "tiny", "codes", "main_hash", "main_hash", "main_hash", "tiny",
-         "sorted", "codes", "codes", "codes", "many_pairs", "fallback", "codes", "tiny"]
+         "sorted", "codes", "codes", "codes", "codes_outliers", "codes", "codes", "many_pairs",
+         "fallback", "codes", "i32_codes", "i32_codes", "i32_codes", "tiny"]
 for i, name in enumerate(order):
     x, path = cols[name]
     x = x if x.dtype in (np.uint64, np.int32, np.uint32) else x.astype(np.int64)
