@@ -228,6 +228,16 @@ int cafs_partition_i64(cafs_ctx_t* ctx, const int64_t* d_x, uint64_t n, int is_s
                        uint64_t g_min, uint64_t g_max, int64_t* d_out, uint64_t* h_counts,
                        void* stream);
 
+/* The exchange plan of the distributed fallback, from every rank's bucket
+ * counts (counts[r * 4096 + b], all-gathered): rank `rank` sends rows
+ * [send_at[d], send_at[d] + send_n[d]) of its partitioned shard to rank d,
+ * receives recv_n[s] rows from rank s (stored in rank order), sorts what it
+ * received and keeps rows [*start, *start + its row count).  Pure host
+ * arithmetic (sharded.py bucket_ranges / _exchange_sort); the native sharded
+ * sort calls it between its two collectives. */
+int cafs_shard_fallback_plan(int world, int rank, const uint32_t* counts, uint64_t* send_at,
+                             uint64_t* send_n, uint64_t* recv_n, uint64_t* start);
+
 /* ---- stream-ordered sharded sort (one process per GPU, row shards) ----
  * The host-driven sharded path (sharded.py) synchronises between every
  * collective; these four calls enqueue the local phases on `stream` with the

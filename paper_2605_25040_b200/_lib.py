@@ -93,6 +93,7 @@ SIGNATURES = {
                                    ctypes.POINTER(_I), _P]),
     "cafs_key_span_i64": (_I, [_P, _P, _U64, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), _P]),
     "cafs_partition_i64": (_I, [_P, _P, _U64, _I, _U64, _U64, _P, ctypes.POINTER(_U64), _P]),
+    "cafs_shard_fallback_plan": (_I, [_I, _I, _P, _P, _P, _P, ctypes.POINTER(_U64)]),
     "cafs_gen_mix": (_I, [_P, _U64, _U64, _U64, _P]),
     "cafs_gen_draw": (_I, [_P, _U64, _U64, _U64, _P, _U64, _P, _P]),
 }

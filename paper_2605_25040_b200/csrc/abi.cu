@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -1916,6 +1917,13 @@ struct cafs_comm_t {
   // columns of that class in a row, else all (the same on every rank)
   uint32_t pred = 7, last_cls = 0;
   int sum_penalty = 0;  // calls left before the window class's sum pipeline is tried again
+  // distributed fallback (sharded_fallback): global span, every rank's bucket
+  // counts, this shard partitioned by bucket, the buckets received
+  u64* fb_span = nullptr;
+  u32* fb_counts = nullptr;
+  u32* h_counts = nullptr;  // pinned mirror of fb_counts
+  u64 *fb_part = nullptr, *fb_recv = nullptr;
+  u64 fb_part_len = 0, fb_recv_len = 0;
 };
 
 int cafs_nccl_unique_id(unsigned char* out) {
@@ -1933,8 +1941,10 @@ int cafs_comm_destroy(cafs_comm_t* comm) {
   for (auto& g : comm->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (comm->nc) ncclCommDestroy(comm->nc);
-  for (u64* p : {comm->hdr, comm->hdr_all, comm->samples, comm->send, comm->recv, comm->tiny_sum})
+  for (u64* p : {comm->hdr, comm->hdr_all, comm->samples, comm->send, comm->recv, comm->tiny_sum,
+                 comm->fb_span, (u64*)comm->fb_counts, comm->fb_part, comm->fb_recv})
     if (p) cudaFree(p);
+  if (comm->h_counts) cudaFreeHost(comm->h_counts);
   delete comm;
   return CAFS_OK;
 }
@@ -1973,6 +1983,47 @@ int cafs_comm_create(int device, const unsigned char* id, int world, int rank,
 }
 
 }  // extern "C"
+
+extern "C" int cafs_shard_fallback_plan(int world, int rank, const uint32_t* counts,
+                                        uint64_t* send_at, uint64_t* send_n, uint64_t* recv_n,
+                                        uint64_t* start) {
+  if (world < 1 || rank < 0 || rank >= world || !counts || !send_at || !send_n || !recv_n || !start)
+    return CAFS_EINVAL;
+  constexpr int B = CAFS_PARTITION_BUCKETS;
+  const int W = world, me = rank;
+  // rows of the sorted column before bucket b, and every rank's rows
+  std::vector<u64> P(B + 1, 0), rows(W, 0);
+  // L[r][b]: rows of rank r's partitioned shard before bucket b
+  std::vector<u64> L((size_t)W * (B + 1), 0);
+  for (int r = 0; r < W; ++r)
+    for (int b = 0; b < B; ++b)
+      L[(size_t)r * (B + 1) + b + 1] = L[(size_t)r * (B + 1) + b] + counts[(size_t)r * B + b];
+  for (int r = 0; r < W; ++r) rows[r] = L[(size_t)r * (B + 1) + B];
+  for (int b = 0; b < B; ++b) {
+    u64 t = 0;
+    for (int r = 0; r < W; ++r) t += counts[(size_t)r * B + b];
+    P[b + 1] = P[b] + t;
+  }
+  // the bucket range [lo, hi) overlapping rank d's rows [off_d, off_d + n_d): a
+  // bucket straddling two ranks' rows is in both ranges
+  std::vector<int> lo(W, 0), hi(W, 0);
+  u64 off = 0, my_off = 0;
+  for (int d = 0; d < W; ++d) {
+    if (d == me) my_off = off;
+    if (rows[d]) {
+      lo[d] = (int)(std::upper_bound(P.begin() + 1, P.end(), off) - (P.begin() + 1));
+      hi[d] = (int)(std::lower_bound(P.begin(), P.end() - 1, off + rows[d]) - P.begin());
+    }
+    off += rows[d];
+  }
+  for (int d = 0; d < W; ++d) {
+    send_at[d] = L[(size_t)me * (B + 1) + lo[d]];
+    send_n[d] = L[(size_t)me * (B + 1) + hi[d]] - send_at[d];
+    recv_n[d] = L[(size_t)d * (B + 1) + hi[me]] - L[(size_t)d * (B + 1) + lo[me]];
+  }
+  *start = rows[me] ? my_off - P[lo[me]] : 0;
+  return CAFS_OK;
+}
 
 namespace {
 
@@ -2062,6 +2113,111 @@ extern "C" {
 }  // extern "C"
 
 namespace {
+
+// The distributed fallback inside the library (fallback_sort, sorter.py:132-138,
+// over row shards), on the communicator's own NCCL ranks:
+//   1. the column's key span: all-reduce (min, max) of the shards' spans;
+//   2. this shard grouped into 4096 buckets by (key - min) >> shift -- the same
+//      digit on every rank, so bucket b precedes bucket b + 1 in the sorted
+//      column -- and an all-gather of every rank's bucket counts;
+//   3. each rank receives, from every rank, the buckets that overlap its rows
+//      of the sorted column (grouped ncclSend / ncclRecv of contiguous bucket
+//      ranges; a bucket straddling two ranks' rows goes to both), sorts them
+//      with the single-GPU fallback and keeps its rows.
+// ~8 B per key cross NVLink once; every rank sorts ~1/world of the column.
+// Two host synchronisations (span, counts): the transfer sizes are data.
+int sharded_fallback(cafs_ctx_t* ctx, cafs_comm_t* cm, u64* x, u64 n, u64 flip, cudaStream_t st) {
+  const int W = cm->world, me = cm->rank;
+  constexpr int B = CAFS_PARTITION_BUCKETS;
+  if (!cm->fb_span) {
+    CK(cudaMalloc(&cm->fb_span, 4 * 8));
+    CK(cudaMalloc(&cm->fb_counts, (size_t)W * B * 4));
+    CK(cudaMallocHost(&cm->h_counts, (size_t)W * B * 4 + 32));
+  }
+  TRY(ensure_radix(ctx, n ? n : 1, false));
+  // 1. span (an empty shard contributes [~0, 0])
+  u64* loc = cm->fb_span + 2;
+  if (n) {
+    launch_msd_span(x, n, flip, ctx->msd, ctx->num_sms, st);
+    ctx->launches++;
+    CKL();
+    CK(cudaMemcpyAsync(loc, (char*)ctx->msd + msd_span_offset(), 16, cudaMemcpyDeviceToDevice, st));
+  } else {
+    CK(cudaMemsetAsync(loc, 0xFF, 8, st));
+    CK(cudaMemsetAsync(loc + 1, 0, 8, st));
+  }
+  if (ncclGroupStart() != ncclSuccess ||
+      ncclAllReduce(loc, cm->fb_span, 1, ncclUint64, ncclMin, cm->nc, st) != ncclSuccess ||
+      ncclAllReduce(loc + 1, cm->fb_span + 1, 1, ncclUint64, ncclMax, cm->nc, st) != ncclSuccess ||
+      ncclGroupEnd() != ncclSuccess)
+    return fail(ctx, CAFS_ECUDA, "ncclAllReduce (key span)");
+  u64* hs = (u64*)((char*)cm->h_counts + (size_t)W * B * 4);
+  CK(cudaMemcpyAsync(hs, cm->fb_span, 16, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const u64 g_min = hs[0], g_max = hs[1];
+  // 2. partition and every rank's bucket counts
+  if (n > cm->fb_part_len) {
+    if (cm->fb_part) CK(cudaFree(cm->fb_part));
+    cm->fb_part = nullptr;
+    cm->fb_part_len = 0;
+    CK(cudaMalloc(&cm->fb_part, n * 8));
+    cm->fb_part_len = n;
+  }
+  u32* hist = (u32*)((char*)ctx->msd + msd_hist_offset());
+  if (n) {
+    launch_msd_partition(x, n, flip, ctx->msd, g_min, g_max, cm->fb_part, ctx->num_sms, st);
+    ctx->launches += 4;
+    CKL();
+  } else {
+    CK(cudaMemsetAsync(hist, 0, B * 4, st));
+  }
+  if (ncclAllGather(hist, cm->fb_counts, B, ncclUint32, cm->nc, st) != ncclSuccess)
+    return fail(ctx, CAFS_ECUDA, "ncclAllGather (bucket counts)");
+  CK(cudaMemcpyAsync(cm->h_counts, cm->fb_counts, (size_t)W * B * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<uint64_t> send_at(W), send_n(W), recv_n(W), recv_at(W + 1, 0);
+  uint64_t start = 0;
+  if (cafs_shard_fallback_plan(W, me, cm->h_counts, send_at.data(), send_n.data(), recv_n.data(),
+                               &start) != CAFS_OK)
+    return fail(ctx, CAFS_EINTERNAL, "sharded fallback: plan");
+  u64 mine = 0;
+  for (int b = 0; b < B; ++b) mine += cm->h_counts[(size_t)me * B + b];
+  if (mine != n) return fail(ctx, CAFS_EINTERNAL, "sharded fallback: bucket counts");
+  for (int r = 0; r < W; ++r) recv_at[r + 1] = recv_at[r] + recv_n[r];
+  const u64 R = recv_at[W];
+  if (R > cm->fb_recv_len) {
+    if (cm->fb_recv) CK(cudaFree(cm->fb_recv));
+    cm->fb_recv = nullptr;
+    cm->fb_recv_len = 0;
+    CK(cudaMalloc(&cm->fb_recv, R * 8));
+    cm->fb_recv_len = R;
+  }
+  // 3. the exchange: contiguous bucket ranges of the partitioned shard
+  if (ncclGroupStart() != ncclSuccess) return fail(ctx, CAFS_ECUDA, "ncclGroupStart");
+  bool nccl_ok = true;
+  for (int d = 0; d < W; ++d) {
+    const u64 a = send_at[d], cnt = send_n[d];
+    if (d == me) {
+      if (cnt)
+        CK(cudaMemcpyAsync(cm->fb_recv + recv_at[me], cm->fb_part + a, cnt * 8,
+                           cudaMemcpyDeviceToDevice, st));
+      continue;
+    }
+    if (cnt) nccl_ok &= ncclSend(cm->fb_part + a, cnt, ncclUint64, d, cm->nc, st) == ncclSuccess;
+    if (recv_n[d])
+      nccl_ok &= ncclRecv(cm->fb_recv + recv_at[d], recv_n[d], ncclUint64, d, cm->nc, st) ==
+                 ncclSuccess;
+  }
+  if (ncclGroupEnd() != ncclSuccess || !nccl_ok)
+    return fail(ctx, CAFS_ECUDA, "ncclSend / ncclRecv (bucket ranges)");
+  if (n == 0) return CAFS_OK;
+  // the received buckets sorted; this rank's rows start at `start`
+  TRY(fallback_sort(ctx, cm->fb_recv, R, flip, st));
+  if (start + n > R) return fail(ctx, CAFS_EINTERNAL, "sharded fallback: slice outside the received rows");
+  CK(cudaMemcpyAsync(x, cm->fb_recv + start, n * 8, cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  return CAFS_OK;
+}
 
 static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t n, int is_signed,
                         uint64_t hash_mult, cafs_telemetry_t* tel, int* h_status, void* stream,
@@ -2174,7 +2330,20 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
     TRY(sharded_exchange(ctx, comm, x, n, flip, st, 1, kk, used));
     CK(cudaStreamSynchronize(st));
   }
-  return shard_result(ctx, x, n, flip, tel, h_status, st, kk);
+  TRY(shard_result(ctx, x, n, flip, tel, h_status, st, kk));
+  static int native_fb = -1;  // CAFS_SHARD_FALLBACK=0: fallback columns return status 1
+  if (native_fb < 0) {
+    const char* e = getenv("CAFS_SHARD_FALLBACK");
+    native_fb = e ? atoi(e) != 0 : 1;
+  }
+  const int eff = ctx->h_ctl->eff_route;
+  if (*h_status == 1 && kk == 0 && native_fb &&
+      (eff == CAFS_FALLBACK_SMALL_N || eff == CAFS_FALLBACK_HIGH_ENTROPY)) {
+    // the dispatcher's fallback branch (every rank takes it: the route is global)
+    TRY(sharded_fallback(ctx, comm, (u64*)x, n, flip, st));
+    *h_status = 0;
+  }
+  return CAFS_OK;
 }
 
 }  // namespace

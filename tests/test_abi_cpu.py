@@ -75,3 +75,65 @@ def test_device_calls_fail_cleanly_without_gpu(lib):
     rc = lib.cafs_ctx_create(0, ctypes.byref(h))
     assert rc != 0 and not h.value
     assert lib.cafs_sort_i64(None, None, 0, 1, 1, 0, None, None) == _lib.EINVAL
+
+
+def test_fallback_exchange_plan_sorts_a_sharded_column(lib):
+    """cafs_shard_fallback_plan (the native distributed fallback's host step)
+    against sharded.bucket_ranges and an end-to-end numpy simulation of the
+    exchange: every rank's received buckets, sorted, hold its rows of the sorted
+    column at the planned offset.  Uneven and empty shards, skewed buckets."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2605_25040_b200.sharded import bucket_ranges, msd_shift
+
+    B = 4096
+    rng = np.random.default_rng(5)
+    cases = [
+        [rng.integers(0, 2**63, n, dtype=np.uint64) for n in (5000, 7000, 1, 9000)],
+        [rng.integers(0, 2**63, n, dtype=np.uint64) for n in (4000, 0, 6000)],          # empty shard
+        [np.full(3000, 7, np.uint64), rng.integers(0, 50, 2000).astype(np.uint64)],     # one bucket
+        [rng.integers(0, 2**63, 3000, dtype=np.uint64)],                                 # one rank
+        [np.concatenate([np.full(4000, 2**62, np.uint64),
+                         rng.integers(0, 2**63, 100, dtype=np.uint64)]) for _ in range(8)],  # straddling
+    ]
+    for shards in cases:
+        W = len(shards)
+        allk = np.concatenate(shards)
+        g_min, g_max = int(allk.min()), int(allk.max())
+        shift = msd_shift(g_min, g_max)
+        parts, counts = [], np.zeros((W, B), np.uint32)
+        for r, x in enumerate(shards):
+            d = ((x - np.uint64(g_min)) >> np.uint64(shift)).astype(np.int64)
+            order = np.argsort(d, kind="stable")
+            parts.append(x[order])
+            counts[r] = np.bincount(d, minlength=B)
+        sizes = [int(x.shape[0]) for x in shards]
+        ranges = bucket_ranges(counts.sum(0).astype(np.int64), sizes)
+        want = np.sort(allk)
+        plans = []
+        for r in range(W):
+            sa, sn, rn = (np.zeros(W, np.uint64) for _ in range(3))
+            start = ctypes.c_uint64(0)
+            rc = lib.cafs_shard_fallback_plan(W, r, counts.ctypes.data, sa.ctypes.data,
+                                              sn.ctypes.data, rn.ctypes.data, ctypes.byref(start))
+            assert rc == 0
+            plans.append((sa, sn, rn, int(start.value)))
+            L = np.concatenate([[0], np.cumsum(counts[r], dtype=np.int64)])
+            for d, (lo, hi) in enumerate(ranges):  # the Python host path's splits
+                assert int(sn[d]) == int(L[hi] - L[lo])
+                if sn[d]:
+                    assert int(sa[d]) == int(L[lo])
+        off = 0
+        for d in range(W):
+            for s_ in range(W):  # what s sends to d is what d expects from s
+                assert int(plans[s_][1][d]) == int(plans[d][2][s_])
+            recv = np.concatenate([parts[s_][int(plans[s_][0][d]):int(plans[s_][0][d] + plans[s_][1][d])]
+                                   for s_ in range(W)])
+            recv.sort()
+            st = plans[d][3]
+            assert np.array_equal(recv[st:st + sizes[d]], want[off:off + sizes[d]])
+            off += sizes[d]
+    bad = np.zeros(B, np.uint32)
+    assert lib.cafs_shard_fallback_plan(0, 0, bad.ctypes.data, None, None, None, None) != 0

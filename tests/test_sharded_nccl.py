@@ -47,10 +47,10 @@ cols = {
     "many_pairs": (rng.choice(rng.integers(-2**62, 2**62, 50_000), 2_000_000), "native"),
     "many_pairs_zipf": (rng.integers(-2**62, 2**62, 300_000)[
         np.minimum(rng.zipf(1.2, 6_000_000), 300_000) - 1], "native"),
-    "fallback": (rng.integers(-2**62, 2**62, 300_000), "host"),
+    "fallback": (rng.integers(-2**62, 2**62, 300_000), "native"),  # the library's own exchange sort
     "sorted": (np.arange(-50_000, 50_000, dtype=np.int64), "native"),
     "uint64": (rng.choice(rng.integers(0, 2**63, 500, dtype=np.uint64) * 2, 600_000), "native"),
-    "small_n": (rng.integers(-9, 9, 1500), "host"),
+    "small_n": (rng.integers(-9, 9, 1500), "native"),
     # 4-byte shards: cafs_sort_i32_sharded, 4 bytes per key read and written
     "i32_codes": (rng.integers(-2000, 2000, 1_500_000).astype(np.int32), "native"),
     "i32_many_pairs": (rng.integers(-2**31, 2**31, 40_000)[
