@@ -114,7 +114,7 @@ enum : int {
   kGateMainHP = 7,    // main route, no window, partitioned count (hashpart.cu)
   kGateMainOld = 8    // main route on the global-table path (window, or not partitioned)
 };
-constexpr int kHpParts = 512;      // key-range partitions of the partitioned count
+constexpr int kHpParts = 592;      // key-range partitions of the partitioned count
 constexpr double kHpMaxKhat = 524288.0;  // above: the global-table count
 
 // Programmatic dependent launch (sm_90+).  Pipeline kernels are launched with

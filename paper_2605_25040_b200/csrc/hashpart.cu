@@ -64,7 +64,7 @@ constexpr u32 kHpPartSlots = 4096;           // hp_reduce exact table
 constexpr u32 kHpPartCap = 2048;             // distinct keys per partition (load <= 1/2)
 constexpr u32 kHpListCap = kHpPartCap + kHpThreads;  // claims may overshoot by one per thread
 constexpr u32 kHpStage = kHpPartCap + 1;     // staged pairs per partition (+ the ~0 sentinel)
-static_assert(kHpP == 512, "scans below are written for 512 partitions");
+static_assert(kHpP % 2 == 0 && kHpP <= 1024, "partition map: half by mass, half by position");
 
 constexpr size_t kHpQueueBytes = (size_t)32 * kHpQ * 8;
 constexpr size_t kHpCountSmem = (size_t)kHpS * 12 + kHpQueueBytes + (size_t)kHpFine * 2;
@@ -128,12 +128,15 @@ __device__ __forceinline__ void hp_range(u64 body_keys, u64 skk, u32 c, u32 G, u
   *k1 = b < body_keys ? b : body_keys;
 }
 
-// Exclusive scan of 512 u32 counters by one warp (16 per lane); out[512] = total.
-__device__ __forceinline__ void hp_scan512(const u32* in, u32* out) {
+// Exclusive scan of the kHpP partition counters by one warp (kHpScanPer per
+// lane; the arrays are padded to a multiple of 32 with zeros); out[kHpP] = total.
+constexpr int kHpScanPer = (kHpP + 31) / 32;
+constexpr int kHpPad = 32 * kHpScanPer + 1;  // padded length of the per-partition arrays
+__device__ __forceinline__ void hp_scan_parts(const u32* in, u32* out) {
   const int lane = threadIdx.x & 31;
-  u32 v[16], s = 0;
+  u32 v[kHpScanPer], s = 0;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) { v[j] = in[lane * 16 + j]; s += v[j]; }
+  for (int j = 0; j < kHpScanPer; ++j) { v[j] = in[lane * kHpScanPer + j]; s += v[j]; }
   u32 inc = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -142,8 +145,9 @@ __device__ __forceinline__ void hp_scan512(const u32* in, u32* out) {
   }
   u32 run = inc - s;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) { out[lane * 16 + j] = run; run += v[j]; }
-  if (lane == 31) out[512] = run;
+  for (int j = 0; j < kHpScanPer; ++j) { out[lane * kHpScanPer + j] = run; run += v[j]; }
+  // (counters past kHpP are zero, so out[kHpP] is already the total when padded)
+  if (lane == 31) out[32 * kHpScanPer] = run;
 }
 
 // The spill of warp w lives in the vectors w itself has streamed: its j-th
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
   u32* tcnt = (u32*)(tkeys + kHpS);                     // [kHpS]
   u64* queue = (u64*)(tcnt + kHpS);                     // [32][kHpQ]
   unsigned short* pmap = (unsigned short*)(queue + 32 * kHpQ);  // [kHpFine]
-  __shared__ u32 shist[kHpP + 1], hstart[kHpP + 1], lhist[kHpP + 1], lstart[kHpP + 1];
+  __shared__ u32 shist[kHpPad], hstart[kHpPad], lhist[kHpPad], lstart[kHpPad];
   __shared__ u32 wsp[33];  // spilled keys per warp, then their prefix
   __shared__ u32 ncell_extra, sclaims;
   __shared__ u64 extra_k[16];
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
     tkeys[i] = hp_marker(a, i >> 1);
     tcnt[i] = 0;
   }
-  for (u32 i = tid; i <= kHpP; i += kHpThreads) shist[i] = 0;
+  for (u32 i = tid; i < kHpPad; i += kHpThreads) shist[i] = 0;
   __syncthreads();
   const u64 plo = s_lo;
   const int psh = s_sh;
@@ -412,7 +416,7 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
     wsp[lane] = inc - x;
     if (lane == 31) wsp[32] = inc;
   }
-  for (u32 i = tid; i <= kHpP; i += kHpThreads) lhist[i] = 0;
+  for (u32 i = tid; i < kHpPad; i += kHpThreads) lhist[i] = 0;
   __syncthreads();
 
   // ---- tail 1: the cells, counting-sorted by partition into this CTA's region.
@@ -438,8 +442,8 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
     cpos[kCpt] = pp | (atomicAdd(&lhist[pp], 1u) << 16);
   }
   __syncthreads();
-  if (wid == 0) hp_scan512(lhist, lstart);
-  else if (wid == 1) hp_scan512(shist, hstart);  // the spill's histogram, taken while spilling
+  if (wid == 0) hp_scan_parts(lhist, lstart);
+  else if (wid == 1) hp_scan_parts(shist, hstart);  // the spill's histogram, taken while spilling
   __syncthreads();
   for (u32 i = tid; i <= kHpP; i += kHpThreads) {
     a.cpofs[(size_t)c * (kHpP + 1) + i] = lstart[i];
