@@ -20,6 +20,13 @@ for c in cfg4 cfg1 cfg2 cfg3 cfg5 cfg4r; do
       -c 40 -o $O/r02_ncu_${c}_full python bench.py $args \
       > $O/r02_ncu_${c}_full.log 2>&1
 done
+# per-call device time at the per-rank shard sizes of an 8-GPU split, single-GPU
+# entry point and the native sharded one at one NCCL rank (profiles/percall.py)
+: > $O/r02_percall.txt
+for a in "cfg4 134217728" "cfg4 1073741824" "cfg2 3750000" "cfg3 3750000" "cfg4r 134217728"; do
+  python profiles/percall.py $a 30 2>&1 | tail -1 >> $O/r02_percall.txt
+  python profiles/percall.py $a 30 sharded 2>&1 | tail -1 >> $O/r02_percall.txt
+done
 echo done
 # summaries (the .ncu-rep files are too large to bring back): written next to
 # the launch lists, plus the DRAM-traffic table bench.py reads
