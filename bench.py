@@ -274,6 +274,10 @@ def main():
     sharded = world > 1 or args.sharded
     if sharded:
         import torch.distributed as dist
+        # NCCL_DEBUG=VERSION makes NCCL print its version on stdout: keep stdout
+        # to the one JSON line
+        if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+            del os.environ["NCCL_DEBUG"]
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
         os.environ.setdefault("RANK", str(rank))
@@ -305,7 +309,9 @@ def main():
     # warm-up with the timed region's own call (no telemetry): the library
     # captures a CUDA graph per (buffer, shape, flags) on its second sighting,
     # so the timed steps replay it rather than paying the capture
-    for _ in range(args.warmup):
+    # (the native sharded path settles later: its communicator predicts the
+    # column's route class after two calls and then captures that class's graph)
+    for _ in range(max(args.warmup, 6) if sharded else args.warmup):
         x.copy_(pristine)
         one_step(None)
     torch.cuda.synchronize()

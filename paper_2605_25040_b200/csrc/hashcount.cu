@@ -122,8 +122,6 @@ __device__ __forceinline__ u32 resolve_miss(bool active, u64 v, u64* skeys, u32*
 template <int STAGES, int STAGE_KEYS, int QCAP, bool RANGE, int KK, int SLOG2 = kSLog2>
 __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   constexpr u32 kS = 1u << SLOG2;
-  pdl_begin();
-  if (!gate_open(a.ctl, a.gate)) return;
   using K = typename KeyT<KK>::T;
   constexpr int KPV = 16 / sizeof(K);                         // keys per 16-byte vector
   constexpr u64 SK = (u64)STAGE_KEYS * 8 / sizeof(K);         // keys per stage
@@ -143,9 +141,10 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u64 flip = a.flip, mult = a.mult;
-  const u64 base = (RANGE && a.use_range) ? a.ctl->range_base : 0ull;
-  const u64 rlen = (RANGE && a.use_range) ? a.ctl->range_len : 0u;
 
+  // ---- before the programmatic dependency resolves (the estimate kernel may
+  // still be running): nothing here reads what it writes -- the tables are
+  // cleared and the ring's first stages are already on their way from HBM ----
   for (u32 i = tid; i < kS; i += kHcThreads) { skeys[i] = kEmpty; scnt[i] = 0; }
   if (RANGE)
     for (u32 i = tid; i < kRange; i += kHcThreads) dcnt[i] = 0;
@@ -170,6 +169,25 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   const u64 nchunks = (body + SK - 1) / SK;
   const u64 my_chunks =
       nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const u64 pre_chunks = my_chunks < (u64)STAGES ? my_chunks : (u64)STAGES;
+  if (tid == 0) {
+    for (u64 it = 0; it < pre_chunks; ++it) {
+      const u64 off = (blockIdx.x + it * gridDim.x) * SK;
+      const u32 bytes = (u32)(((body - off) < SK ? (body - off) : SK) * sizeof(K));
+      mbar_arrive_expect_tx(&full[it], bytes);
+      tma_load_1d(stage + (size_t)it * STAGE_KEYS, xb + off, bytes, &full[it]);
+    }
+  }
+  pdl_begin();
+  if (!gate_open(a.ctl, a.gate)) {
+    // not this column's shape: let the stages in flight land before the CTA
+    // (and its shared memory) goes
+    if (tid == 0)
+      for (u64 it = 0; it < pre_chunks; ++it) mbar_wait(&full[it], 0);
+    return;
+  }
+  const u64 base = (RANGE && a.use_range) ? a.ctl->range_base : 0ull;
+  const u64 rlen = (RANGE && a.use_range) ? a.ctl->range_len : 0u;
 
   u64 empty_cnt = 0;
   u32 glob_cnt = 0;
@@ -190,8 +208,8 @@ __global__ void __launch_bounds__(kHcThreads, 1) hash_count_kernel(HcArgs a) {
   if (wid == 0) {
     // ---- TMA producer ----
     if (lane == 0) {
-      u32 s = 0, ph = 0;
-      for (u64 it = 0; it < my_chunks; ++it) {
+      u32 s = 0, ph = 1;  // the first STAGES chunks were issued above: one lap done
+      for (u64 it = pre_chunks; it < my_chunks; ++it) {
         if (it >= (u64)STAGES) mbar_wait(&empty[s], ph ^ 1);
         const u64 off = (blockIdx.x + it * gridDim.x) * SK;
         const u32 bytes = (u32)(((body - off) < SK ? (body - off) : SK) * sizeof(K));
@@ -601,27 +619,42 @@ __global__ void __launch_bounds__(1024) dense_pairs_kernel(DevCtl* ctl, u64* den
                                                            u64* pcnt, u64* skeys, u64* scnt,
                                                            u64* soffs, u64 n_expect, int gate) {
   pdl_begin();
-  if (!gate_open(ctl, gate)) return;  // the count kernel was gated off too: dense untouched
-  if (ctl->overflow) {  // guard: the fallback sorts; leave the window zeroed for the next call
-    for (u32 d = threadIdx.x; d < ctl->range_len; d += blockDim.x) dense[d] = 0;
-    return;
-  }
   __shared__ u32 wsum[32];
   __shared__ unsigned long long csum[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const u64 base = ctl->range_base;
-  const u32 rlen = ctl->range_len;
-  // ~0: the counts were all-reduced over the ranks of a sharded sort and must
-  // sum to the whole column
-  if (n_expect == ~0ull) n_expect = ctl->n_global;
+  // one round trip: the control words and the whole window are loaded together
+  // (the window is kRange words whatever its open length, zero outside it),
+  // the gate is checked afterwards
   constexpr int IT = kRange / 1024;
   u64 c[IT];
+  {
+    const ulonglong2* dv = (const ulonglong2*)(dense + tid * IT);
+#pragma unroll
+    for (int q = 0; q < IT / 2; ++q) {
+      const ulonglong2 w = __ldcg(dv + q);
+      c[2 * q] = w.x;
+      c[2 * q + 1] = w.y;
+    }
+  }
+  const u64 base = ctl->range_base;
+  const u32 rlen = ctl->range_len;
+  const int ovf = ctl->overflow;
+  const u64 m = ctl->npairs;  // pairs compacted from the hash table
+  // ~0: the counts were all-reduced over the ranks of a sharded sort and must
+  // sum to the whole column
+  const u64 ng = ctl->n_global;
+  if (n_expect == ~0ull) n_expect = ng;
+  if (!gate_open(ctl, gate)) return;  // the count kernel was gated off too: dense untouched
+  if (ovf) {  // guard: the fallback sorts; leave the window zeroed for the next call
+    for (u32 d = threadIdx.x; d < rlen; d += blockDim.x) dense[d] = 0;
+    return;
+  }
   u32 nz = 0;
   u64 local = 0;
 #pragma unroll
   for (int q = 0; q < IT; ++q) {
     const u32 d = tid * IT + q;
-    c[q] = d < rlen ? dense[d] : 0;
+    if (d >= rlen) c[q] = 0;
     nz += c[q] != 0;
     local += c[q];
   }
@@ -651,7 +684,6 @@ __global__ void __launch_bounds__(1024) dense_pairs_kernel(DevCtl* ctl, u64* den
   __syncthreads();
   const u32 ndense = wsum[31];
   const u64 dtotal = csum[31];
-  const u64 m = ctl->npairs;  // pairs compacted from the hash table
   const bool direct = (m == 0);
   u32 slot = inz - nz + (wid ? wsum[wid - 1] : 0);
   u64 off = icnt - local + (wid ? csum[wid - 1] : 0);
