@@ -682,9 +682,12 @@ enum : uint32_t {
 
 uint32_t groups_needed(const DevCtl& c) {
   const int r = c.eff_route;
-  uint32_t main = c.range_len > 0 ? (kGrpDense | kGrpOld | kGrpDensePairs)
-                  : c.hp_ok       ? kGrpHp
-                                  : (kGrpTable | kGrpOld);
+  // (a dense-window column whose keys all fell inside the window needs neither
+  // the compaction nor the pair sort: its window counts are the sorted pairs)
+  uint32_t main = c.range_len > 0
+                      ? (kGrpDense | kGrpDensePairs | ((c.dense_outside || c.overflow) ? kGrpOld : 0u))
+                  : c.hp_ok ? kGrpHp
+                            : (kGrpTable | kGrpOld);
   if (r == CAFS_TINY_COUNT) return kGrpTiny | (c.tiny_failed ? main : 0u);
   if (r == CAFS_MAIN) return main;
   return 0;  // sorted input (or its scan), fallback routes: the host's
@@ -1318,6 +1321,14 @@ static int sort_impl(cafs_ctx_t* ctx, void* d_x, uint64_t n, int is_signed, uint
       // the whole pipeline (nothing was written to the column)
       tm.n = 0;
       int rc2 = CAFS_OK;
+      if ((used & kGrpDense) && !(used & kGrpOld) && ctx->h_ctl->dense_outside &&
+          !ctx->h_ctl->overflow) {
+        // the window-only pipeline counted keys outside the window into the
+        // global table and held no compaction: empty the table first
+        launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
+                       ctx->num_sms, st, kGateNone);
+        ctx->launches++;
+      }
       pipeline_direct(ctx, x, n, flip, hash_mult, flags, tm, st, exact, &mark, &rc2, kk);
       TRY(rc2);
       CKL();

@@ -71,7 +71,8 @@ struct DevCtl {
   int32_t eff_route;             // route with the monotone prefix applied (kNeedScan: unknown)
   int32_t tiny_failed;           // the tiny pass missed a value -> main route runs
   u32 tiny_done;                 // CTAs of the tiny count finished (last one finalizes)
-  u32 _pad2;
+  u32 dense_outside;             // dense-window route: keys fell outside the window (they sit in
+                                 // the global table and need the compaction + pair sort group)
   // --- sharded (stream-ordered) pipeline: this rank's rows of the sorted column ---
   u64 slice[2];                  // [begin, end) in global positions
   u64 n_global;

@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(1024, 1)
     ctl->sum_error = 0;
     ctl->tiny_failed = 0;
     ctl->tiny_done = 0;
+    ctl->dense_outside = 0;
     ctl->hp_overflow = 0;
     ctl->merge_bad = 0;
     ctl->local_hp = 0;

@@ -713,6 +713,9 @@ __global__ void __launch_bounds__(1024) dense_pairs_kernel(DevCtl* ctl, u64* den
       ctl->sum_error = (dtotal != n_expect);
       ctl->pairs_ready = (dtotal == n_expect);
     }
+    // keys outside the window: compacted pairs, or (when the pipeline held no
+    // compaction) window counts short of the rows
+    ctl->dense_outside = (m != 0) || dtotal != n_expect;
   }
 }
 

@@ -193,10 +193,19 @@ def test_route_changes_on_one_buffer():
         "fallback": torch.randint(-2**62, 2**62, (n,), device="cuda", generator=g),
         "sorted": torch.arange(n, device="cuda", dtype=torch.int64) * 3 - n,
     }
+    # dictionary codes with a few keys outside the window the sample opens: a
+    # pipeline cached for in-window codes holds no compaction / pair sort and
+    # must be re-run with them (and the next in-window column must not see
+    # leftovers in the global table)
+    outl = cols["dense"].clone()
+    outl[11::300_007] = 2**55 + torch.arange(outl[11::300_007].shape[0], device="cuda")
+    cols["dense_outliers"] = outl
     want = {k: np.sort(v.cpu().numpy()) for k, v in cols.items()}
     buf = torch.empty(n, dtype=torch.int64, device="cuda")
     order = ["tiny", "dense", "dense", "partitioned", "partitioned", "tiny", "fallback",
-             "dense", "sorted", "partitioned", "tiny", "tiny", "fallback", "dense"]
+             "dense", "sorted", "partitioned", "tiny", "tiny", "fallback", "dense",
+             "dense", "dense_outliers", "dense", "dense", "dense_outliers", "dense_outliers",
+             "dense_outliers", "dense"]
     for rep in range(2):
         for name in order:
             buf.copy_(cols[name])
