@@ -2348,10 +2348,30 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
     native_fb = e ? atoi(e) != 0 : 1;
   }
   const int eff = ctx->h_ctl->eff_route;
-  if (*h_status == 1 && kk == 0 && native_fb &&
+  if (*h_status == 1 && native_fb &&
       (eff == CAFS_FALLBACK_SMALL_N || eff == CAFS_FALLBACK_HIGH_ENTROPY)) {
     // the dispatcher's fallback branch (every rank takes it: the route is global)
-    TRY(sharded_fallback(ctx, comm, (u64*)x, n, flip, st));
+    if (kk == 0) {
+      TRY(sharded_fallback(ctx, comm, (u64*)x, n, flip, st));
+    } else {
+      // 4-byte shards: exchanged and sorted as their order-preserving 64-bit
+      // widening (like the single-GPU fallback of 4-byte columns)
+      if (n > ctx->wide_elems) {
+        if (ctx->wide) CK(cudaFree(ctx->wide));
+        ctx->wide = nullptr;
+        ctx->wide_elems = 0;
+        CK(cudaMalloc(&ctx->wide, (n ? n : 1) * 8));
+        ctx->wide_elems = n ? n : 1;
+      }
+      if (n) launch_widen(x, n, kk, ctx->wide, ctx->num_sms, st);
+      TRY(sharded_fallback(ctx, comm, ctx->wide, n, kSign, st));
+      if (n) {
+        launch_narrow(ctx->wide, n, kk, x, ctx->num_sms, st);
+        ctx->launches += 2;
+        CKL();
+        CK(cudaStreamSynchronize(st));
+      }
+    }
     *h_status = 0;
   }
   return CAFS_OK;

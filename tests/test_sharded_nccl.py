@@ -5,7 +5,8 @@ across direct, captured and replayed calls; columns the device cannot finish
 finish natively too (> 8192 pairs per rank: the partitioned count sorts each
 shard's pairs, the library grows its exchange row once and merges the
 gathered lists on device); int32 / uint32 shards run natively at 4 bytes per
-key (cafs_sort_i32_sharded); fallback routes take the host-driven path ("host").  (More ranks need more GPUs than this pool
+key (cafs_sort_i32_sharded); fallback routes are exchanged and sorted inside
+the library too (the distributed fallback; 4-byte shards as their widening).  (More ranks need more GPUs than this pool
 gives: the 2-rank tests in test_sharded_gpu.py share one GPU over gloo.)"""
 
 import os
@@ -57,6 +58,8 @@ cols = {
         rng.integers(0, 40_000, 2_000_000)].astype(np.int32), "native"),
     "i32_extremes": (rng.choice(np.array([-2**31, 2**31 - 1, -1, 0, 7], np.int64),
                                 900_001).astype(np.int32), "native"),
+    "i32_fallback": (rng.integers(-2**31, 2**31, 300_000).astype(np.int32), "native"),
+    "u32_small_n": (rng.integers(0, 2**32, 900, dtype=np.uint64).astype(np.uint32), "native"),
     "u32_main": (rng.choice(rng.integers(0, 2**32, 3000, dtype=np.uint64), 1_000_000)
                  .astype(np.uint32), "native"),
 }
