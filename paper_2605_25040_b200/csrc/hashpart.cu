@@ -615,16 +615,29 @@ __global__ void __launch_bounds__(kHpThreads, 2) hp_reduce_kernel(HpArgs a, u32 
   for (u32 i0 = 0; i0 < total; i0 += kHpThreads * kRdUnroll) {  // CTA-uniform
     u64 k[kRdUnroll];
     u32 w[kRdUnroll];
+    u32 j = 0;  // the segment of this thread's previous item (its items ascend)
 #pragma unroll
     for (int r = 0; r < kRdUnroll; ++r) {
-      const u32 i = i0 + r * kHpThreads + tid;
+      // a warp takes 128 consecutive items, 32 per step: the first item's
+      // segment by binary search, the next ones' by a short walk from it
+      const u32 i = i0 + (u32)wid * (32 * kRdUnroll) + r * 32 + lane;
       w[r] = 0;
       k[r] = 0;
       if (i < total) {
-        u32 j = 0;
+        bool found = false;
+        if (r > 0) {
 #pragma unroll
-        for (u32 st = SH ? 16 : 256; st > 0; st >>= 1)  // sharded: nseg < 32 ranks
-          if (j + st < nseg && segs[j + st] <= i) j += st;
+          for (int s2 = 0; s2 < 6 && !found; ++s2) {
+            if (segs[j + 1] > i) found = true;
+            else ++j;
+          }
+        }
+        if (!found) {
+          j = 0;
+#pragma unroll
+          for (u32 st = SH ? 16 : 256; st > 0; st >>= 1)  // sharded: nseg < 32 ranks
+            if (j + st < nseg && segs[j + st] <= i) j += st;
+        }
         const u32 off = sbeg[j] + (i - segs[j]);
         if (SH) {
           const u64* L = a.recv + (size_t)j * a.row;
