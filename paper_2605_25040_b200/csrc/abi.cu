@@ -704,6 +704,8 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
   TRY(ensure_main(ctx));
   DevCtl* c = ctx->d_ctl;
   int ts, tk;
+  // CAFS_EMIT_MAP=1 (experiment): the map for every route-specific pipeline
+  static const int force_map = getenv("CAFS_EMIT_MAP") ? atoi(getenv("CAFS_EMIT_MAP")) : 0;
   if (groups & kGrpTiny) {
     ts = tm.begin();
     tk = tm.begin();
@@ -727,8 +729,11 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
       ctx->launches++;
     }
     if (hp && e == cudaSuccess) {  // the partitioned count: the sorted pairs, no pair sort
+      // a pipeline that holds only the partitioned count (its route predicted)
+      // also gets the emit's tile -> pair map, written with the pairs' offsets
       e = launch_hp_count(hp_bufs(ctx), x, n, flip, c, ctx->pk_b, ctx->pc_b, ctx->poffs,
-                          ctx->num_sms, st, kGateMainHP, kk);
+                          ctx->num_sms, st, kGateMainHP, kk,
+                          (with_emit && groups == kGrpHp && !force_map) ? ctx->tile_map : nullptr);
       ctx->launches += 3;
     }
     if (e == cudaSuccess && (groups & kGrpTable)) {
@@ -761,13 +766,14 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
   }
   // a pipeline that holds only the partitioned count (its route predicted)
   // also writes the emit's tile -> pair map: its pair sets are large
-  static const int force_map = getenv("CAFS_EMIT_MAP") ? atoi(getenv("CAFS_EMIT_MAP")) : 0;
-  bool map = hp && groups == kGrpHp;
-  if (force_map && with_emit && groups != kGrpAll && groups != 0 && !(groups & kGrpTiny)) {
+  bool map = hp && groups == kGrpHp;  // written by hp_place
+  const bool map_kernel = force_map && with_emit && groups != kGrpAll && groups != 0 &&
+                          !(groups & kGrpTiny);
+  if (map_kernel) {
     TRY(ensure_tile_map(ctx, n, kk));
     map = true;
   }
-  if (with_emit && map) {
+  if (with_emit && map_kernel) {
     launch_emit_map(ctx->poffs, c, x, 0, n, ctx->tile_map, (u64)ctx->num_sms * 8 * 256,
                     ctx->num_sms, st, kk);
     ctx->launches++;

@@ -106,6 +106,10 @@ struct HpArgs {
   const u64* recv;
   u64 row, cap;
   int shard;
+  // the emit's tile -> pair map (emit.cu), written by hp_place for the
+  // single-GPU pipeline's emit of the whole column; null: not wanted
+  u32* tile_pair;
+  int kk;
 };
 
 __device__ __forceinline__ u64 hp_marker(const HpArgs& a, u32 b) {
@@ -784,10 +788,36 @@ __global__ void __launch_bounds__(256) hp_place_kernel(HpArgs a) {
       before += w2 < wid ? wsc[w2] : 0;
       all += wsc[w2];
     }
+    const u64 rs = run + before + inc - cnt;  // the pair's first row
     if (i < dd) {
       a.pk[D + i] = sk[i];
       a.pc[D + i] = cnt;
-      a.poffs[D + i] = run + before + inc - cnt;
+      a.poffs[D + i] = rs;
+    }
+    if (a.tile_pair) {
+      // tile_pair[t] = the pair holding the first key of the emit's tile t
+      // (the emit of rows [0, n) into x: same head / tile geometry as emit.cu)
+      const u64 TK = a.kk ? 2048 : 1024, VK = a.kk ? 8 : 4, ksz = a.kk ? 4 : 8;
+      const u64 mis = (((uintptr_t)a.x) & 31) / ksz;
+      const u64 hd = mis ? ((VK - mis) < a.n ? (VK - mis) : a.n) : 0;
+      const u64 nkeys = (a.n - hd) / VK * VK;
+      const u64 ntiles = (nkeys + TK - 1) / TK;
+      u64 t_lo = 0, t_hi = 0;
+      if (i < dd && cnt) {
+        const u64 re = rs + cnt;
+        t_lo = rs <= hd ? 0 : (rs - hd + TK - 1) / TK;
+        t_hi = re <= hd ? 0 : (re - hd + TK - 1) / TK;
+        if (t_hi > ntiles) t_hi = ntiles;
+      }
+      const bool longrun = t_hi > t_lo + 32;
+      if (!longrun)
+        for (u64 t = t_lo; t < t_hi; ++t) a.tile_pair[t] = (u32)(D + i);
+      for (u32 m = __ballot_sync(0xffffffffu, longrun); m; m &= m - 1) {
+        const int r = __ffs(m) - 1;
+        const u64 lo = __shfl_sync(0xffffffffu, t_lo, r), hi = __shfl_sync(0xffffffffu, t_hi, r);
+        const u32 pr = (u32)(D + b0 + (u32)(wid * 32 + r));
+        for (u64 t = lo + lane; t < hi; t += 32) a.tile_pair[t] = pr;
+      }
     }
     run += all;
     __syncthreads();
@@ -985,9 +1015,11 @@ static cudaError_t hp_launch_t(const HpArgs& a, int G, cudaStream_t st) {
 
 cudaError_t launch_hp_count(const HpBufs& b, const void* x, u64 n, u64 flip, DevCtl* ctl,
                             u64* pk, u64* pc, u64* poffs, int num_sms, cudaStream_t st, int gate,
-                            int kk) {
+                            int kk, u32* tile_pair) {
   const int G = hp_grid(n, kk, num_sms);
-  const HpArgs a = hp_args(b, x, n, flip, ctl, pk, pc, poffs, gate, G);
+  HpArgs a = hp_args(b, x, n, flip, ctl, pk, pc, poffs, gate, G);
+  a.tile_pair = tile_pair;
+  a.kk = kk;
   if (kk == 1) return hp_launch_t<1>(a, G, st);
   if (kk == 2) return hp_launch_t<2>(a, G, st);
   return hp_launch_t<0>(a, G, st);

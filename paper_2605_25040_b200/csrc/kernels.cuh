@@ -60,8 +60,10 @@ struct HpBufs {
   u64* pc_stage;
 };
 size_t hp_scratch_bytes(int num_sms);
+// tile_pair: the emit's tile -> pair map for the whole column (null: not written)
 cudaError_t launch_hp_count(const HpBufs& b, const void* x, u64 n, u64 flip, DevCtl* ctl, u64* pk,
-                            u64* pc, u64* poffs, int num_sms, cudaStream_t st, int gate, int kk);
+                            u64* pc, u64* poffs, int num_sms, cudaStream_t st, int gate, int kk,
+                            u32* tile_pair = nullptr);
 cudaError_t launch_hp_shard_merge(const HpBufs& b, const u64* recv, int world, u64 cap, u64 row,
                                   DevCtl* ctl, u64* pk, u64* pc, u64* poffs, cudaStream_t st);
 void launch_hp_restore(const HpBufs& b, void* x, u64 n, u64 flip, int num_sms, cudaStream_t st,
