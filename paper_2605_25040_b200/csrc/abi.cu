@@ -1088,13 +1088,14 @@ uint32_t shard_class(const DevCtl& h) {
 // sorted local pairs -> this rank's send row [np, keys[cap], counts[cap]]
 int shard_count_enqueue(cafs_ctx_t* ctx, const void* x, u64 n, u64 flip, u64 mult,
                         const u64* hdr_all, int world, const u64* samples, u64* tiny, u64* send,
-                        u64 cap, cudaStream_t st, int kk = 0, uint32_t cls = kClsAll) {
+                        u64 cap, cudaStream_t st, int kk = 0, uint32_t cls = kClsAll,
+                        int est_opts = 0) {
   DevCtl* c = ctx->d_ctl;
   // the partitioned count gives this shard's pairs sorted on device for any
   // number of keys (the table path's pair sort stops at 8192)
   const bool hp = hp_allowed(n, false);
   if (hp) TRY(ensure_hp(ctx, n, kk));
-  launch_estimate_sharded(samples, hdr_all, world, c, st, hp ? kEstHp : 0);
+  launch_estimate_sharded(samples, hdr_all, world, c, st, (hp ? kEstHp : 0) | est_opts);
   ctx->launches++;
   if (cls & kClsTiny) {
     launch_tiny_count(x, n, flip, c, ctx->num_sms, st, kGateTiny, kk);
@@ -2089,7 +2090,7 @@ int comm_resize(cafs_ctx_t* ctx, cafs_comm_t* c, u64 cap) {
 }
 
 int sharded_enqueue(cafs_ctx_t* ctx, cafs_comm_t* cm, void* x, u64 n, u64 flip, u64 mult,
-                    cudaStream_t st, int kk, uint32_t cls) {
+                    cudaStream_t st, int kk, uint32_t cls, int est_opts = 0) {
   const u64 cap = cm->cap, row = cm->row, tiny_off = 1 + 2 * cap;
   launch_shard_header(x, n, flip, cm->hdr, ctx->num_sms, st, kk);
   if (ncclAllGather(cm->hdr, cm->hdr_all, kShardHdrWords, ncclUint64, cm->nc, st) != ncclSuccess)
@@ -2101,7 +2102,7 @@ int sharded_enqueue(cafs_ctx_t* ctx, cafs_comm_t* cm, void* x, u64 n, u64 flip, 
     return fail(ctx, CAFS_ECUDA, "ncclAllReduce (samples)");
   if (cls == kClsWindowSum) {
     DevCtl* c = ctx->d_ctl;
-    launch_estimate_sharded(cm->samples, cm->hdr_all, cm->world, c, st, 0);
+    launch_estimate_sharded(cm->samples, cm->hdr_all, cm->world, c, st, est_opts);
     cudaError_t e = launch_hash_count(x, n, flip, mult, c, ctx->gkeys, ctx->gcnt, ctx->glist, 1,
                                       ctx->num_sms, st, 0, kGateMainDense, ctx->dense, kk);
     if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
@@ -2118,7 +2119,7 @@ int sharded_enqueue(cafs_ctx_t* ctx, cafs_comm_t* cm, void* x, u64 n, u64 flip, 
     return CAFS_OK;
   }
   TRY(shard_count_enqueue(ctx, x, n, flip, mult, cm->hdr_all, cm->world, cm->samples,
-                          cm->send + tiny_off, cm->send, cap, st, kk, cls));
+                          cm->send + tiny_off, cm->send, cap, st, kk, cls, est_opts));
   ctx->launches += 3;  // header (2), samples
   return sharded_exchange(ctx, cm, x, n, flip, st, 0, kk, cls);
 }
@@ -2336,6 +2337,16 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
       comm->last_cls = now;
     }
   }
+  bool tiny_retry = false;
+  if (h.eff_route == CAFS_TINY_COUNT && h.tiny_failed) {
+    // some rank met a value the sample missed (every rank sees it in the
+    // gathered counters): MAIN with the same estimate (sorter.py:378-385), the
+    // full pipeline again with the route forced
+    used = kClsAll;
+    TRY(sharded_enqueue(ctx, comm, x, n, flip, hash_mult, st, kk, used, kEstForceMain));
+    CK(cudaStreamSynchronize(st));
+    tiny_retry = true;
+  }
   if (h.eff_route == CAFS_MAIN && h.merge_bad && h.shard_grow > comm->cap &&
       h.shard_grow <= kShardCapMax) {
     // some rank's sorted pairs did not fit the exchange row: every rank saw it
@@ -2348,6 +2359,7 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
     CK(cudaStreamSynchronize(st));
   }
   TRY(shard_result(ctx, x, n, flip, tel, h_status, st, kk));
+  if (tiny_retry && tel) tel->tiny_count_failed = 1;
   static int native_fb = -1;  // CAFS_SHARD_FALLBACK=0: fallback columns return status 1
   if (native_fb < 0) {
     const char* e = getenv("CAFS_SHARD_FALLBACK");

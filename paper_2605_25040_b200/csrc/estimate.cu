@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(1024, 1)
   else if (k_hat <= 8.0 && u <= 8) route = CAFS_TINY_COUNT;
   else if (__dmul_rn(k_hat, 2.0) > (double)nn) route = CAFS_FALLBACK_HIGH_ENTROPY;
   else route = CAFS_MAIN;
+  if ((opts & kEstForceMain) && route == CAFS_TINY_COUNT) route = CAFS_MAIN;
 
   // ---- tiny route: perfect hash of the <= 8 keys into 16 slots ----
   if (route == CAFS_TINY_COUNT) {

@@ -11,8 +11,10 @@ constexpr u64 kExpectCtlN = ~0ull - 1;  // pair-sort `expect`: the sharded colum
 
 // estimate.cu
 // `kk`: key kind (common.cuh): 0 = 64-bit, 1 = int32, 2 = uint32
-// opts: kEstHp (the partitioned count may run), kEstNoWindow (no dense window)
-enum : int { kEstHp = 1, kEstNoWindow = 2 };
+// opts: kEstHp (the partitioned count may run), kEstNoWindow (no dense window),
+// kEstForceMain (a tiny route becomes MAIN with the same estimate: the re-entry
+// after a tiny miss, sorter.py:378-385)
+enum : int { kEstHp = 1, kEstNoWindow = 2, kEstForceMain = 4 };
 void launch_estimate(const void* x, u64 n, u64 flip, int check_prefix, DevCtl* ctl,
                      cudaStream_t st, int kk = 0, int opts = 0);
 void launch_monotone_scan(const void* x, u64 n, u64 flip, DevCtl* ctl, int num_sms,

@@ -553,6 +553,7 @@ def _sort_sharded_native(x_local, comm, ops, tel, mult: int) -> bool:
     tel.sharded_path = "native"
     tel.counted_total = int(t.counted_total)
     tel.pairs = int(t.pairs)
+    tel.tiny_count_failed = bool(t.tiny_count_failed)  # re-entered MAIN inside the call
     if tel.decision.route is Route.MAIN:
         tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, 4)
     return True
@@ -580,6 +581,7 @@ def _sort_sharded_native32(x_local, group, mult: int, telemetry) -> bool:
     tel.sharded_path = "native"
     tel.counted_total = int(t.counted_total)
     tel.pairs = int(t.pairs)
+    tel.tiny_count_failed = bool(t.tiny_count_failed)
     if tel.decision.route is Route.MAIN:
         # the reference's table for 4-byte keys has 8-slot buckets (buckets.py:33-43)
         tel.table_buckets = table_size_for(max(1.0, tel.decision.estimate.k_hat), tel.n, 8)

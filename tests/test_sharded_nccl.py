@@ -39,6 +39,7 @@ rng = np.random.default_rng(3)
 cols = {
     "tiny": (rng.choice(rng.integers(-2**62, 2**62, 6), 400_000), "native"),
     "codes": (rng.integers(0, 4000, 2_000_000), "native"),
+    "tiny_miss": (None, "native"),  # filled below: a value the 1024 strided samples do not see
     # a few keys outside the dense window the sample opens: the window class's
     # all-reduce of the count arrays comes up short and the column is re-run
     # with the pair-table exchange
@@ -63,6 +64,9 @@ cols = {
     "u32_main": (rng.choice(rng.integers(0, 2**32, 3000, dtype=np.uint64), 1_000_000)
                  .astype(np.uint32), "native"),
 }
+_tm = rng.choice(rng.integers(-2**62, 2**62, 6), 400_000)
+_tm[1:4] = 12345  # rows 1..3: not multiples of the sample stride 400000 // 1024
+cols["tiny_miss"] = (_tm, "native")  # the tiny count misses -> MAIN inside the native call
 TDT = {np.dtype(np.uint64): torch.uint64, np.dtype(np.int64): torch.int64,
        np.dtype(np.int32): torch.int32, np.dtype(np.uint32): torch.uint32}
 MULTS = {"main_hash": 0x2545F4914F6CDD1D}  # a caller's odd hash multiplier (buckets.py:54-67)
@@ -82,13 +86,14 @@ for name, (x, path) in cols.items():
         torch.cuda.synchronize()
         got_path = tel.sharded_path
         if (not np.array_equal(t.cpu().numpy(), want) or tel.route.value != route
-                or got_path != path):
+                or got_path != path or tel.tiny_count_failed != (name == "tiny_miss")):
             bad.append((name, rep, tel.route.value, route, got_path, path))
 # columns of changing route classes on one communicator: a prediction that
 # left the column's class out is re-run with the full pipeline
 order = ["tiny", "tiny", "tiny", "codes", "main_hash", "main_hash", "main_hash", "tiny",
          "sorted", "codes", "codes", "codes", "codes_outliers", "codes", "codes", "many_pairs",
-         "fallback", "codes", "i32_codes", "i32_codes", "i32_codes", "tiny"]
+         "fallback", "codes", "i32_codes", "i32_codes", "i32_codes", "tiny", "tiny", "tiny_miss",
+         "tiny", "tiny_miss", "tiny_miss", "codes"]
 for i, name in enumerate(order):
     x, path = cols[name]
     x = x if x.dtype in (np.uint64, np.int32, np.uint32) else x.astype(np.int64)
