@@ -70,7 +70,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", os.environ.get("CAFS_BENCH_SMI_MS", "100")],
                 stdout=fd, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
