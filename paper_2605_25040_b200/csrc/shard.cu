@@ -26,6 +26,12 @@ __global__ void __launch_bounds__(1024) shard_header_kernel(const typename KeyT<
   // thread t checks rows [16t, 16t + 16]: 17 loads in flight at once (one
   // DRAM round trip for the reference's first chunk, not 16)
   const u64 i0 = (u64)threadIdx.x * 16;
+  // (thread 0's first / last key ride in the same round trip)
+  u64 kfirst = 0, klast = 0;
+  if (threadIdx.x == 0 && n) {
+    kfirst = key_map<KK>(x[0], flip);
+    klast = key_map<KK>(x[n - 1], flip);
+  }
   u64 a[17];
 #pragma unroll
   for (int j = 0; j < 17; ++j) a[j] = i0 + j < P ? key_map<KK>(x[i0 + j], flip) : 0;
@@ -37,8 +43,8 @@ __global__ void __launch_bounds__(1024) shard_header_kernel(const typename KeyT<
   if (threadIdx.x == 0) {
     hdr[0] = n;
     hdr[1] = n <= 1 ? 1 : (inv ? 0 : (n <= kMonoPrefix ? 1 : 2));
-    hdr[2] = n ? key_map<KK>(x[0], flip) : 0;
-    hdr[3] = n ? key_map<KK>(x[n - 1], flip) : 0;
+    hdr[2] = kfirst;
+    hdr[3] = klast;
     hdr[4] = 0;
     hdr[5] = hdr[6] = hdr[7] = 0;
   }
@@ -48,6 +54,7 @@ __global__ void __launch_bounds__(1024) shard_header_kernel(const typename KeyT<
 template <int KK>
 __global__ void shard_scan_kernel(const typename KeyT<KK>::T* __restrict__ x, u64 n, u64 flip,
                                   u64* hdr) {
+  pdl_begin();
   if (hdr[1] != 2) return;
   const u64 stride = (u64)gridDim.x * blockDim.x;
   int found = 0;
@@ -225,13 +232,13 @@ void launch_shard_header(const void* x, u64 n, u64 flip, u64* hdr, int num_sms, 
                          int kk) {
   if (kk == 1) {
     shard_header_kernel<1><<<1, 1024, 0, st>>>((const u32*)x, n, flip, hdr);
-    shard_scan_kernel<1><<<num_sms * 4, 512, 0, st>>>((const u32*)x, n, flip, hdr);
+    launch_pdl(kPdlEstimate, shard_scan_kernel<1>, num_sms * 4, 512, 0, st, (const u32*)x, n, flip, hdr);
   } else if (kk == 2) {
     shard_header_kernel<2><<<1, 1024, 0, st>>>((const u32*)x, n, flip, hdr);
-    shard_scan_kernel<2><<<num_sms * 4, 512, 0, st>>>((const u32*)x, n, flip, hdr);
+    launch_pdl(kPdlEstimate, shard_scan_kernel<2>, num_sms * 4, 512, 0, st, (const u32*)x, n, flip, hdr);
   } else {
     shard_header_kernel<0><<<1, 1024, 0, st>>>((const u64*)x, n, flip, hdr);
-    shard_scan_kernel<0><<<num_sms * 4, 512, 0, st>>>((const u64*)x, n, flip, hdr);
+    launch_pdl(kPdlEstimate, shard_scan_kernel<0>, num_sms * 4, 512, 0, st, (const u64*)x, n, flip, hdr);
   }
 }
 
