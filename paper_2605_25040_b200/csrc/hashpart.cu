@@ -513,8 +513,8 @@ __global__ void __launch_bounds__(kHpThreads, 1) hp_count_kernel(HpArgs a) {
 // ---- hp_reduce: one CTA per partition ----
 // The partition's items are the segments [cpofs[c][p], cpofs[c][p+1]) of every
 // CTA c's cells and [spofs[c][p], spofs[c][p+1]) of its spill, read as one flat
-// list (a segment table in shared memory), a warp per segment with kRdUnroll
-// loads per lane in flight.  Output:
+// list (a segment table in shared memory): a warp takes 128 consecutive items
+// with kRdUnroll loads per lane in flight.  Output:
 // the partition's sorted distinct keys and counts in its staging slot, and its
 // (pairs, rows) in pd / pr for hp_place.
 constexpr int kRdUnroll = 4;
