@@ -2367,8 +2367,14 @@ static int sharded_impl(cafs_ctx_t* ctx, cafs_comm_t* comm, void* d_x, uint64_t 
   }
   const int eff = ctx->h_ctl->eff_route;
   if (*h_status == 1 && native_fb &&
-      (eff == CAFS_FALLBACK_SMALL_N || eff == CAFS_FALLBACK_HIGH_ENTROPY)) {
-    // the dispatcher's fallback branch (every rank takes it: the route is global)
+      (eff == CAFS_FALLBACK_SMALL_N || eff == CAFS_FALLBACK_HIGH_ENTROPY || eff == CAFS_MAIN)) {
+    // the dispatcher's fallback branch (every rank takes it: the route is
+    // global) -- and a main-route column whose tables the device could not
+    // merge (a rank's lost table: the guard, sorter.py:264-273; a list over
+    // 2^20 pairs; a merge partition over 2048 keys): every rank saw that in
+    // the same gathered rows and its shard is intact (shard_result rebuilt a
+    // shard the partitioned count spilled into), so the column is exchanged
+    // and sorted like a fallback column
     if (kk == 0) {
       TRY(sharded_fallback(ctx, comm, (u64*)x, n, flip, st));
     } else {

@@ -53,6 +53,11 @@ cols = {
     "tiny": rng.choice(rng.integers(-2**62, 2**62, 6), 1_000_003),
     "many_pairs": rng.choice(rng.integers(-2**62, 2**62, 50_000), 3_000_000),
     "skew_guard": rng.permutation(skew),
+    # main route, more distinct keys than the device merge takes: exchanged and
+    # sorted inside the library like a fallback column
+    "main_too_many_pairs": rng.permutation(np.concatenate([
+        rng.choice(rng.integers(-2**62, 2**62, 100), 4_000_000),
+        rng.integers(-2**62, 2**62, 1_500_000)[rng.integers(0, 1_500_000, 4_000_000)]])),
     "fallback": rng.integers(-2**62, 2**62, 2_000_000),
     "sorted": np.arange(-100_000, 100_001, dtype=np.int64),
 }

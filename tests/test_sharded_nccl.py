@@ -49,6 +49,11 @@ cols = {
     "many_pairs": (rng.choice(rng.integers(-2**62, 2**62, 50_000), 2_000_000), "native"),
     "many_pairs_zipf": (rng.integers(-2**62, 2**62, 300_000)[
         np.minimum(rng.zipf(1.2, 6_000_000), 300_000) - 1], "native"),
+    # more pairs than the exchange row grows to (2^20): main route, the merge is
+    # not possible on device -> exchanged and sorted like a fallback column
+    "main_too_many_pairs": (rng.permutation(np.concatenate([
+        rng.choice(rng.integers(-2**62, 2**62, 100), 4_000_000),
+        rng.integers(-2**62, 2**62, 1_500_000)[rng.integers(0, 1_500_000, 4_000_000)]])), "native"),
     "fallback": (rng.integers(-2**62, 2**62, 300_000), "native"),  # the library's own exchange sort
     "sorted": (np.arange(-50_000, 50_000, dtype=np.int64), "native"),
     "uint64": (rng.choice(rng.integers(0, 2**63, 500, dtype=np.uint64) * 2, 600_000), "native"),
