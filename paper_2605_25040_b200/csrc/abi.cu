@@ -744,7 +744,10 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
     }
     if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "hash_count", e);
     tm.end(tk, L_K_COUNT, C_MAIN);
-    if (groups & kGrpOld) {
+    // a pipeline that holds only the table route (predicted) and emits: the
+    // pair sort gathers the pairs from the table itself, no compaction kernel
+    const bool gather = with_emit && groups == (kGrpTable | kGrpOld);
+    if ((groups & kGrpOld) && !gather) {
       launch_compact(c, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a, ctx->num_sms, st,
                      kGateMainOld);
       ctx->launches++;
@@ -758,7 +761,8 @@ int launch_fused(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, u64 mult, uint32_t f
     if (groups & kGrpOld) {
       ts = tm.begin();
       e = launch_small_sort_pairs(ctx->pk_a, ctx->pc_a, 0, c, n, ctx->pk_b, ctx->pc_b, ctx->poffs,
-                                  st, kGateMainOld);
+                                  st, kGateMainOld, gather ? ctx->gkeys : nullptr,
+                                  gather ? ctx->gcnt : nullptr, gather ? ctx->glist : nullptr);
       if (e != cudaSuccess) return fail(ctx, CAFS_ECUDA, "pair sort", e);
       tm.end(ts, L_STAGE_SORT_K, C_MAIN);
       ctx->launches++;
@@ -898,6 +902,15 @@ int main_finish(cafs_ctx_t* ctx, void* x, u64 n, u64 flip, cafs_telemetry_t* tel
     return CAFS_OK;
   }
   if (c.need_large) {
+    if (c.need_compact) {
+      // the pipeline held no compaction and its pair sort found too many pairs
+      // to gather: compact now (npairs is read back with the next sync)
+      launch_compact(ctx->d_ctl, ctx->gkeys, ctx->gcnt, ctx->glist, ctx->pk_a, ctx->pc_a,
+                     ctx->num_sms, st, kGateNone);
+      ctx->launches++;
+      CKL();
+      TRY(sync_ctl(ctx, st));
+    }
     const u64 np = c.npairs;
     bool check = false;
     for (int pass = 0; pass < 2; ++pass) {

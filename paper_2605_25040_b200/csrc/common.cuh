@@ -47,7 +47,8 @@ struct DevCtl {
   int64_t u, f1, f2;
   double k_hat;
   int32_t nkeys;
-  int32_t _pad0;
+  int32_t need_compact;    // the pair sort gathered from the table itself and found too many
+                           // pairs: the host compacts the table before the large sort
   u64 keys[CAFS_TINY_MAX_KEYS];  // ascending, unsigned domain
   u64 tiny_mult;                 // perfect-hash multiplier for the tiny keys (16 slots)
   int32_t tiny_slot[CAFS_TINY_MAX_KEYS];

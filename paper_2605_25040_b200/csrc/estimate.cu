@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(1024, 1)
     ctl->empty_key_count = 0;
     ctl->overflow = 0;
     ctl->need_large = 0;
+    ctl->need_compact = 0;
     ctl->npairs = 0;
     ctl->total = 0;
     ctl->pairs_ready = 0;

@@ -90,7 +90,9 @@ size_t small_sort_smem();
 cudaError_t launch_small_sort_keys(u64* keys, u64 n, u64 flip, cudaStream_t st);
 cudaError_t launch_small_sort_pairs(u64* keys, const u64* cnt, u64 n, DevCtl* ctl, u64 expect,
                                     u64* out_keys, u64* out_cnt, u64* out_offs, cudaStream_t st,
-                                    int gate);
+                                    int gate, u64* gkeys = nullptr, u64* gcnt = nullptr,
+                                    const u32* glist = nullptr);  // table given: gather mode (no
+                                                                  // compaction kernel before it)
 void launch_scan(const u64* in, u64 n, u64* bsum, u64* out_offs, DevCtl* ctl, u64 expect,
                  cudaStream_t st);
 // msd.cu

@@ -221,7 +221,8 @@ __global__ void __launch_bounds__(kOsThreads)
 template <bool PAIRS>
 __global__ void __launch_bounds__(1024, 1)
     small_sort_kernel(u64* keys_io, const u64* in_cnt, u64 n_arg, u64 flip, DevCtl* ctl,
-                      u64 expect_total, u64* out_keys, u64* out_cnt, u64* out_offs, int gate) {
+                      u64 expect_total, u64* out_keys, u64* out_cnt, u64* out_offs, int gate,
+                      u64* gkeys, u64* gcnt, const u32* glist) {
   pdl_begin();
   extern __shared__ __align__(16) unsigned char smem[];
   u64* kb = (u64*)smem;                                       // [2][kSmallSortMax]
@@ -235,10 +236,64 @@ __global__ void __launch_bounds__(1024, 1)
   if (ctl && expect_total == kExpectCtlN) expect_total = ctl->n_global;  // sharded merge
   if (PAIRS && ctl) {
     if (ctl->overflow || ctl->pairs_ready || !gate_open(ctl, gate)) return;  // ready: dense path
-    n = ctl->npairs;
-    if (n > (u64)kSmallSortMax) {
-      if (tid == 0) ctl->need_large = 1;
-      return;
+    if (gkeys) {
+      // gather mode (the pipeline holds no compaction kernel): the table's
+      // claimed slots, listed per stripe, become the pairs in keys_io / in_cnt
+      // (what compact_kernel writes) and are re-zeroed; too many for this
+      // kernel: the host compacts before its large sort
+      __shared__ u32 spre[kListStripes + 1];
+      __shared__ u32 wtot[4];
+      u32 f = 0;
+      if (tid < (int)kListStripes) {
+        const u32 g = ctl->g_fill[tid];
+        f = g < kStripeCap ? g : (u32)kStripeCap;
+      }
+      u32 inc = f;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      if (tid < (int)kListStripes && lane == 31) wtot[wid] = inc;
+      __syncthreads();
+      if (tid < (int)kListStripes) {
+        u32 pre = 0;
+        for (int w = 0; w < wid; ++w) pre += wtot[w];
+        spre[tid] = pre + inc - f;
+        if (tid == (int)kListStripes - 1) spre[kListStripes] = pre + inc;
+      }
+      __syncthreads();
+      const u64 tot = spre[kListStripes];
+      const u64 e = ctl->empty_key_count;
+      if (tot > kGlobalCap) {  // stripes have headroom; the table's capacity is the guard
+        if (tid == 0) ctl->overflow = 1;
+        return;
+      }
+      if (tot + (e ? 1 : 0) > (u64)kSmallSortMax) {
+        if (tid == 0) { ctl->need_large = 1; ctl->need_compact = 1; }
+        return;
+      }
+      u64* cnt_io = const_cast<u64*>(in_cnt);
+      for (u32 i = tid; i < (u32)tot; i += 1024) {
+        u32 s2 = 0;  // the stripe holding pair i
+#pragma unroll
+        for (u32 st2 = kListStripes / 2; st2 > 0; st2 >>= 1)
+          if (spre[s2 + st2] <= i) s2 += st2;
+        const u32 h = glist[(u64)s2 * kStripeCap + (i - spre[s2])];
+        keys_io[i] = gkeys[h];
+        cnt_io[i] = gcnt[h];
+        gkeys[h] = kEmpty;
+        gcnt[h] = 0;
+      }
+      if (tid == 0 && e) { keys_io[tot] = kEmpty; cnt_io[tot] = e; }
+      n = tot + (e ? 1 : 0);
+      __syncthreads();  // the pairs are read back below by other threads
+    } else {
+      n = ctl->npairs;
+      if (n > (u64)kSmallSortMax) {
+        if (tid == 0) ctl->need_large = 1;
+        return;
+      }
     }
   }
   u64 vor = 0, vand = ~0ull;
@@ -586,13 +641,14 @@ cudaError_t launch_small_sort_keys(u64* keys, u64 n, u64 flip, cudaStream_t st) 
     attr_dev = dev;
   }
   small_sort_kernel<false><<<1, 1024, sm, st>>>(keys, nullptr, n, flip, nullptr, 0, nullptr,
-                                                nullptr, nullptr, kGateNone);
+                                                nullptr, nullptr, kGateNone, nullptr, nullptr,
+                                                nullptr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_small_sort_pairs(u64* keys, const u64* cnt, u64 n, DevCtl* ctl, u64 expect,
                                     u64* out_keys, u64* out_cnt, u64* out_offs, cudaStream_t st,
-                                    int gate) {
+                                    int gate, u64* gkeys, u64* gcnt, const u32* glist) {
   const size_t sm = small_sort_smem();
   static int attr_dev = -1;
   int dev = 0;
@@ -604,7 +660,7 @@ cudaError_t launch_small_sort_pairs(u64* keys, const u64* cnt, u64 n, DevCtl* ct
     attr_dev = dev;
   }
   return launch_pdl(kPdlPairSort, small_sort_kernel<true>, 1, 1024, sm, st, keys, cnt, n, (u64)0, ctl, expect,
-                    out_keys, out_cnt, out_offs, gate);
+                    out_keys, out_cnt, out_offs, gate, gkeys, gcnt, glist);
 }
 
 void launch_scan(const u64* in, u64 n, u64* bsum, u64* out_offs, DevCtl* ctl, u64 expect,
