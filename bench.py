@@ -328,16 +328,6 @@ def main():
         # process takes ~10 ms; timeit does the same)
         gc.collect()
         gc.disable()
-        # ... and no preemption of the launching thread by other host processes
-        # (a 1 ms scheduler hiccup between a step's start event and its graph
-        # launch showed as a 3.5 ms step): real-time priority for the loop when
-        # the process may ask for it
-        sched = None
-        try:
-            sched = (os.sched_getscheduler(0), os.sched_getparam(0))
-            os.sched_setscheduler(0, os.SCHED_FIFO, os.sched_param(10))
-        except (AttributeError, OSError, PermissionError):
-            sched = None
         # the GPU sat idle while nvidia-smi started (up to a second) and may have
         # dropped its clocks: two more untimed steps right before the timed ones
         # (a first timed step of 3.5-4 ms against 2.38 ms showed in 3 of ~8 runs)
@@ -357,11 +347,6 @@ def main():
         torch.cuda.synchronize()
         barrier()
         wall = time.perf_counter() - wall0
-        if sched is not None:
-            try:
-                os.sched_setscheduler(0, sched[0], sched[1])
-            except OSError:
-                pass
         gc.enable()
         return [a.elapsed_time(b) for a, b in zip(ev0, ev1)], tels, wall
 
